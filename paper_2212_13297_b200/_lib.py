@@ -1,0 +1,79 @@
+"""ctypes binding of libseriesearch_b200.so (include/seriesearch_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (``make -C
+paper_2212_13297_b200/csrc``).  There is no CPU fallback: if the library or a
+CUDA device is missing, every entry point raises ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import DataFileError, DeviceError, IntegrityError, UsageError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libseriesearch_b200.so")
+
+_lib = None
+_lock = threading.Lock()
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+_SIGS = {
+    "ssb_version": [],
+    "ssb_last_error": [],
+    "ssb_launch_count": [],
+    "ssb_device_ok": [],
+    "ssb_words": [P, I64, I32, P, P, P, P],
+    "ssb_segment_stats": [P, I64, I32, P, P, I32, P, P, P],
+    "ssb_bruteforce_knn": [P, I64, I32, P, I32, I32, I64, P, P, P],
+}
+_RESTYPES = {
+    "ssb_version": ctypes.c_int32,
+    "ssb_last_error": ctypes.c_char_p,
+    "ssb_launch_count": ctypes.c_int64,
+    "ssb_device_ok": ctypes.c_int32,
+}
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def load():
+    """Load (once) and return the CDLL; raises DeviceError if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                    "(there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, args in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPES.get(name, ctypes.c_int)
+            _lib = lib
+    return _lib
+
+
+_ERRORS = {1: UsageError, 2: DataFileError, 3: IntegrityError, 4: DeviceError, 5: DeviceError}
+
+
+def call(name: str, *args) -> None:
+    """Invoke an ``int``-returning entry point; map its code to an exception."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.ssb_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, DeviceError)(f"{name}: {msg}")
+
+
+def launch_count() -> int:
+    return int(load().ssb_launch_count())

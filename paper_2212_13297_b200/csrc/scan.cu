@@ -1,0 +1,377 @@
+// scan.cu -- K-scan (exact squared ED + top-k) and K-select.
+//
+// Replaces: core.py:50-57 ed2_batch (the canonical f32 distance),
+// pscan.py:23-30 brute_force_knn / pscan.py:33-135 pscan_query (full scans),
+// query.py:177-192, 253-292 (leaf scans, candidate refinement).
+//
+// Layout: rows are 4n-byte f32 vectors, contiguous; a "tile" is <= 32
+// consecutive rows.  Tiles are staged into shared memory with TMA 1-D bulk
+// copies (cp.async.bulk ... mbarrier::complete_tx), double-buffered.  An
+// 8-lane group owns one query (its n values live in registers, lane j holds
+// q[8i+j]) and walks the tile rows; lane j is numpy's pairwise accumulator
+// r[j], so d2 is bit-identical to ed2_batch (ssb_common.cuh group_ed2).
+//
+// Two launch shapes share that arithmetic:
+//  * dense  (brute force): CTA = (row range) x (block of 4*WARPS queries); each
+//    group keeps a sorted top-k of its range in shared memory and dumps it to
+//    the per-query candidate buffer at the end.
+//  * sparse (index path): CTA walks a list of tiles; each tile carries
+//    (query, 32-bit row mask) entries; a pair whose (d2, id) key is <= the
+//    query's bound is appended to the query's candidate buffer.
+// K-select then sorts each query's candidates and keeps the first k.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ssb_common.cuh"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+// ---------------------------------------------------------------------------
+// dense scan
+
+template <int NT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    scan_dense_kernel(const float *__restrict__ X, int64_t N, const float *__restrict__ Q,
+                      const int32_t *__restrict__ qidx, int nq, int k, uint32_t id_base,
+                      int64_t rows_per_range, ScanOut out)
+{
+    constexpr int G = WARPS * 4;  // groups (queries) per CTA
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);                      // 2 x TILE_ROWS x NT
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tiles + 2 * TILE_ROWS * NT);  // 2
+    uint64_t *lists = bars + 2;                                             // G x k
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = warp * 4 + (lane >> 3);
+    const int j = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_range;
+    const int64_t r1 = tmin<int64_t>(N, r0 + rows_per_range);
+    const int qslot = blockIdx.y * G + g;
+    const bool active = qslot < nq;
+    const int q = active ? qidx[qslot] : 0;
+
+    for (int e = tid; e < G * k; e += blockDim.x) lists[e] = KEY_EMPTY;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    float qv[NT / 8];
+#pragma unroll
+    for (int i = 0; i < NT / 8; i++) qv[i] = active ? Q[(int64_t)q * NT + 8 * i + j] : 0.0f;
+    __syncthreads();
+
+    const int64_t ntiles = r1 > r0 ? (r1 - r0 + TILE_ROWS - 1) / TILE_ROWS : 0;
+    auto issue = [&](int64_t t) {
+        int64_t row = r0 + t * TILE_ROWS;
+        int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row);
+        unsigned bytes = (unsigned)nr * NT * 4u;
+        uint64_t *bar = &bars[t & 1];
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(tiles + (t & 1) * TILE_ROWS * NT, X + row * NT, bytes, bar);
+    };
+    if (tid == 0 && ntiles > 0) issue(0);
+    uint64_t *mylist = lists + (size_t)g * k;
+
+    for (int64_t t = 0; t < ntiles; t++) {
+        if (tid == 0 && t + 1 < ntiles) issue(t + 1);
+        mbar_wait(&bars[t & 1], (unsigned)((t >> 1) & 1));
+        const int64_t row0 = r0 + t * TILE_ROWS;
+        const int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row0);
+        const float *buf = tiles + (t & 1) * TILE_ROWS * NT;
+        if (active) {
+            for (int r = 0; r < nr; r++) {
+                float d2 = group_ed2<NT>(buf + r * NT, qv, j, gmask);
+                if (j == 0) {
+                    uint64_t key = make_key(d2, id_base + (uint32_t)(row0 + r));
+                    if (key < mylist[k - 1]) {
+                        int p = k - 1;
+                        while (p > 0 && mylist[p - 1] > key) {
+                            mylist[p] = mylist[p - 1];
+                            p--;
+                        }
+                        mylist[p] = key;
+                    }
+                }
+                __syncwarp(gmask);
+            }
+        }
+        __syncthreads();
+    }
+
+    // dump the range's top-k (only keys within the query's bound)
+    if (active) {
+        const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
+        int c = 0;
+        uint32_t base = 0;
+        if (j == 0) {
+            while (c < k && mylist[c] != KEY_EMPTY && mylist[c] <= bound) c++;
+            base = c ? atomicAdd(&out.cnt[q], (uint32_t)c) : 0u;
+        }
+        c = __shfl_sync(gmask, c, lane & 24);
+        base = __shfl_sync(gmask, base, lane & 24);
+        for (int e = j; e < c; e += 8) {
+            uint32_t slot = base + e;
+            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = mylist[e];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// sparse scan over (tile, query, row-mask) work lists
+
+template <int NT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    scan_sparse_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
+                       TileList tl, const float *__restrict__ Q, ScanOut out)
+{
+    constexpr int G = WARPS * 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tiles + 2 * TILE_ROWS * NT);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = warp * 4 + (lane >> 3);
+    const int j = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    // static round-robin tile assignment: tile = blockIdx.x + it * gridDim.x
+    const int64_t my_tiles =
+        tl.ntiles > (int64_t)blockIdx.x ? (tl.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto issue = [&](int64_t it) {
+        int64_t t = blockIdx.x + it * gridDim.x;
+        uint32_t row0 = tl.row0[t];
+        uint32_t um = tl.umask[t];
+        float *buf = tiles + (it & 1) * TILE_ROWS * NT;
+        uint64_t *bar = &bars[it & 1];
+        mbar_expect_tx(bar, (unsigned)__popc(um) * NT * 4u);
+        while (um) {
+            int r = __ffs(um) - 1;
+            um &= um - 1;
+            bulk_g2s(buf + r * NT, X + (int64_t)(row0 + r) * NT, NT * 4u, bar);
+        }
+    };
+    if (tid == 0 && my_tiles > 0) issue(0);
+
+    for (int64_t it = 0; it < my_tiles; it++) {
+        if (tid == 0 && it + 1 < my_tiles) issue(it + 1);
+        mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
+        const int64_t t = blockIdx.x + it * gridDim.x;
+        const uint32_t row0 = tl.row0[t];
+        const float *buf = tiles + (it & 1) * TILE_ROWS * NT;
+        const uint32_t e0 = tl.eptr[t], e1 = tl.eptr[t + 1];
+        for (uint32_t e = e0 + g; e < e1; e += G) {
+            const uint2 ent = tl.entries[e];
+            const int q = (int)ent.x;
+            uint32_t mask = ent.y;
+            float qv[NT / 8];
+#pragma unroll
+            for (int i = 0; i < NT / 8; i++) qv[i] = Q[(int64_t)q * NT + 8 * i + j];
+            const uint64_t bound = out.thr[q];
+            while (mask) {
+                int r = __ffs(mask) - 1;
+                mask &= mask - 1;
+                float d2 = group_ed2<NT>(buf + r * NT, qv, j, gmask);
+                if (j == 0) {
+                    uint32_t pos = row0 + r;
+                    uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
+                    if (key <= bound) {
+                        uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+                        if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-select: per query, sort its candidates (bitonic in shared memory) and
+// emit the first k; flag overflow and tighten the bound when it happened.
+
+__global__ void select_topk_kernel(const uint64_t *__restrict__ cand, uint32_t *__restrict__ cnt,
+                                   int cap, int P, int k, uint64_t *__restrict__ thr,
+                                   uint64_t *__restrict__ out_keys, int32_t *__restrict__ flags)
+{
+    extern __shared__ __align__(16) uint64_t sk[];
+    const int q = blockIdx.x;
+    const uint32_t total = cnt[q];
+    const int c = (int)tmin<uint32_t>(total, (uint32_t)cap);
+    // smallest power of two >= max(c, k), capped at P
+    int p2 = 1;
+    while (p2 < c || p2 < k) p2 <<= 1;
+    if (p2 > P) p2 = P;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x)
+        sk[i] = i < c ? cand[(size_t)q * cap + i] : KEY_EMPTY;
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+                int lo = 2 * i - (i & (stride - 1));
+                int hi = lo + stride;
+                bool up = ((lo & size) == 0);
+                uint64_t a = sk[lo], b = sk[hi];
+                if ((a > b) == up) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        out_keys[(size_t)q * k + i] = i < p2 ? sk[i] : KEY_EMPTY;
+    if (threadIdx.x == 0) {
+        int over = total > (uint32_t)cap;
+        flags[q] = over;
+        if (over) thr[q] = sk[k - 1];  // k-th best of real distances: a valid, tighter bound
+    }
+}
+
+__global__ void keys_to_results_kernel(const uint64_t *__restrict__ keys, int64_t count,
+                                       const uint32_t *__restrict__ inv_perm, float *out_d2,
+                                       int64_t *out_id, int64_t *out_pos)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint64_t key = keys[i];
+    if (key == KEY_EMPTY) {
+        out_d2[i] = __int_as_float(0x7f800000);
+        out_id[i] = -1;
+        if (out_pos) out_pos[i] = -1;
+    } else {
+        out_d2[i] = key_d2(key);
+        uint32_t id = key_id(key);
+        out_id[i] = id;
+        if (out_pos) out_pos[i] = inv_perm ? (int64_t)inv_perm[id] : (int64_t)id;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+// Row ranges of the dense scan: each range dumps <= k keys per query, so
+// ranges * k <= cap; aim for >= 2 waves of 2 CTAs/SM, >= 4 tiles per range.
+int64_t dense_ranges(int64_t N, int nq, int k, int cap)
+{
+    constexpr int G = 32;
+    int64_t qblocks = (nq + G - 1) / G;
+    int64_t max_ranges = std::max<int64_t>(1, cap / k);
+    int64_t want = std::max<int64_t>(1, (4 * (int64_t)num_sms() + qblocks - 1) / qblocks);
+    int64_t by_rows = std::max<int64_t>(1, N / (4 * TILE_ROWS));
+    return std::max<int64_t>(1, std::min(std::min(max_ranges, want), by_rows));
+}
+
+static int dense_smem_bytes(int nt, int warps, int k)
+{
+    return 2 * TILE_ROWS * nt * 4 + 16 + warps * 4 * k * 8;
+}
+
+template <int NT>
+static int launch_dense_t(const float *X, int64_t N, const float *Q, const int32_t *qidx, int nq,
+                          int k, uint32_t id_base, ScanOut out, cudaStream_t s)
+{
+    constexpr int WARPS = 8;
+    constexpr int G = WARPS * 4;
+    int smem = dense_smem_bytes(NT, WARPS, k);
+    SSB_CUDA(cudaFuncSetAttribute(scan_dense_kernel<NT, WARPS>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int qblocks = (nq + G - 1) / G;
+    int64_t ranges = dense_ranges(N, nq, k, out.cap);
+    int64_t rpr = (N + ranges - 1) / ranges;
+    rpr = (rpr + TILE_ROWS - 1) / TILE_ROWS * TILE_ROWS;
+    ranges = (N + rpr - 1) / rpr;
+    dim3 grid((unsigned)ranges, (unsigned)qblocks);
+    scan_dense_kernel<NT, WARPS><<<grid, WARPS * 32, smem, s>>>(X, N, Q, qidx, nq, k, id_base, rpr, out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
+                      int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s)
+{
+    if (nq == 0 || N == 0) return OK;
+    switch (n) {
+    case 64: return launch_dense_t<64>(X, N, Q, qidx, nq, k, id_base, out, s);
+    case 96: return launch_dense_t<96>(X, N, Q, qidx, nq, k, id_base, out, s);
+    case 128: return launch_dense_t<128>(X, N, Q, qidx, nq, k, id_base, out, s);
+    case 256: return launch_dense_t<256>(X, N, Q, qidx, nq, k, id_base, out, s);
+    default: break;
+    }
+    set_error(ERR_USAGE, "series length " + std::to_string(n) +
+                          " has no compiled scan kernel (supported: 64, 96, 128, 256)");
+    return ERR_USAGE;
+}
+
+template <int NT>
+static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileList &tl,
+                           const float *Q, ScanOut out, cudaStream_t s)
+{
+    constexpr int WARPS = 8;
+    int smem = 2 * TILE_ROWS * NT * 4 + 16;
+    SSB_CUDA(cudaFuncSetAttribute(scan_sparse_kernel<NT, WARPS>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int64_t grid = std::min<int64_t>(tl.ntiles, (int64_t)num_sms() * 4);
+    if (grid < 1) return OK;
+    scan_sparse_kernel<NT, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(X, row_id, tl, Q, out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
+                       const float *Q, ScanOut out, cudaStream_t s)
+{
+    if (tl.ntiles == 0) return OK;
+    switch (n) {
+    case 64: return launch_sparse_t<64>(X, row_id, tl, Q, out, s);
+    case 96: return launch_sparse_t<96>(X, row_id, tl, Q, out, s);
+    case 128: return launch_sparse_t<128>(X, row_id, tl, Q, out, s);
+    case 256: return launch_sparse_t<256>(X, row_id, tl, Q, out, s);
+    default: break;
+    }
+    set_error(ERR_USAGE, "series length " + std::to_string(n) +
+                          " has no compiled scan kernel (supported: 64, 96, 128, 256)");
+    return ERR_USAGE;
+}
+
+int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
+                  uint64_t *out_keys, int32_t *flags, cudaStream_t s)
+{
+    if (nq == 0) return OK;
+    int P = 1;
+    while (P < cap || P < k) P <<= 1;
+    int smem = P * 8;
+    SSB_REQUIRE(smem <= 200 * 1024, "candidate capacity too large for K-select");
+    SSB_CUDA(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    select_topk_kernel<<<nq, 1024, smem, s>>>(cand, cnt, cap, P, k, thr, out_keys, flags);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm,
+                           float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s)
+{
+    if (count == 0) return OK;
+    keys_to_results_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(keys, count, inv_perm,
+                                                                          out_d2, out_id, out_pos);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+}  // namespace ssb

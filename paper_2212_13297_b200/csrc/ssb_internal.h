@@ -1,0 +1,67 @@
+// ssb_internal.h -- internal (C++) interfaces between the translation units of
+// libseriesearch_b200.  Nothing here is part of the C ABI (include/*.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace ssb {
+
+int num_sms();
+
+// per-query candidate buffers written by the scan kernels
+struct ScanOut {
+    uint64_t *cand;       // [nq_total][cap] (d2 bits << 32 | original id)
+    uint32_t *cnt;        // [nq_total] append counters (may exceed cap: overflow)
+    const uint64_t *thr;  // [nq_total] inclusive key bound, KEY_EMPTY = +inf (nullable)
+    int cap;
+};
+
+// sparse scan work: tiles of <= 32 consecutive rows, each with (query, row mask) entries
+struct TileList {
+    const uint32_t *row0;   // [ntiles] first row (position) of the tile
+    const uint32_t *umask;  // [ntiles] union of the entry masks (rows to stage)
+    const uint32_t *eptr;   // [ntiles + 1] CSR into entries
+    const uint2 *entries;   // (query, row mask)
+    int64_t ntiles;
+};
+
+int64_t dense_ranges(int64_t N, int nq, int k, int cap);
+int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
+                      int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
+int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
+                       const float *Q, ScanOut out, cudaStream_t s);
+int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
+                  uint64_t *out_keys, int32_t *flags, cudaStream_t s);
+int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm,
+                           float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s);
+
+// stream-ordered device scratch (cudaMallocAsync pool); freed on scope exit
+struct DevBuf {
+    void *p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf()
+    {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t st)
+    {
+        s = st;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    }
+    template <typename T>
+    T *as() const
+    {
+        return reinterpret_cast<T *>(p);
+    }
+};
+
+// host-side launch accounting (counts kernels this library launched)
+void note_launch(int count = 1);
+
+}  // namespace ssb

@@ -1,0 +1,212 @@
+// summarize.cu -- K-sum: PAA -> SAX words, EAPCA segment statistics, query prep.
+//
+// Replaces: summarize.py:89-121 (paa_batch, isax_from_paa), summarize.py:34-82
+// (prefix_sums, stats_from_prefix, segment_stats_matrix), persist.py:222-225
+// (words computed per leaf at write time), query.py:117-125 (_QueryState).
+//
+// PAA: float32 pairwise sum of the w = n/16 points, then a correctly rounded
+// division by w (numpy's mean divides by an intp count, which promotes to
+// float64 and rounds back; double rounding is innocuous for division, so it
+// equals __fdiv_rn).  Symbol: #{breakpoints <= (double)paa} by binary search
+// over the 255 float64 breakpoints staged in shared memory.
+// Stats: float64 prefix sums accumulated strictly sequentially (np.cumsum),
+// mean=(cs[e]-cs[s])/w, msq likewise, sd=sqrt(max(msq-mean*mean,0)), both
+// rounded to float32 -- no FMA anywhere (--fmad=false + _rn intrinsics).
+#include <cuda_runtime.h>
+
+#include "ssb_common.cuh"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+__device__ __forceinline__ int sax_symbol(double v, const double *bp)
+{
+    int lo = 0, hi = ALPHABET - 1;  // first index with bp[i] > v
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (bp[mid] <= v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// one thread per (row, word segment); W = n/16 points per segment
+template <int W>
+__global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
+                             const double *__restrict__ bp_g, uint8_t *__restrict__ words,
+                             float *__restrict__ paa_out)
+{
+    __shared__ double bp[ALPHABET];
+    for (int i = threadIdx.x; i < ALPHABET - 1; i += blockDim.x) bp[i] = bp_g[i];
+    __syncthreads();
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * WORD_SEGMENTS) return;
+    const int64_t row = t / WORD_SEGMENTS;
+    const int seg = (int)(t % WORD_SEGMENTS);
+    const float *x = X + row * n + seg * (n / WORD_SEGMENTS);
+    float sum;
+    if constexpr (W > 0) {
+        float v[W];
+        if constexpr (W % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < W / 4; i++) {
+                float4 f = __ldg(reinterpret_cast<const float4 *>(x) + i);
+                v[4 * i] = f.x;
+                v[4 * i + 1] = f.y;
+                v[4 * i + 2] = f.z;
+                v[4 * i + 3] = f.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < W; i++) v[i] = __ldg(x + i);
+        }
+        sum = pw_f32_seq<W>([&](int i) { return v[i]; });
+    } else {
+        sum = pw_f32_rt(x, n / WORD_SEGMENTS);
+    }
+    const float p = __fdiv_rn(sum, (float)(n / WORD_SEGMENTS));
+    words[t] = (uint8_t)sax_symbol((double)p, bp);
+    if (paa_out) paa_out[t] = p;
+}
+
+int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words,
+                 float *paa_out, cudaStream_t s)
+{
+    SSB_REQUIRE(n % WORD_SEGMENTS == 0, "series length must be divisible by 16 word segments");
+    if (N == 0) return OK;
+    const int64_t threads = N * WORD_SEGMENTS;
+    const unsigned grid = (unsigned)((threads + 255) / 256);
+    switch (n / WORD_SEGMENTS) {
+    case 4: words_kernel<4><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    case 6: words_kernel<6><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    case 8: words_kernel<8><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    case 16: words_kernel<16><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    case 32: words_kernel<32><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    default: words_kernel<0><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    }
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// segment statistics for arbitrary segments of every row.
+// pts: sorted unique boundary points (npts <= 2*m), seg_s/seg_e: indices into pts.
+
+__device__ __forceinline__ void stats_from(double cs_s, double cs_e, double c2_s, double c2_e,
+                                           int w, float &mean_out, float &sd_out)
+{
+    const double wd = (double)w;
+    const double mean = __ddiv_rn(__dsub_rn(cs_e, cs_s), wd);
+    const double msq = __ddiv_rn(__dsub_rn(c2_e, c2_s), wd);
+    const double var = __dsub_rn(msq, __dmul_rn(mean, mean));
+    const double sd = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    mean_out = __double2float_rn(mean);
+    sd_out = __double2float_rn(sd);
+}
+
+constexpr int MAX_PTS = 130;
+
+__global__ void segment_stats_kernel(const float *__restrict__ X, int64_t N, int n,
+                                     const int32_t *__restrict__ pts_g, int npts,
+                                     const int32_t *__restrict__ seg_s, const int32_t *__restrict__ seg_e,
+                                     int m, float *__restrict__ mean, float *__restrict__ sd)
+{
+    __shared__ int32_t pts[MAX_PTS];
+    for (int i = threadIdx.x; i < npts; i += blockDim.x) pts[i] = pts_g[i];
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= N) return;
+    double cs[MAX_PTS], c2[MAX_PTS];
+    const float *x = X + row * n;
+    double a = 0.0, b = 0.0;
+    int p = 0;
+    while (p < npts && pts[p] == 0) {
+        cs[p] = 0.0;
+        c2[p] = 0.0;
+        p++;
+    }
+    for (int i = 0; i < n && p < npts; i++) {
+        const double v = (double)__ldg(x + i);
+        a = __dadd_rn(a, v);
+        b = __dadd_rn(b, __dmul_rn(v, v));
+        while (p < npts && pts[p] == i + 1) {
+            cs[p] = a;
+            c2[p] = b;
+            p++;
+        }
+    }
+    for (int jj = 0; jj < m; jj++) {
+        const int s = seg_s[jj], e = seg_e[jj];
+        stats_from(cs[s], cs[e], c2[s], c2[e], pts[e] - pts[s], mean[row * m + jj], sd[row * m + jj]);
+    }
+}
+
+int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, int npts,
+                         const int32_t *seg_s, const int32_t *seg_e, int m, float *mean, float *sd,
+                         cudaStream_t s)
+{
+    SSB_REQUIRE(npts <= MAX_PTS, "too many distinct segment boundaries");
+    if (N == 0 || m == 0) return OK;
+    segment_stats_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(X, N, n, pts, npts, seg_s,
+                                                                     seg_e, m, mean, sd);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// query prep (query.py:117-125): fp64 prefix sums (n+1 each) and PAA (16)
+
+template <int W>
+__device__ float paa_one(const float *x, int n)
+{
+    if constexpr (W > 0)
+        return __fdiv_rn(pw_f32_seq<W>([&](int i) { return x[i]; }), (float)W);
+    else
+        return __fdiv_rn(pw_f32_rt(x, n / WORD_SEGMENTS), (float)(n / WORD_SEGMENTS));
+}
+
+__global__ void query_prep_kernel(const float *__restrict__ Q, int B, int n, double *__restrict__ cs,
+                                  double *__restrict__ c2, float *__restrict__ qpaa)
+{
+    const int q = blockIdx.x;
+    const float *x = Q + (int64_t)q * n;
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        double *o = cs + (int64_t)q * (n + 1), *o2 = c2 + (int64_t)q * (n + 1);
+        o[0] = 0.0;
+        o2[0] = 0.0;
+        for (int i = 0; i < n; i++) {
+            const double v = (double)x[i];
+            a = __dadd_rn(a, v);
+            b = __dadd_rn(b, __dmul_rn(v, v));
+            o[i + 1] = a;
+            o2[i + 1] = b;
+        }
+    } else if (threadIdx.x >= 32 && threadIdx.x < 32 + WORD_SEGMENTS) {
+        const int seg = threadIdx.x - 32;
+        const int w = n / WORD_SEGMENTS;
+        const float *xs = x + seg * w;
+        float p;
+        switch (w) {
+        case 4: p = paa_one<4>(xs, n); break;
+        case 6: p = paa_one<6>(xs, n); break;
+        case 8: p = paa_one<8>(xs, n); break;
+        case 16: p = paa_one<16>(xs, n); break;
+        default: p = paa_one<0>(xs, n); break;
+        }
+        qpaa[(int64_t)q * WORD_SEGMENTS + seg] = p;
+    }
+}
+
+int launch_query_prep(const float *Q, int B, int n, double *cs, double *c2, float *qpaa,
+                      cudaStream_t s)
+{
+    if (B == 0) return OK;
+    query_prep_kernel<<<B, 64, 0, s>>>(Q, B, n, cs, c2, qpaa);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+}  // namespace ssb
