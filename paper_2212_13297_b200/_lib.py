@@ -29,6 +29,10 @@ _SIGS = {
     "ssb_last_error": [],
     "ssb_launch_count": [],
     "ssb_device_ok": [],
+    "ssb_prof_enable": [I32],
+    "ssb_prof_reset": [],
+    "ssb_prof_read": [I32, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_double),
+                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)],
     "ssb_words": [P, I64, I32, P, P, P, P],
     "ssb_segment_stats": [P, I64, I32, P, P, I32, P, P, P],
     "ssb_bruteforce_knn": [P, I64, I32, P, I32, I32, I64, P, P, P],
@@ -38,6 +42,8 @@ _RESTYPES = {
     "ssb_last_error": ctypes.c_char_p,
     "ssb_launch_count": ctypes.c_int64,
     "ssb_device_ok": ctypes.c_int32,
+    "ssb_prof_enable": None,
+    "ssb_prof_reset": None,
 }
 
 
@@ -77,3 +83,26 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().ssb_launch_count())
+
+
+def prof_enable(on: bool = True) -> None:
+    load().ssb_prof_enable(1 if on else 0)
+
+
+def prof_reset() -> None:
+    load().ssb_prof_reset()
+
+
+def prof_read() -> dict:
+    """{kernel: (ms_total, launches, algorithmic_bytes_total)} (synchronizes)."""
+    lib = load()
+    out = {}
+    i = 0
+    buf = ctypes.create_string_buffer(64)
+    while True:
+        ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        if lib.ssb_prof_read(i, buf, 64, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)) != 0:
+            break
+        out[buf.value.decode()] = (ms.value, n.value, b.value)
+        i += 1
+    return out

@@ -1,0 +1,107 @@
+// prof.cu -- in-library per-kernel device timing with CUDA events recorded on
+// the launching stream (bench.py's roofline "achieved" = algorithmic bytes /
+// these durations).  Off by default; ssb_prof_enable(1) turns it on.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/seriesearch_b200.h"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+    double bytes;
+};
+
+static std::mutex g_mu;
+static bool g_on = false;
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_pool;
+
+static cudaEvent_t take_event()
+{
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(const char *name, cudaStream_t s, double bytes) : name_(name), s_(s), bytes_(bytes)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!g_on) return;
+    a_ = take_event();
+    b_ = take_event();
+    cudaEventRecord((cudaEvent_t)a_, s_);
+}
+
+ProfScope::~ProfScope()
+{
+    if (!a_) return;
+    cudaEventRecord((cudaEvent_t)b_, s_);
+    std::lock_guard<std::mutex> g(g_mu);
+    g_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_, bytes_});
+}
+
+}  // namespace ssb
+
+using namespace ssb;
+
+extern "C" {
+
+void ssb_prof_enable(int32_t on)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    g_on = on != 0;
+}
+
+void ssb_prof_reset(void)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    for (auto &r : g_recs) {
+        cudaEventSynchronize(r.b);
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+}
+
+int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, int64_t *launches,
+                  double *bytes_total)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    std::map<std::string, std::pair<double, std::pair<int64_t, double>>> agg;
+    for (auto &r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto &e = agg[r.name];
+        e.first += ms;
+        e.second.first += 1;
+        e.second.second += r.bytes;
+    }
+    int i = 0;
+    for (auto &kv : agg) {
+        if (i++ != idx) continue;
+        std::strncpy(name, kv.first.c_str(), (size_t)name_cap - 1);
+        name[name_cap - 1] = 0;
+        *ms_total = kv.second.first;
+        *launches = kv.second.second.first;
+        *bytes_total = kv.second.second.second;
+        return 0;
+    }
+    return 1;
+}
+
+}  // extern "C"

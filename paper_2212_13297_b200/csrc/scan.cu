@@ -297,7 +297,12 @@ static int launch_dense_t(const float *X, int64_t N, const float *Q, const int32
     rpr = (rpr + TILE_ROWS - 1) / TILE_ROWS * TILE_ROWS;
     ranges = (N + rpr - 1) / rpr;
     dim3 grid((unsigned)ranges, (unsigned)qblocks);
-    scan_dense_kernel<NT, WARPS><<<grid, WARPS * 32, smem, s>>>(X, N, Q, qidx, nq, k, id_base, rpr, out);
+    {
+        // algorithmic bytes: every row once + the queries + the dumped keys
+        ProfScope ps("scan_dense", s, (double)N * NT * 4 + (double)nq * NT * 4 +
+                                          (double)ranges * nq * k * 8);
+        scan_dense_kernel<NT, WARPS><<<grid, WARPS * 32, smem, s>>>(X, N, Q, qidx, nq, k, id_base, rpr, out);
+    }
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -359,7 +364,10 @@ int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, u
     SSB_REQUIRE(smem <= 200 * 1024, "candidate capacity too large for K-select");
     SSB_CUDA(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
-    select_topk_kernel<<<nq, 1024, smem, s>>>(cand, cnt, cap, P, k, thr, out_keys, flags);
+    {
+        ProfScope ps("select", s, 0.0);
+        select_topk_kernel<<<nq, 1024, smem, s>>>(cand, cnt, cap, P, k, thr, out_keys, flags);
+    }
     SSB_CHECK_LAUNCH();
     return OK;
 }

@@ -61,6 +61,20 @@ struct DevBuf {
     }
 };
 
+// RAII event pair around one kernel launch (prof.cu); no-op unless enabled.
+// `bytes` = algorithmic bytes of the launch (DESIGN.md per-kernel formulas).
+class ProfScope {
+  public:
+    ProfScope(const char *name, cudaStream_t s, double bytes);
+    ~ProfScope();
+
+  private:
+    const char *name_;
+    cudaStream_t s_;
+    double bytes_;
+    void *a_ = nullptr, *b_ = nullptr;
+};
+
 // host-side launch accounting (counts kernels this library launched)
 void note_launch(int count = 1);
 

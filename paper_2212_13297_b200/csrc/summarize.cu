@@ -78,6 +78,7 @@ int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *wo
     if (N == 0) return OK;
     const int64_t threads = N * WORD_SEGMENTS;
     const unsigned grid = (unsigned)((threads + 255) / 256);
+    ProfScope ps("words", s, (double)N * n * 4 + (double)N * 16 + (paa_out ? (double)N * 64 : 0.0));
     switch (n / WORD_SEGMENTS) {
     case 4: words_kernel<4><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
     case 6: words_kernel<6><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
