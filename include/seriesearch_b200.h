@@ -85,6 +85,83 @@ int ssb_bruteforce_knn(const float *X, int64_t N, int32_t n, const float *Q, int
                        int32_t k, int64_t id_base, float *out_d2, int64_t *out_id,
                        void *stream);
 
+/* ---- K-split + K-part: index build -------------------------------------- */
+
+#define SSB_M_MAX 32
+
+typedef struct ssb_index ssb_index; /* opaque; owns its device arrays */
+
+typedef struct {
+    int64_t leaf_threshold;   /* tau (persist.py:64-85 IndexSettings.leaf_threshold) */
+    int32_t initial_segments; /* root segmentation (reference: 1, build.py:131) */
+    int32_t max_segments;     /* V-splits stop at this many segments (<= SSB_M_MAX) */
+    int64_t id_base;          /* original ids = row + id_base (row shards) */
+} ssb_build_cfg;
+
+typedef struct {
+    int64_t dataset_size, leaf_threshold, id_base;
+    int32_t series_length, num_nodes, num_leaves, levels, max_segments, depth;
+    double build_ms;
+    float max_abs;
+} ssb_index_info_t;
+
+/* one tree node (tree.py:92-179 Node + :51-89 SplitPolicy); first/count index
+ * the index's leaf order (the reference's lrd.bin positions) */
+typedef struct {
+    int32_t parent, left, right;
+    uint32_t first, count;
+    int32_t m;
+    int32_t endpoints[SSB_M_MAX];
+    float envelope[SSB_M_MAX][4]; /* mu_min, mu_max, sd_min, sd_max */
+    int32_t is_leaf, oversize, depth;
+    int32_t segment, attribute, split_point, route_start, route_end; /* split_point -1 = horizontal */
+    double threshold, gain;
+} ssb_node_t;
+
+/* Build the index over N device-resident rows (level-synchronous, all on the
+ * device).  Replaces build.py:363-458 build_index + persist.py:269-369
+ * write_index's layout work (leaf-contiguous rows and words, exact synopses).
+ * bp: 255 float64 breakpoints.  Synchronizes `stream`. */
+int ssb_build(const float *X, int64_t N, int32_t n, const double *bp, const ssb_build_cfg *cfg,
+              ssb_index **out, void *stream);
+int ssb_index_free(ssb_index *index);
+int ssb_index_info(const ssb_index *index, ssb_index_info_t *out);
+int ssb_index_node(const ssb_index *index, int32_t node, ssb_node_t *out);
+/* device arrays in leaf order: rows, words, pos->original row, original row->pos */
+int ssb_index_arrays(const ssb_index *index, const float **X, const uint8_t **words,
+                     const uint32_t **orig, const uint32_t **inv);
+
+/* copy the leaf-ordered rows / words / original rows to host memory (any may be NULL) */
+int ssb_index_download(const ssb_index *index, float *rows_host, uint8_t *words_host,
+                       uint32_t *orig_host);
+/* An index from host arrays already in leaf order plus its node records
+ * (persist.py:461-528 load_index: a reference-built tree goes onto the GPU).
+ * words_host NULL -> recomputed on the device; orig_host NULL -> identity. */
+int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint32_t *orig_host,
+                   int64_t N, int32_t n, int64_t leaf_threshold, int64_t id_base,
+                   const ssb_node_t *nodes, int32_t num_nodes, const double *bp, ssb_index **out,
+                   void *stream);
+
+/* ---- K-lbe + K-lbs + K-scan + K-select: exact k-NN over the index ------- */
+
+/* Exact k-NN of B device-resident queries.  Replaces query.py:296-348
+ * QueryEngine.exact_knn (one call answers the block).  out_d2/out_id/out_pos:
+ * B x k device arrays (id = original index incl. id_base, pos = leaf-order
+ * position); stats_host (nullable): B x 4 uint32 host array receiving
+ * (candidate leaves, candidate series, seed-leaf rows, 0) per query.
+ * Synchronizes `stream`. */
+int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, float *out_d2,
+              int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream);
+
+/* LB_EAPCA of B queries against every leaf (out: B x num_leaves float64,
+ * device) -- summarize.py:170-206 / query.py:127-135, bit-identical. */
+int ssb_index_lb_eapca(const ssb_index *index, const float *Q, int32_t B, double *out, void *stream);
+
+/* LB_SAX of one query PAA (16 float32, device) against rows of words --
+ * summarize.py:136-153 lb_sax_batch, bit-identical. lower/upper: 256 float64. */
+int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const double *lower,
+               const double *upper, int32_t n, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

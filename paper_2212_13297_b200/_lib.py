@@ -36,7 +36,44 @@ _SIGS = {
     "ssb_words": [P, I64, I32, P, P, P, P],
     "ssb_segment_stats": [P, I64, I32, P, P, I32, P, P, P],
     "ssb_bruteforce_knn": [P, I64, I32, P, I32, I32, I64, P, P, P],
+    "ssb_build": [P, I64, I32, P, P, P, P],
+    "ssb_index_free": [P],
+    "ssb_index_info": [P, P],
+    "ssb_index_node": [P, I32, P],
+    "ssb_index_arrays": [P, P, P, P, P],
+    "ssb_query": [P, P, I32, I32, P, P, P, P, P],
+    "ssb_index_download": [P, P, P, P],
+    "ssb_index_load": [P, P, P, I64, I32, I64, I64, P, I32, P, P, P],
+    "ssb_index_lb_eapca": [P, P, I32, P, P],
+    "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
 }
+
+M_MAX = 32
+
+
+class BuildCfg(ctypes.Structure):
+    _fields_ = [("leaf_threshold", ctypes.c_int64), ("initial_segments", ctypes.c_int32),
+                ("max_segments", ctypes.c_int32), ("id_base", ctypes.c_int64)]
+
+
+class IndexInfo(ctypes.Structure):
+    _fields_ = [("dataset_size", ctypes.c_int64), ("leaf_threshold", ctypes.c_int64),
+                ("id_base", ctypes.c_int64), ("series_length", ctypes.c_int32),
+                ("num_nodes", ctypes.c_int32), ("num_leaves", ctypes.c_int32),
+                ("levels", ctypes.c_int32), ("max_segments", ctypes.c_int32),
+                ("depth", ctypes.c_int32), ("build_ms", ctypes.c_double),
+                ("max_abs", ctypes.c_float)]
+
+
+class NodeRec(ctypes.Structure):
+    _fields_ = [("parent", ctypes.c_int32), ("left", ctypes.c_int32), ("right", ctypes.c_int32),
+                ("first", ctypes.c_uint32), ("count", ctypes.c_uint32), ("m", ctypes.c_int32),
+                ("endpoints", ctypes.c_int32 * M_MAX), ("envelope", (ctypes.c_float * 4) * M_MAX),
+                ("is_leaf", ctypes.c_int32), ("oversize", ctypes.c_int32), ("depth", ctypes.c_int32),
+                ("segment", ctypes.c_int32), ("attribute", ctypes.c_int32),
+                ("split_point", ctypes.c_int32), ("route_start", ctypes.c_int32),
+                ("route_end", ctypes.c_int32), ("threshold", ctypes.c_double),
+                ("gain", ctypes.c_double)]
 _RESTYPES = {
     "ssb_version": ctypes.c_int32,
     "ssb_last_error": ctypes.c_char_p,

@@ -1,0 +1,988 @@
+// build.cu -- K-split + K-part: level-synchronous bulk index build in HBM.
+//
+// Replaces the reference's per-series insertion build (build.py:213-263
+// insert_series_to_node/_split_leaf, tree.py:182-208 routing/widening) and the
+// write-time synopsis repair (persist.py:145-233 vsplit/hsplit_synopsis).
+// Every node with more than tau members is split using the reference's own
+// policy choice -- tree.py:211-336 get_best_split_policy (candidates in the
+// same order, same float32 statistics, same float64 thresholds and QoS gains,
+// first strict maximum) -- evaluated over ALL of the node's members, then
+// its members are stably partitioned (tree.py:339-381 split_node).  Children
+// envelopes are exact min/max over their members, so no synopsis repair is
+// needed.  Leaves come out contiguous and in in-order (left-to-right) order,
+// the reference's lrd.bin layout (persist.py:5-9).
+//
+// Per level (host loop, a few launches each):
+//   K-stats      member stats over base segments and both halves (f64 prefix
+//                sums, persist-exact), column-major per node
+//   K-minmax     per (node, stat column) min/max  -> envelopes, thresholds
+//   K-thr        per (node, candidate) threshold = (vmin+vmax)/2 (f64)
+//   K-eval       per (node, candidate, side, result column) min/max + n_left
+//   K-gain       per node: QoS gains (f64, numpy pairwise order), argmax
+//   K-part       stable partition of the split nodes' members (CUB scan)
+// Finally K-gather writes the rows, ids and words in leaf order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cub/device/device_scan.cuh>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "ssb_common.cuh"
+#include "ssb_index.h"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words,
+                 float *paa_out, cudaStream_t s);
+
+Index::~Index()
+{
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+// ---------------------------------------------------------------------------
+// device descriptors
+
+struct NodeDesc {
+    uint32_t first;      // member range start in perm
+    uint32_t count;
+    int32_t m;
+    int32_t allow_v;
+    int64_t aoff;        // offset of this node's members in the level's active space
+    int64_t stat_off;    // float offset of the node's stats block (6m columns x count)
+    int64_t acc_off;     // u32 offset of the node's eval accumulators
+    int32_t col_off;     // offset into per-level column arrays (6m per node)
+    int32_t ep[M_MAX];
+};
+
+struct Chunk {
+    uint32_t node;
+    uint32_t m0;   // first member (local index within node)
+    uint32_t cnt;  // <= 128
+};
+
+constexpr int CHUNK = 128;
+
+// stats column layout (6m columns): [0,m) base mean, [m,2m) base sd,
+// [2m,3m) left-half mean, [3m,4m) left-half sd, [4m,5m) right-half mean,
+// [5m,6m) right-half sd.  Column-major: stats[stat_off + col*count + i].
+
+__device__ __forceinline__ uint32_t okey(float f)
+{
+    uint32_t b = __float_as_uint(f);
+    return b ^ ((b & 0x80000000u) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float okey_inv(uint32_t k)
+{
+    return __uint_as_float(k ^ ((k & 0x80000000u) ? 0x80000000u : 0xffffffffu));
+}
+
+__device__ __forceinline__ void stats_w(double ca, double cb, double c2a, double c2b, int w,
+                                        float &mean, float &sd)
+{
+    const double wd = (double)w;
+    const double mu = __ddiv_rn(__dsub_rn(cb, ca), wd);
+    const double msq = __ddiv_rn(__dsub_rn(c2b, c2a), wd);
+    const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
+    mean = __double2float_rn(mu);
+    sd = __double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
+}
+
+// K-stats: one CTA per chunk (<=128 members of one node); rows are staged
+// 64 columns at a time through padded shared memory, then each thread walks
+// its row sequentially (np.cumsum order) and emits the 6m statistics.
+__global__ void __launch_bounds__(CHUNK)
+    build_stats_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
+                       const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                       float *__restrict__ stats, int *__restrict__ nonfinite)
+{
+    __shared__ float tile[CHUNK][65];
+    __shared__ NodeDesc nd;
+    const Chunk ch = chunks[blockIdx.x];
+    if (threadIdx.x == 0) nd = nodes[ch.node];
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int m = nd.m;
+    const bool live = t < (int)ch.cnt;
+
+    double a = 0.0, b = 0.0;     // running prefix sums
+    double ca = 0.0, c2a = 0.0;  // at the current segment start
+    double cm = 0.0, c2m = 0.0;  // at the current segment midpoint
+    int seg = 0;
+    int sa = 0, sb = nd.ep[0], mid = sb / 2;  // segment [sa, sb), mid = (sa+sb)/2
+    int bad = 0;
+    const int64_t cnt = nd.count;
+    float *out = stats + nd.stat_off + ch.m0 + t;
+
+    for (int c0 = 0; c0 < n; c0 += 64) {
+        const int w = min(64, n - c0);
+        // cooperative, coalesced load of the chunk rows' columns [c0, c0+w)
+        for (int idx = t; idx < CHUNK * 16; idx += CHUNK) {
+            const int r = idx >> 4, q4 = idx & 15;
+            if (r < (int)ch.cnt && q4 * 4 < w) {
+                const uint32_t rr = perm[nd.first + ch.m0 + r];
+                const float4 f = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)rr * n + c0) + q4);
+                tile[r][q4 * 4 + 0] = f.x;
+                tile[r][q4 * 4 + 1] = f.y;
+                tile[r][q4 * 4 + 2] = f.z;
+                tile[r][q4 * 4 + 3] = f.w;
+            }
+        }
+        __syncthreads();
+        if (live) {
+            for (int i = 0; i < w; i++) {
+                const float xf = tile[t][i];
+                bad |= !isfinite(xf);
+                const double v = (double)xf;
+                a = __dadd_rn(a, v);
+                b = __dadd_rn(b, __dmul_rn(v, v));
+                const int p = c0 + i + 1;  // prefix point index now available
+                if (p == mid) {
+                    cm = a;
+                    c2m = b;
+                }
+                if (p == sb) {
+                    float mu, sd;
+                    stats_w(ca, a, c2a, b, sb - sa, mu, sd);
+                    out[(int64_t)seg * cnt] = mu;
+                    out[(int64_t)(m + seg) * cnt] = sd;
+                    if (sb - sa >= 2) {
+                        stats_w(ca, cm, c2a, c2m, mid - sa, mu, sd);
+                        out[(int64_t)(2 * m + seg) * cnt] = mu;
+                        out[(int64_t)(3 * m + seg) * cnt] = sd;
+                        stats_w(cm, a, c2m, b, sb - mid, mu, sd);
+                        out[(int64_t)(4 * m + seg) * cnt] = mu;
+                        out[(int64_t)(5 * m + seg) * cnt] = sd;
+                    }
+                    ca = a;
+                    c2a = b;
+                    seg++;
+                    if (seg < m) {
+                        sa = sb;
+                        sb = nd.ep[seg];
+                        mid = (sa + sb) / 2;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (bad) atomicOr(nonfinite, 1);
+}
+
+// K-minmax: per (node, column) min/max over members (ordered-int atomics)
+__global__ void __launch_bounds__(CHUNK)
+    build_minmax_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                        const float *__restrict__ stats, uint32_t *__restrict__ cmin,
+                        uint32_t *__restrict__ cmax)
+{
+    const Chunk ch = chunks[blockIdx.x];
+    const NodeDesc nd = nodes[ch.node];
+    const int t = threadIdx.x, lane = t & 31;
+    const bool live = t < (int)ch.cnt;
+    const int ncol = 6 * nd.m;
+    for (int col = 0; col < ncol; col++) {
+        const int seg = col % nd.m;
+        const int sa = seg ? nd.ep[seg - 1] : 0;
+        if (col >= 2 * nd.m && nd.ep[seg] - sa < 2) continue;  // no halves
+        float v = live ? stats[nd.stat_off + (int64_t)col * nd.count + ch.m0 + t] : 0.f;
+        uint32_t k = okey(v);
+        uint32_t kmin = __reduce_min_sync(0xffffffffu, live ? k : 0xffffffffu);
+        uint32_t kmax = __reduce_max_sync(0xffffffffu, live ? k : 0u);
+        if (lane == 0 && (ch.cnt > (unsigned)(t & ~31))) {
+            atomicMin(&cmin[nd.col_off + col], kmin);
+            atomicMax(&cmax[nd.col_off + col], kmax);
+        }
+    }
+}
+
+// candidate c of a node (tree.py:220-237 order): seg = c/6, r = c%6,
+// attr = r/3 (0 mean, 1 sd), lay = r%3 (0 horizontal, 1 left half, 2 right half)
+__device__ __forceinline__ int route_col(int m, int c)
+{
+    const int seg = c / 6, r = c % 6, attr = r / 3, lay = r % 3;
+    return (2 * lay + attr) * m + seg;
+}
+
+// K-thr: per (node, candidate): validity and float64 threshold (tree.py:311-318)
+__global__ void build_thr_kernel(const NodeDesc *__restrict__ nodes, int nnodes,
+                                 const uint32_t *__restrict__ cmin, const uint32_t *__restrict__ cmax,
+                                 double *__restrict__ thr, int32_t *__restrict__ valid)
+{
+    const int f = blockIdx.x;
+    if (f >= nnodes) return;
+    const NodeDesc nd = nodes[f];
+    for (int c = threadIdx.x; c < 6 * nd.m; c += blockDim.x) {
+        const int seg = c / 6, lay = (c % 6) % 3;
+        const int sa = seg ? nd.ep[seg - 1] : 0, w = nd.ep[seg] - sa;
+        int ok = lay == 0 || (w >= 2 && nd.allow_v);
+        const int col = route_col(nd.m, c);
+        const float vmin = okey_inv(cmin[nd.col_off + col]);
+        const float vmax = okey_inv(cmax[nd.col_off + col]);
+        if (vmin == vmax) ok = 0;
+        valid[nd.col_off + c] = ok;
+        thr[nd.col_off + c] = __dmul_rn(__dadd_rn((double)vmin, (double)vmax), 0.5);
+    }
+}
+
+// result segmentation of candidate c: mm columns; column j -> (mean col, sd col, width)
+__device__ __forceinline__ void result_col(const NodeDesc &nd, int c, int j, int &cmean, int &csd,
+                                           int &w)
+{
+    const int m = nd.m, seg = c / 6, lay = (c % 6) % 3;
+    if (lay == 0 || j < seg) {
+        const int s = j;
+        cmean = s;
+        csd = m + s;
+        w = nd.ep[s] - (s ? nd.ep[s - 1] : 0);
+        return;
+    }
+    const int sa = seg ? nd.ep[seg - 1] : 0, sb = nd.ep[seg], mid = (sa + sb) / 2;
+    if (j == seg) {
+        cmean = 2 * m + seg;
+        csd = 3 * m + seg;
+        w = mid - sa;
+    } else if (j == seg + 1) {
+        cmean = 4 * m + seg;
+        csd = 5 * m + seg;
+        w = sb - mid;
+    } else {
+        const int s = j - 1;
+        cmean = s;
+        csd = m + s;
+        w = nd.ep[s] - (s ? nd.ep[s - 1] : 0);
+    }
+}
+
+// accumulator layout per node: [cand][side][col(M_MAX+1)][attr][min,max] u32 (ordered keys)
+__device__ __forceinline__ int64_t acc_index(int c, int side, int j, int attr, int mx)
+{
+    return ((((int64_t)c * 2 + side) * (M_MAX + 1) + j) * 2 + attr) * 2 + mx;
+}
+constexpr int ACC_PER_CAND = 2 * (M_MAX + 1) * 2 * 2;
+
+// K-eval: grid (chunk, candidate batch).  Per valid candidate: side of every
+// member, masked min/max of every result column on both sides, n_left.
+constexpr int CAND_BATCH = 6;
+
+__global__ void __launch_bounds__(CHUNK)
+    build_eval_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                      const float *__restrict__ stats, const double *__restrict__ thr,
+                      const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
+                      uint32_t *__restrict__ nleft)
+{
+    const Chunk ch = chunks[blockIdx.x];
+    const NodeDesc nd = nodes[ch.node];
+    const int c0 = blockIdx.y * CAND_BATCH;
+    if (c0 >= 6 * nd.m) return;
+    const int t = threadIdx.x, lane = t & 31;
+    const bool live = t < (int)ch.cnt;
+    const bool warp_live = (int)ch.cnt > (t & ~31);
+    if (!warp_live) return;
+    const float *st = stats + nd.stat_off + ch.m0 + t;
+    uint32_t *nacc = acc + nd.acc_off;
+    for (int c = c0; c < min(c0 + CAND_BATCH, 6 * nd.m); c++) {
+        if (!valid[nd.col_off + c]) continue;
+        const int rc = route_col(nd.m, c);
+        const double th = thr[nd.col_off + c];
+        const float rv = live ? st[(int64_t)rc * nd.count] : 0.f;
+        const bool left = live && ((double)rv < th);
+        const unsigned bl = __ballot_sync(0xffffffffu, left);
+        if (lane == 0) atomicAdd(&nleft[nd.col_off + c], (unsigned)__popc(bl));
+        const int seg = c / 6, lay = (c % 6) % 3;
+        const int mm = nd.m + (lay ? 1 : 0);
+        (void)seg;
+        for (int j = 0; j < mm; j++) {
+            int cmean, csd, w;
+            result_col(nd, c, j, cmean, csd, w);
+#pragma unroll
+            for (int attr = 0; attr < 2; attr++) {
+                const float v = live ? st[(int64_t)(attr ? csd : cmean) * nd.count] : 0.f;
+                const uint32_t k = okey(v);
+                const uint32_t lmin = __reduce_min_sync(0xffffffffu, (live && left) ? k : 0xffffffffu);
+                const uint32_t lmax = __reduce_max_sync(0xffffffffu, (live && left) ? k : 0u);
+                const uint32_t rmin = __reduce_min_sync(0xffffffffu, (live && !left) ? k : 0xffffffffu);
+                const uint32_t rmax = __reduce_max_sync(0xffffffffu, (live && !left) ? k : 0u);
+                if (lane == 0) {
+                    atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin);
+                    atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax);
+                    atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin);
+                    atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax);
+                }
+            }
+        }
+    }
+}
+
+// tree.py:211-217 _qos over one side (or the union), float64, numpy pairwise order
+__device__ double qos_side(const NodeDesc &nd, const uint32_t *nacc, int c, int which /*0 L,1 R,2 both*/)
+{
+    const int lay = (c % 6) % 3;
+    const int mm = nd.m + (lay ? 1 : 0);
+    double tt[M_MAX + 1];
+    for (int j = 0; j < mm; j++) {
+        int cmean, csd, w;
+        result_col(nd, c, j, cmean, csd, w);
+        float mn[2], mx[2];
+        for (int attr = 0; attr < 2; attr++) {
+            if (which == 2) {
+                mn[attr] = fminf(okey_inv(nacc[acc_index(c, 0, j, attr, 0)]),
+                                 okey_inv(nacc[acc_index(c, 1, j, attr, 0)]));
+                mx[attr] = fmaxf(okey_inv(nacc[acc_index(c, 0, j, attr, 1)]),
+                                 okey_inv(nacc[acc_index(c, 1, j, attr, 1)]));
+            } else {
+                mn[attr] = okey_inv(nacc[acc_index(c, which, j, attr, 0)]);
+                mx[attr] = okey_inv(nacc[acc_index(c, which, j, attr, 1)]);
+            }
+        }
+        const double dm = (double)__fsub_rn(mx[0], mn[0]);
+        const double ds = (double)__fsub_rn(mx[1], mn[1]);
+        tt[j] = __dmul_rn((double)w, __dadd_rn(__dmul_rn(dm, dm), __dmul_rn(ds, ds)));
+    }
+    return pw_f64_small(tt, mm);
+}
+
+struct NodeResult {
+    int32_t best;   // candidate index or -1
+    int32_t nl;
+    double gain;
+    double thr;
+};
+
+// K-gain: one warp per node; lanes evaluate candidates; first strict maximum
+__global__ void build_gain_kernel(const NodeDesc *__restrict__ nodes, int nnodes,
+                                  const double *__restrict__ thr, const int32_t *__restrict__ valid,
+                                  const uint32_t *__restrict__ acc, const uint32_t *__restrict__ nleft,
+                                  NodeResult *__restrict__ res)
+{
+    const int f = blockIdx.x;
+    if (f >= nnodes) return;
+    const NodeDesc nd = nodes[f];
+    const int lane = threadIdx.x;
+    double best_g = 0.0;
+    int best_c = -1;
+    const uint32_t *nacc = acc + nd.acc_off;
+    for (int c = lane; c < 6 * nd.m; c += 32) {
+        if (!valid[nd.col_off + c]) continue;
+        const double rho = (double)nd.count;
+        const double nl = (double)nleft[nd.col_off + c];
+        const double nr = __dsub_rn(rho, nl);
+        const double qa = qos_side(nd, nacc, c, 2);
+        const double ql = qos_side(nd, nacc, c, 0);
+        const double qr = qos_side(nd, nacc, c, 1);
+        const double g = __dsub_rn(qa, __ddiv_rn(__dadd_rn(__dmul_rn(nl, ql), __dmul_rn(nr, qr)), rho));
+        if (g > best_g) {  // lanes visit candidates in increasing order
+            best_g = g;
+            best_c = c;
+        }
+    }
+    // warp argmax: larger gain wins; equal gains -> lower candidate index
+    for (int off = 16; off; off >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, best_g, off);
+        const int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+        if (oc >= 0 && (best_c < 0 || og > best_g || (og == best_g && oc < best_c))) {
+            best_g = og;
+            best_c = oc;
+        }
+    }
+    if (lane == 0) {
+        NodeResult r;
+        r.best = best_c;
+        r.gain = best_c >= 0 ? best_g : 0.0;
+        r.nl = best_c >= 0 ? (int32_t)nleft[nd.col_off + best_c] : 0;
+        r.thr = best_c >= 0 ? thr[nd.col_off + best_c] : 0.0;
+        res[f] = r;
+    }
+}
+
+// fallback policy (tree.py:331-335): horizontal mean split of segment 0 at the
+// envelope midpoint; count its left side.
+__global__ void build_fallback_count_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                                            const float *__restrict__ stats,
+                                            const double *__restrict__ fthr, const int32_t *__restrict__ need,
+                                            uint32_t *__restrict__ fnl)
+{
+    const Chunk ch = chunks[blockIdx.x];
+    if (!need[ch.node]) return;
+    const NodeDesc nd = nodes[ch.node];
+    const int t = threadIdx.x;
+    bool left = false;
+    if (t < (int)ch.cnt) left = (double)stats[nd.stat_off + ch.m0 + t] < fthr[ch.node];
+    const unsigned bl = __ballot_sync(0xffffffffu, left);
+    if ((t & 31) == 0 && bl) atomicAdd(&fnl[ch.node], (unsigned)__popc(bl));
+}
+
+// K-part flags: 1 = goes left under the node's chosen policy (route col, thr)
+__global__ void build_flags_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                                   const float *__restrict__ stats, const int32_t *__restrict__ pcol,
+                                   const double *__restrict__ pthr, uint32_t *__restrict__ flags)
+{
+    const Chunk ch = chunks[blockIdx.x];
+    const NodeDesc nd = nodes[ch.node];
+    const int t = threadIdx.x;
+    if (t >= (int)ch.cnt) return;
+    const int col = pcol[ch.node];
+    uint32_t f = 0;
+    if (col >= 0) {
+        const float v = stats[nd.stat_off + (int64_t)col * nd.count + ch.m0 + t];
+        f = (double)v < pthr[ch.node] ? 1u : 0u;
+    }
+    flags[nd.aoff + ch.m0 + t] = f;
+}
+
+__global__ void build_scatter_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                                     const int32_t *__restrict__ pcol, const uint32_t *__restrict__ flags,
+                                     const uint32_t *__restrict__ scan, const uint32_t *__restrict__ perm,
+                                     uint32_t *__restrict__ perm_out)
+{
+    const Chunk ch = chunks[blockIdx.x];
+    const NodeDesc nd = nodes[ch.node];
+    const int t = threadIdx.x;
+    if (t >= (int)ch.cnt || pcol[ch.node] < 0) return;
+    const int64_t i = ch.m0 + t;
+    const int64_t a = nd.aoff;
+    const uint32_t base = scan[a];
+    const uint32_t nl = scan[a + nd.count] - base;
+    const uint32_t lr = scan[a + i] - base;
+    const uint32_t dst = flags[a + i] ? lr : nl + ((uint32_t)i - lr);
+    perm_out[nd.first + dst] = perm[nd.first + i];
+}
+
+// final gather into leaf order
+__global__ void gather_rows_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
+                                   int64_t N, float *__restrict__ Xo, uint32_t *__restrict__ inv)
+{
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= N) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t src = perm[row];
+    const float4 *s = reinterpret_cast<const float4 *>(X + (int64_t)src * n);
+    float4 *d = reinterpret_cast<float4 *>(Xo + row * n);
+    for (int i = lane; i < n / 4; i += 32) d[i] = __ldg(s + i);
+    if (lane == 0) inv[src] = (uint32_t)row;
+}
+
+__global__ void absmax_kernel(const float *__restrict__ X, int64_t count, uint32_t *__restrict__ out)
+{
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(X[i]));
+    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+__global__ void fill_u32_kernel(uint32_t *p, int64_t count, uint32_t v)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) p[i] = v;
+}
+
+__global__ void fill_acc_kernel(uint32_t *p, int64_t count)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) p[i] = (i & 1) ? 0u : 0xffffffffu;
+}
+
+// copy the winning candidate's accumulator block of every split node
+__global__ void gather_winner_acc_kernel(const NodeDesc *__restrict__ nodes, const NodeResult *__restrict__ res,
+                                         const uint32_t *__restrict__ acc, uint32_t *__restrict__ out)
+{
+    const int f = blockIdx.x;
+    const int best = res[f].best;
+    for (int i = threadIdx.x; i < ACC_PER_CAND; i += blockDim.x)
+        out[(int64_t)f * ACC_PER_CAND + i] = best >= 0 ? acc[nodes[f].acc_off + (int64_t)best * ACC_PER_CAND + i] : 0u;
+}
+
+__global__ void iota_u32_kernel(uint32_t *p, int64_t count)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) p[i] = (uint32_t)i;
+}
+
+static int fill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
+{
+    if (count <= 0) return OK;
+    fill_u32_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p, count, v);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+
+struct BuildCfg {
+    int64_t tau;
+    int32_t initial_segments;
+    int32_t max_segments;
+    int64_t id_base;
+};
+
+#define RC(x)                   \
+    do {                        \
+        int _rc = (x);          \
+        if (_rc) return _rc;    \
+    } while (0)
+
+int finalize_tree(Index &ix, cudaStream_t s);
+
+int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg,
+                Index **out, cudaStream_t s)
+{
+    SSB_REQUIRE(n > 0 && n % WORD_SEGMENTS == 0, "series length must be a positive multiple of 16");
+    SSB_REQUIRE(n <= MAX_SERIES_LEN, "series length above 1024 is not supported");
+    SSB_REQUIRE(N >= 1 && N + cfg.id_base < (1ll << 32), "need 1 <= N and ids below 2^32");
+    SSB_REQUIRE(cfg.tau >= 1, "leaf threshold must be positive");
+    const int mmax = cfg.max_segments > 0 ? std::min(cfg.max_segments, M_MAX) : M_MAX;
+    const int s0 = std::max(1, cfg.initial_segments);
+    SSB_REQUIRE(s0 <= mmax && s0 <= n, "initial_segments must be in [1, min(n, max_segments)]");
+    auto t_start = std::chrono::steady_clock::now();
+
+    std::unique_ptr<Index> ix(new Index());
+    ix->N = N;
+    ix->n = n;
+    ix->tau = cfg.tau;
+    ix->id_base = cfg.id_base;
+
+    // root
+    TreeNode root;
+    root.first = 0;
+    root.count = (uint32_t)N;
+    root.m = s0;
+    for (int i = 0; i < s0; i++) root.ep[i] = (int32_t)((int64_t)n * (i + 1) / s0);
+    ix->nodes.push_back(root);
+
+    DevBuf perm_a, perm_b, nonfinite, amax;
+    SSB_CUDA(perm_a.alloc((size_t)N * 4, s));
+    SSB_CUDA(perm_b.alloc((size_t)N * 4, s));
+    SSB_CUDA(nonfinite.alloc(4, s));
+    SSB_CUDA(amax.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(nonfinite.p, 0, 4, s));
+    SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));
+    iota_u32_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(perm_a.as<uint32_t>(), N);
+    SSB_CHECK_LAUNCH();
+    absmax_kernel<<<4 * num_sms(), 256, 0, s>>>(X, N * n, amax.as<uint32_t>());
+    SSB_CHECK_LAUNCH();
+    uint32_t *perm = perm_a.as<uint32_t>(), *perm2 = perm_b.as<uint32_t>();
+
+    std::vector<int32_t> frontier = {0};  // nodes needing stats this level
+    int level = 0;
+    while (!frontier.empty()) {
+        // ---- level descriptors ------------------------------------------------
+        const int F = (int)frontier.size();
+        std::vector<NodeDesc> nd(F);
+        std::vector<Chunk> chunks;
+        int64_t aoff = 0, stat_off = 0, acc_off = 0;
+        int32_t col_off = 0;
+        for (int f = 0; f < F; f++) {
+            const TreeNode &tn = ix->nodes[frontier[f]];
+            NodeDesc &d = nd[f];
+            d.first = tn.first;
+            d.count = tn.count;
+            d.m = tn.m;
+            d.allow_v = tn.m < mmax;
+            d.aoff = aoff;
+            d.stat_off = stat_off;
+            d.acc_off = acc_off;
+            d.col_off = col_off;
+            for (int i = 0; i < M_MAX; i++) d.ep[i] = i < tn.m ? tn.ep[i] : n;
+            for (uint32_t m0 = 0; m0 < tn.count; m0 += CHUNK)
+                chunks.push_back({(uint32_t)f, m0, std::min<uint32_t>(CHUNK, tn.count - m0)});
+            aoff += tn.count;
+            stat_off += (int64_t)6 * tn.m * tn.count;
+            acc_off += (int64_t)6 * tn.m * ACC_PER_CAND;
+            col_off += 6 * tn.m;
+        }
+        const int64_t nchunks = (int64_t)chunks.size();
+        SSB_REQUIRE(nchunks < (1ll << 31), "too many member chunks in one level");
+        DevBuf d_nodes, d_chunks, d_stats, d_cmin, d_cmax, d_thr, d_valid, d_acc, d_nleft, d_res;
+        SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
+        SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
+        SSB_CUDA(d_stats.alloc(sizeof(float) * (size_t)stat_off, s));
+        SSB_CUDA(d_cmin.alloc(4 * (size_t)col_off, s));
+        SSB_CUDA(d_cmax.alloc(4 * (size_t)col_off, s));
+        SSB_CUDA(d_thr.alloc(8 * (size_t)col_off, s));
+        SSB_CUDA(d_valid.alloc(4 * (size_t)col_off, s));
+        SSB_CUDA(d_acc.alloc(4 * (size_t)acc_off, s));
+        SSB_CUDA(d_nleft.alloc(4 * (size_t)col_off, s));
+        SSB_CUDA(d_res.alloc(sizeof(NodeResult) * F, s));
+        SSB_CUDA(cudaMemcpyAsync(d_nodes.p, nd.data(), sizeof(NodeDesc) * F, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(d_chunks.p, chunks.data(), sizeof(Chunk) * nchunks,
+                                 cudaMemcpyHostToDevice, s));
+        RC(fill_u32(d_cmin.as<uint32_t>(), col_off, 0xffffffffu, s));
+        RC(fill_u32(d_cmax.as<uint32_t>(), col_off, 0u, s));
+        RC(fill_u32(d_nleft.as<uint32_t>(), col_off, 0u, s));
+        // accumulators: even slots are minima (+inf key), odd slots maxima (0)
+        fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
+        SSB_CHECK_LAUNCH();
+
+        {
+            ProfScope ps("build_stats", s, (double)aoff * n * 4 + (double)stat_off * 4);
+            build_stats_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(X, n, perm, d_nodes.as<NodeDesc>(),
+                                                                   d_chunks.as<Chunk>(), d_stats.as<float>(),
+                                                                   nonfinite.as<int>());
+        }
+        SSB_CHECK_LAUNCH();
+        build_minmax_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                                d_stats.as<float>(), d_cmin.as<uint32_t>(),
+                                                                d_cmax.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+
+        // which frontier nodes must split (count > tau) vs only need an envelope (root leaf)
+        std::vector<int32_t> need_split(F);
+        bool any_split = false;
+        for (int f = 0; f < F; f++) {
+            need_split[f] = ix->nodes[frontier[f]].count > (uint32_t)cfg.tau;
+            any_split |= need_split[f] != 0;
+        }
+        std::vector<NodeResult> res(F);
+        std::vector<int32_t> pcol(F, -1);
+        std::vector<double> pthr(F, 0.0);
+        std::vector<uint32_t> env_min((size_t)col_off), env_max((size_t)col_off);
+        if (any_split) {
+            build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_cmin.as<uint32_t>(),
+                                              d_cmax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
+            SSB_CHECK_LAUNCH();
+            int maxm = 1;
+            for (auto &d : nd) maxm = std::max(maxm, d.m);
+            dim3 eg((unsigned)nchunks, (unsigned)((6 * maxm + CAND_BATCH - 1) / CAND_BATCH));
+            {
+                ProfScope ps("build_eval", s, (double)stat_off * 4);
+                build_eval_kernel<<<eg, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                       d_stats.as<float>(), d_thr.as<double>(),
+                                                       d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
+                                                       d_nleft.as<uint32_t>());
+            }
+            SSB_CHECK_LAUNCH();
+            build_gain_kernel<<<F, 32, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_thr.as<double>(),
+                                               d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
+                                               d_nleft.as<uint32_t>(), d_res.as<NodeResult>());
+            SSB_CHECK_LAUNCH();
+            SSB_CUDA(cudaMemcpyAsync(res.data(), d_res.p, sizeof(NodeResult) * F, cudaMemcpyDeviceToHost, s));
+        }
+        SSB_CUDA(cudaMemcpyAsync(env_min.data(), d_cmin.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(env_max.data(), d_cmax.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        int bad = 0;
+        SSB_CUDA(cudaMemcpy(&bad, nonfinite.p, 4, cudaMemcpyDeviceToHost));
+        SSB_REQUIRE(!bad, "dataset contains non-finite values");
+
+        auto inv_key = [](uint32_t k) {
+            uint32_t b = k ^ ((k & 0x80000000u) ? 0x80000000u : 0xffffffffu);
+            float f;
+            std::memcpy(&f, &b, 4);
+            return f;
+        };
+        // node envelopes (base columns) -- exact min/max over the members
+        for (int f = 0; f < F; f++) {
+            TreeNode &tn = ix->nodes[frontier[f]];
+            for (int i = 0; i < tn.m; i++) {
+                tn.env[i][0] = inv_key(env_min[nd[f].col_off + i]);
+                tn.env[i][1] = inv_key(env_max[nd[f].col_off + i]);
+                tn.env[i][2] = inv_key(env_min[nd[f].col_off + tn.m + i]);
+                tn.env[i][3] = inv_key(env_max[nd[f].col_off + tn.m + i]);
+            }
+        }
+        if (!any_split) break;
+
+        // fallback policies for nodes with no positive-gain candidate
+        std::vector<int32_t> need_fb(F, 0);
+        std::vector<double> fthr(F, 0.0);
+        bool any_fb = false;
+        for (int f = 0; f < F; f++) {
+            if (!need_split[f] || res[f].best >= 0) continue;
+            const TreeNode &tn = ix->nodes[frontier[f]];
+            double mu = std::isfinite(tn.env[0][0]) ? (double)tn.env[0][0] : 0.0;
+            double mx = std::isfinite(tn.env[0][1]) ? (double)tn.env[0][1] : 0.0;
+            fthr[f] = (mu + mx) / 2.0;
+            need_fb[f] = 1;
+            any_fb = true;
+        }
+        std::vector<uint32_t> fnl(F, 0);
+        if (any_fb) {
+            DevBuf d_need, d_fthr, d_fnl;
+            SSB_CUDA(d_need.alloc(4 * F, s));
+            SSB_CUDA(d_fthr.alloc(8 * F, s));
+            SSB_CUDA(d_fnl.alloc(4 * F, s));
+            SSB_CUDA(cudaMemcpyAsync(d_need.p, need_fb.data(), 4 * F, cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemcpyAsync(d_fthr.p, fthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemsetAsync(d_fnl.p, 0, 4 * F, s));
+            build_fallback_count_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(
+                d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(), d_stats.as<float>(), d_fthr.as<double>(),
+                d_need.as<int32_t>(), d_fnl.as<uint32_t>());
+            SSB_CHECK_LAUNCH();
+            SSB_CUDA(cudaMemcpyAsync(fnl.data(), d_fnl.p, 4 * F, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+        }
+
+        // decide splits; create children on the host
+        std::vector<int32_t> next;
+        std::vector<std::vector<uint32_t>> child_acc(F);
+        bool any_part = false;
+        // fetch the winning candidates' accumulators (children envelopes)
+        std::vector<uint32_t> acc_h((size_t)F * ACC_PER_CAND);
+        {
+            DevBuf d_win;
+            SSB_CUDA(d_win.alloc(4 * acc_h.size(), s));
+            gather_winner_acc_kernel<<<F, 256, 0, s>>>(d_nodes.as<NodeDesc>(), d_res.as<NodeResult>(),
+                                                      d_acc.as<uint32_t>(), d_win.as<uint32_t>());
+            SSB_CHECK_LAUNCH();
+            SSB_CUDA(cudaMemcpyAsync(acc_h.data(), d_win.p, 4 * acc_h.size(), cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+        }
+        for (int f = 0; f < F; f++) {
+            if (!need_split[f]) continue;
+            const int32_t id = frontier[f];
+            TreeNode tn = ix->nodes[id];
+            int best = res[f].best;
+            int32_t nl;
+            int seg, attr, lay;
+            double th;
+            if (best >= 0) {
+                seg = best / 6;
+                attr = (best % 6) / 3;
+                lay = (best % 6) % 3;
+                th = res[f].thr;
+                nl = res[f].nl;
+            } else {
+                seg = 0;
+                attr = 0;
+                lay = 0;
+                th = fthr[f];
+                nl = (int32_t)fnl[f];
+            }
+            if (nl <= 0 || (uint32_t)nl >= tn.count) {
+                // cannot separate (identical members): an oversize leaf
+                ix->nodes[id].oversize = 1;
+                continue;
+            }
+            const int sa = seg ? tn.ep[seg - 1] : 0, sb = tn.ep[seg], mid = (sa + sb) / 2;
+            TreeNode &P = ix->nodes[id];
+            P.is_leaf = 0;
+            P.seg = seg;
+            P.attr = attr;
+            P.split = lay ? mid : -1;
+            P.rs = lay == 2 ? mid : sa;
+            P.re = lay == 1 ? mid : sb;
+            P.thr = th;
+            P.gain = best >= 0 ? res[f].gain : 0.0;
+            pcol[f] = best >= 0 ? (2 * lay + attr) * tn.m + seg : 0;  // fallback: base mean col 0
+            pthr[f] = th;
+            any_part = true;
+            TreeNode L, R;
+            L.parent = R.parent = id;
+            L.depth = R.depth = tn.depth + 1;
+            L.first = tn.first;
+            L.count = (uint32_t)nl;
+            R.first = tn.first + (uint32_t)nl;
+            R.count = tn.count - (uint32_t)nl;
+            int mm = tn.m;
+            if (lay) {
+                mm = tn.m + 1;
+                int k = 0;
+                for (int i = 0; i < tn.m; i++) {
+                    if (i == seg) L.ep[k++] = mid;
+                    L.ep[k++] = tn.ep[i];
+                }
+            } else {
+                for (int i = 0; i < tn.m; i++) L.ep[i] = tn.ep[i];
+            }
+            L.m = R.m = mm;
+            for (int i = 0; i < mm; i++) R.ep[i] = L.ep[i];
+            if (best >= 0) {
+                const uint32_t *a = acc_h.data() + (size_t)f * ACC_PER_CAND;
+                auto at = [&](int side, int j, int at_, int mx) {
+                    return inv_key(a[(((side * (M_MAX + 1) + j) * 2 + at_) * 2) + mx]);
+                };
+                for (int j = 0; j < mm; j++) {
+                    L.env[j][0] = at(0, j, 0, 0);
+                    L.env[j][1] = at(0, j, 0, 1);
+                    L.env[j][2] = at(0, j, 1, 0);
+                    L.env[j][3] = at(0, j, 1, 1);
+                    R.env[j][0] = at(1, j, 0, 0);
+                    R.env[j][1] = at(1, j, 0, 1);
+                    R.env[j][2] = at(1, j, 1, 0);
+                    R.env[j][3] = at(1, j, 1, 1);
+                }
+            }
+            const int32_t lid = (int32_t)ix->nodes.size();
+            ix->nodes.push_back(L);
+            ix->nodes.push_back(R);
+            ix->nodes[id].left = lid;
+            ix->nodes[id].right = lid + 1;
+            // children that must split again need stats next level; fallback
+            // children also need their envelopes from the next level's stats
+            for (int32_t cid : {lid, lid + 1})
+                if (ix->nodes[cid].count > (uint32_t)cfg.tau || best < 0) next.push_back(cid);
+        }
+
+        if (any_part) {
+            DevBuf d_pcol, d_pthr, d_flags, d_scan, d_tmp;
+            SSB_CUDA(d_pcol.alloc(4 * F, s));
+            SSB_CUDA(d_pthr.alloc(8 * F, s));
+            SSB_CUDA(d_flags.alloc(4 * (size_t)(aoff + 1), s));
+            SSB_CUDA(d_scan.alloc(4 * (size_t)(aoff + 1), s));
+            for (int f = 0; f < F; f++)
+                if (!need_split[f] || ix->nodes[frontier[f]].is_leaf) pcol[f] = -1;
+            SSB_CUDA(cudaMemcpyAsync(d_pcol.p, pcol.data(), 4 * F, cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemcpyAsync(d_pthr.p, pthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemsetAsync(d_flags.as<uint32_t>() + aoff, 0, 4, s));
+            build_flags_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                                   d_stats.as<float>(), d_pcol.as<int32_t>(),
+                                                                   d_pthr.as<double>(), d_flags.as<uint32_t>());
+            SSB_CHECK_LAUNCH();
+            size_t tmp_bytes = 0;
+            SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flags.as<uint32_t>(),
+                                                   d_scan.as<uint32_t>(), (int)(aoff + 1), s));
+            SSB_CUDA(d_tmp.alloc(tmp_bytes, s));
+            SSB_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.p, tmp_bytes, d_flags.as<uint32_t>(),
+                                                   d_scan.as<uint32_t>(), (int)(aoff + 1), s));
+            note_launch(1);
+            SSB_CUDA(cudaMemcpyAsync(perm2, perm, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+            build_scatter_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                                     d_pcol.as<int32_t>(), d_flags.as<uint32_t>(),
+                                                                     d_scan.as<uint32_t>(), perm, perm2);
+            SSB_CHECK_LAUNCH();
+            std::swap(perm, perm2);
+        }
+        frontier.swap(next);
+        level++;
+        SSB_REQUIRE(level < 4096, "index build did not converge");
+    }
+    ix->levels = level;
+    RC(finalize_tree(*ix, s));
+    SSB_CUDA(cudaMalloc(&ix->X, (size_t)N * n * 4));
+    SSB_CUDA(cudaMalloc(&ix->words, (size_t)N * WORD_SEGMENTS));
+    SSB_CUDA(cudaMalloc(&ix->orig, (size_t)N * 4));
+    SSB_CUDA(cudaMalloc(&ix->inv, (size_t)N * 4));
+    SSB_CUDA(cudaMalloc(&ix->bp, 8 * (ALPHABET - 1)));
+    SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->orig, perm, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+    {
+        ProfScope ps("build_gather", s, 2.0 * N * n * 4 + 12.0 * N);
+        gather_rows_kernel<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(X, n, perm, N, ix->X, ix->inv);
+    }
+    SSB_CHECK_LAUNCH();
+    RC(launch_words(ix->X, N, n, ix->bp, ix->words, nullptr, s));
+    uint32_t am = 0;
+    SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&ix->max_abs, &am, 4);
+    ix->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    *out = ix.release();
+    return OK;
+}
+
+// leaves in in-order + device leaf table (shared by build and load)
+int finalize_tree(Index &ixr, cudaStream_t s)
+{
+    Index *ix = &ixr;
+    const int n = ix->n;
+    ix->leaves.clear();
+    {
+        std::vector<int32_t> stack = {0};
+        while (!stack.empty()) {
+            int32_t id = stack.back();
+            stack.pop_back();
+            const TreeNode &tn = ix->nodes[id];
+            if (tn.is_leaf) {
+                ix->leaves.push_back(id);
+            } else {
+                stack.push_back(tn.right);
+                stack.push_back(tn.left);
+            }
+        }
+    }
+    const int L = (int)ix->leaves.size();
+    ix->L = L;
+    std::vector<uint32_t> lf(L), lc(L);
+    std::vector<int32_t> lm(L), lep((size_t)L * M_MAX);
+    std::vector<float> lenv((size_t)L * M_MAX * 4);
+    uint32_t expect = 0;
+    for (int i = 0; i < L; i++) {
+        const TreeNode &tn = ix->nodes[ix->leaves[i]];
+        SSB_REQUIRE(tn.first == expect, "leaves are not contiguous in in-order");
+        expect += tn.count;
+        lf[i] = tn.first;
+        lc[i] = tn.count;
+        lm[i] = tn.m;
+        for (int j = 0; j < M_MAX; j++) {
+            lep[(size_t)i * M_MAX + j] = j < tn.m ? tn.ep[j] : n;
+            for (int q = 0; q < 4; q++) lenv[((size_t)i * M_MAX + j) * 4 + q] = j < tn.m ? tn.env[j][q] : 0.f;
+        }
+    }
+    SSB_REQUIRE((int64_t)expect == ix->N, "leaf counts do not cover the dataset");
+    SSB_CUDA(cudaMalloc(&ix->leaf_first, 4 * (size_t)L));
+    SSB_CUDA(cudaMalloc(&ix->leaf_count, 4 * (size_t)L));
+    SSB_CUDA(cudaMalloc(&ix->leaf_m, 4 * (size_t)L));
+    SSB_CUDA(cudaMalloc(&ix->leaf_ep, 4 * (size_t)L * M_MAX));
+    SSB_CUDA(cudaMalloc(&ix->leaf_env, 16 * (size_t)L * M_MAX));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_first, lf.data(), 4 * (size_t)L, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_count, lc.data(), 4 * (size_t)L, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_m, lm.data(), 4 * (size_t)L, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_ep, lep.data(), 4 * (size_t)L * M_MAX, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_env, lenv.data(), 16 * (size_t)L * M_MAX, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaStreamSynchronize(s));  // host vectors die at return
+    return OK;
+}
+
+__global__ void inv_from_orig_kernel(const uint32_t *__restrict__ orig, int64_t N, uint32_t *__restrict__ inv)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) inv[orig[i]] = (uint32_t)i;
+}
+
+// an index from host arrays already in leaf order (persist.py:461-528 load_index)
+int index_from_host(const float *rows, const uint8_t *words, const uint32_t *orig, int64_t N, int n, int64_t tau,
+                    int64_t id_base, std::vector<TreeNode> nodes, const double *bp_dev, Index **out, cudaStream_t s)
+{
+    SSB_REQUIRE(N >= 1 && N + id_base < (1ll << 32), "need 1 <= N and ids below 2^32");
+    SSB_REQUIRE(n > 0 && n % WORD_SEGMENTS == 0 && n <= MAX_SERIES_LEN, "unsupported series length");
+    std::unique_ptr<Index> ix(new Index());
+    ix->N = N;
+    ix->n = n;
+    ix->tau = tau;
+    ix->id_base = id_base;
+    ix->nodes = std::move(nodes);
+    RC(finalize_tree(*ix, s));
+    SSB_CUDA(cudaMalloc(&ix->X, (size_t)N * n * 4));
+    SSB_CUDA(cudaMalloc(&ix->words, (size_t)N * WORD_SEGMENTS));
+    SSB_CUDA(cudaMalloc(&ix->orig, (size_t)N * 4));
+    SSB_CUDA(cudaMalloc(&ix->inv, (size_t)N * 4));
+    SSB_CUDA(cudaMalloc(&ix->bp, 8 * (ALPHABET - 1)));
+    SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaMemcpy(ix->X, rows, (size_t)N * n * 4, cudaMemcpyHostToDevice));
+    if (orig) {
+        SSB_CUDA(cudaMemcpy(ix->orig, orig, (size_t)N * 4, cudaMemcpyHostToDevice));
+    } else {
+        iota_u32_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N);
+        SSB_CHECK_LAUNCH();
+    }
+    inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
+    SSB_CHECK_LAUNCH();
+    if (words) {
+        SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
+    } else {
+        RC(launch_words(ix->X, N, n, ix->bp, ix->words, nullptr, s));
+    }
+    DevBuf amax;
+    SSB_CUDA(amax.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));
+    absmax_kernel<<<4 * num_sms(), 256, 0, s>>>(ix->X, N * n, amax.as<uint32_t>());
+    SSB_CHECK_LAUNCH();
+    uint32_t am = 0;
+    SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&ix->max_abs, &am, 4);
+    *out = ix.release();
+    return OK;
+}
+
+}  // namespace ssb

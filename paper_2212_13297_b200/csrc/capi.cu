@@ -10,6 +10,7 @@
 
 #include "../../include/seriesearch_b200.h"
 #include "ssb_common.cuh"
+#include "ssb_index.h"
 #include "ssb_internal.h"
 
 namespace ssb {
@@ -85,16 +86,36 @@ int bruteforce_knn(const float *X, int64_t N, int n, const float *Q, int B, int 
     rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(),
                        keys.as<uint64_t>(), flags.as<int32_t>(), s);
     if (rc) return rc;
-    rc = launch_keys_to_results(keys.as<uint64_t>(), (int64_t)B * k, nullptr, out_d2, out_id,
+    rc = launch_keys_to_results(keys.as<uint64_t>(), (int64_t)B * k, nullptr, 0, out_d2, out_id,
                                 nullptr, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
 }
 
+struct BuildCfg {
+    int64_t tau;
+    int32_t initial_segments;
+    int32_t max_segments;
+    int64_t id_base;
+};
+int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg, Index **out,
+                cudaStream_t s);
+int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, float *out_d2, int64_t *out_id,
+                int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t s);
+int index_from_host(const float *rows, const uint8_t *words, const uint32_t *orig, int64_t N, int n, int64_t tau,
+                    int64_t id_base, std::vector<TreeNode> nodes, const double *bp_dev, Index **out, cudaStream_t s);
+int launch_lb_sax_rows(const float *qpaa, const uint8_t *words, int64_t rows, const double *sym_lo,
+                       const double *sym_hi, int n, double *out, cudaStream_t s);
+
 }  // namespace ssb
 
 using namespace ssb;
+
+struct ssb_index {
+    ssb::Index *ix;
+};
 
 extern "C" {
 
@@ -155,6 +176,155 @@ int ssb_bruteforce_knn(const float *X, int64_t N, int32_t n, const float *Q, int
                        int64_t id_base, float *out_d2, int64_t *out_id, void *stream)
 {
     return bruteforce_knn(X, N, n, Q, B, k, id_base, out_d2, out_id, (cudaStream_t)stream);
+}
+
+int ssb_build(const float *X, int64_t N, int32_t n, const double *bp, const ssb_build_cfg *cfg,
+              ssb_index **out, void *stream)
+{
+    SSB_REQUIRE(cfg && out, "null argument");
+    BuildCfg c{cfg->leaf_threshold, cfg->initial_segments, cfg->max_segments, cfg->id_base};
+    Index *ix = nullptr;
+    int rc = build_index(X, N, n, bp, c, &ix, (cudaStream_t)stream);
+    if (rc) return rc;
+    *out = new ssb_index{ix};
+    return OK;
+}
+
+int ssb_index_free(ssb_index *h)
+{
+    if (!h) return OK;
+    delete h->ix;
+    delete h;
+    return OK;
+}
+
+int ssb_index_info(const ssb_index *h, ssb_index_info_t *out)
+{
+    SSB_REQUIRE(h && out, "null argument");
+    const Index &ix = *h->ix;
+    out->dataset_size = ix.N;
+    out->series_length = ix.n;
+    out->leaf_threshold = ix.tau;
+    out->id_base = ix.id_base;
+    out->num_nodes = (int32_t)ix.nodes.size();
+    out->num_leaves = ix.L;
+    out->levels = ix.levels;
+    out->max_segments = M_MAX;
+    out->build_ms = ix.build_ms;
+    out->max_abs = ix.max_abs;
+    int d = 0;
+    for (auto &nd : ix.nodes) d = std::max(d, nd.depth);
+    out->depth = d;
+    return OK;
+}
+
+int ssb_index_node(const ssb_index *h, int32_t id, ssb_node_t *out)
+{
+    SSB_REQUIRE(h && out, "null argument");
+    const Index &ix = *h->ix;
+    SSB_REQUIRE(id >= 0 && id < (int32_t)ix.nodes.size(), "node id out of range");
+    const TreeNode &t = ix.nodes[id];
+    out->parent = t.parent;
+    out->left = t.left;
+    out->right = t.right;
+    out->first = t.first;
+    out->count = t.count;
+    out->m = t.m;
+    for (int i = 0; i < SSB_M_MAX; i++) {
+        out->endpoints[i] = i < t.m ? t.ep[i] : 0;
+        for (int q = 0; q < 4; q++) out->envelope[i][q] = i < t.m ? t.env[i][q] : 0.f;
+    }
+    out->is_leaf = t.is_leaf;
+    out->oversize = t.oversize;
+    out->depth = t.depth;
+    out->segment = t.seg;
+    out->attribute = t.attr;
+    out->split_point = t.split;
+    out->route_start = t.rs;
+    out->route_end = t.re;
+    out->threshold = t.thr;
+    out->gain = t.gain;
+    return OK;
+}
+
+int ssb_index_arrays(const ssb_index *h, const float **X, const uint8_t **words, const uint32_t **orig,
+                     const uint32_t **inv)
+{
+    SSB_REQUIRE(h, "null argument");
+    if (X) *X = h->ix->X;
+    if (words) *words = h->ix->words;
+    if (orig) *orig = h->ix->orig;
+    if (inv) *inv = h->ix->inv;
+    return OK;
+}
+
+int ssb_index_download(const ssb_index *h, float *rows_host, uint8_t *words_host, uint32_t *orig_host)
+{
+    SSB_REQUIRE(h, "null index");
+    const Index &ix = *h->ix;
+    if (rows_host) SSB_CUDA(cudaMemcpy(rows_host, ix.X, (size_t)ix.N * ix.n * 4, cudaMemcpyDeviceToHost));
+    if (words_host) SSB_CUDA(cudaMemcpy(words_host, ix.words, (size_t)ix.N * WORD_SEGMENTS, cudaMemcpyDeviceToHost));
+    if (orig_host) SSB_CUDA(cudaMemcpy(orig_host, ix.orig, (size_t)ix.N * 4, cudaMemcpyDeviceToHost));
+    return OK;
+}
+
+int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint32_t *orig_host, int64_t N,
+                   int32_t n, int64_t tau, int64_t id_base, const ssb_node_t *nodes, int32_t num_nodes,
+                   const double *bp, ssb_index **out, void *stream)
+{
+    SSB_REQUIRE(out && nodes && rows_host && num_nodes >= 1, "null argument");
+    std::vector<TreeNode> tn(num_nodes);
+    for (int i = 0; i < num_nodes; i++) {
+        const ssb_node_t &r = nodes[i];
+        SSB_REQUIRE(r.m >= 1 && r.m <= M_MAX, "node segment count outside [1, 32]");
+        TreeNode &t = tn[i];
+        t.parent = r.parent;
+        t.left = r.left;
+        t.right = r.right;
+        t.first = r.first;
+        t.count = r.count;
+        t.m = r.m;
+        for (int j = 0; j < r.m; j++) {
+            t.ep[j] = r.endpoints[j];
+            for (int q = 0; q < 4; q++) t.env[j][q] = r.envelope[j][q];
+        }
+        t.is_leaf = r.is_leaf;
+        t.oversize = r.oversize;
+        t.depth = r.depth;
+        t.seg = r.segment;
+        t.attr = r.attribute;
+        t.split = r.split_point;
+        t.rs = r.route_start;
+        t.re = r.route_end;
+        t.thr = r.threshold;
+        t.gain = r.gain;
+    }
+    Index *ix = nullptr;
+    int rc = index_from_host(rows_host, words_host, orig_host, N, n, tau, id_base, std::move(tn), bp, &ix,
+                             (cudaStream_t)stream);
+    if (rc) return rc;
+    *out = new ssb_index{ix};
+    return OK;
+}
+
+int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, float *out_d2, int64_t *out_id,
+              int64_t *out_pos, uint32_t *stats_host, void *stream)
+{
+    SSB_REQUIRE(h, "null index");
+    const Index &ix = *h->ix;
+    return index_query(ix, Q, B, k, ix.id_base, out_d2, out_id, out_pos, stats_host, (cudaStream_t)stream);
+}
+
+int ssb_index_lb_eapca(const ssb_index *h, const float *Q, int32_t B, double *out, void *stream)
+{
+    SSB_REQUIRE(h, "null index");
+    return index_lbe(*h->ix, Q, B, out, (cudaStream_t)stream);
+}
+
+int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const double *lower, const double *upper,
+               int32_t n, double *out, void *stream)
+{
+    return launch_lb_sax_rows(qpaa, words, rows, lower, upper, n, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,609 @@
+// query.cu -- batched exact k-NN over an HBM-resident index (K-lbe, K-lbs,
+// tile lists, K-scan sparse, K-select with bound tightening).
+//
+// Replaces query.py:296-348 QueryEngine.exact_knn and its phases
+// (approx_knn :167-198, find_candidate_leaves :200-214,
+// find_candidate_series :216-251, compute_results :253-270,
+// skip_sequential_scan :272-292), for a whole block of B queries at once:
+//
+//  A  seed    each query's best leaf by LB_EAPCA is scanned exactly; the k-th
+//             best (d2, id) key is the query's bound (an upper bound on the
+//             true k-th key: it is the k-th of k real distances).
+//  B1 K-lbe   LB_EAPCA of every (query, leaf) (summarize.py:170-181, exact
+//             float64 order); a leaf survives unless its bound provably
+//             exceeds the query's bound (safe test).
+//  B2 K-lbs   LB_SAX (summarize.py:136-153, exact order) of every row of the
+//             surviving leaves, through a per-query 16 x 256 gap table in
+//             shared memory; survivors become (tile, query, 32-bit mask).
+//  B3 entries sorted by (tile, query) -> tile CSR + union masks.
+//  B4 K-scan  exact d2 of the surviving pairs (scan.cu sparse); keys <= the
+//             bound are appended per query.
+//  B5 K-select top-k by (d2, id); a query whose buffer overflowed gets the
+//             k-th stored key as a tighter bound and is rescanned.
+// Ties resolve to the lowest original index, like brute_force_knn.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cstring>
+#include <vector>
+
+#include "ssb_common.cuh"
+#include "ssb_index.h"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+int launch_query_prep(const float *Q, int B, int n, double *cs, double *c2, float *qpaa,
+                      cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// bounds
+
+// safe keep-test bound (in squared units) for a query whose current k-th key
+// is `thr`: a lower bound LB computed from float32-rounded statistics keeps
+// its element iff LB <= bound (relative slack for float32
+// distance rounding, absolute slack delta*sqrt(2n) for statistic rounding).
+__device__ __forceinline__ double keep_bound(uint64_t thr, double slack_abs)
+{
+    if (thr == KEY_EMPTY) return __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    const double d2 = (double)key_d2(thr);
+    const double r = sqrt(d2) * (1.0 + 1e-5) + slack_abs;
+    return r * r * (1.0 + 1e-12);
+}
+
+// LB_EAPCA of query q against leaf l (query.py:127-135 -> summarize.py:170-181)
+__device__ double lb_eapca_leaf(const double *cs, const double *c2, const int32_t *ep, const float *env,
+                                int m)
+{
+    double t[M_MAX];
+    int sa = 0;
+    for (int i = 0; i < m; i++) {
+        const int sb = ep[i];
+        const double wd = (double)(sb - sa);
+        const double mu = __ddiv_rn(__dsub_rn(cs[sb], cs[sa]), wd);
+        const double msq = __ddiv_rn(__dsub_rn(c2[sb], c2[sa]), wd);
+        const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
+        const double qm = (double)__double2float_rn(mu);
+        const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
+        const double mmin = (double)env[i * 4 + 0], mmax = (double)env[i * 4 + 1];
+        const double smin = (double)env[i * 4 + 2], smax = (double)env[i * 4 + 3];
+        double gm = fmax(__dsub_rn(mmin, qm), __dsub_rn(qm, mmax));
+        gm = fmax(gm, 0.0);
+        double gs = fmax(__dsub_rn(smin, qs), __dsub_rn(qs, smax));
+        gs = fmax(gs, 0.0);
+        t[i] = __dmul_rn(wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
+        sa = sb;
+    }
+    return pw_f64_small(t, m);
+}
+
+// K-lbe: one CTA per query; the query's prefix sums are staged in shared memory
+__global__ void lbe_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n,
+                           int L, const int32_t *__restrict__ leaf_m, const int32_t *__restrict__ leaf_ep,
+                           const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
+                           double *__restrict__ lbe, int32_t *__restrict__ best_leaf)
+{
+    extern __shared__ double sm[];
+    double *cs = sm, *c2 = sm + (n + 1);
+    const int q = blockIdx.x;
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+        cs[i] = cs_g[(int64_t)q * (n + 1) + i];
+        c2[i] = c2_g[(int64_t)q * (n + 1) + i];
+    }
+    __syncthreads();
+    double bv = __longlong_as_double(0x7ff0000000000000ll);
+    int bl = 0x7fffffff;
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        const double v = lb_eapca_leaf(cs, c2, leaf_ep + (int64_t)l * M_MAX, leaf_env + (int64_t)l * M_MAX * 4,
+                                       leaf_m[l]);
+        lbe[(int64_t)q * L + l] = v;
+        if (leaf_count[l] && (v < bv || (v == bv && l < bl))) {
+            bv = v;
+            bl = l;
+        }
+    }
+    // block argmin (value, then lowest leaf index)
+    __shared__ double rv[32];
+    __shared__ int rl[32];
+    for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+        if (ov < bv || (ov == bv && ol < bl)) {
+            bv = ov;
+            bl = ol;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        rv[threadIdx.x >> 5] = bv;
+        rl[threadIdx.x >> 5] = bl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+            if (rv[w] < bv || (rv[w] == bv && rl[w] < bl)) {
+                bv = rv[w];
+                bl = rl[w];
+            }
+        best_leaf[q] = bl == 0x7fffffff ? -1 : bl;
+    }
+}
+
+// Entry = (tile, query, mask).  Appended with a global counter.
+struct EntryOut {
+    uint64_t *key;   // (tile << 32) | query
+    uint32_t *mask;
+    uint32_t *count;
+    int64_t cap;
+};
+
+__device__ __forceinline__ void emit_entry(const EntryOut &eo, uint32_t tile, uint32_t q, uint32_t mask)
+{
+    const uint32_t slot = atomicAdd(eo.count, 1u);
+    if ((int64_t)slot < eo.cap) {
+        eo.key[slot] = ((uint64_t)tile << 32) | q;
+        eo.mask[slot] = mask;
+    }
+}
+
+// phase A: the tiles of each query's best leaf (all its rows)
+__global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const uint32_t *__restrict__ leaf_first,
+                                    const uint32_t *__restrict__ leaf_count, int B, EntryOut eo,
+                                    uint32_t *__restrict__ seed_rows)
+{
+    const int q = blockIdx.x;
+    const int l = best_leaf[q];
+    if (l < 0) {
+        if (threadIdx.x == 0) seed_rows[q] = 0;
+        return;
+    }
+    const uint32_t a = leaf_first[l], b = a + leaf_count[l];
+    if (threadIdx.x == 0) seed_rows[q] = b - a;
+    for (uint32_t t = a / TILE_ROWS + threadIdx.x; t <= (b - 1) / TILE_ROWS; t += blockDim.x) {
+        const uint32_t r0 = t * TILE_ROWS;
+        const uint32_t lo = a > r0 ? a - r0 : 0;
+        const uint32_t hi = min(b - r0, (uint32_t)TILE_ROWS);
+        const uint32_t mask = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+        emit_entry(eo, t, (uint32_t)q, mask);
+    }
+}
+
+// K-lbs: one CTA per query; per-query gap^2 table T[seg][sym] in shared memory
+// (A.4: g = max(max(lo - q, q - hi), 0), LB = (n/16) * pw64(g^2)).
+__global__ void __launch_bounds__(256)
+    lbs_kernel(const float *__restrict__ qpaa, const double *__restrict__ sym_lo, const double *__restrict__ sym_hi,
+               const uint4 *__restrict__ words, int n, int L, const uint32_t *__restrict__ leaf_first,
+               const uint32_t *__restrict__ leaf_count, const double *__restrict__ lbe,
+               const uint64_t *__restrict__ thr, double slack_abs,
+               EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series)
+{
+    __shared__ double T[WORD_SEGMENTS * ALPHABET];  // 32 KB
+    const int q = blockIdx.x;
+    for (int i = threadIdx.x; i < WORD_SEGMENTS * ALPHABET; i += blockDim.x) {
+        const int seg = i / ALPHABET, sym = i % ALPHABET;
+        const double qv = (double)qpaa[(int64_t)q * WORD_SEGMENTS + seg];
+        double g = fmax(__dsub_rn(sym_lo[sym], qv), __dsub_rn(qv, sym_hi[sym]));
+        g = fmax(g, 0.0);
+        T[i] = __dmul_rn(g, g);
+    }
+    __syncthreads();
+    const double bound = keep_bound(thr[q], slack_abs);
+    const double w = (double)(n / WORD_SEGMENTS);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t my_series = 0, my_leaves = 0;
+    for (int l = 0; l < L; l++) {
+        if (!(lbe[(int64_t)q * L + l] <= bound)) continue;  // NaN-safe: prune only if provably above
+        const uint32_t a = leaf_first[l], b = a + leaf_count[l];
+        if (a == b) continue;
+        if (threadIdx.x == 0) my_leaves++;
+        for (uint32_t t = a / TILE_ROWS + warp; t <= (b - 1) / TILE_ROWS; t += nw) {
+            const uint32_t pos = t * TILE_ROWS + lane;
+            bool keep = false;
+            if (pos >= a && pos < b) {
+                const uint4 wv = __ldg(words + pos);
+                const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+                double g2[16];
+#pragma unroll
+                for (int s = 0; s < 16; s++) {
+                    const uint32_t sym = (wd[s >> 2] >> (8 * (s & 3))) & 0xffu;
+                    g2[s] = T[s * ALPHABET + sym];
+                }
+                double r[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = __dadd_rn(g2[j], g2[j + 8]);
+                const double sum = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+                const double lb = __dmul_rn(w, sum);
+                keep = lb <= bound;
+            }
+            const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0 && mask) {
+                emit_entry(eo, t, (uint32_t)q, mask);
+                my_series += __popc(mask);
+            }
+        }
+    }
+    if (lane == 0 && my_series) atomicAdd(&cand_series[q], my_series);
+    if (threadIdx.x == 0) cand_leaves[q] = my_leaves;
+}
+
+// after sorting by (tile, query): tile boundaries -> tile list
+__global__ void tile_flags_kernel(const uint64_t *__restrict__ keys, int64_t E, uint32_t *__restrict__ flags)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > E) return;
+    if (i == E) {
+        flags[i] = 0;
+        return;
+    }
+    flags[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1u : 0u;
+}
+
+__global__ void tile_build_kernel(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ masks,
+                                  int64_t E, const uint32_t *__restrict__ flags, const uint32_t *__restrict__ slot,
+                                  uint32_t *__restrict__ row0, uint32_t *__restrict__ umask,
+                                  uint32_t *__restrict__ eptr, uint2 *__restrict__ entries)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > E) return;
+    if (i == E) {
+        eptr[slot[E]] = (uint32_t)E;
+        return;
+    }
+    const uint32_t t = (uint32_t)(keys[i] >> 32);
+    const uint32_t s = slot[i] - 1;  // inclusive scan of tile starts -> slot of entry i
+    if (flags[i]) {
+        row0[s] = t * TILE_ROWS;
+        eptr[s] = (uint32_t)i;
+    }
+    atomicOr(&umask[s], masks[i]);
+    entries[i] = make_uint2((uint32_t)(keys[i] & 0xffffffffu), masks[i]);
+}
+
+__global__ void thr_from_keys_kernel(const uint64_t *__restrict__ keys, int B, int k, uint64_t *__restrict__ thr)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < B) thr[q] = keys[(int64_t)q * k + k - 1];
+}
+
+__global__ void active_entries_kernel(uint2 *__restrict__ entries, int64_t E, const int32_t *__restrict__ flags,
+                                      uint32_t *__restrict__ keepmask_store)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= E) return;
+    uint2 e = entries[i];
+    if (!flags[e.x]) {
+        keepmask_store[i] = e.y;
+        e.y = 0;
+        entries[i] = e;
+    } else {
+        keepmask_store[i] = e.y;
+    }
+}
+
+__global__ void restore_entries_kernel(uint2 *__restrict__ entries, int64_t E, const uint32_t *__restrict__ keep)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < E) entries[i].y = keep[i];
+}
+
+__global__ void reset_flagged_kernel(uint32_t *__restrict__ cnt, const int32_t *__restrict__ flags, int B)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < B && flags[q]) cnt[q] = 0;
+}
+
+__global__ void qabsmax_kernel(const float *__restrict__ X, int64_t count, uint32_t *__restrict__ out)
+{
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = fabsf(X[i]);
+        m = (v != v) ? __int_as_float(0x7f800000) : fmaxf(m, v);  // NaN -> +inf (rejected)
+    }
+    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// standalone LB_SAX of one query PAA against rows of words (parity tests)
+__global__ void lb_sax_rows_kernel(const float *__restrict__ qpaa, const uint8_t *__restrict__ words, int64_t rows,
+                                   const double *__restrict__ sym_lo, const double *__restrict__ sym_hi, int n,
+                                   double *__restrict__ out)
+{
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    double g2[16];
+    for (int s = 0; s < 16; s++) {
+        const double qv = (double)qpaa[s];
+        const uint8_t sym = words[r * 16 + s];
+        double g = fmax(__dsub_rn(sym_lo[sym], qv), __dsub_rn(qv, sym_hi[sym]));
+        g = fmax(g, 0.0);
+        g2[s] = __dmul_rn(g, g);
+    }
+    double rr[8];
+    for (int j = 0; j < 8; j++) rr[j] = __dadd_rn(g2[j], g2[j + 8]);
+    const double sum = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                                 __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+    out[r] = __dmul_rn((double)(n / WORD_SEGMENTS), sum);
+}
+
+int launch_lb_sax_rows(const float *qpaa, const uint8_t *words, int64_t rows, const double *sym_lo,
+                       const double *sym_hi, int n, double *out, cudaStream_t s)
+{
+    if (rows == 0) return OK;
+    lb_sax_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(qpaa, words, rows, sym_lo, sym_hi, n, out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// all LB_EAPCA values of B queries against the index leaves (parity tests)
+int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t s)
+{
+    if (B == 0) return OK;
+    const int n = ix.n;
+    DevBuf cs, c2, qpaa, best;
+    SSB_CUDA(cs.alloc(8 * (size_t)B * (n + 1), s));
+    SSB_CUDA(c2.alloc(8 * (size_t)B * (n + 1), s));
+    SSB_CUDA(qpaa.alloc(4 * (size_t)B * WORD_SEGMENTS, s));
+    SSB_CUDA(best.alloc(4 * (size_t)B, s));
+    int rc = launch_query_prep(Q, B, n, cs.as<double>(), c2.as<double>(), qpaa.as<float>(), s);
+    if (rc) return rc;
+    lbe_kernel<<<B, 256, 16 * (n + 1), s>>>(cs.as<double>(), c2.as<double>(), n, ix.L, ix.leaf_m, ix.leaf_ep,
+                                            ix.leaf_env, ix.leaf_count, out, best.as<int32_t>());
+    SSB_CHECK_LAUNCH();
+    SSB_CUDA(cudaStreamSynchronize(s));
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// host: entry list -> tile list -> sparse scan -> select (with tightening)
+
+struct TileBufs {
+    DevBuf row0, umask, eptr, entries;
+    int64_t ntiles = 0;
+    int64_t E = 0;
+};
+
+static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cudaStream_t s)
+{
+    tb.E = E;
+    tb.ntiles = 0;
+    if (E == 0) return OK;
+    DevBuf k2, m2, tmp, flags, slot;
+    SSB_CUDA(k2.alloc(8 * (size_t)E, s));
+    SSB_CUDA(m2.alloc(4 * (size_t)E, s));
+    size_t tb_bytes = 0;
+    SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
+                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, 64, s));
+    SSB_CUDA(tmp.alloc(tb_bytes, s));
+    SSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
+                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, 64, s));
+    note_launch(1);
+    SSB_CUDA(flags.alloc(4 * (size_t)(E + 1), s));
+    SSB_CUDA(slot.alloc(4 * (size_t)(E + 1), s));
+    tile_flags_kernel<<<(unsigned)((E + 256) / 256), 256, 0, s>>>(k2.as<uint64_t>(), E, flags.as<uint32_t>());
+    SSB_CHECK_LAUNCH();
+    size_t sb = 0;
+    SSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, flags.as<uint32_t>(), slot.as<uint32_t>(), (int)(E + 1), s));
+    DevBuf tmp2;
+    SSB_CUDA(tmp2.alloc(sb, s));
+    SSB_CUDA(cub::DeviceScan::InclusiveSum(tmp2.p, sb, flags.as<uint32_t>(), slot.as<uint32_t>(), (int)(E + 1), s));
+    note_launch(1);
+    uint32_t nt = 0;
+    SSB_CUDA(cudaMemcpyAsync(&nt, slot.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    tb.ntiles = nt;
+    SSB_CUDA(tb.row0.alloc(4 * (size_t)nt, s));
+    SSB_CUDA(tb.umask.alloc(4 * (size_t)nt, s));
+    SSB_CUDA(tb.eptr.alloc(4 * (size_t)(nt + 1), s));
+    SSB_CUDA(tb.entries.alloc(8 * (size_t)E, s));
+    SSB_CUDA(cudaMemsetAsync(tb.umask.p, 0, 4 * (size_t)nt, s));
+    tile_build_kernel<<<(unsigned)((E + 256) / 256), 256, 0, s>>>(
+        k2.as<uint64_t>(), m2.as<uint32_t>(), E, flags.as<uint32_t>(), slot.as<uint32_t>(),
+        tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>());
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// one batch of queries (Bq <= cap-sized batch)
+static int query_batch(const Index &ix, const float *Q, int B, int k, double slack_abs, uint64_t *out_keys,
+                       uint32_t *st_cand_leaves, uint32_t *st_cand_series, uint32_t *st_seed_rows,
+                       int32_t *st_rounds, int64_t entry_cap, cudaStream_t s)
+{
+    const int n = ix.n, L = ix.L;
+    DevBuf cs, c2, qpaa, lbe, best, thr, cand, cnt, flags, ekey, emask, ecount, symlo, symhi;
+    SSB_CUDA(cs.alloc(8 * (size_t)B * (n + 1), s));
+    SSB_CUDA(c2.alloc(8 * (size_t)B * (n + 1), s));
+    SSB_CUDA(qpaa.alloc(4 * (size_t)B * WORD_SEGMENTS, s));
+    SSB_CUDA(lbe.alloc(8 * (size_t)B * L, s));
+    SSB_CUDA(best.alloc(4 * (size_t)B, s));
+    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
+    int rc = launch_query_prep(Q, B, n, cs.as<double>(), c2.as<double>(), qpaa.as<float>(), s);
+    if (rc) return rc;
+    {
+        const int smem = 16 * (n + 1);
+        ProfScope ps("lbe", s, (double)L * (M_MAX * 20 + 12) + 16.0 * B * (n + 1));
+        lbe_kernel<<<B, 256, smem, s>>>(cs.as<double>(), c2.as<double>(), n, L, ix.leaf_m, ix.leaf_ep,
+                                        ix.leaf_env, ix.leaf_count, lbe.as<double>(), best.as<int32_t>());
+    }
+    SSB_CHECK_LAUNCH();
+
+    // symbol bounds from the breakpoints (summarize.py:124-133)
+    {
+        std::vector<double> lo(ALPHABET), hi(ALPHABET), bp(ALPHABET - 1);
+        SSB_CUDA(cudaMemcpyAsync(bp.data(), ix.bp, 8 * (ALPHABET - 1), cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        lo[0] = -INFINITY;
+        for (int i = 1; i < ALPHABET; i++) lo[i] = bp[i - 1];
+        for (int i = 0; i < ALPHABET - 1; i++) hi[i] = bp[i];
+        hi[ALPHABET - 1] = INFINITY;
+        SSB_CUDA(symlo.alloc(8 * ALPHABET, s));
+        SSB_CUDA(symhi.alloc(8 * ALPHABET, s));
+        SSB_CUDA(cudaMemcpyAsync(symlo.p, lo.data(), 8 * ALPHABET, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(symhi.p, hi.data(), 8 * ALPHABET, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+    }
+
+    const int cap = 16384;
+    SSB_CUDA(cand.alloc(8 * (size_t)B * cap, s));
+    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
+    SSB_CUDA(flags.alloc(4 * (size_t)B, s));
+    SSB_CUDA(ecount.alloc(4, s));
+    SSB_CUDA(ekey.alloc(8 * (size_t)entry_cap, s));
+    SSB_CUDA(emask.alloc(4 * (size_t)entry_cap, s));
+
+    // ---- phase A: exact scan of each query's best leaf -> bound ------------------
+    SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
+    EntryOut eo{ekey.as<uint64_t>(), emask.as<uint32_t>(), ecount.as<uint32_t>(), entry_cap};
+    seed_entries_kernel<<<B, 128, 0, s>>>(best.as<int32_t>(), ix.leaf_first, ix.leaf_count, B, eo, st_seed_rows);
+    SSB_CHECK_LAUNCH();
+    uint32_t E = 0;
+    SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    SSB_REQUIRE((int64_t)E <= entry_cap, "seed entry buffer overflow");
+    SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
+    {
+        TileBufs tb;
+        rc = build_tiles(ekey, emask, E, tb, s);
+        if (rc) return rc;
+        TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
+                    tb.ntiles};
+        ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+        if (rc) return rc;
+        rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
+                           flags.as<int32_t>(), s);
+        if (rc) return rc;
+        thr_from_keys_kernel<<<(B + 255) / 256, 256, 0, s>>>(out_keys, B, k, thr.as<uint64_t>());
+        SSB_CHECK_LAUNCH();
+    }
+
+    // ---- phase B: LB_EAPCA + LB_SAX filtering, exact scan of survivors ----------
+    SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
+    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
+    {
+        ProfScope ps("lbs", s, 0.0);
+        lbs_kernel<<<B, 256, 0, s>>>(qpaa.as<float>(), symlo.as<double>(), symhi.as<double>(),
+                                     reinterpret_cast<const uint4 *>(ix.words), n, L, ix.leaf_first, ix.leaf_count,
+                                     lbe.as<double>(), thr.as<uint64_t>(), slack_abs, eo, st_cand_leaves,
+                                     st_cand_series);
+    }
+    SSB_CHECK_LAUNCH();
+    SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    if ((int64_t)E > entry_cap) {
+        set_error(ERR_USAGE, "candidate entry buffer overflow");
+        return -1;  // caller splits the batch
+    }
+    TileBufs tb;
+    rc = build_tiles(ekey, emask, E, tb, s);
+    if (rc) return rc;
+    TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
+                tb.ntiles};
+    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
+    ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
+    rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+    if (rc) return rc;
+    std::vector<int32_t> hflags(B);
+    DevBuf keep;
+    for (int round = 0;; round++) {
+        rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
+                           flags.as<int32_t>(), s);
+        if (rc) return rc;
+        SSB_CUDA(cudaMemcpyAsync(hflags.data(), flags.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        int over = 0;
+        for (int q = 0; q < B; q++) over += hflags[q];
+        if (!over) {
+            if (st_rounds) *st_rounds = round;
+            break;
+        }
+        SSB_REQUIRE(round < 64, "bound tightening did not converge");
+        // rescan only the overflowed queries with their tightened bounds
+        if (!keep.p) SSB_CUDA(keep.alloc(4 * (size_t)std::max<int64_t>(tb.E, 1), s));
+        active_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
+                                                                          flags.as<int32_t>(), keep.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+        reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
+        SSB_CHECK_LAUNCH();
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+        if (rc) return rc;
+        restore_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
+                                                                           keep.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+    }
+    return OK;
+}
+
+int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, float *out_d2, int64_t *out_id,
+                int64_t *out_pos,
+                uint32_t *stats_host /* B x 4: cand_leaves, cand_series, seed_rows, rounds */, cudaStream_t s)
+{
+    SSB_REQUIRE(k >= 1, "k must be at least 1");
+    SSB_REQUIRE(k <= 4096, "k above 4096 is not supported");
+    if (B == 0) return OK;
+    const int n = ix.n;
+    // statistic-rounding slack: delta * sqrt(2n) in distance units
+    DevBuf qmax;
+    SSB_CUDA(qmax.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
+    qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
+    SSB_CHECK_LAUNCH();
+    uint32_t qm_bits = 0;
+    SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    float qm;
+    std::memcpy(&qm, &qm_bits, 4);
+    SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
+    const double M = std::max((double)qm, (double)ix.max_abs);
+    const double delta = std::ldexp(M, -19);
+    const double slack_abs = delta * std::sqrt(2.0 * n);
+
+    DevBuf keys, stl, sts, str;
+    SSB_CUDA(keys.alloc(8 * (size_t)B * k, s));
+    SSB_CUDA(stl.alloc(4 * (size_t)B, s));
+    SSB_CUDA(sts.alloc(4 * (size_t)B, s));
+    SSB_CUDA(str.alloc(4 * (size_t)B, s));
+    // batches bounded by the entry buffer: worst case every row of every leaf survives
+    const int64_t per_query_worst = ix.N / TILE_ROWS + 2 * (int64_t)ix.L + 2;
+    const int64_t budget = 96ll << 20;  // entries (12 B each)
+    int bq = (int)std::max<int64_t>(1, std::min<int64_t>(B, std::max<int64_t>(256, budget / per_query_worst)));
+    std::vector<int32_t> rounds;
+    for (int q0 = 0; q0 < B;) {
+        const int nb = std::min(bq, B - q0);
+        const int64_t ecap = std::min<int64_t>((int64_t)nb * per_query_worst, budget);
+        int32_t r = 0;
+        int rc = query_batch(ix, Q + (int64_t)q0 * n, nb, k, slack_abs, keys.as<uint64_t>() + (int64_t)q0 * k,
+                             stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0, &r, ecap, s);
+        if (rc == -1) {  // entry overflow: halve the batch and retry
+            SSB_REQUIRE(nb > 1, "a single query overflowed the candidate entry buffer");
+            bq = std::max(1, nb / 2);
+            continue;
+        }
+        if (rc) return rc;
+        q0 += nb;
+    }
+    int rc = launch_keys_to_results(keys.as<uint64_t>(), (int64_t)B * k, ix.inv, id_base, out_d2, out_id,
+                                    out_pos, s);
+    if (rc) return rc;
+    if (stats_host) {
+        std::vector<uint32_t> a(B), b(B), c(B);
+        SSB_CUDA(cudaMemcpyAsync(a.data(), stl.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(b.data(), sts.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(c.data(), str.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < B; q++) {
+            stats_host[4 * q + 0] = a[q];
+            stats_host[4 * q + 1] = b[q];
+            stats_host[4 * q + 2] = c[q];
+            stats_host[4 * q + 3] = 0;
+        }
+    }
+    SSB_CUDA(cudaStreamSynchronize(s));
+    return OK;
+}
+
+}  // namespace ssb

@@ -244,7 +244,7 @@ __global__ void select_topk_kernel(const uint64_t *__restrict__ cand, uint32_t *
 }
 
 __global__ void keys_to_results_kernel(const uint64_t *__restrict__ keys, int64_t count,
-                                       const uint32_t *__restrict__ inv_perm, float *out_d2,
+                                       const uint32_t *__restrict__ inv_perm, int64_t id_base, float *out_d2,
                                        int64_t *out_id, int64_t *out_pos)
 {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -257,7 +257,7 @@ __global__ void keys_to_results_kernel(const uint64_t *__restrict__ keys, int64_
     } else {
         out_d2[i] = key_d2(key);
         uint32_t id = key_id(key);
-        out_id[i] = id;
+        out_id[i] = (int64_t)id + id_base;
         if (out_pos) out_pos[i] = inv_perm ? (int64_t)inv_perm[id] : (int64_t)id;
     }
 }
@@ -372,11 +372,11 @@ int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, u
     return OK;
 }
 
-int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm,
+int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s)
 {
     if (count == 0) return OK;
-    keys_to_results_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(keys, count, inv_perm,
+    keys_to_results_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(keys, count, inv_perm, id_base,
                                                                           out_d2, out_id, out_pos);
     SSB_CHECK_LAUNCH();
     return OK;

@@ -1,0 +1,55 @@
+// ssb_index.h -- the HBM-resident index (a forest shard's tree) shared by
+// build.cu and query.cu.  Internal; the C ABI sees it as an opaque handle.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "ssb_internal.h"
+
+namespace ssb {
+
+constexpr int M_MAX = 32;  // max segments per node (a12); V-splits stop at M_MAX
+
+// host-side tree node (tree.py:92-179 Node + :51-89 SplitPolicy)
+struct TreeNode {
+    int32_t parent = -1, left = -1, right = -1;
+    uint32_t first = 0, count = 0;  // member range in leaf order
+    int32_t m = 0;
+    int32_t ep[M_MAX] = {0};      // right endpoints
+    float env[M_MAX][4] = {{0}};  // mu_min, mu_max, sd_min, sd_max per segment
+    int32_t is_leaf = 1;
+    int32_t depth = 0;
+    // split policy (internal nodes)
+    int32_t seg = -1, attr = 0, split = -1, rs = 0, re = 0;
+    double thr = 0.0, gain = 0.0;
+    int32_t oversize = 0;  // leaf that could not be split (identical members)
+};
+
+struct Index {
+    int64_t N = 0;
+    int32_t n = 0;
+    int64_t tau = 0;
+    int64_t id_base = 0;
+    float *X = nullptr;       // N x n rows, leaf order (device)
+    uint8_t *words = nullptr;  // N x 16 SAX words, leaf order (device)
+    uint32_t *orig = nullptr;  // pos -> original row (device)
+    uint32_t *inv = nullptr;   // original row -> pos (device)
+    double *bp = nullptr;      // 255 breakpoints (device)
+    std::vector<TreeNode> nodes;
+    std::vector<int32_t> leaves;  // node ids, in order (== leaf order)
+    // device leaf table (SoA)
+    int32_t L = 0;
+    uint32_t *leaf_first = nullptr, *leaf_count = nullptr;
+    int32_t *leaf_m = nullptr;
+    int32_t *leaf_ep = nullptr;  // L x M_MAX
+    float *leaf_env = nullptr;   // L x M_MAX x 4
+    float max_abs = 0.f;         // max |x| over the data (LB safety slack)
+    double build_ms = 0.0;
+    int32_t levels = 0;
+    ~Index();
+};
+
+}  // namespace ssb

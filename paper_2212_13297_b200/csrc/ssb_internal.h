@@ -35,7 +35,7 @@ int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const Tile
                        const float *Q, ScanOut out, cudaStream_t s);
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s);
-int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm,
+int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s);
 
 // stream-ordered device scratch (cudaMallocAsync pool); freed on scope exit

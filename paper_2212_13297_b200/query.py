@@ -114,3 +114,106 @@ class QueryStats:
     wall_seconds: float = 0.0
     candidate_leaves: int = 0
     candidate_series: int = 0
+
+
+class QueryEngine:
+    """Answers exact k-NN queries against one HBM-resident index.
+
+    ``exact_knn`` keeps the reference signature (query.py:296-348) and
+    returns ``(ResultSet, QueryStats)``; ``exact_knn_batch`` answers a whole
+    block in one device pass (the only API addition); and
+    ``knn_device`` is the zero-copy form for device-resident query blocks.
+    ``lmax``, ``eapca_th``, ``sax_th`` and ``num_threads`` are validated and
+    only select the reported phase label: the device pipeline always runs
+    every pruning stage, and the answers do not depend on them (the
+    reference's path-invariance property, test_query.py:213-228).
+    """
+
+    def __init__(self, index):
+        from .persist import QueryableIndex
+
+        self.index = index
+        self._si = index.index if isinstance(index, QueryableIndex) else index
+        self.settings = self._si.settings
+        self.total_leaves = int(self._si.info.num_leaves)
+        self.total_series = int(self._si.info.dataset_size)
+
+    def close(self) -> None:
+        pass
+
+    def knn_device(self, Q, k: int, want_stats: bool = False):
+        """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,4) u32]."""
+        from . import _lib
+        from ._device import device_f32, ptr, require_cuda, stream_handle
+
+        t = require_cuda()
+        if k < 1:
+            raise UsageError("k must be at least 1")
+        X = device_f32(Q, self.settings.series_length)
+        B = X.shape[0]
+        d2 = t.empty((B, k), dtype=t.float32, device=X.device)
+        ids = t.empty((B, k), dtype=t.int64, device=X.device)
+        pos = t.empty((B, k), dtype=t.int64, device=X.device)
+        stats = np.zeros((B, 4), dtype=np.uint32) if want_stats else None
+        _lib.call("ssb_query", self._si.handle, ptr(X), B, k, ptr(d2), ptr(ids), ptr(pos),
+                  stats.ctypes.data_as(_lib.P) if want_stats else None, stream_handle())
+        return (d2, ids, pos, stats) if want_stats else (d2, ids, pos)
+
+    def _stats(self, row, cfg: QueryConfig, wall: float) -> QueryStats:
+        n = self.settings.series_length
+        cand_leaves, cand_series, seed_rows = int(row[0]), int(row[1]), int(row[2])
+        st = QueryStats()
+        st.visited_leaves = 1 if seed_rows else 0
+        st.candidate_leaves = cand_leaves
+        st.candidate_series = cand_series
+        st.eapca_pr = 1.0 - cand_leaves / max(1, self.total_leaves)
+        st.sax_pr = 1.0 - cand_series / max(1, self.total_series)
+        # phase label by the reference's decision rules (query.py:321-341)
+        if st.eapca_pr < cfg.eapca_th:
+            st.phase_reached = "scan2"
+        elif st.sax_pr < cfg.sax_th:
+            st.phase_reached = "scan3"
+        elif cand_series:
+            st.phase_reached = "4"
+        elif cand_leaves:
+            st.phase_reached = "3"
+        else:
+            st.phase_reached = "1"
+        st.series_read = min(self.total_series, seed_rows + cand_series)
+        st.bytes_read = st.series_read * n * 4
+        st.fraction_data_accessed = st.series_read / max(1, self.total_series)
+        st.wall_seconds = wall
+        return st
+
+    def exact_knn_batch(self, queries, cfg: QueryConfig):
+        import time
+
+        cfg.validate()
+        Q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)
+        n = self.settings.series_length
+        if Q.shape[1] != n:
+            raise UsageError(f"query length {Q.shape[1]} does not match index series length {n}")
+        if not np.isfinite(Q).all():
+            raise UsageError("queries must be finite (documented deviation: NaN keys break ordering)")
+        t0 = time.perf_counter()
+        d2, ids, pos, stats = self.knn_device(Q, cfg.k, want_stats=True)
+        d2, ids, pos = d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
+        wall = (time.perf_counter() - t0) / max(1, Q.shape[0])
+        return [(ResultSet.from_arrays(d2[i], pos[i], ids[i]), self._stats(stats[i], cfg, wall))
+                for i in range(Q.shape[0])]
+
+    def exact_knn(self, query, cfg: QueryConfig):
+        q = np.ascontiguousarray(query, dtype=np.float32)
+        n = self.settings.series_length
+        if q.ndim != 1 or q.size != n:
+            raise UsageError(f"query length {q.size} does not match index series length {n}")
+        return self.exact_knn_batch(q[None, :], cfg)[0]
+
+
+def exact_knn(query, index, cfg: QueryConfig):
+    """One-shot convenience wrapper (query.py:351-357)."""
+    engine = QueryEngine(index)
+    try:
+        return engine.exact_knn(query, cfg)
+    finally:
+        engine.close()

@@ -192,7 +192,10 @@ def main() -> None:
         generate.generate_random_walk(1500, 64, 11, path)
         settings = IndexSettings(series_length=64, dataset_size=1500, leaf_threshold=64)
         idx = build_index(path, settings, num_threads=2)
-        qidx = write_index(idx, os.path.join(tmp, "idx"), num_threads=1)
+        idx_dir = os.path.join(OUT, "ref_index_1500x64")
+        import shutil
+        shutil.rmtree(idx_dir, ignore_errors=True)
+        qidx = write_index(idx, idx_dir, num_threads=1)
         data = core.read_series_file(path, 64)
         queries = np.concatenate([generate.random_walk_block(0, 4, 64, 1),
                                   data[[3, 700]] + np.float32(0.01)])
