@@ -18,7 +18,12 @@ struct ProfRec {
     const char *name;
     cudaEvent_t a, b;
     double bytes;
+    int slot;  // >= 0: device-side byte counter slot added to `bytes`
 };
+
+constexpr int PROF_SLOTS = 1 << 16;
+static unsigned long long *g_slots = nullptr;  // device counters
+static int g_next_slot = 0;
 
 static std::mutex g_mu;
 static bool g_on = false;
@@ -46,12 +51,25 @@ ProfScope::ProfScope(const char *name, cudaStream_t s, double bytes) : name_(nam
     cudaEventRecord((cudaEvent_t)a_, s_);
 }
 
+unsigned long long *ProfScope::counter()
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!a_) return nullptr;
+    if (!g_slots) {
+        if (cudaMalloc(&g_slots, sizeof(unsigned long long) * PROF_SLOTS) != cudaSuccess) return nullptr;
+        cudaMemset(g_slots, 0, sizeof(unsigned long long) * PROF_SLOTS);
+    }
+    if (g_next_slot >= PROF_SLOTS) return nullptr;
+    slot_ = g_next_slot++;
+    return g_slots + slot_;
+}
+
 ProfScope::~ProfScope()
 {
     if (!a_) return;
     cudaEventRecord((cudaEvent_t)b_, s_);
     std::lock_guard<std::mutex> g(g_mu);
-    g_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_, bytes_});
+    g_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_, bytes_, slot_});
 }
 
 }  // namespace ssb
@@ -75,6 +93,8 @@ void ssb_prof_reset(void)
         g_pool.push_back(r.b);
     }
     g_recs.clear();
+    if (g_slots && g_next_slot) cudaMemset(g_slots, 0, sizeof(unsigned long long) * g_next_slot);
+    g_next_slot = 0;
 }
 
 int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, int64_t *launches,
@@ -82,14 +102,17 @@ int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, i
 {
     std::lock_guard<std::mutex> g(g_mu);
     std::map<std::string, std::pair<double, std::pair<int64_t, double>>> agg;
+    std::vector<unsigned long long> slots(g_next_slot);
+    for (auto &r : g_recs) cudaEventSynchronize(r.b);
+    if (g_next_slot)
+        cudaMemcpy(slots.data(), g_slots, sizeof(unsigned long long) * g_next_slot, cudaMemcpyDeviceToHost);
     for (auto &r : g_recs) {
-        cudaEventSynchronize(r.b);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.a, r.b);
         auto &e = agg[r.name];
         e.first += ms;
         e.second.first += 1;
-        e.second.second += r.bytes;
+        e.second.second += r.bytes + (r.slot >= 0 ? (double)slots[r.slot] : 0.0);
     }
     int i = 0;
     for (auto &kv : agg) {

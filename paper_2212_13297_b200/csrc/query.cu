@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(256)
                const uint4 *__restrict__ words, int n, int L, const uint32_t *__restrict__ leaf_first,
                const uint32_t *__restrict__ leaf_count, const double *__restrict__ lbe,
                const uint64_t *__restrict__ thr, double slack_abs,
-               EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series)
+               EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series,
+               unsigned long long *__restrict__ prof_bytes)
 {
     __shared__ double T[WORD_SEGMENTS * ALPHABET];  // 32 KB
     const int q = blockIdx.x;
@@ -227,6 +228,13 @@ __global__ void __launch_bounds__(256)
     }
     if (lane == 0 && my_series) atomicAdd(&cand_series[q], my_series);
     if (threadIdx.x == 0) cand_leaves[q] = my_leaves;
+    if (threadIdx.x == 0 && prof_bytes) {
+        // words of every row of the surviving leaves + one LB_EAPCA per leaf read
+        unsigned long long b = 8ull * L;
+        for (int l = 0; l < L; l++)
+            if (lbe[(int64_t)q * L + l] <= bound) b += 16ull * leaf_count[l];
+        atomicAdd(prof_bytes, b);
+    }
 }
 
 // after sorting by (tile, query): tile boundaries -> tile list
@@ -489,7 +497,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         lbs_kernel<<<B, 256, 0, s>>>(qpaa.as<float>(), symlo.as<double>(), symhi.as<double>(),
                                      reinterpret_cast<const uint4 *>(ix.words), n, L, ix.leaf_first, ix.leaf_count,
                                      lbe.as<double>(), thr.as<uint64_t>(), slack_abs, eo, st_cand_leaves,
-                                     st_cand_series);
+                                     st_cand_series, ps.counter());
     }
     SSB_CHECK_LAUNCH();
     SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));

@@ -166,12 +166,16 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
     };
     if (tid == 0 && my_tiles > 0) issue(0);
+    unsigned long long my_bytes = 0;
 
     for (int64_t it = 0; it < my_tiles; it++) {
         if (tid == 0 && it + 1 < my_tiles) issue(it + 1);
         mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
         const int64_t t = blockIdx.x + it * gridDim.x;
         const uint32_t row0 = tl.row0[t];
+        if (tid == 0 && tl.bytes)
+            my_bytes += (unsigned long long)__popc(tl.umask[t]) * NT * 4 + 12ull +
+                        8ull * (tl.eptr[t + 1] - tl.eptr[t]);
         const float *buf = tiles + (it & 1) * TILE_ROWS * NT;
         const uint32_t e0 = tl.eptr[t], e1 = tl.eptr[t + 1];
         for (uint32_t e = e0 + g; e < e1; e += G) {
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
         __syncthreads();
     }
+    if (tid == 0 && tl.bytes && my_bytes) atomicAdd(tl.bytes, my_bytes);
 }
 
 // ---------------------------------------------------------------------------
@@ -333,7 +338,10 @@ static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileLis
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int64_t grid = std::min<int64_t>(tl.ntiles, (int64_t)num_sms() * 4);
     if (grid < 1) return OK;
-    scan_sparse_kernel<NT, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(X, row_id, tl, Q, out);
+    ProfScope ps("scan_sparse", s, 0.0);
+    TileList t2 = tl;
+    t2.bytes = ps.counter();
+    scan_sparse_kernel<NT, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(X, row_id, t2, Q, out);
     SSB_CHECK_LAUNCH();
     return OK;
 }

@@ -26,6 +26,7 @@ struct TileList {
     const uint32_t *eptr;   // [ntiles + 1] CSR into entries
     const uint2 *entries;   // (query, row mask)
     int64_t ntiles;
+    unsigned long long *bytes = nullptr;  // profiling: algorithmic bytes (nullable)
 };
 
 int64_t dense_ranges(int64_t N, int nq, int k, int cap);
@@ -67,12 +68,16 @@ class ProfScope {
   public:
     ProfScope(const char *name, cudaStream_t s, double bytes);
     ~ProfScope();
+    // device counter the kernel may atomicAdd its algorithmic bytes into
+    // (nullptr when profiling is off); read back by ssb_prof_read
+    unsigned long long *counter();
 
   private:
     const char *name_;
     cudaStream_t s_;
     double bytes_;
     void *a_ = nullptr, *b_ = nullptr;
+    int slot_ = -1;
 };
 
 // host-side launch accounting (counts kernels this library launched)

@@ -159,6 +159,13 @@ class QueryEngine:
                   stats.ctypes.data_as(_lib.P) if want_stats else None, stream_handle())
         return (d2, ids, pos, stats) if want_stats else (d2, ids, pos)
 
+    def exact_knn_arrays(self, queries, k: int):
+        """Batched public form over HOST buffers: (d2, ids, pos) numpy arrays
+        (B, k); the H2D copy of the queries and the D2H copy of the answers
+        are part of the call."""
+        d2, ids, pos = self.knn_device(queries, k)
+        return d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
+
     def _stats(self, row, cfg: QueryConfig, wall: float) -> QueryStats:
         n = self.settings.series_length
         cand_leaves, cand_series, seed_rows = int(row[0]), int(row[1]), int(row[2])
