@@ -37,8 +37,6 @@
 
 namespace ssb {
 
-int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words,
-                 float *paa_out, cudaStream_t s);
 
 Index::~Index()
 {
@@ -469,6 +467,12 @@ __global__ void gather_rows_kernel(const float *__restrict__ X, int n, const uin
     if (lane == 0) inv[src] = (uint32_t)row;
 }
 
+__global__ void inv_from_orig_kernel(const uint32_t *__restrict__ orig, int64_t N, uint32_t *__restrict__ inv)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) inv[orig[i]] = (uint32_t)i;
+}
+
 __global__ void absmax_kernel(const float *__restrict__ X, int64_t count, uint32_t *__restrict__ out)
 {
     float m = 0.f;
@@ -866,11 +870,12 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
     SSB_CUDA(cudaMemcpyAsync(ix->orig, perm, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
     {
-        ProfScope ps("build_gather", s, 2.0 * N * n * 4 + 12.0 * N);
-        gather_rows_kernel<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(X, n, perm, N, ix->X, ix->inv);
+        ProfScope ps("build_gather", s, 2.0 * N * n * 4);
+        RC(launch_layout_rows(X, perm, N, n, ix->X, true, s));
     }
+    inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
-    RC(launch_words(ix->X, N, n, ix->bp, ix->words, nullptr, s));
+    RC(launch_words(X, N, n, ix->bp, ix->words, nullptr, s, perm));
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
@@ -933,12 +938,6 @@ int finalize_tree(Index &ixr, cudaStream_t s)
     return OK;
 }
 
-__global__ void inv_from_orig_kernel(const uint32_t *__restrict__ orig, int64_t N, uint32_t *__restrict__ inv)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < N) inv[orig[i]] = (uint32_t)i;
-}
-
 // an index from host arrays already in leaf order (persist.py:461-528 load_index)
 int index_from_host(const float *rows, const uint8_t *words, const uint32_t *orig, int64_t N, int n, int64_t tau,
                     int64_t id_base, std::vector<TreeNode> nodes, const double *bp_dev, Index **out, cudaStream_t s)
@@ -958,7 +957,14 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
     SSB_CUDA(cudaMalloc(&ix->inv, (size_t)N * 4));
     SSB_CUDA(cudaMalloc(&ix->bp, 8 * (ALPHABET - 1)));
     SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
-    SSB_CUDA(cudaMemcpy(ix->X, rows, (size_t)N * n * 4, cudaMemcpyHostToDevice));
+    {
+        DevBuf tmp;
+        SSB_CUDA(tmp.alloc((size_t)N * n * 4, s));
+        SSB_CUDA(cudaMemcpyAsync(tmp.p, rows, (size_t)N * n * 4, cudaMemcpyHostToDevice, s));
+        RC(launch_layout_rows(tmp.as<float>(), nullptr, N, n, ix->X, true, s));
+        if (!words) RC(launch_words(tmp.as<float>(), N, n, ix->bp, ix->words, nullptr, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+    }
     if (orig) {
         SSB_CUDA(cudaMemcpy(ix->orig, orig, (size_t)N * 4, cudaMemcpyHostToDevice));
     } else {
@@ -967,11 +973,7 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
     }
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
-    if (words) {
-        SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
-    } else {
-        RC(launch_words(ix->X, N, n, ix->bp, ix->words, nullptr, s));
-    }
+    if (words) SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
     DevBuf amax;
     SSB_CUDA(amax.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));

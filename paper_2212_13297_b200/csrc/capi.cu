@@ -33,8 +33,26 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 
 void note_launch(int count) { g_launches.fetch_add(count, std::memory_order_relaxed); }
 
+// keep freed stream-ordered allocations cached in the device's default pool
+// (the default release threshold of 0 hands them back to the driver at every
+// synchronization, which turns each per-batch cudaMallocAsync into a real
+// allocation)
+static void tune_mempool()
+{
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
 int num_sms()
 {
+    tune_mempool();
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -45,8 +63,6 @@ int num_sms()
     return sms;
 }
 
-int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words,
-                 float *paa_out, cudaStream_t s);
 int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, int npts,
                          const int32_t *seg_s, const int32_t *seg_e, int m, float *mean, float *sd,
                          cudaStream_t s);
@@ -262,7 +278,15 @@ int ssb_index_download(const ssb_index *h, float *rows_host, uint8_t *words_host
 {
     SSB_REQUIRE(h, "null index");
     const Index &ix = *h->ix;
-    if (rows_host) SSB_CUDA(cudaMemcpy(rows_host, ix.X, (size_t)ix.N * ix.n * 4, cudaMemcpyDeviceToHost));
+    if (rows_host) {
+        DevBuf tmp;
+        cudaStream_t s = nullptr;
+        SSB_CUDA(tmp.alloc((size_t)ix.N * ix.n * 4, s));
+        int rc = launch_layout_rows(ix.X, nullptr, ix.N, ix.n, tmp.as<float>(), false, s);
+        if (rc) return rc;
+        SSB_CUDA(cudaMemcpyAsync(rows_host, tmp.p, (size_t)ix.N * ix.n * 4, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+    }
     if (words_host) SSB_CUDA(cudaMemcpy(words_host, ix.words, (size_t)ix.N * WORD_SEGMENTS, cudaMemcpyDeviceToHost));
     if (orig_host) SSB_CUDA(cudaMemcpy(orig_host, ix.orig, (size_t)ix.N * 4, cudaMemcpyDeviceToHost));
     return OK;

@@ -1,0 +1,142 @@
+// layout.cuh -- the index's in-row element layout ("lane-transposed").
+//
+// The exact distance (ssb_common.cuh group_ed2) is computed by an 8-lane
+// group whose lane j accumulates elements 8i+j of each pairwise block
+// (numpy's r[j]).  In HBM and shared memory the index stores each row so that
+// lane j's elements of a block are contiguous: block (off, len), m = len/8
+// elements per lane, element off+8i+j lives at off + j*m + chunk slot.  Lanes
+// read their elements with 16-byte LDS.128 (4 consecutive i), and chunks are
+// rotated per lane (swizzle) so the 8 lanes of a group hit 8 distinct 16-byte
+// bank quads: one shared-memory wavefront per group per load.
+//
+// The layout is a fixed permutation inside each row; words, statistics and
+// all reported values are computed on the logical (reference) element order.
+#pragma once
+
+#include "ssb_common.cuh"
+
+namespace ssb {
+
+__host__ __device__ constexpr int lay_cw(int m) { return (m % 4 == 0) ? 4 : ((m % 2 == 0) ? 2 : 1); }
+
+// chunk rotation of lane j for a block with m elements per lane
+__host__ __device__ constexpr int lay_swz(int m, int j)
+{
+    return (lay_cw(m) == 4 && (m / 4 == 2 || m / 4 == 4)) ? (j * (m / 4)) / 8 : 0;
+}
+
+// physical position of logical element e in a row of n (n % 8 == 0)
+__host__ __device__ inline int layout_pos(int n, int e)
+{
+    int off = 0, len = n;
+    while (len > 128) {
+        const int h = len / 2 - (len / 2) % 8;
+        if (e < off + h) {
+            len = h;
+        } else {
+            off += h;
+            len -= h;
+        }
+    }
+    const int m = len / 8, r = e - off, i = r / 8, j = r % 8;
+    const int cw = lay_cw(m), nch = m / cw, c = i / cw, t = i % cw;
+    const int slot = (c + lay_swz(m, j)) % nch;
+    return off + j * m + slot * cw + t;
+}
+
+// ---------------------------------------------------------------------------
+// exact squared distance of one layout-ordered row (shared memory) against a
+// query held in registers (qv[i] = q[8i + j] for block-relative i, i.e.
+// qv[OFF/8 + i]); bit-identical to group_ed2 / numpy's pairwise sum.
+
+template <int OFF, int LEN, int NQ>
+__device__ __forceinline__ float lay_block(const float *__restrict__ xs, const float (&qv)[NQ], int j,
+                                          unsigned gmask)
+{
+    static_assert(LEN % 8 == 0 && OFF % 8 == 0, "8-aligned blocks");
+    if constexpr (LEN <= 128) {
+        constexpr int m = LEN / 8, cw = lay_cw(m), nch = m / cw;
+        const int sj = lay_swz(m, j);
+        const float *base = xs + OFF + j * m;
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < nch; c++) {
+            const int slot = (c + sj) % nch;
+            float v[cw];
+            if constexpr (cw == 4) {
+                const float4 f = *reinterpret_cast<const float4 *>(base + slot * 4);
+                v[0] = f.x;
+                v[1] = f.y;
+                v[2] = f.z;
+                v[3] = f.w;
+            } else if constexpr (cw == 2) {
+                const float2 f = *reinterpret_cast<const float2 *>(base + slot * 2);
+                v[0] = f.x;
+                v[1] = f.y;
+            } else {
+                v[0] = base[slot];
+            }
+#pragma unroll
+            for (int t = 0; t < cw; t++) {
+                const float d = __fsub_rn(v[t], qv[OFF / 8 + c * cw + t]);
+                acc = (c == 0 && t == 0) ? __fmul_rn(d, d) : __fadd_rn(acc, __fmul_rn(d, d));
+            }
+        }
+        acc = __fadd_rn(acc, __shfl_xor_sync(gmask, acc, 1));
+        acc = __fadd_rn(acc, __shfl_xor_sync(gmask, acc, 2));
+        acc = __fadd_rn(acc, __shfl_xor_sync(gmask, acc, 4));
+        return acc;
+    } else {
+        constexpr int H = LEN / 2 - (LEN / 2) % 8;
+        const float a = lay_block<OFF, H, NQ>(xs, qv, j, gmask);
+        const float b = lay_block<OFF + H, LEN - H, NQ>(xs, qv, j, gmask);
+        return __fadd_rn(a, b);
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ float lay_ed2(const float *__restrict__ xs, const float (&qv)[NT / 8], int j,
+                                        unsigned gmask)
+{
+    return lay_block<0, NT, NT / 8>(xs, qv, j, gmask);
+}
+
+// load lane j's query registers from a layout-ordered query row (global)
+template <int OFF, int LEN, int NQ>
+__device__ __forceinline__ void lay_load_q_block(const float *__restrict__ q, float (&qv)[NQ], int j)
+{
+    if constexpr (LEN <= 128) {
+        constexpr int m = LEN / 8, cw = lay_cw(m), nch = m / cw;
+        const int sj = lay_swz(m, j);
+        const float *base = q + OFF + j * m;
+#pragma unroll
+        for (int c = 0; c < nch; c++) {
+            const int slot = (c + sj) % nch;
+            if constexpr (cw == 4) {
+                const float4 f = __ldg(reinterpret_cast<const float4 *>(base + slot * 4));
+                qv[OFF / 8 + c * 4 + 0] = f.x;
+                qv[OFF / 8 + c * 4 + 1] = f.y;
+                qv[OFF / 8 + c * 4 + 2] = f.z;
+                qv[OFF / 8 + c * 4 + 3] = f.w;
+            } else if constexpr (cw == 2) {
+                const float2 f = __ldg(reinterpret_cast<const float2 *>(base + slot * 2));
+                qv[OFF / 8 + c * 2 + 0] = f.x;
+                qv[OFF / 8 + c * 2 + 1] = f.y;
+            } else {
+                qv[OFF / 8 + c] = __ldg(base + slot);
+            }
+        }
+    } else {
+        constexpr int H = LEN / 2 - (LEN / 2) % 8;
+        lay_load_q_block<OFF, H, NQ>(q, qv, j);
+        lay_load_q_block<OFF + H, LEN - H, NQ>(q, qv, j);
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void lay_load_q(const float *__restrict__ q, float (&qv)[NT / 8], int j)
+{
+    lay_load_q_block<0, NT, NT / 8>(q, qv, j);
+}
+
+}  // namespace ssb

@@ -430,6 +430,11 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
     SSB_CUDA(thr.alloc(8 * (size_t)B, s));
     int rc = launch_query_prep(Q, B, n, cs.as<double>(), c2.as<double>(), qpaa.as<float>(), s);
     if (rc) return rc;
+    DevBuf qlay;
+    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
+    rc = launch_layout_rows(Q, nullptr, B, n, qlay.as<float>(), true, s);
+    if (rc) return rc;
+    const float *Qp = qlay.as<float>();
     {
         const int smem = 16 * (n + 1);
         ProfScope ps("lbe", s, (double)L * (M_MAX * 20 + 12) + 16.0 * B * (n + 1));
@@ -480,7 +485,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
                     tb.ntiles};
         ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
         if (rc) return rc;
         rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                            flags.as<int32_t>(), s);
@@ -513,7 +518,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
                 tb.ntiles};
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-    rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+    rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
     if (rc) return rc;
     std::vector<int32_t> hflags(B);
     DevBuf keep;
@@ -537,7 +542,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         SSB_CHECK_LAUNCH();
         reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
         SSB_CHECK_LAUNCH();
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Q, so, s);
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
         if (rc) return rc;
         restore_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
                                                                            keep.as<uint32_t>());

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "layout.cuh"
 #include "ssb_common.cuh"
 #include "ssb_internal.h"
 
@@ -124,12 +125,16 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---------------------------------------------------------------------------
-// sparse scan over (tile, query, row-mask) work lists
+// sparse scan over (tile, query, row-mask) work lists.
+// Rows AND queries are in the lane-transposed layout (layout.cuh): one LDS.128
+// per lane per 4 elements, one shared-memory wavefront per 8-lane group.  A
+// group owns one entry (query, mask) at a time; the next entry's query is
+// prefetched into registers while the current one is computed.
 
 template <int NT, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     scan_sparse_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
-                       TileList tl, const float *__restrict__ Q, ScanOut out)
+                       TileList tl, const float *__restrict__ Qp, ScanOut out)
 {
     constexpr int G = WARPS * 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -170,34 +175,47 @@ __global__ void __launch_bounds__(WARPS * 32)
 
     for (int64_t it = 0; it < my_tiles; it++) {
         if (tid == 0 && it + 1 < my_tiles) issue(it + 1);
-        mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
         const int64_t t = blockIdx.x + it * gridDim.x;
         const uint32_t row0 = tl.row0[t];
-        if (tid == 0 && tl.bytes)
-            my_bytes += (unsigned long long)__popc(tl.umask[t]) * NT * 4 + 12ull +
-                        8ull * (tl.eptr[t + 1] - tl.eptr[t]);
-        const float *buf = tiles + (it & 1) * TILE_ROWS * NT;
         const uint32_t e0 = tl.eptr[t], e1 = tl.eptr[t + 1];
-        for (uint32_t e = e0 + g; e < e1; e += G) {
-            const uint2 ent = tl.entries[e];
+        if (tid == 0 && tl.bytes)
+            my_bytes += (unsigned long long)__popc(tl.umask[t]) * NT * 4 + 12ull + 8ull * (e1 - e0);
+        // first entry's query load overlaps the tile's TMA
+        uint32_t e = e0 + g;
+        float qv[NT / 8], qn[NT / 8];
+        uint2 ent = make_uint2(0, 0), entn = make_uint2(0, 0);
+        if (e < e1) {
+            ent = tl.entries[e];
+            lay_load_q<NT>(Qp + (int64_t)ent.x * NT, qv, j);
+        }
+        mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
+        const float *buf = tiles + (it & 1) * TILE_ROWS * NT;
+        for (; e < e1; e += G) {
+            const bool more = e + G < e1;
+            if (more) {
+                entn = tl.entries[e + G];
+                lay_load_q<NT>(Qp + (int64_t)entn.x * NT, qn, j);
+            }
             const int q = (int)ent.x;
             uint32_t mask = ent.y;
-            float qv[NT / 8];
-#pragma unroll
-            for (int i = 0; i < NT / 8; i++) qv[i] = Q[(int64_t)q * NT + 8 * i + j];
             const uint64_t bound = out.thr[q];
             while (mask) {
-                int r = __ffs(mask) - 1;
+                const int r = __ffs(mask) - 1;
                 mask &= mask - 1;
-                float d2 = group_ed2<NT>(buf + r * NT, qv, j, gmask);
+                const float d2 = lay_ed2<NT>(buf + r * NT, qv, j, gmask);
                 if (j == 0) {
-                    uint32_t pos = row0 + r;
-                    uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
+                    const uint32_t pos = row0 + r;
+                    const uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
                     if (key <= bound) {
-                        uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+                        const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
                         if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
                     }
                 }
+            }
+            if (more) {
+#pragma unroll
+                for (int i = 0; i < NT / 8; i++) qv[i] = qn[i];
+                ent = entn;
             }
         }
         __syncthreads();

@@ -39,6 +39,11 @@ int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, u
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s);
 
+int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words, float *paa_out,
+                 cudaStream_t s, const uint32_t *rows = nullptr);
+int launch_layout_rows(const float *src, const uint32_t *rows, int64_t N, int n, float *dst, bool to_layout,
+                       cudaStream_t s);
+
 // stream-ordered device scratch (cudaMallocAsync pool); freed on scope exit
 struct DevBuf {
     void *p = nullptr;

@@ -14,6 +14,7 @@
 // rounded to float32 -- no FMA anywhere (--fmad=false + _rn intrinsics).
 #include <cuda_runtime.h>
 
+#include "layout.cuh"
 #include "ssb_common.cuh"
 #include "ssb_internal.h"
 
@@ -36,7 +37,7 @@ __device__ __forceinline__ int sax_symbol(double v, const double *bp)
 template <int W>
 __global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
                              const double *__restrict__ bp_g, uint8_t *__restrict__ words,
-                             float *__restrict__ paa_out)
+                             float *__restrict__ paa_out, const uint32_t *__restrict__ rows)
 {
     __shared__ double bp[ALPHABET];
     for (int i = threadIdx.x; i < ALPHABET - 1; i += blockDim.x) bp[i] = bp_g[i];
@@ -45,7 +46,7 @@ __global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
     if (t >= N * WORD_SEGMENTS) return;
     const int64_t row = t / WORD_SEGMENTS;
     const int seg = (int)(t % WORD_SEGMENTS);
-    const float *x = X + row * n + seg * (n / WORD_SEGMENTS);
+    const float *x = X + (rows ? (int64_t)rows[row] : row) * n + seg * (n / WORD_SEGMENTS);
     float sum;
     if constexpr (W > 0) {
         float v[W];
@@ -72,7 +73,7 @@ __global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
 }
 
 int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *words,
-                 float *paa_out, cudaStream_t s)
+                 float *paa_out, cudaStream_t s, const uint32_t *rows)
 {
     SSB_REQUIRE(n % WORD_SEGMENTS == 0, "series length must be divisible by 16 word segments");
     if (N == 0) return OK;
@@ -80,13 +81,45 @@ int launch_words(const float *X, int64_t N, int n, const double *bp, uint8_t *wo
     const unsigned grid = (unsigned)((threads + 255) / 256);
     ProfScope ps("words", s, (double)N * n * 4 + (double)N * 16 + (paa_out ? (double)N * 64 : 0.0));
     switch (n / WORD_SEGMENTS) {
-    case 4: words_kernel<4><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
-    case 6: words_kernel<6><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
-    case 8: words_kernel<8><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
-    case 16: words_kernel<16><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
-    case 32: words_kernel<32><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
-    default: words_kernel<0><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out); break;
+    case 4: words_kernel<4><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
+    case 6: words_kernel<6><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
+    case 8: words_kernel<8><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
+    case 16: words_kernel<16><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
+    case 32: words_kernel<32><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
+    default: words_kernel<0><<<grid, 256, 0, s>>>(X, N, n, bp, words, paa_out, rows); break;
     }
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// row layout conversion (layout.cuh): one warp per row.
+// to_layout: dst[r][layout_pos(e)] = src[rows ? rows[r] : r][e]
+// else     : dst[r][e] = src[r][layout_pos(e)]
+
+__global__ void layout_rows_kernel(const float *__restrict__ src, const uint32_t *__restrict__ rows, int64_t N,
+                                   int n, float *__restrict__ dst, int to_layout)
+{
+    const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    if (r >= N) return;
+    const int lane = threadIdx.x & 31;
+    const float *s = src + (rows ? (int64_t)rows[r] : r) * n;
+    float *d = dst + r * n;
+    for (int e = lane; e < n; e += 32) {
+        const int p = layout_pos(n, e);
+        if (to_layout)
+            d[p] = __ldg(s + e);
+        else
+            d[e] = __ldg(s + p);
+    }
+}
+
+int launch_layout_rows(const float *src, const uint32_t *rows, int64_t N, int n, float *dst, bool to_layout,
+                       cudaStream_t s)
+{
+    SSB_REQUIRE(n % 8 == 0, "layout needs n % 8 == 0");
+    if (N == 0) return OK;
+    layout_rows_kernel<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(src, rows, N, n, dst, to_layout ? 1 : 0);
     SSB_CHECK_LAUNCH();
     return OK;
 }
