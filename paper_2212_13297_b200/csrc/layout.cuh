@@ -94,6 +94,74 @@ __device__ __forceinline__ float lay_block(const float *__restrict__ xs, const f
     }
 }
 
+// two rows against the same query: two independent accumulator chains (ILP)
+template <int OFF, int LEN, int NQ>
+__device__ __forceinline__ void lay_block2(const float *__restrict__ xa, const float *__restrict__ xb,
+                                           const float (&qv)[NQ], int j, unsigned gmask, float &ra, float &rb)
+{
+    if constexpr (LEN <= 128) {
+        constexpr int m = LEN / 8, cw = lay_cw(m), nch = m / cw;
+        const int sj = lay_swz(m, j);
+        const float *ba = xa + OFF + j * m;
+        const float *bb = xb + OFF + j * m;
+        float a = 0.0f, b = 0.0f;
+#pragma unroll
+        for (int c = 0; c < nch; c++) {
+            const int slot = (c + sj) % nch;
+            float va[cw], vb[cw];
+            if constexpr (cw == 4) {
+                const float4 fa = *reinterpret_cast<const float4 *>(ba + slot * 4);
+                const float4 fb = *reinterpret_cast<const float4 *>(bb + slot * 4);
+                va[0] = fa.x; va[1] = fa.y; va[2] = fa.z; va[3] = fa.w;
+                vb[0] = fb.x; vb[1] = fb.y; vb[2] = fb.z; vb[3] = fb.w;
+            } else if constexpr (cw == 2) {
+                const float2 fa = *reinterpret_cast<const float2 *>(ba + slot * 2);
+                const float2 fb = *reinterpret_cast<const float2 *>(bb + slot * 2);
+                va[0] = fa.x; va[1] = fa.y;
+                vb[0] = fb.x; vb[1] = fb.y;
+            } else {
+                va[0] = ba[slot];
+                vb[0] = bb[slot];
+            }
+#pragma unroll
+            for (int t = 0; t < cw; t++) {
+                const float qq = qv[OFF / 8 + c * cw + t];
+                const float da = __fsub_rn(va[t], qq), db = __fsub_rn(vb[t], qq);
+                if (c == 0 && t == 0) {
+                    a = __fmul_rn(da, da);
+                    b = __fmul_rn(db, db);
+                } else {
+                    a = __fadd_rn(a, __fmul_rn(da, da));
+                    b = __fadd_rn(b, __fmul_rn(db, db));
+                }
+            }
+        }
+        a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 1));
+        b = __fadd_rn(b, __shfl_xor_sync(gmask, b, 1));
+        a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 2));
+        b = __fadd_rn(b, __shfl_xor_sync(gmask, b, 2));
+        a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 4));
+        b = __fadd_rn(b, __shfl_xor_sync(gmask, b, 4));
+        ra = a;
+        rb = b;
+    } else {
+        constexpr int H = LEN / 2 - (LEN / 2) % 8;
+        float a0, b0, a1, b1;
+        lay_block2<OFF, H, NQ>(xa, xb, qv, j, gmask, a0, b0);
+        lay_block2<OFF + H, LEN - H, NQ>(xa, xb, qv, j, gmask, a1, b1);
+        ra = __fadd_rn(a0, a1);
+        rb = __fadd_rn(b0, b1);
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void lay_ed2_x2(const float *__restrict__ xa, const float *__restrict__ xb,
+                                           const float (&qv)[NT / 8], int j, unsigned gmask, float &da,
+                                           float &db)
+{
+    lay_block2<0, NT, NT / 8>(xa, xb, qv, j, gmask, da, db);
+}
+
 template <int NT>
 __device__ __forceinline__ float lay_ed2(const float *__restrict__ xs, const float (&qv)[NT / 8], int j,
                                         unsigned gmask)

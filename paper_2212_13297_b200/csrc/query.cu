@@ -133,7 +133,7 @@ __global__ void lbe_kernel(const double *__restrict__ cs_g, const double *__rest
 
 // Entry = (tile, query, mask).  Appended with a global counter.
 struct EntryOut {
-    uint64_t *key;   // (tile << 32) | query
+    uint64_t *key;   // (tile << 32) | ((32 - popc(mask)) << 26) | query
     uint32_t *mask;
     uint32_t *count;
     int64_t cap;
@@ -143,7 +143,7 @@ __device__ __forceinline__ void emit_entry(const EntryOut &eo, uint32_t tile, ui
 {
     const uint32_t slot = atomicAdd(eo.count, 1u);
     if ((int64_t)slot < eo.cap) {
-        eo.key[slot] = ((uint64_t)tile << 32) | q;
+        eo.key[slot] = ((uint64_t)tile << 32) | ((uint64_t)(32 - __popc(mask)) << 26) | q;
         eo.mask[slot] = mask;
     }
 }
@@ -267,7 +267,7 @@ __global__ void tile_build_kernel(const uint64_t *__restrict__ keys, const uint3
         eptr[s] = (uint32_t)i;
     }
     atomicOr(&umask[s], masks[i]);
-    entries[i] = make_uint2((uint32_t)(keys[i] & 0xffffffffu), masks[i]);
+    entries[i] = make_uint2((uint32_t)(keys[i] & 0x3ffffffu), masks[i]);
 }
 
 __global__ void thr_from_keys_kernel(const uint64_t *__restrict__ keys, int B, int k, uint64_t *__restrict__ thr)
@@ -374,8 +374,11 @@ struct TileBufs {
     int64_t E = 0;
 };
 
-static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cudaStream_t s)
+static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cudaStream_t s, int64_t N)
 {
+    int tbits = 1;
+    while ((1ll << tbits) <= N / TILE_ROWS + 1) tbits++;
+    const int end_bit = 32 + tbits;
     tb.E = E;
     tb.ntiles = 0;
     if (E == 0) return OK;
@@ -384,10 +387,10 @@ static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cud
     SSB_CUDA(m2.alloc(4 * (size_t)E, s));
     size_t tb_bytes = 0;
     SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
-                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, 64, s));
+                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, end_bit, s));
     SSB_CUDA(tmp.alloc(tb_bytes, s));
     SSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
-                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, 64, s));
+                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, end_bit, s));
     note_launch(1);
     SSB_CUDA(flags.alloc(4 * (size_t)(E + 1), s));
     SSB_CUDA(slot.alloc(4 * (size_t)(E + 1), s));
@@ -418,7 +421,7 @@ static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cud
 // one batch of queries (Bq <= cap-sized batch)
 static int query_batch(const Index &ix, const float *Q, int B, int k, double slack_abs, uint64_t *out_keys,
                        uint32_t *st_cand_leaves, uint32_t *st_cand_series, uint32_t *st_seed_rows,
-                       int32_t *st_rounds, int64_t entry_cap, cudaStream_t s)
+                       int32_t *st_rounds, uint32_t *st_over, int64_t entry_cap, cudaStream_t s)
 {
     const int n = ix.n, L = ix.L;
     DevBuf cs, c2, qpaa, lbe, best, thr, cand, cnt, flags, ekey, emask, ecount, symlo, symhi;
@@ -459,7 +462,8 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         SSB_CUDA(cudaStreamSynchronize(s));
     }
 
-    const int cap = 16384;
+    // candidate capacity per query: generous, so the bound-tightening rescan is rare
+    const int cap = (int)std::min<int64_t>(std::max<int64_t>(16384, ix.N / 16), 262144);
     SSB_CUDA(cand.alloc(8 * (size_t)B * cap, s));
     SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
     SSB_CUDA(flags.alloc(4 * (size_t)B, s));
@@ -480,12 +484,12 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     {
         TileBufs tb;
-        rc = build_tiles(ekey, emask, E, tb, s);
+        rc = build_tiles(ekey, emask, E, tb, s, ix.N);
         if (rc) return rc;
         TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
                     tb.ntiles};
         ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s, "scan_seed");
         if (rc) return rc;
         rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                            flags.as<int32_t>(), s);
@@ -512,7 +516,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         return -1;  // caller splits the batch
     }
     TileBufs tb;
-    rc = build_tiles(ekey, emask, E, tb, s);
+    rc = build_tiles(ekey, emask, E, tb, s, ix.N);
     if (rc) return rc;
     TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
                 tb.ntiles};
@@ -530,6 +534,8 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         SSB_CUDA(cudaStreamSynchronize(s));
         int over = 0;
         for (int q = 0; q < B; q++) over += hflags[q];
+        if (round == 0 && st_over)
+            SSB_CUDA(cudaMemcpyAsync(st_over, flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
         if (!over) {
             if (st_rounds) *st_rounds = round;
             break;
@@ -542,7 +548,7 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         SSB_CHECK_LAUNCH();
         reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
         SSB_CHECK_LAUNCH();
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s, "scan_retry");
         if (rc) return rc;
         restore_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
                                                                            keep.as<uint32_t>());
@@ -557,6 +563,7 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
 {
     SSB_REQUIRE(k >= 1, "k must be at least 1");
     SSB_REQUIRE(k <= 4096, "k above 4096 is not supported");
+    SSB_REQUIRE(B < (1 << 26), "too many queries in one call");
     if (B == 0) return OK;
     const int n = ix.n;
     // statistic-rounding slack: delta * sqrt(2n) in distance units
@@ -575,8 +582,9 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
     const double delta = std::ldexp(M, -19);
     const double slack_abs = delta * std::sqrt(2.0 * n);
 
-    DevBuf keys, stl, sts, str;
+    DevBuf keys, stl, sts, str, sto;
     SSB_CUDA(keys.alloc(8 * (size_t)B * k, s));
+    SSB_CUDA(sto.alloc(4 * (size_t)B, s));
     SSB_CUDA(stl.alloc(4 * (size_t)B, s));
     SSB_CUDA(sts.alloc(4 * (size_t)B, s));
     SSB_CUDA(str.alloc(4 * (size_t)B, s));
@@ -590,7 +598,8 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
         const int64_t ecap = std::min<int64_t>((int64_t)nb * per_query_worst, budget);
         int32_t r = 0;
         int rc = query_batch(ix, Q + (int64_t)q0 * n, nb, k, slack_abs, keys.as<uint64_t>() + (int64_t)q0 * k,
-                             stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0, &r, ecap, s);
+                             stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0, &r,
+                             sto.as<uint32_t>() + q0, ecap, s);
         if (rc == -1) {  // entry overflow: halve the batch and retry
             SSB_REQUIRE(nb > 1, "a single query overflowed the candidate entry buffer");
             bq = std::max(1, nb / 2);
@@ -603,7 +612,8 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
                                     out_pos, s);
     if (rc) return rc;
     if (stats_host) {
-        std::vector<uint32_t> a(B), b(B), c(B);
+        std::vector<uint32_t> a(B), b(B), c(B), d(B);
+        SSB_CUDA(cudaMemcpyAsync(d.data(), sto.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(a.data(), stl.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(b.data(), sts.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(c.data(), str.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
@@ -612,7 +622,7 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
             stats_host[4 * q + 0] = a[q];
             stats_host[4 * q + 1] = b[q];
             stats_host[4 * q + 2] = c[q];
-            stats_host[4 * q + 3] = 0;
+            stats_host[4 * q + 3] = d[q];  // 1 = candidate buffer overflowed once
         }
     }
     SSB_CUDA(cudaStreamSynchronize(s));

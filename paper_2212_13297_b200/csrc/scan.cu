@@ -200,15 +200,28 @@ __global__ void __launch_bounds__(WARPS * 32)
             uint32_t mask = ent.y;
             const uint64_t bound = out.thr[q];
             while (mask) {
-                const int r = __ffs(mask) - 1;
+                const int r0 = __ffs(mask) - 1;
                 mask &= mask - 1;
-                const float d2 = lay_ed2<NT>(buf + r * NT, qv, j, gmask);
+                float d0, d1 = 0.f;
+                int r1 = -1;
+                if (mask) {
+                    r1 = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    lay_ed2_x2<NT>(buf + r0 * NT, buf + r1 * NT, qv, j, gmask, d0, d1);
+                } else {
+                    d0 = lay_ed2<NT>(buf + r0 * NT, qv, j, gmask);
+                }
                 if (j == 0) {
-                    const uint32_t pos = row0 + r;
-                    const uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
-                    if (key <= bound) {
-                        const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
-                        if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int r = h ? r1 : r0;
+                        if (r < 0) break;
+                        const uint32_t pos = row0 + r;
+                        const uint64_t key = make_key(h ? d1 : d0, row_id ? row_id[pos] : pos);
+                        if (key <= bound) {
+                            const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+                            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+                        }
                     }
                 }
             }
@@ -224,31 +237,24 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---------------------------------------------------------------------------
-// K-select: per query, sort its candidates (bitonic in shared memory) and
-// emit the first k; flag overflow and tighten the bound when it happened.
+// K-select: per query, the k smallest (d2, id) keys of its candidate buffer.
+// Up to SELECT_SMALL candidates: bitonic sort in shared memory.  Above that:
+// an exact MSB radix select of the k-th key (8 passes of 8 bits over the
+// 64-bit keys, 256-bin shared histograms), then the k keys <= it are
+// collected and sorted.  A query whose buffer overflowed gets the k-th
+// stored key as its new, tighter bound (a valid bound: k real distances).
 
-__global__ void select_topk_kernel(const uint64_t *__restrict__ cand, uint32_t *__restrict__ cnt,
-                                   int cap, int P, int k, uint64_t *__restrict__ thr,
-                                   uint64_t *__restrict__ out_keys, int32_t *__restrict__ flags)
+constexpr int SELECT_SMALL = 8192;
+
+__device__ void bitonic_sort_smem(uint64_t *sk, int p2)
 {
-    extern __shared__ __align__(16) uint64_t sk[];
-    const int q = blockIdx.x;
-    const uint32_t total = cnt[q];
-    const int c = (int)tmin<uint32_t>(total, (uint32_t)cap);
-    // smallest power of two >= max(c, k), capped at P
-    int p2 = 1;
-    while (p2 < c || p2 < k) p2 <<= 1;
-    if (p2 > P) p2 = P;
-    for (int i = threadIdx.x; i < p2; i += blockDim.x)
-        sk[i] = i < c ? cand[(size_t)q * cap + i] : KEY_EMPTY;
-    __syncthreads();
     for (int size = 2; size <= p2; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
-                int lo = 2 * i - (i & (stride - 1));
-                int hi = lo + stride;
-                bool up = ((lo & size) == 0);
-                uint64_t a = sk[lo], b = sk[hi];
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const uint64_t a = sk[lo], b = sk[hi];
                 if ((a > b) == up) {
                     sk[lo] = b;
                     sk[hi] = a;
@@ -257,12 +263,74 @@ __global__ void select_topk_kernel(const uint64_t *__restrict__ cand, uint32_t *
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < k; i += blockDim.x)
-        out_keys[(size_t)q * k + i] = i < p2 ? sk[i] : KEY_EMPTY;
+}
+
+__global__ void __launch_bounds__(1024)
+    select_topk_kernel(const uint64_t *__restrict__ cand, uint32_t *__restrict__ cnt, int cap, int k,
+                       uint64_t *__restrict__ thr, uint64_t *__restrict__ out_keys, int32_t *__restrict__ flags)
+{
+    extern __shared__ __align__(16) uint64_t sk[];
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ uint32_t s_rank, s_fill;
+    const int q = blockIdx.x;
+    const uint32_t total = cnt[q];
+    const int c = (int)tmin<uint32_t>(total, (uint32_t)cap);
+    const uint64_t *keys = cand + (size_t)q * cap;
+    int p2 = 1;
+    if (c <= SELECT_SMALL) {
+        while (p2 < c || p2 < k) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) sk[i] = i < c ? keys[i] : KEY_EMPTY;
+        __syncthreads();
+    } else {
+        // exact k-th smallest key (k <= c)
+        if (threadIdx.x == 0) {
+            s_prefix = 0;
+            s_rank = (uint32_t)k;
+        }
+        uint64_t mask = 0;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            const uint64_t prefix = s_prefix;
+            for (int i = threadIdx.x; i < c; i += blockDim.x) {
+                const uint64_t key = keys[i];
+                if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t rank = s_rank, acc = 0;
+                int b = 0;
+                for (; b < 256; b++) {
+                    if (acc + hist[b] >= rank) break;
+                    acc += hist[b];
+                }
+                s_rank = rank - acc;
+                s_prefix = prefix | ((uint64_t)b << shift);
+            }
+            mask |= 0xffull << shift;
+            __syncthreads();
+        }
+        const uint64_t kth = s_prefix;  // exact k-th smallest key
+        if (threadIdx.x == 0) s_fill = 0;
+        while (p2 < k) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) sk[i] = KEY_EMPTY;
+        __syncthreads();
+        for (int i = threadIdx.x; i < c; i += blockDim.x) {
+            const uint64_t key = keys[i];
+            if (key <= kth) {
+                const uint32_t slot = atomicAdd(&s_fill, 1u);
+                if (slot < (uint32_t)p2) sk[slot] = key;
+            }
+        }
+        __syncthreads();
+    }
+    bitonic_sort_smem(sk, p2);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) out_keys[(size_t)q * k + i] = i < p2 ? sk[i] : KEY_EMPTY;
     if (threadIdx.x == 0) {
-        int over = total > (uint32_t)cap;
+        const int over = total > (uint32_t)cap;
         flags[q] = over;
-        if (over) thr[q] = sk[k - 1];  // k-th best of real distances: a valid, tighter bound
+        if (over) thr[q] = sk[k - 1];
     }
 }
 
@@ -348,7 +416,7 @@ int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const in
 
 template <int NT>
 static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileList &tl,
-                           const float *Q, ScanOut out, cudaStream_t s)
+                           const float *Q, ScanOut out, cudaStream_t s, const char *tag)
 {
     constexpr int WARPS = 8;
     int smem = 2 * TILE_ROWS * NT * 4 + 16;
@@ -356,7 +424,7 @@ static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileLis
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int64_t grid = std::min<int64_t>(tl.ntiles, (int64_t)num_sms() * 4);
     if (grid < 1) return OK;
-    ProfScope ps("scan_sparse", s, 0.0);
+    ProfScope ps(tag, s, 0.0);
     TileList t2 = tl;
     t2.bytes = ps.counter();
     scan_sparse_kernel<NT, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(X, row_id, t2, Q, out);
@@ -365,14 +433,14 @@ static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileLis
 }
 
 int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
-                       const float *Q, ScanOut out, cudaStream_t s)
+                       const float *Q, ScanOut out, cudaStream_t s, const char *tag)
 {
     if (tl.ntiles == 0) return OK;
     switch (n) {
-    case 64: return launch_sparse_t<64>(X, row_id, tl, Q, out, s);
-    case 96: return launch_sparse_t<96>(X, row_id, tl, Q, out, s);
-    case 128: return launch_sparse_t<128>(X, row_id, tl, Q, out, s);
-    case 256: return launch_sparse_t<256>(X, row_id, tl, Q, out, s);
+    case 64: return launch_sparse_t<64>(X, row_id, tl, Q, out, s, tag);
+    case 96: return launch_sparse_t<96>(X, row_id, tl, Q, out, s, tag);
+    case 128: return launch_sparse_t<128>(X, row_id, tl, Q, out, s, tag);
+    case 256: return launch_sparse_t<256>(X, row_id, tl, Q, out, s, tag);
     default: break;
     }
     set_error(ERR_USAGE, "series length " + std::to_string(n) +
@@ -384,15 +452,14 @@ int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, u
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s)
 {
     if (nq == 0) return OK;
-    int P = 1;
-    while (P < cap || P < k) P <<= 1;
-    int smem = P * 8;
-    SSB_REQUIRE(smem <= 200 * 1024, "candidate capacity too large for K-select");
-    SSB_CUDA(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    int P = SELECT_SMALL;
+    while (P < k) P <<= 1;
+    const int smem = P * 8;
+    SSB_REQUIRE(smem <= 200 * 1024, "k too large for K-select");
+    SSB_CUDA(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     {
         ProfScope ps("select", s, 0.0);
-        select_topk_kernel<<<nq, 1024, smem, s>>>(cand, cnt, cap, P, k, thr, out_keys, flags);
+        select_topk_kernel<<<nq, 1024, smem, s>>>(cand, cnt, cap, k, thr, out_keys, flags);
     }
     SSB_CHECK_LAUNCH();
     return OK;

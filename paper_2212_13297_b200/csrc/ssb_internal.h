@@ -33,7 +33,7 @@ int64_t dense_ranges(int64_t N, int nq, int k, int cap);
 int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
                       int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
 int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
-                       const float *Q, ScanOut out, cudaStream_t s);
+                       const float *Q, ScanOut out, cudaStream_t s, const char *tag = "scan_sparse");
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s);
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,

@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--queries", type=int, default=1000)
     ap.add_argument("--tau", type=int, default=10_000)
     ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--sigmas", default="0.01,0.1,1.0")
+    ap.add_argument("--ks", default="1,10")
     a = ap.parse_args()
     import torch
 
@@ -34,9 +36,9 @@ def main():
     torch.cuda.synchronize()
     print(json.dumps({"build_s": round(time.perf_counter() - t0, 3), "leaves": idx.info.num_leaves}))
     eng = ssb.QueryEngine(idx)
-    for sigma in (0.01, 0.1, 1.0):
+    for sigma in [float(v) for v in a.sigmas.split(",")]:
         Q = torch.from_numpy(G.noise_queries(X, a.queries, sigma, 1)).cuda()
-        for k in (1, 10):
+        for k in [int(v) for v in a.ks.split(",")]:
             eng.knn_device(Q, k)  # warm
             torch.cuda.synchronize()
             _lib.prof_reset()
@@ -50,7 +52,7 @@ def main():
             print(json.dumps({
                 "sigma": sigma, "k": k, "ms": round(1000 * dt, 2),
                 "cand_leaves": float(st[:, 0].mean()), "cand_series": float(st[:, 1].mean()),
-                "seed_rows": float(st[:, 2].mean()),
+                "seed_rows": float(st[:, 2].mean()), "overflowed": int(st[:, 3].sum()),
                 "kernels": {kk: [round(v[0], 3), v[1], round(v[2] / 1e9, 3)] for kk, v in prof.items()}}))
 
 
