@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 #include <cstring>
 #include <vector>
 
@@ -171,7 +172,14 @@ __global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const
 }
 
 // K-lbs: one CTA per query; per-query gap^2 table T[seg][sym] in shared memory
-// (A.4: g = max(max(lo - q, q - hi), 0), LB = (n/16) * pw64(g^2)).
+// (A.4: g = max(max(lo - q, q - hi), 0), LB = (n/16) * sum g^2).  The hot path
+// keeps the table and the sum in float32 (16 KB, one LDS.32 per lookup): the
+// float32 sum of 16 non-negative terms exceeds the exact float64 value by at
+// most ~17 * 2^-24 relatively, which the keep-bound absorbs (x (1 + 4e-6)), so
+// a row is never dropped that the exact LB_SAX would keep.  Each thread
+// evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
+constexpr int LBS_ROWS = 4;
+
 __global__ void __launch_bounds__(256)
     lbs_kernel(const float *__restrict__ qpaa, const double *__restrict__ sym_lo, const double *__restrict__ sym_hi,
                const uint4 *__restrict__ words, int n, int L, const uint32_t *__restrict__ leaf_first,
@@ -180,60 +188,63 @@ __global__ void __launch_bounds__(256)
                EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series,
                unsigned long long *__restrict__ prof_bytes)
 {
-    __shared__ double T[WORD_SEGMENTS * ALPHABET];  // 32 KB
+    __shared__ float T[WORD_SEGMENTS * ALPHABET];  // 16 KB
     const int q = blockIdx.x;
+    const double w = (double)(n / WORD_SEGMENTS);
     for (int i = threadIdx.x; i < WORD_SEGMENTS * ALPHABET; i += blockDim.x) {
         const int seg = i / ALPHABET, sym = i % ALPHABET;
         const double qv = (double)qpaa[(int64_t)q * WORD_SEGMENTS + seg];
         double g = fmax(__dsub_rn(sym_lo[sym], qv), __dsub_rn(qv, sym_hi[sym]));
         g = fmax(g, 0.0);
-        T[i] = __dmul_rn(g, g);
+        T[i] = __double2float_rn(__dmul_rn(w, __dmul_rn(g, g)));  // w folded in
     }
     __syncthreads();
     const double bound = keep_bound(thr[q], slack_abs);
-    const double w = (double)(n / WORD_SEGMENTS);
+    const float fbound = isinf(bound) ? __int_as_float(0x7f800000)
+                                      : __double2float_ru(bound * (1.0 + 4e-6));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     uint32_t my_series = 0, my_leaves = 0;
+    unsigned long long my_bytes = 0;
     for (int l = 0; l < L; l++) {
         if (!(lbe[(int64_t)q * L + l] <= bound)) continue;  // NaN-safe: prune only if provably above
         const uint32_t a = leaf_first[l], b = a + leaf_count[l];
         if (a == b) continue;
-        if (threadIdx.x == 0) my_leaves++;
-        for (uint32_t t = a / TILE_ROWS + warp; t <= (b - 1) / TILE_ROWS; t += nw) {
-            const uint32_t pos = t * TILE_ROWS + lane;
-            bool keep = false;
-            if (pos >= a && pos < b) {
-                const uint4 wv = __ldg(words + pos);
-                const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
-                double g2[16];
+        my_leaves++;
+        my_bytes += 16ull * (b - a);
+        const uint32_t t0 = a / TILE_ROWS, t1 = (b - 1) / TILE_ROWS;
+        for (uint32_t tb = t0 + (uint32_t)warp * LBS_ROWS; tb <= t1; tb += (uint32_t)nw * LBS_ROWS) {
+            uint4 wv[LBS_ROWS];
+            bool in[LBS_ROWS];
 #pragma unroll
-                for (int s = 0; s < 16; s++) {
-                    const uint32_t sym = (wd[s >> 2] >> (8 * (s & 3))) & 0xffu;
-                    g2[s] = T[s * ALPHABET + sym];
-                }
-                double r[8];
-#pragma unroll
-                for (int j = 0; j < 8; j++) r[j] = __dadd_rn(g2[j], g2[j + 8]);
-                const double sum = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-                const double lb = __dmul_rn(w, sum);
-                keep = lb <= bound;
+            for (int u = 0; u < LBS_ROWS; u++) {
+                const uint32_t pos = (tb + u) * TILE_ROWS + lane;
+                in[u] = (tb + u) <= t1 && pos >= a && pos < b;
+                wv[u] = in[u] ? __ldg(words + pos) : make_uint4(0, 0, 0, 0);
             }
-            const uint32_t mask = __ballot_sync(0xffffffffu, keep);
-            if (lane == 0 && mask) {
-                emit_entry(eo, t, (uint32_t)q, mask);
-                my_series += __popc(mask);
+            float lb[LBS_ROWS];
+#pragma unroll
+            for (int u = 0; u < LBS_ROWS; u++) {
+                const uint32_t wd[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+                float acc = 0.f;
+#pragma unroll
+                for (int sg = 0; sg < 16; sg++) acc += T[sg * ALPHABET + ((wd[sg >> 2] >> (8 * (sg & 3))) & 0xffu)];
+                lb[u] = acc;
+            }
+#pragma unroll
+            for (int u = 0; u < LBS_ROWS; u++) {
+                if (tb + u > t1) break;  // warp-uniform
+                const uint32_t mask = __ballot_sync(0xffffffffu, in[u] && lb[u] <= fbound);
+                if (lane == 0 && mask) {
+                    emit_entry(eo, tb + u, (uint32_t)q, mask);
+                    my_series += __popc(mask);
+                }
             }
         }
     }
     if (lane == 0 && my_series) atomicAdd(&cand_series[q], my_series);
-    if (threadIdx.x == 0) cand_leaves[q] = my_leaves;
-    if (threadIdx.x == 0 && prof_bytes) {
-        // words of every row of the surviving leaves + one LB_EAPCA per leaf read
-        unsigned long long b = 8ull * L;
-        for (int l = 0; l < L; l++)
-            if (lbe[(int64_t)q * L + l] <= bound) b += 16ull * leaf_count[l];
-        atomicAdd(prof_bytes, b);
+    if (threadIdx.x == 0) {
+        cand_leaves[q] = my_leaves;
+        if (prof_bytes) atomicAdd(prof_bytes, my_bytes + 8ull * L);
     }
 }
 
@@ -295,6 +306,13 @@ __global__ void restore_entries_kernel(uint2 *__restrict__ entries, int64_t E, c
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < E) entries[i].y = keep[i];
+}
+
+__global__ void entry_flags_kernel(const uint64_t *__restrict__ keys, int64_t E, const int32_t *__restrict__ qflags,
+                                   uint8_t *__restrict__ eflags)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < E) eflags[i] = qflags[keys[i] & 0x3ffffffu] ? 1 : 0;
 }
 
 __global__ void reset_flagged_kernel(uint32_t *__restrict__ cnt, const int32_t *__restrict__ flags, int B)
@@ -369,7 +387,7 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 // host: entry list -> tile list -> sparse scan -> select (with tightening)
 
 struct TileBufs {
-    DevBuf row0, umask, eptr, entries;
+    DevBuf row0, umask, eptr, entries, keys, masks;  // keys/masks: the sorted entries
     int64_t ntiles = 0;
     int64_t E = 0;
 };
@@ -382,7 +400,8 @@ static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cud
     tb.E = E;
     tb.ntiles = 0;
     if (E == 0) return OK;
-    DevBuf k2, m2, tmp, flags, slot;
+    DevBuf &k2 = tb.keys, &m2 = tb.masks;
+    DevBuf tmp, flags, slot;
     SSB_CUDA(k2.alloc(8 * (size_t)E, s));
     SSB_CUDA(m2.alloc(4 * (size_t)E, s));
     size_t tb_bytes = 0;
@@ -525,7 +544,6 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
     rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
     if (rc) return rc;
     std::vector<int32_t> hflags(B);
-    DevBuf keep;
     for (int round = 0;; round++) {
         rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                            flags.as<int32_t>(), s);
@@ -541,18 +559,39 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
             break;
         }
         SSB_REQUIRE(round < 64, "bound tightening did not converge");
-        // rescan only the overflowed queries with their tightened bounds
-        if (!keep.p) SSB_CUDA(keep.alloc(4 * (size_t)std::max<int64_t>(tb.E, 1), s));
-        active_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
-                                                                          flags.as<int32_t>(), keep.as<uint32_t>());
+        // rescan only the overflowed queries (their entries, compacted) with
+        // their tightened bounds
+        DevBuf ef, ck, cm, nsel, tmp;
+        SSB_CUDA(ef.alloc((size_t)std::max<int64_t>(tb.E, 1), s));
+        SSB_CUDA(ck.alloc(8 * (size_t)std::max<int64_t>(tb.E, 1), s));
+        SSB_CUDA(cm.alloc(4 * (size_t)std::max<int64_t>(tb.E, 1), s));
+        SSB_CUDA(nsel.alloc(8, s));
+        entry_flags_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.keys.as<uint64_t>(), tb.E,
+                                                                       flags.as<int32_t>(), ef.as<uint8_t>());
         SSB_CHECK_LAUNCH();
+        size_t tbytes = 0, t2 = 0;
+        SSB_CUDA(cub::DeviceSelect::Flagged(nullptr, tbytes, tb.keys.as<uint64_t>(), ef.as<uint8_t>(),
+                                            ck.as<uint64_t>(), nsel.as<int64_t>(), tb.E, s));
+        SSB_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, tb.masks.as<uint32_t>(), ef.as<uint8_t>(),
+                                            cm.as<uint32_t>(), nsel.as<int64_t>(), tb.E, s));
+        SSB_CUDA(tmp.alloc(std::max(tbytes, t2), s));
+        SSB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tbytes, tb.keys.as<uint64_t>(), ef.as<uint8_t>(),
+                                            ck.as<uint64_t>(), nsel.as<int64_t>(), tb.E, s));
+        SSB_CUDA(cub::DeviceSelect::Flagged(tmp.p, t2, tb.masks.as<uint32_t>(), ef.as<uint8_t>(),
+                                            cm.as<uint32_t>(), nsel.as<int64_t>(), tb.E, s));
+        note_launch(2);
+        int64_t E2 = 0;
+        SSB_CUDA(cudaMemcpyAsync(&E2, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        TileBufs tb2;
+        rc = build_tiles(ck, cm, E2, tb2, s, ix.N);
+        if (rc) return rc;
+        TileList tl2{tb2.row0.as<uint32_t>(), tb2.umask.as<uint32_t>(), tb2.eptr.as<uint32_t>(),
+                     tb2.entries.as<uint2>(), tb2.ntiles};
         reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
         SSB_CHECK_LAUNCH();
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s, "scan_retry");
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl2, Qp, so, s, "scan_retry");
         if (rc) return rc;
-        restore_entries_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.entries.as<uint2>(), tb.E,
-                                                                           keep.as<uint32_t>());
-        SSB_CHECK_LAUNCH();
     }
     return OK;
 }
