@@ -179,6 +179,7 @@ __global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const
 // a row is never dropped that the exact LB_SAX would keep.  Each thread
 // evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
 constexpr int LBS_ROWS = 4;
+constexpr int LBS_STAGE = 1024;
 
 __global__ void __launch_bounds__(256)
     lbs_kernel(const float *__restrict__ qpaa, const double *__restrict__ sym_lo, const double *__restrict__ sym_hi,
@@ -205,14 +206,40 @@ __global__ void __launch_bounds__(256)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     uint32_t my_series = 0, my_leaves = 0;
     unsigned long long my_bytes = 0;
+    // entries are staged per CTA and flushed with ONE global reservation per
+    // LBS_STAGE entries (a single hot counter would serialise millions of atomics)
+    __shared__ uint64_t st_key[LBS_STAGE];
+    __shared__ uint32_t st_mask[LBS_STAGE];
+    __shared__ uint32_t st_n, st_base;
+    if (threadIdx.x == 0) st_n = 0;
+    __syncthreads();
+    auto flush = [&]() {
+        __syncthreads();
+        const uint32_t cnt = min(st_n, (uint32_t)LBS_STAGE);
+        if (threadIdx.x == 0) st_base = cnt ? atomicAdd(eo.count, cnt) : 0u;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const uint32_t slot = st_base + i;
+            if ((int64_t)slot < eo.cap) {
+                eo.key[slot] = st_key[i];
+                eo.mask[slot] = st_mask[i];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) st_n = 0;
+        __syncthreads();
+    };
     for (int l = 0; l < L; l++) {
-        if (!(lbe[(int64_t)q * L + l] <= bound)) continue;  // NaN-safe: prune only if provably above
+        if (!(lbe[(int64_t)q * L + l] <= bound)) continue;  // NaN-safe: prune only if provably above (uniform)
         const uint32_t a = leaf_first[l], b = a + leaf_count[l];
         if (a == b) continue;
         my_leaves++;
         my_bytes += 16ull * (b - a);
         const uint32_t t0 = a / TILE_ROWS, t1 = (b - 1) / TILE_ROWS;
-        for (uint32_t tb = t0 + (uint32_t)warp * LBS_ROWS; tb <= t1; tb += (uint32_t)nw * LBS_ROWS) {
+        // the CTA sweeps the leaf in rounds of nw*LBS_ROWS tiles; flush between rounds
+        for (uint32_t base = t0; base <= t1; base += (uint32_t)nw * LBS_ROWS) {
+            if (st_n > LBS_STAGE - (uint32_t)nw * LBS_ROWS) flush();
+            const uint32_t tb = base + (uint32_t)warp * LBS_ROWS;
             uint4 wv[LBS_ROWS];
             bool in[LBS_ROWS];
 #pragma unroll
@@ -232,15 +259,18 @@ __global__ void __launch_bounds__(256)
             }
 #pragma unroll
             for (int u = 0; u < LBS_ROWS; u++) {
-                if (tb + u > t1) break;  // warp-uniform
                 const uint32_t mask = __ballot_sync(0xffffffffu, in[u] && lb[u] <= fbound);
                 if (lane == 0 && mask) {
-                    emit_entry(eo, tb + u, (uint32_t)q, mask);
+                    const uint32_t i = atomicAdd(&st_n, 1u);
+                    st_key[i] = ((uint64_t)(tb + u) << 32) | ((uint64_t)(32 - __popc(mask)) << 26) | (uint32_t)q;
+                    st_mask[i] = mask;
                     my_series += __popc(mask);
                 }
             }
+            __syncthreads();
         }
     }
+    flush();
     if (lane == 0 && my_series) atomicAdd(&cand_series[q], my_series);
     if (threadIdx.x == 0) {
         cand_leaves[q] = my_leaves;
@@ -491,31 +521,53 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
     SSB_CUDA(emask.alloc(4 * (size_t)entry_cap, s));
 
     // ---- phase A: exact scan of each query's best leaf -> bound ------------------
-    SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
+    // jobs: (leaf row chunk) x (<= 32 queries whose best leaf it is)
     EntryOut eo{ekey.as<uint64_t>(), emask.as<uint32_t>(), ecount.as<uint32_t>(), entry_cap};
-    seed_entries_kernel<<<B, 128, 0, s>>>(best.as<int32_t>(), ix.leaf_first, ix.leaf_count, B, eo, st_seed_rows);
-    SSB_CHECK_LAUNCH();
-    uint32_t E = 0;
-    SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    SSB_REQUIRE((int64_t)E <= entry_cap, "seed entry buffer overflow");
     SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     {
-        TileBufs tb;
-        rc = build_tiles(ekey, emask, E, tb, s, ix.N);
-        if (rc) return rc;
-        TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
-                    tb.ntiles};
-        ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s, "scan_seed");
+        std::vector<int32_t> hbest(B);
+        SSB_CUDA(cudaMemcpyAsync(hbest.data(), best.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        std::vector<std::vector<int32_t>> byleaf(L);
+        std::vector<uint32_t> seed_rows(B, 0);
+        for (int q = 0; q < B; q++)
+            if (hbest[q] >= 0) byleaf[hbest[q]].push_back(q);
+        std::vector<int32_t> qlist;
+        std::vector<ScanJob> jobs;
+        const uint32_t CH = 1024;  // rows per job
+        for (int l = 0; l < L; l++) {
+            if (byleaf[l].empty()) continue;
+            const TreeNode &tn = ix.nodes[ix.leaves[l]];
+            for (size_t g0 = 0; g0 < byleaf[l].size(); g0 += 32) {
+                const uint32_t qoff = (uint32_t)qlist.size();
+                const uint32_t qn = (uint32_t)std::min<size_t>(32, byleaf[l].size() - g0);
+                for (uint32_t i = 0; i < qn; i++) {
+                    qlist.push_back(byleaf[l][g0 + i]);
+                    seed_rows[byleaf[l][g0 + i]] = tn.count;
+                }
+                for (uint32_t r = tn.first; r < tn.first + tn.count; r += CH)
+                    jobs.push_back({r, std::min(tn.first + tn.count, r + CH), qoff, qn});
+            }
+        }
+        DevBuf djobs, dql;
+        SSB_CUDA(djobs.alloc(sizeof(ScanJob) * std::max<size_t>(jobs.size(), 1), s));
+        SSB_CUDA(dql.alloc(4 * std::max<size_t>(qlist.size(), 1), s));
+        SSB_CUDA(cudaMemcpyAsync(djobs.p, jobs.data(), sizeof(ScanJob) * jobs.size(), cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(dql.p, qlist.data(), 4 * qlist.size(), cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(st_seed_rows, seed_rows.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+        ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
+        rc = launch_scan_jobs(ix.X, n, ix.orig, djobs.as<ScanJob>(), (int)jobs.size(), dql.as<int32_t>(), Qp, k,
+                              so, s);
         if (rc) return rc;
         rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                            flags.as<int32_t>(), s);
         if (rc) return rc;
         thr_from_keys_kernel<<<(B + 255) / 256, 256, 0, s>>>(out_keys, B, k, thr.as<uint64_t>());
         SSB_CHECK_LAUNCH();
+        SSB_CUDA(cudaStreamSynchronize(s));  // host job vectors die here
     }
+    uint32_t E = 0;
 
     // ---- phase B: LB_EAPCA + LB_SAX filtering, exact scan of survivors ----------
     SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));

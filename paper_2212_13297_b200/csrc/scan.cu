@@ -237,6 +237,133 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---------------------------------------------------------------------------
+// job scan (layout rows): each CTA scans a contiguous row range for up to
+// 4*WARPS queries (one per 8-lane group, all groups on the same row: the
+// LDS.128 addresses are shared), keeping a per-query top-k of the range in
+// shared memory and dumping it to the query's candidate buffer.  Used for the
+// seed phase (each query's best leaf).
+
+template <int NT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    scan_jobs_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id, const ScanJob *__restrict__ jobs,
+                     const int32_t *__restrict__ qlist, const float *__restrict__ Qp, int k, ScanOut out)
+{
+    constexpr int G = WARPS * 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tiles + 2 * TILE_ROWS * NT);
+    uint64_t *lists = bars + 2;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = warp * 4 + (lane >> 3);
+    const int j = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const ScanJob job = jobs[blockIdx.x];
+    const bool active = g < (int)job.qn;
+    const int q = active ? qlist[job.qoff + g] : 0;
+
+    for (int e = tid; e < G * k; e += blockDim.x) lists[e] = KEY_EMPTY;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    float qv[NT / 8];
+    if (active) lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
+    __syncthreads();
+
+    const int64_t r0 = job.r0, r1 = job.r1;
+    const int64_t ntiles = (r1 - r0 + TILE_ROWS - 1) / TILE_ROWS;
+    auto issue = [&](int64_t t) {
+        const int64_t row = r0 + t * TILE_ROWS;
+        const int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row);
+        const unsigned bytes = (unsigned)nr * NT * 4u;
+        mbar_expect_tx(&bars[t & 1], bytes);
+        bulk_g2s(tiles + (t & 1) * TILE_ROWS * NT, X + row * NT, bytes, &bars[t & 1]);
+    };
+    if (tid == 0 && ntiles > 0) issue(0);
+    uint64_t *mylist = lists + (size_t)g * k;
+    for (int64_t t = 0; t < ntiles; t++) {
+        if (tid == 0 && t + 1 < ntiles) issue(t + 1);
+        mbar_wait(&bars[t & 1], (unsigned)((t >> 1) & 1));
+        const int64_t row0 = r0 + t * TILE_ROWS;
+        const int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row0);
+        const float *buf = tiles + (t & 1) * TILE_ROWS * NT;
+        if (active) {
+            for (int r = 0; r < nr; r += 2) {
+                float d0, d1 = 0.f;
+                const bool two = r + 1 < nr;
+                if (two)
+                    lay_ed2_x2<NT>(buf + r * NT, buf + (r + 1) * NT, qv, j, gmask, d0, d1);
+                else
+                    d0 = lay_ed2<NT>(buf + r * NT, qv, j, gmask);
+                if (j == 0) {
+                    for (int h = 0; h < (two ? 2 : 1); h++) {
+                        const uint32_t pos = (uint32_t)(row0 + r + h);
+                        const uint64_t key = make_key(h ? d1 : d0, row_id ? row_id[pos] : pos);
+                        if (key < mylist[k - 1]) {
+                            int p = k - 1;
+                            while (p > 0 && mylist[p - 1] > key) {
+                                mylist[p] = mylist[p - 1];
+                                p--;
+                            }
+                            mylist[p] = key;
+                        }
+                    }
+                }
+                __syncwarp(gmask);
+            }
+        }
+        __syncthreads();
+    }
+    if (active) {
+        const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
+        int c = 0;
+        uint32_t base = 0;
+        if (j == 0) {
+            while (c < k && mylist[c] != KEY_EMPTY && mylist[c] <= bound) c++;
+            base = c ? atomicAdd(&out.cnt[q], (uint32_t)c) : 0u;
+        }
+        c = __shfl_sync(gmask, c, lane & 24);
+        base = __shfl_sync(gmask, base, lane & 24);
+        for (int e = j; e < c; e += 8) {
+            const uint32_t slot = base + e;
+            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = mylist[e];
+        }
+    }
+}
+
+template <int NT>
+static int launch_jobs_t(const float *X, const uint32_t *row_id, const ScanJob *jobs, int njobs,
+                         const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s)
+{
+    constexpr int WARPS = 8;
+    const int smem = 2 * TILE_ROWS * NT * 4 + 16 + WARPS * 4 * k * 8;
+    SSB_REQUIRE(smem <= 227 * 1024, "k too large for the job scan");
+    SSB_CUDA(cudaFuncSetAttribute(scan_jobs_kernel<NT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ProfScope ps("scan_jobs", s, 0.0);
+    scan_jobs_kernel<NT, WARPS><<<njobs, WARPS * 32, smem, s>>>(X, row_id, jobs, qlist, Qp, k, out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+int launch_scan_jobs(const float *X, int n, const uint32_t *row_id, const ScanJob *jobs, int njobs,
+                     const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s)
+{
+    if (njobs == 0) return OK;
+    switch (n) {
+    case 64: return launch_jobs_t<64>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
+    case 96: return launch_jobs_t<96>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
+    case 128: return launch_jobs_t<128>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
+    case 256: return launch_jobs_t<256>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
+    default: break;
+    }
+    set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled scan kernel");
+    return ERR_USAGE;
+}
+
+// ---------------------------------------------------------------------------
 // K-select: per query, the k smallest (d2, id) keys of its candidate buffer.
 // Up to SELECT_SMALL candidates: bitonic sort in shared memory.  Above that:
 // an exact MSB radix select of the k-th key (8 passes of 8 bits over the

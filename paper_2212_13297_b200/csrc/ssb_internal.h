@@ -29,6 +29,14 @@ struct TileList {
     unsigned long long *bytes = nullptr;  // profiling: algorithmic bytes (nullable)
 };
 
+struct ScanJob {
+    uint32_t r0, r1;  // row range
+    uint32_t qoff;    // offset into the job query list
+    uint32_t qn;      // queries (<= 32)
+};
+int launch_scan_jobs(const float *X, int n, const uint32_t *row_id, const ScanJob *jobs, int njobs,
+                     const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s);
+
 int64_t dense_ranges(int64_t N, int nq, int k, int cap);
 int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
                       int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
