@@ -175,18 +175,10 @@ class IndexEngine:
 
 
 def merge_shards(d2, ids, k, world):
-    """All-gather every rank's top-k (NCCL) and keep the k best (d2, id) keys."""
-    import torch
-    import torch.distributed as dist
+    """One NCCL all-gather of every rank's top-k keys + the K-merge kernel."""
+    from paper_2212_13297_b200.distributed import merge_topk
 
-    B = d2.shape[0]
-    keys = (d2.contiguous().view(torch.int32).to(torch.int64) << 32) | ids.clamp_min(0)
-    keys = torch.where(ids < 0, torch.full_like(keys, torch.iinfo(torch.int64).max), keys)
-    gathered = torch.empty((world, B, k), dtype=torch.int64, device=keys.device)
-    dist.all_gather_into_tensor(gathered, keys)
-    allk = gathered.permute(1, 0, 2).reshape(B, world * k)
-    best = torch.topk(allk, k, dim=1, largest=False, sorted=True).values
-    return best
+    return merge_topk(d2, ids, k)
 
 
 # --------------------------------------------------------------------------

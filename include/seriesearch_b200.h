@@ -153,6 +153,13 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
 int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, float *out_d2,
               int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream);
 
+/* K-merge: per query, the k smallest of m (d2, id) keys -- the merge after the
+ * NCCL all-gather of per-shard top-k lists.  keys: B x m uint64
+ * device array, key = (float bits of d2 << 32) | id, UINT64_MAX = empty;
+ * ids must fit in 32 bits.  out_d2 / out_id: B x k device arrays. */
+int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2,
+                   int64_t *out_id, void *stream);
+
 /* LB_EAPCA of B queries against every leaf (out: B x num_leaves float64,
  * device) -- summarize.py:170-206 / query.py:127-135, bit-identical. */
 int ssb_index_lb_eapca(const ssb_index *index, const float *Q, int32_t B, double *out, void *stream);

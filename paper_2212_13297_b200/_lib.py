@@ -46,6 +46,7 @@ _SIGS = {
     "ssb_index_load": [P, P, P, I64, I32, I64, I64, P, I32, P, P, P],
     "ssb_index_lb_eapca": [P, P, I32, P, P],
     "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
+    "ssb_merge_topk": [P, I32, I32, I32, P, P, P],
 }
 
 M_MAX = 32

@@ -119,6 +119,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 cudaStream_t s);
 int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, float *out_d2, int64_t *out_id,
                 int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_t *out_id, cudaStream_t s);
 int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t s);
 int index_from_host(const float *rows, const uint8_t *words, const uint32_t *orig, int64_t N, int n, int64_t tau,
                     int64_t id_base, std::vector<TreeNode> nodes, const double *bp_dev, Index **out, cudaStream_t s);
@@ -343,6 +344,12 @@ int ssb_index_lb_eapca(const ssb_index *h, const float *Q, int32_t B, double *ou
 {
     SSB_REQUIRE(h, "null index");
     return index_lbe(*h->ix, Q, B, out, (cudaStream_t)stream);
+}
+
+int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2, int64_t *out_id,
+                   void *stream)
+{
+    return merge_topk(keys, B, m, k, out_d2, out_id, (cudaStream_t)stream);
 }
 
 int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const double *lower, const double *upper,

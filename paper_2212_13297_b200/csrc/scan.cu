@@ -592,6 +592,30 @@ int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, u
     return OK;
 }
 
+// per-query merge of M candidate keys (e.g. all-gathered shard top-k lists)
+__global__ void copy_counts_kernel(uint32_t *cnt, int nq, uint32_t m)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nq) cnt[i] = m;
+}
+
+int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_t *out_id, cudaStream_t s)
+{
+    SSB_REQUIRE(k >= 1 && m >= 0, "bad merge sizes");
+    if (nq == 0) return OK;
+    DevBuf cnt, thr, out, flags;
+    SSB_CUDA(cnt.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(thr.alloc(8 * (size_t)nq, s));
+    SSB_CUDA(out.alloc(8 * (size_t)nq * k, s));
+    SSB_CUDA(flags.alloc(4 * (size_t)nq, s));
+    copy_counts_kernel<<<(nq + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), nq, (uint32_t)m);
+    SSB_CHECK_LAUNCH();
+    int rc = launch_select(keys, cnt.as<uint32_t>(), std::max(m, 1), nq, k, thr.as<uint64_t>(), out.as<uint64_t>(),
+                           flags.as<int32_t>(), s);
+    if (rc) return rc;
+    return launch_keys_to_results(out.as<uint64_t>(), (int64_t)nq * k, nullptr, 0, out_d2, out_id, nullptr, s);
+}
+
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s)
 {

@@ -1,0 +1,106 @@
+"""Row-sharded multi-GPU exact k-NN.
+
+One process per GPU (torchrun, NCCL).  The dataset is split into contiguous
+original-index ranges; each rank builds its own index over its shard with
+``id_base`` = the shard's first original index (no communication in the
+build).  Queries are replicated; every rank answers them over its shard and the
+per-shard top-k (d2, id) keys are merged with ONE all-gather of B x k keys per
+rank followed by the K-merge kernel (``ssb_merge_topk``).  Ids are global and
+the order is the global (d2, id) order, so the answer equals a single-GPU
+answer over the whole dataset.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+EMPTY = np.iinfo(np.int64).max
+
+
+def shard_range(N: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous original-index range [lo, hi) of ``rank``'s shard."""
+    return rank * N // world, (rank + 1) * N // world
+
+
+def pack_keys(d2, ids):
+    """(d2 float32, ids int64) -> int64 keys (d2 bits << 32 | id); missing -> EMPTY.
+    Works on numpy arrays and torch tensors (CPU or CUDA)."""
+    try:
+        import torch
+
+        if isinstance(d2, torch.Tensor):
+            keys = (d2.contiguous().view(torch.int32).to(torch.int64) << 32) | ids.clamp_min(0)
+            return torch.where(ids < 0, torch.full_like(keys, EMPTY), keys)
+    except ImportError:  # pragma: no cover
+        pass
+    d2 = np.ascontiguousarray(d2, np.float32)
+    keys = (d2.view(np.int32).astype(np.int64) << 32) | np.maximum(ids, 0)
+    return np.where(ids < 0, EMPTY, keys)
+
+
+def unpack_keys(keys):
+    """int64 keys -> (d2 float32, ids int64) with (inf, -1) for EMPTY (numpy)."""
+    keys = np.asarray(keys)
+    empty = keys == EMPTY
+    d2 = (keys >> 32).astype(np.int32).view(np.float32)
+    ids = (keys & 0xFFFFFFFF).astype(np.int64)
+    d2 = np.where(empty, np.float32(np.inf), d2)
+    ids = np.where(empty, -1, ids)
+    return d2, ids
+
+
+def gather_keys(keys, group=None):
+    """All-gather every rank's (B, k) key block -> (B, world*k), rank-major."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if keys.is_cuda:
+        out = torch.empty((world,) + tuple(keys.shape), dtype=keys.dtype, device=keys.device)
+        dist.all_gather_into_tensor(out, keys.contiguous(), group=group)
+    else:  # gloo (CPU tests)
+        parts = [torch.empty_like(keys) for _ in range(world)]
+        dist.all_gather(parts, keys.contiguous(), group=group)
+        out = torch.stack(parts)
+    return out.permute(1, 0, 2).reshape(keys.shape[0], world * keys.shape[1]).contiguous()
+
+
+def merge_device(all_keys, k: int):
+    """K-merge on the device: the k best of each row of (B, M) keys."""
+    import torch
+
+    from . import _lib
+    from ._device import ptr, stream_handle
+
+    B, M = all_keys.shape
+    d2 = torch.empty((B, k), dtype=torch.float32, device=all_keys.device)
+    ids = torch.empty((B, k), dtype=torch.int64, device=all_keys.device)
+    _lib.call("ssb_merge_topk", ptr(all_keys), B, M, k, ptr(d2), ptr(ids), stream_handle())
+    return d2, ids
+
+
+def merge_topk(d2, ids, k: int, group=None, merge_fn=None):
+    """Global top-k from every rank's shard top-k: one all-gather + K-merge.
+
+    ``merge_fn(all_keys, k) -> (d2, ids)`` defaults to the device kernel; the
+    CPU multi-process tests pass a host merge (the gloo backend has no GPU).
+    """
+    keys = pack_keys(d2, ids)
+    all_keys = gather_keys(keys, group)
+    return (merge_fn or merge_device)(all_keys, k)
+
+
+class ShardedIndex:
+    """This rank's shard of a row-sharded index (build + query + merge)."""
+
+    def __init__(self, data_shard, settings, id_base: int, **build_kw):
+        from .build import build_index_array
+        from .query import QueryEngine
+
+        self.id_base = id_base
+        self.index = build_index_array(data_shard, settings, id_base=id_base, **build_kw)
+        self.engine = QueryEngine(self.index)
+
+    def knn(self, Q, k: int, group=None):
+        d2, ids, _ = self.engine.knn_device(Q, k)
+        return merge_topk(d2, ids, k, group)

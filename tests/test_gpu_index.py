@@ -296,3 +296,31 @@ def test_api_surface_and_errors(ssb, small, tmp_path):
         ssb.build_index(path, s, num_threads=1)
     b = ssb.build_index(path, s, num_threads=2)
     assert b.info.num_leaves == idx.info.num_leaves
+
+
+def test_sharded_forest_merge_on_device(ssb, oracle):
+    """Row shards as separate device indexes + the K-merge kernel: the answer
+    equals one global scan (multi-GPU data path, emulated on one GPU without
+    any rank waiting on another)."""
+    import torch
+
+    from paper_2212_13297_b200.distributed import merge_device, pack_keys, shard_range
+
+    X = random_walks(9000, 64, 31)
+    X[8500] = X[7]
+    Q = np.concatenate([noisy(X, 10, 0.3, 32), X[[7]]])
+    k = 10
+    world = 3
+    parts = []
+    for r in range(world):
+        lo, hi = shard_range(len(X), r, world)
+        s = ssb.IndexSettings(series_length=64, dataset_size=hi - lo, leaf_threshold=200)
+        idx = ssb.build_index_array(X[lo:hi], s, id_base=lo)
+        d2, ids, _ = ssb.QueryEngine(idx).knn_device(Q, k)
+        parts.append(pack_keys(d2, ids))
+    all_keys = torch.stack(parts).permute(1, 0, 2).reshape(len(Q), world * k).contiguous()
+    gd2, gids = merge_device(all_keys, k)
+    od2, oid = oracle.knn_scan(X, Q, k)
+    assert np.array_equal(gids.cpu().numpy(), oid)
+    assert np.array_equal(bits(gd2.cpu().numpy()), bits(od2))
+    assert list(gids.cpu().numpy()[-1][:2]) == [7, 8500]
