@@ -150,8 +150,17 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
  * position); stats_host (nullable): B x 4 uint32 host array receiving
  * (candidate leaves, candidate series, seed-leaf rows, 0) per query.
  * Synchronizes `stream`. */
-int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, float *out_d2,
-              int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream);
+typedef struct {
+    /* query.py:45 QueryConfig.eapca_th: a query whose seed bound keeps more than
+     * (1 - eapca_th) of the leaves takes the dense "scan" path (K-tc tensor-core
+     * filter + exact rescoring) instead of LB_SAX + sparse exact scan
+     * (query.py:321-325).  Answers do not depend on it. */
+    float eapca_th;
+    int32_t route; /* 0 auto (eapca_th rule), 1 LB_SAX path only, 2 tensor-core path only */
+} ssb_query_cfg;
+
+int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, const ssb_query_cfg *cfg,
+              float *out_d2, int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream);
 
 /* K-merge: per query, the k smallest of m (d2, id) keys -- the merge after the
  * NCCL all-gather of per-shard top-k lists.  keys: B x m uint64
@@ -159,6 +168,11 @@ int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, floa
  * ids must fit in 32 bits.  out_d2 / out_id: B x k device arrays. */
 int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2,
                    int64_t *out_id, void *stream);
+
+/* K-tc parity hook: S (B x N float32, device) = bf16(Q) . bf16(X)^T computed by
+ * the tcgen05 kernel of the tensor-core filter (rows row-major, n <= 256). */
+int ssb_tc_dot_debug(const float *Q, int32_t B, const float *X, int64_t N, int32_t n, float *S,
+                     void *stream);
 
 /* LB_EAPCA of B queries against every leaf (out: B x num_leaves float64,
  * device) -- summarize.py:170-206 / query.py:127-135, bit-identical. */

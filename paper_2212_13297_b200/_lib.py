@@ -41,7 +41,8 @@ _SIGS = {
     "ssb_index_info": [P, P],
     "ssb_index_node": [P, I32, P],
     "ssb_index_arrays": [P, P, P, P, P],
-    "ssb_query": [P, P, I32, I32, P, P, P, P, P],
+    "ssb_query": [P, P, I32, I32, P, P, P, P, P, P],
+    "ssb_tc_dot_debug": [P, I32, P, I64, I32, P, P],
     "ssb_index_download": [P, P, P, P],
     "ssb_index_load": [P, P, P, I64, I32, I64, I64, P, I32, P, P, P],
     "ssb_index_lb_eapca": [P, P, I32, P, P],
@@ -55,6 +56,10 @@ M_MAX = 32
 class BuildCfg(ctypes.Structure):
     _fields_ = [("leaf_threshold", ctypes.c_int64), ("initial_segments", ctypes.c_int32),
                 ("max_segments", ctypes.c_int32), ("id_base", ctypes.c_int64)]
+
+
+class QueryCfg(ctypes.Structure):
+    _fields_ = [("eapca_th", ctypes.c_float), ("route", ctypes.c_int32)]
 
 
 class IndexInfo(ctypes.Structure):

@@ -40,7 +40,7 @@ namespace ssb {
 
 Index::~Index()
 {
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env};
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -537,6 +537,16 @@ struct BuildCfg {
 
 int finalize_tree(Index &ix, cudaStream_t s);
 
+// BF16 copy + row norms for the tensor-core filter (skipped when n is unsupported)
+static int make_tc_operands(Index &ix, cudaStream_t s)
+{
+    if (ix.n % 8 != 0 || ix.n > 256) return OK;
+    SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
+    SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
+    SSB_CUDA(cudaMalloc(&ix.xnorm, (size_t)ix.N * 4));
+    return launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
+}
+
 int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg,
                 Index **out, cudaStream_t s)
 {
@@ -876,6 +886,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
     RC(launch_words(X, N, n, ix->bp, ix->words, nullptr, s, perm));
+    RC(make_tc_operands(*ix, s));
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
@@ -974,6 +985,7 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
     if (words) SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
+    RC(make_tc_operands(*ix, s));
     DevBuf amax;
     SSB_CUDA(amax.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));

@@ -117,8 +117,9 @@ struct BuildCfg {
 };
 int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg, Index **out,
                 cudaStream_t s);
-int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, float *out_d2, int64_t *out_id,
-                int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
+                int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float *S, cudaStream_t s);
 int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_t *out_id, cudaStream_t s);
 int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t s);
 int index_from_host(const float *rows, const uint8_t *words, const uint32_t *orig, int64_t N, int n, int64_t tau,
@@ -332,18 +333,30 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
     return OK;
 }
 
-int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, float *out_d2, int64_t *out_id,
-              int64_t *out_pos, uint32_t *stats_host, void *stream)
+int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, const ssb_query_cfg *cfg, float *out_d2,
+              int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream)
 {
     SSB_REQUIRE(h, "null index");
     const Index &ix = *h->ix;
-    return index_query(ix, Q, B, k, ix.id_base, out_d2, out_id, out_pos, stats_host, (cudaStream_t)stream);
+    QueryCfg qc;
+    if (cfg) {
+        SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
+        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 2, "route must be 0 (auto), 1 (tree) or 2 (tensor core)");
+        qc.eapca_th = cfg->eapca_th;
+        qc.route = cfg->route;
+    }
+    return index_query(ix, qc, Q, B, k, ix.id_base, out_d2, out_id, out_pos, stats_host, (cudaStream_t)stream);
 }
 
 int ssb_index_lb_eapca(const ssb_index *h, const float *Q, int32_t B, double *out, void *stream)
 {
     SSB_REQUIRE(h, "null index");
     return index_lbe(*h->ix, Q, B, out, (cudaStream_t)stream);
+}
+
+int ssb_tc_dot_debug(const float *Q, int32_t B, const float *X, int64_t N, int32_t n, float *S, void *stream)
+{
+    return tc_dot_debug(Q, B, X, N, n, S, (cudaStream_t)stream);
 }
 
 int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2, int64_t *out_id,

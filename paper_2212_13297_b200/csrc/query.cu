@@ -187,10 +187,10 @@ __global__ void __launch_bounds__(256)
                const uint32_t *__restrict__ leaf_count, const double *__restrict__ lbe,
                const uint64_t *__restrict__ thr, double slack_abs,
                EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series,
-               unsigned long long *__restrict__ prof_bytes)
+               unsigned long long *__restrict__ prof_bytes, const int32_t *__restrict__ qlist)
 {
     __shared__ float T[WORD_SEGMENTS * ALPHABET];  // 16 KB
-    const int q = blockIdx.x;
+    const int q = qlist ? qlist[blockIdx.x] : blockIdx.x;
     const double w = (double)(n / WORD_SEGMENTS);
     for (int i = threadIdx.x; i < WORD_SEGMENTS * ALPHABET; i += blockDim.x) {
         const int seg = i / ALPHABET, sym = i % ALPHABET;
@@ -416,6 +416,54 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 // ---------------------------------------------------------------------------
 // host: entry list -> tile list -> sparse scan -> select (with tightening)
 
+// routing (query.py:321-325): leaves each query keeps under its seed bound
+__global__ void route_kernel(const double *__restrict__ lbe, int L, const uint64_t *__restrict__ thr, double slack_abs,
+                             const uint32_t *__restrict__ leaf_count, float eapca_th, int mode,
+                             uint32_t *__restrict__ cand_leaves, int32_t *__restrict__ use_tc)
+{
+    const int q = blockIdx.x;
+    const double bound = keep_bound(thr[q], slack_abs);
+    uint32_t c = 0;
+    for (int l = threadIdx.x; l < L; l += blockDim.x) c += (leaf_count[l] && lbe[(int64_t)q * L + l] <= bound) ? 1u : 0u;
+    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    __shared__ uint32_t part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+        cand_leaves[q] = t;
+        const double eapca_pr = 1.0 - (double)t / (double)(L > 0 ? L : 1);
+        use_tc[q] = mode == 2 ? 1 : (mode == 1 ? 0 : (eapca_pr < (double)eapca_th ? 1 : 0));
+    }
+}
+
+__global__ void seed_bound_kernel(const uint64_t *__restrict__ thr, const int32_t *__restrict__ qlist, int nq,
+                                  unsigned int *__restrict__ gbound)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    const uint64_t key = thr[qlist[i]];
+    gbound[i] = key == KEY_EMPTY ? 0x7f800000u : (uint32_t)(key >> 32);  // d2 bits; +inf if none
+}
+
+__global__ void tc_count_kernel(const uint2 *__restrict__ cand, int64_t nc, const int32_t *__restrict__ qlist,
+                                uint32_t *__restrict__ cand_series)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nc) atomicAdd(&cand_series[qlist[cand[i].x]], 1u);
+}
+
+__global__ void tc_filter_flagged_kernel(const uint2 *__restrict__ cand, int64_t nc, const int32_t *__restrict__ qlist,
+                                         const int32_t *__restrict__ flags, uint2 *__restrict__ out,
+                                         unsigned int *__restrict__ nout)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nc) return;
+    const uint2 c = cand[i];
+    if (flags[qlist[c.x]]) out[atomicAdd(nout, 1u)] = c;
+}
+
 struct TileBufs {
     DevBuf row0, umask, eptr, entries, keys, masks;  // keys/masks: the sorted entries
     int64_t ntiles = 0;
@@ -468,7 +516,8 @@ static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cud
 }
 
 // one batch of queries (Bq <= cap-sized batch)
-static int query_batch(const Index &ix, const float *Q, int B, int k, double slack_abs, uint64_t *out_keys,
+static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, double slack_abs,
+                       uint64_t *out_keys,
                        uint32_t *st_cand_leaves, uint32_t *st_cand_series, uint32_t *st_seed_rows,
                        int32_t *st_rounds, uint32_t *st_over, int64_t entry_cap, cudaStream_t s)
 {
@@ -569,32 +618,101 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
     }
     uint32_t E = 0;
 
-    // ---- phase B: LB_EAPCA + LB_SAX filtering, exact scan of survivors ----------
-    SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
-    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
-    {
-        ProfScope ps("lbs", s, 0.0);
-        lbs_kernel<<<B, 256, 0, s>>>(qpaa.as<float>(), symlo.as<double>(), symhi.as<double>(),
-                                     reinterpret_cast<const uint4 *>(ix.words), n, L, ix.leaf_first, ix.leaf_count,
-                                     lbe.as<double>(), thr.as<uint64_t>(), slack_abs, eo, st_cand_leaves,
-                                     st_cand_series, ps.counter());
-    }
+    // ---- routing: the reference's eapca_th rule (query.py:321-325) -------------
+    // a query whose seed bound keeps most leaves ("scan" in the reference) goes to
+    // the tensor-core filter; the others to LB_SAX + sparse exact scan.
+    DevBuf use_tc;
+    SSB_CUDA(use_tc.alloc(4 * (size_t)B, s));
+    route_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, thr.as<uint64_t>(), slack_abs, ix.leaf_count, qc.eapca_th,
+                                   (ix.Xb && qc.route != 1) ? qc.route : 1, st_cand_leaves, use_tc.as<int32_t>());
     SSB_CHECK_LAUNCH();
-    SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> h_tc(B);
+    SSB_CUDA(cudaMemcpyAsync(h_tc.data(), use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
-    if ((int64_t)E > entry_cap) {
-        set_error(ERR_USAGE, "candidate entry buffer overflow");
-        return -1;  // caller splits the batch
-    }
-    TileBufs tb;
-    rc = build_tiles(ekey, emask, E, tb, s, ix.N);
-    if (rc) return rc;
-    TileList tl{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
-                tb.ntiles};
+    std::vector<int32_t> qtree, qtc;
+    for (int q = 0; q < B; q++) (h_tc[q] ? qtc : qtree).push_back(q);
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
     ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-    rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
-    if (rc) return rc;
+
+    // ---- tensor-core path ---------------------------------------------------------
+    DevBuf d_qtc, tc_cand, tc_n;
+    int64_t tc_nc = 0;
+    if (!qtc.empty()) {
+        const int nq = (int)qtc.size();
+        const int nq_pad = (nq + 127) / 128 * 128;
+        const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)nq * 8192);
+        DevBuf qb, qn2, qnrm, gb;
+        SSB_CUDA(d_qtc.alloc(4 * (size_t)nq, s));
+        SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
+        SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
+        SSB_CUDA(qnrm.alloc(4 * (size_t)nq_pad, s));
+        SSB_CUDA(gb.alloc(4 * (size_t)nq, s));
+        SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
+        SSB_CUDA(tc_n.alloc(4, s));
+        SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
+        SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 4, s));
+        rc = launch_to_bf16_norms(Q, d_qtc.as<int32_t>(), nq, n, false, qb.p, qn2.as<float>(), qnrm.as<float>(), s);
+        if (rc) return rc;
+        seed_bound_kernel<<<(nq + 255) / 256, 256, 0, s>>>(thr.as<uint64_t>(), d_qtc.as<int32_t>(), nq,
+                                                          gb.as<unsigned int>());
+        SSB_CHECK_LAUNCH();
+        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), nq, ix.Xb, ix.xn2, ix.xnorm, ix.N, n, k,
+                              gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_n.as<unsigned int>(), tc_cap, nullptr,
+                              s);
+        if (rc) return rc;
+        uint32_t hn = 0;
+        SSB_CUDA(cudaMemcpyAsync(&hn, tc_n.p, 4, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        if ((int64_t)hn > tc_cap) {  // too many candidates: answer these queries on the tree path
+            for (int q : qtc) qtree.push_back(q);
+            std::sort(qtree.begin(), qtree.end());
+            qtc.clear();
+        } else {
+            tc_nc = hn;
+            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_nc, so, s);
+            if (rc) return rc;
+            if (tc_nc) {
+                tc_count_kernel<<<(unsigned)((tc_nc + 255) / 256), 256, 0, s>>>(tc_cand.as<uint2>(), tc_nc,
+                                                                              d_qtc.as<int32_t>(), st_cand_series);
+                SSB_CHECK_LAUNCH();
+            }
+        }
+    }
+
+    // ---- tree path: LB_SAX filtering, exact scan of survivors --------------------
+    TileBufs tb;
+    TileList tl{nullptr, nullptr, nullptr, nullptr, 0};
+    E = 0;
+    if (!qtree.empty()) {
+        DevBuf d_qt;
+        SSB_CUDA(d_qt.alloc(4 * qtree.size(), s));
+        SSB_CUDA(cudaMemcpyAsync(d_qt.p, qtree.data(), 4 * qtree.size(), cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
+        {
+            ProfScope ps("lbs", s, 0.0);
+            lbs_kernel<<<(unsigned)qtree.size(), 256, 0, s>>>(
+                qpaa.as<float>(), symlo.as<double>(), symhi.as<double>(), reinterpret_cast<const uint4 *>(ix.words), n,
+                L, ix.leaf_first, ix.leaf_count, lbe.as<double>(), thr.as<uint64_t>(), slack_abs, eo, st_cand_leaves,
+                st_cand_series, ps.counter(), d_qt.as<int32_t>());
+        }
+        SSB_CHECK_LAUNCH();
+        SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        if ((int64_t)E > entry_cap) {
+            set_error(ERR_USAGE, "candidate entry buffer overflow");
+            return -1;  // caller splits the batch
+        }
+        rc = build_tiles(ekey, emask, E, tb, s, ix.N);
+        if (rc) return rc;
+        tl = TileList{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
+                      tb.ntiles};
+        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
+        if (rc) return rc;
+    }
+
+    // ---- select; overflowed queries get a tighter bound and are rescanned ---------
     std::vector<int32_t> hflags(B);
     for (int round = 0;; round++) {
         rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
@@ -611,8 +729,27 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
             break;
         }
         SSB_REQUIRE(round < 64, "bound tightening did not converge");
-        // rescan only the overflowed queries (their entries, compacted) with
-        // their tightened bounds
+        reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
+        SSB_CHECK_LAUNCH();
+        // tensor-core queries: rescore their candidates again under the tighter bound
+        if (tc_nc) {
+            DevBuf sub, nsub;
+            SSB_CUDA(sub.alloc(8 * (size_t)tc_nc, s));
+            SSB_CUDA(nsub.alloc(4, s));
+            SSB_CUDA(cudaMemsetAsync(nsub.p, 0, 4, s));
+            tc_filter_flagged_kernel<<<(unsigned)((tc_nc + 255) / 256), 256, 0, s>>>(
+                tc_cand.as<uint2>(), tc_nc, d_qtc.as<int32_t>(), flags.as<int32_t>(), sub.as<uint2>(),
+                nsub.as<unsigned int>());
+            SSB_CHECK_LAUNCH();
+            uint32_t ns = 0;
+            SSB_CUDA(cudaMemcpyAsync(&ns, nsub.p, 4, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), ns, so, s);
+            if (rc) return rc;
+            SSB_CUDA(cudaStreamSynchronize(s));
+        }
+        if (tb.E == 0) continue;
+        // tree queries: rescan only the overflowed queries' (compacted) entries
         DevBuf ef, ck, cm, nsel, tmp;
         SSB_CUDA(ef.alloc((size_t)std::max<int64_t>(tb.E, 1), s));
         SSB_CUDA(ck.alloc(8 * (size_t)std::max<int64_t>(tb.E, 1), s));
@@ -640,16 +777,15 @@ static int query_batch(const Index &ix, const float *Q, int B, int k, double sla
         if (rc) return rc;
         TileList tl2{tb2.row0.as<uint32_t>(), tb2.umask.as<uint32_t>(), tb2.eptr.as<uint32_t>(),
                      tb2.entries.as<uint2>(), tb2.ntiles};
-        reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
-        SSB_CHECK_LAUNCH();
         rc = launch_scan_sparse(ix.X, n, ix.orig, tl2, Qp, so, s, "scan_retry");
         if (rc) return rc;
+        SSB_CUDA(cudaStreamSynchronize(s));
     }
     return OK;
 }
 
-int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, float *out_d2, int64_t *out_id,
-                int64_t *out_pos,
+int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
+                int64_t *out_id, int64_t *out_pos,
                 uint32_t *stats_host /* B x 4: cand_leaves, cand_series, seed_rows, rounds */, cudaStream_t s)
 {
     SSB_REQUIRE(k >= 1, "k must be at least 1");
@@ -688,7 +824,7 @@ int index_query(const Index &ix, const float *Q, int B, int k, int64_t id_base, 
         const int nb = std::min(bq, B - q0);
         const int64_t ecap = std::min<int64_t>((int64_t)nb * per_query_worst, budget);
         int32_t r = 0;
-        int rc = query_batch(ix, Q + (int64_t)q0 * n, nb, k, slack_abs, keys.as<uint64_t>() + (int64_t)q0 * k,
+        int rc = query_batch(ix, qc, Q + (int64_t)q0 * n, nb, k, slack_abs, keys.as<uint64_t>() + (int64_t)q0 * k,
                              stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0, &r,
                              sto.as<uint32_t>() + q0, ecap, s);
         if (rc == -1) {  // entry overflow: halve the batch and retry

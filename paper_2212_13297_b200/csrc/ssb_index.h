@@ -47,9 +47,26 @@ struct Index {
     int32_t *leaf_ep = nullptr;  // L x M_MAX
     float *leaf_env = nullptr;   // L x M_MAX x 4
     float max_abs = 0.f;         // max |x| over the data (LB safety slack)
+    // tensor-core filter operands: BF16 copy (row-major, logical element order,
+    // leaf order) and exact squared norms / norms (rounded up) of every row
+    void *Xb = nullptr;
+    float *xn2 = nullptr, *xnorm = nullptr;
     double build_ms = 0.0;
     int32_t levels = 0;
     ~Index();
 };
+
+struct QueryCfg {
+    float eapca_th = 0.25f;  // query.py:45 default; < eapca_th -> tensor-core "scan" path
+    int route = 0;           // 0 auto, 1 tree only, 2 tensor-core for every query
+};
+
+int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
+                     const float *xn2, const float *xnorm, int64_t N, int n, int k, unsigned int *gbound,
+                     uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s);
+int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
+                         float *n2, float *nrm, cudaStream_t s);
+int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
+                   const uint2 *cand, int64_t nc, ScanOut out, cudaStream_t s);
 
 }  // namespace ssb

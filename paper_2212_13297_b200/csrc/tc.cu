@@ -1,0 +1,493 @@
+// tc.cu -- K-tc: tensor-core (tcgen05 / TMEM / TMA) dense filter for exact k-NN.
+//
+// For a block of queries Q and the index rows X, the squared distance is
+// ||q||^2 + ||x||^2 - 2 q.x.  q.x is computed by tcgen05.mma (kind::f16, BF16
+// operands, FP32 accumulation in TMEM) on BF16 copies of Q and X staged by TMA
+// (SWIZZLE_128B, K-major).  With RN-to-bf16 inputs the dot-product error is
+// at most c*||q||*||x||, c = 2^-8 + 2^-15 (input rounding 2*2^-9 plus fp32
+// accumulation of <= 256 exact products), so every (query, row) pair gets a
+// rigorous interval [LB, UB] around its real squared distance.  The epilogue
+// (4 warps, one query per thread = one TMEM lane) keeps, per query, the k
+// smallest UB seen (a valid bound on the k-th distance: k real rows lie
+// below it), shares it across CTAs with an atomicMin, and emits every row
+// whose LB does not exceed the current bound as a candidate.  Candidates are
+// then rescored with the exact float32 pairwise distance (scan.cu arithmetic),
+// so answers stay bit-identical to the oracle; the tensor cores only decide
+// which rows need the exact arithmetic.
+//
+// This is the "scan" fallback of the reference's adaptive query
+// (query.py:321-334: when envelope pruning is weak the reference scans the
+// candidate leaves sequentially): queries whose LB_EAPCA keeps most leaves
+// are answered here instead of by K-lbs + sparse K-scan.
+//
+// Warp roles (6 warps): w0 TMA producer, w1 MMA issuer (+ TMEM allocation),
+// w2..w5 epilogue.  Query block: 128 queries (M=128), row tile: 128 rows
+// (N=128), K = n padded to a multiple of 64 (one 128-byte swizzle atom per
+// 64 BF16 columns).  A (queries) stays resident; B tiles are double-buffered;
+// two TMEM accumulators (2 x 128 columns) overlap MMA and epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "layout.cuh"
+#include "ssb_common.cuh"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+constexpr int TC_BM = 128;   // queries per block (MMA M)
+constexpr int TC_BN = 128;   // rows per tile (MMA N)
+constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
+constexpr int TC_THREADS = 192;
+constexpr int TC_KTOP = 32;  // in-register top-k of upper bounds (k <= 32 tightens)
+
+// tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
+// N = 128 (>>3 = 16 at bit 17), M = 128 (>>4 = 8 at bit 24)
+constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr)
+{
+    // K-major SWIZZLE_128B canonical layout: 8-row groups 1024 B apart (SBO),
+    // LBO unused (1), version 1 (sm100), layout type 2 (128B swizzle)
+    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int x, int y, uint64_t *bar)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(d),
+        "l"(map), "r"(b), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a) : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcParams {
+    int n;                 // series length (K, zero-padded to KB*64 by TMA)
+    int KB;                // 64-column chunks
+    int64_t N;             // rows
+    int nq;                // queries in this launch (<= QB*128)
+    int QB;                // query blocks
+    int64_t tiles;         // ceil(N / 128)
+    int64_t tiles_per_cta; // contiguous tile chunk per CTA
+    int ctas_per_qb;
+    const float *qn2, *qnorm;  // per query (launch-local index)
+    const float *xn2, *xnorm;  // per row
+    unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
+    int k;
+    float c_rel;               // dot-product error coefficient
+    uint2 *cand;               // (query, row) candidates
+    unsigned int *cand_n;
+    int64_t cand_cap;
+    float *dump;               // debug: full S matrix (nq x N) when non-null
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_filter_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle atoms
+    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int KB = p.KB;
+    const uint32_t chunk_bytes = TC_BM * 128;  // 128 rows x 64 bf16
+    unsigned char *sA = base;
+    unsigned char *sB0 = base + KB * chunk_bytes;
+    unsigned char *sB1 = sB0 + KB * chunk_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB1 + KB * chunk_bytes);
+    uint64_t *a_full = bars + 0;
+    uint64_t *b_full = bars + 1;   // [2]
+    uint64_t *b_empty = bars + 3;  // [2]
+    uint64_t *t_full = bars + 5;   // [2]
+    uint64_t *t_empty = bars + 7;  // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 9);
+    float *s_xn2 = reinterpret_cast<float *>(bars + 10);  // [2][128]
+    float *s_xnorm = s_xn2 + 2 * TC_BN;                    // [2][128]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qb = blockIdx.x % p.QB;
+    const int chunk = blockIdx.x / p.QB;
+    const int64_t t_begin = (int64_t)chunk * p.tiles_per_cta;
+    const int64_t t_end = min(p.tiles, t_begin + p.tiles_per_cta);
+    const int64_t ntile = t_end > t_begin ? t_end - t_begin : 0;
+
+    if (threadIdx.x == 0) {
+        mbar_init(a_full, 1);
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);
+            mbar_init(&t_full[i], 1);
+            mbar_init(&t_empty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {  // TMEM: 2 accumulators x 128 fp32 columns
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(tmem_slot);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(dst));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0 && ntile > 0) {
+            mbar_expect_tx(a_full, KB * chunk_bytes);
+            for (int kb = 0; kb < KB; kb++) tma_load_2d(sA + kb * chunk_bytes, &mapA, kb * 64, qb * TC_BM, a_full);
+            for (int64_t t = 0; t < ntile; t++) {
+                const int s = (int)(t & 1);
+                if (t >= 2) mbar_wait(&b_empty[s], (unsigned)(((t >> 1) - 1) & 1));
+                unsigned char *sB = s ? sB1 : sB0;
+                mbar_expect_tx(&b_full[s], KB * chunk_bytes);
+                const int row0 = (int)((t_begin + t) * TC_BN);
+                for (int kb = 0; kb < KB; kb++) tma_load_2d(sB + kb * chunk_bytes, &mapB, kb * 64, row0, &b_full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0 && ntile > 0) {
+            mbar_wait(a_full, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t a_addr = (uint32_t)__cvta_generic_to_shared(sA);
+            for (int64_t t = 0; t < ntile; t++) {
+                const int s = (int)(t & 1);
+                mbar_wait(&b_full[s], (unsigned)((t >> 1) & 1));
+                if (t >= 2) mbar_wait(&t_empty[s], (unsigned)(((t >> 1) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t b_addr = (uint32_t)__cvta_generic_to_shared(s ? sB1 : sB0);
+                const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
+                for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ks++) {
+                        const uint32_t off = kb * chunk_bytes + ks * 32;
+                        umma_bf16(tmem_d, umma_desc_sw128(a_addr + off), umma_desc_sw128(b_addr + off),
+                                  (kb | ks) ? 1u : 0u);
+                    }
+                umma_commit(&b_empty[s]);
+                umma_commit(&t_full[s]);
+            }
+        }
+    } else {
+        // ---------------- epilogue: one query per thread ----------------
+        const int et = threadIdx.x - 64;           // 0..127
+        const int lane_grp = warp & 3;             // TMEM lanes [32*lane_grp, +32)
+        const int m = lane_grp * 32 + lane;        // query row within the block
+        const int ql = qb * TC_BM + m;             // launch-local query index
+        const bool qvalid = ql < p.nq;
+        const float qn2 = qvalid ? p.qn2[ql] : 0.f;
+        const float qnm = qvalid ? p.qnorm[ql] : 0.f;
+        float top[TC_KTOP];
+#pragma unroll
+        for (int i = 0; i < TC_KTOP; i++) top[i] = __int_as_float(0x7f800000);
+        const bool tighten = p.k <= TC_KTOP;
+        float kth = __int_as_float(0x7f800000);
+        unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
+        for (int64_t t = 0; t < ntile; t++) {
+            const int s = (int)(t & 1);
+            const int64_t row0 = (t_begin + t) * TC_BN;
+            // row norms of this tile (one row per epilogue thread)
+            {
+                const int64_t r = row0 + et;
+                s_xn2[s * TC_BN + et] = r < p.N ? p.xn2[r] : 0.f;
+                s_xnorm[s * TC_BN + et] = r < p.N ? p.xnorm[r] : 0.f;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float bound = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : 0.f;
+            bound = fminf(bound, kth);
+            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN);
+            for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int c = c0 + i;
+                    const int64_t r = row0 + c;
+                    const float sdot = __uint_as_float(v[i]);
+                    if (p.dump) {
+                        if (qvalid && r < p.N) p.dump[(int64_t)ql * p.N + r] = sdot;
+                        continue;
+                    }
+                    const float xn2 = s_xn2[s * TC_BN + c];
+                    const float approx = (qn2 + xn2) - 2.f * sdot;
+                    const float marg = 2.f * p.c_rel * qnm * s_xnorm[s * TC_BN + c] + 1.0e-6f * (qn2 + xn2);
+                    const float lb = (approx - marg) * (1.f - 4e-6f);
+                    const bool ok = qvalid && r < p.N;
+                    bool emit = ok && lb <= bound;
+                    if (ok && tighten) {
+                        const float ub = (approx + marg) * (1.f + 4e-6f);
+                        if (ub < kth) {
+                            float x = ub;
+#pragma unroll
+                            for (int j = 0; j < TC_KTOP; j++) {
+                                const float lo = fminf(top[j], x);
+                                x = fmaxf(top[j], x);
+                                top[j] = lo;
+                            }
+#pragma unroll
+                            for (int j = 0; j < TC_KTOP; j++)
+                                if (j == p.k - 1) kth = top[j];
+                            bound = fminf(bound, kth);
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, emit);
+                    if (bal) {
+                        unsigned base_slot = 0;
+                        if (lane == 0) base_slot = atomicAdd(p.cand_n, (unsigned)__popc(bal));
+                        base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+                        if (emit) {
+                            const unsigned slot = base_slot + __popc(bal & ((1u << lane) - 1u));
+                            if ((int64_t)slot < p.cand_cap) p.cand[slot] = make_uint2((unsigned)ql, (unsigned)r);
+                        }
+                    }
+                }
+            }
+            // publish this thread's bound for the other CTAs of the query block
+            if (qvalid && tighten && kth < __uint_as_float(*(volatile unsigned int *)gb))
+                atomicMin(gb, __float_as_uint(kth));
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&t_empty[s]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// helpers: bf16 copies with exact norms, and the tensor maps
+
+__global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
+                                     int n, int layout, __nv_bfloat16 *__restrict__ dst, float *__restrict__ n2,
+                                     float *__restrict__ nrm)
+{
+    // one warp per row; src rows may be in the lane-transposed layout
+    const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    if (r >= R) return;
+    const int lane = threadIdx.x & 31;
+    const float *s = src + (int64_t)(rows ? rows[r] : r) * n;
+    double acc = 0.0;
+    for (int e = lane; e < n; e += 32) {
+        const float v = s[layout ? layout_pos(n, e) : e];
+        dst[r * n + e] = __float2bfloat16_rn(v);
+        acc += (double)v * (double)v;
+    }
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+        n2[r] = __double2float_rn(acc);
+        nrm[r] = __double2float_ru(sqrt(acc));
+    }
+}
+
+int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
+                         float *n2, float *nrm, cudaStream_t s)
+{
+    if (R == 0) return OK;
+    to_bf16_norms_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(src, rows, R, n, layout ? 1 : 0,
+                                                                  (__nv_bfloat16 *)dst_bf16, n2, nrm);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n)
+{
+    auto enc = get_encode();
+    if (!enc) {
+        set_error(ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return ERR_CUDA;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)n * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error(ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        return ERR_CUDA;
+    }
+    return OK;
+}
+
+// Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
+// gbound: per-query float bits (initialised by the caller: the seed bound).
+int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
+                     const float *xn2, const float *xnorm, int64_t N, int n, int k, unsigned int *gbound,
+                     uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s)
+{
+    SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
+    SSB_REQUIRE(N < (1ll << 31), "too many rows for the tensor-core filter");
+    if (nq == 0 || N == 0) return OK;
+    CUtensorMap mA, mB;
+    int rc = make_map(&mA, Qb, ((nq + TC_BM - 1) / TC_BM) * TC_BM, n);
+    if (rc) return rc;
+    rc = make_map(&mB, Xb, N, n);
+    if (rc) return rc;
+    TcParams p;
+    p.n = n;
+    p.KB = (n + 63) / 64;
+    p.N = N;
+    p.nq = nq;
+    p.QB = (nq + TC_BM - 1) / TC_BM;
+    p.tiles = (N + TC_BN - 1) / TC_BN;
+    const int sms = num_sms();
+    p.ctas_per_qb = std::max(1, std::min<int>((int)std::min<int64_t>(p.tiles, 1 << 20), sms / std::max(1, p.QB)));
+    if (p.QB > sms) p.ctas_per_qb = 1;
+    p.tiles_per_cta = (p.tiles + p.ctas_per_qb - 1) / p.ctas_per_qb;
+    p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
+    p.qn2 = qn2;
+    p.qnorm = qnorm;
+    p.xn2 = xn2;
+    p.xnorm = xnorm;
+    p.gbound = gbound;
+    p.k = k;
+    p.c_rel = (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -15));
+    p.cand = cand;
+    p.cand_n = cand_n;
+    p.cand_cap = cand_cap;
+    p.dump = dump;
+    const int smem = 1024 + 3 * p.KB * TC_BM * 128 + 256 + 4 * TC_BN * 4;
+    SSB_CUDA(cudaFuncSetAttribute(tc_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
+    {
+        // algorithmic bytes: every row's bf16 copy once per query block + the queries
+        ProfScope ps("tc_filter", s, (double)p.QB * N * n * 2 + (double)nq * n * 2);
+        tc_filter_kernel<<<grid, TC_THREADS, smem, s>>>(mA, mB, p);
+    }
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// debug/parity hook: S = bf16(Q) . bf16(X)^T through the same tcgen05 kernel
+int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float *S, cudaStream_t s)
+{
+    SSB_REQUIRE(B >= 1 && N >= 1, "empty operands");
+    const int Bp = (B + TC_BM - 1) / TC_BM * TC_BM;
+    DevBuf qb, xb, qn2, qnm, xn2, xnm, gb, cand, cn;
+    SSB_CUDA(qb.alloc(2 * (size_t)Bp * n, s));
+    SSB_CUDA(xb.alloc(2 * (size_t)N * n, s));
+    SSB_CUDA(qn2.alloc(4 * (size_t)Bp, s));
+    SSB_CUDA(qnm.alloc(4 * (size_t)Bp, s));
+    SSB_CUDA(xn2.alloc(4 * (size_t)N, s));
+    SSB_CUDA(xnm.alloc(4 * (size_t)N, s));
+    SSB_CUDA(gb.alloc(4 * (size_t)B, s));
+    SSB_CUDA(cand.alloc(8, s));
+    SSB_CUDA(cn.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)Bp * n, s));
+    SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
+    int rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnm.as<float>(), s);
+    if (rc) return rc;
+    rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float>(), s);
+    if (rc) return rc;
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, xn2.as<float>(), xnm.as<float>(), N, n,
+                          1, gb.as<unsigned int>(), cand.as<uint2>(), cn.as<unsigned int>(), 0, S, s);
+    if (rc) return rc;
+    SSB_CUDA(cudaStreamSynchronize(s));
+    return OK;
+}
+
+// exact rescoring of (query, row) candidates: one 8-lane group per pair,
+// rows and queries in the lane-transposed layout (global memory)
+template <int NT>
+__global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
+                               const float *__restrict__ Qp, const int32_t *__restrict__ qmap,
+                               const uint2 *__restrict__ cand, int64_t nc, ScanOut out)
+{
+    const int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    const int lane = threadIdx.x & 31, j = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    if (gp >= nc) return;
+    const uint2 c = cand[gp];
+    const int q = qmap ? qmap[c.x] : (int)c.x;
+    float qv[NT / 8];
+    lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
+    const float d2 = lay_ed2<NT>(X + (int64_t)c.y * NT, qv, j, gmask);
+    if (j == 0) {
+        const uint64_t key = make_key(d2, row_id ? row_id[c.y] : c.y);
+        const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
+        if (key <= bound) {
+            const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+        }
+    }
+}
+
+int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
+                   const uint2 *cand, int64_t nc, ScanOut out, cudaStream_t s)
+{
+    if (nc == 0) return OK;
+    const unsigned grid = (unsigned)((nc * 8 + 255) / 256);
+    ProfScope ps("rescore", s, (double)nc * n * 4);
+    switch (n) {
+    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
+    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
+    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
+    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
+    default:
+        set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled rescore kernel");
+        return ERR_USAGE;
+    }
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+}  // namespace ssb

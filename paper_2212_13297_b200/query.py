@@ -141,8 +141,15 @@ class QueryEngine:
     def close(self) -> None:
         pass
 
-    def knn_device(self, Q, k: int, want_stats: bool = False):
-        """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,4) u32]."""
+    ROUTES = {"auto": 0, "tree": 1, "tensor": 2}
+
+    def knn_device(self, Q, k: int, want_stats: bool = False, eapca_th: float = 0.25,
+                   route: str = "auto"):
+        """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,4) u32].
+
+        ``route``: "auto" applies the reference's eapca_th rule per query
+        (weak envelope pruning -> tensor-core scan path, else LB_SAX path);
+        "tree" / "tensor" force one path.  Answers are identical either way."""
         from . import _lib
         from ._device import device_f32, ptr, require_cuda, stream_handle
 
@@ -155,15 +162,20 @@ class QueryEngine:
         ids = t.empty((B, k), dtype=t.int64, device=X.device)
         pos = t.empty((B, k), dtype=t.int64, device=X.device)
         stats = np.zeros((B, 4), dtype=np.uint32) if want_stats else None
-        _lib.call("ssb_query", self._si.handle, ptr(X), B, k, ptr(d2), ptr(ids), ptr(pos),
+        if route not in self.ROUTES:
+            raise UsageError(f"route must be one of {sorted(self.ROUTES)}")
+        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route])
+        import ctypes as _ct
+
+        _lib.call("ssb_query", self._si.handle, ptr(X), B, k, _ct.byref(cfg), ptr(d2), ptr(ids), ptr(pos),
                   stats.ctypes.data_as(_lib.P) if want_stats else None, stream_handle())
         return (d2, ids, pos, stats) if want_stats else (d2, ids, pos)
 
-    def exact_knn_arrays(self, queries, k: int):
+    def exact_knn_arrays(self, queries, k: int, eapca_th: float = 0.25):
         """Batched public form over HOST buffers: (d2, ids, pos) numpy arrays
         (B, k); the H2D copy of the queries and the D2H copy of the answers
         are part of the call."""
-        d2, ids, pos = self.knn_device(queries, k)
+        d2, ids, pos = self.knn_device(queries, k, eapca_th=eapca_th)
         return d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
 
     def _stats(self, row, cfg: QueryConfig, wall: float) -> QueryStats:
@@ -203,7 +215,7 @@ class QueryEngine:
         if not np.isfinite(Q).all():
             raise UsageError("queries must be finite (documented deviation: NaN keys break ordering)")
         t0 = time.perf_counter()
-        d2, ids, pos, stats = self.knn_device(Q, cfg.k, want_stats=True)
+        d2, ids, pos, stats = self.knn_device(Q, cfg.k, want_stats=True, eapca_th=cfg.eapca_th)
         d2, ids, pos = d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
         wall = (time.perf_counter() - t0) / max(1, Q.shape[0])
         return [(ResultSet.from_arrays(d2[i], pos[i], ids[i]), self._stats(stats[i], cfg, wall))

@@ -1,0 +1,82 @@
+"""K-tc: tcgen05/TMEM/TMA tensor-core filter.  The raw dot products must match
+a BF16 matmul; the tensor-core query path must give answers identical to the
+oracle (the filter only selects rows for exact float32 rescoring)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import random_walks
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ssb():
+    import paper_2212_13297_b200 as ssb
+
+    return ssb
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("n,B,N", [(256, 200, 1000), (96, 130, 777), (64, 5, 300), (128, 128, 128)])
+def test_tc_dot_matches_bf16_matmul(ssb, n, B, N):
+    import torch
+
+    from paper_2212_13297_b200 import _lib
+
+    Q = torch.from_numpy(random_walks(B, n, 1)).cuda()
+    X = torch.from_numpy(random_walks(N, n, 2)).cuda()
+    S = torch.full((B, N), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.call("ssb_tc_dot_debug", ctypes.c_void_p(Q.data_ptr()), B, ctypes.c_void_p(X.data_ptr()), N, n,
+              ctypes.c_void_p(S.data_ptr()), None)
+    ref = Q.bfloat16().double() @ X.bfloat16().double().T
+    err = (S.double() - ref).abs().max().item()
+    assert np.isfinite(S.cpu().numpy()).all()
+    assert err < 1e-3, err
+
+
+@pytest.mark.parametrize("k", [1, 10, 50])
+def test_tensor_route_equals_oracle(ssb, oracle, k):
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(20_000, 256, 0, workers=4)
+    s = ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=1000)
+    idx = ssb.build_index_array(X, s)
+    Q = np.concatenate([G.noise_queries(X, 40, 1.0, 1), G.noise_queries(X, 20, 0.1, 2),
+                        random_walks(10, 256, 3)])
+    d2, ids, _, st = ssb.QueryEngine(idx).knn_device(Q, k, want_stats=True, route="tensor")
+    od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+def test_auto_route_mixed_block(ssb, oracle):
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(30_000, 256, 0, workers=4)
+    s = ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=1000)
+    idx = ssb.build_index_array(X, s)
+    Q = np.concatenate([G.noise_queries(X, 50, 1.0, 1), G.noise_queries(X, 50, 0.01, 1)])
+    eng = ssb.QueryEngine(idx)
+    for k in (1, 10):
+        d2, ids, _ = eng.knn_device(Q, k)
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+        t2, tid, _ = eng.knn_device(Q, k, route="tree")
+        assert np.array_equal(tid.cpu().numpy(), oid)
+
+
+def test_tensor_route_ties(ssb, oracle):
+    X = random_walks(5000, 128, 7)
+    X[4000] = X[17]
+    X[4999] = X[17]
+    s = ssb.IndexSettings(series_length=128, dataset_size=len(X), leaf_threshold=300)
+    idx = ssb.build_index_array(X, s)
+    d2, ids, _ = ssb.QueryEngine(idx).knn_device(X[[17]], 3, route="tensor")
+    assert list(ids.cpu().numpy()[0]) == [17, 4000, 4999]
