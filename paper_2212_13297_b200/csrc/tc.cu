@@ -43,7 +43,9 @@ namespace ssb {
 constexpr int TC_BM = 128;   // queries per block (MMA M)
 constexpr int TC_BN = 128;   // rows per tile (MMA N)
 constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
-constexpr int TC_THREADS = 192;
+constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
+constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
+constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
 constexpr int TC_KTOP = 32;  // in-register top-k of upper bounds (k <= 32 tightens)
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
@@ -140,8 +142,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t *t_full = bars + 5;   // [2]
     uint64_t *t_empty = bars + 7;  // [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 9);
-    float *s_xn2 = reinterpret_cast<float *>(bars + 10);  // [2][128]
-    float *s_xnorm = s_xn2 + 2 * TC_BN;                    // [2][128]
+    float4 *s_row = reinterpret_cast<float4 *>(bars + 10);          // [2][128] row constants
+    uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 2 * TC_BN);  // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qb = blockIdx.x % p.QB;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
             mbar_init(&t_full[i], 1);
-            mbar_init(&t_empty[i], 128);
+            mbar_init(&t_empty[i], TC_EPI_THREADS);
         }
         fence_barrier_init();
     }
@@ -209,55 +211,81 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else {
-        // ---------------- epilogue: one query per thread ----------------
-        const int et = threadIdx.x - 64;           // 0..127
+        // ---------------- epilogue: 8 warps, two per TMEM lane quarter ----------------
+        // thread <-> query m (TMEM lane), column half h of every 128-row tile
+        const int ew = warp - 2;                   // 0..7
+        const int et = threadIdx.x - 64;           // 0..255
         const int lane_grp = warp & 3;             // TMEM lanes [32*lane_grp, +32)
-        const int m = lane_grp * 32 + lane;        // query row within the block
-        const int ql = qb * TC_BM + m;             // launch-local query index
+        const int h = ew >> 2;                     // column half
+        const int m = lane_grp * 32 + lane;
+        const int ql = qb * TC_BM + m;
         const bool qvalid = ql < p.nq;
+        // lb = f*(1-e)*(qn2 + xn2) - 2f*s - 2cf*qn*xn,  ub = g*(1+e)*(qn2 + xn2) - 2g*s + 2cg*qn*xn
+        // with f = 1 - 4e-6, g = 1 + 4e-6, e = 2e-6 (fp32 evaluation slack); per-row
+        // constants (xn2 and xn terms) live in shared memory, per-query ones here.
+        const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
         const float qn2 = qvalid ? p.qn2[ql] : 0.f;
         const float qnm = qvalid ? p.qnorm[ql] : 0.f;
+        const float alpha_l = f * (1.f - e) * qn2, alpha_u = g * (1.f + e) * qn2;
+        const float m2f = -2.f * f, m2g = -2.f * g;
         float top[TC_KTOP];
 #pragma unroll
         for (int i = 0; i < TC_KTOP; i++) top[i] = __int_as_float(0x7f800000);
         const bool tighten = p.k <= TC_KTOP;
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
+        uint2 *stage = s_stage + ew * TC_STAGE;
+        unsigned stage_n = 0;  // warp-uniform
+        auto flush = [&]() {
+            unsigned base_slot = 0;
+            if (lane == 0 && stage_n) base_slot = atomicAdd(p.cand_n, stage_n);
+            base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+            __syncwarp();
+            for (unsigned i = lane; i < stage_n; i += 32)
+                if ((int64_t)(base_slot + i) < p.cand_cap) p.cand[base_slot + i] = stage[i];
+            __syncwarp();
+            stage_n = 0;
+        };
         for (int64_t t = 0; t < ntile; t++) {
             const int s = (int)(t & 1);
             const int64_t row0 = (t_begin + t) * TC_BN;
-            // row norms of this tile (one row per epilogue thread)
-            {
+            if (et < TC_BN) {
                 const int64_t r = row0 + et;
-                s_xn2[s * TC_BN + et] = r < p.N ? p.xn2[r] : 0.f;
-                s_xnorm[s * TC_BN + et] = r < p.N ? p.xnorm[r] : 0.f;
+                float4 rc = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
+                if (r < p.N) {
+                    const float xn2 = p.xn2[r], xn = p.xnorm[r];
+                    rc = make_float4(f * (1.f - e) * xn2, 2.f * p.c_rel * f * xn, g * (1.f + e) * xn2,
+                                     2.f * p.c_rel * g * xn);
+                }
+                s_row[s * TC_BN + et] = rc;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float bound = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : 0.f;
-            bound = fminf(bound, kth);
-            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN);
-            for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+            float bound = qvalid ? fminf(__uint_as_float(*(volatile unsigned int *)gb), kth) : -1.f;
+            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
+            const float4 *rows = s_row + s * TC_BN + h * 64;
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 16) {
                 uint32_t v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
+                if (p.dump) {
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int64_t r = row0 + h * 64 + c0 + i;
+                        if (qvalid && r < p.N) p.dump[(int64_t)ql * p.N + r] = __uint_as_float(v[i]);
+                    }
+                    continue;
+                }
+                uint32_t emit = 0;
 #pragma unroll
                 for (int i = 0; i < 16; i++) {
-                    const int c = c0 + i;
-                    const int64_t r = row0 + c;
-                    const float sdot = __uint_as_float(v[i]);
-                    if (p.dump) {
-                        if (qvalid && r < p.N) p.dump[(int64_t)ql * p.N + r] = sdot;
-                        continue;
-                    }
-                    const float xn2 = s_xn2[s * TC_BN + c];
-                    const float approx = (qn2 + xn2) - 2.f * sdot;
-                    const float marg = 2.f * p.c_rel * qnm * s_xnorm[s * TC_BN + c] + 1.0e-6f * (qn2 + xn2);
-                    const float lb = (approx - marg) * (1.f - 4e-6f);
-                    const bool ok = qvalid && r < p.N;
-                    bool emit = ok && lb <= bound;
-                    if (ok && tighten) {
-                        const float ub = (approx + marg) * (1.f + 4e-6f);
+                    const float sd = __uint_as_float(v[i]);
+                    const float4 rc = rows[c0 + i];
+                    const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                    emit |= (lb <= bound ? 1u : 0u) << i;
+                    if (tighten) {
+                        const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
                         if (ub < kth) {
                             float x = ub;
 #pragma unroll
@@ -272,15 +300,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             bound = fminf(bound, kth);
                         }
                     }
-                    const unsigned bal = __ballot_sync(0xffffffffu, emit);
-                    if (bal) {
-                        unsigned base_slot = 0;
-                        if (lane == 0) base_slot = atomicAdd(p.cand_n, (unsigned)__popc(bal));
-                        base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
-                        if (emit) {
-                            const unsigned slot = base_slot + __popc(bal & ((1u << lane) - 1u));
-                            if ((int64_t)slot < p.cand_cap) p.cand[slot] = make_uint2((unsigned)ql, (unsigned)r);
+                }
+                // warp-staged emission of (query, row) candidates
+                unsigned cnt = __popc(emit);
+                unsigned incl = cnt;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += y;
+                }
+                const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total) {
+                    if (stage_n + total > TC_STAGE) flush();
+                    if (total > TC_STAGE) {  // pathological: write through
+                        unsigned b0 = 0;
+                        if (lane == 31) b0 = atomicAdd(p.cand_n, total);
+                        b0 = __shfl_sync(0xffffffffu, b0, 31);
+                        unsigned slot = b0 + incl - cnt;
+                        while (emit) {
+                            const int i = __ffs(emit) - 1;
+                            emit &= emit - 1;
+                            if ((int64_t)slot < p.cand_cap)
+                                p.cand[slot] = make_uint2((unsigned)ql, (unsigned)(row0 + h * 64 + c0 + i));
+                            slot++;
                         }
+                    } else {
+                        unsigned slot = stage_n + incl - cnt;
+                        while (emit) {
+                            const int i = __ffs(emit) - 1;
+                            emit &= emit - 1;
+                            stage[slot++] = make_uint2((unsigned)ql, (unsigned)(row0 + h * 64 + c0 + i));
+                        }
+                        stage_n += total;
                     }
                 }
             }
@@ -290,6 +341,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&t_empty[s]);
         }
+        __syncwarp();
+        flush();
     }
     __syncthreads();
     if (warp == 1) {
@@ -404,7 +457,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.cand_n = cand_n;
     p.cand_cap = cand_cap;
     p.dump = dump;
-    const int smem = 1024 + 3 * p.KB * TC_BM * 128 + 256 + 4 * TC_BN * 4;
+    const int smem = 1024 + 3 * p.KB * TC_BM * 128 + 128 + 2 * TC_BN * 16 + 8 * TC_STAGE * 8;
     SSB_CUDA(cudaFuncSetAttribute(tc_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     {
