@@ -124,6 +124,7 @@ struct TcParams {
     float *dump;               // debug: full S matrix (nq x N) when non-null
 };
 
+template <int KTOP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_filter_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p)
 {
@@ -228,10 +229,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const float qnm = qvalid ? p.qnorm[ql] : 0.f;
         const float alpha_l = f * (1.f - e) * qn2, alpha_u = g * (1.f + e) * qn2;
         const float m2f = -2.f * f, m2g = -2.f * g;
-        float top[TC_KTOP];
+        float top[KTOP > 0 ? KTOP : 1];
 #pragma unroll
-        for (int i = 0; i < TC_KTOP; i++) top[i] = __int_as_float(0x7f800000);
-        const bool tighten = p.k <= TC_KTOP;
+        for (int i = 0; i < (KTOP > 0 ? KTOP : 1); i++) top[i] = __int_as_float(0x7f800000);
+        constexpr bool tighten = KTOP > 0;
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
         uint2 *stage = s_stage + ew * TC_STAGE;
@@ -284,23 +285,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const float4 rc = rows[c0 + i];
                     const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
                     emit |= (lb <= bound ? 1u : 0u) << i;
-                    if (tighten) {
-                        const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
-                        if (ub < kth) {
-                            float x = ub;
+                    if constexpr (tighten) {
+                        if (lb < kth) {  // ub >= lb: only then can ub improve the k-th bound
+                            const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
+                            if (ub < kth) {
+                                float x = ub;
 #pragma unroll
-                            for (int j = 0; j < TC_KTOP; j++) {
-                                const float lo = fminf(top[j], x);
-                                x = fmaxf(top[j], x);
-                                top[j] = lo;
+                                for (int j = 0; j < KTOP; j++) {
+                                    const float lo = fminf(top[j], x);
+                                    x = fmaxf(top[j], x);
+                                    top[j] = lo;
+                                }
+#pragma unroll
+                                for (int j = 0; j < KTOP; j++)
+                                    if (j == p.k - 1) kth = top[j];
+                                bound = fminf(bound, kth);
                             }
-#pragma unroll
-                            for (int j = 0; j < TC_KTOP; j++)
-                                if (j == p.k - 1) kth = top[j];
-                            bound = fminf(bound, kth);
                         }
                     }
                 }
+                if (!__any_sync(0xffffffffu, emit != 0)) continue;
                 // warp-staged emission of (query, row) candidates
                 unsigned cnt = __popc(emit);
                 unsigned incl = cnt;
@@ -458,13 +462,25 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.cand_cap = cand_cap;
     p.dump = dump;
     const int smem = 1024 + 3 * p.KB * TC_BM * 128 + 128 + 2 * TC_BN * 16 + 8 * TC_STAGE * 8;
-    SSB_CUDA(cudaFuncSetAttribute(tc_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
-    {
+    auto go = [&](auto kern) -> int {
+        SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         // algorithmic bytes: every row's bf16 copy once per query block + the queries
         ProfScope ps("tc_filter", s, (double)p.QB * N * n * 2 + (double)nq * n * 2);
-        tc_filter_kernel<<<grid, TC_THREADS, smem, s>>>(mA, mB, p);
-    }
+        kern<<<grid, TC_THREADS, smem, s>>>(mA, mB, p);
+        return OK;
+    };
+    if (k <= 1)
+        rc = go(tc_filter_kernel<1>);
+    else if (k <= 4)
+        rc = go(tc_filter_kernel<4>);
+    else if (k <= 16)
+        rc = go(tc_filter_kernel<16>);
+    else if (k <= 32)
+        rc = go(tc_filter_kernel<32>);
+    else
+        rc = go(tc_filter_kernel<0>);
+    if (rc) return rc;
     SSB_CHECK_LAUNCH();
     return OK;
 }
