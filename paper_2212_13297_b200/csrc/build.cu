@@ -40,7 +40,7 @@ namespace ssb {
 
 Index::~Index()
 {
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm};
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm, rowc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -544,7 +544,10 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
     SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
     SSB_CUDA(cudaMalloc(&ix.xnorm, (size_t)ix.N * 4));
-    return launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
+    SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)ix.N * 16));
+    int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
+    if (rc) return rc;
+    return launch_tc_row_consts(ix.xn2, ix.xnorm, ix.N, ix.rowc, s);
 }
 
 int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg,

@@ -115,6 +115,7 @@ struct TcParams {
     int ctas_per_qb;
     const float *qn2, *qnorm;  // per query (launch-local index)
     const float *xn2, *xnorm;  // per row
+    const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
     int k;
     float c_rel;               // dot-product error coefficient
@@ -247,26 +248,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             stage_n = 0;
         };
+        // row constants and the shared bound are prefetched one tile ahead
+        const float4 inf4 = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
+        float4 pre = inf4;
+        if (et < TC_BN && ntile > 0) {
+            const int64_t r = t_begin * TC_BN + et;
+            if (r < p.N) pre = p.rowc[r];
+        }
+        float gnext = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : -1.f;
         for (int64_t t = 0; t < ntile; t++) {
             const int s = (int)(t & 1);
             const int64_t row0 = (t_begin + t) * TC_BN;
-            if (et < TC_BN) {
-                const int64_t r = row0 + et;
-                float4 rc = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
-                if (r < p.N) {
-                    const float xn2 = p.xn2[r], xn = p.xnorm[r];
-                    rc = make_float4(f * (1.f - e) * xn2, 2.f * p.c_rel * f * xn, g * (1.f + e) * xn2,
-                                     2.f * p.c_rel * g * xn);
-                }
-                s_row[s * TC_BN + et] = rc;
-            }
+            if (et < TC_BN) s_row[s * TC_BN + et] = pre;
             asm volatile("bar.sync 1, 256;" ::: "memory");
+            float bound = qvalid ? fminf(gnext, kth) : -1.f;
+            if (et < TC_BN && t + 1 < ntile) {
+                const int64_t r = row0 + TC_BN + et;
+                pre = r < p.N ? p.rowc[r] : inf4;
+            }
+            if (qvalid) gnext = __uint_as_float(*(volatile unsigned int *)gb);
             mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float bound = qvalid ? fminf(__uint_as_float(*(volatile unsigned int *)gb), kth) : -1.f;
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
             const float4 *rows = s_row + s * TC_BN + h * 64;
-#pragma unroll 1
+#pragma unroll
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 uint32_t v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
@@ -390,6 +395,28 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
     return OK;
 }
 
+// per-row constants of the bound formulas (see the epilogue):
+// (f(1-e) xn2, 2 c f xn, g(1+e) xn2, 2 c g xn)
+__global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float *__restrict__ xn, int64_t N,
+                                     float c_rel, float4 *__restrict__ out)
+{
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= N) return;
+    const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
+    out[r] = make_float4(f * (1.f - e) * xn2[r], 2.f * c_rel * f * xn[r], g * (1.f + e) * xn2[r],
+                         2.f * c_rel * g * xn[r]);
+}
+
+static float tc_c_rel() { return (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -15)); }
+
+int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s)
+{
+    if (N == 0) return OK;
+    tc_row_consts_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(xn2, xn, N, tc_c_rel(), out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -427,7 +454,7 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n)
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
 int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
-                     const float *xn2, const float *xnorm, int64_t N, int n, int k, unsigned int *gbound,
+                     const float4 *rowc, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s)
 {
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
@@ -452,11 +479,12 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
     p.qn2 = qn2;
     p.qnorm = qnorm;
-    p.xn2 = xn2;
-    p.xnorm = xnorm;
+    p.xn2 = nullptr;
+    p.xnorm = nullptr;
+    p.rowc = rowc;
     p.gbound = gbound;
     p.k = k;
-    p.c_rel = (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -15));
+    p.c_rel = tc_c_rel();
     p.cand = cand;
     p.cand_n = cand_n;
     p.cand_cap = cand_cap;
@@ -507,7 +535,11 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     if (rc) return rc;
     rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float>(), s);
     if (rc) return rc;
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, xn2.as<float>(), xnm.as<float>(), N, n,
+    DevBuf rcb;
+    SSB_CUDA(rcb.alloc(16 * (size_t)N, s));
+    rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float>(), N, rcb.as<float4>(), s);
+    if (rc) return rc;
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, rcb.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), cn.as<unsigned int>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
