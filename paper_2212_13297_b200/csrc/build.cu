@@ -40,7 +40,7 @@ namespace ssb {
 
 Index::~Index()
 {
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm, rowc};
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm, rowc, tilec};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -547,7 +547,10 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
     SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)ix.N * 16));
     int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
     if (rc) return rc;
-    return launch_tc_row_consts(ix.xn2, ix.xnorm, ix.N, ix.rowc, s);
+    SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 2) * 16));
+    rc = launch_tc_row_consts(ix.xn2, ix.xnorm, ix.N, ix.rowc, s);
+    if (rc) return rc;
+    return launch_tc_tile_consts(ix.rowc, ix.N, ix.tilec, s);
 }
 
 int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg,

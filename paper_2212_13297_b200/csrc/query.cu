@@ -658,7 +658,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         seed_bound_kernel<<<(nq + 255) / 256, 256, 0, s>>>(thr.as<uint64_t>(), d_qtc.as<int32_t>(), nq,
                                                           gb.as<unsigned int>());
         SSB_CHECK_LAUNCH();
-        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), nq, ix.Xb, ix.rowc, ix.N, n, k,
+        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
                               gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_n.as<unsigned int>(), tc_cap, nullptr,
                               s);
         if (rc) return rc;

@@ -116,6 +116,7 @@ struct TcParams {
     const float *qn2, *qnorm;  // per query (launch-local index)
     const float *xn2, *xnorm;  // per row
     const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
+    const float4 *tilec;       // per 64-row half tile: (min a, max b, min a', min b')
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
     int k;
     float c_rel;               // dot-product error coefficient
@@ -256,22 +257,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (r < p.N) pre = p.rowc[r];
         }
         float gnext = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : -1.f;
+        float4 tnext = ntile > 0 ? p.tilec[t_begin * 2 + h] : inf4;
+        const float inv2f = 0.5f / f, inv2g = 0.5f / g;
         for (int64_t t = 0; t < ntile; t++) {
             const int s = (int)(t & 1);
             const int64_t row0 = (t_begin + t) * TC_BN;
             if (et < TC_BN) s_row[s * TC_BN + et] = pre;
             asm volatile("bar.sync 1, 256;" ::: "memory");
             float bound = qvalid ? fminf(gnext, kth) : -1.f;
-            if (et < TC_BN && t + 1 < ntile) {
-                const int64_t r = row0 + TC_BN + et;
-                pre = r < p.N ? p.rowc[r] : inf4;
+            const float4 tc4 = tnext;
+            if (t + 1 < ntile) {
+                tnext = p.tilec[(t_begin + t + 1) * 2 + h];
+                if (et < TC_BN) {
+                    const int64_t r = row0 + TC_BN + et;
+                    pre = r < p.N ? p.rowc[r] : inf4;
+                }
             }
             if (qvalid) gnext = __uint_as_float(*(volatile unsigned int *)gb);
             mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
             const float4 *rows = s_row + s * TC_BN + h * 64;
-#pragma unroll
+            // tile-level necessary conditions on the dot product s:
+            //   lb_r <= bound  =>  s >= s_lo ;   ub_r < kth  =>  s > s_need
+            const float base_lo = alpha_l + tc4.x - qnm * tc4.y;
+            const float base_need = alpha_u + tc4.z + qnm * tc4.w;
+#pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 uint32_t v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
@@ -283,28 +294,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                     continue;
                 }
+                float mx = __uint_as_float(v[0]);
+#pragma unroll
+                for (int i = 1; i < 16; i++) mx = fmaxf(mx, __uint_as_float(v[i]));
+                // lowered by a relative 1e-5 so float32 rounding can only make the
+                // fast path take the precise per-row test more often, never less
+                float s_lo = (base_lo - bound) * inv2f;
+                s_lo -= 1e-5f * (fabsf(s_lo) + 1.f);
+                float s_need = __int_as_float(0x7f800000);
+                if (tighten) {
+                    s_need = (base_need - kth) * inv2g;
+                    s_need -= 1e-5f * (fabsf(s_need) + 1.f);
+                }
                 uint32_t emit = 0;
+                if (mx >= fminf(s_lo, s_need)) {
 #pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    const float sd = __uint_as_float(v[i]);
-                    const float4 rc = rows[c0 + i];
-                    const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
-                    emit |= (lb <= bound ? 1u : 0u) << i;
-                    if constexpr (tighten) {
-                        if (lb < kth) {  // ub >= lb: only then can ub improve the k-th bound
-                            const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
-                            if (ub < kth) {
-                                float x = ub;
+                    for (int i = 0; i < 16; i++) {
+                        const float sd = __uint_as_float(v[i]);
+                        const float4 rc = rows[c0 + i];
+                        const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                        emit |= (lb <= bound ? 1u : 0u) << i;
+                        if constexpr (tighten) {
+                            if (lb < kth) {  // ub >= lb: only then can ub improve the k-th bound
+                                const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
+                                if (ub < kth) {
+                                    float x = ub;
 #pragma unroll
-                                for (int j = 0; j < KTOP; j++) {
-                                    const float lo = fminf(top[j], x);
-                                    x = fmaxf(top[j], x);
-                                    top[j] = lo;
+                                    for (int j = 0; j < KTOP; j++) {
+                                        const float lo = fminf(top[j], x);
+                                        x = fmaxf(top[j], x);
+                                        top[j] = lo;
+                                    }
+#pragma unroll
+                                    for (int j = 0; j < KTOP; j++)
+                                        if (j == p.k - 1) kth = top[j];
+                                    bound = fminf(bound, kth);
                                 }
-#pragma unroll
-                                for (int j = 0; j < KTOP; j++)
-                                    if (j == p.k - 1) kth = top[j];
-                                bound = fminf(bound, kth);
                             }
                         }
                     }
@@ -407,6 +432,42 @@ __global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float 
                          2.f * c_rel * g * xn[r]);
 }
 
+// per 64-row half tile: (min a, max b, min a', min b') of the row constants
+__global__ void tc_tile_consts_kernel(const float4 *__restrict__ rowc, int64_t N, int64_t halves, float4 *__restrict__ out)
+{
+    const int64_t hidx = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    if (hidx >= halves) return;
+    const int lane = threadIdx.x & 31;
+    float mina = __int_as_float(0x7f800000), maxb = 0.f, mina2 = __int_as_float(0x7f800000),
+          minb2 = __int_as_float(0x7f800000);
+    for (int i = lane; i < 64; i += 32) {
+        const int64_t r = hidx * 64 + i;
+        if (r < N) {
+            const float4 c = rowc[r];
+            mina = fminf(mina, c.x);
+            maxb = fmaxf(maxb, c.y);
+            mina2 = fminf(mina2, c.z);
+            minb2 = fminf(minb2, c.w);
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        mina = fminf(mina, __shfl_xor_sync(0xffffffffu, mina, off));
+        maxb = fmaxf(maxb, __shfl_xor_sync(0xffffffffu, maxb, off));
+        mina2 = fminf(mina2, __shfl_xor_sync(0xffffffffu, mina2, off));
+        minb2 = fminf(minb2, __shfl_xor_sync(0xffffffffu, minb2, off));
+    }
+    if (lane == 0) out[hidx] = make_float4(mina, maxb, mina2, minb2 == __int_as_float(0x7f800000) ? 0.f : minb2);
+}
+
+int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s)
+{
+    const int64_t halves = (N + TC_BN - 1) / TC_BN * 2;
+    if (halves == 0) return OK;
+    tc_tile_consts_kernel<<<(unsigned)((halves + 7) / 8), 256, 0, s>>>(rowc, N, halves, out);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
 static float tc_c_rel() { return (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -15)); }
 
 int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s)
@@ -454,7 +515,7 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n)
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
 int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
-                     const float4 *rowc, int64_t N, int n, int k, unsigned int *gbound,
+                     const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s)
 {
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
@@ -482,6 +543,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.xn2 = nullptr;
     p.xnorm = nullptr;
     p.rowc = rowc;
+    p.tilec = tilec;
     p.gbound = gbound;
     p.k = k;
     p.c_rel = tc_c_rel();
@@ -539,7 +601,11 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     SSB_CUDA(rcb.alloc(16 * (size_t)N, s));
     rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float>(), N, rcb.as<float4>(), s);
     if (rc) return rc;
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, rcb.as<float4>(), N, n,
+    DevBuf tcb;
+    SSB_CUDA(tcb.alloc(16 * (size_t)((N + TC_BN - 1) / TC_BN * 2), s));
+    rc = launch_tc_tile_consts(rcb.as<float4>(), N, tcb.as<float4>(), s);
+    if (rc) return rc;
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), cn.as<unsigned int>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
