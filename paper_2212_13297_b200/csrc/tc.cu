@@ -71,6 +71,31 @@ __device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_mc(void *smem, const CUtensorMap *map, int x, int y, uint64_t *bar,
+                                               uint16_t mask)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(d),
+        "l"(map), "r"(b), "r"(x), "r"(y), "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(a),
+                 "h"(mask)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -111,8 +136,9 @@ struct TcParams {
     int nq;                // queries in this launch (<= QB*128)
     int QB;                // query blocks
     int64_t tiles;         // ceil(N / 128)
-    int64_t tiles_per_cta; // contiguous tile chunk per CTA
-    int ctas_per_qb;
+    int64_t tiles_per_cta; // contiguous tile chunk per CTA (per cluster)
+    int ctas_per_qb;       // chunks
+    int CS;                // cluster size: CTAs (query blocks) sharing each B tile by multicast
     const float *qn2, *qnorm;  // per query (launch-local index)
     const float *xn2, *xnorm;  // per row
     const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
@@ -130,6 +156,8 @@ template <int KTOP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_filter_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p)
 {
+    // mapB's box covers 128/CS rows: every CTA of the cluster loads one row
+    // slice of each B tile and multicasts it to the whole cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms
     unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -149,8 +177,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 2 * TC_BN);  // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qb = blockIdx.x % p.QB;
-    const int chunk = blockIdx.x / p.QB;
+    const int CS = p.CS;
+    const int rank = (int)(blockIdx.x % CS);  // == %cluster_ctarank (clusters are consecutive blocks)
+    const int cid = (int)(blockIdx.x / CS);
+    const int chunk = cid % p.ctas_per_qb;
+    const int qb = (cid / p.ctas_per_qb) * CS + rank;
+    const uint16_t cmask = (uint16_t)((1u << CS) - 1u);
     const int64_t t_begin = (int64_t)chunk * p.tiles_per_cta;
     const int64_t t_end = min(p.tiles, t_begin + p.tiles_per_cta);
     const int64_t ntile = t_end > t_begin ? t_end - t_begin : 0;
@@ -159,7 +191,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_init(a_full, 1);
         for (int i = 0; i < 2; i++) {
             mbar_init(&b_full[i], 1);
-            mbar_init(&b_empty[i], 1);
+            mbar_init(&b_empty[i], CS);  // one multicast commit from every CTA of the cluster
             mbar_init(&t_full[i], 1);
             mbar_init(&t_empty[i], TC_EPI_THREADS);
         }
@@ -172,6 +204,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (CS > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast lands
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem_base = *tmem_slot;
 
@@ -184,9 +217,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int s = (int)(t & 1);
                 if (t >= 2) mbar_wait(&b_empty[s], (unsigned)(((t >> 1) - 1) & 1));
                 unsigned char *sB = s ? sB1 : sB0;
-                mbar_expect_tx(&b_full[s], KB * chunk_bytes);
+                mbar_expect_tx(&b_full[s], KB * chunk_bytes);  // the whole tile lands here
                 const int row0 = (int)((t_begin + t) * TC_BN);
-                for (int kb = 0; kb < KB; kb++) tma_load_2d(sB + kb * chunk_bytes, &mapB, kb * 64, row0, &b_full[s]);
+                if (CS == 1) {
+                    for (int kb = 0; kb < KB; kb++)
+                        tma_load_2d(sB + kb * chunk_bytes, &mapB, kb * 64, row0, &b_full[s]);
+                } else {
+                    const int srows = TC_BN / CS;
+                    for (int kb = 0; kb < KB; kb++)
+                        tma_load_2d_mc(sB + kb * chunk_bytes + rank * srows * 128, &mapB, kb * 64, row0 + rank * srows,
+                                       &b_full[s], cmask);
+                }
             }
         }
     } else if (warp == 1) {
@@ -209,7 +250,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         umma_bf16(tmem_d, umma_desc_sw128(a_addr + off), umma_desc_sw128(b_addr + off),
                                   (kb | ks) ? 1u : 0u);
                     }
-                umma_commit(&b_empty[s]);
+                if (CS == 1)
+                    umma_commit(&b_empty[s]);
+                else
+                    umma_commit_mc(&b_empty[s], cmask);  // frees stage s in every CTA's producer
                 umma_commit(&t_full[s]);
             }
         }
@@ -379,6 +423,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         flush();
     }
     __syncthreads();
+    if (CS > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
@@ -491,7 +536,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n)
+static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int box_rows = 128)
 {
     auto enc = get_encode();
     if (!enc) {
@@ -500,7 +545,7 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n)
     }
     cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)n * 2};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -521,23 +566,30 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
     SSB_REQUIRE(N < (1ll << 31), "too many rows for the tensor-core filter");
     if (nq == 0 || N == 0) return OK;
-    CUtensorMap mA, mB;
-    int rc = make_map(&mA, Qb, ((nq + TC_BM - 1) / TC_BM) * TC_BM, n);
-    if (rc) return rc;
-    rc = make_map(&mB, Xb, N, n);
-    if (rc) return rc;
     TcParams p;
     p.n = n;
     p.KB = (n + 63) / 64;
     p.N = N;
     p.nq = nq;
-    p.QB = (nq + TC_BM - 1) / TC_BM;
+    const int QB = (nq + TC_BM - 1) / TC_BM;
+    // cluster: up to 8 query blocks share every B tile through TMA multicast
+    int CS = 1;
+    while (CS < QB && CS < 8) CS <<= 1;
+    const int groups = (QB + CS - 1) / CS;
+    p.QB = groups * CS;  // padded; blocks past nq are all-invalid queries
+    p.CS = CS;
     p.tiles = (N + TC_BN - 1) / TC_BN;
     const int sms = num_sms();
-    p.ctas_per_qb = std::max(1, std::min<int>((int)std::min<int64_t>(p.tiles, 1 << 20), sms / std::max(1, p.QB)));
-    if (p.QB > sms) p.ctas_per_qb = 1;
-    p.tiles_per_cta = (p.tiles + p.ctas_per_qb - 1) / p.ctas_per_qb;
+    int clusters_per_group = std::max(1, sms / CS / groups);
+    clusters_per_group = (int)std::min<int64_t>(clusters_per_group, p.tiles);
+    p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
+    CUtensorMap mA, mB;
+    // rows beyond the allocated ceil(nq/128)*128 are zero-filled by TMA (padded blocks)
+    int rc = make_map(&mA, Qb, (int64_t)((nq + TC_BM - 1) / TC_BM) * TC_BM, n);
+    if (rc) return rc;
+    rc = make_map(&mB, Xb, N, n, TC_BN / CS);
+    if (rc) return rc;
     p.qn2 = qn2;
     p.qnorm = qnorm;
     p.xn2 = nullptr;
@@ -555,9 +607,21 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        // algorithmic bytes: every row's bf16 copy once per query block + the queries
-        ProfScope ps("tc_filter", s, (double)p.QB * N * n * 2 + (double)nq * n * 2);
-        kern<<<grid, TC_THREADS, smem, s>>>(mA, mB, p);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
+        ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2);
+        SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mA, mB, p));
         return OK;
     };
     if (k <= 1)
