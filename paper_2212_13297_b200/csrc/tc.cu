@@ -46,6 +46,7 @@ constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
 constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
+constexpr int TC_NSLOT = 8;          // B pipeline depth in 16 KB K-chunks
 constexpr int TC_KTOP = 32;  // in-register top-k of upper bounds (k <= 32 tightens)
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
@@ -164,16 +165,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int KB = p.KB;
     const uint32_t chunk_bytes = TC_BM * 128;  // 128 rows x 64 bf16
     unsigned char *sA = base;
-    unsigned char *sB0 = base + KB * chunk_bytes;
-    unsigned char *sB1 = sB0 + KB * chunk_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB1 + KB * chunk_bytes);
+    unsigned char *sRing = base + KB * chunk_bytes;  // TC_NSLOT chunk slots (128 rows x 64 cols each)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sRing + TC_NSLOT * chunk_bytes);
     uint64_t *a_full = bars + 0;
-    uint64_t *b_full = bars + 1;   // [2]
-    uint64_t *b_empty = bars + 3;  // [2]
-    uint64_t *t_full = bars + 5;   // [2]
-    uint64_t *t_empty = bars + 7;  // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 9);
-    float4 *s_row = reinterpret_cast<float4 *>(bars + 10);          // [2][128] row constants
+    uint64_t *b_full = bars + 1;               // [TC_NSLOT]
+    uint64_t *b_empty = bars + 1 + TC_NSLOT;   // [TC_NSLOT]
+    uint64_t *t_full = bars + 1 + 2 * TC_NSLOT;   // [2]
+    uint64_t *t_empty = bars + 3 + 2 * TC_NSLOT;  // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5 + 2 * TC_NSLOT);
+    float4 *s_row = reinterpret_cast<float4 *>(bars + 6 + 2 * TC_NSLOT);  // [2][128] row constants
     uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 2 * TC_BN);  // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,9 +189,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(a_full, 1);
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < TC_NSLOT; i++) {
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], CS);  // one multicast commit from every CTA of the cluster
+        }
+        for (int i = 0; i < 2; i++) {
             mbar_init(&t_full[i], 1);
             mbar_init(&t_empty[i], TC_EPI_THREADS);
         }
@@ -213,20 +215,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0 && ntile > 0) {
             mbar_expect_tx(a_full, KB * chunk_bytes);
             for (int kb = 0; kb < KB; kb++) tma_load_2d(sA + kb * chunk_bytes, &mapA, kb * 64, qb * TC_BM, a_full);
+            // ring of K-chunk slots: chunk c = t*KB + kb -> slot c % NSLOT, use c / NSLOT
+            int64_t c = 0;
             for (int64_t t = 0; t < ntile; t++) {
-                const int s = (int)(t & 1);
-                if (t >= 2) mbar_wait(&b_empty[s], (unsigned)(((t >> 1) - 1) & 1));
-                unsigned char *sB = s ? sB1 : sB0;
-                mbar_expect_tx(&b_full[s], KB * chunk_bytes);  // the whole tile lands here
                 const int row0 = (int)((t_begin + t) * TC_BN);
-                if (CS == 1) {
-                    for (int kb = 0; kb < KB; kb++)
-                        tma_load_2d(sB + kb * chunk_bytes, &mapB, kb * 64, row0, &b_full[s]);
-                } else {
-                    const int srows = TC_BN / CS;
-                    for (int kb = 0; kb < KB; kb++)
-                        tma_load_2d_mc(sB + kb * chunk_bytes + rank * srows * 128, &mapB, kb * 64, row0 + rank * srows,
-                                       &b_full[s], cmask);
+                for (int kb = 0; kb < KB; kb++, c++) {
+                    const int slot = (int)(c % TC_NSLOT);
+                    const int64_t use = c / TC_NSLOT;
+                    if (use >= 1) mbar_wait(&b_empty[slot], (unsigned)((use - 1) & 1));
+                    unsigned char *dst = sRing + slot * chunk_bytes;
+                    mbar_expect_tx(&b_full[slot], chunk_bytes);  // the whole chunk lands here
+                    if (CS == 1) {
+                        tma_load_2d(dst, &mapB, kb * 64, row0, &b_full[slot]);
+                    } else {
+                        const int srows = TC_BN / CS;
+                        tma_load_2d_mc(dst + rank * srows * 128, &mapB, kb * 64, row0 + rank * srows, &b_full[slot],
+                                       cmask);
+                    }
                 }
             }
         }
@@ -236,24 +241,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_wait(a_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t a_addr = (uint32_t)__cvta_generic_to_shared(sA);
+            int64_t c = 0;
             for (int64_t t = 0; t < ntile; t++) {
                 const int s = (int)(t & 1);
-                mbar_wait(&b_full[s], (unsigned)((t >> 1) & 1));
                 if (t >= 2) mbar_wait(&t_empty[s], (unsigned)(((t >> 1) - 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t b_addr = (uint32_t)__cvta_generic_to_shared(s ? sB1 : sB0);
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
-                for (int kb = 0; kb < KB; kb++)
+                for (int kb = 0; kb < KB; kb++, c++) {
+                    const int slot = (int)(c % TC_NSLOT);
+                    mbar_wait(&b_full[slot], (unsigned)((c / TC_NSLOT) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t b_addr = (uint32_t)__cvta_generic_to_shared(sRing + slot * chunk_bytes);
 #pragma unroll
                     for (int ks = 0; ks < 4; ks++) {
-                        const uint32_t off = kb * chunk_bytes + ks * 32;
-                        umma_bf16(tmem_d, umma_desc_sw128(a_addr + off), umma_desc_sw128(b_addr + off),
+                        const uint32_t offa = kb * chunk_bytes + ks * 32;
+                        umma_bf16(tmem_d, umma_desc_sw128(a_addr + offa), umma_desc_sw128(b_addr + ks * 32),
                                   (kb | ks) ? 1u : 0u);
                     }
-                if (CS == 1)
-                    umma_commit(&b_empty[s]);
-                else
-                    umma_commit_mc(&b_empty[s], cmask);  // frees stage s in every CTA's producer
+                    if (CS == 1)
+                        umma_commit(&b_empty[slot]);
+                    else
+                        umma_commit_mc(&b_empty[slot], cmask);  // frees the slot in every CTA's producer
+                }
                 umma_commit(&t_full[s]);
             }
         }
@@ -603,7 +611,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.cand_n = cand_n;
     p.cand_cap = cand_cap;
     p.dump = dump;
-    const int smem = 1024 + 3 * p.KB * TC_BM * 128 + 128 + 2 * TC_BN * 16 + 8 * TC_STAGE * 8;
+    const int smem = 1024 + (p.KB + TC_NSLOT) * TC_BM * 128 + 8 * (6 + 2 * TC_NSLOT) + 2 * TC_BN * 16 +
+                     8 * TC_STAGE * 8;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
