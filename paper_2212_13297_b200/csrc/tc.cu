@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "layout.cuh"
@@ -151,6 +152,7 @@ struct TcParams {
     unsigned int *cand_n;
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
+    int skip_epi;              // diagnostics (SSB_TC_DIAG=1): epilogue only releases TMEM
 };
 
 template <int KTOP>
@@ -173,8 +175,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t *t_full = bars + 1 + 2 * TC_NSLOT;   // [2]
     uint64_t *t_empty = bars + 3 + 2 * TC_NSLOT;  // [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5 + 2 * TC_NSLOT);
-    float4 *s_row = reinterpret_cast<float4 *>(bars + 6 + 2 * TC_NSLOT);  // [2][128] row constants
-    uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 2 * TC_BN);  // [8 warps][TC_STAGE]
+    float4 *s_row = reinterpret_cast<float4 *>(bars + 6 + 2 * TC_NSLOT);  // [8 warps][2][64] row constants
+    uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 8 * 2 * 64);     // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int CS = p.CS;
@@ -301,35 +303,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             stage_n = 0;
         };
-        // row constants and the shared bound are prefetched one tile ahead
+        // row constants (warp-private copy of this warp's 64 columns) and the
+        // shared bound are prefetched one tile ahead; no cross-warp barrier
         const float4 inf4 = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
-        float4 pre = inf4;
-        if (et < TC_BN && ntile > 0) {
-            const int64_t r = t_begin * TC_BN + et;
-            if (r < p.N) pre = p.rowc[r];
+        float4 pre0 = inf4, pre1 = inf4;
+        if (ntile > 0) {
+            const int64_t r = t_begin * TC_BN + h * 64 + 2 * lane;
+            if (r < p.N) pre0 = p.rowc[r];
+            if (r + 1 < p.N) pre1 = p.rowc[r + 1];
         }
         float gnext = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : -1.f;
         float4 tnext = ntile > 0 ? p.tilec[t_begin * 2 + h] : inf4;
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
+        float4 *wrow = s_row + ew * 2 * 64;
         for (int64_t t = 0; t < ntile; t++) {
             const int s = (int)(t & 1);
             const int64_t row0 = (t_begin + t) * TC_BN;
-            if (et < TC_BN) s_row[s * TC_BN + et] = pre;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            float bound = qvalid ? fminf(gnext, kth) : -1.f;
+            wrow[s * 64 + 2 * lane] = pre0;
+            wrow[s * 64 + 2 * lane + 1] = pre1;
+            __syncwarp();
+            const float gcur = gnext;
+            float bound = qvalid ? fminf(gcur, kth) : -1.f;
             const float4 tc4 = tnext;
             if (t + 1 < ntile) {
                 tnext = p.tilec[(t_begin + t + 1) * 2 + h];
-                if (et < TC_BN) {
-                    const int64_t r = row0 + TC_BN + et;
-                    pre = r < p.N ? p.rowc[r] : inf4;
-                }
+                const int64_t r = row0 + TC_BN + h * 64 + 2 * lane;
+                pre0 = r < p.N ? p.rowc[r] : inf4;
+                pre1 = r + 1 < p.N ? p.rowc[r + 1] : inf4;
             }
             if (qvalid) gnext = __uint_as_float(*(volatile unsigned int *)gb);
             mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
+            if (p.skip_epi == 1) {
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                mbar_arrive(&t_empty[s]);
+                continue;
+            }
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
-            const float4 *rows = s_row + s * TC_BN + h * 64;
+            const float4 *rows = wrow + s * 64;
             // tile-level necessary conditions on the dot product s:
             //   lb_r <= bound  =>  s >= s_lo ;   ub_r < kth  =>  s > s_need
             const float base_lo = alpha_l + tc4.x - qnm * tc4.y;
@@ -349,27 +360,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 float mx = __uint_as_float(v[0]);
 #pragma unroll
                 for (int i = 1; i < 16; i++) mx = fmaxf(mx, __uint_as_float(v[i]));
+                if (p.skip_epi == 2) {  // diagnostics: TMEM loads + max only
+                    if (mx == -12345.f) atomicAdd(p.cand_n, 1u);
+                    continue;
+                }
                 // lowered by a relative 1e-5 so float32 rounding can only make the
-                // fast path take the precise per-row test more often, never less
+                // fast path take the precise per-row test more often, never less.
+                // Only rows whose upper bound beats the CURRENT effective bound
+                // (min of the shared bound and this thread's k-th) are inserted:
+                // rows between the two could never tighten what is used.
                 float s_lo = (base_lo - bound) * inv2f;
                 s_lo -= 1e-5f * (fabsf(s_lo) + 1.f);
                 float s_need = __int_as_float(0x7f800000);
                 if (tighten) {
-                    s_need = (base_need - kth) * inv2g;
+                    s_need = (base_need - bound) * inv2g;
                     s_need -= 1e-5f * (fabsf(s_need) + 1.f);
                 }
                 uint32_t emit = 0;
                 if (mx >= fminf(s_lo, s_need)) {
+                    const float thr_s = fminf(s_lo, s_need);
+                    uint32_t work = 0;
 #pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const float sd = __uint_as_float(v[i]);
+                    for (int i = 0; i < 16; i++) work |= (__uint_as_float(v[i]) >= thr_s ? 1u : 0u) << i;
+                    while (work) {
+                        const int i = __ffs(work) - 1;
+                        work &= work - 1;
+                        float sd = 0.f;
+#pragma unroll
+                        for (int u = 0; u < 16; u++)
+                            if (u == i) sd = __uint_as_float(v[u]);
                         const float4 rc = rows[c0 + i];
                         const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
                         emit |= (lb <= bound ? 1u : 0u) << i;
                         if constexpr (tighten) {
-                            if (lb < kth) {  // ub >= lb: only then can ub improve the k-th bound
+                            if (lb < bound) {  // ub >= lb: only then can ub tighten the bound
                                 const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
-                                if (ub < kth) {
+                                if (ub < bound && ub < kth) {
                                     float x = ub;
 #pragma unroll
                                     for (int j = 0; j < KTOP; j++) {
@@ -422,8 +448,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
             }
             // publish this thread's bound for the other CTAs of the query block
-            if (qvalid && tighten && kth < __uint_as_float(*(volatile unsigned int *)gb))
-                atomicMin(gb, __float_as_uint(kth));
+            if (qvalid && tighten && kth < gcur) atomicMin(gb, __float_as_uint(kth));
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&t_empty[s]);
         }
@@ -581,8 +606,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.nq = nq;
     const int QB = (nq + TC_BM - 1) / TC_BM;
     // cluster: up to 8 query blocks share every B tile through TMA multicast
+    int csmax = 2;
+    if (const char *e = getenv("SSB_TC_CSMAX")) csmax = std::max(1, std::min(8, atoi(e)));  // diagnostics
     int CS = 1;
-    while (CS < QB && CS < 8) CS <<= 1;
+    while (CS < QB && CS < csmax) CS <<= 1;
     const int groups = (QB + CS - 1) / CS;
     p.QB = groups * CS;  // padded; blocks past nq are all-invalid queries
     p.CS = CS;
@@ -611,7 +638,11 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.cand_n = cand_n;
     p.cand_cap = cand_cap;
     p.dump = dump;
-    const int smem = 1024 + (p.KB + TC_NSLOT) * TC_BM * 128 + 8 * (6 + 2 * TC_NSLOT) + 2 * TC_BN * 16 +
+    {
+        const char *d = getenv("SSB_TC_DIAG");
+        p.skip_epi = d ? atoi(d) : 0;
+    }
+    const int smem = 1024 + (p.KB + TC_NSLOT) * TC_BM * 128 + 8 * (6 + 2 * TC_NSLOT) + 8 * 2 * 64 * 16 +
                      8 * TC_STAGE * 8;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
@@ -623,7 +654,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)CS;
+        attr[0].val.clusterDim.x = (unsigned)p.CS;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
