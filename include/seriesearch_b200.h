@@ -156,7 +156,12 @@ typedef struct {
      * filter + exact rescoring) instead of LB_SAX + sparse exact scan
      * (query.py:321-325).  Answers do not depend on it. */
     float eapca_th;
-    int32_t route; /* 0 auto (eapca_th rule), 1 LB_SAX path only, 2 tensor-core path only */
+    /* 0 auto: per query, the cheaper exact path by a B200-calibrated cost model
+     *   (tensor-core filter over N rows vs LB_SAX over the rows of the leaves the
+     *   seed bound keeps; the seed itself is skipped when the dense filter is
+     *   cheaper than it); 1 LB_SAX path only; 2 tensor-core path only;
+     * 3 the reference's eapca_th rule. */
+    int32_t route;
 } ssb_query_cfg;
 
 int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, const ssb_query_cfg *cfg,

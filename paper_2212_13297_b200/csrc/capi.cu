@@ -341,7 +341,8 @@ int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, const ss
     QueryCfg qc;
     if (cfg) {
         SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
-        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 2, "route must be 0 (auto), 1 (tree) or 2 (tensor core)");
+        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
+                    "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
         qc.eapca_th = cfg->eapca_th;
         qc.route = cfg->route;
     }

@@ -179,6 +179,7 @@ __global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const
 // a row is never dropped that the exact LB_SAX would keep.  Each thread
 // evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
 constexpr int LBS_ROWS = 4;
+constexpr int TC_KTOP_MAX = 32;  // tc.cu TC_KTOP
 constexpr int LBS_STAGE = 1024;
 
 __global__ void __launch_bounds__(256)
@@ -417,24 +418,58 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 // host: entry list -> tile list -> sparse scan -> select (with tightening)
 
 // routing (query.py:321-325): leaves each query keeps under its seed bound
+// Cost model of the two exact paths (B200-measured, per row per query, in units
+// of one tensor-core filter row): LB_SAX filtering of a
+// candidate-leaf row costs ~14 units, an exact float32 pair ~190.  The dense
+// filter costs N units per query.
+constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 190.0;
+
+// routing: leaves (and their rows) each query keeps under its seed bound.
+// mode 0 auto (cost model), 1 tree, 2 tensor, 3 the reference's eapca_th rule
+// (query.py:321-325: eapca_pr < eapca_th -> "scan").
 __global__ void route_kernel(const double *__restrict__ lbe, int L, const uint64_t *__restrict__ thr, double slack_abs,
-                             const uint32_t *__restrict__ leaf_count, float eapca_th, int mode,
+                             const uint32_t *__restrict__ leaf_count, float eapca_th, int mode, int64_t N,
                              uint32_t *__restrict__ cand_leaves, int32_t *__restrict__ use_tc)
 {
     const int q = blockIdx.x;
     const double bound = keep_bound(thr[q], slack_abs);
     uint32_t c = 0;
-    for (int l = threadIdx.x; l < L; l += blockDim.x) c += (leaf_count[l] && lbe[(int64_t)q * L + l] <= bound) ? 1u : 0u;
-    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    unsigned long long rows = 0;
+    for (int l = threadIdx.x; l < L; l += blockDim.x)
+        if (leaf_count[l] && lbe[(int64_t)q * L + l] <= bound) {
+            c++;
+            rows += leaf_count[l];
+        }
+    for (int off = 16; off; off >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, off);
+        rows += __shfl_xor_sync(0xffffffffu, rows, off);
+    }
     __shared__ uint32_t part[32];
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __shared__ unsigned long long prow[32];
+    if ((threadIdx.x & 31) == 0) {
+        part[threadIdx.x >> 5] = c;
+        prow[threadIdx.x >> 5] = rows;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+        unsigned long long rt = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            t += part[w];
+            rt += prow[w];
+        }
         cand_leaves[q] = t;
         const double eapca_pr = 1.0 - (double)t / (double)(L > 0 ? L : 1);
-        use_tc[q] = mode == 2 ? 1 : (mode == 1 ? 0 : (eapca_pr < (double)eapca_th ? 1 : 0));
+        int tc;
+        if (mode == 2)
+            tc = 1;
+        else if (mode == 1)
+            tc = 0;
+        else if (mode == 3)
+            tc = eapca_pr < (double)eapca_th ? 1 : 0;
+        else
+            tc = (double)rt * COST_LBS_ROW > (double)N * COST_TC_ROW ? 1 : 0;
+        use_tc[q] = tc;
     }
 }
 
@@ -570,11 +605,18 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     SSB_CUDA(emask.alloc(4 * (size_t)entry_cap, s));
 
     // ---- phase A: exact scan of each query's best leaf -> bound ------------------
-    // jobs: (leaf row chunk) x (<= 32 queries whose best leaf it is)
+    // jobs: (leaf row chunk) x (<= 32 queries whose best leaf it is).
+    // Skipped when every query goes to the tensor-core filter anyway: forced,
+    // or (auto) when the dense filter over all N rows costs less than the seed
+    // scan alone (the filter derives its own bound from its upper bounds).
     EntryOut eo{ekey.as<uint64_t>(), emask.as<uint32_t>(), ecount.as<uint32_t>(), entry_cap};
     SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
-    {
+    const double avg_leaf = (double)ix.N / (double)std::max(1, L);
+    const bool tc_all = ix.Xb && k <= TC_KTOP_MAX &&
+                        (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    if (tc_all) SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
+    if (!tc_all) {
         std::vector<int32_t> hbest(B);
         SSB_CUDA(cudaMemcpyAsync(hbest.data(), best.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
@@ -623,8 +665,11 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     // the tensor-core filter; the others to LB_SAX + sparse exact scan.
     DevBuf use_tc;
     SSB_CUDA(use_tc.alloc(4 * (size_t)B, s));
+    int mode = ix.Xb ? qc.route : 1;
+    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;  // the filter only tightens its own bound for k <= 32
+    if (tc_all) mode = 2;
     route_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, thr.as<uint64_t>(), slack_abs, ix.leaf_count, qc.eapca_th,
-                                   (ix.Xb && qc.route != 1) ? qc.route : 1, st_cand_leaves, use_tc.as<int32_t>());
+                                   mode, ix.N, st_cand_leaves, use_tc.as<int32_t>());
     SSB_CHECK_LAUNCH();
     std::vector<int32_t> h_tc(B);
     SSB_CUDA(cudaMemcpyAsync(h_tc.data(), use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));

@@ -141,14 +141,15 @@ class QueryEngine:
     def close(self) -> None:
         pass
 
-    ROUTES = {"auto": 0, "tree": 1, "tensor": 2}
+    ROUTES = {"auto": 0, "tree": 1, "tensor": 2, "eapca": 3}
 
     def knn_device(self, Q, k: int, want_stats: bool = False, eapca_th: float = 0.25,
                    route: str = "auto"):
         """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,4) u32].
 
-        ``route``: "auto" applies the reference's eapca_th rule per query
-        (weak envelope pruning -> tensor-core scan path, else LB_SAX path);
+        ``route``: "auto" picks, per query, the cheaper exact path by a
+        B200-calibrated cost model; "eapca" applies the
+        reference's eapca_th rule (weak envelope pruning -> dense scan path);
         "tree" / "tensor" force one path.  Answers are identical either way."""
         from . import _lib
         from ._device import device_f32, ptr, require_cuda, stream_handle

@@ -80,3 +80,18 @@ def test_tensor_route_ties(ssb, oracle):
     idx = ssb.build_index_array(X, s)
     d2, ids, _ = ssb.QueryEngine(idx).knn_device(X[[17]], 3, route="tensor")
     assert list(ids.cpu().numpy()[0]) == [17, 4000, 4999]
+
+
+@pytest.mark.parametrize("route", ["auto", "eapca", "tree", "tensor"])
+def test_every_route_is_exact(ssb, oracle, route):
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(12_000, 256, 0, workers=4)
+    s = ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=500)
+    idx = ssb.build_index_array(X, s)
+    Q = np.concatenate([G.noise_queries(X, 30, 1.0, 1), G.noise_queries(X, 30, 0.01, 1)])
+    for k in (1, 5, 40):
+        d2, ids, _ = ssb.QueryEngine(idx).knn_device(Q, k, route=route)
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid), (route, k)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2)), (route, k)
