@@ -615,8 +615,9 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.CS = CS;
     p.tiles = (N + TC_BN - 1) / TC_BN;
     const int sms = num_sms();
+    // >= 16 tiles per CTA so each thread's running k-th bound tightens early
     int clusters_per_group = std::max(1, sms / CS / groups);
-    clusters_per_group = (int)std::min<int64_t>(clusters_per_group, p.tiles);
+    clusters_per_group = (int)std::max<int64_t>(1, std::min<int64_t>(clusters_per_group, p.tiles / 16));
     p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
     CUtensorMap mA, mB;

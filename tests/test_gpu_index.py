@@ -151,12 +151,13 @@ def test_query_c2_shape_small(ssb, oracle, sigma, k):
     idx = build(ssb, X, 1000)
     Q = G.noise_queries(X, 64, sigma, 1)
     eng = ssb.QueryEngine(idx)
-    d2, ids, pos, st = eng.knn_device(Q, k, want_stats=True)
     od2, oid = oracle.knn_scan(X, Q, k, threads=8)
-    assert np.array_equal(ids.cpu().numpy(), oid)
-    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
-    if sigma <= 0.1:   # pruning must actually prune on easy queries
-        assert st[:, 1].mean() < 0.2 * len(X)
+    for route in ("tree", "auto"):
+        d2, ids, pos, st = eng.knn_device(Q, k, want_stats=True, route=route)
+        assert np.array_equal(ids.cpu().numpy(), oid), route
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2)), route
+        if sigma <= 0.1:   # the filters must actually filter on easy queries
+            assert st[:, 1].mean() < 0.2 * len(X), route
 
 
 def test_query_ties_and_duplicates(ssb, oracle):
