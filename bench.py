@@ -351,13 +351,21 @@ def main():
     top = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
     roof = None
     if top:
-        name, (kms, klaunch, kbytes) = top
-        achieved = (kbytes / klaunch) / ((kms / klaunch) / 1000.0) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": round(achieved, 1),
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                "traffic": None, "share_of_step": round(kms / ms, 4),
-                "avg_launch_ms": round(kms / klaunch, 4),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+        name, (kms, klaunch, kbytes, kflops) = top
+        avg_s = (kms / klaunch) / 1000.0
+        if kflops > 0:  # tensor-core kernel: FLOPs against the measured bf16 peak
+            tf_peak = float(peaks.get("bf16_tflops", 1590.0))
+            achieved = (kflops / klaunch) / avg_s / 1e12
+            roof = {"kernel": name, "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_peak,
+                    "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": None,
+                    "hbm_GBps": round((kbytes / klaunch) / avg_s / 1e9, 1),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF"}
+        else:
+            achieved = (kbytes / klaunch) / avg_s / 1e9
+            roof = {"kernel": name, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+        roof.update({"share_of_step": round(kms / ms, 4), "avg_launch_ms": round(kms / klaunch, 4)})
     cb = None
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(X, Qs, args.cpu_sample)
@@ -373,8 +381,8 @@ def main():
                    "engine": engine.name, "shards": world,
                    "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (X.nbytes / 1e9)},
         "roofline": roof,
-        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3)}
-                    for k, v in prof.items()},
+        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3),
+                        "TFLOP": round(v[3] / 1e12, 3)} for k, v in prof.items()},
         "cpu_baseline": cb,
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

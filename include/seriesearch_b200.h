@@ -48,13 +48,13 @@ int64_t ssb_launch_count(void);
 /* 1 if a CUDA device is visible and the sm_100a image loads on it */
 int32_t ssb_device_ok(void);
 
-/* per-kernel device time (CUDA events on the launching stream) and
- * algorithmic bytes, aggregated by kernel name.  ssb_prof_read enumerates
+/* per-kernel device time (CUDA events on the launching stream), algorithmic
+ * bytes and algorithmic FLOPs (tensor-core kernels), aggregated by kernel name.  ssb_prof_read enumerates
  * kernels by idx (returns 1 past the end) and synchronizes the events. */
 void ssb_prof_enable(int32_t on);
 void ssb_prof_reset(void);
 int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, int64_t *launches,
-                  double *bytes_total);
+                  double *bytes_total, double *flops_total);
 
 /* ---- K-sum: summarisation ----------------------------------------------- */
 

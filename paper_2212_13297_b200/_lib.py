@@ -32,7 +32,8 @@ _SIGS = {
     "ssb_prof_enable": [I32],
     "ssb_prof_reset": [],
     "ssb_prof_read": [I32, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_double),
-                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)],
+                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                      ctypes.POINTER(ctypes.c_double)],
     "ssb_words": [P, I64, I32, P, P, P, P],
     "ssb_segment_stats": [P, I64, I32, P, P, I32, P, P, P],
     "ssb_bruteforce_knn": [P, I64, I32, P, I32, I32, I64, P, P, P],
@@ -137,15 +138,16 @@ def prof_reset() -> None:
 
 
 def prof_read() -> dict:
-    """{kernel: (ms_total, launches, algorithmic_bytes_total)} (synchronizes)."""
+    """{kernel: (ms_total, launches, algorithmic_bytes_total, algorithmic_flops_total)}."""
     lib = load()
     out = {}
     i = 0
     buf = ctypes.create_string_buffer(64)
     while True:
-        ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
-        if lib.ssb_prof_read(i, buf, 64, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)) != 0:
+        ms, n, b, f = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        if lib.ssb_prof_read(i, buf, 64, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b),
+                             ctypes.byref(f)) != 0:
             break
-        out[buf.value.decode()] = (ms.value, n.value, b.value)
+        out[buf.value.decode()] = (ms.value, n.value, b.value, f.value)
         i += 1
     return out

@@ -17,7 +17,7 @@ namespace ssb {
 struct ProfRec {
     const char *name;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, flops;
     int slot;  // >= 0: device-side byte counter slot added to `bytes`
 };
 
@@ -42,7 +42,8 @@ static cudaEvent_t take_event()
     return e;
 }
 
-ProfScope::ProfScope(const char *name, cudaStream_t s, double bytes) : name_(name), s_(s), bytes_(bytes)
+ProfScope::ProfScope(const char *name, cudaStream_t s, double bytes, double flops)
+    : name_(name), s_(s), bytes_(bytes), flops_(flops)
 {
     std::lock_guard<std::mutex> g(g_mu);
     if (!g_on) return;
@@ -69,7 +70,7 @@ ProfScope::~ProfScope()
     if (!a_) return;
     cudaEventRecord((cudaEvent_t)b_, s_);
     std::lock_guard<std::mutex> g(g_mu);
-    g_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_, bytes_, slot_});
+    g_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_, bytes_, flops_, slot_});
 }
 
 }  // namespace ssb
@@ -98,10 +99,11 @@ void ssb_prof_reset(void)
 }
 
 int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, int64_t *launches,
-                  double *bytes_total)
+                  double *bytes_total, double *flops_total)
 {
     std::lock_guard<std::mutex> g(g_mu);
     std::map<std::string, std::pair<double, std::pair<int64_t, double>>> agg;
+    std::map<std::string, double> aflops;
     std::vector<unsigned long long> slots(g_next_slot);
     for (auto &r : g_recs) cudaEventSynchronize(r.b);
     if (g_next_slot)
@@ -113,6 +115,7 @@ int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, i
         e.first += ms;
         e.second.first += 1;
         e.second.second += r.bytes + (r.slot >= 0 ? (double)slots[r.slot] : 0.0);
+        aflops[r.name] += r.flops;
     }
     int i = 0;
     for (auto &kv : agg) {
@@ -122,6 +125,7 @@ int ssb_prof_read(int32_t idx, char *name, int32_t name_cap, double *ms_total, i
         *ms_total = kv.second.first;
         *launches = kv.second.second.first;
         *bytes_total = kv.second.second.second;
+        if (flops_total) *flops_total = aflops[kv.first];
         return 0;
     }
     return 1;

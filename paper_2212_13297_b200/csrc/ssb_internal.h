@@ -79,7 +79,7 @@ struct DevBuf {
 // `bytes` = algorithmic bytes of the launch (DESIGN.md per-kernel formulas).
 class ProfScope {
   public:
-    ProfScope(const char *name, cudaStream_t s, double bytes);
+    ProfScope(const char *name, cudaStream_t s, double bytes, double flops = 0.0);
     ~ProfScope();
     // device counter the kernel may atomicAdd its algorithmic bytes into
     // (nullptr when profiling is off); read back by ssb_prof_read
@@ -88,7 +88,7 @@ class ProfScope {
   private:
     const char *name_;
     cudaStream_t s_;
-    double bytes_;
+    double bytes_, flops_;
     void *a_ = nullptr, *b_ = nullptr;
     int slot_ = -1;
 };

@@ -661,7 +661,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
-        ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2);
+        ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
+                     2.0 * (double)nq * (double)N * (double)(p.KB * 64));
         SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mA, mB, p));
         return OK;
     };
