@@ -36,7 +36,7 @@ KS = (1, 10)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--rows", type=int, default=1_000_000)
@@ -78,7 +78,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -140,7 +140,8 @@ class IndexEngine:
     """The product path: level-synchronous GPU build, then batched pruned
     exact queries (K-lbe -> K-lbs -> sparse K-scan -> K-select)."""
 
-    name = "index (K-lbe + K-lbs + sparse K-scan + K-select)"
+    name = ("index: K-lbe seed/route, then per query K-tc tensor-core filter + exact rescoring "
+            "or K-lbs + sparse K-scan (auto cost model); K-select")
 
     def __init__(self, X_dev, tau: int, id_base: int = 0):
         import torch
