@@ -27,6 +27,8 @@
 #include <chrono>
 #include <cmath>
 #include <cub/device/device_scan.cuh>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -564,6 +566,13 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     const int s0 = std::max(1, cfg.initial_segments);
     SSB_REQUIRE(s0 <= mmax && s0 <= n, "initial_segments must be in [1, min(n, max_segments)]");
     auto t_start = std::chrono::steady_clock::now();
+    const bool trace = getenv("SSB_BUILD_TRACE") != nullptr;
+    auto lap = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[ssb build] %-28s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
 
     std::unique_ptr<Index> ix(new Index());
     ix->N = N;
@@ -594,6 +603,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
 
     std::vector<int32_t> frontier = {0};  // nodes needing stats this level
     int level = 0;
+    lap("init");
     while (!frontier.empty()) {
         // ---- level descriptors ------------------------------------------------
         const int F = (int)frontier.size();
@@ -874,10 +884,12 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         }
         frontier.swap(next);
         level++;
+        lap("level");
         SSB_REQUIRE(level < 4096, "index build did not converge");
     }
     ix->levels = level;
     RC(finalize_tree(*ix, s));
+    lap("finalize_tree");
     SSB_CUDA(cudaMalloc(&ix->X, (size_t)N * n * 4));
     SSB_CUDA(cudaMalloc(&ix->words, (size_t)N * WORD_SEGMENTS));
     SSB_CUDA(cudaMalloc(&ix->orig, (size_t)N * 4));
@@ -891,8 +903,11 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     }
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
+    lap("allocs+gather");
     RC(launch_words(X, N, n, ix->bp, ix->words, nullptr, s, perm));
+    lap("words");
     RC(make_tc_operands(*ix, s));
+    lap("tc operands");
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));

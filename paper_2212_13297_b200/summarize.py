@@ -23,10 +23,18 @@ _bp_cache: dict = {}
 
 
 def normal_breakpoints(alphabet_size: int = 256) -> np.ndarray:
-    """Standard-normal quantiles at i/a, i = 1..a-1 (summarize.py:107-114)."""
+    """Standard-normal quantiles at i/a, i = 1..a-1 (summarize.py:107-114).
+
+    The 256-symbol table (the only alphabet the index uses, persist.py:84) is
+    shipped pre-computed (_breakpoints.py, checked against scipy in the tests);
+    other alphabets go through scipy like the reference."""
     if alphabet_size not in SUPPORTED_ALPHABETS:
         raise UsageError(
             f"alphabet size must be a power of two in [2, 256], got {alphabet_size}")
+    if alphabet_size == 256:
+        from ._breakpoints import BREAKPOINTS_256_HEX
+
+        return np.array([float.fromhex(h) for h in BREAKPOINTS_256_HEX], dtype=np.float64)
     from scipy.stats import norm
 
     return norm.ppf(np.arange(1, alphabet_size) / alphabet_size)
