@@ -1,15 +1,18 @@
 """bench.py -- exact k-NN data-series search on B200.
 
-Default workload = BASELINE.json configs[1] ("C2"): 1M random-walk series x 256
+Default workload = BASELINE.json configs[1] ("c2"): 1M random-walk series x 256
 (float32, z-normalised, reference generator recipe, seed 0); 1000 noisy queries
 per sigma in {0.01, 0.1, 1.0} (seed 1); k in {1, 10}.  One step answers the
 whole workload (3 sigmas x 2 k x 1000 queries = 6000 exact k-NN answers).
+Other BASELINE.json configs: --workload c1 | c3 | c4 | c5 (explicit runs).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2]
 
-Multi-GPU (torchrun, one rank per GPU): the dataset is row-sharded, every rank
-answers every query over its shard, and per-shard top-k lists are merged with
-one NCCL all-gather (strong scaling: the dataset is fixed).
+Multi-GPU (torchrun, one rank per GPU): the dataset is row-sharded (each rank
+generates and indexes only its shard), every rank answers every query over its
+shard, and the per-shard top-k lists are merged with one NCCL all-gather and
+the K-merge kernel (strong scaling: the dataset is fixed).
 Prints ONE JSON line on rank 0.
 """
 
@@ -24,13 +27,62 @@ import sys
 import threading
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SIGMAS = (0.01, 0.1, 1.0)
-KS = (1, 10)
+
+# --------------------------------------------------------------------------
+# workloads (BASELINE.json configs)
+
+class Workload:
+    """A dataset (generated per shard) plus query cells answered every step."""
+
+    def __init__(self, name, desc, N, n, tau, cells, data_fn, batch=None):
+        self.name, self.desc, self.N, self.n, self.tau = name, desc, N, n, tau
+        self.cells = cells          # [(label, queries_fn, k)]
+        self.data_fn = data_fn      # (lo, hi) -> rows [lo, hi)
+        self.batch = batch          # queries per launch (None = the whole cell)
+
+
+def make_workload(name: str, args) -> Workload:
+    from paper_2212_13297_b200 import generate as G
+
+    nq = args.queries
+    if name == "c1":
+        N, n = args.rows or 100_000, 256
+        cells = [("random-walk queries, seed 1", lambda: G.random_walks(100, n, 1, workers=1), 1)]
+        return Workload("c1", f"C1: {N} x {n} random walks (seed 0), 100 random-walk queries "
+                              f"(seed 1), k=1, tau={args.tau or 1000}", N, n, args.tau or 1000, cells,
+                        lambda lo, hi: G.random_walks(hi - lo, n, 0, start=lo))
+    if name == "c2":
+        N, n = args.rows or 1_000_000, 256
+        cells = [(f"sigma={s} k={k}", (lambda s=s: G.noise_queries_stream(N, n, nq, s, 1)), k)
+                 for s in (0.01, 0.1, 1.0) for k in (1, 10)]
+        return Workload("c2", f"C2: {N} x {n} random walks, {nq} noisy queries per sigma in "
+                              f"[0.01, 0.1, 1.0], k in [1, 10] ({6 * nq} answers per step), "
+                              f"tau={args.tau or 10_000}", N, n, args.tau or 10_000, cells,
+                        lambda lo, hi: G.random_walks(hi - lo, n, 0, start=lo))
+    if name == "c3":
+        N, n = args.rows or 10_000_000, 96
+        cells = [("unit-Gaussian queries seed 3", lambda: G.unit_gaussian_rows(0, nq, n, 3), 10)]
+        return Workload("c3", f"C3: {N} x {n} unit-norm Gaussian vectors (seed 2), {nq} queries "
+                              f"(seed 3), k=10, 256 queries per launch", N, n, args.tau or 10_000,
+                        cells, lambda lo, hi: G.unit_gaussian_rows(lo, hi, n, 2), batch=256)
+    if name == "c4":
+        N, n = args.rows or 25_000_000, 256
+        cells = [("sigma=0.1 k=100", lambda: G.noise_queries_stream(N, n, nq, 0.1, 1), 100)]
+        return Workload("c4", f"C4: {N} x {n} random walks, {nq} noisy queries sigma=0.1, k=100, "
+                              f"tau={args.tau or 10_000}", N, n, args.tau or 10_000, cells,
+                        lambda lo, hi: G.random_walks(hi - lo, n, 0, start=lo))
+    if name == "c5":
+        N, n = args.rows or 50_000_000, 256
+        cells = [(f"sigma={s} k=10", (lambda s=s: G.noise_queries_stream(N, n, nq, s, 1)), 10)
+                 for s in (0.01, 1.0)]
+        return Workload("c5", f"C5: {N} x {n} random walks, build tau={args.tau or 100_000}, then "
+                              f"{nq} queries k=10 at sigma in [0.01, 1.0]", N, n,
+                        args.tau or 100_000, cells,
+                        lambda lo, hi: G.random_walks(hi - lo, n, 0, start=lo))
+    raise SystemExit(f"unknown workload {name}")
 
 
 def parse():
@@ -39,26 +91,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--rows", type=int, default=1_000_000)
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--workload", default="c2", choices=("c1", "c2", "c3", "c4", "c5"))
+    ap.add_argument("--rows", type=int, default=0, help="override the dataset size")
     ap.add_argument("--queries", type=int, default=1000)
-    ap.add_argument("--tau", type=int, default=10_000)
+    ap.add_argument("--tau", type=int, default=0, help="override the leaf threshold")
+    ap.add_argument("--route", default="auto", choices=("auto", "tree", "tensor", "eapca"))
     ap.add_argument("--engine", default="index", choices=("index", "bruteforce"))
-    ap.add_argument("--cpu-sample", type=int, default=4, help="queries per (sigma,k) cell "
-                    "for the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=4, help="queries per cell for the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
-
-
-# --------------------------------------------------------------------------
-# data (reference generator recipe)
-
-def make_inputs(rows: int, n: int, queries: int):
-    from paper_2212_13297_b200 import generate as G
-
-    X = G.random_walks(rows, n, 0)
-    Qs = {s: G.noise_queries(X, queries, s, 1) for s in SIGMAS}
-    return X, Qs
 
 
 # --------------------------------------------------------------------------
@@ -121,29 +162,36 @@ class Clocks:
 # engines
 
 class BruteForceEngine:
-    """Full exact scan (K-scan dense + K-select) -- the reference's own
-    exactness path (pscan.py:23-30 / 33-135) on the device."""
+    """Full exact scan (K-scan dense + K-select): pscan.py:23-135 on the device."""
 
     name = "bruteforce (K-scan dense + K-select)"
 
-    def __init__(self, X_dev, id_base: int = 0):
+    def __init__(self, X_dev, id_base: int = 0, **_):
         self.X = X_dev
         self.id_base = id_base
+
+    def build_info(self, N):
+        return None
 
     def query(self, Q_dev, k):
         from paper_2212_13297_b200 import knn_batch
 
         return knn_batch(self.X, Q_dev, k, id_base=self.id_base)
 
+    def query_host(self, Q_host, k):
+        d2, ids = self.query(Q_host, k)
+        return d2.cpu().numpy(), ids.cpu().numpy()
+
 
 class IndexEngine:
-    """The product path: level-synchronous GPU build, then batched pruned
-    exact queries (K-lbe -> K-lbs -> sparse K-scan -> K-select)."""
+    """The product path: level-synchronous GPU build, then batched exact
+    queries routed per query (auto cost model) between the K-tc tensor-core
+    filter + exact rescoring and K-lbe/K-lbs + sparse K-scan; K-select."""
 
-    name = ("index: K-lbe seed/route, then per query K-tc tensor-core filter + exact rescoring "
-            "or K-lbs + sparse K-scan (auto cost model); K-select")
+    name = ("index: K-lbe, then per query K-tc tensor-core filter + exact rescoring "
+            "or K-lbs + sparse K-scan (route={route}); K-select")
 
-    def __init__(self, X_dev, tau: int, id_base: int = 0):
+    def __init__(self, X_dev, tau: int, id_base: int = 0, route: str = "auto"):
         import torch
 
         from paper_2212_13297_b200 import IndexSettings, QueryEngine, build_index_array
@@ -159,7 +207,8 @@ class IndexEngine:
         self.build_wall_s = time.perf_counter() - t0
         self.build_dev_ms = ev0.elapsed_time(ev1)
         self.engine = QueryEngine(self.index)
-        self.id_base = id_base
+        self.route = route
+        self.name = IndexEngine.name.format(route=route)
 
     def build_info(self, N):
         info = self.index.info
@@ -168,14 +217,15 @@ class IndexEngine:
                 "nodes": info.num_nodes, "levels": info.levels, "depth": info.depth}
 
     def query(self, Q_dev, k):
-        d2, ids, _ = self.engine.knn_device(Q_dev, k)
+        d2, ids, _ = self.engine.knn_device(Q_dev, k, route=self.route)
         return d2, ids
 
     def query_host(self, Q_host, k):
-        return self.engine.exact_knn_arrays(Q_host, k)
+        d2, ids, _ = self.engine.knn_device(Q_host, k, route=self.route)
+        return d2.cpu().numpy(), ids.cpu().numpy()
 
 
-def merge_shards(d2, ids, k, world):
+def merge_shards(d2, ids, k):
     """One NCCL all-gather of every rank's top-k keys + the K-merge kernel."""
     from paper_2212_13297_b200.distributed import merge_topk
 
@@ -185,34 +235,35 @@ def merge_shards(d2, ids, k, world):
 # --------------------------------------------------------------------------
 # reference arm: the oracle port timed on host cores
 
-def cpu_baseline(X, Qs, sample: int):
+def cpu_baseline(wl: Workload, X, cellq, sample: int):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     nq = 0
-    for s in SIGMAS:
-        for k in KS:
-            oracle.knn_scan(X, Qs[s][:sample], k, threads=threads)
-            nq += sample
+    for (_, _, k), Q in zip(wl.cells, cellq):
+        oracle.knn_scan(X, Q[:sample], k, threads=threads)
+        nq += min(sample, len(Q))
     dt = time.perf_counter() - t0
     return {"value": nq / dt, "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"{nq} queries ({sample} per sigma x k cell) of the C2 workload through the "
-                      f"C oracle's exact scan (pscan.py:23-135 restated, {threads} threads)",
+            "sample": f"{nq} queries ({sample} per cell) of workload {wl.name} through the C "
+                      f"oracle's exact scan (pscan.py:23-135 restated, {threads} threads)",
             "seconds": dt}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    X, Qs = make_inputs(args.rows, args.n, args.queries)
+    wl = make_workload(args.workload, args)
+    X = wl.data_fn(0, wl.N)
+    cellq = [fn() for _, fn, _ in wl.cells]
     for _ in range(args.warmup):
-        cpu_baseline(X, Qs, 1)
+        cpu_baseline(wl, X, cellq, 1)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline(X, Qs, args.cpu_sample))
+        vals.append(cpu_baseline(wl, X, cellq, args.cpu_sample))
     total = time.perf_counter() - t0
     nq = sum(v["value"] * v["seconds"] for v in vals)
     value = nq / sum(v["seconds"] for v in vals)
@@ -224,9 +275,8 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator recipe)",
-        "config": {"workload": f"C2: {args.rows} x {args.n} random walks, {args.queries} queries per "
-                               f"sigma in {list(SIGMAS)}, k in {list(KS)}; each step is a bounded "
-                               f"sample of {args.cpu_sample} queries per cell"},
+        "config": {"workload": wl.desc + f"; each step is a bounded sample of {args.cpu_sample} "
+                                         "queries per cell"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -252,28 +302,36 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2212_13297_b200 import _lib
+    from paper_2212_13297_b200.distributed import shard_range
 
-    X, Qs = make_inputs(args.rows, args.n, args.queries)
-    N = X.shape[0]
-    lo = rank * N // world
-    hi = (rank + 1) * N // world
-    X_dev = torch.from_numpy(X[lo:hi]).cuda()
-    Q_dev = {s: torch.from_numpy(Qs[s]).cuda() for s in SIGMAS}
+    wl = make_workload(args.workload, args)
+    N = wl.N
+    lo, hi = shard_range(N, rank, world)
+    t_gen = time.perf_counter()
+    X = wl.data_fn(lo, hi)
+    cellq = [fn() for _, fn, _ in wl.cells]
+    t_gen = time.perf_counter() - t_gen
+    X_dev = torch.from_numpy(X).cuda()
+    Q_dev = [torch.from_numpy(Q).cuda() for Q in cellq]
     if args.engine == "index":
-        engine = IndexEngine(X_dev, args.tau, id_base=lo)
+        engine = IndexEngine(X_dev, wl.tau, id_base=lo, route=args.route)
     else:
         engine = BruteForceEngine(X_dev, id_base=lo)
+    batch = wl.batch
+
+    def answer(Q, k, host=False):
+        chunks = [Q] if not batch else [Q[i:i + batch] for i in range(0, len(Q), batch)]
+        out = []
+        for c in chunks:
+            if host:
+                out.append(engine.query_host(c, k))
+            else:
+                d2, ids = engine.query(c, k)
+                out.append(merge_shards(d2, ids, k) if world > 1 else ids)
+        return out
 
     def step():
-        outs = []
-        for s in SIGMAS:
-            for k in KS:
-                d2, ids = engine.query(Q_dev[s], k)
-                if world > 1:
-                    outs.append(merge_shards(d2, ids, k, world))
-                else:
-                    outs.append(ids)
-        return outs
+        return [answer(Q, k) for (_, _, k), Q in zip(wl.cells, Q_dev)]
 
     def barrier():
         if world > 1:
@@ -306,29 +364,19 @@ def main():
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    answers = len(SIGMAS) * len(KS) * args.queries
+    answers = sum(len(Q) for Q in cellq)
     value = answers * args.steps / (ms / 1000.0)
 
     # ---- e2e: the public API with host buffers, copies inside the region ------
-    from paper_2212_13297_b200 import knn_batch
-
-    Q_host = {s: torch.from_numpy(Qs[s]).pin_memory() for s in SIGMAS}
-    if args.engine == "index":
-        def host_call(Qh, k):
-            return engine.query_host(Qh, k)
-    else:
-        def host_call(Qh, k):
-            d2, ids = knn_batch(X_dev, Qh, k, id_base=lo)
-            return d2.cpu(), ids.cpu()
-    h2d = sum(Q_host[s].numel() * 4 for s in SIGMAS) * len(KS)
-    d2h = sum(args.queries * k * (4 + 8) for k in KS) * len(SIGMAS)
+    Q_host = [torch.from_numpy(Q).pin_memory() for Q in cellq]
+    h2d = sum(Q.numel() * 4 for Q in Q_host)
+    d2h = sum(len(Q) * k * (4 + 8) for (_, _, k), Q in zip(wl.cells, cellq))
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        for s in SIGMAS:
-            for k in KS:
-                host_call(Q_host[s], k)
+        for (_, _, k), Qh in zip(wl.cells, Q_host):
+            answer(Qh, k, host=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -369,18 +417,17 @@ def main():
         roof.update({"share_of_step": round(kms / ms, 4), "avg_launch_ms": round(kms / klaunch, 4)})
     cb = None
     if not args.no_cpu_baseline and world == 1:
-        cb = cpu_baseline(X, Qs, args.cpu_sample)
+        cb = cpu_baseline(wl, X, cellq, args.cpu_sample)
         cb.pop("seconds", None)
     line = {
         "metric": "exact kNN queries/s", "value": round(value, 1), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: reference generator recipe (Philox random walks, seed 0; noisy queries, seed 1)",
-        "config": {"workload": f"C2: {N} x {args.n} random walks, {args.queries} queries per sigma in "
-                               f"{list(SIGMAS)}, k in {list(KS)} ({answers} answers per step)",
-                   "engine": engine.name, "shards": world,
-                   "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (X.nbytes / 1e9)},
+        "data": "synthetic: reference generator recipe (seeded Philox streams; see DESIGN.md Inputs)",
+        "config": {"workload": wl.desc, "engine": engine.name, "shards": world,
+                   "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (N * wl.n * 4 / 1e9),
+                   "data_gen_s": round(t_gen, 1)},
         "roofline": roof,
         "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3),
                         "TFLOP": round(v[3] / 1e12, 3)} for k, v in prof.items()},
@@ -388,7 +435,7 @@ def main():
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "build": engine.build_info(N) if args.engine == "index" else None,
+        "build": engine.build_info(hi - lo),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

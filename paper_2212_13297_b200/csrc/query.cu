@@ -179,7 +179,7 @@ __global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const
 // a row is never dropped that the exact LB_SAX would keep.  Each thread
 // evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
 constexpr int LBS_ROWS = 4;
-constexpr int TC_KTOP_MAX = 32;  // tc.cu TC_KTOP
+constexpr int TC_KTOP_MAX = 128;  // tc.cu TC_KTOP
 constexpr int LBS_STAGE = 1024;
 
 __global__ void __launch_bounds__(256)
@@ -666,7 +666,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     DevBuf use_tc;
     SSB_CUDA(use_tc.alloc(4 * (size_t)B, s));
     int mode = ix.Xb ? qc.route : 1;
-    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;  // the filter only tightens its own bound for k <= 32
+    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;  // the filter only tightens its own bound for k <= 128
     if (tc_all) mode = 2;
     route_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, thr.as<uint64_t>(), slack_abs, ix.leaf_count, qc.eapca_th,
                                    mode, ix.N, st_cand_leaves, use_tc.as<int32_t>());

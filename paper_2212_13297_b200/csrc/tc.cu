@@ -48,7 +48,7 @@ constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
 constexpr int TC_NSLOT = 8;          // B pipeline depth in 16 KB K-chunks
-constexpr int TC_KTOP = 32;  // in-register top-k of upper bounds (k <= 32 tightens)
+constexpr int TC_KTOP = 128;  // in-register top-k of upper bounds (k <= 128 tightens)
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
 // N = 128 (>>3 = 16 at bit 17), M = 128 (>>4 = 8 at bit 24)
@@ -674,6 +674,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         rc = go(tc_filter_kernel<16>);
     else if (k <= 32)
         rc = go(tc_filter_kernel<32>);
+    else if (k <= 128)
+        rc = go(tc_filter_kernel<128>);
     else
         rc = go(tc_filter_kernel<0>);
     if (rc) return rc;

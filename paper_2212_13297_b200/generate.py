@@ -46,20 +46,36 @@ def _rw_chunk(args):
 
 
 def random_walks(count: int, n: int, seed: int, workers: int | None = None,
-                 chunk: int = 8192) -> np.ndarray:
-    """The first ``count`` series of the stream, generated in parallel."""
+                 chunk: int = 8192, start: int = 0) -> np.ndarray:
+    """Series [start, start+count) of the stream, generated in parallel
+    (prefix-stable: any row range equals the same rows of the full dataset)."""
     out = np.empty((count, n), dtype=DTYPE)
-    jobs = [(s, min(chunk, count - s), n, seed) for s in range(0, count, chunk)]
+    jobs = [(start + s, min(chunk, count - s), n, seed) for s in range(0, count, chunk)]
     workers = workers or min(len(jobs), os.cpu_count() or 1)
     if workers <= 1 or len(jobs) == 1:
         for job in jobs:
             s, blk = _rw_chunk(job)
-            out[s : s + len(blk)] = blk
+            out[s - start : s - start + len(blk)] = blk
         return out
     with ProcessPoolExecutor(max_workers=workers) as ex:
         for s, blk in ex.map(_rw_chunk, jobs):
-            out[s : s + len(blk)] = blk
+            out[s - start : s - start + len(blk)] = blk
     return out
+
+
+def noise_queries_stream(total: int, n: int, count: int, sigma: float, seed: int,
+                         data_seed: int = 0) -> np.ndarray:
+    """``noise_queries`` over the random-walk dataset (total, n, data_seed)
+    without materialising it: each query's source row is regenerated from the
+    prefix-stable stream (identical to noise_queries(X, ...))."""
+    queries = np.empty((count, n), dtype=DTYPE)
+    for j in range(count):
+        rng = _series_rng(seed, j)
+        src = int(rng.integers(total))
+        row = random_walk_block(src, 1, n, data_seed)[0]
+        noisy = row.astype(np.float64) + rng.normal(0.0, sigma, n)
+        queries[j] = z_normalize(noisy.astype(DTYPE))
+    return queries
 
 
 def noise_queries(data: np.ndarray, count: int, sigma: float, seed: int) -> np.ndarray:
@@ -73,6 +89,24 @@ def noise_queries(data: np.ndarray, count: int, sigma: float, seed: int) -> np.n
         noisy = data[src].astype(np.float64) + rng.normal(0.0, sigma, n)
         queries[j] = z_normalize(noisy.astype(DTYPE))
     return queries
+
+
+def unit_gaussian_rows(lo: int, hi: int, n: int, seed: int, chunk: int = 65536,
+                       workers: int | None = None) -> np.ndarray:
+    """Rows [lo, hi) of unit_gaussian(total, n, seed) (chunk-aligned generation)."""
+    c0, c1 = lo // chunk, (hi + chunk - 1) // chunk
+    jobs = [(c, chunk, n, seed) for c in range(c0, c1)]
+    out = np.empty(((c1 - c0) * chunk, n), dtype=DTYPE)
+    workers = workers or min(len(jobs), os.cpu_count() or 1)
+    if workers <= 1 or len(jobs) <= 1:
+        for job in jobs:
+            c, blk = _ug_chunk(job)
+            out[(c - c0) * chunk : (c - c0) * chunk + len(blk)] = blk
+    else:
+        with ProcessPoolExecutor(max_workers=workers) as ex:
+            for c, blk in ex.map(_ug_chunk, jobs):
+                out[(c - c0) * chunk : (c - c0) * chunk + len(blk)] = blk
+    return out[lo - c0 * chunk : hi - c0 * chunk]
 
 
 def _ug_chunk(args):

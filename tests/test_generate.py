@@ -39,3 +39,16 @@ def test_unit_gaussian_rows_are_unit():
     x = G.unit_gaussian(1000, 96, 2, chunk=300, workers=1)
     assert np.allclose(np.linalg.norm(x.astype(np.float64), axis=1), 1.0, atol=1e-6)
     assert np.array_equal(x, G.unit_gaussian(1000, 96, 2, chunk=300, workers=2))
+
+
+def test_sharded_generation_matches_full():
+    from paper_2212_13297_b200 import generate as G
+
+    full = G.random_walks(40, 32, 0, workers=1)
+    assert np.array_equal(G.random_walks(15, 32, 0, workers=2, chunk=4, start=20), full[20:35])
+    assert np.array_equal(G.random_walks(15, 32, 0, workers=1, chunk=4, start=20), full[20:35])
+    q1 = G.noise_queries(full, 6, 0.1, 1)
+    q2 = G.noise_queries_stream(40, 32, 6, 0.1, 1, data_seed=0)
+    assert np.array_equal(q1, q2)
+    u = G.unit_gaussian(3000, 16, 2, chunk=500, workers=1)
+    assert np.array_equal(G.unit_gaussian_rows(1234, 2777, 16, 2, chunk=500, workers=2), u[1234:2777])
