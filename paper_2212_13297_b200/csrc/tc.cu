@@ -412,6 +412,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         }
                     }
                 }
+                {   // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
+                    const int64_t left = p.N - (row0 + h * 64 + c0);
+                    if (left < 16) emit &= left > 0 ? ((1u << left) - 1u) : 0u;
+                }
                 if (!__any_sync(0xffffffffu, emit != 0)) continue;
                 // warp-staged emission of (query, row) candidates
                 unsigned cnt = __popc(emit);
