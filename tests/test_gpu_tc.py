@@ -95,3 +95,16 @@ def test_every_route_is_exact(ssb, oracle, route):
         od2, oid = oracle.knn_scan(X, Q, k, threads=8)
         assert np.array_equal(ids.cpu().numpy(), oid), (route, k)
         assert np.array_equal(bits(d2.cpu().numpy()), bits(od2)), (route, k)
+
+
+@pytest.mark.parametrize("N,k", [(70, 100), (70, 20), (200, 100), (130, 1)])
+def test_tensor_route_small_and_ragged(ssb, oracle, N, k):
+    """Tiles past N are zero-filled by TMA; they must never become candidates
+    (k > N keeps the bound at +inf)."""
+    X = random_walks(N, 64, 9)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=64, dataset_size=N, leaf_threshold=4))
+    Q = random_walks(3, 64, 10)
+    od2, oid = oracle.knn_scan(X, Q, k)
+    d2, ids, _, st = ssb.QueryEngine(idx).knn_device(Q, k, want_stats=True, route="tensor")
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert (st[:, 1] <= N).all()
