@@ -132,6 +132,42 @@ __global__ void lbe_kernel(const double *__restrict__ cs_g, const double *__rest
     }
 }
 
+// rows of the leaves whose LB_EAPCA equals the query's minimum: every valid
+// bound is >= d(NN) >= min LB, so these rows are candidates of the LB_SAX path
+// whatever the seed finds -- a seed-free lower bound on that path's cost.
+__global__ void floor_rows_kernel(const double *__restrict__ lbe, int L, const uint32_t *__restrict__ leaf_count,
+                                  uint64_t *__restrict__ floor_rows)
+{
+    const int q = blockIdx.x;
+    double mn = __longlong_as_double(0x7ff0000000000000ll);
+    for (int l = threadIdx.x; l < L; l += blockDim.x)
+        if (leaf_count[l]) mn = fmin(mn, lbe[(int64_t)q * L + l]);
+    for (int off = 16; off; off >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    __shared__ double wm[32];
+    __shared__ unsigned long long wr[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
+        for (int off = 16; off; off >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (threadIdx.x == 0) wm[0] = m;
+    }
+    __syncthreads();
+    mn = wm[0];
+    unsigned long long rows = 0;
+    for (int l = threadIdx.x; l < L; l += blockDim.x)
+        if (leaf_count[l] && lbe[(int64_t)q * L + l] <= mn) rows += leaf_count[l];
+    for (int off = 16; off; off >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, off);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) wr[threadIdx.x >> 5] = rows;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wr[w];
+        floor_rows[q] = t;
+    }
+}
+
 // Entry = (tile, query, mask).  Appended with a global counter.
 struct EntryOut {
     uint64_t *key;   // (tile << 32) | ((32 - popc(mask)) << 26) | query
@@ -613,8 +649,22 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     const double avg_leaf = (double)ix.N / (double)std::max(1, L);
-    const bool tc_all = ix.Xb && k <= TC_KTOP_MAX &&
-                        (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    const bool tc_ok = ix.Xb && k <= TC_KTOP_MAX;
+    const bool tc_all = tc_ok && (qc.route == 2 ||
+                                  (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    // auto: queries whose seed-free lower bound on the LB_SAX path already
+    // exceeds the dense filter skip the seed and go to the tensor cores
+    std::vector<int32_t> pre_tc(B, tc_all ? 1 : 0);
+    if (tc_ok && !tc_all && qc.route == 0) {
+        DevBuf fr;
+        SSB_CUDA(fr.alloc(8 * (size_t)B, s));
+        floor_rows_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, ix.leaf_count, fr.as<uint64_t>());
+        SSB_CHECK_LAUNCH();
+        std::vector<uint64_t> hfr(B);
+        SSB_CUDA(cudaMemcpyAsync(hfr.data(), fr.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < B; q++) pre_tc[q] = (double)hfr[q] * COST_LBS_ROW > (double)ix.N * COST_TC_ROW ? 1 : 0;
+    }
     if (tc_all) SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
     if (!tc_all) {
         std::vector<int32_t> hbest(B);
@@ -623,7 +673,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         std::vector<std::vector<int32_t>> byleaf(L);
         std::vector<uint32_t> seed_rows(B, 0);
         for (int q = 0; q < B; q++)
-            if (hbest[q] >= 0) byleaf[hbest[q]].push_back(q);
+            if (hbest[q] >= 0 && !pre_tc[q]) byleaf[hbest[q]].push_back(q);
         std::vector<int32_t> qlist;
         std::vector<ScanJob> jobs;
         const uint32_t CH = 1024;  // rows per job
@@ -674,6 +724,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     std::vector<int32_t> h_tc(B);
     SSB_CUDA(cudaMemcpyAsync(h_tc.data(), use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < B; q++) h_tc[q] |= pre_tc[q];
     std::vector<int32_t> qtree, qtc;
     for (int q = 0; q < B; q++) (h_tc[q] ? qtc : qtree).push_back(q);
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
