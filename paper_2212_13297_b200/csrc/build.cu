@@ -546,7 +546,7 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
     SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
     SSB_CUDA(cudaMalloc(&ix.xnorm, (size_t)ix.N * 4));
-    SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)ix.N * 16));
+    SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)((ix.N + 127) / 128 * 128) * 16));  // padded to whole tiles
     int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
     if (rc) return rc;
     SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 2) * 16));

@@ -743,7 +743,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
         SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
         SSB_CUDA(qnrm.alloc(4 * (size_t)nq_pad, s));
-        SSB_CUDA(gb.alloc(4 * (size_t)nq, s));
+        SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
+        SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
         SSB_CUDA(tc_n.alloc(4, s));
         SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));

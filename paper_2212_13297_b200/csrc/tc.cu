@@ -47,7 +47,7 @@ constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
 constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
-constexpr int TC_NSLOT = 8;          // B pipeline depth in 16 KB K-chunks
+constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB K-chunks
 constexpr int TC_KTOP = 128;  // in-register top-k of upper bounds (k <= 128 tightens)
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
@@ -110,31 +110,45 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar)
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a) : "memory");
 }
 
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t *r)
 {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *r)
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]^T: the query block stays resident in TMEM, so
+// the tensor core reads only B from shared memory (half the SS-mode traffic)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
 }
 
 struct TcParams {
     int n;                 // series length (K, zero-padded to KB*64 by TMA)
     int KB;                // 64-column chunks
     int64_t N;             // rows
+    const uint4 *qb;       // BF16 queries, row-major (n per row), nq rows
     int nq;                // queries in this launch (<= QB*128)
     int QB;                // query blocks
     int64_t tiles;         // ceil(N / 128)
@@ -155,9 +169,20 @@ struct TcParams {
     int skip_epi;              // diagnostics (SSB_TC_DIAG=1): epilogue only releases TMEM
 };
 
+// per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
+constexpr int TC_RS = 4;  // tile-slot ring depth
+struct TileSlot {
+    float4 rowc[TC_BN];  // row bound constants of the tile's 128 rows
+    float4 tilec[2];     // per 64-row half: (min a, max b, min a', min b')
+    float gb[TC_BM];     // snapshot of the shared per-query bounds (float bits)
+};
+static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
+
+// KTOP > 0: keep the k smallest upper bounds per thread (k <= KTOP);
+// KTOP == 0: filter against the given bounds only; KTOP < 0: debug dump of S.
 template <int KTOP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    tc_filter_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p)
+    tc_filter_kernel(const __grid_constant__ CUtensorMap mapB, TcParams p)
 {
     // mapB's box covers 128/CS rows: every CTA of the cluster loads one row
     // slice of each B tile and multicasts it to the whole cluster
@@ -166,17 +191,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int KB = p.KB;
     const uint32_t chunk_bytes = TC_BM * 128;  // 128 rows x 64 bf16
-    unsigned char *sA = base;
-    unsigned char *sRing = base + KB * chunk_bytes;  // TC_NSLOT chunk slots (128 rows x 64 cols each)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sRing + TC_NSLOT * chunk_bytes);
+    unsigned char *sRing = base;  // TC_NSLOT chunk slots (128 rows x 64 cols each)
+    TileSlot *slots = reinterpret_cast<TileSlot *>(sRing + TC_NSLOT * chunk_bytes);  // [TC_RS]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(slots + TC_RS);
     uint64_t *a_full = bars + 0;
-    uint64_t *b_full = bars + 1;               // [TC_NSLOT]
-    uint64_t *b_empty = bars + 1 + TC_NSLOT;   // [TC_NSLOT]
-    uint64_t *t_full = bars + 1 + 2 * TC_NSLOT;   // [2]
-    uint64_t *t_empty = bars + 3 + 2 * TC_NSLOT;  // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5 + 2 * TC_NSLOT);
-    float4 *s_row = reinterpret_cast<float4 *>(bars + 6 + 2 * TC_NSLOT);  // [8 warps][2][64] row constants
-    uint2 *s_stage = reinterpret_cast<uint2 *>(s_row + 8 * 2 * 64);     // [8 warps][TC_STAGE]
+    uint64_t *b_full = bars + 1;                      // [TC_NSLOT]
+    uint64_t *b_empty = b_full + TC_NSLOT;            // [TC_NSLOT]
+    uint64_t *t_full = b_empty + TC_NSLOT;            // [2]
+    uint64_t *t_empty = t_full + 2;                   // [2]
+    uint64_t *r_full = t_empty + 2;                   // [TC_RS]
+    uint64_t *r_empty = r_full + TC_RS;               // [TC_RS]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(r_empty + TC_RS);
+    uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int CS = p.CS;
@@ -187,10 +213,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint16_t cmask = (uint16_t)((1u << CS) - 1u);
     const int64_t t_begin = (int64_t)chunk * p.tiles_per_cta;
     const int64_t t_end = min(p.tiles, t_begin + p.tiles_per_cta);
-    const int64_t ntile = t_end > t_begin ? t_end - t_begin : 0;
+    const int ntile = t_end > t_begin ? (int)(t_end - t_begin) : 0;
 
     if (threadIdx.x == 0) {
-        mbar_init(a_full, 1);
+        mbar_init(a_full, 128);  // the four h == 0 epilogue warps write A into TMEM
         for (int i = 0; i < TC_NSLOT; i++) {
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], CS);  // one multicast commit from every CTA of the cluster
@@ -199,11 +225,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&t_full[i], 1);
             mbar_init(&t_empty[i], TC_EPI_THREADS);
         }
+        for (int i = 0; i < TC_RS; i++) {
+            mbar_init(&r_full[i], 1);
+            mbar_init(&r_empty[i], TC_EPI_THREADS / 32);  // one arrive per epilogue warp
+        }
         fence_barrier_init();
     }
-    if (warp == 1) {  // TMEM: 2 accumulators x 128 fp32 columns
+    if (warp == 1) {  // TMEM: 2 accumulators x 128 fp32 columns + A (128 x K bf16 = K/2 columns)
         const unsigned dst = (unsigned)__cvta_generic_to_shared(tmem_slot);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(dst));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -212,83 +242,170 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem_base = *tmem_slot;
 
+    // Producer and MMA roles run warp-wide (every value stays warp-uniform, in
+    // uniform registers); one elected lane issues each TMA / tcgen05 instruction.
     if (warp == 0) {
         // ---------------- TMA producer ----------------
-        if (lane == 0 && ntile > 0) {
-            mbar_expect_tx(a_full, KB * chunk_bytes);
-            for (int kb = 0; kb < KB; kb++) tma_load_2d(sA + kb * chunk_bytes, &mapA, kb * 64, qb * TC_BM, a_full);
+        if (ntile > 0) {
             // ring of K-chunk slots: chunk c = t*KB + kb -> slot c % NSLOT, use c / NSLOT
-            int64_t c = 0;
-            for (int64_t t = 0; t < ntile; t++) {
-                const int row0 = (int)((t_begin + t) * TC_BN);
+            const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sRing);
+            const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(b_full);
+            const uint32_t rfull0 = (uint32_t)__cvta_generic_to_shared(r_full);
+            const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(slots);
+            const int srows = TC_BN / CS;
+            uint32_t slot = 0, phase = 0, c = 0;
+            for (int t = 0; t < ntile; t++) {
+                const int64_t tile = t_begin + t;
+                // side data of this tile: row constants, half-tile extremes, bounds snapshot
+                const int rs = t % TC_RS;
+                if (t >= TC_RS) mbar_wait(&r_empty[rs], (unsigned)(((t / TC_RS) - 1) & 1));
+                {
+                    const uint32_t dst = slot0 + (uint32_t)(rs * sizeof(TileSlot));
+                    const uint32_t bar = rfull0 + (uint32_t)rs * 8;
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %8;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %5, [%1];\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2048], [%3], %6, [%1];\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2080], [%4], %7, [%1];\n"
+                        "}" ::"r"(dst),
+                        "r"(bar), "l"(p.rowc + tile * TC_BN), "l"(p.tilec + tile * 2), "l"(p.gbound + qb * TC_BM),
+                        "n"(TC_BN * 16), "n"(32), "n"(TC_BM * 4), "n"((int)sizeof(TileSlot))
+                        : "memory");
+                }
+                const int row0 = (int)(tile * TC_BN) + rank * srows;
                 for (int kb = 0; kb < KB; kb++, c++) {
-                    const int slot = (int)(c % TC_NSLOT);
-                    const int64_t use = c / TC_NSLOT;
-                    if (use >= 1) mbar_wait(&b_empty[slot], (unsigned)((use - 1) & 1));
-                    unsigned char *dst = sRing + slot * chunk_bytes;
-                    mbar_expect_tx(&b_full[slot], chunk_bytes);  // the whole chunk lands here
-                    if (CS == 1) {
-                        tma_load_2d(dst, &mapB, kb * 64, row0, &b_full[slot]);
-                    } else {
-                        const int srows = TC_BN / CS;
-                        tma_load_2d_mc(dst + rank * srows * 128, &mapB, kb * 64, row0 + rank * srows, &b_full[slot],
-                                       cmask);
+                    if (c >= (uint32_t)TC_NSLOT) {
+                        if (p.skip_epi == 3) break;  // diagnostics: MMA on stale slots only
+                        mbar_wait(&b_empty[slot], phase ^ 1u);
+                    }
+                    const uint32_t dst = ring + slot * chunk_bytes + (uint32_t)(rank * srows * 128);
+                    const uint32_t bar = full0 + slot * 8;
+                    // the whole chunk (every CTA's slice) lands in this CTA's slot
+                    if (CS == 1)
+                        asm volatile(
+                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                            "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %4;\n"
+                            "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%5, {%2, %3}], [%1];\n}" ::"r"(dst),
+                            "r"(bar), "r"(kb * 64), "r"(row0), "r"(chunk_bytes), "l"(&mapB)
+                            : "memory");
+                    else
+                        asm volatile(
+                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                            "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %4;\n"
+                            "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            ".multicast::cluster [%0], [%5, {%2, %3}], [%1], %6;\n}" ::"r"(dst),
+                            "r"(bar), "r"(kb * 64), "r"(row0), "r"(chunk_bytes), "l"(&mapB), "h"(cmask)
+                            : "memory");
+                    if (++slot == (uint32_t)TC_NSLOT) {
+                        slot = 0;
+                        phase ^= 1u;
                     }
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0 && ntile > 0) {
+        if (ntile > 0) {
             mbar_wait(a_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t a_addr = (uint32_t)__cvta_generic_to_shared(sA);
-            int64_t c = 0;
-            for (int64_t t = 0; t < ntile; t++) {
-                const int s = (int)(t & 1);
+            const uint32_t a_tmem = tmem_base + 2 * TC_BN;  // 8 columns per K=16 step
+            const uint64_t bdesc0 = umma_desc_sw128((uint32_t)__cvta_generic_to_shared(sRing));
+            const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
+            const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
+            uint32_t slot = 0, phase = 0, c = 0;
+            for (int t = 0; t < ntile; t++) {
+                const int s = t & 1;
                 if (t >= 2) mbar_wait(&t_empty[s], (unsigned)(((t >> 1) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
                 for (int kb = 0; kb < KB; kb++, c++) {
-                    const int slot = (int)(c % TC_NSLOT);
-                    mbar_wait(&b_full[slot], (unsigned)((c / TC_NSLOT) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t b_addr = (uint32_t)__cvta_generic_to_shared(sRing + slot * chunk_bytes);
+                    if (p.skip_epi != 3 || c < (uint32_t)TC_NSLOT) mbar_wait(&b_full[slot], phase);
+                    if (p.skip_epi == 4) {  // diagnostics (CS == 1): TMA stream only, no MMA
+                        if (lane == 0) mbar_arrive(&b_empty[slot]);
+                    } else {
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        // descriptor start address advances 32 B (>> 4 = 2) per K=16 step
+                        const uint64_t bdesc = bdesc0 + (uint64_t)(slot * (chunk_bytes >> 4));
 #pragma unroll
-                    for (int ks = 0; ks < 4; ks++) {
-                        const uint32_t offa = kb * chunk_bytes + ks * 32;
-                        umma_bf16(tmem_d, umma_desc_sw128(a_addr + offa), umma_desc_sw128(b_addr + ks * 32),
-                                  (kb | ks) ? 1u : 0u);
+                        for (int ks = 0; ks < 4; ks++)
+                            asm volatile(
+                                "{\n.reg .pred p, q;\nelect.sync _|q, 0xffffffff;\n"
+                                "setp.ne.b32 p, %4, 0;\n"
+                                "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+                                "r"(a_tmem + (uint32_t)((kb * 4 + ks) * 8)), "l"(bdesc + (uint64_t)(2 * ks)),
+                                "r"(TC_IDESC), "r"((kb | ks) ? 1u : 0u));
+                        // frees the slot in every CTA's producer (multicast commit)
+                        asm volatile(
+                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                            "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%0], %1;\n}" ::"r"(empty0 + slot * 8),
+                            "h"(cmask)
+                            : "memory");
                     }
-                    if (CS == 1)
-                        umma_commit(&b_empty[slot]);
-                    else
-                        umma_commit_mc(&b_empty[slot], cmask);  // frees the slot in every CTA's producer
+                    if (++slot == (uint32_t)TC_NSLOT) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
                 }
-                umma_commit(&t_full[s]);
+                if (p.skip_epi == 4) {
+                    if (lane == 0) mbar_arrive(&t_full[s]);
+                } else {
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+                            tfull0 + (uint32_t)s * 8)
+                        : "memory");
+                }
             }
         }
     } else {
         // ---------------- epilogue: 8 warps, two per TMEM lane quarter ----------------
         // thread <-> query m (TMEM lane), column half h of every 128-row tile
         const int ew = warp - 2;                   // 0..7
-        const int et = threadIdx.x - 64;           // 0..255
         const int lane_grp = warp & 3;             // TMEM lanes [32*lane_grp, +32)
         const int h = ew >> 2;                     // column half
         const int m = lane_grp * 32 + lane;
         const int ql = qb * TC_BM + m;
         const bool qvalid = ql < p.nq;
+        if (h == 0 && ntile > 0) {
+            // stage this thread's query row as A: TMEM lane m, column c = bf16 pair (2c, 2c+1),
+            // zero past n (the B chunks are zero-filled there by TMA)
+            const int rowv = p.n / 8;  // uint4 per row
+            const uint32_t a_lane = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + 2 * TC_BN;
+            for (int c0 = 0; c0 < KB * 32; c0 += 16) {
+                uint32_t r[16];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int v = c0 / 4 + j;  // uint4 index within the row (8 bf16 = 4 columns)
+                    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                    if (qvalid && v < rowv) x = p.qb[(int64_t)ql * rowv + v];
+                    r[4 * j] = x.x;
+                    r[4 * j + 1] = x.y;
+                    r[4 * j + 2] = x.z;
+                    r[4 * j + 3] = x.w;
+                }
+                tmem_st16(a_lane + (uint32_t)c0, r);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(a_full);
+        }
         // lb = f*(1-e)*(qn2 + xn2) - 2f*s - 2cf*qn*xn,  ub = g*(1+e)*(qn2 + xn2) - 2g*s + 2cg*qn*xn
         // with f = 1 - 4e-6, g = 1 + 4e-6, e = 2e-6 (fp32 evaluation slack); per-row
-        // constants (xn2 and xn terms) live in shared memory, per-query ones here.
+        // constants (xn2 and xn terms) come from the tile slot, per-query ones live here.
         const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
         const float qn2 = qvalid ? p.qn2[ql] : 0.f;
         const float qnm = qvalid ? p.qnorm[ql] : 0.f;
         const float alpha_l = f * (1.f - e) * qn2, alpha_u = g * (1.f + e) * qn2;
         const float m2f = -2.f * f, m2g = -2.f * g;
-        float top[KTOP > 0 ? KTOP : 1];
-#pragma unroll
-        for (int i = 0; i < (KTOP > 0 ? KTOP : 1); i++) top[i] = __int_as_float(0x7f800000);
+        constexpr int KT = KTOP > 0 ? KTOP : 1;
         constexpr bool tighten = KTOP > 0;
+        float top[KT];
+#pragma unroll
+        for (int i = 0; i < KT; i++)  // -inf prefix: the k-th smallest sits at top[KT-1]
+            top[i] = i < KT - p.k ? __int_as_float(0xff800000) : __int_as_float(0x7f800000);
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
         uint2 *stage = s_stage + ew * TC_STAGE;
@@ -303,130 +420,110 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             stage_n = 0;
         };
-        // row constants (warp-private copy of this warp's 64 columns) and the
-        // shared bound are prefetched one tile ahead; no cross-warp barrier
-        const float4 inf4 = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
-        float4 pre0 = inf4, pre1 = inf4;
-        if (ntile > 0) {
-            const int64_t r = t_begin * TC_BN + h * 64 + 2 * lane;
-            if (r < p.N) pre0 = p.rowc[r];
-            if (r + 1 < p.N) pre1 = p.rowc[r + 1];
-        }
-        float gnext = qvalid ? __uint_as_float(*(volatile unsigned int *)gb) : -1.f;
-        float4 tnext = ntile > 0 ? p.tilec[t_begin * 2 + h] : inf4;
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
-        float4 *wrow = s_row + ew * 2 * 64;
-        for (int64_t t = 0; t < ntile; t++) {
-            const int s = (int)(t & 1);
-            const int64_t row0 = (t_begin + t) * TC_BN;
-            wrow[s * 64 + 2 * lane] = pre0;
-            wrow[s * 64 + 2 * lane + 1] = pre1;
-            __syncwarp();
-            const float gcur = gnext;
+        const bool diag_skip = p.skip_epi == 1 || p.skip_epi >= 3;
+        for (int t = 0; t < ntile; t++) {
+            const int s = t & 1;
+            const int rs = t % TC_RS;
+            const int64_t row0 = (t_begin + t) * TC_BN + h * 64;  // first row of this thread's half
+            const TileSlot &ts = slots[rs];
+            mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
+            const float gcur = qvalid ? ts.gb[m] : -1.f;
             float bound = qvalid ? fminf(gcur, kth) : -1.f;
-            const float4 tc4 = tnext;
-            if (t + 1 < ntile) {
-                tnext = p.tilec[(t_begin + t + 1) * 2 + h];
-                const int64_t r = row0 + TC_BN + h * 64 + 2 * lane;
-                pre0 = r < p.N ? p.rowc[r] : inf4;
-                pre1 = r + 1 < p.N ? p.rowc[r + 1] : inf4;
-            }
-            if (qvalid) gnext = __uint_as_float(*(volatile unsigned int *)gb);
+            const float4 tc4 = ts.tilec[h];
             mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (p.skip_epi == 1) {
+            if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 mbar_arrive(&t_empty[s]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&r_empty[rs]);
                 continue;
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
-            const float4 *rows = wrow + s * 64;
+            uint32_t v[64];
+#pragma unroll
+            for (int j = 0; j < 64; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
+            tmem_wait_ld();
+            // the accumulator is in registers: release it to the MMA warp right away
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&t_empty[s]);
+            if constexpr (KTOP < 0) {  // debug: dump S
+#pragma unroll
+                for (int i = 0; i < 64; i++)
+                    if (qvalid && row0 + i < p.N) p.dump[(int64_t)ql * p.N + row0 + i] = __uint_as_float(v[i]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&r_empty[rs]);
+                continue;
+            }
             // tile-level necessary conditions on the dot product s:
             //   lb_r <= bound  =>  s >= s_lo ;   ub_r < kth  =>  s > s_need
-            const float base_lo = alpha_l + tc4.x - qnm * tc4.y;
-            const float base_need = alpha_u + tc4.z + qnm * tc4.w;
-#pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(taddr + (uint32_t)c0, v);
-                if (p.dump) {
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int64_t r = row0 + h * 64 + c0 + i;
-                        if (qvalid && r < p.N) p.dump[(int64_t)ql * p.N + r] = __uint_as_float(v[i]);
-                    }
-                    continue;
-                }
-                float mx = __uint_as_float(v[0]);
-#pragma unroll
-                for (int i = 1; i < 16; i++) mx = fmaxf(mx, __uint_as_float(v[i]));
-                if (p.skip_epi == 2) {  // diagnostics: TMEM loads + max only
-                    if (mx == -12345.f) atomicAdd(p.cand_n, 1u);
-                    continue;
-                }
-                // lowered by a relative 1e-5 so float32 rounding can only make the
-                // fast path take the precise per-row test more often, never less.
-                // Only rows whose upper bound beats the CURRENT effective bound
-                // (min of the shared bound and this thread's k-th) are inserted:
-                // rows between the two could never tighten what is used.
-                float s_lo = (base_lo - bound) * inv2f;
+            // (lowered by a relative 1e-5 so float32 rounding can only send more
+            // rows to the precise per-row test, never fewer)
+            float thr_s;
+            {
+                float s_lo = ((alpha_l + tc4.x - qnm * tc4.y) - bound) * inv2f;
                 s_lo -= 1e-5f * (fabsf(s_lo) + 1.f);
-                float s_need = __int_as_float(0x7f800000);
+                thr_s = s_lo;
                 if (tighten) {
-                    s_need = (base_need - bound) * inv2g;
+                    float s_need = ((alpha_u + tc4.z + qnm * tc4.w) - bound) * inv2g;
                     s_need -= 1e-5f * (fabsf(s_need) + 1.f);
+                    thr_s = fminf(s_lo, s_need);
                 }
-                uint32_t emit = 0;
-                if (mx >= fminf(s_lo, s_need)) {
-                    const float thr_s = fminf(s_lo, s_need);
-                    uint32_t work = 0;
+            }
+            float mx = __uint_as_float(v[0]);
 #pragma unroll
-                    for (int i = 0; i < 16; i++) work |= (__uint_as_float(v[i]) >= thr_s ? 1u : 0u) << i;
-                    while (work) {
-                        const int i = __ffs(work) - 1;
-                        work &= work - 1;
-                        float sd = 0.f;
+            for (int i = 1; i < 64; i++) mx = fmaxf(mx, __uint_as_float(v[i]));
+            if (__any_sync(0xffffffffu, mx >= thr_s)) {
+                // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
+                const int64_t left = p.N - row0;
+                const float4 *rows = ts.rowc + h * 64;
 #pragma unroll
-                        for (int u = 0; u < 16; u++)
-                            if (u == i) sd = __uint_as_float(v[u]);
-                        const float4 rc = rows[c0 + i];
-                        const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
-                        emit |= (lb <= bound ? 1u : 0u) << i;
-                        if constexpr (tighten) {
-                            if (lb < bound) {  // ub >= lb: only then can ub tighten the bound
-                                const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
-                                if (ub < bound && ub < kth) {
-                                    float x = ub;
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t emit = 0;
+                    if (mx >= thr_s) {
+                        uint32_t work = 0;
 #pragma unroll
-                                    for (int j = 0; j < KTOP; j++) {
-                                        const float lo = fminf(top[j], x);
-                                        x = fmaxf(top[j], x);
-                                        top[j] = lo;
+                        for (int i = 0; i < 16; i++) work |= (__uint_as_float(v[c0 + i]) >= thr_s ? 1u : 0u) << i;
+                        while (work) {
+                            const int i = __ffs(work) - 1;
+                            work &= work - 1;
+                            float sd = 0.f;
+#pragma unroll
+                            for (int u = 0; u < 16; u++)
+                                if (u == i) sd = __uint_as_float(v[c0 + u]);
+                            const float4 rc = rows[c0 + i];
+                            const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                            emit |= (lb <= bound ? 1u : 0u) << i;
+                            if constexpr (tighten) {
+                                if (lb < bound) {  // ub >= lb: only then can ub tighten the bound
+                                    const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
+                                    if (ub < bound && ub < kth) {
+                                        float x = ub;
+#pragma unroll
+                                        for (int j = 0; j < KT; j++) {
+                                            const float lo = fminf(top[j], x);
+                                            x = fmaxf(top[j], x);
+                                            top[j] = lo;
+                                        }
+                                        kth = top[KT - 1];
+                                        bound = fminf(bound, kth);
                                     }
-#pragma unroll
-                                    for (int j = 0; j < KTOP; j++)
-                                        if (j == p.k - 1) kth = top[j];
-                                    bound = fminf(bound, kth);
                                 }
                             }
                         }
+                        if (left < c0 + 16) emit &= left > c0 ? ((1u << (left - c0)) - 1u) : 0u;
                     }
-                }
-                {   // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
-                    const int64_t left = p.N - (row0 + h * 64 + c0);
-                    if (left < 16) emit &= left > 0 ? ((1u << left) - 1u) : 0u;
-                }
-                if (!__any_sync(0xffffffffu, emit != 0)) continue;
-                // warp-staged emission of (query, row) candidates
-                unsigned cnt = __popc(emit);
-                unsigned incl = cnt;
+                    if (!__any_sync(0xffffffffu, emit != 0)) continue;
+                    // warp-staged emission of (query, row) candidates
+                    unsigned cnt = __popc(emit);
+                    unsigned incl = cnt;
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += y;
-                }
-                const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-                if (total) {
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+                        if (lane >= off) incl += y;
+                    }
+                    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
                     if (stage_n + total > TC_STAGE) flush();
                     if (total > TC_STAGE) {  // pathological: write through
                         unsigned b0 = 0;
@@ -437,7 +534,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
                             if ((int64_t)slot < p.cand_cap)
-                                p.cand[slot] = make_uint2((unsigned)ql, (unsigned)(row0 + h * 64 + c0 + i));
+                                p.cand[slot] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
                             slot++;
                         }
                     } else {
@@ -445,16 +542,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
-                            stage[slot++] = make_uint2((unsigned)ql, (unsigned)(row0 + h * 64 + c0 + i));
+                            stage[slot++] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
                         }
                         stage_n += total;
                     }
                 }
             }
+            // the tile slot (row constants) is no longer read by this warp
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&r_empty[rs]);
             // publish this thread's bound for the other CTAs of the query block
             if (qvalid && tighten && kth < gcur) atomicMin(gb, __float_as_uint(kth));
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            mbar_arrive(&t_empty[s]);
         }
         __syncwarp();
         flush();
@@ -463,7 +561,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (CS > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 }
 
@@ -508,7 +606,11 @@ __global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float 
                                      float c_rel, float4 *__restrict__ out)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= N) return;
+    if (r >= (N + 127) / 128 * 128) return;
+    if (r >= N) {  // padding rows of the last tile: lb = ub = +inf
+        out[r] = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
+        return;
+    }
     const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
     out[r] = make_float4(f * (1.f - e) * xn2[r], 2.f * c_rel * f * xn[r], g * (1.f + e) * xn2[r],
                          2.f * c_rel * g * xn[r]);
@@ -555,7 +657,8 @@ static float tc_c_rel() { return (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -
 int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s)
 {
     if (N == 0) return OK;
-    tc_row_consts_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(xn2, xn, N, tc_c_rel(), out);
+    const int64_t padded = (N + 127) / 128 * 128;  // out holds ceil(N/128)*128 entries
+    tc_row_consts_kernel<<<(unsigned)((padded + 255) / 256), 256, 0, s>>>(xn2, xn, N, tc_c_rel(), out);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -594,6 +697,10 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int 
     return OK;
 }
 
+// per-query bound slots the caller allocates for nq queries: the producer
+// copies whole 128-query blocks of bounds (query blocks padded to clusters)
+int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
+
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
 int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
@@ -624,12 +731,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     clusters_per_group = (int)std::max<int64_t>(1, std::min<int64_t>(clusters_per_group, p.tiles / 16));
     p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
-    CUtensorMap mA, mB;
-    // rows beyond the allocated ceil(nq/128)*128 are zero-filled by TMA (padded blocks)
-    int rc = make_map(&mA, Qb, (int64_t)((nq + TC_BM - 1) / TC_BM) * TC_BM, n);
+    CUtensorMap mB;
+    int rc = make_map(&mB, Xb, N, n, TC_BN / CS);
     if (rc) return rc;
-    rc = make_map(&mB, Xb, N, n, TC_BN / CS);
-    if (rc) return rc;
+    p.qb = reinterpret_cast<const uint4 *>(Qb);
     p.qn2 = qn2;
     p.qnorm = qnorm;
     p.xn2 = nullptr;
@@ -647,8 +752,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         const char *d = getenv("SSB_TC_DIAG");
         p.skip_epi = d ? atoi(d) : 0;
     }
-    const int smem = 1024 + (p.KB + TC_NSLOT) * TC_BM * 128 + 8 * (6 + 2 * TC_NSLOT) + 8 * 2 * 64 * 16 +
-                     8 * TC_STAGE * 8;
+    const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
+                     8 * (1 + 2 * TC_NSLOT + 4 + 2 * TC_RS) + 16 + 8 * TC_STAGE * 8;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -667,10 +772,12 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
         ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
                      2.0 * (double)nq * (double)N * (double)(p.KB * 64));
-        SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mA, mB, p));
+        SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mB, p));
         return OK;
     };
-    if (k <= 1)
+    if (dump)
+        rc = go(tc_filter_kernel<-1>);
+    else if (k <= 1)
         rc = go(tc_filter_kernel<1>);
     else if (k <= 4)
         rc = go(tc_filter_kernel<4>);
@@ -699,18 +806,18 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     SSB_CUDA(qnm.alloc(4 * (size_t)Bp, s));
     SSB_CUDA(xn2.alloc(4 * (size_t)N, s));
     SSB_CUDA(xnm.alloc(4 * (size_t)N, s));
-    SSB_CUDA(gb.alloc(4 * (size_t)B, s));
+    SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(B), s));
     SSB_CUDA(cand.alloc(8, s));
     SSB_CUDA(cn.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)Bp * n, s));
-    SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(B), s));
     SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
     int rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnm.as<float>(), s);
     if (rc) return rc;
     rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float>(), s);
     if (rc) return rc;
     DevBuf rcb;
-    SSB_CUDA(rcb.alloc(16 * (size_t)N, s));
+    SSB_CUDA(rcb.alloc(16 * (size_t)((N + 127) / 128 * 128), s));
     rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float>(), N, rcb.as<float4>(), s);
     if (rc) return rc;
     DevBuf tcb;
