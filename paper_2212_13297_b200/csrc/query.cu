@@ -215,7 +215,7 @@ __global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const
 // a row is never dropped that the exact LB_SAX would keep.  Each thread
 // evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
 constexpr int LBS_ROWS = 4;
-constexpr int TC_KTOP_MAX = 128;  // tc.cu TC_KTOP
+constexpr int TC_KTOP_MAX = 4096;  // the filter tightens its bound for every k (buckets)
 constexpr int LBS_STAGE = 1024;
 
 __global__ void __launch_bounds__(256)
@@ -716,7 +716,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     DevBuf use_tc;
     SSB_CUDA(use_tc.alloc(4 * (size_t)B, s));
     int mode = ix.Xb ? qc.route : 1;
-    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;  // the filter only tightens its own bound for k <= 128
+    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;
     if (tc_all) mode = 2;
     route_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, thr.as<uint64_t>(), slack_abs, ix.leaf_count, qc.eapca_th,
                                    mode, ix.N, st_cand_leaves, use_tc.as<int32_t>());
@@ -732,13 +732,13 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
 
     // ---- tensor-core path ---------------------------------------------------------
-    DevBuf d_qtc, tc_cand, tc_n;
+    DevBuf d_qtc, tc_cand, tc_lb, tc_n, gb;
     int64_t tc_nc = 0;
     if (!qtc.empty()) {
         const int nq = (int)qtc.size();
         const int nq_pad = (nq + 127) / 128 * 128;
         const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)nq * 8192);
-        DevBuf qb, qn2, qnrm, gb;
+        DevBuf qb, qn2, qnrm;
         SSB_CUDA(d_qtc.alloc(4 * (size_t)nq, s));
         SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
         SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
@@ -746,6 +746,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
+        SSB_CUDA(tc_lb.alloc(4 * (size_t)tc_cap, s));
         SSB_CUDA(tc_n.alloc(4, s));
         SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
@@ -756,8 +757,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
                                                           gb.as<unsigned int>());
         SSB_CHECK_LAUNCH();
         rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
-                              gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_n.as<unsigned int>(), tc_cap, nullptr,
-                              s);
+                              gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(), tc_n.as<unsigned int>(),
+                              tc_cap, nullptr, s);
         if (rc) return rc;
         uint32_t hn = 0;
         SSB_CUDA(cudaMemcpyAsync(&hn, tc_n.p, 4, cudaMemcpyDeviceToHost, s));
@@ -768,7 +769,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             qtc.clear();
         } else {
             tc_nc = hn;
-            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_nc, so, s);
+            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
+                                gb.as<unsigned int>(), tc_nc, so, s);
             if (rc) return rc;
             if (tc_nc) {
                 tc_count_kernel<<<(unsigned)((tc_nc + 255) / 256), 256, 0, s>>>(tc_cand.as<uint2>(), tc_nc,
@@ -841,7 +843,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             uint32_t ns = 0;
             SSB_CUDA(cudaMemcpyAsync(&ns, nsub.p, 4, cudaMemcpyDeviceToHost, s));
             SSB_CUDA(cudaStreamSynchronize(s));
-            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), ns, so, s);
+            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), nullptr, nullptr, ns, so,
+                                s);
             if (rc) return rc;
             SSB_CUDA(cudaStreamSynchronize(s));
         }

@@ -65,13 +65,15 @@ struct QueryCfg {
 
 int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
-                     uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s);
+                     uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
+                     cudaStream_t s);
 int64_t tc_bound_slots(int nq);
 int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s);
 int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float *nrm, cudaStream_t s);
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
-                   const uint2 *cand, int64_t nc, ScanOut out, cudaStream_t s);
+                   const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
+                   cudaStream_t s);
 
 }  // namespace ssb

@@ -47,8 +47,9 @@ constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
 constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
+constexpr int TC_NACC = 3;           // TMEM accumulators (3 x 128 columns + A <= 128 columns)
 constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB K-chunks
-constexpr int TC_KTOP = 128;  // in-register top-k of upper bounds (k <= 128 tightens)
+constexpr int TC_KTOP = 32;   // in-register top-k of upper bounds for k <= 32; larger k: buckets only
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
 // N = 128 (>>3 = 16 at bit 17), M = 128 (>>4 = 8 at bit 24)
@@ -119,6 +120,19 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t *r)
         : "r"(taddr));
 }
 
+// v[i] for a runtime i in [0,16): a 4-level select tree (depth 4, no local memory)
+__device__ __forceinline__ float sel16(const uint32_t *v, int i)
+{
+    uint32_t a[8], b[4], c[2];
+#pragma unroll
+    for (int j = 0; j < 8; j++) a[j] = (i & 1) ? v[2 * j + 1] : v[2 * j];
+#pragma unroll
+    for (int j = 0; j < 4; j++) b[j] = (i & 2) ? a[2 * j + 1] : a[2 * j];
+#pragma unroll
+    for (int j = 0; j < 2; j++) c[j] = (i & 4) ? b[2 * j + 1] : b[2 * j];
+    return __uint_as_float((i & 8) ? c[1] : c[0]);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *r)
@@ -160,9 +174,11 @@ struct TcParams {
     const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
     const float4 *tilec;       // per 64-row half tile: (min a, max b, min a', min b')
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
+    unsigned int *gbucket;     // per query x k (k >= 2): min upper bound of the rows r with r % k == b
     int k;
     float c_rel;               // dot-product error coefficient
     uint2 *cand;               // (query, row) candidates
+    float *cand_lb;            // their lower bounds (rescoring skips rows above the final bound)
     unsigned int *cand_n;
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
@@ -188,7 +204,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // slice of each B tile and multicasts it to the whole cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms
-    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // (pointer arithmetic on smem_raw keeps the shared address space visible to the compiler)
+    unsigned char *base = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
     const int KB = p.KB;
     const uint32_t chunk_bytes = TC_BM * 128;  // 128 rows x 64 bf16
     unsigned char *sRing = base;  // TC_NSLOT chunk slots (128 rows x 64 cols each)
@@ -197,12 +214,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t *a_full = bars + 0;
     uint64_t *b_full = bars + 1;                      // [TC_NSLOT]
     uint64_t *b_empty = b_full + TC_NSLOT;            // [TC_NSLOT]
-    uint64_t *t_full = b_empty + TC_NSLOT;            // [2]
-    uint64_t *t_empty = t_full + 2;                   // [2]
-    uint64_t *r_full = t_empty + 2;                   // [TC_RS]
+    uint64_t *t_full = b_empty + TC_NSLOT;            // [TC_NACC]
+    uint64_t *t_empty = t_full + TC_NACC;             // [TC_NACC]
+    uint64_t *r_full = t_empty + TC_NACC;             // [TC_RS]
     uint64_t *r_empty = r_full + TC_RS;               // [TC_RS]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(r_empty + TC_RS);
     uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [8 warps][TC_STAGE]
+    float *s_stage_lb = reinterpret_cast<float *>(s_stage + 8 * TC_STAGE);  // [8 warps][TC_STAGE]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int CS = p.CS;
@@ -221,7 +239,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], CS);  // one multicast commit from every CTA of the cluster
         }
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < TC_NACC; i++) {
             mbar_init(&t_full[i], 1);
             mbar_init(&t_empty[i], TC_EPI_THREADS);
         }
@@ -310,14 +328,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (ntile > 0) {
             mbar_wait(a_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t a_tmem = tmem_base + 2 * TC_BN;  // 8 columns per K=16 step
+            const uint32_t a_tmem = tmem_base + TC_NACC * TC_BN;  // 8 columns per K=16 step
             const uint64_t bdesc0 = umma_desc_sw128((uint32_t)__cvta_generic_to_shared(sRing));
             const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
             const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
             uint32_t slot = 0, phase = 0, c = 0;
             for (int t = 0; t < ntile; t++) {
-                const int s = t & 1;
-                if (t >= 2) mbar_wait(&t_empty[s], (unsigned)(((t >> 1) - 1) & 1));
+                const int s = t % TC_NACC;
+                if (t >= TC_NACC) mbar_wait(&t_empty[s], (unsigned)(((t / TC_NACC) - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
                 for (int kb = 0; kb < KB; kb++, c++) {
@@ -328,20 +346,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         // descriptor start address advances 32 B (>> 4 = 2) per K=16 step
                         const uint64_t bdesc = bdesc0 + (uint64_t)(slot * (chunk_bytes >> 4));
-#pragma unroll
-                        for (int ks = 0; ks < 4; ks++)
-                            asm volatile(
-                                "{\n.reg .pred p, q;\nelect.sync _|q, 0xffffffff;\n"
-                                "setp.ne.b32 p, %4, 0;\n"
-                                "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
-                                "r"(a_tmem + (uint32_t)((kb * 4 + ks) * 8)), "l"(bdesc + (uint64_t)(2 * ks)),
-                                "r"(TC_IDESC), "r"((kb | ks) ? 1u : 0u));
-                        // frees the slot in every CTA's producer (multicast commit)
+                        // one elected lane issues the chunk's four K=16 MMAs (B descriptor start
+                        // +32 B = +2, A +8 TMEM columns each) and the commit that frees the slot
+                        // in every CTA's producer (multicast)
                         asm volatile(
-                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                            "{\n.reg .pred p, q;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
+                            "elect.sync _|q, 0xffffffff;\n"
+                            "setp.ne.b32 p, %4, 0;\n"
+                            "add.s64 d1, %2, 2;\nadd.s64 d2, %2, 4;\nadd.s64 d3, %2, 6;\n"
+                            "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n"
                             "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-                            " [%0], %1;\n}" ::"r"(empty0 + slot * 8),
-                            "h"(cmask)
+                            " [%5], %6;\n}" ::"r"(tmem_d),
+                            "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u),
+                            "r"(empty0 + slot * 8), "h"(cmask)
                             : "memory");
                     }
                     if (++slot == (uint32_t)TC_NSLOT) {
@@ -373,7 +394,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // stage this thread's query row as A: TMEM lane m, column c = bf16 pair (2c, 2c+1),
             // zero past n (the B chunks are zero-filled there by TMA)
             const int rowv = p.n / 8;  // uint4 per row
-            const uint32_t a_lane = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + 2 * TC_BN;
+            const uint32_t a_lane = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + TC_NACC * TC_BN;
             for (int c0 = 0; c0 < KB * 32; c0 += 16) {
                 uint32_t r[16];
 #pragma unroll
@@ -408,7 +429,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             top[i] = i < KT - p.k ? __int_as_float(0xff800000) : __int_as_float(0x7f800000);
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
+        // bucket bound (k >= 2): rows are split into k classes by r % k; the
+        // largest per-class minimum of the upper bounds bounds the k-th
+        // smallest distance (k distinct rows lie below it), and it pools the
+        // upper bounds of every thread and CTA that scans this query
+        unsigned int *bk = (qvalid && p.gbucket) ? p.gbucket + (int64_t)ql * p.k : nullptr;
+        const uint32_t kk = (uint32_t)p.k;
+        float bmax = __int_as_float(0x7f800000);  // last bucket bound read by this thread
+        bool touched = false;
         uint2 *stage = s_stage + ew * TC_STAGE;
+        float *stage_lb = s_stage_lb + ew * TC_STAGE;
         unsigned stage_n = 0;  // warp-uniform
         auto flush = [&]() {
             unsigned base_slot = 0;
@@ -416,22 +446,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
             __syncwarp();
             for (unsigned i = lane; i < stage_n; i += 32)
-                if ((int64_t)(base_slot + i) < p.cand_cap) p.cand[base_slot + i] = stage[i];
+                if ((int64_t)(base_slot + i) < p.cand_cap) {
+                    p.cand[base_slot + i] = stage[i];
+                    p.cand_lb[base_slot + i] = stage_lb[i];
+                }
             __syncwarp();
             stage_n = 0;
         };
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
         const bool diag_skip = p.skip_epi == 1 || p.skip_epi >= 3;
         for (int t = 0; t < ntile; t++) {
-            const int s = t & 1;
+            const int s = t % TC_NACC;
             const int rs = t % TC_RS;
             const int64_t row0 = (t_begin + t) * TC_BN + h * 64;  // first row of this thread's half
             const TileSlot &ts = slots[rs];
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
             const float gcur = qvalid ? ts.gb[m] : -1.f;
-            float bound = qvalid ? fminf(gcur, kth) : -1.f;
+            float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
             const float4 tc4 = ts.tilec[h];
-            mbar_wait(&t_full[s], (unsigned)((t >> 1) & 1));
+            mbar_wait(&t_full[s], (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -471,34 +504,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     thr_s = fminf(s_lo, s_need);
                 }
             }
-            float mx = __uint_as_float(v[0]);
+            float mg[4];  // per 16-column group maxima
 #pragma unroll
-            for (int i = 1; i < 64; i++) mx = fmaxf(mx, __uint_as_float(v[i]));
+            for (int g = 0; g < 4; g++) {
+                float a = fmaxf(__uint_as_float(v[16 * g]), __uint_as_float(v[16 * g + 1]));
+#pragma unroll
+                for (int i = 2; i < 16; i++) a = fmaxf(a, __uint_as_float(v[16 * g + i]));
+                mg[g] = a;
+            }
+            float mx = fmaxf(fmaxf(mg[0], mg[1]), fmaxf(mg[2], mg[3]));
+            if (p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: TMEM loads + max only
             if (__any_sync(0xffffffffu, mx >= thr_s)) {
                 // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
                 const int64_t left = p.N - row0;
+                const uint64_t valid = left >= 64 ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
                 const float4 *rows = ts.rowc + h * 64;
+                auto row_lb = [&](int c0, int i) {
+                    const float sd = sel16(v + c0, i);
+                    const float4 rc = rows[c0 + i];
+                    return fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                };
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 16) {
                     uint32_t emit = 0;
-                    if (mx >= thr_s) {
+                    if (mg[c0 / 16] >= thr_s) {
                         uint32_t work = 0;
 #pragma unroll
                         for (int i = 0; i < 16; i++) work |= (__uint_as_float(v[c0 + i]) >= thr_s ? 1u : 0u) << i;
                         while (work) {
                             const int i = __ffs(work) - 1;
                             work &= work - 1;
-                            float sd = 0.f;
-#pragma unroll
-                            for (int u = 0; u < 16; u++)
-                                if (u == i) sd = __uint_as_float(v[c0 + u]);
+                            const float sd = sel16(v + c0, i);
                             const float4 rc = rows[c0 + i];
                             const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
                             emit |= (lb <= bound ? 1u : 0u) << i;
-                            if constexpr (tighten) {
-                                if (lb < bound) {  // ub >= lb: only then can ub tighten the bound
-                                    const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
-                                    if (ub < bound && ub < kth) {
+                            if (lb < bound && (tighten || bk)) {  // ub >= lb: only then can ub tighten the bound
+                                const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
+                                if (ub < bound && ub < kth) {
+                                    if constexpr (tighten) {
                                         float x = ub;
 #pragma unroll
                                         for (int j = 0; j < KT; j++) {
@@ -509,10 +552,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                         kth = top[KT - 1];
                                         bound = fminf(bound, kth);
                                     }
+                                    if (bk) {  // bucket = multiplicative hash of the row, in [0, k)
+                                        const uint32_t r = (uint32_t)(row0 + c0 + i);
+                                        atomicMin(bk + __umulhi(r * 0x9E3779B1u, kk), __float_as_uint(ub));
+                                        touched = true;
+                                    }
                                 }
                             }
                         }
-                        if (left < c0 + 16) emit &= left > c0 ? ((1u << (left - c0)) - 1u) : 0u;
+                        emit &= (uint32_t)(valid >> c0) & 0xffffu;
                     }
                     if (!__any_sync(0xffffffffu, emit != 0)) continue;
                     // warp-staged emission of (query, row) candidates
@@ -533,8 +581,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
-                            if ((int64_t)slot < p.cand_cap)
+                            if ((int64_t)slot < p.cand_cap) {
                                 p.cand[slot] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
+                                p.cand_lb[slot] = row_lb(c0, i);
+                            }
                             slot++;
                         }
                     } else {
@@ -542,6 +592,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
+                            stage_lb[slot] = row_lb(c0, i);
                             stage[slot++] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
                         }
                         stage_n += total;
@@ -551,8 +602,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // the tile slot (row constants) is no longer read by this warp
             __syncwarp();
             if (lane == 0) mbar_arrive(&r_empty[rs]);
+            // refresh the bucket bound after this thread's own updates
+            // (every 8th tile; the loads are independent so their latencies overlap)
+            if (touched && ((t & 7) == 7 || t == ntile - 1)) {
+                uint32_t mxb = 0;
+                if constexpr (KTOP > 0) {
+#pragma unroll
+                    for (int b = 0; b < KT; b++)
+                        if (b < (int)kk) mxb = max(mxb, __ldcg(bk + b));
+                } else {
+                    for (uint32_t b0 = 0; b0 < kk; b0 += 8) {
+                        uint32_t x[8];
+#pragma unroll
+                        for (int j = 0; j < 8; j++) x[j] = b0 + j < kk ? __ldcg(bk + b0 + j) : 0u;
+#pragma unroll
+                        for (int j = 0; j < 8; j++) mxb = max(mxb, x[j]);
+                    }
+                }
+                bmax = fminf(bmax, __uint_as_float(mxb));  // 0xffffffff (unset) reads as NaN: ignored
+                touched = false;
+            }
             // publish this thread's bound for the other CTAs of the query block
-            if (qvalid && tighten && kth < gcur) atomicMin(gb, __float_as_uint(kth));
+            const float mine = fminf(kth, bmax);
+            if (qvalid && mine < gcur) atomicMin(gb, __float_as_uint(mine));
         }
         __syncwarp();
         flush();
@@ -705,7 +777,8 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 // gbound: per-query float bits (initialised by the caller: the seed bound).
 int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
-                     uint2 *cand, unsigned int *cand_n, int64_t cand_cap, float *dump, cudaStream_t s)
+                     uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
+                     cudaStream_t s)
 {
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
     SSB_REQUIRE(N < (1ll << 31), "too many rows for the tensor-core filter");
@@ -742,9 +815,18 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.rowc = rowc;
     p.tilec = tilec;
     p.gbound = gbound;
+    p.gbucket = nullptr;
+    DevBuf buckets;
+    if (k >= 2 && !dump) {
+        const size_t bytes = 4 * (size_t)tc_bound_slots(nq) * (size_t)k;
+        SSB_CUDA(buckets.alloc(bytes, s));
+        SSB_CUDA(cudaMemsetAsync(buckets.p, 0xff, bytes, s));  // unset (NaN bits; atomicMin on the bits)
+        p.gbucket = buckets.as<unsigned int>();
+    }
     p.k = k;
     p.c_rel = tc_c_rel();
     p.cand = cand;
+    p.cand_lb = cand_lb;
     p.cand_n = cand_n;
     p.cand_cap = cand_cap;
     p.dump = dump;
@@ -753,7 +835,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         p.skip_epi = d ? atoi(d) : 0;
     }
     const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
-                     8 * (1 + 2 * TC_NSLOT + 4 + 2 * TC_RS) + 16 + 8 * TC_STAGE * 8;
+                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -775,8 +857,11 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mB, p));
         return OK;
     };
+    const bool nolist = getenv("SSB_TC_NOLIST") != nullptr;  // diagnostics: bucket bound only for k >= 2
     if (dump)
         rc = go(tc_filter_kernel<-1>);
+    else if (nolist && k >= 2)
+        rc = go(tc_filter_kernel<0>);
     else if (k <= 1)
         rc = go(tc_filter_kernel<1>);
     else if (k <= 4)
@@ -785,8 +870,6 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         rc = go(tc_filter_kernel<16>);
     else if (k <= 32)
         rc = go(tc_filter_kernel<32>);
-    else if (k <= 128)
-        rc = go(tc_filter_kernel<128>);
     else
         rc = go(tc_filter_kernel<0>);
     if (rc) return rc;
@@ -825,7 +908,7 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     rc = launch_tc_tile_consts(rcb.as<float4>(), N, tcb.as<float4>(), s);
     if (rc) return rc;
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
-                          1, gb.as<unsigned int>(), cand.as<uint2>(), cn.as<unsigned int>(), 0, S, s);
+                          1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned int>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
@@ -836,13 +919,17 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
 template <int NT>
 __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
                                const float *__restrict__ Qp, const int32_t *__restrict__ qmap,
-                               const uint2 *__restrict__ cand, int64_t nc, ScanOut out)
+                               const uint2 *__restrict__ cand, const float *__restrict__ cand_lb,
+                               const unsigned int *__restrict__ fbound, int64_t nc, ScanOut out)
 {
     const int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
     const int lane = threadIdx.x & 31, j = lane & 7;
     const unsigned gmask = 0xffu << (lane & 24);
     if (gp >= nc) return;
     const uint2 c = cand[gp];
+    // emitted under the bound of the moment; the final bound of the filter
+    // (still >= the k-th distance) settles most of them without the row
+    if (cand_lb && cand_lb[gp] > __uint_as_float(fbound[c.x])) return;
     const int q = qmap ? qmap[c.x] : (int)c.x;
     float qv[NT / 8];
     lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
@@ -858,16 +945,17 @@ __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__re
 }
 
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
-                   const uint2 *cand, int64_t nc, ScanOut out, cudaStream_t s)
+                   const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
+                   cudaStream_t s)
 {
     if (nc == 0) return OK;
     const unsigned grid = (unsigned)((nc * 8 + 255) / 256);
     ProfScope ps("rescore", s, (double)nc * n * 4);
     switch (n) {
-    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
-    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
-    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
-    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, nc, out); break;
+    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
+    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
+    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
+    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
     default:
         set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled rescore kernel");
         return ERR_USAGE;
