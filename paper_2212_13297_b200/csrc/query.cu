@@ -884,6 +884,107 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     return OK;
 }
 
+
+__global__ void qfill_u32_kernel(uint32_t *__restrict__ p, int64_t count, uint32_t v)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) p[i] = v;
+}
+
+__global__ void tc_count_dev_kernel(const uint2 *__restrict__ cand, const unsigned int *__restrict__ nc_dev,
+                                    int64_t cap, uint32_t *__restrict__ cand_series)
+{
+    const int64_t nc = min(cap, (int64_t)*nc_dev);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cand_series[cand[i].x], 1u);
+}
+
+static int qfill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
+{
+    if (count == 0) return OK;
+    qfill_u32_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p, count, v);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// Every query of the batch on the tensor-core filter (route "tensor", or auto
+// when the dense filter costs less than one seed-leaf scan): layout + BF16
+// copies, K-tc, device-counted exact rescoring, K-select, and ONE host round
+// trip at the end.  *redo is set when a buffer overflowed (the caller then
+// answers the batch on the general path, which tightens bounds and rescans).
+static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_t *out_keys, uint32_t *st_cand_leaves,
+                          uint32_t *st_cand_series, uint32_t *st_seed_rows, uint32_t *st_over, uint32_t leaves_nonempty,
+                          bool *redo, cudaStream_t s)
+{
+    const int n = ix.n;
+    *redo = false;
+    DevBuf qlay, qb, qn2, qnrm, gb, cand, clb, cn, keys, cnt, thr, flags, qmax;
+    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
+    int rc = launch_layout_rows(Q, nullptr, B, n, qlay.as<float>(), true, s);
+    if (rc) return rc;
+    const int nq_pad = (B + 127) / 128 * 128;
+    SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
+    SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
+    SSB_CUDA(qnrm.alloc(4 * (size_t)nq_pad, s));
+    SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
+    rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnrm.as<float>(), s);
+    if (rc) return rc;
+    SSB_CUDA(qmax.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
+    qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
+    SSB_CHECK_LAUNCH();
+    const int64_t slots = tc_bound_slots(B);
+    SSB_CUDA(gb.alloc(4 * (size_t)slots, s));
+    rc = qfill_u32(gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)
+    if (rc) return rc;
+    const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * 8192);
+    SSB_CUDA(cand.alloc(8 * (size_t)tc_cap, s));
+    SSB_CUDA(clb.alloc(4 * (size_t)tc_cap, s));
+    SSB_CUDA(cn.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+                          gb.as<unsigned int>(), cand.as<uint2>(), clb.as<float>(), cn.as<unsigned int>(), tc_cap,
+                          nullptr, s);
+    if (rc) return rc;
+    // exact rescoring of the candidates whose lower bound is within the final bound
+    const int cap = std::max(16384, 4 * k);
+    SSB_CUDA(keys.alloc(8 * (size_t)B * cap, s));
+    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
+    ScanOut so{keys.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
+    rc = launch_rescore(ix.X, n, ix.orig, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
+                        gb.as<unsigned int>(), tc_cap, so, s, cn.as<unsigned int>());
+    if (rc) return rc;
+    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
+    tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(cand.as<uint2>(), cn.as<unsigned int>(), tc_cap,
+                                                                   st_cand_series);
+    SSB_CHECK_LAUNCH();
+    rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
+    if (rc) return rc;
+    SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
+    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
+    SSB_CUDA(flags.alloc(4 * (size_t)B, s));
+    rc = launch_select(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
+                       flags.as<int32_t>(), s);
+    if (rc) return rc;
+    if (st_over) SSB_CUDA(cudaMemcpyAsync(st_over, flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
+    // the one host round trip: filter count, per-query overflow flags, max |q|
+    std::vector<int32_t> hf(B);
+    uint32_t hn = 0, qm_bits = 0;
+    SSB_CUDA(cudaMemcpyAsync(&hn, cn.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(hf.data(), flags.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    float qm;
+    std::memcpy(&qm, &qm_bits, 4);
+    SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
+    if ((int64_t)hn > tc_cap) *redo = true;
+    for (int q = 0; q < B && !*redo; q++)
+        if (hf[q]) *redo = true;
+    return OK;
+}
+
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
                 int64_t *out_id, int64_t *out_pos,
                 uint32_t *stats_host /* B x 4: cand_leaves, cand_series, seed_rows, rounds */, cudaStream_t s)
@@ -893,21 +994,37 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
     SSB_REQUIRE(B < (1 << 26), "too many queries in one call");
     if (B == 0) return OK;
     const int n = ix.n;
-    // statistic-rounding slack: delta * sqrt(2n) in distance units
-    DevBuf qmax;
-    SSB_CUDA(qmax.alloc(4, s));
-    SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
-    qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
-    SSB_CHECK_LAUNCH();
-    uint32_t qm_bits = 0;
-    SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    float qm;
-    std::memcpy(&qm, &qm_bits, 4);
-    SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
-    const double M = std::max((double)qm, (double)ix.max_abs);
-    const double delta = std::ldexp(M, -19);
-    const double slack_abs = delta * std::sqrt(2.0 * n);
+    // every query on the tensor-core filter: forced, or (auto) when the dense
+    // filter over all N rows costs less than the seed scan of one average leaf
+    const double avg_leaf = (double)ix.N / (double)std::max(1, ix.L);
+    const bool tc_all = ix.Xb && k <= TC_KTOP_MAX &&
+                        (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    uint32_t leaves_nonempty = 0;
+    for (int32_t l : ix.leaves) leaves_nonempty += ix.nodes[l].count > 0 ? 1u : 0u;
+    // statistic-rounding slack: delta * sqrt(2n) in distance
+    // units; needs max |q| on the host, so only the general path computes it
+    double slack_abs = -1.0;
+    auto need_slack = [&]() -> int {
+        if (slack_abs >= 0.0) return OK;
+        DevBuf qmax;
+        SSB_CUDA(qmax.alloc(4, s));
+        SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
+        qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+        uint32_t qm_bits = 0;
+        SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        float qm;
+        std::memcpy(&qm, &qm_bits, 4);
+        SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
+        const double M = std::max((double)qm, (double)ix.max_abs);
+        slack_abs = std::ldexp(M, -19) * std::sqrt(2.0 * n);
+        return OK;
+    };
+    if (!tc_all) {
+        const int rc0 = need_slack();
+        if (rc0) return rc0;
+    }
 
     DevBuf keys, stl, sts, str, sto;
     SSB_CUDA(keys.alloc(8 * (size_t)B * k, s));
@@ -921,6 +1038,20 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
     int bq = (int)std::max<int64_t>(1, std::min<int64_t>(B, std::max<int64_t>(256, budget / per_query_worst)));
     std::vector<int32_t> rounds;
     for (int q0 = 0; q0 < B;) {
+        if (tc_all) {
+            const int nb = std::min(8192, B - q0);
+            bool redo = false;
+            const int rc1 = query_batch_tc(ix, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
+                                           stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0,
+                                           sto.as<uint32_t>() + q0, leaves_nonempty, &redo, s);
+            if (rc1) return rc1;
+            if (!redo) {
+                q0 += nb;
+                continue;
+            }
+            const int rc2 = need_slack();  // a buffer overflowed: this batch takes the general path
+            if (rc2) return rc2;
+        }
         const int nb = std::min(bq, B - q0);
         const int64_t ecap = std::min<int64_t>((int64_t)nb * per_query_worst, budget);
         int32_t r = 0;

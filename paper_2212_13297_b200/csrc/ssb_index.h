@@ -74,6 +74,6 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
                          float *n2, float *nrm, cudaStream_t s);
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
-                   cudaStream_t s);
+                   cudaStream_t s, const unsigned int *nc_dev = nullptr);
 
 }  // namespace ssb

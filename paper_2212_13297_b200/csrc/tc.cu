@@ -920,42 +920,48 @@ template <int NT>
 __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
                                const float *__restrict__ Qp, const int32_t *__restrict__ qmap,
                                const uint2 *__restrict__ cand, const float *__restrict__ cand_lb,
-                               const unsigned int *__restrict__ fbound, int64_t nc, ScanOut out)
+                               const unsigned int *__restrict__ fbound, int64_t nc,
+                               const unsigned int *__restrict__ nc_dev, ScanOut out)
 {
-    const int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    // candidate count from the host (nc) or, without a host round trip, from
+    // the filter's device counter (clamped to the buffer: nc is then its capacity)
+    if (nc_dev) nc = min(nc, (int64_t)*nc_dev);
     const int lane = threadIdx.x & 31, j = lane & 7;
     const unsigned gmask = 0xffu << (lane & 24);
-    if (gp >= nc) return;
-    const uint2 c = cand[gp];
-    // emitted under the bound of the moment; the final bound of the filter
-    // (still >= the k-th distance) settles most of them without the row
-    if (cand_lb && cand_lb[gp] > __uint_as_float(fbound[c.x])) return;
-    const int q = qmap ? qmap[c.x] : (int)c.x;
-    float qv[NT / 8];
-    lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
-    const float d2 = lay_ed2<NT>(X + (int64_t)c.y * NT, qv, j, gmask);
-    if (j == 0) {
-        const uint64_t key = make_key(d2, row_id ? row_id[c.y] : c.y);
-        const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
-        if (key <= bound) {
-            const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
-            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    for (int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; gp < nc; gp += stride) {
+        const uint2 c = cand[gp];
+        // emitted under the bound of the moment; the final bound of the filter
+        // (still >= the k-th distance) settles most of them without the row
+        if (cand_lb && cand_lb[gp] > __uint_as_float(fbound[c.x])) continue;
+        const int q = qmap ? qmap[c.x] : (int)c.x;
+        float qv[NT / 8];
+        lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
+        const float d2 = lay_ed2<NT>(X + (int64_t)c.y * NT, qv, j, gmask);
+        if (j == 0) {
+            const uint64_t key = make_key(d2, row_id ? row_id[c.y] : c.y);
+            const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
+            if (key <= bound) {
+                const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+                if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+            }
         }
     }
 }
 
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
-                   cudaStream_t s)
+                   cudaStream_t s, const unsigned int *nc_dev)
 {
     if (nc == 0) return OK;
-    const unsigned grid = (unsigned)((nc * 8 + 255) / 256);
-    ProfScope ps("rescore", s, (double)nc * n * 4);
+    // host count: one 8-lane group per pair; device count: a grid-stride sweep
+    const unsigned grid = nc_dev ? (unsigned)(num_sms() * 8) : (unsigned)((nc * 8 + 255) / 256);
+    ProfScope ps("rescore", s, nc_dev ? 0.0 : (double)nc * n * 4);
     switch (n) {
-    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
-    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
-    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
-    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, out); break;
+    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
     default:
         set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled rescore kernel");
         return ERR_USAGE;
