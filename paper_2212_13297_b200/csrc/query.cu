@@ -458,7 +458,7 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 // of one tensor-core filter row): LB_SAX filtering of a
 // candidate-leaf row costs ~14 units, an exact float32 pair ~190.  The dense
 // filter costs N units per query.
-constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 190.0;
+constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 2000.0;
 
 // routing: leaves (and their rows) each query keeps under its seed bound.
 // mode 0 auto (cost model), 1 tree, 2 tensor, 3 the reference's eapca_th rule
@@ -937,19 +937,26 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     SSB_CUDA(gb.alloc(4 * (size_t)slots, s));
     rc = qfill_u32(gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)
     if (rc) return rc;
-    const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * 8192);
+    // candidates emitted before the pooled bound settles grow with k
+    const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * std::max(8192, 192 * k));
     SSB_CUDA(cand.alloc(8 * (size_t)tc_cap, s));
     SSB_CUDA(clb.alloc(4 * (size_t)tc_cap, s));
     SSB_CUDA(cn.alloc(4, s));
+    const int cap = std::max(16384, 4 * k);
+    SSB_CUDA(keys.alloc(8 * (size_t)B * cap, s));
+    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
+    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
+    SSB_CUDA(flags.alloc(4 * (size_t)B, s));
+    std::vector<int32_t> hf(B);
+    // a candidate-buffer overflow is retried with the bounds the filter ended
+    // with (valid, and much tighter than +inf); select overflows go to the caller
+    for (int attempt = 0;; attempt++) {
     SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
                           gb.as<unsigned int>(), cand.as<uint2>(), clb.as<float>(), cn.as<unsigned int>(), tc_cap,
                           nullptr, s);
     if (rc) return rc;
     // exact rescoring of the candidates whose lower bound is within the final bound
-    const int cap = std::max(16384, 4 * k);
-    SSB_CUDA(keys.alloc(8 * (size_t)B * cap, s));
-    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     ScanOut so{keys.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
     rc = launch_rescore(ix.X, n, ix.orig, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
@@ -962,15 +969,12 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
     if (rc) return rc;
     SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
-    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
-    SSB_CUDA(flags.alloc(4 * (size_t)B, s));
     rc = launch_select(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                        flags.as<int32_t>(), s);
     if (rc) return rc;
     if (st_over) SSB_CUDA(cudaMemcpyAsync(st_over, flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
     // the one host round trip: filter count, per-query overflow flags, max |q|
-    std::vector<int32_t> hf(B);
     uint32_t hn = 0, qm_bits = 0;
     SSB_CUDA(cudaMemcpyAsync(&hn, cn.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
@@ -979,10 +983,18 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     float qm;
     std::memcpy(&qm, &qm_bits, 4);
     SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
-    if ((int64_t)hn > tc_cap) *redo = true;
+    if (getenv("SSB_TC_TRACE"))
+        fprintf(stderr, "[ssb] tc batch B=%d k=%d attempt %d: %u candidates (cap %lld)\n", B, k, attempt, hn,
+                (long long)tc_cap);
+    if ((int64_t)hn > tc_cap) {
+        if (attempt < 2) continue;
+        *redo = true;
+        return OK;
+    }
     for (int q = 0; q < B && !*redo; q++)
         if (hf[q]) *redo = true;
     return OK;
+    }
 }
 
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,

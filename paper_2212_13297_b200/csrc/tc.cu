@@ -182,6 +182,7 @@ struct TcParams {
     unsigned int *cand_n;
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
+    int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
     int skip_epi;              // diagnostics (SSB_TC_DIAG=1): epilogue only releases TMEM
 };
 
@@ -232,6 +233,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int64_t t_begin = (int64_t)chunk * p.tiles_per_cta;
     const int64_t t_end = min(p.tiles, t_begin + p.tiles_per_cta);
     const int ntile = t_end > t_begin ? (int)(t_end - t_begin) : 0;
+    // warm-up: the first nwarm tiles are scanned once only to tighten the
+    // bounds (no emission) and again at the end with emission, so candidates
+    // are never emitted against an infinite bound
+    const int nwarm = min(p.warm, ntile);
+    const int niter = ntile + nwarm;
+    auto tile_of = [&](int t) -> int64_t { return t_begin + (t < nwarm ? t : t - nwarm); };
 
     if (threadIdx.x == 0) {
         mbar_init(a_full, 128);  // the four h == 0 epilogue warps write A into TMEM
@@ -272,8 +279,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(slots);
             const int srows = TC_BN / CS;
             uint32_t slot = 0, phase = 0, c = 0;
-            for (int t = 0; t < ntile; t++) {
-                const int64_t tile = t_begin + t;
+            for (int t = 0; t < niter; t++) {
+                const int64_t tile = tile_of(t);
                 // side data of this tile: row constants, half-tile extremes, bounds snapshot
                 const int rs = t % TC_RS;
                 if (t >= TC_RS) mbar_wait(&r_empty[rs], (unsigned)(((t / TC_RS) - 1) & 1));
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
             const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
             uint32_t slot = 0, phase = 0, c = 0;
-            for (int t = 0; t < ntile; t++) {
+            for (int t = 0; t < niter; t++) {
                 const int s = t % TC_NACC;
                 if (t >= TC_NACC) mbar_wait(&t_empty[s], (unsigned)(((t / TC_NACC) - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -455,10 +462,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         };
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
         const bool diag_skip = p.skip_epi == 1 || p.skip_epi >= 3;
-        for (int t = 0; t < ntile; t++) {
+        for (int t = 0; t < niter; t++) {
             const int s = t % TC_NACC;
             const int rs = t % TC_RS;
-            const int64_t row0 = (t_begin + t) * TC_BN + h * 64;  // first row of this thread's half
+            const int64_t row0 = tile_of(t) * TC_BN + h * 64;  // first row of this thread's half
+            const bool emit_ok = t >= nwarm;
+            // second visit of a warm-up tile: its rows are already in this thread's
+            // list (a row counted twice would make the k-th bound invalid)
+            const bool revisit = t >= nwarm && t < 2 * nwarm;
             const TileSlot &ts = slots[rs];
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
             const float gcur = qvalid ? ts.gb[m] : -1.f;
@@ -501,7 +512,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 if (tighten) {
                     float s_need = ((alpha_u + tc4.z + qnm * tc4.w) - bound) * inv2g;
                     s_need -= 1e-5f * (fabsf(s_need) + 1.f);
-                    thr_s = fminf(s_lo, s_need);
+                    thr_s = emit_ok ? fminf(s_lo, s_need) : s_need;
                 }
             }
             float mg[4];  // per 16-column group maxima
@@ -537,11 +548,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const float sd = sel16(v + c0, i);
                             const float4 rc = rows[c0 + i];
                             const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
-                            emit |= (lb <= bound ? 1u : 0u) << i;
+                            emit |= (emit_ok && lb <= bound ? 1u : 0u) << i;
                             if (lb < bound && (tighten || bk)) {  // ub >= lb: only then can ub tighten the bound
                                 const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
                                 if (ub < bound && ub < kth) {
-                                    if constexpr (tighten) {
+                                    if (tighten && !revisit) {
                                         float x = ub;
 #pragma unroll
                                         for (int j = 0; j < KT; j++) {
@@ -604,19 +615,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (lane == 0) mbar_arrive(&r_empty[rs]);
             // refresh the bucket bound after this thread's own updates
             // (every 8th tile; the loads are independent so their latencies overlap)
-            if (touched && ((t & 7) == 7 || t == ntile - 1)) {
+            if (touched && ((t & 7) == 7 || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
                 uint32_t mxb = 0;
                 if constexpr (KTOP > 0) {
 #pragma unroll
                     for (int b = 0; b < KT; b++)
                         if (b < (int)kk) mxb = max(mxb, __ldcg(bk + b));
                 } else {
-                    for (uint32_t b0 = 0; b0 < kk; b0 += 8) {
-                        uint32_t x[8];
+                    for (uint32_t b0 = 0; b0 < kk; b0 += 16) {
+                        uint32_t x[16];
 #pragma unroll
-                        for (int j = 0; j < 8; j++) x[j] = b0 + j < kk ? __ldcg(bk + b0 + j) : 0u;
+                        for (int j = 0; j < 16; j++) x[j] = b0 + j < kk ? __ldcg(bk + b0 + j) : 0u;
 #pragma unroll
-                        for (int j = 0; j < 8; j++) mxb = max(mxb, x[j]);
+                        for (int j = 0; j < 16; j++) mxb = max(mxb, x[j]);
                     }
                 }
                 bmax = fminf(bmax, __uint_as_float(mxb));  // 0xffffffff (unset) reads as NaN: ignored
@@ -825,6 +836,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     }
     p.k = k;
     p.c_rel = tc_c_rel();
+    p.warm = 2;
     p.cand = cand;
     p.cand_lb = cand_lb;
     p.cand_n = cand_n;

@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_tc.py tests/test_gpu_index.py -q -x 2>&1 | tail -1
-timeout 60 python tools/cell_profile.py --rows 1000000 --sigmas 1.0 --ks 1,10 2>&1 | tail -2 | cut -c1-300
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/b_c2.json 2> gpurun_out/b_c2.err; head -c 700 gpurun_out/b_c2.json
+SSB_TC_TRACE=1 timeout 900 python bench.py --workload c4 --route tensor --steps 1 --warmup 1 --cpu-sample 0 > gpurun_out/b_c4_tensor.json 2> gpurun_out/b_c4_tensor.err
+grep ssb gpurun_out/b_c4_tensor.err | head
+SSB_TC_TRACE=1 timeout 900 python bench.py --workload c2 --steps 1 --warmup 1 --cpu-sample 0 2>&1 >/dev/null | grep ssb | head -20
