@@ -456,9 +456,10 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 // routing (query.py:321-325): leaves each query keeps under its seed bound
 // Cost model of the two exact paths (B200-measured, per row per query, in units
 // of one tensor-core filter row): LB_SAX filtering of a
-// candidate-leaf row costs ~14 units, an exact float32 pair ~190.  The dense
-// filter costs N units per query.
-constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 2000.0;
+// candidate-leaf row costs ~14 units; the seed scan (exact float32 scan of a
+// query's best leaf, one query per leaf on typical batches) ~5000 per row.
+// The dense filter costs N units per query.
+constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 5000.0;
 
 // routing: leaves (and their rows) each query keeps under its seed bound.
 // mode 0 auto (cost model), 1 tree, 2 tensor, 3 the reference's eapca_th rule
