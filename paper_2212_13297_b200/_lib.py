@@ -14,7 +14,9 @@ import threading
 from .errors import DataFileError, DeviceError, IntegrityError, UsageError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libseriesearch_b200.so")
+# SSB_LIB_VARIANT=name loads libseriesearch_b200.<name>.so (A/B builds of the same sources)
+LIB_PATH = os.path.join(HERE, "libseriesearch_b200.so" if not os.environ.get("SSB_LIB_VARIANT")
+                        else "libseriesearch_b200.%s.so" % os.environ["SSB_LIB_VARIANT"])
 
 _lib = None
 _lock = threading.Lock()
