@@ -116,6 +116,11 @@ typedef struct {
     int32_t is_leaf, oversize, depth;
     int32_t segment, attribute, split_point, route_start, route_end; /* split_point -1 = horizontal */
     double threshold, gain;
+    /* insertion-order build semantics (build.py:213-263): the node was created
+     * holding `inherited` members of its parent's split set; it splits on its
+     * first `split_set` = max(inherited + 1, leaf_threshold + 1) members in
+     * original order (0 when never evaluated); ignored by ssb_index_load */
+    uint32_t inherited, split_set;
 } ssb_node_t;
 
 /* Build the index over N device-resident rows (level-synchronous, all on the

@@ -82,7 +82,7 @@ class NodeRec(ctypes.Structure):
                 ("segment", ctypes.c_int32), ("attribute", ctypes.c_int32),
                 ("split_point", ctypes.c_int32), ("route_start", ctypes.c_int32),
                 ("route_end", ctypes.c_int32), ("threshold", ctypes.c_double),
-                ("gain", ctypes.c_double)]
+                ("gain", ctypes.c_double), ("inherited", ctypes.c_uint32), ("split_set", ctypes.c_uint32)]
 _RESTYPES = {
     "ssb_version": ctypes.c_int32,
     "ssb_last_error": ctypes.c_char_p,

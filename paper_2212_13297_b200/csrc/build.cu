@@ -53,6 +53,7 @@ Index::~Index()
 struct NodeDesc {
     uint32_t first;      // member range start in perm
     uint32_t count;
+    uint32_t ecount;     // split set: the first ecount members (original order); 0 = no split
     int32_t m;
     int32_t allow_v;
     int64_t aoff;        // offset of this node's members in the level's active space
@@ -181,12 +182,16 @@ __global__ void __launch_bounds__(CHUNK)
 __global__ void __launch_bounds__(CHUNK)
     build_minmax_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
                         const float *__restrict__ stats, uint32_t *__restrict__ cmin,
-                        uint32_t *__restrict__ cmax)
+                        uint32_t *__restrict__ cmax, int subset)
 {
+    // subset = 0: every member (node envelopes); 1: the split set only (thresholds)
     const Chunk ch = chunks[blockIdx.x];
     const NodeDesc nd = nodes[ch.node];
+    const uint32_t limit = subset ? nd.ecount : nd.count;
+    if (ch.m0 >= limit) return;
     const int t = threadIdx.x, lane = t & 31;
-    const bool live = t < (int)ch.cnt;
+    const bool live = t < (int)ch.cnt && ch.m0 + (uint32_t)t < limit;
+    if (!__any_sync(0xffffffffu, live)) return;  // whole warp past the limit
     const int ncol = 6 * nd.m;
     for (int col = 0; col < ncol; col++) {
         const int seg = col % nd.m;
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(CHUNK)
         uint32_t k = okey(v);
         uint32_t kmin = __reduce_min_sync(0xffffffffu, live ? k : 0xffffffffu);
         uint32_t kmax = __reduce_max_sync(0xffffffffu, live ? k : 0u);
-        if (lane == 0 && (ch.cnt > (unsigned)(t & ~31))) {
+        if (lane == 0) {
             atomicMin(&cmin[nd.col_off + col], kmin);
             atomicMax(&cmax[nd.col_off + col], kmax);
         }
@@ -281,11 +286,10 @@ __global__ void __launch_bounds__(CHUNK)
     const Chunk ch = chunks[blockIdx.x];
     const NodeDesc nd = nodes[ch.node];
     const int c0 = blockIdx.y * CAND_BATCH;
-    if (c0 >= 6 * nd.m) return;
+    if (c0 >= 6 * nd.m || ch.m0 >= nd.ecount) return;  // only the split set is evaluated
     const int t = threadIdx.x, lane = t & 31;
-    const bool live = t < (int)ch.cnt;
-    const bool warp_live = (int)ch.cnt > (t & ~31);
-    if (!warp_live) return;
+    const bool live = t < (int)ch.cnt && ch.m0 + (uint32_t)t < nd.ecount;
+    if (!__any_sync(0xffffffffu, live)) return;
     const float *st = stats + nd.stat_off + ch.m0 + t;
     uint32_t *nacc = acc + nd.acc_off;
     for (int c = c0; c < min(c0 + CAND_BATCH, 6 * nd.m); c++) {
@@ -371,7 +375,7 @@ __global__ void build_gain_kernel(const NodeDesc *__restrict__ nodes, int nnodes
     const uint32_t *nacc = acc + nd.acc_off;
     for (int c = lane; c < 6 * nd.m; c += 32) {
         if (!valid[nd.col_off + c]) continue;
-        const double rho = (double)nd.count;
+        const double rho = (double)nd.ecount;  // the split set (tree.py:320-330 over its members)
         const double nl = (double)nleft[nd.col_off + c];
         const double nr = __dsub_rn(rho, nl);
         const double qa = qos_side(nd, nacc, c, 2);
@@ -414,7 +418,8 @@ __global__ void build_fallback_count_kernel(const NodeDesc *__restrict__ nodes, 
     const NodeDesc nd = nodes[ch.node];
     const int t = threadIdx.x;
     bool left = false;
-    if (t < (int)ch.cnt) left = (double)stats[nd.stat_off + ch.m0 + t] < fthr[ch.node];
+    if (t < (int)ch.cnt && ch.m0 + (uint32_t)t < nd.ecount)
+        left = (double)stats[nd.stat_off + ch.m0 + t] < fthr[ch.node];
     const unsigned bl = __ballot_sync(0xffffffffu, left);
     if ((t & 31) == 0 && bl) atomicAdd(&fnl[ch.node], (unsigned)__popc(bl));
 }
@@ -453,6 +458,14 @@ __global__ void build_scatter_kernel(const NodeDesc *__restrict__ nodes, const C
     const uint32_t lr = scan[a + i] - base;
     const uint32_t dst = flags[a + i] ? lr : nl + ((uint32_t)i - lr);
     perm_out[nd.first + dst] = perm[nd.first + i];
+}
+
+// per node: members (all of them) routed left by its policy
+__global__ void node_left_kernel(const NodeDesc *__restrict__ nodes, int nnodes, const uint32_t *__restrict__ scan,
+                                 uint32_t *__restrict__ out)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < nnodes) out[f] = scan[nodes[f].aoff + nodes[f].count] - scan[nodes[f].aoff];
 }
 
 // final gather into leaf order
@@ -606,16 +619,26 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     lap("init");
     while (!frontier.empty()) {
         // ---- level descriptors ------------------------------------------------
+        // A frontier node splits when a member arriving after its creation makes it
+        // exceed tau (build.py:232-234), i.e. iff count >= split_set; its policy is
+        // chosen on that split set: its first split_set members in original order
+        // (the perm keeps original order inside every node: stable partitions).
         const int F = (int)frontier.size();
         std::vector<NodeDesc> nd(F);
         std::vector<Chunk> chunks;
+        std::vector<int32_t> need_split(F);
+        bool any_split = false;
         int64_t aoff = 0, stat_off = 0, acc_off = 0;
         int32_t col_off = 0;
         for (int f = 0; f < F; f++) {
-            const TreeNode &tn = ix->nodes[frontier[f]];
+            TreeNode &tn = ix->nodes[frontier[f]];
+            tn.split_set = (uint32_t)std::max<int64_t>((int64_t)tn.c0 + 1, cfg.tau + 1);
+            need_split[f] = tn.count >= tn.split_set;
+            any_split |= need_split[f] != 0;
             NodeDesc &d = nd[f];
             d.first = tn.first;
             d.count = tn.count;
+            d.ecount = need_split[f] ? tn.split_set : 0u;
             d.m = tn.m;
             d.allow_v = tn.m < mmax;
             d.aoff = aoff;
@@ -627,31 +650,22 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 chunks.push_back({(uint32_t)f, m0, std::min<uint32_t>(CHUNK, tn.count - m0)});
             aoff += tn.count;
             stat_off += (int64_t)6 * tn.m * tn.count;
-            acc_off += (int64_t)6 * tn.m * ACC_PER_CAND;
+            acc_off += need_split[f] ? (int64_t)6 * tn.m * ACC_PER_CAND : 0;
             col_off += 6 * tn.m;
         }
         const int64_t nchunks = (int64_t)chunks.size();
         SSB_REQUIRE(nchunks < (1ll << 31), "too many member chunks in one level");
-        DevBuf d_nodes, d_chunks, d_stats, d_cmin, d_cmax, d_thr, d_valid, d_acc, d_nleft, d_res;
+        DevBuf d_nodes, d_chunks, d_stats, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
         SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
         SSB_CUDA(d_stats.alloc(sizeof(float) * (size_t)stat_off, s));
         SSB_CUDA(d_cmin.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(d_cmax.alloc(4 * (size_t)col_off, s));
-        SSB_CUDA(d_thr.alloc(8 * (size_t)col_off, s));
-        SSB_CUDA(d_valid.alloc(4 * (size_t)col_off, s));
-        SSB_CUDA(d_acc.alloc(4 * (size_t)acc_off, s));
-        SSB_CUDA(d_nleft.alloc(4 * (size_t)col_off, s));
-        SSB_CUDA(d_res.alloc(sizeof(NodeResult) * F, s));
         SSB_CUDA(cudaMemcpyAsync(d_nodes.p, nd.data(), sizeof(NodeDesc) * F, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemcpyAsync(d_chunks.p, chunks.data(), sizeof(Chunk) * nchunks,
                                  cudaMemcpyHostToDevice, s));
         RC(fill_u32(d_cmin.as<uint32_t>(), col_off, 0xffffffffu, s));
         RC(fill_u32(d_cmax.as<uint32_t>(), col_off, 0u, s));
-        RC(fill_u32(d_nleft.as<uint32_t>(), col_off, 0u, s));
-        // accumulators: even slots are minima (+inf key), odd slots maxima (0)
-        fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
-        SSB_CHECK_LAUNCH();
 
         {
             ProfScope ps("build_stats", s, (double)aoff * n * 4 + (double)stat_off * 4);
@@ -660,31 +674,43 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                                                                    nonfinite.as<int>());
         }
         SSB_CHECK_LAUNCH();
+        // exact envelopes over every member
         build_minmax_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
                                                                 d_stats.as<float>(), d_cmin.as<uint32_t>(),
-                                                                d_cmax.as<uint32_t>());
+                                                                d_cmax.as<uint32_t>(), 0);
         SSB_CHECK_LAUNCH();
 
-        // which frontier nodes must split (count > tau) vs only need an envelope (root leaf)
-        std::vector<int32_t> need_split(F);
-        bool any_split = false;
-        for (int f = 0; f < F; f++) {
-            need_split[f] = ix->nodes[frontier[f]].count > (uint32_t)cfg.tau;
-            any_split |= need_split[f] != 0;
-        }
         std::vector<NodeResult> res(F);
-        std::vector<int32_t> pcol(F, -1);
-        std::vector<double> pthr(F, 0.0);
         std::vector<uint32_t> env_min((size_t)col_off), env_max((size_t)col_off);
+        std::vector<uint32_t> senv_min, senv_max;  // split-set envelopes (fallback thresholds)
         if (any_split) {
-            build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_cmin.as<uint32_t>(),
-                                              d_cmax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
+            SSB_CUDA(d_emin.alloc(4 * (size_t)col_off, s));
+            SSB_CUDA(d_emax.alloc(4 * (size_t)col_off, s));
+            SSB_CUDA(d_thr.alloc(8 * (size_t)col_off, s));
+            SSB_CUDA(d_valid.alloc(4 * (size_t)col_off, s));
+            SSB_CUDA(d_acc.alloc(4 * (size_t)std::max<int64_t>(acc_off, 1), s));
+            SSB_CUDA(d_nleft.alloc(4 * (size_t)col_off, s));
+            SSB_CUDA(d_res.alloc(sizeof(NodeResult) * F, s));
+            RC(fill_u32(d_emin.as<uint32_t>(), col_off, 0xffffffffu, s));
+            RC(fill_u32(d_emax.as<uint32_t>(), col_off, 0u, s));
+            RC(fill_u32(d_nleft.as<uint32_t>(), col_off, 0u, s));
+            // accumulators: even slots are minima (+inf key), odd slots maxima (0)
+            fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
+            SSB_CHECK_LAUNCH();
+            build_minmax_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                                    d_stats.as<float>(), d_emin.as<uint32_t>(),
+                                                                    d_emax.as<uint32_t>(), 1);
+            SSB_CHECK_LAUNCH();
+            build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_emin.as<uint32_t>(),
+                                              d_emax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
             SSB_CHECK_LAUNCH();
             int maxm = 1;
             for (auto &d : nd) maxm = std::max(maxm, d.m);
             dim3 eg((unsigned)nchunks, (unsigned)((6 * maxm + CAND_BATCH - 1) / CAND_BATCH));
             {
-                ProfScope ps("build_eval", s, (double)stat_off * 4);
+                double ev = 0.0;
+                for (int f = 0; f < F; f++) ev += (double)nd[f].ecount * 6 * nd[f].m * 4;
+                ProfScope ps("build_eval", s, ev);
                 build_eval_kernel<<<eg, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
                                                        d_stats.as<float>(), d_thr.as<double>(),
                                                        d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
@@ -696,6 +722,10 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                                                d_nleft.as<uint32_t>(), d_res.as<NodeResult>());
             SSB_CHECK_LAUNCH();
             SSB_CUDA(cudaMemcpyAsync(res.data(), d_res.p, sizeof(NodeResult) * F, cudaMemcpyDeviceToHost, s));
+            senv_min.resize((size_t)col_off);
+            senv_max.resize((size_t)col_off);
+            SSB_CUDA(cudaMemcpyAsync(senv_min.data(), d_emin.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaMemcpyAsync(senv_max.data(), d_emax.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
         }
         SSB_CUDA(cudaMemcpyAsync(env_min.data(), d_cmin.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(env_max.data(), d_cmax.p, 4 * (size_t)col_off, cudaMemcpyDeviceToHost, s));
@@ -722,15 +752,18 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         }
         if (!any_split) break;
 
-        // fallback policies for nodes with no positive-gain candidate
+        // fallback policies (tree.py:331-335) for split nodes with no valid candidate:
+        // horizontal mean split of segment 0 at the midpoint of the node's envelope
+        // at split time (the split set's)
         std::vector<int32_t> need_fb(F, 0);
         std::vector<double> fthr(F, 0.0);
         bool any_fb = false;
         for (int f = 0; f < F; f++) {
             if (!need_split[f] || res[f].best >= 0) continue;
-            const TreeNode &tn = ix->nodes[frontier[f]];
-            double mu = std::isfinite(tn.env[0][0]) ? (double)tn.env[0][0] : 0.0;
-            double mx = std::isfinite(tn.env[0][1]) ? (double)tn.env[0][1] : 0.0;
+            double mu = (double)inv_key(senv_min[nd[f].col_off]);
+            double mx = (double)inv_key(senv_max[nd[f].col_off]);
+            if (!std::isfinite(mu)) mu = 0.0;
+            if (!std::isfinite(mx)) mx = 0.0;
             fthr[f] = (mu + mx) / 2.0;
             need_fb[f] = 1;
             any_fb = true;
@@ -752,46 +785,74 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             SSB_CUDA(cudaStreamSynchronize(s));
         }
 
-        // decide splits; create children on the host
-        std::vector<int32_t> next;
-        std::vector<std::vector<uint32_t>> child_acc(F);
-        bool any_part = false;
-        // fetch the winning candidates' accumulators (children envelopes)
-        std::vector<uint32_t> acc_h((size_t)F * ACC_PER_CAND);
-        {
-            DevBuf d_win;
-            SSB_CUDA(d_win.alloc(4 * acc_h.size(), s));
-            gather_winner_acc_kernel<<<F, 256, 0, s>>>(d_nodes.as<NodeDesc>(), d_res.as<NodeResult>(),
-                                                      d_acc.as<uint32_t>(), d_win.as<uint32_t>());
-            SSB_CHECK_LAUNCH();
-            SSB_CUDA(cudaMemcpyAsync(acc_h.data(), d_win.p, 4 * acc_h.size(), cudaMemcpyDeviceToHost, s));
-            SSB_CUDA(cudaStreamSynchronize(s));
+        // policies of the split nodes (route column + threshold), then K-part flags
+        std::vector<int32_t> pcol(F, -1), best_of(F, -1);
+        std::vector<double> pthr(F, 0.0);
+        std::vector<uint32_t> nl_set(F, 0);  // split-set members routed left (children's c0)
+        for (int f = 0; f < F; f++) {
+            if (!need_split[f]) continue;
+            const int best = res[f].best;
+            best_of[f] = best;
+            if (best >= 0) {
+                const int m = nd[f].m, seg = best / 6, attr = (best % 6) / 3, lay = (best % 6) % 3;
+                pcol[f] = (2 * lay + attr) * m + seg;
+                pthr[f] = res[f].thr;
+                nl_set[f] = (uint32_t)res[f].nl;
+            } else {
+                pcol[f] = 0;  // base mean column of segment 0
+                pthr[f] = fthr[f];
+                nl_set[f] = fnl[f];
+            }
         }
+        DevBuf d_pcol, d_pthr, d_flags, d_scan, d_tmp, d_nl;
+        SSB_CUDA(d_pcol.alloc(4 * F, s));
+        SSB_CUDA(d_pthr.alloc(8 * F, s));
+        SSB_CUDA(d_flags.alloc(4 * (size_t)(aoff + 1), s));
+        SSB_CUDA(d_scan.alloc(4 * (size_t)(aoff + 1), s));
+        SSB_CUDA(d_nl.alloc(4 * F, s));
+        SSB_CUDA(cudaMemcpyAsync(d_pcol.p, pcol.data(), 4 * F, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(d_pthr.p, pthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemsetAsync(d_flags.as<uint32_t>() + aoff, 0, 4, s));
+        build_flags_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
+                                                               d_stats.as<float>(), d_pcol.as<int32_t>(),
+                                                               d_pthr.as<double>(), d_flags.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+        size_t tmp_bytes = 0;
+        SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flags.as<uint32_t>(), d_scan.as<uint32_t>(),
+                                               (int)(aoff + 1), s));
+        SSB_CUDA(d_tmp.alloc(tmp_bytes, s));
+        SSB_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.p, tmp_bytes, d_flags.as<uint32_t>(), d_scan.as<uint32_t>(),
+                                               (int)(aoff + 1), s));
+        note_launch(1);
+        node_left_kernel<<<(F + 255) / 256, 256, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_scan.as<uint32_t>(),
+                                                         d_nl.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
+        std::vector<uint32_t> nl_all(F);
+        SSB_CUDA(cudaMemcpyAsync(nl_all.data(), d_nl.p, 4 * F, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+
+        // create the children on the host (tree.py:339-381 split_node)
+        std::vector<int32_t> next;
+        bool any_part = false;
         for (int f = 0; f < F; f++) {
             if (!need_split[f]) continue;
             const int32_t id = frontier[f];
-            TreeNode tn = ix->nodes[id];
-            int best = res[f].best;
-            int32_t nl;
-            int seg, attr, lay;
-            double th;
+            const TreeNode tn = ix->nodes[id];
+            const int best = best_of[f];
+            const uint32_t nl = nl_all[f];
+            if (best < 0 && (nl == 0 || nl == tn.count)) {
+                // no candidate separates anything and the fallback moves every member
+                // one way: the reference would grow a chain one arrival per level; this
+                // node stays an oversize leaf (identical members)
+                ix->nodes[id].oversize = 1;
+                pcol[f] = -1;
+                continue;
+            }
+            int seg = 0, attr = 0, lay = 0;
             if (best >= 0) {
                 seg = best / 6;
                 attr = (best % 6) / 3;
                 lay = (best % 6) % 3;
-                th = res[f].thr;
-                nl = res[f].nl;
-            } else {
-                seg = 0;
-                attr = 0;
-                lay = 0;
-                th = fthr[f];
-                nl = (int32_t)fnl[f];
-            }
-            if (nl <= 0 || (uint32_t)nl >= tn.count) {
-                // cannot separate (identical members): an oversize leaf
-                ix->nodes[id].oversize = 1;
-                continue;
             }
             const int sa = seg ? tn.ep[seg - 1] : 0, sb = tn.ep[seg], mid = (sa + sb) / 2;
             TreeNode &P = ix->nodes[id];
@@ -801,18 +862,18 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             P.split = lay ? mid : -1;
             P.rs = lay == 2 ? mid : sa;
             P.re = lay == 1 ? mid : sb;
-            P.thr = th;
+            P.thr = pthr[f];
             P.gain = best >= 0 ? res[f].gain : 0.0;
-            pcol[f] = best >= 0 ? (2 * lay + attr) * tn.m + seg : 0;  // fallback: base mean col 0
-            pthr[f] = th;
             any_part = true;
             TreeNode L, R;
             L.parent = R.parent = id;
             L.depth = R.depth = tn.depth + 1;
             L.first = tn.first;
-            L.count = (uint32_t)nl;
-            R.first = tn.first + (uint32_t)nl;
-            R.count = tn.count - (uint32_t)nl;
+            L.count = nl;
+            R.first = tn.first + nl;
+            R.count = tn.count - nl;
+            L.c0 = nl_set[f];
+            R.c0 = tn.split_set - nl_set[f];
             int mm = tn.m;
             if (lay) {
                 mm = tn.m + 1;
@@ -826,55 +887,20 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             }
             L.m = R.m = mm;
             for (int i = 0; i < mm; i++) R.ep[i] = L.ep[i];
-            if (best >= 0) {
-                const uint32_t *a = acc_h.data() + (size_t)f * ACC_PER_CAND;
-                auto at = [&](int side, int j, int at_, int mx) {
-                    return inv_key(a[(((side * (M_MAX + 1) + j) * 2 + at_) * 2) + mx]);
-                };
-                for (int j = 0; j < mm; j++) {
-                    L.env[j][0] = at(0, j, 0, 0);
-                    L.env[j][1] = at(0, j, 0, 1);
-                    L.env[j][2] = at(0, j, 1, 0);
-                    L.env[j][3] = at(0, j, 1, 1);
-                    R.env[j][0] = at(1, j, 0, 0);
-                    R.env[j][1] = at(1, j, 0, 1);
-                    R.env[j][2] = at(1, j, 1, 0);
-                    R.env[j][3] = at(1, j, 1, 1);
-                }
-            }
             const int32_t lid = (int32_t)ix->nodes.size();
             ix->nodes.push_back(L);
             ix->nodes.push_back(R);
             ix->nodes[id].left = lid;
             ix->nodes[id].right = lid + 1;
-            // children that must split again need stats next level; fallback
-            // children also need their envelopes from the next level's stats
-            for (int32_t cid : {lid, lid + 1})
-                if (ix->nodes[cid].count > (uint32_t)cfg.tau || best < 0) next.push_back(cid);
+            // every child needs its exact envelope (next level's statistics); those
+            // that overflow also get split there
+            next.push_back(lid);
+            next.push_back(lid + 1);
         }
 
         if (any_part) {
-            DevBuf d_pcol, d_pthr, d_flags, d_scan, d_tmp;
-            SSB_CUDA(d_pcol.alloc(4 * F, s));
-            SSB_CUDA(d_pthr.alloc(8 * F, s));
-            SSB_CUDA(d_flags.alloc(4 * (size_t)(aoff + 1), s));
-            SSB_CUDA(d_scan.alloc(4 * (size_t)(aoff + 1), s));
-            for (int f = 0; f < F; f++)
-                if (!need_split[f] || ix->nodes[frontier[f]].is_leaf) pcol[f] = -1;
+            // nodes that stayed leaves keep their members in place
             SSB_CUDA(cudaMemcpyAsync(d_pcol.p, pcol.data(), 4 * F, cudaMemcpyHostToDevice, s));
-            SSB_CUDA(cudaMemcpyAsync(d_pthr.p, pthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
-            SSB_CUDA(cudaMemsetAsync(d_flags.as<uint32_t>() + aoff, 0, 4, s));
-            build_flags_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
-                                                                   d_stats.as<float>(), d_pcol.as<int32_t>(),
-                                                                   d_pthr.as<double>(), d_flags.as<uint32_t>());
-            SSB_CHECK_LAUNCH();
-            size_t tmp_bytes = 0;
-            SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flags.as<uint32_t>(),
-                                                   d_scan.as<uint32_t>(), (int)(aoff + 1), s));
-            SSB_CUDA(d_tmp.alloc(tmp_bytes, s));
-            SSB_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.p, tmp_bytes, d_flags.as<uint32_t>(),
-                                                   d_scan.as<uint32_t>(), (int)(aoff + 1), s));
-            note_launch(1);
             SSB_CUDA(cudaMemcpyAsync(perm2, perm, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
             build_scatter_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
                                                                      d_pcol.as<int32_t>(), d_flags.as<uint32_t>(),

@@ -262,6 +262,8 @@ int ssb_index_node(const ssb_index *h, int32_t id, ssb_node_t *out)
     out->route_end = t.re;
     out->threshold = t.thr;
     out->gain = t.gain;
+    out->inherited = t.c0;
+    out->split_set = t.split_set;
     return OK;
 }
 

@@ -939,11 +939,13 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     rc = qfill_u32(gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)
     if (rc) return rc;
     // candidates emitted before the pooled bound settles grow with k
-    const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * std::max(8192, 192 * k));
+    int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * std::max(8192, 192 * k));
+    if (const char *e = getenv("SSB_TEST_TC_CAP")) tc_cap = std::max<int64_t>(1, atoll(e));  // test hook
     SSB_CUDA(cand.alloc(8 * (size_t)tc_cap, s));
     SSB_CUDA(clb.alloc(4 * (size_t)tc_cap, s));
     SSB_CUDA(cn.alloc(4, s));
-    const int cap = std::max(16384, 4 * k);
+    int cap = std::max(16384, 4 * k);
+    if (const char *e = getenv("SSB_TEST_SELECT_CAP")) cap = std::max(k, atoi(e));  // test hook
     SSB_CUDA(keys.alloc(8 * (size_t)B * cap, s));
     SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
     SSB_CUDA(thr.alloc(8 * (size_t)B, s));

@@ -26,6 +26,11 @@ struct TreeNode {
     int32_t seg = -1, attr = 0, split = -1, rs = 0, re = 0;
     double thr = 0.0, gain = 0.0;
     int32_t oversize = 0;  // leaf that could not be split (identical members)
+    // insertion-order semantics (build.py:213-263): a node is created holding the
+    // c0 members of its parent's split set routed to it and splits when a later
+    // member makes it exceed tau -- on its first split_set = max(c0+1, tau+1)
+    // members in original order, the set the reference's _split_leaf sees
+    uint32_t c0 = 0, split_set = 0;
 };
 
 struct Index {

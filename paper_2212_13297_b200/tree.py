@@ -54,6 +54,8 @@ class Node:
         self.file_position: tuple[int, int] | None = None
         self.oversize = False
         self.depth = 0
+        self.inherited = 0
+        self.split_set = 0
 
     @property
     def starts(self) -> np.ndarray:
@@ -106,6 +108,8 @@ def tree_from_records(records) -> Node:
         nd.rho = int(r.count)
         nd.is_leaf = bool(r.is_leaf)
         nd.oversize = bool(r.oversize)
+        nd.inherited = int(getattr(r, "inherited", 0))  # members it was created with (parent's split set)
+        nd.split_set = int(getattr(r, "split_set", 0))  # members its policy was chosen on
         nd.depth = int(r.depth)
         nd.file_position = (int(r.first), int(r.count))
         if not nd.is_leaf:

@@ -3,8 +3,11 @@ K-select) on the B200, checked against the oracle and reference goldens.
 
 Bars: ids identical to the oracle's full scan (ties -> lowest index), squared
 distances bit-identical; every split policy identical to the reference's
-get_best_split_policy on the same members (threshold and gain bit-equal);
-envelopes bit-equal to min/max of the members' statistics; words bit-equal.
+get_best_split_policy on the node's split set -- the members the reference's
+sequential insertion build splits on (build.py:213-263): the node's first
+max(inherited + 1, tau + 1) members in original order -- (threshold and gain
+bit-equal); the whole tree identical to a reference-built index; envelopes
+bit-equal to min/max of the members' statistics; words bit-equal.
 """
 
 import os
@@ -64,7 +67,7 @@ def check_tree(ssb, oracle, X, idx, tau, max_policy_checks=10_000):
         first, count = leaf.file_position
         assert first == pos
         pos += count
-        assert count <= tau or leaf.oversize
+        assert count <= tau or leaf.oversize or count == leaf.inherited
     assert pos == N
     for node in idx.root.iter_nodes():
         first, count = node.file_position
@@ -76,8 +79,12 @@ def check_tree(ssb, oracle, X, idx, tau, max_policy_checks=10_000):
         assert np.array_equal(bits(node.sd_min), bits(sd.min(0)))
         assert np.array_equal(bits(node.sd_max), bits(sd.max(0)))
         if not node.is_leaf and checked < max_policy_checks:
-            pol = oracle.best_split(members, node.endpoints, float(node.mu_min[0]),
-                                    float(node.mu_max[0]),
+            S = node.split_set
+            assert S == max(node.inherited + 1, tau + 1) and S <= count
+            split_set = X[np.sort(ids[first:first + count])[:S]]
+            smean, _ = oracle.segment_stats(split_set, node.starts, node.endpoints)
+            pol = oracle.best_split(split_set, node.endpoints, float(smean[:, 0].min()),
+                                    float(smean[:, 0].max()),
                                     allow_vsplit=node.num_segments < 32)
             p = node.policy
             assert (p.segment_index, p.attribute, p.split_point, p.route_start, p.route_end) == (
@@ -85,7 +92,8 @@ def check_tree(ssb, oracle, X, idx, tau, max_policy_checks=10_000):
                 pol["route_end"]), node
             assert p.threshold == pol["threshold"]
             assert p.gain == pol["gain"]
-            assert node.left.rho == pol["n_left"]
+            assert node.left.inherited == pol["n_left"]
+            assert node.right.inherited == S - pol["n_left"]
             assert node.left.file_position[1] + node.right.file_position[1] == count
             checked += 1
     return checked
@@ -203,6 +211,38 @@ def test_engine_matches_reference_engine_golden(ssb):
         res = eng.exact_knn_batch(g["queries"], ssb.QueryConfig(k=k))
         got = np.array([r.distances_sq() for r, _ in res], np.float32)
         assert np.array_equal(bits(got), bits(g[f"d2_k{k}"])), k
+
+
+def test_build_reproduces_reference_built_tree(ssb):
+    """The reference's build_index (one insert worker: sequential insertion in
+    file order) wrote tests/golden/ref_index_1500x64 from the same 1500 series;
+    the level-synchronous GPU build must give the same tree: node by node the
+    same structure, segmentations, policies (threshold bits) and envelopes, and
+    leaf by leaf the same series in the same order."""
+    g = golden("engine")
+    qi = ssb.load_index(os.path.join(GOLDEN, "ref_index_1500x64"))
+    ours = build(ssb, g["data"], 64)
+    rows, _, _ = ours.host_arrays()
+    ref_rows = qi.store.data
+
+    def walk(a, b, path="root"):
+        assert a.is_leaf == b.is_leaf, path
+        assert np.array_equal(a.endpoints, b.endpoints), path
+        for f in ("mu_min", "mu_max", "sd_min", "sd_max"):
+            assert np.array_equal(bits(getattr(a, f)), bits(getattr(b, f))), (path, f)
+        fa, ca = a.file_position
+        fb, cb = b.file_position
+        assert ca == cb, path
+        if a.is_leaf:
+            assert np.array_equal(rows[fa:fa + ca], ref_rows[fb:fb + cb]), path
+            return 1
+        pa, pb = a.policy, b.policy
+        assert (pa.segment_index, pa.attribute, pa.split_point, pa.route_start, pa.route_end) == (
+            pb.segment_index, pb.attribute, pb.split_point, pb.route_start, pb.route_end), path
+        assert pa.threshold == pb.threshold, path
+        return walk(a.left, b.left, path + "L") + walk(a.right, b.right, path + "R")
+
+    assert walk(ours.root, qi.root) == qi.total_leaves
 
 
 def test_reference_written_index_loads_and_answers(ssb, oracle):

@@ -108,3 +108,50 @@ def test_tensor_route_small_and_ragged(ssb, oracle, N, k):
     d2, ids, _, st = ssb.QueryEngine(idx).knn_device(Q, k, want_stats=True, route="tensor")
     assert np.array_equal(ids.cpu().numpy(), oid)
     assert (st[:, 1] <= N).all()
+
+
+@pytest.mark.parametrize("k", [33, 100, 300])
+def test_tensor_route_large_k_buckets(ssb, oracle, k):
+    """k > 32: no per-thread list, only the pooled bucket bound; 300 queries
+    span three query blocks (one padded)."""
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(20_000, 128, 4, workers=4)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=128, dataset_size=len(X), leaf_threshold=800))
+    Q = np.concatenate([G.noise_queries(X, 200, 0.1, 5), random_walks(100, 128, 6)])
+    d2, ids, _ = ssb.QueryEngine(idx).knn_device(Q, k, route="tensor")
+    od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+@pytest.mark.parametrize("N,k", [(300, 32), (1000, 31), (2000, 2), (517, 17)])
+def test_tensor_route_warmup_revisits(ssb, oracle, N, k):
+    """Few tiles per CTA: the warm-up tiles are rescanned; their rows must not
+    enter a thread's own top-k list twice."""
+    X = random_walks(N, 96, 11)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=96, dataset_size=N, leaf_threshold=50))
+    Q = np.concatenate([X[:5] + 0.01, random_walks(60, 96, 12)]).astype(np.float32)
+    d2, ids, _ = ssb.QueryEngine(idx).knn_device(Q, k, route="tensor")
+    od2, oid = oracle.knn_scan(X, Q, k)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+@pytest.mark.parametrize("hook,value", [("SSB_TEST_TC_CAP", "300"), ("SSB_TEST_TC_CAP", "1"),
+                                        ("SSB_TEST_SELECT_CAP", "12")])
+def test_tensor_route_overflow_paths(ssb, oracle, monkeypatch, hook, value):
+    """Candidate-buffer overflow: retried with the filter's final bounds, then
+    (still overflowing) answered on the general path; a select overflow goes
+    to the general path too.  Answers stay exact."""
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(8000, 256, 13, workers=4)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=400))
+    Q = np.concatenate([G.noise_queries(X, 30, 1.0, 14), G.noise_queries(X, 10, 0.01, 15)])
+    monkeypatch.setenv(hook, value)
+    for k in (1, 10):
+        d2, ids, _ = ssb.QueryEngine(idx).knn_device(Q, k, route="tensor")
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid), (hook, value, k)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2)), (hook, value, k)

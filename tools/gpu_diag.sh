@@ -1,3 +1,2 @@
-SSB_TC_TRACE=1 timeout 900 python bench.py --workload c4 --route tensor --steps 1 --warmup 1 --cpu-sample 0 > gpurun_out/b_c4_tensor.json 2> gpurun_out/b_c4_tensor.err
-grep ssb gpurun_out/b_c4_tensor.err | head
-SSB_TC_TRACE=1 timeout 900 python bench.py --workload c2 --steps 1 --warmup 1 --cpu-sample 0 2>&1 >/dev/null | grep ssb | head -20
+timeout 900 python -m pytest tests/test_gpu_index.py tests/test_gpu_tc.py -q -x 2>&1 | grep -v "Warning\|popen\|self.pid\|^$" | tail -25
+timeout 600 python tools/build_profile.py --rows 10000000 2>&1 | tail -1
