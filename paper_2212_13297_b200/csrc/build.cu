@@ -15,9 +15,11 @@
 // Per level (host loop, a few launches each):
 //   K-stats      member stats over base segments and both halves (f64 prefix
 //                sums, persist-exact), column-major per node
-//   K-minmax     per (node, stat column) min/max  -> envelopes, thresholds
+//   K-minmax     per (node, stat column) min/max over all members -> envelopes,
+//                and over the split set -> thresholds
 //   K-thr        per (node, candidate) threshold = (vmin+vmax)/2 (f64)
 //   K-eval       per (node, candidate, side, result column) min/max + n_left
+//                over the split set (the members the reference splits on)
 //   K-gain       per node: QoS gains (f64, numpy pairwise order), argmax
 //   K-part       stable partition of the split nodes' members (CUB scan)
 // Finally K-gather writes the rows, ids and words in leaf order.
@@ -178,36 +180,6 @@ __global__ void __launch_bounds__(CHUNK)
     if (bad) atomicOr(nonfinite, 1);
 }
 
-// K-minmax: per (node, column) min/max over members (ordered-int atomics)
-__global__ void __launch_bounds__(CHUNK)
-    build_minmax_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
-                        const float *__restrict__ stats, uint32_t *__restrict__ cmin,
-                        uint32_t *__restrict__ cmax, int subset)
-{
-    // subset = 0: every member (node envelopes); 1: the split set only (thresholds)
-    const Chunk ch = chunks[blockIdx.x];
-    const NodeDesc nd = nodes[ch.node];
-    const uint32_t limit = subset ? nd.ecount : nd.count;
-    if (ch.m0 >= limit) return;
-    const int t = threadIdx.x, lane = t & 31;
-    const bool live = t < (int)ch.cnt && ch.m0 + (uint32_t)t < limit;
-    if (!__any_sync(0xffffffffu, live)) return;  // whole warp past the limit
-    const int ncol = 6 * nd.m;
-    for (int col = 0; col < ncol; col++) {
-        const int seg = col % nd.m;
-        const int sa = seg ? nd.ep[seg - 1] : 0;
-        if (col >= 2 * nd.m && nd.ep[seg] - sa < 2) continue;  // no halves
-        float v = live ? stats[nd.stat_off + (int64_t)col * nd.count + ch.m0 + t] : 0.f;
-        uint32_t k = okey(v);
-        uint32_t kmin = __reduce_min_sync(0xffffffffu, live ? k : 0xffffffffu);
-        uint32_t kmax = __reduce_max_sync(0xffffffffu, live ? k : 0u);
-        if (lane == 0) {
-            atomicMin(&cmin[nd.col_off + col], kmin);
-            atomicMax(&cmax[nd.col_off + col], kmax);
-        }
-    }
-}
-
 // candidate c of a node (tree.py:220-237 order): seg = c/6, r = c%6,
 // attr = r/3 (0 mean, 1 sd), lay = r%3 (0 horizontal, 1 left half, 2 right half)
 __device__ __forceinline__ int route_col(int m, int c)
@@ -273,53 +245,135 @@ __device__ __forceinline__ int64_t acc_index(int c, int side, int j, int attr, i
 }
 constexpr int ACC_PER_CAND = 2 * (M_MAX + 1) * 2 * 2;
 
-// K-eval: grid (chunk, candidate batch).  Per valid candidate: side of every
-// member, masked min/max of every result column on both sides, n_left.
-constexpr int CAND_BATCH = 6;
+// ---- range kernels: a CTA reduces a long member range in registers/shared
+// memory and touches each global accumulator once (an atomic per warp per
+// column would serialise on the same few addresses)
+constexpr int RTHREADS = 256;
+constexpr uint32_t MM_RANGE = 65536;   // members per CTA in K-minmax
+constexpr uint32_t EV_PER_THREAD = 16;  // members per thread in K-eval
+constexpr uint32_t EV_RANGE = RTHREADS * EV_PER_THREAD;
 
-__global__ void __launch_bounds__(CHUNK)
-    build_eval_kernel(const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
-                      const float *__restrict__ stats, const double *__restrict__ thr,
-                      const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
-                      uint32_t *__restrict__ nleft)
+struct Range {
+    uint32_t node;
+    uint32_t m0;
+    uint32_t cnt;
+};
+
+template <bool MAX>
+__device__ __forceinline__ uint32_t block_reduce_u32(uint32_t v, uint32_t *sh)
 {
-    const Chunk ch = chunks[blockIdx.x];
-    const NodeDesc nd = nodes[ch.node];
-    const int c0 = blockIdx.y * CAND_BATCH;
-    if (c0 >= 6 * nd.m || ch.m0 >= nd.ecount) return;  // only the split set is evaluated
-    const int t = threadIdx.x, lane = t & 31;
-    const bool live = t < (int)ch.cnt && ch.m0 + (uint32_t)t < nd.ecount;
-    if (!__any_sync(0xffffffffu, live)) return;
-    const float *st = stats + nd.stat_off + ch.m0 + t;
-    uint32_t *nacc = acc + nd.acc_off;
-    for (int c = c0; c < min(c0 + CAND_BATCH, 6 * nd.m); c++) {
-        if (!valid[nd.col_off + c]) continue;
-        const int rc = route_col(nd.m, c);
-        const double th = thr[nd.col_off + c];
-        const float rv = live ? st[(int64_t)rc * nd.count] : 0.f;
-        const bool left = live && ((double)rv < th);
-        const unsigned bl = __ballot_sync(0xffffffffu, left);
-        if (lane == 0) atomicAdd(&nleft[nd.col_off + c], (unsigned)__popc(bl));
-        const int seg = c / 6, lay = (c % 6) % 3;
-        const int mm = nd.m + (lay ? 1 : 0);
-        (void)seg;
-        for (int j = 0; j < mm; j++) {
-            int cmean, csd, w;
-            result_col(nd, c, j, cmean, csd, w);
+    v = MAX ? __reduce_max_sync(0xffffffffu, v) : __reduce_min_sync(0xffffffffu, v);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : (MAX ? 0u : 0xffffffffu);
+        v = MAX ? __reduce_max_sync(0xffffffffu, v) : __reduce_min_sync(0xffffffffu, v);
+    }
+    return v;  // valid in thread 0
+}
+
+// K-minmax: grid (range, column); the ranges cover every member (envelopes) or
+// the split sets (policy thresholds)
+__global__ void __launch_bounds__(RTHREADS)
+    build_minmax_range_kernel(const NodeDesc *__restrict__ nodes, const Range *__restrict__ ranges,
+                              const float *__restrict__ stats, uint32_t *__restrict__ cmin,
+                              uint32_t *__restrict__ cmax)
+{
+    __shared__ uint32_t sh[RTHREADS / 32];
+    const Range rg = ranges[blockIdx.x];
+    const NodeDesc nd = nodes[rg.node];
+    const int col = blockIdx.y;
+    if (col >= 6 * nd.m) return;
+    const int seg = col % nd.m;
+    const int sa = seg ? nd.ep[seg - 1] : 0;
+    if (col >= 2 * nd.m && nd.ep[seg] - sa < 2) return;  // no halves
+    const float *v = stats + nd.stat_off + (int64_t)col * nd.count + rg.m0;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (uint32_t i = threadIdx.x; i < rg.cnt; i += RTHREADS) {
+        const uint32_t k = okey(v[i]);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+    }
+    kmin = block_reduce_u32<false>(kmin, sh);
+    kmax = block_reduce_u32<true>(kmax, sh);
+    if (threadIdx.x == 0) {
+        atomicMin(&cmin[nd.col_off + col], kmin);
+        atomicMax(&cmax[nd.col_off + col], kmax);
+    }
+}
+
+// K-eval: grid (split-set range, candidate).  Each thread holds 16 members'
+// sides in a bit mask; per result column both sides' min/max are reduced in
+// the block and merged into the candidate's accumulators once.
+__global__ void __launch_bounds__(RTHREADS)
+    build_eval_range_kernel(const NodeDesc *__restrict__ nodes, const Range *__restrict__ ranges,
+                            const float *__restrict__ stats, const double *__restrict__ thr,
+                            const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
+                            uint32_t *__restrict__ nleft)
+{
+    __shared__ uint32_t sh[RTHREADS / 32];
+    const Range rg = ranges[blockIdx.x];
+    const NodeDesc nd = nodes[rg.node];
+    const int c = blockIdx.y;
+    if (c >= 6 * nd.m || !valid[nd.col_off + c]) return;
+    const int t = threadIdx.x;
+    const int64_t cnt = nd.count;
+    const float *st = stats + nd.stat_off + rg.m0;
+    const double th = thr[nd.col_off + c];
+    const float *rv = st + (int64_t)route_col(nd.m, c) * cnt;
+    uint32_t lmask = 0, live = 0;
 #pragma unroll
-            for (int attr = 0; attr < 2; attr++) {
-                const float v = live ? st[(int64_t)(attr ? csd : cmean) * nd.count] : 0.f;
-                const uint32_t k = okey(v);
-                const uint32_t lmin = __reduce_min_sync(0xffffffffu, (live && left) ? k : 0xffffffffu);
-                const uint32_t lmax = __reduce_max_sync(0xffffffffu, (live && left) ? k : 0u);
-                const uint32_t rmin = __reduce_min_sync(0xffffffffu, (live && !left) ? k : 0xffffffffu);
-                const uint32_t rmax = __reduce_max_sync(0xffffffffu, (live && !left) ? k : 0u);
-                if (lane == 0) {
-                    atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin);
-                    atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax);
-                    atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin);
-                    atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax);
+    for (uint32_t r = 0; r < EV_PER_THREAD; r++) {
+        const uint32_t i = r * RTHREADS + t;
+        if (i < rg.cnt) {
+            live |= 1u << r;
+            if ((double)rv[i] < th) lmask |= 1u << r;
+        }
+    }
+    {   // n_left
+        uint32_t nl = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(lmask));
+        __syncthreads();
+        if ((t & 31) == 0) sh[t >> 5] = nl;
+        __syncthreads();
+        if (t == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < RTHREADS / 32; w++) tot += sh[w];
+            atomicAdd(&nleft[nd.col_off + c], tot);
+        }
+    }
+    uint32_t *nacc = acc + nd.acc_off;
+    const int lay = (c % 6) % 3;
+    const int mm = nd.m + (lay ? 1 : 0);
+    for (int j = 0; j < mm; j++) {
+        int cmean, csd, w;
+        result_col(nd, c, j, cmean, csd, w);
+#pragma unroll
+        for (int attr = 0; attr < 2; attr++) {
+            const float *cv = st + (int64_t)(attr ? csd : cmean) * cnt;
+            uint32_t lmin = 0xffffffffu, lmax = 0u, rmin = 0xffffffffu, rmax = 0u;
+#pragma unroll
+            for (uint32_t r = 0; r < EV_PER_THREAD; r++) {
+                if (!(live >> r & 1u)) continue;
+                const uint32_t k = okey(cv[r * RTHREADS + t]);
+                if (lmask >> r & 1u) {
+                    lmin = min(lmin, k);
+                    lmax = max(lmax, k);
+                } else {
+                    rmin = min(rmin, k);
+                    rmax = max(rmax, k);
                 }
+            }
+            lmin = block_reduce_u32<false>(lmin, sh);
+            lmax = block_reduce_u32<true>(lmax, sh);
+            rmin = block_reduce_u32<false>(rmin, sh);
+            rmax = block_reduce_u32<true>(rmax, sh);
+            if (t == 0) {
+                atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin);
+                atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax);
+                atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin);
+                atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax);
             }
         }
     }
@@ -510,16 +564,6 @@ __global__ void fill_acc_kernel(uint32_t *p, int64_t count)
     if (i < count) p[i] = (i & 1) ? 0u : 0xffffffffu;
 }
 
-// copy the winning candidate's accumulator block of every split node
-__global__ void gather_winner_acc_kernel(const NodeDesc *__restrict__ nodes, const NodeResult *__restrict__ res,
-                                         const uint32_t *__restrict__ acc, uint32_t *__restrict__ out)
-{
-    const int f = blockIdx.x;
-    const int best = res[f].best;
-    for (int i = threadIdx.x; i < ACC_PER_CAND; i += blockDim.x)
-        out[(int64_t)f * ACC_PER_CAND + i] = best >= 0 ? acc[nodes[f].acc_off + (int64_t)best * ACC_PER_CAND + i] : 0u;
-}
-
 __global__ void iota_u32_kernel(uint32_t *p, int64_t count)
 {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -655,6 +699,27 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         }
         const int64_t nchunks = (int64_t)chunks.size();
         SSB_REQUIRE(nchunks < (1ll << 31), "too many member chunks in one level");
+        // long ranges for the reductions: all members, the split sets (min/max),
+        // the split sets in K-eval granules
+        std::vector<Range> r_all, r_ss, r_ev;
+        int maxm = 1;
+        for (int f = 0; f < F; f++) {
+            maxm = std::max(maxm, nd[f].m);
+            for (uint32_t m0 = 0; m0 < nd[f].count; m0 += MM_RANGE)
+                r_all.push_back({(uint32_t)f, m0, std::min<uint32_t>(MM_RANGE, nd[f].count - m0)});
+            for (uint32_t m0 = 0; m0 < nd[f].ecount; m0 += MM_RANGE)
+                r_ss.push_back({(uint32_t)f, m0, std::min<uint32_t>(MM_RANGE, nd[f].ecount - m0)});
+            for (uint32_t m0 = 0; m0 < nd[f].ecount; m0 += EV_RANGE)
+                r_ev.push_back({(uint32_t)f, m0, std::min<uint32_t>(EV_RANGE, nd[f].ecount - m0)});
+        }
+        std::vector<Range> r_cat(r_all);
+        r_cat.insert(r_cat.end(), r_ss.begin(), r_ss.end());
+        r_cat.insert(r_cat.end(), r_ev.begin(), r_ev.end());
+        DevBuf d_ranges;
+        SSB_CUDA(d_ranges.alloc(sizeof(Range) * r_cat.size(), s));
+        SSB_CUDA(cudaMemcpyAsync(d_ranges.p, r_cat.data(), sizeof(Range) * r_cat.size(), cudaMemcpyHostToDevice, s));
+        const Range *d_r_all = d_ranges.as<Range>(), *d_r_ss = d_r_all + r_all.size(),
+                    *d_r_ev = d_r_ss + r_ss.size();
         DevBuf d_nodes, d_chunks, d_stats, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
         SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
@@ -675,9 +740,8 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         }
         SSB_CHECK_LAUNCH();
         // exact envelopes over every member
-        build_minmax_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
-                                                                d_stats.as<float>(), d_cmin.as<uint32_t>(),
-                                                                d_cmax.as<uint32_t>(), 0);
+        build_minmax_range_kernel<<<dim3((unsigned)r_all.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
+            d_nodes.as<NodeDesc>(), d_r_all, d_stats.as<float>(), d_cmin.as<uint32_t>(), d_cmax.as<uint32_t>());
         SSB_CHECK_LAUNCH();
 
         std::vector<NodeResult> res(F);
@@ -697,24 +761,19 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             // accumulators: even slots are minima (+inf key), odd slots maxima (0)
             fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
             SSB_CHECK_LAUNCH();
-            build_minmax_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
-                                                                    d_stats.as<float>(), d_emin.as<uint32_t>(),
-                                                                    d_emax.as<uint32_t>(), 1);
+            build_minmax_range_kernel<<<dim3((unsigned)r_ss.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
+                d_nodes.as<NodeDesc>(), d_r_ss, d_stats.as<float>(), d_emin.as<uint32_t>(), d_emax.as<uint32_t>());
             SSB_CHECK_LAUNCH();
             build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_emin.as<uint32_t>(),
                                               d_emax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
             SSB_CHECK_LAUNCH();
-            int maxm = 1;
-            for (auto &d : nd) maxm = std::max(maxm, d.m);
-            dim3 eg((unsigned)nchunks, (unsigned)((6 * maxm + CAND_BATCH - 1) / CAND_BATCH));
             {
                 double ev = 0.0;
                 for (int f = 0; f < F; f++) ev += (double)nd[f].ecount * 6 * nd[f].m * 4;
                 ProfScope ps("build_eval", s, ev);
-                build_eval_kernel<<<eg, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
-                                                       d_stats.as<float>(), d_thr.as<double>(),
-                                                       d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
-                                                       d_nleft.as<uint32_t>());
+                build_eval_range_kernel<<<dim3((unsigned)r_ev.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
+                    d_nodes.as<NodeDesc>(), d_r_ev, d_stats.as<float>(), d_thr.as<double>(), d_valid.as<int32_t>(),
+                    d_acc.as<uint32_t>(), d_nleft.as<uint32_t>());
             }
             SSB_CHECK_LAUNCH();
             build_gain_kernel<<<F, 32, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_thr.as<double>(),
