@@ -3,13 +3,15 @@
 // Replaces the reference's per-series insertion build (build.py:213-263
 // insert_series_to_node/_split_leaf, tree.py:182-208 routing/widening) and the
 // write-time synopsis repair (persist.py:145-233 vsplit/hsplit_synopsis).
-// Every node with more than tau members is split using the reference's own
-// policy choice -- tree.py:211-336 get_best_split_policy (candidates in the
-// same order, same float32 statistics, same float64 thresholds and QoS gains,
-// first strict maximum) -- evaluated over ALL of the node's members, then
-// its members are stably partitioned (tree.py:339-381 split_node).  Children
-// envelopes are exact min/max over their members, so no synopsis repair is
-// needed.  Leaves come out contiguous and in in-order (left-to-right) order,
+// The tree is the one the reference's sequential insertion build produces: a
+// node created with `inherited` members of its parent's split set splits once a
+// later member (original order) makes it exceed tau, on its split set = its
+// first max(inherited+1, tau+1) members, with the reference's own policy choice
+// -- tree.py:211-336 get_best_split_policy (candidates in the same order, same
+// float32 statistics, same float64 thresholds and QoS gains, first strict
+// maximum) -- and then ALL its members are stably partitioned by that policy
+// (tree.py:339-381 split_node).  Envelopes are exact min/max over all members,
+// so no synopsis repair is needed.  Leaves come out contiguous and in in-order (left-to-right) order,
 // the reference's lrd.bin layout (persist.py:5-9).
 //
 // Per level (host loop, a few launches each):
