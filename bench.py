@@ -415,6 +415,15 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
         roof.update({"share_of_step": round(kms / ms, 4), "avg_launch_ms": round(kms / klaunch, 4)})
+        # DRAM traffic per launch of this kernel from a committed `ncu --set full`
+        # capture of the same workload (profiles/traffic.json), when there is one
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(wl.name, {})
+            if tr.get("kernel") == name:
+                roof["traffic"] = tr["bytes_per_launch"]
+                roof["traffic_source"] = tr["source"]
+        except (OSError, ValueError, KeyError):
+            pass
     cb = None
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(wl, X, cellq, args.cpu_sample)
