@@ -915,7 +915,7 @@ static int qfill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
 // answers the batch on the general path, which tightens bounds and rescans).
 static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_t *out_keys, uint32_t *st_cand_leaves,
                           uint32_t *st_cand_series, uint32_t *st_seed_rows, uint32_t *st_over, uint32_t leaves_nonempty,
-                          bool *redo, cudaStream_t s)
+                          bool want_stats, bool *redo, cudaStream_t s)
 {
     const int n = ix.n;
     *redo = false;
@@ -965,13 +965,15 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     rc = launch_rescore(ix.X, n, ix.orig, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
                         gb.as<unsigned int>(), tc_cap, so, s, cn.as<unsigned int>());
     if (rc) return rc;
-    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
-    tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(cand.as<uint2>(), cn.as<unsigned int>(), tc_cap,
-                                                                   st_cand_series);
-    SSB_CHECK_LAUNCH();
-    rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
-    if (rc) return rc;
-    SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
+    if (want_stats) {  // QueryStats only
+        SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
+        tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(cand.as<uint2>(), cn.as<unsigned int>(),
+                                                                       tc_cap, st_cand_series);
+        SSB_CHECK_LAUNCH();
+        rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
+        if (rc) return rc;
+        SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
+    }
     SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
     rc = launch_select(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
                        flags.as<int32_t>(), s);
@@ -1058,7 +1060,7 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
             bool redo = false;
             const int rc1 = query_batch_tc(ix, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
                                            stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0,
-                                           sto.as<uint32_t>() + q0, leaves_nonempty, &redo, s);
+                                           sto.as<uint32_t>() + q0, leaves_nonempty, stats_host != nullptr, &redo, s);
             if (rc1) return rc1;
             if (!redo) {
                 q0 += nb;

@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             stage_n = 0;
         };
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
-        const bool diag_skip = p.skip_epi == 1 || p.skip_epi >= 3;
+        const bool diag_skip = p.skip_epi == 1 || p.skip_epi == 3 || p.skip_epi == 4;
         for (int t = 0; t < niter; t++) {
             const int s = t % TC_NACC;
             const int rs = t % TC_RS;
@@ -836,7 +836,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     }
     p.k = k;
     p.c_rel = tc_c_rel();
-    p.warm = 2;
+    p.warm = 4;
+    if (const char *e = getenv("SSB_TC_WARM")) p.warm = std::max(0, atoi(e));  // diagnostics
     p.cand = cand;
     p.cand_lb = cand_lb;
     p.cand_n = cand_n;

@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_index.py -q -x 2>&1 | tail -1
-timeout 600 python tools/build_profile.py --rows 10000000 2>&1 | tail -1
-SSB_BUILD_TRACE=1 timeout 900 python tools/build_profile.py --rows 20000000 --tau 100000 2>&1 | grep -v "^\[ssb build\] level" | tail -6
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+for w in c2 c1 c3; do
+  timeout 600 python bench.py --workload $w > gpurun_out/b_$w.json 2> gpurun_out/b_$w.err
+  python -c "
+import json; j=json.load(open('gpurun_out/b_$w.json')); print('$w', j['value'], j['e2e']['value'], j['ms_per_step'], j['roofline']['frac'], j['roofline'].get('traffic'), j['build']['series_per_s'], {k:(round(v['ms'],1),v['launches']) for k,v in j['kernels'].items()})"
+done
