@@ -828,7 +828,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     p.gbound = gbound;
     p.gbucket = nullptr;
     DevBuf buckets;
-    if (k >= 2 && !dump) {
+    if (k >= 2 && !dump && !(getenv("SSB_TC_NOBUCKET") && k <= TC_KTOP)) {  // env: diagnostics
         const size_t bytes = 4 * (size_t)tc_bound_slots(nq) * (size_t)k;
         SSB_CUDA(buckets.alloc(bytes, s));
         SSB_CUDA(cudaMemsetAsync(buckets.p, 0xff, bytes, s));  // unset (NaN bits; atomicMin on the bits)
