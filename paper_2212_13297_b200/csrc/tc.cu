@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(r_empty + TC_RS);
     uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [8 warps][TC_STAGE]
     float *s_stage_lb = reinterpret_cast<float *>(s_stage + 8 * TC_STAGE);  // [8 warps][TC_STAGE]
+    unsigned *s_fill = reinterpret_cast<unsigned *>(s_stage_lb + 8 * TC_STAGE);  // [8 warps]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int CS = p.CS;
@@ -446,19 +447,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         bool touched = false;
         uint2 *stage = s_stage + ew * TC_STAGE;
         float *stage_lb = s_stage_lb + ew * TC_STAGE;
-        unsigned stage_n = 0;  // warp-uniform
-        auto flush = [&]() {
+        unsigned *stage_fill = s_fill + ew;  // reserved slots of this warp's stage (may pass TC_STAGE)
+        if (lane == 0) *stage_fill = 0;
+        __syncwarp();
+        auto flush = [&]() {  // warp-uniform
+            const unsigned n_st = min(*(volatile unsigned *)stage_fill, (unsigned)TC_STAGE);
             unsigned base_slot = 0;
-            if (lane == 0 && stage_n) base_slot = atomicAdd(p.cand_n, stage_n);
+            if (lane == 0 && n_st) base_slot = atomicAdd(p.cand_n, n_st);
             base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
-            __syncwarp();
-            for (unsigned i = lane; i < stage_n; i += 32)
+            for (unsigned i = lane; i < n_st; i += 32)
                 if ((int64_t)(base_slot + i) < p.cand_cap) {
                     p.cand[base_slot + i] = stage[i];
                     p.cand_lb[base_slot + i] = stage_lb[i];
                 }
             __syncwarp();
-            stage_n = 0;
+            if (lane == 0) *stage_fill = 0;
+            __syncwarp();
         };
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
         const bool diag_skip = p.skip_epi == 1 || p.skip_epi == 3 || p.skip_epi == 4;
@@ -573,46 +577,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         }
                         emit &= (uint32_t)(valid >> c0) & 0xffffu;
                     }
-                    if (!__any_sync(0xffffffffu, emit != 0)) continue;
-                    // warp-staged emission of (query, row) candidates
-                    unsigned cnt = __popc(emit);
-                    unsigned incl = cnt;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
-                        if (lane >= off) incl += y;
-                    }
-                    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-                    if (stage_n + total > TC_STAGE) flush();
-                    if (total > TC_STAGE) {  // pathological: write through
-                        unsigned b0 = 0;
-                        if (lane == 31) b0 = atomicAdd(p.cand_n, total);
-                        b0 = __shfl_sync(0xffffffffu, b0, 31);
-                        unsigned slot = b0 + incl - cnt;
+                    if (p.skip_epi == 10) continue;  // diagnostics: no emission stage
+                    // emission of (query, row, LB): every lane with candidates reserves
+                    // its slots in the warp's stage with one shared-memory atomic (no
+                    // warp scan on the epilogue's critical path); a reservation crossing
+                    // the stage end fills it and writes the rest straight to global
+                    if (emit) {
+                        const unsigned cnt = __popc(emit);
+                        unsigned slot = atomicAdd(stage_fill, cnt);
+                        unsigned gslot = 0;
+                        if (slot + cnt > (unsigned)TC_STAGE)
+                            gslot = atomicAdd(p.cand_n, slot + cnt - max(slot, (unsigned)TC_STAGE));
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
-                            if ((int64_t)slot < p.cand_cap) {
-                                p.cand[slot] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
-                                p.cand_lb[slot] = row_lb(c0, i);
+                            const float lbv = row_lb(c0, i);
+                            const uint2 cv = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
+                            if (slot < (unsigned)TC_STAGE) {
+                                stage_lb[slot] = lbv;
+                                stage[slot] = cv;
+                            } else if ((int64_t)gslot < p.cand_cap) {
+                                p.cand[gslot] = cv;
+                                p.cand_lb[gslot] = lbv;
+                                gslot++;
+                            } else {
+                                gslot++;
                             }
                             slot++;
                         }
-                    } else {
-                        unsigned slot = stage_n + incl - cnt;
-                        while (emit) {
-                            const int i = __ffs(emit) - 1;
-                            emit &= emit - 1;
-                            stage_lb[slot] = row_lb(c0, i);
-                            stage[slot++] = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
-                        }
-                        stage_n += total;
                     }
                 }
             }
             // the tile slot (row constants) is no longer read by this warp
             __syncwarp();
             if (lane == 0) mbar_arrive(&r_empty[rs]);
+            // drain the stage once it is half full (a tile adds at most 4 x 32 x 16
+            // entries; reservations past its end already went to global memory)
+            if (*(volatile unsigned *)stage_fill >= (unsigned)(TC_STAGE / 2)) flush();
             // refresh the bucket bound after this thread's own updates
             // (every 8th tile; the loads are independent so their latencies overlap)
             if (touched && ((t & 7) == 7 || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
@@ -848,7 +849,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         p.skip_epi = d ? atoi(d) : 0;
     }
     const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
-                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12;
+                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 32;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
