@@ -880,6 +880,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         rc = go(tc_filter_kernel<1>);
     else if (k <= 4)
         rc = go(tc_filter_kernel<4>);
+    else if (k <= 8)
+        rc = go(tc_filter_kernel<8>);
+    else if (k <= 10)
+        rc = go(tc_filter_kernel<10>);  // the configs' k = 10: no idle stages in the insertion network
     else if (k <= 16)
         rc = go(tc_filter_kernel<16>);
     else if (k <= 32)
