@@ -273,13 +273,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (ntile > 0) {
-            // ring of K-chunk slots: chunk c = t*KB + kb -> slot c % NSLOT, use c / NSLOT
+            // ring of tile slots: a slot holds a whole B tile (KB K-chunks of 16 KB);
+            // tile t -> slot t % NS, one barrier wait / commit per tile
+            const int NS = TC_NSLOT / KB;
+            const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
             const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sRing);
             const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(b_full);
             const uint32_t rfull0 = (uint32_t)__cvta_generic_to_shared(r_full);
             const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(slots);
             const int srows = TC_BN / CS;
-            uint32_t slot = 0, phase = 0, c = 0;
+            int slot = 0;
+            uint32_t phase = 0;
             for (int t = 0; t < niter; t++) {
                 const int64_t tile = tile_of(t);
                 // side data of this tile: row constants, half-tile extremes, bounds snapshot
@@ -300,34 +304,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         : "memory");
                 }
                 const int row0 = (int)(tile * TC_BN) + rank * srows;
-                for (int kb = 0; kb < KB; kb++, c++) {
-                    if (c >= (uint32_t)TC_NSLOT) {
-                        if (p.skip_epi == 3) break;  // diagnostics: MMA on stale slots only
-                        mbar_wait(&b_empty[slot], phase ^ 1u);
-                    }
-                    const uint32_t dst = ring + slot * chunk_bytes + (uint32_t)(rank * srows * 128);
-                    const uint32_t bar = full0 + slot * 8;
-                    // the whole chunk (every CTA's slice) lands in this CTA's slot
+                if (t >= NS) mbar_wait(&b_empty[slot], phase ^ 1u);
+                const uint32_t bar = full0 + (uint32_t)slot * 8;
+                const uint32_t dst0 = ring + (uint32_t)slot * tile_bytes + (uint32_t)(rank * srows * 128);
+                // the whole tile (every CTA's row slice of every K-chunk) lands in this CTA's slot
+                asm volatile(
+                    "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                    "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
+                    "r"(tile_bytes)
+                    : "memory");
+                for (int kb = 0; kb < KB; kb++) {
+                    const uint32_t dst = dst0 + (uint32_t)kb * chunk_bytes;
                     if (CS == 1)
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %4;\n"
                             "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%5, {%2, %3}], [%1];\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * 64), "r"(row0), "r"(chunk_bytes), "l"(&mapB)
+                            " [%0], [%4, {%2, %3}], [%1];\n}" ::"r"(dst),
+                            "r"(bar), "r"(kb * 64), "r"(row0), "l"(&mapB)
                             : "memory");
                     else
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %4;\n"
                             "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            ".multicast::cluster [%0], [%5, {%2, %3}], [%1], %6;\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * 64), "r"(row0), "r"(chunk_bytes), "l"(&mapB), "h"(cmask)
+                            ".multicast::cluster [%0], [%4, {%2, %3}], [%1], %5;\n}" ::"r"(dst),
+                            "r"(bar), "r"(kb * 64), "r"(row0), "l"(&mapB), "h"(cmask)
                             : "memory");
-                    if (++slot == (uint32_t)TC_NSLOT) {
-                        slot = 0;
-                        phase ^= 1u;
-                    }
+                }
+                if (++slot == NS) {
+                    slot = 0;
+                    phase ^= 1u;
                 }
             }
         }
@@ -336,56 +341,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (ntile > 0) {
             mbar_wait(a_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
+            const int NS = TC_NSLOT / KB;
+            const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
             const uint32_t a_tmem = tmem_base + TC_NACC * TC_BN;  // 8 columns per K=16 step
             const uint64_t bdesc0 = umma_desc_sw128((uint32_t)__cvta_generic_to_shared(sRing));
             const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
             const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
-            uint32_t slot = 0, phase = 0, c = 0;
+            int slot = 0;
+            uint32_t phase = 0;
             for (int t = 0; t < niter; t++) {
                 const int s = t % TC_NACC;
                 if (t >= TC_NACC) mbar_wait(&t_empty[s], (unsigned)(((t / TC_NACC) - 1) & 1));
+                mbar_wait(&b_full[slot], phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
-                for (int kb = 0; kb < KB; kb++, c++) {
-                    if (p.skip_epi != 3 || c < (uint32_t)TC_NSLOT) mbar_wait(&b_full[slot], phase);
-                    if (p.skip_epi == 4) {  // diagnostics (CS == 1): TMA stream only, no MMA
-                        if (lane == 0) mbar_arrive(&b_empty[slot]);
-                    } else {
-                        asm volatile("tcgen05.fence::after_thread_sync;");
-                        // descriptor start address advances 32 B (>> 4 = 2) per K=16 step
-                        const uint64_t bdesc = bdesc0 + (uint64_t)(slot * (chunk_bytes >> 4));
-                        // one elected lane issues the chunk's four K=16 MMAs (B descriptor start
-                        // +32 B = +2, A +8 TMEM columns each) and the commit that frees the slot
-                        // in every CTA's producer (multicast)
-                        asm volatile(
-                            "{\n.reg .pred p, q;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
-                            "elect.sync _|q, 0xffffffff;\n"
-                            "setp.ne.b32 p, %4, 0;\n"
-                            "add.s64 d1, %2, 2;\nadd.s64 d2, %2, 4;\nadd.s64 d3, %2, 6;\n"
-                            "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\n"
-                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
-                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
-                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n"
-                            "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-                            " [%5], %6;\n}" ::"r"(tmem_d),
-                            "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u),
-                            "r"(empty0 + slot * 8), "h"(cmask)
-                            : "memory");
-                    }
-                    if (++slot == (uint32_t)TC_NSLOT) {
-                        slot = 0;
-                        phase ^= 1u;
-                    }
-                }
-                if (p.skip_epi == 4) {
-                    if (lane == 0) mbar_arrive(&t_full[s]);
-                } else {
+                for (int kb = 0; kb < KB; kb++) {
+                    // descriptor start address advances 32 B (>> 4 = 2) per K=16 step, a chunk
+                    // (16 KB) per 64 columns; A advances 8 TMEM columns per K=16 step
+                    const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)slot * tile_bytes + kb * chunk_bytes) >> 4);
                     asm volatile(
-                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
-                            tfull0 + (uint32_t)s * 8)
+                        "{\n.reg .pred p, q;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
+                        "elect.sync _|q, 0xffffffff;\n"
+                        "setp.ne.b32 p, %4, 0;\n"
+                        "add.s64 d1, %2, 2;\nadd.s64 d2, %2, 4;\nadd.s64 d3, %2, 6;\n"
+                        "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\n"
+                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
+                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
+                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n}" ::"r"(tmem_d),
+                        "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u)
                         : "memory");
+                }
+                // the slot is free in every CTA's producer (multicast), the accumulator is ready
+                asm volatile(
+                    "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                    "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                    " [%0], %2;\n"
+                    "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n}" ::"r"(
+                        empty0 + (uint32_t)slot * 8),
+                    "r"(tfull0 + (uint32_t)s * 8), "h"(cmask)
+                    : "memory");
+                if (++slot == NS) {
+                    slot = 0;
+                    phase ^= 1u;
                 }
             }
         }

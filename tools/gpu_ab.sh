@@ -7,3 +7,4 @@ for v in head new head new; do
 import sys,json
 for l in sys.stdin: j=json.loads(l); print(j['k'], j['ms'], j['cand_series'], {k:v[0] for k,v in j['kernels'].items()})"
 done
+for v in head new; do export SSB_LIB_VARIANT=$v; echo "== diag1 $v"; SSB_TC_DIAG=1 timeout 120 python tools/cell_profile.py --rows 1000000 --sigmas 1.0 --ks 1 2>&1 | tail -1 | cut -c1-250; done
