@@ -142,13 +142,21 @@ __global__ void __launch_bounds__(CHUNK)
         }
         __syncthreads();
         if (live) {
-            for (int i = 0; i < w; i++) {
-                const float xf = tile[t][i];
-                bad |= !isfinite(xf);
-                const double v = (double)xf;
-                a = __dadd_rn(a, v);
-                b = __dadd_rn(b, __dmul_rn(v, v));
-                const int p = c0 + i + 1;  // prefix point index now available
+            int i = 0;
+            while (i < w) {
+                // run to the next prefix point that matters (segment midpoint or end):
+                // the inner loop is just the two float64 chains (non-finite values
+                // surface in the running sums, checked once at the end)
+                const int ev = (mid > c0 + i && mid < sb) ? min(mid, sb) : sb;  // next event prefix index
+                const int stop = min(w, ev - c0);
+#pragma unroll 4
+                for (; i < stop; i++) {
+                    const double v = (double)tile[t][i];
+                    a = __dadd_rn(a, v);
+                    b = __dadd_rn(b, __dmul_rn(v, v));
+                }
+                if (i < stop || c0 + i != ev) continue;  // stage exhausted before the event
+                const int p = ev;  // prefix point index now available
                 if (p == mid) {
                     cm = a;
                     c2m = b;
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(CHUNK)
         }
         __syncthreads();
     }
+    bad |= live && !(isfinite(a) && isfinite(b));
     if (bad) atomicOr(nonfinite, 1);
 }
 
