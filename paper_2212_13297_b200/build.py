@@ -80,13 +80,21 @@ class SeriesIndex:
         info = _lib.IndexInfo()
         _lib.call("ssb_index_info", handle.raw, ctypes.byref(info))
         self.info = info
-        recs = []
-        for i in range(info.num_nodes):
-            r = _lib.NodeRec()
-            _lib.call("ssb_index_node", handle.raw, i, ctypes.byref(r))
-            recs.append(r)
-        self.root: Node = tree_from_records(recs)
+        self._root: Node | None = None
         self.id_base = int(info.id_base)
+
+    @property
+    def root(self) -> Node:
+        """Host view of the tree (tree.py Node graph), materialised on first use:
+        the device index does not need it to answer queries."""
+        if self._root is None:
+            recs = []
+            for i in range(self.info.num_nodes):
+                r = _lib.NodeRec()
+                _lib.call("ssb_index_node", self._handle.raw, i, ctypes.byref(r))
+                recs.append(r)
+            self._root = tree_from_records(recs)
+        return self._root
 
     @property
     def handle(self):

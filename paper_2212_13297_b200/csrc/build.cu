@@ -670,6 +670,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     uint32_t *perm = perm_a.as<uint32_t>(), *perm2 = perm_b.as<uint32_t>();
 
     std::vector<int32_t> frontier = {0};  // nodes needing stats this level
+    GrowBuf lv_stats, lv_flags, lv_scan, lv_tmp;  // per-level scratch, grown not re-allocated
     int level = 0;
     lap("init");
     while (!frontier.empty()) {
@@ -731,10 +732,11 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         SSB_CUDA(cudaMemcpyAsync(d_ranges.p, r_cat.data(), sizeof(Range) * r_cat.size(), cudaMemcpyHostToDevice, s));
         const Range *d_r_all = d_ranges.as<Range>(), *d_r_ss = d_r_all + r_all.size(),
                     *d_r_ev = d_r_ss + r_ss.size();
-        DevBuf d_nodes, d_chunks, d_stats, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
+        DevBuf d_nodes, d_chunks, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
+        GrowBuf &d_stats = lv_stats;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
         SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
-        SSB_CUDA(d_stats.alloc(sizeof(float) * (size_t)stat_off, s));
+        SSB_CUDA(d_stats.ensure(sizeof(float) * (size_t)stat_off, s));
         SSB_CUDA(d_cmin.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(d_cmax.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(cudaMemcpyAsync(d_nodes.p, nd.data(), sizeof(NodeDesc) * F, cudaMemcpyHostToDevice, s));
@@ -874,11 +876,12 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 nl_set[f] = fnl[f];
             }
         }
-        DevBuf d_pcol, d_pthr, d_flags, d_scan, d_tmp, d_nl;
+        DevBuf d_pcol, d_pthr, d_nl;
+        GrowBuf &d_flags = lv_flags, &d_scan = lv_scan, &d_tmp = lv_tmp;
         SSB_CUDA(d_pcol.alloc(4 * F, s));
         SSB_CUDA(d_pthr.alloc(8 * F, s));
-        SSB_CUDA(d_flags.alloc(4 * (size_t)(aoff + 1), s));
-        SSB_CUDA(d_scan.alloc(4 * (size_t)(aoff + 1), s));
+        SSB_CUDA(d_flags.ensure(4 * (size_t)(aoff + 1), s));
+        SSB_CUDA(d_scan.ensure(4 * (size_t)(aoff + 1), s));
         SSB_CUDA(d_nl.alloc(4 * F, s));
         SSB_CUDA(cudaMemcpyAsync(d_pcol.p, pcol.data(), 4 * F, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemcpyAsync(d_pthr.p, pthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
@@ -890,7 +893,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         size_t tmp_bytes = 0;
         SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flags.as<uint32_t>(), d_scan.as<uint32_t>(),
                                                (int)(aoff + 1), s));
-        SSB_CUDA(d_tmp.alloc(tmp_bytes, s));
+        SSB_CUDA(d_tmp.ensure(tmp_bytes, s));
         SSB_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp.p, tmp_bytes, d_flags.as<uint32_t>(), d_scan.as<uint32_t>(),
                                                (int)(aoff + 1), s));
         note_launch(1);

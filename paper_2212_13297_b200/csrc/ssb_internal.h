@@ -75,6 +75,35 @@ struct DevBuf {
     }
 };
 
+// Grow-only device buffer reused across iterations (e.g. the build's levels):
+// re-allocates with 25% headroom only when a request exceeds its capacity.
+struct GrowBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaStream_t s = nullptr;
+    GrowBuf() = default;
+    GrowBuf(const GrowBuf &) = delete;
+    GrowBuf &operator=(const GrowBuf &) = delete;
+    ~GrowBuf()
+    {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t ensure(size_t bytes, cudaStream_t st)
+    {
+        s = st;
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+        cap = bytes + bytes / 4 + 256;
+        return cudaMallocAsync(&p, cap, st);
+    }
+    template <typename T>
+    T *as() const
+    {
+        return reinterpret_cast<T *>(p);
+    }
+};
+
 // RAII event pair around one kernel launch (prof.cu); no-op unless enabled.
 // `bytes` = algorithmic bytes of the launch (DESIGN.md per-kernel formulas).
 class ProfScope {
