@@ -2,29 +2,34 @@
 //
 // For a block of queries Q and the index rows X, the squared distance is
 // ||q||^2 + ||x||^2 - 2 q.x.  q.x is computed by tcgen05.mma (kind::f16, BF16
-// operands, FP32 accumulation in TMEM) on BF16 copies of Q and X staged by TMA
-// (SWIZZLE_128B, K-major).  With RN-to-bf16 inputs the dot-product error is
-// at most c*||q||*||x||, c = 2^-8 + 2^-15 (input rounding 2*2^-9 plus fp32
-// accumulation of <= 256 exact products), so every (query, row) pair gets a
-// rigorous interval [LB, UB] around its real squared distance.  The epilogue
-// (4 warps, one query per thread = one TMEM lane) keeps, per query, the k
-// smallest UB seen (a valid bound on the k-th distance: k real rows lie
-// below it), shares it across CTAs with an atomicMin, and emits every row
-// whose LB does not exceed the current bound as a candidate.  Candidates are
-// then rescored with the exact float32 pairwise distance (scan.cu arithmetic),
-// so answers stay bit-identical to the oracle; the tensor cores only decide
-// which rows need the exact arithmetic.
+// operands, FP32 accumulation in TMEM).  With RN-to-bf16 inputs the dot-product
+// error is at most c*||q||*||x||, c = 2^-8 + 2^-15 (input rounding 2*2^-9 plus
+// fp32 accumulation of <= 256 exact products), so every (query, row) pair gets
+// a rigorous interval [LB, UB] around its real squared distance.  Any k
+// distinct rows' upper bounds bound the k-th distance: each epilogue thread
+// keeps the k smallest UB of its own rows (k <= 32), k >= 2 also pools rows
+// hashed into k buckets per query (global atomicMin; the largest bucket minimum
+// is a bound), and the bound is shared across CTAs.  Every row whose LB does
+// not exceed the bound of the moment is emitted with its LB; rescoring skips
+// those above the filter's final bound and rescores the rest with the exact
+// float32 pairwise distance (scan.cu arithmetic), so answers stay bit-identical
+// to the oracle: the tensor cores only decide which rows need exact arithmetic.
 //
 // This is the "scan" fallback of the reference's adaptive query
 // (query.py:321-334: when envelope pruning is weak the reference scans the
-// candidate leaves sequentially): queries whose LB_EAPCA keeps most leaves
-// are answered here instead of by K-lbs + sparse K-scan.
+// candidate leaves sequentially), run densely on the tensor cores.
 //
-// Warp roles (6 warps): w0 TMA producer, w1 MMA issuer (+ TMEM allocation),
-// w2..w5 epilogue.  Query block: 128 queries (M=128), row tile: 128 rows
-// (N=128), K = n padded to a multiple of 64 (one 128-byte swizzle atom per
-// 64 BF16 columns).  A (queries) stays resident; B tiles are double-buffered;
-// two TMEM accumulators (2 x 128 columns) overlap MMA and epilogue.
+// One CTA = one block of 128 queries (M = 128) x a contiguous range of
+// 128-row tiles (N = 128); two query blocks form a cluster and get every B
+// tile by TMA multicast.  Warp roles (10 warps): w0 producer (tile side data
+// by 1-D bulk copies into a 4-deep tile-slot ring; whole B tiles, KB 16 KB
+// K-chunks each, into a ring of tile slots), w1 TMEM allocation + MMA issue
+// (A = the query block, resident in TMEM; 3 accumulators of 128 columns; one
+// barrier wait and one commit per tile), w2..w9 epilogue (two warps per TMEM
+// lane quarter, one query per thread, 64 columns per tile).  The first `warm`
+// tiles of every CTA are scanned once without emission (bounds only) and
+// rescanned at the end.
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

@@ -1,5 +1,3 @@
-for w in c4 c5; do
-  timeout 1500 python bench.py --workload $w --steps 3 --warmup 2 --cpu-sample 1 > gpurun_out/b_$w.json 2> gpurun_out/b_$w.err
-  python -c "
-import json; j=json.load(open('gpurun_out/b_$w.json')); print('$w', j['value'], j['e2e']['value'], j['ms_per_step'], j['roofline']['frac'], j['build'], {k:(round(v['ms'],1),v['launches']) for k,v in j['kernels'].items()})"
-done
+for cs in 2 4 1; do for d in 1 0; do echo "cs=$cs diag=$d"; SSB_TC_CSMAX=$cs SSB_TC_DIAG=$d timeout 120 python tools/cell_profile.py --rows 1000000 --sigmas 1.0 --ks 1,10 2>&1 | tail -2 | python -c "
+import sys,json
+for l in sys.stdin: j=json.loads(l); print('  ', j['k'], j['ms'], j['cand_series'], {k:v[0] for k,v in j['kernels'].items()})"; done; done
