@@ -46,7 +46,7 @@ namespace ssb {
 
 Index::~Index()
 {
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xnorm, rowc, tilec};
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -613,12 +613,12 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
     if (ix.n % 8 != 0 || ix.n > 256) return OK;
     SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
-    SSB_CUDA(cudaMalloc(&ix.xnorm, (size_t)ix.N * 4));
+    SSB_CUDA(cudaMalloc(&ix.xen, (size_t)ix.N * 8));
     SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)((ix.N + 127) / 128 * 128) * 16));  // padded to whole tiles
-    int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xnorm, s);
+    int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xen, false, s);
     if (rc) return rc;
-    SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 2) * 16));
-    rc = launch_tc_row_consts(ix.xn2, ix.xnorm, ix.N, ix.rowc, s);
+    SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 4) * 16));
+    rc = launch_tc_row_consts(ix.xn2, ix.xen, ix.N, ix.rowc, s);
     if (rc) return rc;
     return launch_tc_tile_consts(ix.rowc, ix.N, ix.tilec, s);
 }

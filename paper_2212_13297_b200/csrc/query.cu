@@ -743,7 +743,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(d_qtc.alloc(4 * (size_t)nq, s));
         SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
         SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
-        SSB_CUDA(qnrm.alloc(4 * (size_t)nq_pad, s));
+        SSB_CUDA(qnrm.alloc(8 * (size_t)nq_pad, s));
         SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
@@ -752,12 +752,12 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
         SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 4, s));
-        rc = launch_to_bf16_norms(Q, d_qtc.as<int32_t>(), nq, n, false, qb.p, qn2.as<float>(), qnrm.as<float>(), s);
+        rc = launch_to_bf16_norms(Q, d_qtc.as<int32_t>(), nq, n, false, qb.p, qn2.as<float>(), qnrm.as<float2>(), true, s);
         if (rc) return rc;
         seed_bound_kernel<<<(nq + 255) / 256, 256, 0, s>>>(thr.as<uint64_t>(), d_qtc.as<int32_t>(), nq,
                                                           gb.as<unsigned int>());
         SSB_CHECK_LAUNCH();
-        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
                               gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(), tc_n.as<unsigned int>(),
                               tc_cap, nullptr, s);
         if (rc) return rc;
@@ -926,9 +926,9 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     const int nq_pad = (B + 127) / 128 * 128;
     SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
     SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
-    SSB_CUDA(qnrm.alloc(4 * (size_t)nq_pad, s));
+    SSB_CUDA(qnrm.alloc(8 * (size_t)nq_pad, s));
     SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
-    rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnrm.as<float>(), s);
+    rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnrm.as<float2>(), true, s);
     if (rc) return rc;
     SSB_CUDA(qmax.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
@@ -955,7 +955,7 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     // with (valid, and much tighter than +inf); select overflows go to the caller
     for (int attempt = 0;; attempt++) {
     SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
                           gb.as<unsigned int>(), cand.as<uint2>(), clb.as<float>(), cn.as<unsigned int>(), tc_cap,
                           nullptr, s);
     if (rc) return rc;

@@ -55,9 +55,10 @@ struct Index {
     // tensor-core filter operands: BF16 copy (row-major, logical element order,
     // leaf order) and exact squared norms / norms (rounded up) of every row
     void *Xb = nullptr;
-    float *xn2 = nullptr, *xnorm = nullptr;
+    float *xn2 = nullptr;    // ||x||^2 per row
+    float2 *xen = nullptr;   // per row (U, V): BF16 rounding-error norms (to_bf16_norms_kernel)
     float4 *rowc = nullptr;   // per-row constants of the K-tc bounds
-    float4 *tilec = nullptr;  // per 64-row half tile extremes of rowc
+    float4 *tilec = nullptr;  // per 64-row half tile: two float4 of extremes of rowc
     double build_ms = 0.0;
     int32_t levels = 0;
     ~Index();
@@ -68,15 +69,15 @@ struct QueryCfg {
     int route = 0;           // 0 auto, 1 tree only, 2 tensor-core for every query
 };
 
-int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
+int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s);
 int64_t tc_bound_slots(int nq);
-int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s);
+int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *out, cudaStream_t s);
 int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
-                         float *n2, float *nrm, cudaStream_t s);
+                         float *n2, float2 *en, bool is_query, cudaStream_t s);
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
                    cudaStream_t s, const unsigned int *nc_dev = nullptr);

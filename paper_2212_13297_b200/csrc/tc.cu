@@ -174,14 +174,13 @@ struct TcParams {
     int64_t tiles_per_cta; // contiguous tile chunk per CTA (per cluster)
     int ctas_per_qb;       // chunks
     int CS;                // cluster size: CTAs (query blocks) sharing each B tile by multicast
-    const float *qn2, *qnorm;  // per query (launch-local index)
-    const float *xn2, *xnorm;  // per row
+    const float *qn2;          // per query (launch-local index): ||q||^2
+    const float2 *qen;         // per query: (||qh||, ||ql||) rounded up
     const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
-    const float4 *tilec;       // per 64-row half tile: (min a, max b, min a', min b')
+    const float4 *tilec;       // per 64-row half tile: two float4 of extremes (tc_tile_consts_kernel)
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
     unsigned int *gbucket;     // per query x k (k >= 2): min upper bound of the rows r with r % k == b
     int k;
-    float c_rel;               // dot-product error coefficient
     uint2 *cand;               // (query, row) candidates
     float *cand_lb;            // their lower bounds (rescoring skips rows above the final bound)
     unsigned int *cand_n;
@@ -195,7 +194,7 @@ struct TcParams {
 constexpr int TC_RS = 4;  // tile-slot ring depth
 struct TileSlot {
     float4 rowc[TC_BN];  // row bound constants of the tile's 128 rows
-    float4 tilec[2];     // per 64-row half: (min a, max b, min a', min b')
+    float4 tilec[4];     // per 64-row half: (min a_l, max u, max v, -), (min a_u, min u, min v, -)
     float gb[TC_BM];     // snapshot of the shared per-query bounds (float bits)
 };
 static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
@@ -302,10 +301,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %8;\n"
                         "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %5, [%1];\n"
                         "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2048], [%3], %6, [%1];\n"
-                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2080], [%4], %7, [%1];\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2112], [%4], %7, [%1];\n"
                         "}" ::"r"(dst),
-                        "r"(bar), "l"(p.rowc + tile * TC_BN), "l"(p.tilec + tile * 2), "l"(p.gbound + qb * TC_BM),
-                        "n"(TC_BN * 16), "n"(32), "n"(TC_BM * 4), "n"((int)sizeof(TileSlot))
+                        "r"(bar), "l"(p.rowc + tile * TC_BN), "l"(p.tilec + tile * 4), "l"(p.gbound + qb * TC_BM),
+                        "n"(TC_BN * 16), "n"(64), "n"(TC_BM * 4), "n"((int)sizeof(TileSlot))
                         : "memory");
                 }
                 const int row0 = (int)(tile * TC_BN) + rank * srows;
@@ -424,12 +423,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(a_full);
         }
-        // lb = f*(1-e)*(qn2 + xn2) - 2f*s - 2cf*qn*xn,  ub = g*(1+e)*(qn2 + xn2) - 2g*s + 2cg*qn*xn
-        // with f = 1 - 4e-6, g = 1 + 4e-6, e = 2e-6 (fp32 evaluation slack); per-row
-        // constants (xn2 and xn terms) come from the tile slot, per-query ones live here.
+        // lb = f(1-e)(qn2 + xn2) - 2f t - 2g E,  ub = g(1+e)(qn2 + xn2) - 2g t + 2g E,
+        // E = QH U + QL V (to_bf16_norms_kernel), f = 1 - 4e-6, g = 1 + 4e-6, e = 2e-6
+        // (fp32 evaluation slack); per-row constants (a_l, a_u, 2gU, 2gV) come from the
+        // tile slot, per-query ones live here.
         const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
         const float qn2 = qvalid ? p.qn2[ql] : 0.f;
-        const float qnm = qvalid ? p.qnorm[ql] : 0.f;
+        const float2 qe = qvalid ? p.qen[ql] : make_float2(0.f, 0.f);
+        const float QH = qe.x, QL = qe.y;
         const float alpha_l = f * (1.f - e) * qn2, alpha_u = g * (1.f + e) * qn2;
         const float m2f = -2.f * f, m2g = -2.f * g;
         constexpr int KT = KTOP > 0 ? KTOP : 1;
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
             const float gcur = qvalid ? ts.gb[m] : -1.f;
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
-            const float4 tc4 = ts.tilec[h];
+            const float4 tcl = ts.tilec[2 * h], tcu = ts.tilec[2 * h + 1];
             mbar_wait(&t_full[s], (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
@@ -513,11 +514,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // rows to the precise per-row test, never fewer)
             float thr_s;
             {
-                float s_lo = ((alpha_l + tc4.x - qnm * tc4.y) - bound) * inv2f;
+                float s_lo = ((alpha_l + tcl.x - QH * tcl.y - QL * tcl.z) - bound) * inv2f;
                 s_lo -= 1e-5f * (fabsf(s_lo) + 1.f);
                 thr_s = s_lo;
                 if (tighten) {
-                    float s_need = ((alpha_u + tc4.z + qnm * tc4.w) - bound) * inv2g;
+                    float s_need = ((alpha_u + tcu.x + QH * tcu.y + QL * tcu.z) - bound) * inv2g;
                     s_need -= 1e-5f * (fabsf(s_need) + 1.f);
                     thr_s = emit_ok ? fminf(s_lo, s_need) : s_need;
                 }
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 auto row_lb = [&](int c0, int i) {
                     const float sd = sel16(v + c0, i);
                     const float4 rc = rows[c0 + i];
-                    return fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                    return fmaf(m2f, sd, fmaf(-QH, rc.z, fmaf(-QL, rc.w, alpha_l + rc.x)));
                 };
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 16) {
@@ -554,10 +555,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             work &= work - 1;
                             const float sd = sel16(v + c0, i);
                             const float4 rc = rows[c0 + i];
-                            const float lb = fmaf(m2f, sd, fmaf(-qnm, rc.y, alpha_l + rc.x));
+                            const float lb = fmaf(m2f, sd, fmaf(-QH, rc.z, fmaf(-QL, rc.w, alpha_l + rc.x)));
                             emit |= (emit_ok && lb <= bound ? 1u : 0u) << i;
                             if (lb < bound && (tighten || bk)) {  // ub >= lb: only then can ub tighten the bound
-                                const float ub = fmaf(m2g, sd, fmaf(qnm, rc.w, alpha_u + rc.z));
+                                const float ub = fmaf(m2g, sd, fmaf(QH, rc.z, fmaf(QL, rc.w, alpha_u + rc.y)));
                                 if (ub < bound && ub < kth) {
                                     if (tighten && !revisit) {
                                         float x = ub;
@@ -655,79 +656,104 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // ---------------------------------------------------------------------------
 // helpers: bf16 copies with exact norms, and the tensor maps
 
+// BF16 copy (RN) of each row plus its rounding-error norms.  With q = qh + ql,
+// x = xh + xl (qh, xh the BF16 values, ql, xl the exact residuals) and the
+// tensor core's fp32 accumulation of the exact products (error <= 2^-15 ||qh|| ||xh||
+// for K <= 256, with margin), Cauchy-Schwarz on q.x - qh.xh = qh.xl + ql.(xh + xl) gives
+//   |q.x - t| <= ||qh|| (||xl|| + 2^-15 ||xh||) + ||ql|| (||xh|| + ||xl||) = QH U + QL V.
+// Rows get en = (U, V), queries en = (QH, QL), all rounded up (float64 sums with
+// a relative margin, then float32 RU).
 __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
                                      int n, int layout, __nv_bfloat16 *__restrict__ dst, float *__restrict__ n2,
-                                     float *__restrict__ nrm)
+                                     float2 *__restrict__ en, int is_query)
 {
     // one warp per row; src rows may be in the lane-transposed layout
     const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
     if (r >= R) return;
     const int lane = threadIdx.x & 31;
     const float *s = src + (int64_t)(rows ? rows[r] : r) * n;
-    double acc = 0.0;
+    double acc = 0.0, hh = 0.0, ll = 0.0;
     for (int e = lane; e < n; e += 32) {
         const float v = s[layout ? layout_pos(n, e) : e];
-        dst[r * n + e] = __float2bfloat16_rn(v);
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        dst[r * n + e] = b;
+        const double vb = (double)__bfloat162float(b), dv = (double)v - vb;  // exact in float64
         acc += (double)v * (double)v;
+        hh += vb * vb;
+        ll += dv * dv;
     }
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = 16; off; off >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        hh += __shfl_xor_sync(0xffffffffu, hh, off);
+        ll += __shfl_xor_sync(0xffffffffu, ll, off);
+    }
     if (lane == 0) {
         n2[r] = __double2float_rn(acc);
-        nrm[r] = __double2float_ru(sqrt(acc));
+        const double m = 1.0 + 0x1p-40;  // covers the float64 sums and square roots
+        const double H = sqrt(hh * m) * m, L = sqrt(ll * m) * m;
+        en[r] = is_query ? make_float2(__double2float_ru(H), __double2float_ru(L))
+                         : make_float2(__double2float_ru((L + 0x1p-15 * H) * m), __double2float_ru((H + L) * m));
     }
 }
 
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
-                         float *n2, float *nrm, cudaStream_t s)
+                         float *n2, float2 *en, bool is_query, cudaStream_t s)
 {
     if (R == 0) return OK;
     to_bf16_norms_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(src, rows, R, n, layout ? 1 : 0,
-                                                                  (__nv_bfloat16 *)dst_bf16, n2, nrm);
+                                                                  (__nv_bfloat16 *)dst_bf16, n2, en, is_query ? 1 : 0);
     SSB_CHECK_LAUNCH();
     return OK;
 }
 
 // per-row constants of the bound formulas (see the epilogue):
-// (f(1-e) xn2, 2 c f xn, g(1+e) xn2, 2 c g xn)
-__global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float *__restrict__ xn, int64_t N,
-                                     float c_rel, float4 *__restrict__ out)
+// (a_l, a_u, u, v) = (f(1-e) xn2, g(1+e) xn2, 2g U, 2g V) with (U, V) = en
+__global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float2 *__restrict__ en, int64_t N,
+                                     float4 *__restrict__ out)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= (N + 127) / 128 * 128) return;
     if (r >= N) {  // padding rows of the last tile: lb = ub = +inf
-        out[r] = make_float4(__int_as_float(0x7f800000), 0.f, __int_as_float(0x7f800000), 0.f);
+        out[r] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000), 0.f, 0.f);
         return;
     }
     const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
-    out[r] = make_float4(f * (1.f - e) * xn2[r], 2.f * c_rel * f * xn[r], g * (1.f + e) * xn2[r],
-                         2.f * c_rel * g * xn[r]);
+    const float2 uv = en[r];
+    out[r] = make_float4(f * (1.f - e) * xn2[r], g * (1.f + e) * xn2[r], 2.f * g * uv.x, 2.f * g * uv.y);
 }
 
-// per 64-row half tile: (min a, max b, min a', min b') of the row constants
+// per 64-row half tile, two float4: (min a_l, max u, max v, -), (min a_u, min u, min v, -)
 __global__ void tc_tile_consts_kernel(const float4 *__restrict__ rowc, int64_t N, int64_t halves, float4 *__restrict__ out)
 {
     const int64_t hidx = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
     if (hidx >= halves) return;
     const int lane = threadIdx.x & 31;
-    float mina = __int_as_float(0x7f800000), maxb = 0.f, mina2 = __int_as_float(0x7f800000),
-          minb2 = __int_as_float(0x7f800000);
+    const float inf = __int_as_float(0x7f800000);
+    float mal = inf, mxu = 0.f, mxv = 0.f, mau = inf, mnu = inf, mnv = inf;
     for (int i = lane; i < 64; i += 32) {
         const int64_t r = hidx * 64 + i;
         if (r < N) {
             const float4 c = rowc[r];
-            mina = fminf(mina, c.x);
-            maxb = fmaxf(maxb, c.y);
-            mina2 = fminf(mina2, c.z);
-            minb2 = fminf(minb2, c.w);
+            mal = fminf(mal, c.x);
+            mau = fminf(mau, c.y);
+            mxu = fmaxf(mxu, c.z);
+            mnu = fminf(mnu, c.z);
+            mxv = fmaxf(mxv, c.w);
+            mnv = fminf(mnv, c.w);
         }
     }
     for (int off = 16; off; off >>= 1) {
-        mina = fminf(mina, __shfl_xor_sync(0xffffffffu, mina, off));
-        maxb = fmaxf(maxb, __shfl_xor_sync(0xffffffffu, maxb, off));
-        mina2 = fminf(mina2, __shfl_xor_sync(0xffffffffu, mina2, off));
-        minb2 = fminf(minb2, __shfl_xor_sync(0xffffffffu, minb2, off));
+        mal = fminf(mal, __shfl_xor_sync(0xffffffffu, mal, off));
+        mau = fminf(mau, __shfl_xor_sync(0xffffffffu, mau, off));
+        mxu = fmaxf(mxu, __shfl_xor_sync(0xffffffffu, mxu, off));
+        mnu = fminf(mnu, __shfl_xor_sync(0xffffffffu, mnu, off));
+        mxv = fmaxf(mxv, __shfl_xor_sync(0xffffffffu, mxv, off));
+        mnv = fminf(mnv, __shfl_xor_sync(0xffffffffu, mnv, off));
     }
-    if (lane == 0) out[hidx] = make_float4(mina, maxb, mina2, minb2 == __int_as_float(0x7f800000) ? 0.f : minb2);
+    if (lane == 0) {
+        out[2 * hidx] = make_float4(mal, mxu, mxv, 0.f);
+        out[2 * hidx + 1] = make_float4(mau, mnu == inf ? 0.f : mnu, mnv == inf ? 0.f : mnv, 0.f);
+    }
 }
 
 int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s)
@@ -739,13 +765,12 @@ int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream
     return OK;
 }
 
-static float tc_c_rel() { return (float)(std::ldexp(1.0, -8) + std::ldexp(1.0, -15)); }
 
-int launch_tc_row_consts(const float *xn2, const float *xn, int64_t N, float4 *out, cudaStream_t s)
+int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *out, cudaStream_t s)
 {
     if (N == 0) return OK;
     const int64_t padded = (N + 127) / 128 * 128;  // out holds ceil(N/128)*128 entries
-    tc_row_consts_kernel<<<(unsigned)((padded + 255) / 256), 256, 0, s>>>(xn2, xn, N, tc_c_rel(), out);
+    tc_row_consts_kernel<<<(unsigned)((padded + 255) / 256), 256, 0, s>>>(xn2, en, N, out);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -790,7 +815,7 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
-int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int nq, const void *Xb,
+int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s)
@@ -824,9 +849,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
     if (rc) return rc;
     p.qb = reinterpret_cast<const uint4 *>(Qb);
     p.qn2 = qn2;
-    p.qnorm = qnorm;
-    p.xn2 = nullptr;
-    p.xnorm = nullptr;
+    p.qen = qen;
     p.rowc = rowc;
     p.tilec = tilec;
     p.gbound = gbound;
@@ -839,7 +862,6 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float *qnorm, int n
         p.gbucket = buckets.as<unsigned int>();
     }
     p.k = k;
-    p.c_rel = tc_c_rel();
     p.warm = 4;
     if (const char *e = getenv("SSB_TC_WARM")) p.warm = std::max(0, atoi(e));  // diagnostics
     p.cand = cand;
@@ -903,32 +925,32 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
 {
     SSB_REQUIRE(B >= 1 && N >= 1, "empty operands");
     const int Bp = (B + TC_BM - 1) / TC_BM * TC_BM;
-    DevBuf qb, xb, qn2, qnm, xn2, xnm, gb, cand, cn;
+    DevBuf qb, xb, qn2, qnm, xn2, xnm, gb, cand, cn;  // qnm, xnm: float2 error norms
     SSB_CUDA(qb.alloc(2 * (size_t)Bp * n, s));
     SSB_CUDA(xb.alloc(2 * (size_t)N * n, s));
     SSB_CUDA(qn2.alloc(4 * (size_t)Bp, s));
-    SSB_CUDA(qnm.alloc(4 * (size_t)Bp, s));
+    SSB_CUDA(qnm.alloc(8 * (size_t)Bp, s));
     SSB_CUDA(xn2.alloc(4 * (size_t)N, s));
-    SSB_CUDA(xnm.alloc(4 * (size_t)N, s));
+    SSB_CUDA(xnm.alloc(8 * (size_t)N, s));
     SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(B), s));
     SSB_CUDA(cand.alloc(8, s));
     SSB_CUDA(cn.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)Bp * n, s));
     SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(B), s));
     SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
-    int rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnm.as<float>(), s);
+    int rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnm.as<float2>(), true, s);
     if (rc) return rc;
-    rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float>(), s);
+    rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float2>(), false, s);
     if (rc) return rc;
     DevBuf rcb;
     SSB_CUDA(rcb.alloc(16 * (size_t)((N + 127) / 128 * 128), s));
-    rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float>(), N, rcb.as<float4>(), s);
+    rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float2>(), N, rcb.as<float4>(), s);
     if (rc) return rc;
     DevBuf tcb;
-    SSB_CUDA(tcb.alloc(16 * (size_t)((N + TC_BN - 1) / TC_BN * 2), s));
+    SSB_CUDA(tcb.alloc(16 * (size_t)((N + TC_BN - 1) / TC_BN * 4), s));
     rc = launch_tc_tile_consts(rcb.as<float4>(), N, tcb.as<float4>(), s);
     if (rc) return rc;
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned int>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
