@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--rows", type=int, default=10_000_000)
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--tau", type=int, default=10_000)
+    ap.add_argument("--no-warm", action="store_true", help="skip the small warm-up build (profilers)")
     a = ap.parse_args()
     import torch
 
@@ -25,7 +26,9 @@ def main():
 
     X = torch.from_numpy(G.random_walks(a.rows, a.n, 0)).cuda()
     s = ssb.IndexSettings(series_length=a.n, dataset_size=a.rows, leaf_threshold=a.tau)
-    ssb.build_index_array(X[: min(a.rows, 200_000)], ssb.IndexSettings(series_length=a.n, dataset_size=min(a.rows, 200_000), leaf_threshold=a.tau))  # warm
+    if not a.no_warm:  # module loading and pool growth outside the measured build
+        w = min(a.rows, 200_000)
+        ssb.build_index_array(X[:w], ssb.IndexSettings(series_length=a.n, dataset_size=w, leaf_threshold=a.tau))
     torch.cuda.synchronize()
     _lib.prof_reset()
     _lib.prof_enable(True)

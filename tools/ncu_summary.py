@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches <launches.csv>      # per-kernel share of device time
     python tools/ncu_summary.py details <report.ncu-rep>     # key --set full metrics per kernel
+    python tools/ncu_summary.py kernels <rep.ncu-rep>...     # duration, DRAM GB/s vs the HBM peak, SM%
 """
 
 import collections
@@ -69,5 +70,47 @@ def details(path):
                     print(f"{d.get('Kernel Name', '?').split('(')[0][:50]:50s} {k:60s} {d[k]:>16s} {u[k]}")
 
 
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6,
+          "ms": 1e-3, "s": 1.0,
+          "hz": 1.0, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "cycle/nsecond": 1e9, "cycle/usecond": 1e6,
+          "cycle/second": 1.0}
+
+
+def kernels(*reps, hbm_peak=6542.4):
+    """Per kernel (longest launch in each capture): duration, DRAM bytes and
+    GB/s against the measured HBM peak, SM and memory throughput (% of peak)."""
+    print(f"{'kernel':34s} {'us':>9s} {'DRAM MB':>9s} {'GB/s':>8s} {'%HBM':>6s} {'SM%':>6s} {'Mem%':>6s} {'GHz':>5s}")
+    for rep in reps:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        if len(rows) < 3:
+            continue
+        hdr, units = rows[0], rows[1]
+
+        def val(r, k):
+            if k not in hdr:
+                return 0.0
+            i = hdr.index(k)
+            try:
+                return float(r[i].replace(",", "")) * _SCALE.get(units[i], 1.0)
+            except ValueError:
+                return 0.0
+
+        best = collections.OrderedDict()
+        for r in rows[2:]:
+            name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+            t = val(r, "gpu__time_duration.sum")
+            if name not in best or t > best[name][0]:
+                best[name] = (t, val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"),
+                              val(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                              val(r, "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
+                              val(r, "sm__cycles_elapsed.avg.per_second"))
+        for name, (t, b, sm, mem, hz) in best.items():
+            gbs = b / t / 1e9 if t else 0.0
+            print(f"{name[:34]:34s} {t * 1e6:9.1f} {b / 1e6:9.1f} {gbs:8.1f} {100 * gbs / hbm_peak:6.1f} "
+                  f"{sm:6.1f} {mem:6.1f} {hz / 1e9:5.2f}")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "details": details}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "details": details, "kernels": kernels}[sys.argv[1]](*sys.argv[2:])
