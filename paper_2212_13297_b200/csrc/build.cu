@@ -101,14 +101,15 @@ __device__ __forceinline__ void stats_w(double ca, double cb, double c2a, double
 }
 
 // K-stats: one CTA per chunk (<=128 members of one node); rows are staged
-// 64 columns at a time through padded shared memory, then each thread walks
+// 32 columns at a time through padded shared memory, then each thread walks
 // its row sequentially (np.cumsum order) and emits the 6m statistics.
 __global__ void __launch_bounds__(CHUNK)
     build_stats_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
                        const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
                        float *__restrict__ stats, int *__restrict__ nonfinite)
 {
-    __shared__ float tile[CHUNK][65];
+    constexpr int SW = 32;  // columns per stage (16.5 KB of shared memory: 12 CTAs per SM)
+    __shared__ float tile[CHUNK][SW + 1];
     __shared__ NodeDesc nd;
     const Chunk ch = chunks[blockIdx.x];
     if (threadIdx.x == 0) nd = nodes[ch.node];
@@ -126,11 +127,11 @@ __global__ void __launch_bounds__(CHUNK)
     const int64_t cnt = nd.count;
     float *out = stats + nd.stat_off + ch.m0 + t;
 
-    for (int c0 = 0; c0 < n; c0 += 64) {
-        const int w = min(64, n - c0);
+    for (int c0 = 0; c0 < n; c0 += SW) {
+        const int w = min(SW, n - c0);
         // cooperative, coalesced load of the chunk rows' columns [c0, c0+w)
-        for (int idx = t; idx < CHUNK * 16; idx += CHUNK) {
-            const int r = idx >> 4, q4 = idx & 15;
+        for (int idx = t; idx < CHUNK * (SW / 4); idx += CHUNK) {
+            const int r = idx / (SW / 4), q4 = idx % (SW / 4);
             if (r < (int)ch.cnt && q4 * 4 < w) {
                 const uint32_t rr = perm[nd.first + ch.m0 + r];
                 const float4 f = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)rr * n + c0) + q4);
