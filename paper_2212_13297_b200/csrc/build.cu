@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(CHUNK)
                        const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
                        float *__restrict__ stats, int *__restrict__ nonfinite)
 {
-    constexpr int SW = 32;  // columns per stage (16.5 KB of shared memory: 12 CTAs per SM)
+    constexpr int SW = 16;  // columns per stage
     __shared__ float tile[CHUNK][SW + 1];
     __shared__ NodeDesc nd;
     const Chunk ch = chunks[blockIdx.x];
