@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int NS = TC_NSLOT / KB;
             const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
             const uint32_t a_tmem = tmem_base + TC_NACC * TC_BN;  // 8 columns per K=16 step
+            const int KS = (p.n + 15) / 16;                        // K=16 steps with data
             const uint64_t bdesc0 = umma_desc_sw128((uint32_t)__cvta_generic_to_shared(sRing));
             const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
             const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
@@ -363,17 +364,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     // descriptor start address advances 32 B (>> 4 = 2) per K=16 step, a chunk
                     // (16 KB) per 64 columns; A advances 8 TMEM columns per K=16 step
                     const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)slot * tile_bytes + kb * chunk_bytes) >> 4);
+                    // K=16 steps of this chunk that hold data (n = 96: the last chunk has 2
+                    // of 4; the zero-filled rest is skipped)
+                    const int ksn = min(4, KS - kb * 4);
                     asm volatile(
-                        "{\n.reg .pred p, q;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
+                        "{\n.reg .pred p, q, q1, q2, q3;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
                         "elect.sync _|q, 0xffffffff;\n"
                         "setp.ne.b32 p, %4, 0;\n"
+                        "setp.gt.and.s32 q1, %5, 1, q;\nsetp.gt.and.s32 q2, %5, 2, q;\nsetp.gt.and.s32 q3, %5, 3, q;\n"
                         "add.s64 d1, %2, 2;\nadd.s64 d2, %2, 4;\nadd.s64 d3, %2, 6;\n"
                         "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\n"
                         "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
-                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
-                        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n}" ::"r"(tmem_d),
-                        "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u)
+                        "@q1 tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
+                        "@q2 tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
+                        "@q3 tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n}" ::"r"(tmem_d),
+                        "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u), "r"(ksn)
                         : "memory");
                 }
                 // the slot is free in every CTA's producer (multicast), the accumulator is ready
@@ -892,7 +897,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         cfg.numAttrs = 1;
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
         ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
-                     2.0 * (double)nq * (double)N * (double)(p.KB * 64));
+                     2.0 * (double)nq * (double)N * (double)n);  // algorithmic FLOPs (unpadded K)
         SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mB, p));
         return OK;
     };
