@@ -663,9 +663,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // BF16 copy (RN) of each row plus its rounding-error norms.  With q = qh + ql,
 // x = xh + xl (qh, xh the BF16 values, ql, xl the exact residuals) and the
-// tensor core's fp32 accumulation of the exact products (error <= 2^-15 ||qh|| ||xh||
-// for K <= 256, with margin), Cauchy-Schwarz on q.x - qh.xh = qh.xl + ql.(xh + xl) gives
-//   |q.x - t| <= ||qh|| (||xl|| + 2^-15 ||xh||) + ||ql|| (||xh|| + ||xl||) = QH U + QL V.
+// tensor core's fp32 accumulation of the exact products (error <= K 2^-23 sum|qh_i xh_i|
+// even with truncating adds, <= 2^-15 ||qh|| ||xh|| for K <= 256; 2^-14 is used),
+// Cauchy-Schwarz on q.x - qh.xh = qh.xl + ql.(xh + xl) gives
+//   |q.x - t| <= ||qh|| (||xl|| + 2^-14 ||xh||) + ||ql|| (||xh|| + ||xl||) = QH U + QL V.
 // Rows get en = (U, V), queries en = (QH, QL), all rounded up (float64 sums with
 // a relative margin, then float32 RU).
 __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
@@ -697,7 +698,7 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
         const double m = 1.0 + 0x1p-40;  // covers the float64 sums and square roots
         const double H = sqrt(hh * m) * m, L = sqrt(ll * m) * m;
         en[r] = is_query ? make_float2(__double2float_ru(H), __double2float_ru(L))
-                         : make_float2(__double2float_ru((L + 0x1p-15 * H) * m), __double2float_ru((H + L) * m));
+                         : make_float2(__double2float_ru((L + 0x1p-14 * H) * m), __double2float_ru((H + L) * m));
     }
 }
 
