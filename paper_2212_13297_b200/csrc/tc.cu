@@ -2,10 +2,10 @@
 //
 // For a block of queries Q and the index rows X, the squared distance is
 // ||q||^2 + ||x||^2 - 2 q.x.  q.x is computed by tcgen05.mma (kind::f16, BF16
-// operands, FP32 accumulation in TMEM).  With RN-to-bf16 inputs the dot-product
-// error is at most c*||q||*||x||, c = 2^-8 + 2^-15 (input rounding 2*2^-9 plus
-// fp32 accumulation of <= 256 exact products), so every (query, row) pair gets
-// a rigorous interval [LB, UB] around its real squared distance.  Any k
+// operands, FP32 accumulation in TMEM).  The dot-product error is bounded per
+// pair by the BF16 rounding-error norms of the query and the row (QH U + QL V,
+// see to_bf16_norms_kernel), so every (query, row) pair gets a rigorous
+// interval [LB, UB] around its real squared distance.  Any k
 // distinct rows' upper bounds bound the k-th distance: each epilogue thread
 // keeps the k smallest UB of its own rows (k <= 32), k >= 2 also pools rows
 // hashed into k buckets per query (global atomicMin; the largest bucket minimum
