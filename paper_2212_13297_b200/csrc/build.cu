@@ -737,6 +737,15 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         GrowBuf &d_stats = lv_stats;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
         SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
+        if (trace) {  // allocation cost, separately
+            cudaStreamSynchronize(s);
+            auto a0 = std::chrono::steady_clock::now();
+            SSB_CUDA(d_stats.ensure(sizeof(float) * (size_t)stat_off, s));
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "[ssb build]   stats buffer %.2f GB (cap %.2f GB): %.3f ms\n", 4e-9 * stat_off,
+                    1e-9 * d_stats.cap,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count());
+        }
         SSB_CUDA(d_stats.ensure(sizeof(float) * (size_t)stat_off, s));
         SSB_CUDA(d_cmin.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(d_cmax.alloc(4 * (size_t)col_off, s));
