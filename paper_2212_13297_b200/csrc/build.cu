@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cstdio>
 #include <cstdlib>
@@ -46,7 +47,8 @@ namespace ssb {
 
 Index::~Index()
 {
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec};
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec,
+                    tcperm};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -609,6 +611,20 @@ struct BuildCfg {
 int finalize_tree(Index &ix, cudaStream_t s);
 
 // BF16 copy + row norms for the tensor-core filter (skipped when n is unsupported)
+__global__ void hash_keys_kernel(uint32_t *__restrict__ keys, uint32_t *__restrict__ pos, int64_t N)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    uint32_t h = (uint32_t)i;  // murmur3 fmix32: a bijection of 32-bit integers
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    keys[i] = h;
+    pos[i] = (uint32_t)i;
+}
+
 static int make_tc_operands(Index &ix, cudaStream_t s)
 {
     if (ix.n % 8 != 0 || ix.n > 256) return OK;
@@ -616,7 +632,29 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
     SSB_CUDA(cudaMalloc(&ix.xen, (size_t)ix.N * 8));
     SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)((ix.N + 127) / 128 * 128) * 16));  // padded to whole tiles
-    int rc = launch_to_bf16_norms(ix.X, nullptr, ix.N, ix.n, true, ix.Xb, ix.xn2, ix.xen, false, s);
+    // K-tc row order: a hashed permutation of the leaf order.  Leaf order puts a
+    // query's near neighbours next to each other, so its hits come in bursts in
+    // a few tiles, and a tile's epilogue (and with it the whole CTA) waits for the
+    // lane with the longest burst; hashing spreads the hits over the tiles.
+    const char *ord = getenv("SSB_TC_ROWORDER");  // "leaf": identity (diagnostics)
+    if (!(ord && !strcmp(ord, "leaf"))) {
+        DevBuf keys, keys2, pos, tmp;
+        SSB_CUDA(keys.alloc(4 * (size_t)ix.N, s));
+        SSB_CUDA(keys2.alloc(4 * (size_t)ix.N, s));
+        SSB_CUDA(pos.alloc(4 * (size_t)ix.N, s));
+        SSB_CUDA(cudaMalloc(&ix.tcperm, (size_t)ix.N * 4));
+        hash_keys_kernel<<<(unsigned)((ix.N + 255) / 256), 256, 0, s>>>(keys.as<uint32_t>(), pos.as<uint32_t>(), ix.N);
+        SSB_CHECK_LAUNCH();
+        size_t tb = 0;
+        SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                                 pos.as<uint32_t>(), ix.tcperm, (int)ix.N, 0, 32, s));
+        SSB_CUDA(tmp.alloc(tb, s));
+        SSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                                 pos.as<uint32_t>(), ix.tcperm, (int)ix.N, 0, 32, s));
+        note_launch(1);
+    }
+    int rc = launch_to_bf16_norms(ix.X, reinterpret_cast<const int32_t *>(ix.tcperm), ix.N, ix.n, true, ix.Xb,
+                                  ix.xn2, ix.xen, false, s);
     if (rc) return rc;
     SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 4) * 16));
     rc = launch_tc_row_consts(ix.xn2, ix.xen, ix.N, ix.rowc, s);

@@ -770,7 +770,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             qtc.clear();
         } else {
             tc_nc = hn;
-            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
+            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
                                 gb.as<unsigned int>(), tc_nc, so, s);
             if (rc) return rc;
             if (tc_nc) {
@@ -844,7 +844,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             uint32_t ns = 0;
             SSB_CUDA(cudaMemcpyAsync(&ns, nsub.p, 4, cudaMemcpyDeviceToHost, s));
             SSB_CUDA(cudaStreamSynchronize(s));
-            rc = launch_rescore(ix.X, n, ix.orig, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), nullptr, nullptr, ns, so,
+            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), nullptr, nullptr, ns, so,
                                 s);
             if (rc) return rc;
             SSB_CUDA(cudaStreamSynchronize(s));
@@ -962,7 +962,7 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     // exact rescoring of the candidates whose lower bound is within the final bound
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
     ScanOut so{keys.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
-    rc = launch_rescore(ix.X, n, ix.orig, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
+    rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
                         gb.as<unsigned int>(), tc_cap, so, s, cn.as<unsigned int>());
     if (rc) return rc;
     if (want_stats) {  // QueryStats only

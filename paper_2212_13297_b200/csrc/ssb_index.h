@@ -57,6 +57,7 @@ struct Index {
     void *Xb = nullptr;
     float *xn2 = nullptr;    // ||x||^2 per row
     float2 *xen = nullptr;   // per row (U, V): BF16 rounding-error norms (to_bf16_norms_kernel)
+    uint32_t *tcperm = nullptr;  // K-tc row order -> leaf-order position (null: identity)
     float4 *rowc = nullptr;   // per-row constants of the K-tc bounds
     float4 *tilec = nullptr;  // per 64-row half tile: two float4 of extremes of rowc
     double build_ms = 0.0;
@@ -78,7 +79,8 @@ int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *
 int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
-int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
+int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
+                   const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
                    cudaStream_t s, const unsigned int *nc_dev = nullptr);
 

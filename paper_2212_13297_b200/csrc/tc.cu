@@ -967,6 +967,7 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
 // rows and queries in the lane-transposed layout (global memory)
 template <int NT>
 __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
+                               const uint32_t *__restrict__ tcperm,
                                const float *__restrict__ Qp, const int32_t *__restrict__ qmap,
                                const uint2 *__restrict__ cand, const float *__restrict__ cand_lb,
                                const unsigned int *__restrict__ fbound, int64_t nc,
@@ -984,11 +985,12 @@ __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__re
         // (still >= the k-th distance) settles most of them without the row
         if (cand_lb && cand_lb[gp] > __uint_as_float(fbound[c.x])) continue;
         const int q = qmap ? qmap[c.x] : (int)c.x;
+        const uint32_t pos = tcperm ? tcperm[c.y] : c.y;  // K-tc row -> leaf-order position
         float qv[NT / 8];
         lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
-        const float d2 = lay_ed2<NT>(X + (int64_t)c.y * NT, qv, j, gmask);
+        const float d2 = lay_ed2<NT>(X + (int64_t)pos * NT, qv, j, gmask);
         if (j == 0) {
-            const uint64_t key = make_key(d2, row_id ? row_id[c.y] : c.y);
+            const uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
             const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
             if (key <= bound) {
                 const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
@@ -998,7 +1000,8 @@ __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__re
     }
 }
 
-int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Qp, const int32_t *qmap,
+int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
+                   const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
                    cudaStream_t s, const unsigned int *nc_dev)
 {
@@ -1007,10 +1010,10 @@ int launch_rescore(const float *X, int n, const uint32_t *row_id, const float *Q
     const unsigned grid = nc_dev ? (unsigned)(num_sms() * 8) : (unsigned)((nc * 8 + 255) / 256);
     ProfScope ps("rescore", s, nc_dev ? 0.0 : (double)nc * n * 4);
     switch (n) {
-    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
-    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
-    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
-    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 64: rescore_kernel<64><<<grid, 256, 0, s>>>(X, row_id, tcperm, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 96: rescore_kernel<96><<<grid, 256, 0, s>>>(X, row_id, tcperm, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 128: rescore_kernel<128><<<grid, 256, 0, s>>>(X, row_id, tcperm, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
+    case 256: rescore_kernel<256><<<grid, 256, 0, s>>>(X, row_id, tcperm, Qp, qmap, cand, cand_lb, fbound, nc, nc_dev, out); break;
     default:
         set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled rescore kernel");
         return ERR_USAGE;

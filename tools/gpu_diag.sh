@@ -1,4 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_tc.py -q -x 2>&1 | tail -1
-timeout 900 python bench.py --workload c3 > gpurun_out/b_c3.json 2> gpurun_out/b_c3.err
-python -c "
-import json; j=json.load(open('gpurun_out/b_c3.json')); print('c3', j['value'], j['e2e']['value'], j['ms_per_step'], j['roofline']['frac'], {k:(round(v['ms'],1),v['launches']) for k,v in j['kernels'].items()})"
+timeout 600 python -m pytest tests/test_gpu_tc.py tests/test_gpu_index.py -q -x 2>&1 | tail -1
+for o in leaf hash leaf hash; do echo "== $o"; SSB_TC_ROWORDER=$o timeout 120 python tools/cell_profile.py --rows 1000000 --sigmas 1.0,0.01 --ks 1,10 2>&1 | tail -4 | python -c "
+import sys,json
+for l in sys.stdin: j=json.loads(l); print(j['sigma'], j['k'], j['ms'], j['cand_series'], {k:v[0] for k,v in j['kernels'].items()})"; done
