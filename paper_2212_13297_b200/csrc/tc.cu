@@ -868,7 +868,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         p.gbucket = buckets.as<unsigned int>();
     }
     p.k = k;
-    p.warm = 4;
+    p.warm = 8;
     if (const char *e = getenv("SSB_TC_WARM")) p.warm = std::max(0, atoi(e));  // diagnostics
     p.cand = cand;
     p.cand_lb = cand_lb;
