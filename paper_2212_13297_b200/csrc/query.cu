@@ -920,20 +920,16 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     const int n = ix.n;
     *redo = false;
     DevBuf qlay, qb, qn2, qnrm, gb, cand, clb, cn, keys, cnt, thr, flags, qmax;
-    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
-    int rc = launch_layout_rows(Q, nullptr, B, n, qlay.as<float>(), true, s);
-    if (rc) return rc;
     const int nq_pad = (B + 127) / 128 * 128;
+    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
     SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
     SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
     SSB_CUDA(qnrm.alloc(8 * (size_t)nq_pad, s));
-    SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
-    rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnrm.as<float2>(), true, s);
-    if (rc) return rc;
     SSB_CUDA(qmax.alloc(4, s));
     SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
-    qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
-    SSB_CHECK_LAUNCH();
+    int rc = launch_tc_query_prep(Q, B, nq_pad, n, qlay.as<float>(), qb.p, qn2.as<float>(), qnrm.as<float2>(),
+                                  qmax.as<uint32_t>(), s);
+    if (rc) return rc;
     const int64_t slots = tc_bound_slots(B);
     SSB_CUDA(gb.alloc(4 * (size_t)slots, s));
     rc = qfill_u32(gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)

@@ -79,6 +79,8 @@ int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *
 int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
+int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,
+                         uint32_t *qmax, cudaStream_t s);
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
                    const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,

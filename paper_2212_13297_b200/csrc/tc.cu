@@ -702,6 +702,60 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
     }
 }
 
+// Everything the lean tensor-core batch needs from the raw queries in one pass
+// (one warp per query row; rows B..nq_pad-1 of the BF16 block are zeroed): the
+// lane-transposed float32 copy for rescoring, the BF16 operand, ||q||^2, the
+// rounding-error norms (QH, QL) and max |q| (NaN -> +inf, rejected by the host).
+__global__ void tc_query_prep_kernel(const float *__restrict__ Q, int B, int nq_pad, int n, float *__restrict__ qlay,
+                                     __nv_bfloat16 *__restrict__ qb, float *__restrict__ qn2,
+                                     float2 *__restrict__ qen, uint32_t *__restrict__ qmax)
+{
+    const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (r >= nq_pad) return;
+    const int lane = threadIdx.x & 31;
+    if (r >= B) {
+        for (int e = lane; e < n; e += 32) qb[(int64_t)r * n + e] = __float2bfloat16_rn(0.f);
+        return;
+    }
+    const float *s = Q + (int64_t)r * n;
+    double acc = 0.0, hh = 0.0, ll = 0.0;
+    float m = 0.f;
+    for (int e = lane; e < n; e += 32) {
+        const float v = __ldg(s + e);
+        qlay[(int64_t)r * n + layout_pos(n, e)] = v;
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        qb[(int64_t)r * n + e] = b;
+        const double vb = (double)__bfloat162float(b), dv = (double)v - vb;
+        acc += (double)v * (double)v;
+        hh += vb * vb;
+        ll += dv * dv;
+        const float a = fabsf(v);
+        m = (a != a) ? __int_as_float(0x7f800000) : fmaxf(m, a);
+    }
+    for (int off = 16; off; off >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        hh += __shfl_xor_sync(0xffffffffu, hh, off);
+        ll += __shfl_xor_sync(0xffffffffu, ll, off);
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    }
+    if (lane == 0) {
+        qn2[r] = __double2float_rn(acc);
+        const double mm = 1.0 + 0x1p-40;
+        qen[r] = make_float2(__double2float_ru(sqrt(hh * mm) * mm), __double2float_ru(sqrt(ll * mm) * mm));
+        atomicMax(qmax, __float_as_uint(m));
+    }
+}
+
+int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,
+                         uint32_t *qmax, cudaStream_t s)
+{
+    if (nq_pad == 0) return OK;
+    tc_query_prep_kernel<<<(unsigned)((nq_pad + 7) / 8), 256, 0, s>>>(Q, B, nq_pad, n, qlay, (__nv_bfloat16 *)qb, qn2,
+                                                                      qen, qmax);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float2 *en, bool is_query, cudaStream_t s)
 {
