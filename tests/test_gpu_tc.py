@@ -155,3 +155,14 @@ def test_tensor_route_overflow_paths(ssb, oracle, monkeypatch, hook, value):
         od2, oid = oracle.knn_scan(X, Q, k, threads=8)
         assert np.array_equal(ids.cpu().numpy(), oid), (hook, value, k)
         assert np.array_equal(bits(d2.cpu().numpy()), bits(od2)), (hook, value, k)
+
+
+@pytest.mark.parametrize("route", ["auto", "tensor", "tree"])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+def test_non_finite_queries_rejected(ssb, route, bad):
+    X = random_walks(3000, 64, 21)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=64, dataset_size=len(X), leaf_threshold=100))
+    Q = random_walks(5, 64, 22)
+    Q[3, 17] = bad
+    with pytest.raises(ssb.UsageError):
+        ssb.QueryEngine(idx).knn_device(Q, 3, route=route)
