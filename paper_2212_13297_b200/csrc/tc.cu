@@ -187,6 +187,7 @@ struct TcParams {
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
+    int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
     int skip_epi;              // diagnostics (SSB_TC_DIAG=1): epilogue only releases TMEM
 };
 
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (*(volatile unsigned *)stage_fill >= (unsigned)(TC_STAGE / 2)) flush();
             // refresh the bucket bound after this thread's own updates
             // (every 8th tile; the loads are independent so their latencies overlap)
-            if (touched && ((t & 7) == 7 || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
+            if (touched && ((t & p.rmask) == p.rmask || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
                 uint32_t mxb = 0;
                 if constexpr (KTOP > 0) {
 #pragma unroll
@@ -923,6 +924,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     }
     p.k = k;
     p.warm = 8;
+    p.rmask = 7;
+    if (const char *e = getenv("SSB_TC_RMASK")) p.rmask = std::max(0, atoi(e));  // diagnostics
     if (const char *e = getenv("SSB_TC_WARM")) p.warm = std::max(0, atoi(e));  // diagnostics
     p.cand = cand;
     p.cand_lb = cand_lb;
