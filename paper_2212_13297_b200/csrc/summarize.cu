@@ -142,18 +142,26 @@ __device__ __forceinline__ void stats_from(double cs_s, double cs_e, double c2_s
 
 constexpr int MAX_PTS = 130;
 
-__global__ void segment_stats_kernel(const float *__restrict__ X, int64_t N, int n,
-                                     const int32_t *__restrict__ pts_g, int npts,
-                                     const int32_t *__restrict__ seg_s, const int32_t *__restrict__ seg_e,
-                                     int m, float *__restrict__ mean, float *__restrict__ sd)
+// One thread per row, 128 rows per CTA; the rows are staged 16 columns at a time
+// through padded shared memory with coalesced float4 loads, and each thread runs
+// its float64 prefix sums (np.cumsum order) straight to the next boundary point.
+constexpr int SS_ROWS = 128, SS_W = 16;
+
+__global__ void __launch_bounds__(SS_ROWS)
+    segment_stats_kernel(const float *__restrict__ X, int64_t N, int n, const int32_t *__restrict__ pts_g, int npts,
+                         const int32_t *__restrict__ seg_s, const int32_t *__restrict__ seg_e, int m,
+                         float *__restrict__ mean, float *__restrict__ sd)
 {
     __shared__ int32_t pts[MAX_PTS];
+    __shared__ float tile[SS_ROWS][SS_W + 1];
     for (int i = threadIdx.x; i < npts; i += blockDim.x) pts[i] = pts_g[i];
     __syncthreads();
-    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (row >= N) return;
+    const int t = threadIdx.x;
+    const int64_t row0 = blockIdx.x * (int64_t)SS_ROWS;
+    const int64_t row = row0 + t;
+    const bool live = row < N;
+    const int rows_here = (int)min((int64_t)SS_ROWS, N - row0);
     double cs[MAX_PTS], c2[MAX_PTS];
-    const float *x = X + row * n;
     double a = 0.0, b = 0.0;
     int p = 0;
     while (p < npts && pts[p] == 0) {
@@ -161,16 +169,45 @@ __global__ void segment_stats_kernel(const float *__restrict__ X, int64_t N, int
         c2[p] = 0.0;
         p++;
     }
-    for (int i = 0; i < n && p < npts; i++) {
-        const double v = (double)__ldg(x + i);
-        a = __dadd_rn(a, v);
-        b = __dadd_rn(b, __dmul_rn(v, v));
-        while (p < npts && pts[p] == i + 1) {
-            cs[p] = a;
-            c2[p] = b;
-            p++;
+    for (int c0 = 0; c0 < n; c0 += SS_W) {
+        const int w = min(SS_W, n - c0);
+        if ((n & 3) == 0) {  // 16-byte aligned rows: float4 loads
+            for (int idx = t; idx < SS_ROWS * (SS_W / 4); idx += SS_ROWS) {
+                const int r = idx / (SS_W / 4), q4 = idx % (SS_W / 4);
+                if (r < rows_here && q4 * 4 < w) {
+                    const float4 f = __ldg(reinterpret_cast<const float4 *>(X + (row0 + r) * n + c0) + q4);
+                    tile[r][q4 * 4 + 0] = f.x;
+                    tile[r][q4 * 4 + 1] = f.y;
+                    tile[r][q4 * 4 + 2] = f.z;
+                    tile[r][q4 * 4 + 3] = f.w;
+                }
+            }
+        } else {
+            for (int idx = t; idx < SS_ROWS * SS_W; idx += SS_ROWS) {
+                const int r = idx / SS_W, e = idx % SS_W;
+                if (r < rows_here && e < w) tile[r][e] = __ldg(X + (row0 + r) * n + c0 + e);
+            }
         }
+        __syncthreads();
+        if (live) {
+            int i = 0;
+            while (i < w && p < npts) {
+                const int stop = min(w, pts[p] - c0);  // run to the next boundary point
+                for (; i < stop; i++) {
+                    const double v = (double)tile[t][i];
+                    a = __dadd_rn(a, v);
+                    b = __dadd_rn(b, __dmul_rn(v, v));
+                }
+                while (p < npts && pts[p] == c0 + i) {
+                    cs[p] = a;
+                    c2[p] = b;
+                    p++;
+                }
+            }
+        }
+        __syncthreads();
     }
+    if (!live) return;
     for (int jj = 0; jj < m; jj++) {
         const int s = seg_s[jj], e = seg_e[jj];
         stats_from(cs[s], cs[e], c2[s], c2[e], pts[e] - pts[s], mean[row * m + jj], sd[row * m + jj]);
@@ -183,8 +220,8 @@ int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, i
 {
     SSB_REQUIRE(npts <= MAX_PTS, "too many distinct segment boundaries");
     if (N == 0 || m == 0) return OK;
-    segment_stats_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(X, N, n, pts, npts, seg_s,
-                                                                     seg_e, m, mean, sd);
+    segment_stats_kernel<<<(unsigned)((N + SS_ROWS - 1) / SS_ROWS), SS_ROWS, 0, s>>>(X, N, n, pts, npts, seg_s, seg_e,
+                                                                                  m, mean, sd);
     SSB_CHECK_LAUNCH();
     return OK;
 }
