@@ -7,8 +7,8 @@
 // PAA: float32 pairwise sum of the w = n/16 points, then a correctly rounded
 // division by w (numpy's mean divides by an intp count, which promotes to
 // float64 and rounds back; double rounding is innocuous for division, so it
-// equals __fdiv_rn).  Symbol: #{breakpoints <= (double)paa} by binary search
-// over the 255 float64 breakpoints staged in shared memory.
+// equals __fdiv_rn).  Symbol: #{breakpoints <= (double)paa}, searched over the
+// breakpoints rounded up to float32 (exact for float32 PAA values).
 // Stats: float64 prefix sums accumulated strictly sequentially (np.cumsum),
 // mean=(cs[e]-cs[s])/w, msq likewise, sd=sqrt(max(msq-mean*mean,0)), both
 // rounded to float32 -- no FMA anywhere (--fmad=false + _rn intrinsics).
@@ -26,8 +26,11 @@ __global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
                              const double *__restrict__ bp_g, uint8_t *__restrict__ words,
                              float *__restrict__ paa_out, const uint32_t *__restrict__ rows)
 {
-    __shared__ double bp[ALPHABET];
-    for (int i = threadIdx.x; i < ALPHABET - 1; i += blockDim.x) bp[i] = bp_g[i];
+    // float thresholds thr[i] = RU(bp[i]): for a float p, (double)p >= bp[i] iff
+    // p >= thr[i]; a +inf sentinel makes the search 8 branch-free steps
+    __shared__ float thr[ALPHABET];
+    for (int i = threadIdx.x; i < ALPHABET; i += blockDim.x)
+        thr[i] = i < ALPHABET - 1 ? __double2float_ru(bp_g[i]) : __int_as_float(0x7f800000);
     __syncthreads();
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= N * WORD_SEGMENTS) return;
@@ -55,7 +58,11 @@ __global__ void words_kernel(const float *__restrict__ X, int64_t N, int n,
         sum = pw_f32_rt(x, n / WORD_SEGMENTS);
     }
     const float p = __fdiv_rn(sum, (float)(n / WORD_SEGMENTS));
-    words[t] = (uint8_t)sax_symbol((double)p, bp);
+    int lo = 0;
+#pragma unroll
+    for (int step = ALPHABET / 2; step; step >>= 1)
+        if (thr[lo + step - 1] <= p) lo += step;
+    words[t] = (uint8_t)lo;
     if (paa_out) paa_out[t] = p;
 }
 
