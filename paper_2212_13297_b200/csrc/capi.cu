@@ -65,7 +65,7 @@ int num_sms()
 
 int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, int npts,
                          const int32_t *seg_s, const int32_t *seg_e, int m, float *mean, float *sd,
-                         cudaStream_t s);
+                         cudaStream_t s, bool contig);
 
 __global__ void iota_kernel(int32_t *a, int n)
 {
@@ -183,8 +183,10 @@ int ssb_segment_stats(const float *X, int64_t N, int32_t n, const int64_t *start
     SSB_CUDA(cudaMemcpyAsync(dp.p, pts.data(), pts.size() * 4, cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaMemcpyAsync(ds.p, hs.data(), (size_t)m * 4, cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaMemcpyAsync(de.p, he.data(), (size_t)m * 4, cudaMemcpyHostToDevice, s));
+    bool contig = (int)pts.size() == m + 1;  // segment j = [pts[j], pts[j+1])
+    for (int j = 0; j < m && contig; j++) contig = hs[j] == j && he[j] == j + 1;
     int rc = launch_segment_stats(X, N, n, dp.as<int32_t>(), (int)pts.size(), ds.as<int32_t>(),
-                                  de.as<int32_t>(), m, mean, sd, s);
+                                  de.as<int32_t>(), m, mean, sd, s, contig);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));  // host vectors die at return
     return OK;

@@ -14,6 +14,9 @@
 // rounded to float32 -- no FMA anywhere (--fmad=false + _rn intrinsics).
 #include <cuda_runtime.h>
 
+#include <climits>
+#include <cstdlib>
+
 #include "layout.cuh"
 #include "ssb_common.cuh"
 #include "ssb_internal.h"
@@ -139,8 +142,12 @@ constexpr int MAX_PTS = 130;
 // One thread per row, 128 rows per CTA; the rows are staged 16 columns at a time
 // through padded shared memory with coalesced float4 loads, and each thread runs
 // its float64 prefix sums (np.cumsum order) straight to the next boundary point.
+// CONTIG: segments j = [pts[j], pts[j+1]) (the common contiguous case): each
+// segment's statistics are emitted at its end point from two running prefix
+// values, with no per-thread point arrays (which would live in local memory).
 constexpr int SS_ROWS = 128, SS_W = 16;
 
+template <bool CONTIG>
 __global__ void __launch_bounds__(SS_ROWS)
     segment_stats_kernel(const float *__restrict__ X, int64_t N, int n, const int32_t *__restrict__ pts_g, int npts,
                          const int32_t *__restrict__ seg_s, const int32_t *__restrict__ seg_e, int m,
@@ -155,12 +162,14 @@ __global__ void __launch_bounds__(SS_ROWS)
     const int64_t row = row0 + t;
     const bool live = row < N;
     const int rows_here = (int)min((int64_t)SS_ROWS, N - row0);
-    double cs[MAX_PTS], c2[MAX_PTS];
-    double a = 0.0, b = 0.0;
+    double cs[CONTIG ? 1 : MAX_PTS], c2[CONTIG ? 1 : MAX_PTS];
+    double a = 0.0, b = 0.0, pa = 0.0, pb = 0.0;  // running sums; CONTIG: at the last point
     int p = 0;
     while (p < npts && pts[p] == 0) {
-        cs[p] = 0.0;
-        c2[p] = 0.0;
+        if constexpr (!CONTIG) {
+            cs[p] = 0.0;
+            c2[p] = 0.0;
+        }
         p++;
     }
     for (int c0 = 0; c0 < n; c0 += SS_W) {
@@ -193,29 +202,177 @@ __global__ void __launch_bounds__(SS_ROWS)
                     b = __dadd_rn(b, __dmul_rn(v, v));
                 }
                 while (p < npts && pts[p] == c0 + i) {
-                    cs[p] = a;
-                    c2[p] = b;
+                    if constexpr (CONTIG) {  // segment p-1 = [pts[p-1], pts[p]) ends here
+                        if (p > 0)
+                            stats_from(pa, a, pb, b, pts[p] - pts[p - 1], mean[row * m + p - 1], sd[row * m + p - 1]);
+                        pa = a;
+                        pb = b;
+                    } else {
+                        cs[p] = a;
+                        c2[p] = b;
+                    }
                     p++;
                 }
             }
         }
         __syncthreads();
     }
-    if (!live) return;
+    if (CONTIG || !live) return;
     for (int jj = 0; jj < m; jj++) {
         const int s = seg_s[jj], e = seg_e[jj];
         stats_from(cs[s], cs[e], c2[s], c2[e], pts[e] - pts[s], mean[row * m + jj], sd[row * m + jj]);
     }
 }
 
+// Aligned rows (n % 4 == 0): a 3-stage cp.async pipeline of 128-row x W-column
+// stages keeps two stages of loads in flight behind the float64 chains.  Each
+// stage row is W/4 16-byte chunks stored at a row-dependent XOR slot, so the
+// per-thread float4 reads of its own row are conflict-free.  A chunk with no
+// boundary point inside runs its four elements without per-element checks.
+constexpr int SA_ROWS = 128, SA_STG = 3;
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int W>
+__device__ __forceinline__ int sa_slot(int c, int r)
+{
+    static_assert(W == 16 || W == 32, "stage width");
+    return W == 32 ? c ^ (r & 7) : c ^ ((r >> 1) & 3);  // 8 distinct 16-byte bank groups per 8 rows
+}
+
+template <bool CONTIG, int W>
+__global__ void __launch_bounds__(SA_ROWS)
+    segment_stats_async_kernel(const float *__restrict__ X, int64_t N, int n, const int32_t *__restrict__ pts_g,
+                               int npts, const int32_t *__restrict__ seg_s, const int32_t *__restrict__ seg_e,
+                               int m, float *__restrict__ mean, float *__restrict__ sd)
+{
+    constexpr int CH = W / 4;
+    extern __shared__ float4 stage4[];  // [SA_STG][SA_ROWS][CH]
+    __shared__ int32_t pts[MAX_PTS + 1];
+    for (int i = threadIdx.x; i < npts; i += blockDim.x) pts[i] = pts_g[i];
+    if (threadIdx.x == 0) pts[npts] = INT32_MAX;
+    const int t = threadIdx.x;
+    const int64_t row0 = blockIdx.x * (int64_t)SA_ROWS;
+    const int64_t row = row0 + t;
+    const bool live = row < N;
+    const int rows_here = (int)min((int64_t)SA_ROWS, N - row0);
+    const int nst = (n + W - 1) / W;
+    auto load = [&](int st) {
+        if (st < nst) {
+            const int c0 = st * W, ch = min(W, n - c0) / 4;
+            float4 *dst = stage4 + (size_t)(st % SA_STG) * SA_ROWS * CH;
+            for (int idx = t; idx < SA_ROWS * CH; idx += SA_ROWS) {
+                const int r = idx / CH, c = idx % CH;
+                if (r < rows_here && c < ch)
+                    cp_async16(dst + r * CH + sa_slot<W>(c, r), X + (row0 + r) * n + c0 + c * 4);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load(0);
+    load(1);
+    __syncthreads();  // pts
+    double cs[CONTIG ? 1 : MAX_PTS], c2[CONTIG ? 1 : MAX_PTS];
+    double a = 0.0, b = 0.0, pa = 0.0, pb = 0.0;
+    int p = 0, nextp = pts[0];
+    auto at_point = [&](int col) {
+        while (nextp == col) {
+            if constexpr (CONTIG) {
+                if (p > 0) stats_from(pa, a, pb, b, col - pts[p - 1], mean[row * m + p - 1], sd[row * m + p - 1]);
+                pa = a;
+                pb = b;
+            } else {
+                cs[p] = a;
+                c2[p] = b;
+            }
+            nextp = pts[++p];
+        }
+    };
+    auto add = [&](float x) {
+        const double v = (double)x;
+        a = __dadd_rn(a, v);
+        b = __dadd_rn(b, __dmul_rn(v, v));
+    };
+    for (int st = 0; st < nst; st++) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // stage st landed for every thread; stage st-1 fully consumed
+        load(st + 2);
+        if (live) {
+            const float4 *src = stage4 + (size_t)(st % SA_STG) * SA_ROWS * CH + t * CH;
+            const int c0 = st * W, ch = min(W, n - c0) / 4;
+            for (int c = 0; c < ch; c++) {
+                const float4 f = src[sa_slot<W>(c, t)];
+                const int col = c0 + c * 4;
+                if (nextp >= col + 4) {  // no boundary point before any of the four
+                    add(f.x);
+                    add(f.y);
+                    add(f.z);
+                    add(f.w);
+                } else {
+                    at_point(col);
+                    add(f.x);
+                    at_point(col + 1);
+                    add(f.y);
+                    at_point(col + 2);
+                    add(f.z);
+                    at_point(col + 3);
+                    add(f.w);
+                }
+            }
+        }
+    }
+    if (!live) return;
+    at_point(n);
+    if constexpr (!CONTIG) {
+        for (int jj = 0; jj < m; jj++) {
+            const int s = seg_s[jj], e = seg_e[jj];
+            stats_from(cs[s], cs[e], c2[s], c2[e], pts[e] - pts[s], mean[row * m + jj], sd[row * m + jj]);
+        }
+    }
+}
+
+template <int W>
+static int launch_stats_async(const float *X, int64_t N, int n, const int32_t *pts, int npts, const int32_t *seg_s,
+                              const int32_t *seg_e, int m, float *mean, float *sd, cudaStream_t s, bool contig)
+{
+    constexpr size_t smem = (size_t)SA_STG * SA_ROWS * W * 4;
+    static bool attr = false;
+    if (!attr) {
+        SSB_CUDA(cudaFuncSetAttribute(segment_stats_async_kernel<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        SSB_CUDA(cudaFuncSetAttribute(segment_stats_async_kernel<false, W>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((N + SA_ROWS - 1) / SA_ROWS);
+    if (contig)
+        segment_stats_async_kernel<true, W><<<grid, SA_ROWS, smem, s>>>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd);
+    else
+        segment_stats_async_kernel<false, W><<<grid, SA_ROWS, smem, s>>>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
 int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, int npts,
                          const int32_t *seg_s, const int32_t *seg_e, int m, float *mean, float *sd,
-                         cudaStream_t s)
+                         cudaStream_t s, bool contig)
 {
     SSB_REQUIRE(npts <= MAX_PTS, "too many distinct segment boundaries");
     if (N == 0 || m == 0) return OK;
-    segment_stats_kernel<<<(unsigned)((N + SS_ROWS - 1) / SS_ROWS), SS_ROWS, 0, s>>>(X, N, n, pts, npts, seg_s, seg_e,
-                                                                                  m, mean, sd);
+    if ((n & 3) == 0 && !getenv("SSB_STATS_SYNC")) {
+        static const int w = getenv("SSB_STATS_W") ? atoi(getenv("SSB_STATS_W")) : 32;
+        return w != 16 ? launch_stats_async<32>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd, s, contig)
+                       : launch_stats_async<16>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd, s, contig);
+    }
+    const unsigned grid = (unsigned)((N + SS_ROWS - 1) / SS_ROWS);
+    if (contig)
+        segment_stats_kernel<true><<<grid, SS_ROWS, 0, s>>>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd);
+    else
+        segment_stats_kernel<false><<<grid, SS_ROWS, 0, s>>>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd);
     SSB_CHECK_LAUNCH();
     return OK;
 }

@@ -118,3 +118,16 @@ def test_segment_stats_match_golden(ssb):
         mean, sd = segment_stats_matrix(g["X"], g[f"starts_{name}"], g[f"ends_{name}"])
         assert np.array_equal(bits(mean.cpu().numpy()), bits(g[f"mean_{name}"])), name
         assert np.array_equal(bits(sd.cpu().numpy()), bits(g[f"sd_{name}"])), name
+
+
+@pytest.mark.parametrize("starts,ends", [([5, 20], [20, 31]),  # contiguous, not from 0
+                                         ([0, 10, 3], [64, 40, 9]),  # overlapping / unsorted
+                                         ([1, 63], [2, 64])])  # gaps
+def test_segment_stats_general_segments(ssb, oracle, starts, ends):
+    from paper_2212_13297_b200.summarize import segment_stats_matrix
+
+    X = random_walks(3000, 64, 31)
+    mean, sd = segment_stats_matrix(X, np.array(starts), np.array(ends))
+    omean, osd = oracle.segment_stats(X, np.array(starts), np.array(ends))
+    assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
+    assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))

@@ -21,7 +21,9 @@ def main():
     starts = np.arange(16) * 16
     ends = starts + 16
     for name, fn in (("words", lambda: S.paa_words(X)), ("words+paa", lambda: S.paa_words(X, with_paa=True)),
-                     ("segment_stats m=16", lambda: S.segment_stats_matrix(X, starts, ends))):
+                     ("segment_stats m=16", lambda: S.segment_stats_matrix(X, starts, ends)),
+                     ("segment_stats m=16 overlapping",
+                      lambda: S.segment_stats_matrix(X, starts // 2, ends))):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
