@@ -25,6 +25,7 @@
 //   K-gain       per node: QoS gains (f64, numpy pairwise order), argmax
 //   K-part       stable partition of the split nodes' members (CUB scan)
 // Finally K-gather writes the rows, ids and words in leaf order.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,6 +39,7 @@
 #include <memory>
 #include <vector>
 
+#include "layout.cuh"
 #include "ssb_common.cuh"
 #include "ssb_index.h"
 #include "ssb_internal.h"
@@ -194,6 +196,166 @@ __global__ void __launch_bounds__(CHUNK)
     if (bad) atomicOr(nonfinite, 1);
 }
 
+// K-stats, pipelined: the same arithmetic and outputs as build_stats_kernel,
+// with the chunk's rows staged W columns at a time through a 3-stage cp.async
+// ring (two stages of loads in flight behind the float64 chains).  Thread t
+// copies 16-byte piece t % (W/4) of rows t / (W/4) + k * (128 / (W/4)); each
+// thread then walks its own row from shared memory (XOR-swizzled float4 slots,
+// conflict-free), handling prefix events (segment midpoints and ends) only in
+// the float4 chunks that contain one.  Needs n % 4 == 0.
+constexpr int BS_STG = 3;
+
+template <int W>
+__global__ void __launch_bounds__(CHUNK)
+    build_stats_async_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
+                             const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
+                             float *__restrict__ stats, int *__restrict__ nonfinite)
+{
+    constexpr int CH = W / 4;            // 16-byte pieces per staged row
+    constexpr int RPP = CHUNK / CH;      // rows per copy pass
+    extern __shared__ float4 bs_stage[];  // [BS_STG][CHUNK][CH]
+    __shared__ NodeDesc nd;
+    const Chunk ch = chunks[blockIdx.x];
+    if (threadIdx.x == 0) nd = nodes[ch.node];
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int cnt_here = (int)ch.cnt;
+    // rows this thread copies: t / CH + k * RPP
+    const int pc = t % CH;
+    const float *rowp[CH];
+#pragma unroll
+    for (int k = 0; k < CH; k++) {
+        const int r = t / CH + k * RPP;
+        rowp[k] = r < cnt_here ? X + (int64_t)perm[nd.first + ch.m0 + r] * n + pc * 4 : nullptr;
+    }
+    const int nst = (n + W - 1) / W;
+    auto load = [&](int st) {
+        if (st < nst) {
+            const int c0 = st * W;
+            if (pc * 4 < n - c0) {
+                float4 *dst = bs_stage + (size_t)(st % BS_STG) * CHUNK * CH;
+#pragma unroll
+                for (int k = 0; k < CH; k++) {
+                    const int r = t / CH + k * RPP;
+                    if (rowp[k]) cp_async16(dst + r * CH + sa_slot<W>(pc, r), rowp[k] + c0);
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load(0);
+    load(1);
+    const int m = nd.m;
+    const bool live = t < cnt_here;
+    double a = 0.0, b = 0.0;     // running prefix sums
+    double ca = 0.0, c2a = 0.0;  // at the current segment start
+    double cm = 0.0, c2m = 0.0;  // at the current segment midpoint
+    int seg = 0;
+    int sa = 0, sb = nd.ep[0], mid = sb / 2;
+    int ev = mid > sa ? mid : sb;  // next prefix event
+    const int64_t cnt = nd.count;
+    float *out = stats + nd.stat_off + ch.m0 + t;
+    auto at_event = [&](int col) {  // prefix index col reached (before adding element col)
+        while (ev == col) {
+            if (ev == mid && mid < sb) {
+                cm = a;
+                c2m = b;
+                ev = sb;
+            } else {
+                float mu, sd;
+                stats_w(ca, a, c2a, b, sb - sa, mu, sd);
+                out[(int64_t)seg * cnt] = mu;
+                out[(int64_t)(m + seg) * cnt] = sd;
+                if (sb - sa >= 2) {
+                    stats_w(ca, cm, c2a, c2m, mid - sa, mu, sd);
+                    out[(int64_t)(2 * m + seg) * cnt] = mu;
+                    out[(int64_t)(3 * m + seg) * cnt] = sd;
+                    stats_w(cm, a, c2m, b, sb - mid, mu, sd);
+                    out[(int64_t)(4 * m + seg) * cnt] = mu;
+                    out[(int64_t)(5 * m + seg) * cnt] = sd;
+                }
+                ca = a;
+                c2a = b;
+                seg++;
+                if (seg < m) {
+                    sa = sb;
+                    sb = nd.ep[seg];
+                    mid = (sa + sb) / 2;
+                    ev = mid > sa ? mid : sb;
+                } else {
+                    ev = INT_MAX;
+                }
+            }
+        }
+    };
+    auto add = [&](float x) {
+        const double v = (double)x;
+        a = __dadd_rn(a, v);
+        b = __dadd_rn(b, __dmul_rn(v, v));
+    };
+    for (int st = 0; st < nst; st++) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // stage st landed for every thread; stage st-1 fully consumed
+        load(st + 2);
+        if (live) {
+            const float4 *src = bs_stage + (size_t)(st % BS_STG) * CHUNK * CH + t * CH;
+            const int c0 = st * W, nch = min(W, n - c0) / 4;
+            for (int c = 0; c < nch; c++) {
+                const float4 f = src[sa_slot<W>(c, t)];
+                const int col = c0 + c * 4;
+                if (ev >= col + 4) {  // no prefix event before any of the four
+                    add(f.x);
+                    add(f.y);
+                    add(f.z);
+                    add(f.w);
+                } else {
+                    at_event(col);
+                    add(f.x);
+                    at_event(col + 1);
+                    add(f.y);
+                    at_event(col + 2);
+                    add(f.z);
+                    at_event(col + 3);
+                    add(f.w);
+                }
+            }
+        }
+    }
+    if (!live) return;
+    at_event(n);
+    if (!(isfinite(a) && isfinite(b))) atomicOr(nonfinite, 1);
+}
+
+template <int W>
+static int launch_build_stats_async(const float *X, int n, const uint32_t *perm, const NodeDesc *nodes,
+                                    const Chunk *chunks, int64_t nchunks, float *stats, int *nonfinite,
+                                    cudaStream_t s)
+{
+    constexpr size_t smem = (size_t)BS_STG * CHUNK * W * 4;
+    static bool attr = false;
+    if (!attr) {
+        SSB_CUDA(cudaFuncSetAttribute(build_stats_async_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+    }
+    build_stats_async_kernel<W><<<(unsigned)nchunks, CHUNK, smem, s>>>(X, n, perm, nodes, chunks, stats, nonfinite);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+static int launch_build_stats(const float *X, int n, const uint32_t *perm, const NodeDesc *nodes,
+                              const Chunk *chunks, int64_t nchunks, float *stats, int *nonfinite, cudaStream_t s)
+{
+    static const int w = getenv("SSB_BSTATS_W") ? atoi(getenv("SSB_BSTATS_W")) : 16;
+    if (n % 4 == 0 && w == 16)
+        return launch_build_stats_async<16>(X, n, perm, nodes, chunks, nchunks, stats, nonfinite, s);
+    if (n % 4 == 0 && w == 32)
+        return launch_build_stats_async<32>(X, n, perm, nodes, chunks, nchunks, stats, nonfinite, s);
+    build_stats_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(X, n, perm, nodes, chunks, stats, nonfinite);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
 // candidate c of a node (tree.py:220-237 order): seg = c/6, r = c%6,
 // attr = r/3 (0 mean, 1 sd), lay = r%3 (0 horizontal, 1 left half, 2 right half)
 __device__ __forceinline__ int route_col(int m, int c)
@@ -264,8 +426,6 @@ constexpr int ACC_PER_CAND = 2 * (M_MAX + 1) * 2 * 2;
 // column would serialise on the same few addresses)
 constexpr int RTHREADS = 256;
 constexpr uint32_t MM_RANGE = 65536;   // members per CTA in K-minmax
-constexpr uint32_t EV_PER_THREAD = 16;  // members per thread in K-eval
-constexpr uint32_t EV_RANGE = RTHREADS * EV_PER_THREAD;
 
 struct Range {
     uint32_t node;
@@ -293,13 +453,13 @@ __device__ __forceinline__ uint32_t block_reduce_u32(uint32_t v, uint32_t *sh)
 __global__ void __launch_bounds__(RTHREADS)
     build_minmax_range_kernel(const NodeDesc *__restrict__ nodes, const Range *__restrict__ ranges,
                               const float *__restrict__ stats, uint32_t *__restrict__ cmin,
-                              uint32_t *__restrict__ cmax)
+                              uint32_t *__restrict__ cmax, int cols_per_seg)
 {
     __shared__ uint32_t sh[RTHREADS / 32];
     const Range rg = ranges[blockIdx.x];
     const NodeDesc nd = nodes[rg.node];
     const int col = blockIdx.y;
-    if (col >= 6 * nd.m) return;
+    if (col >= cols_per_seg * nd.m) return;
     const int seg = col % nd.m;
     const int sa = seg ? nd.ep[seg - 1] : 0;
     if (col >= 2 * nd.m && nd.ep[seg] - sa < 2) return;  // no halves
@@ -318,79 +478,139 @@ __global__ void __launch_bounds__(RTHREADS)
     }
 }
 
-// K-eval: grid (split-set range, candidate).  Each thread holds 16 members'
-// sides in a bit mask; per result column both sides' min/max are reduced in
-// the block and merged into the candidate's accumulators once.
-__global__ void __launch_bounds__(RTHREADS)
-    build_eval_range_kernel(const NodeDesc *__restrict__ nodes, const Range *__restrict__ ranges,
-                            const float *__restrict__ stats, const double *__restrict__ thr,
-                            const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
-                            uint32_t *__restrict__ nleft)
+// K-eval, warp per candidate: grid = (split-set range, candidate group).  The
+// CTA stages 64-member tiles of ALL the node's stat columns (ordered keys,
+// column-major, padded) in shared memory; warp w owns candidate
+// c = group * EV_WARPS + w, computes its sides with two ballots per tile, and
+// lane l owns the result tasks q = l, l + 32, ... (q = 2j + attr): per member a
+// warp-uniform side bit picks the L or R accumulators, so each (member,
+// candidate, task) costs one shared load and two integer min/max.  Partial
+// results go to the node's accumulators once per CTA.
+constexpr int EV_WARPS = 16;
+constexpr int EV_T = 64;                 // members per tile
+constexpr uint32_t EV2_RANGE = 2048;     // members per CTA
+
+struct EvTask {
+    uint32_t node;
+    uint32_t m0;
+    uint32_t cnt;
+    uint32_t cg;  // candidate group
+};
+
+template <int S>  // result-task slots per lane: 2 * (m + 1) <= 32 * S
+__global__ void __launch_bounds__(EV_WARPS * 32)
+    build_eval_warp_kernel(const NodeDesc *__restrict__ nodes, const EvTask *__restrict__ tasks,
+                           const float *__restrict__ stats, const double *__restrict__ thr,
+                           const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
+                           uint32_t *__restrict__ nleft)
 {
-    __shared__ uint32_t sh[RTHREADS / 32];
-    const Range rg = ranges[blockIdx.x];
-    const NodeDesc nd = nodes[rg.node];
-    const int c = blockIdx.y;
-    if (c >= 6 * nd.m || !valid[nd.col_off + c]) return;
-    const int t = threadIdx.x;
+    extern __shared__ uint4 ev_tile4[];  // [6m][EV_T + 4] u32
+    uint32_t *ev_tile = reinterpret_cast<uint32_t *>(ev_tile4);
+    __shared__ NodeDesc nd;
+    __shared__ EvTask tk;
+    if (threadIdx.x == 0) {
+        tk = tasks[blockIdx.x];
+        nd = nodes[tk.node];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = nd.m, ncol = 6 * m;
+    const int c = (int)tk.cg * EV_WARPS + warp;
+    const bool active = c < ncol && valid[nd.col_off + c];
+    constexpr int TS = EV_T + 4;  // 16-byte aligned columns
+    // this lane's result tasks: column offsets in the tile (or -1)
+    int coff[S];
+    const int lay = active ? (c % 6) % 3 : 0;
+    const int mm = m + (lay ? 1 : 0);
+#pragma unroll
+    for (int sl = 0; sl < S; sl++) {
+        const int q = lane + 32 * sl;
+        coff[sl] = -1;
+        if (active && q < 2 * mm) {
+            int cmean, csd, w;
+            result_col(nd, c, q >> 1, cmean, csd, w);
+            coff[sl] = ((q & 1) ? csd : cmean) * TS;
+        }
+    }
+    const int rcol = active ? route_col(m, c) * TS : 0;
+    const double th = active ? thr[nd.col_off + c] : 0.0;
+    uint32_t lmin[S], lmax[S], rmin[S], rmax[S];
+#pragma unroll
+    for (int sl = 0; sl < S; sl++) {
+        lmin[sl] = rmin[sl] = 0xffffffffu;
+        lmax[sl] = rmax[sl] = 0u;
+    }
+    uint32_t nl = 0;
     const int64_t cnt = nd.count;
-    const float *st = stats + nd.stat_off + rg.m0;
-    const double th = thr[nd.col_off + c];
-    const float *rv = st + (int64_t)route_col(nd.m, c) * cnt;
-    uint32_t lmask = 0, live = 0;
-#pragma unroll
-    for (uint32_t r = 0; r < EV_PER_THREAD; r++) {
-        const uint32_t i = r * RTHREADS + t;
-        if (i < rg.cnt) {
-            live |= 1u << r;
-            if ((double)rv[i] < th) lmask |= 1u << r;
+    const float *st = stats + nd.stat_off + tk.m0;
+    for (uint32_t t0 = 0; t0 < tk.cnt; t0 += EV_T) {
+        const int tn = (int)min((uint32_t)EV_T, tk.cnt - t0);
+        __syncthreads();  // previous tile consumed
+        for (int idx = threadIdx.x; idx < ncol * EV_T; idx += blockDim.x) {
+            const int col = idx / EV_T, i = idx % EV_T;
+            if (i < tn) ev_tile[col * TS + i] = okey(__ldg(st + (int64_t)col * cnt + t0 + i));
         }
-    }
-    {   // n_left
-        uint32_t nl = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(lmask));
         __syncthreads();
-        if ((t & 31) == 0) sh[t >> 5] = nl;
-        __syncthreads();
-        if (t == 0) {
-            uint32_t tot = 0;
-            for (int w = 0; w < RTHREADS / 32; w++) tot += sh[w];
-            atomicAdd(&nleft[nd.col_off + c], tot);
+        if (!active) continue;
+        uint32_t mk[EV_T / 32];
+#pragma unroll
+        for (int h = 0; h < EV_T / 32; h++) {
+            const int i = lane + 32 * h;
+            const bool left = i < tn && (double)okey_inv(ev_tile[rcol + i]) < th;
+            mk[h] = __ballot_sync(0xffffffffu, left);
+            nl += __popc(mk[h]);
         }
-    }
-    uint32_t *nacc = acc + nd.acc_off;
-    const int lay = (c % 6) % 3;
-    const int mm = nd.m + (lay ? 1 : 0);
-    for (int j = 0; j < mm; j++) {
-        int cmean, csd, w;
-        result_col(nd, c, j, cmean, csd, w);
+        auto upd = [&](int sl, uint32_t k, bool bit) {
+            if (bit) {
+                lmin[sl] = min(lmin[sl], k);
+                lmax[sl] = max(lmax[sl], k);
+            } else {
+                rmin[sl] = min(rmin[sl], k);
+                rmax[sl] = max(rmax[sl], k);
+            }
+        };
 #pragma unroll
-        for (int attr = 0; attr < 2; attr++) {
-            const float *cv = st + (int64_t)(attr ? csd : cmean) * cnt;
-            uint32_t lmin = 0xffffffffu, lmax = 0u, rmin = 0xffffffffu, rmax = 0u;
+        for (int h = 0; h < EV_T / 32; h++) {
+            const int i0 = 32 * h;
+            const uint32_t b = mk[h];
+            if (tn - i0 >= 32) {  // full 32 members: unrolled, 16-byte loads, predicated updates
 #pragma unroll
-            for (uint32_t r = 0; r < EV_PER_THREAD; r++) {
-                if (!(live >> r & 1u)) continue;
-                const uint32_t k = okey(cv[r * RTHREADS + t]);
-                if (lmask >> r & 1u) {
-                    lmin = min(lmin, k);
-                    lmax = max(lmax, k);
-                } else {
-                    rmin = min(rmin, k);
-                    rmax = max(rmax, k);
+                for (int sl = 0; sl < S; sl++) {
+                    if (coff[sl] < 0) continue;
+                    const uint4 *src = reinterpret_cast<const uint4 *>(ev_tile + coff[sl] + i0);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; i4++) {
+                        const uint4 k = src[i4];
+                        upd(sl, k.x, (b >> (4 * i4 + 0)) & 1u);
+                        upd(sl, k.y, (b >> (4 * i4 + 1)) & 1u);
+                        upd(sl, k.z, (b >> (4 * i4 + 2)) & 1u);
+                        upd(sl, k.w, (b >> (4 * i4 + 3)) & 1u);
+                    }
                 }
-            }
-            lmin = block_reduce_u32<false>(lmin, sh);
-            lmax = block_reduce_u32<true>(lmax, sh);
-            rmin = block_reduce_u32<false>(rmin, sh);
-            rmax = block_reduce_u32<true>(rmax, sh);
-            if (t == 0) {
-                atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin);
-                atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax);
-                atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin);
-                atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax);
+            } else {
+                for (int i = 0; i < tn - i0; i++)
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++)
+                        if (coff[sl] >= 0) upd(sl, ev_tile[coff[sl] + i0 + i], (b >> i) & 1u);
             }
         }
     }
+    if (!active) return;
+    uint32_t *nacc = acc + nd.acc_off;
+#pragma unroll
+    for (int sl = 0; sl < S; sl++) {
+        if (coff[sl] < 0) continue;
+        const int q = lane + 32 * sl, j = q >> 1, attr = q & 1;
+        if (lmin[sl] != 0xffffffffu) {
+            atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin[sl]);
+            atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax[sl]);
+        }
+        if (rmin[sl] != 0xffffffffu) {
+            atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin[sl]);
+            atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax[sl]);
+        }
+    }
+    if (lane == 0 && nl) atomicAdd(&nleft[nd.col_off + c], nl);
 }
 
 // tree.py:211-217 _qos over one side (or the union), float64, numpy pairwise order
@@ -550,20 +770,168 @@ __global__ void gather_rows_kernel(const float *__restrict__ X, int n, const uin
     if (lane == 0) inv[src] = (uint32_t)row;
 }
 
+// K-gather, fused (the index's one pass over its rows, in leaf order): reads
+// each source row once (logical order, coalesced float4) and writes
+//   * the lane-transposed float32 row (layout.cuh), leaf order;
+//   * the SAX word (summarize.py:89-121 arithmetic, as words_kernel);
+//   * the BF16 K-tc operand + (||x||^2, U, V) at the row's hashed K-tc slot
+//     (to_bf16_norms_kernel arithmetic: float64 sums, rounded up);
+//   * inv[src] = position; max |x| (one atomic per CTA).
+// One warp per row; the logical row is staged in shared memory with one pad
+// word per word segment, so the 16 PAA lanes read distinct banks.
+struct FinalizeArgs {
+    const float *X;         // source rows, logical order
+    const uint32_t *perm;   // position -> source row (null: identity)
+    int64_t N;
+    int n;
+    float *Xo;              // N x n, layout order
+    uint8_t *words;         // N x 16 (null: skip)
+    const double *bp;       // 255 breakpoints
+    uint32_t *inv;          // source row -> position (null: skip)
+    __nv_bfloat16 *Xb;      // K-tc operand (null: skip)
+    float *xn2;
+    float2 *xen;
+    const uint32_t *tcinv;  // position -> K-tc slot (null: identity)
+    uint32_t *amax;
+};
+
+constexpr int FIN_WARPS = 8;
+
+template <int W>
+__global__ void __launch_bounds__(FIN_WARPS * 32) finalize_rows_kernel(FinalizeArgs a)
+{
+    extern __shared__ float fin_sm[];
+    const int n = a.n;
+    const int ws = W > 0 ? W : n / WORD_SEGMENTS;  // points per word segment
+    const int padn = n + WORD_SEGMENTS;
+    float *thr = fin_sm;                                       // [ALPHABET]
+    int *ilay = reinterpret_cast<int *>(fin_sm + ALPHABET);    // physical -> logical
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *buf = fin_sm + ALPHABET + n + warp * padn;
+    for (int i = threadIdx.x; i < ALPHABET; i += blockDim.x)
+        thr[i] = i < ALPHABET - 1 ? __double2float_ru(a.bp[i]) : __int_as_float(0x7f800000);
+    for (int e = threadIdx.x; e < n; e += blockDim.x) ilay[layout_pos(n, e)] = e;
+    __syncthreads();
+    auto lpos = [&](int e) { return e + e / ws; };  // padded logical position
+    float amx = 0.f;
+    const int n4 = n / 4;
+    for (int64_t r = blockIdx.x * (int64_t)FIN_WARPS + warp; r < a.N; r += (int64_t)gridDim.x * FIN_WARPS) {
+        const uint32_t src = a.perm ? a.perm[r] : (uint32_t)r;
+        const float4 *s4 = reinterpret_cast<const float4 *>(a.X + (int64_t)src * n);
+        const int64_t h = a.tcinv ? (int64_t)a.tcinv[r] : r;
+        double acc = 0.0, hh = 0.0, ll = 0.0;
+        for (int c = lane; c < n4; c += 32) {
+            const float4 f = __ldcs(s4 + c);
+            const float v[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                buf[lpos(4 * c + k)] = v[k];
+                amx = fmaxf(amx, fabsf(v[k]));
+            }
+            if (a.Xb) {
+                __nv_bfloat16 b[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    b[k] = __float2bfloat16_rn(v[k]);
+                    const double vb = (double)__bfloat162float(b[k]), dv = (double)v[k] - vb;  // exact
+                    acc += (double)v[k] * (double)v[k];
+                    hh += vb * vb;
+                    ll += dv * dv;
+                }
+                uint2 pk;
+                pk.x = (uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16);
+                pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
+                reinterpret_cast<uint2 *>(a.Xb + h * n)[c] = pk;
+            }
+        }
+        __syncwarp();
+        float4 *d4 = reinterpret_cast<float4 *>(a.Xo + r * n);
+        for (int c = lane; c < n4; c += 32) {
+            float4 o;
+            o.x = buf[lpos(ilay[4 * c + 0])];
+            o.y = buf[lpos(ilay[4 * c + 1])];
+            o.z = buf[lpos(ilay[4 * c + 2])];
+            o.w = buf[lpos(ilay[4 * c + 3])];
+            __stcs(d4 + c, o);
+        }
+        if (a.words && lane < WORD_SEGMENTS) {
+            const float *x = buf + lane * (ws + 1);
+            float sum;
+            if constexpr (W > 0)
+                sum = pw_f32_seq<W>([&](int i) { return x[i]; });
+            else
+                sum = pw_f32_rt(x, ws);
+            const float p = __fdiv_rn(sum, (float)ws);
+            int lo = 0;
+#pragma unroll
+            for (int step = ALPHABET / 2; step; step >>= 1)
+                if (thr[lo + step - 1] <= p) lo += step;
+            a.words[r * WORD_SEGMENTS + lane] = (uint8_t)lo;
+        }
+        if (a.inv && lane == 0) a.inv[src] = (uint32_t)r;
+        if (a.Xb) {
+            for (int off = 16; off; off >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                hh += __shfl_xor_sync(0xffffffffu, hh, off);
+                ll += __shfl_xor_sync(0xffffffffu, ll, off);
+            }
+            if (lane == 0) {
+                a.xn2[h] = __double2float_rn(acc);
+                const double m = 1.0 + 0x1p-40;  // covers the float64 sums and square roots
+                const double H = sqrt(hh * m) * m, L = sqrt(ll * m) * m;
+                a.xen[h] = make_float2(__double2float_ru((L + 0x1p-14 * H) * m), __double2float_ru((H + L) * m));
+            }
+        }
+        __syncwarp();  // buf is reused by the next row
+    }
+    for (int off = 16; off; off >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, off));
+    __shared__ float wmax[FIN_WARPS];
+    if (lane == 0) wmax[warp] = amx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < FIN_WARPS; w++) amx = fmaxf(amx, wmax[w]);
+        atomicMax(a.amax, __float_as_uint(amx));
+    }
+}
+
+static int launch_finalize_rows(const FinalizeArgs &a, cudaStream_t s)
+{
+    if (a.N == 0) return OK;
+    SSB_REQUIRE(a.n % 8 == 0 && a.n % WORD_SEGMENTS == 0, "layout needs n % 16 == 0");
+    const size_t smem = sizeof(float) * ((size_t)ALPHABET + a.n + (size_t)FIN_WARPS * (a.n + WORD_SEGMENTS));
+    const unsigned grid = (unsigned)std::min<int64_t>((a.N + FIN_WARPS - 1) / FIN_WARPS, (int64_t)num_sms() * 8);
+    ProfScope ps("build_finalize", s,
+                 (double)a.N * a.n * 4 * 2 + (a.Xb ? (double)a.N * (a.n * 2 + 12) : 0.0) +
+                     (a.words ? (double)a.N * WORD_SEGMENTS : 0.0));
+#define FIN_CASE(WW)                                                                                       \
+    do {                                                                                                   \
+        SSB_CUDA(cudaFuncSetAttribute(finalize_rows_kernel<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                                         \
+        finalize_rows_kernel<WW><<<grid, FIN_WARPS * 32, smem, s>>>(a);                                    \
+    } while (0)
+    switch (a.n / WORD_SEGMENTS) {
+    case 4: FIN_CASE(4); break;
+    case 6: FIN_CASE(6); break;
+    case 8: FIN_CASE(8); break;
+    case 16: FIN_CASE(16); break;
+    case 32: FIN_CASE(32); break;
+    default: FIN_CASE(0); break;
+    }
+#undef FIN_CASE
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+__global__ void inv_perm_kernel(const uint32_t *__restrict__ p, int64_t N, uint32_t *__restrict__ out)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) out[p[i]] = (uint32_t)i;
+}
+
 __global__ void inv_from_orig_kernel(const uint32_t *__restrict__ orig, int64_t N, uint32_t *__restrict__ inv)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < N) inv[orig[i]] = (uint32_t)i;
-}
-
-__global__ void absmax_kernel(const float *__restrict__ X, int64_t count, uint32_t *__restrict__ out)
-{
-    float m = 0.f;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x)
-        m = fmaxf(m, fabsf(X[i]));
-    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
 
 __global__ void fill_u32_kernel(uint32_t *p, int64_t count, uint32_t v)
@@ -588,6 +956,31 @@ static int fill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
 {
     if (count <= 0) return OK;
     fill_u32_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p, count, v);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+static int launch_eval(const NodeDesc *nodes, const EvTask *tasks, int64_t ntasks, int maxm, const float *stats,
+                       const double *thr, const int32_t *valid, uint32_t *acc, uint32_t *nleft, cudaStream_t s)
+{
+    if (ntasks == 0) return OK;
+    SSB_REQUIRE(ntasks < (1ll << 31), "too many K-eval tasks in one level");
+    const size_t smem = (size_t)6 * maxm * (EV_T + 4) * 4;
+    const int slots = (2 * (maxm + 1) + 31) / 32;
+#define EV_CASE(SS)                                                                                          \
+    do {                                                                                                     \
+        SSB_CUDA(cudaFuncSetAttribute(build_eval_warp_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                                           \
+        build_eval_warp_kernel<SS><<<(unsigned)ntasks, EV_WARPS * 32, smem, s>>>(nodes, tasks, stats, thr, valid, \
+                                                                                 acc, nleft);                \
+    } while (0)
+    if (slots <= 1)
+        EV_CASE(1);
+    else if (slots == 2)
+        EV_CASE(2);
+    else
+        EV_CASE(3);
+#undef EV_CASE
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -625,7 +1018,10 @@ __global__ void hash_keys_kernel(uint32_t *__restrict__ keys, uint32_t *__restri
     pos[i] = (uint32_t)i;
 }
 
-static int make_tc_operands(Index &ix, cudaStream_t s)
+// K-tc operands: the row order (a hashed permutation of the leaf order) and
+// the buffers; the rows themselves are written by the fused gather
+// (finalize_rows_kernel).  Skipped when n is unsupported.
+static int alloc_tc_operands(Index &ix, DevBuf &tcinv, cudaStream_t s)
 {
     if (ix.n % 8 != 0 || ix.n > 256) return OK;
     SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
@@ -652,14 +1048,44 @@ static int make_tc_operands(Index &ix, cudaStream_t s)
         SSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
                                                  pos.as<uint32_t>(), ix.tcperm, (int)ix.N, 0, 32, s));
         note_launch(1);
+        SSB_CUDA(tcinv.alloc(4 * (size_t)ix.N, s));
+        inv_perm_kernel<<<(unsigned)((ix.N + 255) / 256), 256, 0, s>>>(ix.tcperm, ix.N, tcinv.as<uint32_t>());
+        SSB_CHECK_LAUNCH();
     }
-    int rc = launch_to_bf16_norms(ix.X, reinterpret_cast<const int32_t *>(ix.tcperm), ix.N, ix.n, true, ix.Xb,
-                                  ix.xn2, ix.xen, false, s);
+    return OK;
+}
+
+static int finish_tc_operands(Index &ix, cudaStream_t s)
+{
+    if (!ix.Xb) return OK;
+    int rc = launch_tc_row_consts(ix.xn2, ix.xen, ix.N, ix.rowc, s);
     if (rc) return rc;
     SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 4) * 16));
-    rc = launch_tc_row_consts(ix.xn2, ix.xen, ix.N, ix.rowc, s);
-    if (rc) return rc;
     return launch_tc_tile_consts(ix.rowc, ix.N, ix.tilec, s);
+}
+
+// the fused row pass (+ K-tc operands) of a built or loaded index
+static int finalize_rows(Index &ix, const float *src, const uint32_t *perm, bool want_words, uint32_t *amax,
+                         cudaStream_t s)
+{
+    DevBuf tcinv;
+    RC(alloc_tc_operands(ix, tcinv, s));
+    FinalizeArgs fa;
+    fa.X = src;
+    fa.perm = perm;
+    fa.N = ix.N;
+    fa.n = ix.n;
+    fa.Xo = ix.X;
+    fa.words = want_words ? ix.words : nullptr;
+    fa.bp = ix.bp;
+    fa.inv = perm ? ix.inv : nullptr;
+    fa.Xb = reinterpret_cast<__nv_bfloat16 *>(ix.Xb);
+    fa.xn2 = ix.xn2;
+    fa.xen = ix.xen;
+    fa.tcinv = ix.tcperm ? tcinv.as<uint32_t>() : nullptr;
+    fa.amax = amax;
+    RC(launch_finalize_rows(fa, s));
+    return finish_tc_operands(ix, s);
 }
 
 int build_index(const float *X, int64_t N, int n, const double *bp_dev, const BuildCfg &cfg,
@@ -703,8 +1129,6 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     SSB_CUDA(cudaMemsetAsync(nonfinite.p, 0, 4, s));
     SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));
     iota_u32_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(perm_a.as<uint32_t>(), N);
-    SSB_CHECK_LAUNCH();
-    absmax_kernel<<<4 * num_sms(), 256, 0, s>>>(X, N * n, amax.as<uint32_t>());
     SSB_CHECK_LAUNCH();
     uint32_t *perm = perm_a.as<uint32_t>(), *perm2 = perm_b.as<uint32_t>();
 
@@ -752,7 +1176,8 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         SSB_REQUIRE(nchunks < (1ll << 31), "too many member chunks in one level");
         // long ranges for the reductions: all members, the split sets (min/max),
         // the split sets in K-eval granules
-        std::vector<Range> r_all, r_ss, r_ev;
+        std::vector<Range> r_all, r_ss;
+        std::vector<EvTask> ev_tasks;
         int maxm = 1;
         for (int f = 0; f < F; f++) {
             maxm = std::max(maxm, nd[f].m);
@@ -760,17 +1185,22 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 r_all.push_back({(uint32_t)f, m0, std::min<uint32_t>(MM_RANGE, nd[f].count - m0)});
             for (uint32_t m0 = 0; m0 < nd[f].ecount; m0 += MM_RANGE)
                 r_ss.push_back({(uint32_t)f, m0, std::min<uint32_t>(MM_RANGE, nd[f].ecount - m0)});
-            for (uint32_t m0 = 0; m0 < nd[f].ecount; m0 += EV_RANGE)
-                r_ev.push_back({(uint32_t)f, m0, std::min<uint32_t>(EV_RANGE, nd[f].ecount - m0)});
+            for (uint32_t m0 = 0; m0 < nd[f].ecount; m0 += EV2_RANGE)
+                for (int cg = 0; cg * EV_WARPS < 6 * nd[f].m; cg++)
+                    ev_tasks.push_back({(uint32_t)f, m0, std::min<uint32_t>(EV2_RANGE, nd[f].ecount - m0),
+                                        (uint32_t)cg});
         }
         std::vector<Range> r_cat(r_all);
         r_cat.insert(r_cat.end(), r_ss.begin(), r_ss.end());
-        r_cat.insert(r_cat.end(), r_ev.begin(), r_ev.end());
-        DevBuf d_ranges;
+        DevBuf d_ranges, d_evt;
         SSB_CUDA(d_ranges.alloc(sizeof(Range) * r_cat.size(), s));
         SSB_CUDA(cudaMemcpyAsync(d_ranges.p, r_cat.data(), sizeof(Range) * r_cat.size(), cudaMemcpyHostToDevice, s));
-        const Range *d_r_all = d_ranges.as<Range>(), *d_r_ss = d_r_all + r_all.size(),
-                    *d_r_ev = d_r_ss + r_ss.size();
+        const Range *d_r_all = d_ranges.as<Range>(), *d_r_ss = d_r_all + r_all.size();
+        if (!ev_tasks.empty()) {
+            SSB_CUDA(d_evt.alloc(sizeof(EvTask) * ev_tasks.size(), s));
+            SSB_CUDA(cudaMemcpyAsync(d_evt.p, ev_tasks.data(), sizeof(EvTask) * ev_tasks.size(),
+                                     cudaMemcpyHostToDevice, s));
+        }
         DevBuf d_nodes, d_chunks, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
         GrowBuf &d_stats = lv_stats;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
@@ -795,14 +1225,13 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
 
         {
             ProfScope ps("build_stats", s, (double)aoff * n * 4 + (double)stat_off * 4);
-            build_stats_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(X, n, perm, d_nodes.as<NodeDesc>(),
-                                                                   d_chunks.as<Chunk>(), d_stats.as<float>(),
-                                                                   nonfinite.as<int>());
+            RC(launch_build_stats(X, n, perm, d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(), nchunks,
+                                  d_stats.as<float>(), nonfinite.as<int>(), s));
         }
-        SSB_CHECK_LAUNCH();
         // exact envelopes over every member
-        build_minmax_range_kernel<<<dim3((unsigned)r_all.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
-            d_nodes.as<NodeDesc>(), d_r_all, d_stats.as<float>(), d_cmin.as<uint32_t>(), d_cmax.as<uint32_t>());
+        // (base columns only: a node's envelope is over its own segmentation)
+        build_minmax_range_kernel<<<dim3((unsigned)r_all.size(), (unsigned)(2 * maxm)), RTHREADS, 0, s>>>(
+            d_nodes.as<NodeDesc>(), d_r_all, d_stats.as<float>(), d_cmin.as<uint32_t>(), d_cmax.as<uint32_t>(), 2);
         SSB_CHECK_LAUNCH();
 
         std::vector<NodeResult> res(F);
@@ -823,7 +1252,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
             SSB_CHECK_LAUNCH();
             build_minmax_range_kernel<<<dim3((unsigned)r_ss.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
-                d_nodes.as<NodeDesc>(), d_r_ss, d_stats.as<float>(), d_emin.as<uint32_t>(), d_emax.as<uint32_t>());
+                d_nodes.as<NodeDesc>(), d_r_ss, d_stats.as<float>(), d_emin.as<uint32_t>(), d_emax.as<uint32_t>(), 6);
             SSB_CHECK_LAUNCH();
             build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_emin.as<uint32_t>(),
                                               d_emax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
@@ -832,9 +1261,9 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 double ev = 0.0;
                 for (int f = 0; f < F; f++) ev += (double)nd[f].ecount * 6 * nd[f].m * 4;
                 ProfScope ps("build_eval", s, ev);
-                build_eval_range_kernel<<<dim3((unsigned)r_ev.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
-                    d_nodes.as<NodeDesc>(), d_r_ev, d_stats.as<float>(), d_thr.as<double>(), d_valid.as<int32_t>(),
-                    d_acc.as<uint32_t>(), d_nleft.as<uint32_t>());
+                RC(launch_eval(d_nodes.as<NodeDesc>(), d_evt.as<EvTask>(), (int64_t)ev_tasks.size(), maxm,
+                               d_stats.as<float>(), d_thr.as<double>(), d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
+                               d_nleft.as<uint32_t>(), s));
             }
             SSB_CHECK_LAUNCH();
             build_gain_kernel<<<F, 32, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_thr.as<double>(),
@@ -1044,17 +1473,9 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     SSB_CUDA(cudaMalloc(&ix->bp, 8 * (ALPHABET - 1)));
     SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
     SSB_CUDA(cudaMemcpyAsync(ix->orig, perm, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
-    {
-        ProfScope ps("build_gather", s, 2.0 * N * n * 4);
-        RC(launch_layout_rows(X, perm, N, n, ix->X, true, s));
-    }
-    inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
-    SSB_CHECK_LAUNCH();
-    lap("allocs+gather");
-    RC(launch_words(X, N, n, ix->bp, ix->words, nullptr, s, perm));
-    lap("words");
-    RC(make_tc_operands(*ix, s));
-    lap("tc operands");
+    lap("allocs");
+    RC(finalize_rows(*ix, X, perm, true, amax.as<uint32_t>(), s));
+    lap("gather+words+tc operands");
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
@@ -1136,12 +1557,14 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
     SSB_CUDA(cudaMalloc(&ix->inv, (size_t)N * 4));
     SSB_CUDA(cudaMalloc(&ix->bp, 8 * (ALPHABET - 1)));
     SSB_CUDA(cudaMemcpyAsync(ix->bp, bp_dev, 8 * (ALPHABET - 1), cudaMemcpyDeviceToDevice, s));
+    DevBuf amax;
+    SSB_CUDA(amax.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));
     {
         DevBuf tmp;
         SSB_CUDA(tmp.alloc((size_t)N * n * 4, s));
         SSB_CUDA(cudaMemcpyAsync(tmp.p, rows, (size_t)N * n * 4, cudaMemcpyHostToDevice, s));
-        RC(launch_layout_rows(tmp.as<float>(), nullptr, N, n, ix->X, true, s));
-        if (!words) RC(launch_words(tmp.as<float>(), N, n, ix->bp, ix->words, nullptr, s));
+        RC(finalize_rows(*ix, tmp.as<float>(), nullptr, words == nullptr, amax.as<uint32_t>(), s));
         SSB_CUDA(cudaStreamSynchronize(s));
     }
     if (orig) {
@@ -1153,12 +1576,6 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
     if (words) SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
-    RC(make_tc_operands(*ix, s));
-    DevBuf amax;
-    SSB_CUDA(amax.alloc(4, s));
-    SSB_CUDA(cudaMemsetAsync(amax.p, 0, 4, s));
-    absmax_kernel<<<4 * num_sms(), 256, 0, s>>>(ix->X, N * n, amax.as<uint32_t>());
-    SSB_CHECK_LAUNCH();
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));

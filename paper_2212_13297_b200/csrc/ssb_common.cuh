@@ -274,4 +274,19 @@ __device__ __forceinline__ void fence_barrier_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// 16-byte global -> shared asynchronous copy (L2 only), and the stage-row XOR
+// slot that makes per-thread float4 reads of a 16/32-column staged row conflict-free
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int W>
+__device__ __forceinline__ int sa_slot(int c, int r)
+{
+    static_assert(W == 16 || W == 32, "stage width");
+    return W == 32 ? c ^ (r & 7) : c ^ ((r >> 1) & 3);  // 8 distinct 16-byte bank groups per 8 rows
+}
+
 }  // namespace ssb

@@ -231,19 +231,6 @@ __global__ void __launch_bounds__(SS_ROWS)
 // boundary point inside runs its four elements without per-element checks.
 constexpr int SA_ROWS = 128, SA_STG = 3;
 
-__device__ __forceinline__ void cp_async16(void *dst, const void *src)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-
-template <int W>
-__device__ __forceinline__ int sa_slot(int c, int r)
-{
-    static_assert(W == 16 || W == 32, "stage width");
-    return W == 32 ? c ^ (r & 7) : c ^ ((r >> 1) & 3);  // 8 distinct 16-byte bank groups per 8 rows
-}
-
 template <bool CONTIG, int W>
 __global__ void __launch_bounds__(SA_ROWS)
     segment_stats_async_kernel(const float *__restrict__ X, int64_t N, int n, const int32_t *__restrict__ pts_g,

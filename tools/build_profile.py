@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--tau", type=int, default=10_000)
     ap.add_argument("--no-warm", action="store_true", help="skip the small warm-up build (profilers)")
+    ap.add_argument("--repeat", type=int, default=1, help="timed builds (the profile covers the last)")
     a = ap.parse_args()
     import torch
 
@@ -30,16 +31,20 @@ def main():
         w = min(a.rows, 200_000)
         ssb.build_index_array(X[:w], ssb.IndexSettings(series_length=a.n, dataset_size=w, leaf_threshold=a.tau))
     torch.cuda.synchronize()
-    _lib.prof_reset()
-    _lib.prof_enable(True)
-    t0 = time.perf_counter()
-    idx = ssb.build_index_array(X, s)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    walls = []
+    for _ in range(a.repeat):
+        idx = None
+        _lib.prof_reset()
+        _lib.prof_enable(True)
+        t0 = time.perf_counter()
+        idx = ssb.build_index_array(X, s)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        walls.append(round(dt, 4))
     _lib.prof_enable(False)
     prof = _lib.prof_read()
     print(json.dumps({"rows": a.rows, "s": round(dt, 3), "series_per_s": round(a.rows / dt),
-                      "levels": idx.info.levels, "leaves": idx.info.num_leaves,
+                      "levels": idx.info.levels, "leaves": idx.info.num_leaves, "walls": walls,
                       "kernels": {k: [round(v[0], 2), v[1], round(v[2] / 1e9, 2)] for k, v in prof.items()}}))
 
 
