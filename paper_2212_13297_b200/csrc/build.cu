@@ -479,15 +479,19 @@ __global__ void __launch_bounds__(RTHREADS)
 }
 
 // K-eval, warp per candidate: grid = (split-set range, candidate group).  The
-// CTA stages 64-member tiles of ALL the node's stat columns (ordered keys,
-// column-major, padded) in shared memory; warp w owns candidate
-// c = group * EV_WARPS + w, computes its sides with two ballots per tile, and
-// lane l owns the result tasks q = l, l + 32, ... (q = 2j + attr): per member a
-// warp-uniform side bit picks the L or R accumulators, so each (member,
-// candidate, task) costs one shared load and two integer min/max.  Partial
-// results go to the node's accumulators once per CTA.
-constexpr int EV_WARPS = 16;
+// CTA streams 64-member tiles of ALL the node's stat columns (column-major,
+// padded) into shared memory through a 2-stage cp.async ring; warp w owns
+// candidate c = group * EV_WARPS + w, computes its sides with two ballots per
+// tile, and lane l owns the result tasks q = l, l + 32, ... (q = 2j + attr): per
+// member a warp-uniform side bit (predicates from the ballot mask) picks the L
+// or R accumulators, so each (member, candidate, task) costs one quarter of a
+// 16-byte shared load and two float min/max.  The float min/max may pick either
+// zero for {-0, +0}; the accumulators only feed the QoS differences (mx - mn)^2,
+// which are identical for both.  Partial results go to the node's (ordered-key)
+// accumulators once per CTA.
+constexpr int EV_WARPS = 12;             // 6m candidates = m/2 groups for even m
 constexpr int EV_T = 64;                 // members per tile
+constexpr int EV_TS = EV_T + 4;          // padded column stride (16-byte aligned)
 constexpr uint32_t EV2_RANGE = 2048;     // members per CTA
 
 struct EvTask {
@@ -497,6 +501,12 @@ struct EvTask {
     uint32_t cg;  // candidate group
 };
 
+__device__ __forceinline__ void cp_async4(void *dst, const void *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+
 template <int S>  // result-task slots per lane: 2 * (m + 1) <= 32 * S
 __global__ void __launch_bounds__(EV_WARPS * 32)
     build_eval_warp_kernel(const NodeDesc *__restrict__ nodes, const EvTask *__restrict__ tasks,
@@ -504,8 +514,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
                            const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
                            uint32_t *__restrict__ nleft)
 {
-    extern __shared__ uint4 ev_tile4[];  // [6m][EV_T + 4] u32
-    uint32_t *ev_tile = reinterpret_cast<uint32_t *>(ev_tile4);
+    extern __shared__ float4 ev_tile4[];  // [2][6m][EV_TS] floats
+    float *ev_tile = reinterpret_cast<float *>(ev_tile4);
     __shared__ NodeDesc nd;
     __shared__ EvTask tk;
     if (threadIdx.x == 0) {
@@ -515,10 +525,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = nd.m, ncol = 6 * m;
+    const int stage_floats = ncol * EV_TS;
     const int c = (int)tk.cg * EV_WARPS + warp;
     const bool active = c < ncol && valid[nd.col_off + c];
-    constexpr int TS = EV_T + 4;  // 16-byte aligned columns
-    // this lane's result tasks: column offsets in the tile (or -1)
+    // this lane's result tasks: column offsets in a tile stage (or -1)
     int coff[S];
     const int lay = active ? (c % 6) % 3 : 0;
     const int mm = m + (lay ? 1 : 0);
@@ -529,71 +539,85 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
         if (active && q < 2 * mm) {
             int cmean, csd, w;
             result_col(nd, c, q >> 1, cmean, csd, w);
-            coff[sl] = ((q & 1) ? csd : cmean) * TS;
+            coff[sl] = ((q & 1) ? csd : cmean) * EV_TS;
         }
     }
-    const int rcol = active ? route_col(m, c) * TS : 0;
+    const int rcol = active ? route_col(m, c) * EV_TS : 0;
     const double th = active ? thr[nd.col_off + c] : 0.0;
-    uint32_t lmin[S], lmax[S], rmin[S], rmax[S];
+    const float inf = __int_as_float(0x7f800000);
+    float lmin[S], lmax[S], rmin[S], rmax[S];
 #pragma unroll
     for (int sl = 0; sl < S; sl++) {
-        lmin[sl] = rmin[sl] = 0xffffffffu;
-        lmax[sl] = rmax[sl] = 0u;
+        lmin[sl] = rmin[sl] = inf;
+        lmax[sl] = rmax[sl] = -inf;
     }
     uint32_t nl = 0;
     const int64_t cnt = nd.count;
     const float *st = stats + nd.stat_off + tk.m0;
-    for (uint32_t t0 = 0; t0 < tk.cnt; t0 += EV_T) {
-        const int tn = (int)min((uint32_t)EV_T, tk.cnt - t0);
-        __syncthreads();  // previous tile consumed
-        for (int idx = threadIdx.x; idx < ncol * EV_T; idx += blockDim.x) {
-            const int col = idx / EV_T, i = idx % EV_T;
-            if (i < tn) ev_tile[col * TS + i] = okey(__ldg(st + (int64_t)col * cnt + t0 + i));
-        }
-        __syncthreads();
-        if (!active) continue;
-        uint32_t mk[EV_T / 32];
-#pragma unroll
-        for (int h = 0; h < EV_T / 32; h++) {
-            const int i = lane + 32 * h;
-            const bool left = i < tn && (double)okey_inv(ev_tile[rcol + i]) < th;
-            mk[h] = __ballot_sync(0xffffffffu, left);
-            nl += __popc(mk[h]);
-        }
-        auto upd = [&](int sl, uint32_t k, bool bit) {
-            if (bit) {
-                lmin[sl] = min(lmin[sl], k);
-                lmax[sl] = max(lmax[sl], k);
-            } else {
-                rmin[sl] = min(rmin[sl], k);
-                rmax[sl] = max(rmax[sl], k);
+    const int ntiles = (int)((tk.cnt + EV_T - 1) / EV_T);
+    auto load = [&](int tile) {
+        if (tile < ntiles) {
+            const int t0 = tile * EV_T, tn = (int)min((uint32_t)EV_T, tk.cnt - (uint32_t)t0);
+            float *dst = ev_tile + (tile & 1) * stage_floats;
+            for (int idx = threadIdx.x; idx < ncol * EV_T; idx += blockDim.x) {
+                const int col = idx / EV_T, i = idx % EV_T;
+                if (i < tn) cp_async4(dst + col * EV_TS + i, st + (int64_t)col * cnt + t0 + i);
             }
-        };
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load(0);
+    for (int tile = 0; tile < ntiles; tile++) {
+        load(tile + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // tile landed for every thread
+        if (active) {
+            const float *tb = ev_tile + (tile & 1) * stage_floats;
+            const int tn = (int)min((uint32_t)EV_T, tk.cnt - (uint32_t)(tile * EV_T));
+            uint32_t mk[EV_T / 32];
 #pragma unroll
-        for (int h = 0; h < EV_T / 32; h++) {
-            const int i0 = 32 * h;
-            const uint32_t b = mk[h];
-            if (tn - i0 >= 32) {  // full 32 members: unrolled, 16-byte loads, predicated updates
-#pragma unroll
-                for (int sl = 0; sl < S; sl++) {
-                    if (coff[sl] < 0) continue;
-                    const uint4 *src = reinterpret_cast<const uint4 *>(ev_tile + coff[sl] + i0);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; i4++) {
-                        const uint4 k = src[i4];
-                        upd(sl, k.x, (b >> (4 * i4 + 0)) & 1u);
-                        upd(sl, k.y, (b >> (4 * i4 + 1)) & 1u);
-                        upd(sl, k.z, (b >> (4 * i4 + 2)) & 1u);
-                        upd(sl, k.w, (b >> (4 * i4 + 3)) & 1u);
-                    }
+            for (int h = 0; h < EV_T / 32; h++) {
+                const int i = lane + 32 * h;
+                const bool left = i < tn && (double)tb[rcol + i] < th;
+                mk[h] = __ballot_sync(0xffffffffu, left);
+                nl += __popc(mk[h]);
+            }
+            auto upd = [&](int sl, float k, bool bit) {
+                if (bit) {
+                    lmin[sl] = fminf(lmin[sl], k);
+                    lmax[sl] = fmaxf(lmax[sl], k);
+                } else {
+                    rmin[sl] = fminf(rmin[sl], k);
+                    rmax[sl] = fmaxf(rmax[sl], k);
                 }
-            } else {
-                for (int i = 0; i < tn - i0; i++)
+            };
 #pragma unroll
-                    for (int sl = 0; sl < S; sl++)
-                        if (coff[sl] >= 0) upd(sl, ev_tile[coff[sl] + i0 + i], (b >> i) & 1u);
+            for (int h = 0; h < EV_T / 32; h++) {
+                const int i0 = 32 * h;
+                const uint32_t b = mk[h];
+                if (tn - i0 >= 32) {  // full 32 members: unrolled, 16-byte loads, predicated updates
+#pragma unroll
+                    for (int sl = 0; sl < S; sl++) {
+                        if (coff[sl] < 0) continue;
+                        const float4 *src = reinterpret_cast<const float4 *>(tb + coff[sl] + i0);
+#pragma unroll
+                        for (int i4 = 0; i4 < 8; i4++) {
+                            const float4 k = src[i4];
+                            upd(sl, k.x, (b >> (4 * i4 + 0)) & 1u);
+                            upd(sl, k.y, (b >> (4 * i4 + 1)) & 1u);
+                            upd(sl, k.z, (b >> (4 * i4 + 2)) & 1u);
+                            upd(sl, k.w, (b >> (4 * i4 + 3)) & 1u);
+                        }
+                    }
+                } else {
+                    for (int i = 0; i < tn - i0; i++)
+#pragma unroll
+                        for (int sl = 0; sl < S; sl++)
+                            if (coff[sl] >= 0) upd(sl, tb[coff[sl] + i0 + i], (b >> i) & 1u);
+                }
             }
         }
+        __syncthreads();  // stage (tile & 1) consumed before it is refilled
     }
     if (!active) return;
     uint32_t *nacc = acc + nd.acc_off;
@@ -601,13 +625,13 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
     for (int sl = 0; sl < S; sl++) {
         if (coff[sl] < 0) continue;
         const int q = lane + 32 * sl, j = q >> 1, attr = q & 1;
-        if (lmin[sl] != 0xffffffffu) {
-            atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], lmin[sl]);
-            atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], lmax[sl]);
+        if (lmin[sl] != inf) {
+            atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], okey(lmin[sl]));
+            atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], okey(lmax[sl]));
         }
-        if (rmin[sl] != 0xffffffffu) {
-            atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], rmin[sl]);
-            atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], rmax[sl]);
+        if (rmin[sl] != inf) {
+            atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], okey(rmin[sl]));
+            atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], okey(rmax[sl]));
         }
     }
     if (lane == 0 && nl) atomicAdd(&nleft[nd.col_off + c], nl);
@@ -756,20 +780,6 @@ __global__ void node_left_kernel(const NodeDesc *__restrict__ nodes, int nnodes,
     if (f < nnodes) out[f] = scan[nodes[f].aoff + nodes[f].count] - scan[nodes[f].aoff];
 }
 
-// final gather into leaf order
-__global__ void gather_rows_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
-                                   int64_t N, float *__restrict__ Xo, uint32_t *__restrict__ inv)
-{
-    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
-    if (row >= N) return;
-    const int lane = threadIdx.x & 31;
-    const uint32_t src = perm[row];
-    const float4 *s = reinterpret_cast<const float4 *>(X + (int64_t)src * n);
-    float4 *d = reinterpret_cast<float4 *>(Xo + row * n);
-    for (int i = lane; i < n / 4; i += 32) d[i] = __ldg(s + i);
-    if (lane == 0) inv[src] = (uint32_t)row;
-}
-
 // K-gather, fused (the index's one pass over its rows, in leaf order): reads
 // each source row once (logical order, coalesced float4) and writes
 //   * the lane-transposed float32 row (layout.cuh), leaf order;
@@ -798,10 +808,15 @@ struct FinalizeArgs {
 constexpr int FIN_WARPS = 8;
 
 template <int W>
-__global__ void __launch_bounds__(FIN_WARPS * 32) finalize_rows_kernel(FinalizeArgs a)
+__global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(FinalizeArgs a)
 {
+    // W > 0: n = 16 W is a compile-time constant; each lane owns float4 chunks
+    // c = lane + 32 j of every row (their layout sources live in registers) and
+    // the next row's chunks are loaded while the current one is processed
+    constexpr int NN = 16 * W;
+    constexpr int NC = W > 0 ? (NN / 4 + 31) / 32 : 1;
     extern __shared__ float fin_sm[];
-    const int n = a.n;
+    const int n = W > 0 ? NN : a.n;
     const int ws = W > 0 ? W : n / WORD_SEGMENTS;  // points per word segment
     const int padn = n + WORD_SEGMENTS;
     float *thr = fin_sm;                                       // [ALPHABET]
@@ -813,15 +828,36 @@ __global__ void __launch_bounds__(FIN_WARPS * 32) finalize_rows_kernel(FinalizeA
     for (int e = threadIdx.x; e < n; e += blockDim.x) ilay[layout_pos(n, e)] = e;
     __syncthreads();
     auto lpos = [&](int e) { return e + e / ws; };  // padded logical position
-    float amx = 0.f;
     const int n4 = n / 4;
-    for (int64_t r = blockIdx.x * (int64_t)FIN_WARPS + warp; r < a.N; r += (int64_t)gridDim.x * FIN_WARPS) {
+    int src_pos[NC][4];  // padded logical positions of this lane's physical chunks
+#pragma unroll
+    for (int j = 0; j < NC; j++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int c = lane + 32 * j;
+            src_pos[j][k] = (W > 0 && c < n4) ? lpos(ilay[4 * c + k]) : 0;
+        }
+    float amx = 0.f;
+    const int64_t stride = (int64_t)gridDim.x * FIN_WARPS;
+    int64_t r = blockIdx.x * (int64_t)FIN_WARPS + warp;
+    float4 nxt[NC];
+    auto fetch = [&](int64_t rr) {
+        if constexpr (W > 0) {
+            if (rr < a.N) {
+                const uint32_t sr = a.perm ? a.perm[rr] : (uint32_t)rr;
+                const float4 *s4 = reinterpret_cast<const float4 *>(a.X + (int64_t)sr * NN);
+#pragma unroll
+                for (int j = 0; j < NC; j++)
+                    if (lane + 32 * j < NN / 4) nxt[j] = __ldcs(s4 + lane + 32 * j);
+            }
+        }
+    };
+    fetch(r);
+    for (; r < a.N; r += stride) {
         const uint32_t src = a.perm ? a.perm[r] : (uint32_t)r;
-        const float4 *s4 = reinterpret_cast<const float4 *>(a.X + (int64_t)src * n);
         const int64_t h = a.tcinv ? (int64_t)a.tcinv[r] : r;
         double acc = 0.0, hh = 0.0, ll = 0.0;
-        for (int c = lane; c < n4; c += 32) {
-            const float4 f = __ldcs(s4 + c);
+        auto take = [&](int c, const float4 f) {
             const float v[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -843,16 +879,38 @@ __global__ void __launch_bounds__(FIN_WARPS * 32) finalize_rows_kernel(FinalizeA
                 pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
                 reinterpret_cast<uint2 *>(a.Xb + h * n)[c] = pk;
             }
+        };
+        if constexpr (W > 0) {
+            float4 cur[NC];
+#pragma unroll
+            for (int j = 0; j < NC; j++) cur[j] = nxt[j];
+            fetch(r + stride);
+#pragma unroll
+            for (int j = 0; j < NC; j++)
+                if (lane + 32 * j < NN / 4) take(lane + 32 * j, cur[j]);
+        } else {
+            const float4 *s4 = reinterpret_cast<const float4 *>(a.X + (int64_t)src * n);
+            for (int c = lane; c < n4; c += 32) take(c, __ldcs(s4 + c));
         }
         __syncwarp();
         float4 *d4 = reinterpret_cast<float4 *>(a.Xo + r * n);
-        for (int c = lane; c < n4; c += 32) {
-            float4 o;
-            o.x = buf[lpos(ilay[4 * c + 0])];
-            o.y = buf[lpos(ilay[4 * c + 1])];
-            o.z = buf[lpos(ilay[4 * c + 2])];
-            o.w = buf[lpos(ilay[4 * c + 3])];
-            __stcs(d4 + c, o);
+        if constexpr (W > 0) {
+#pragma unroll
+            for (int j = 0; j < NC; j++) {
+                const int c = lane + 32 * j;
+                if (c < NN / 4)
+                    __stcs(d4 + c, make_float4(buf[src_pos[j][0]], buf[src_pos[j][1]], buf[src_pos[j][2]],
+                                               buf[src_pos[j][3]]));
+            }
+        } else {
+            for (int c = lane; c < n4; c += 32) {
+                float4 o;
+                o.x = buf[lpos(ilay[4 * c + 0])];
+                o.y = buf[lpos(ilay[4 * c + 1])];
+                o.z = buf[lpos(ilay[4 * c + 2])];
+                o.w = buf[lpos(ilay[4 * c + 3])];
+                __stcs(d4 + c, o);
+            }
         }
         if (a.words && lane < WORD_SEGMENTS) {
             const float *x = buf + lane * (ws + 1);
@@ -965,7 +1023,7 @@ static int launch_eval(const NodeDesc *nodes, const EvTask *tasks, int64_t ntask
 {
     if (ntasks == 0) return OK;
     SSB_REQUIRE(ntasks < (1ll << 31), "too many K-eval tasks in one level");
-    const size_t smem = (size_t)6 * maxm * (EV_T + 4) * 4;
+    const size_t smem = (size_t)2 * 6 * maxm * EV_TS * 4;
     const int slots = (2 * (maxm + 1) + 31) / 32;
 #define EV_CASE(SS)                                                                                          \
     do {                                                                                                     \
@@ -1121,6 +1179,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     for (int i = 0; i < s0; i++) root.ep[i] = (int32_t)((int64_t)n * (i + 1) / s0);
     ix->nodes.push_back(root);
 
+    SSB_CUDA(cudaMalloc(&ix->X, (size_t)N * n * 4));  // also the levels' statistics scratch
     DevBuf perm_a, perm_b, nonfinite, amax;
     SSB_CUDA(perm_a.alloc((size_t)N * 4, s));
     SSB_CUDA(perm_b.alloc((size_t)N * 4, s));
@@ -1202,19 +1261,25 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                                      cudaMemcpyHostToDevice, s));
         }
         DevBuf d_nodes, d_chunks, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
-        GrowBuf &d_stats = lv_stats;
+        // the level's statistics live in the index's row array (allocated up front,
+        // written only by the final row pass) when they fit: no pool growth
+        const bool stats_in_x = (size_t)stat_off <= (size_t)N * n;
+        float *stats_p = ix->X;
         SSB_CUDA(d_nodes.alloc(sizeof(NodeDesc) * F, s));
         SSB_CUDA(d_chunks.alloc(sizeof(Chunk) * nchunks, s));
-        if (trace) {  // allocation cost, separately
-            cudaStreamSynchronize(s);
-            auto a0 = std::chrono::steady_clock::now();
-            SSB_CUDA(d_stats.ensure(sizeof(float) * (size_t)stat_off, s));
-            cudaStreamSynchronize(s);
-            fprintf(stderr, "[ssb build]   stats buffer %.2f GB (cap %.2f GB): %.3f ms\n", 4e-9 * stat_off,
-                    1e-9 * d_stats.cap,
-                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count());
+        if (!stats_in_x) {
+            if (trace) {  // allocation cost, separately
+                cudaStreamSynchronize(s);
+                auto a0 = std::chrono::steady_clock::now();
+                SSB_CUDA(lv_stats.ensure(sizeof(float) * (size_t)stat_off, s));
+                cudaStreamSynchronize(s);
+                fprintf(stderr, "[ssb build]   stats buffer %.2f GB (cap %.2f GB): %.3f ms\n", 4e-9 * stat_off,
+                        1e-9 * lv_stats.cap,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count());
+            }
+            SSB_CUDA(lv_stats.ensure(sizeof(float) * (size_t)stat_off, s));
+            stats_p = lv_stats.as<float>();
         }
-        SSB_CUDA(d_stats.ensure(sizeof(float) * (size_t)stat_off, s));
         SSB_CUDA(d_cmin.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(d_cmax.alloc(4 * (size_t)col_off, s));
         SSB_CUDA(cudaMemcpyAsync(d_nodes.p, nd.data(), sizeof(NodeDesc) * F, cudaMemcpyHostToDevice, s));
@@ -1226,12 +1291,12 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         {
             ProfScope ps("build_stats", s, (double)aoff * n * 4 + (double)stat_off * 4);
             RC(launch_build_stats(X, n, perm, d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(), nchunks,
-                                  d_stats.as<float>(), nonfinite.as<int>(), s));
+                                  stats_p, nonfinite.as<int>(), s));
         }
         // exact envelopes over every member
         // (base columns only: a node's envelope is over its own segmentation)
         build_minmax_range_kernel<<<dim3((unsigned)r_all.size(), (unsigned)(2 * maxm)), RTHREADS, 0, s>>>(
-            d_nodes.as<NodeDesc>(), d_r_all, d_stats.as<float>(), d_cmin.as<uint32_t>(), d_cmax.as<uint32_t>(), 2);
+            d_nodes.as<NodeDesc>(), d_r_all, stats_p, d_cmin.as<uint32_t>(), d_cmax.as<uint32_t>(), 2);
         SSB_CHECK_LAUNCH();
 
         std::vector<NodeResult> res(F);
@@ -1252,7 +1317,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
             SSB_CHECK_LAUNCH();
             build_minmax_range_kernel<<<dim3((unsigned)r_ss.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
-                d_nodes.as<NodeDesc>(), d_r_ss, d_stats.as<float>(), d_emin.as<uint32_t>(), d_emax.as<uint32_t>(), 6);
+                d_nodes.as<NodeDesc>(), d_r_ss, stats_p, d_emin.as<uint32_t>(), d_emax.as<uint32_t>(), 6);
             SSB_CHECK_LAUNCH();
             build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_emin.as<uint32_t>(),
                                               d_emax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
@@ -1262,7 +1327,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 for (int f = 0; f < F; f++) ev += (double)nd[f].ecount * 6 * nd[f].m * 4;
                 ProfScope ps("build_eval", s, ev);
                 RC(launch_eval(d_nodes.as<NodeDesc>(), d_evt.as<EvTask>(), (int64_t)ev_tasks.size(), maxm,
-                               d_stats.as<float>(), d_thr.as<double>(), d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
+                               stats_p, d_thr.as<double>(), d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
                                d_nleft.as<uint32_t>(), s));
             }
             SSB_CHECK_LAUNCH();
@@ -1327,7 +1392,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             SSB_CUDA(cudaMemcpyAsync(d_fthr.p, fthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
             SSB_CUDA(cudaMemsetAsync(d_fnl.p, 0, 4 * F, s));
             build_fallback_count_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(
-                d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(), d_stats.as<float>(), d_fthr.as<double>(),
+                d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(), stats_p, d_fthr.as<double>(),
                 d_need.as<int32_t>(), d_fnl.as<uint32_t>());
             SSB_CHECK_LAUNCH();
             SSB_CUDA(cudaMemcpyAsync(fnl.data(), d_fnl.p, 4 * F, cudaMemcpyDeviceToHost, s));
@@ -1364,7 +1429,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
         SSB_CUDA(cudaMemcpyAsync(d_pthr.p, pthr.data(), 8 * F, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemsetAsync(d_flags.as<uint32_t>() + aoff, 0, 4, s));
         build_flags_kernel<<<(unsigned)nchunks, CHUNK, 0, s>>>(d_nodes.as<NodeDesc>(), d_chunks.as<Chunk>(),
-                                                               d_stats.as<float>(), d_pcol.as<int32_t>(),
+                                                               stats_p, d_pcol.as<int32_t>(),
                                                                d_pthr.as<double>(), d_flags.as<uint32_t>());
         SSB_CHECK_LAUNCH();
         size_t tmp_bytes = 0;
@@ -1466,7 +1531,6 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     ix->levels = level;
     RC(finalize_tree(*ix, s));
     lap("finalize_tree");
-    SSB_CUDA(cudaMalloc(&ix->X, (size_t)N * n * 4));
     SSB_CUDA(cudaMalloc(&ix->words, (size_t)N * WORD_SEGMENTS));
     SSB_CUDA(cudaMalloc(&ix->orig, (size_t)N * 4));
     SSB_CUDA(cudaMalloc(&ix->inv, (size_t)N * 4));
