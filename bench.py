@@ -207,12 +207,19 @@ class IndexEngine:
         build_index_array(X_dev[:w], IndexSettings(series_length=X_dev.shape[1], dataset_size=w,
                                                    leaf_threshold=min(tau, max(1, w // 4))))
         torch.cuda.synchronize()
+        from paper_2212_13297_b200 import _lib
+
+        _lib.prof_reset()
+        _lib.prof_enable(True)  # per-kernel CUDA events of the build (ProfScope)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ev0.record()
         self.index = build_index_array(X_dev, s, id_base=id_base)
         ev1.record()
         torch.cuda.synchronize()
+        _lib.prof_enable(False)
+        self.build_prof = _lib.prof_read()
+        _lib.prof_reset()
         self.build_wall_s = time.perf_counter() - t0
         self.build_dev_ms = ev0.elapsed_time(ev1)
         self.engine = QueryEngine(self.index)
@@ -221,9 +228,23 @@ class IndexEngine:
 
     def build_info(self, N):
         info = self.index.info
-        return {"series_per_s": round(N / self.build_wall_s, 1), "ms": round(1000 * self.build_wall_s, 2),
-                "device_ms": round(self.build_dev_ms, 2), "leaves": info.num_leaves,
-                "nodes": info.num_nodes, "levels": info.levels, "depth": info.depth}
+        out = {"series_per_s": round(N / self.build_wall_s, 1), "ms": round(1000 * self.build_wall_s, 2),
+               "device_ms": round(self.build_dev_ms, 2), "leaves": info.num_leaves,
+               "nodes": info.num_nodes, "levels": info.levels, "depth": info.depth,
+               "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3)}
+                           for k, v in self.build_prof.items()}}
+        if self.build_prof:  # the build's dominant kernel against the measured HBM peak
+            name, (kms, klaunch, kbytes, _) = max(self.build_prof.items(), key=lambda kv: kv[1][0])
+            try:
+                peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0))
+            except OSError:
+                peak = 6650.0
+            gbs = kbytes / (kms / 1000.0) / 1e9
+            out["roofline"] = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
+                               "unit": "GB/s", "frac": round(gbs / peak, 4), "share_of_build": round(
+                                   kms / max(self.build_dev_ms, 1e-9), 4),
+                               "bytes": "per level: 4n B per active series read + 24m B of statistics written"}
+        return out
 
     def query(self, Q_dev, k):
         d2, ids, _ = self.engine.knn_device(Q_dev, k, route=self.route)

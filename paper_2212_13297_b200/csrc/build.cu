@@ -818,7 +818,11 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
     extern __shared__ float fin_sm[];
     const int n = W > 0 ? NN : a.n;
     const int ws = W > 0 ? W : n / WORD_SEGMENTS;  // points per word segment
-    const int padn = n + WORD_SEGMENTS;
+    // padded logical row: PAD words after every word segment (VEC: 4, so float4
+    // chunks stay 16-byte aligned and the 16 PAA lanes' float4 reads hit distinct banks)
+    constexpr bool VEC = W > 0 && W % 4 == 0;
+    constexpr int PAD = VEC ? 4 : 1;
+    const int padn = n + PAD * WORD_SEGMENTS;
     float *thr = fin_sm;                                       // [ALPHABET]
     int *ilay = reinterpret_cast<int *>(fin_sm + ALPHABET);    // physical -> logical
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
         thr[i] = i < ALPHABET - 1 ? __double2float_ru(a.bp[i]) : __int_as_float(0x7f800000);
     for (int e = threadIdx.x; e < n; e += blockDim.x) ilay[layout_pos(n, e)] = e;
     __syncthreads();
-    auto lpos = [&](int e) { return e + e / ws; };  // padded logical position
+    auto lpos = [&](int e) { return e + PAD * (e / ws); };  // padded logical position
     const int n4 = n / 4;
     int src_pos[NC][4];  // padded logical positions of this lane's physical chunks
 #pragma unroll
@@ -859,11 +863,14 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
         double acc = 0.0, hh = 0.0, ll = 0.0;
         auto take = [&](int c, const float4 f) {
             const float v[4] = {f.x, f.y, f.z, f.w};
+            if constexpr (VEC) {
+                *reinterpret_cast<float4 *>(buf + lpos(4 * c)) = f;
+            } else {
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                buf[lpos(4 * c + k)] = v[k];
-                amx = fmaxf(amx, fabsf(v[k]));
+                for (int k = 0; k < 4; k++) buf[lpos(4 * c + k)] = v[k];
             }
+#pragma unroll
+            for (int k = 0; k < 4; k++) amx = fmaxf(amx, fabsf(v[k]));
             if (a.Xb) {
                 __nv_bfloat16 b[4];
 #pragma unroll
@@ -913,9 +920,20 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
             }
         }
         if (a.words && lane < WORD_SEGMENTS) {
-            const float *x = buf + lane * (ws + 1);
+            const float *x = buf + lane * (ws + PAD);
             float sum;
-            if constexpr (W > 0)
+            if constexpr (VEC) {
+                float xv[W];
+#pragma unroll
+                for (int q = 0; q < W / 4; q++) {
+                    const float4 f = reinterpret_cast<const float4 *>(x)[q];
+                    xv[4 * q] = f.x;
+                    xv[4 * q + 1] = f.y;
+                    xv[4 * q + 2] = f.z;
+                    xv[4 * q + 3] = f.w;
+                }
+                sum = pw_f32_seq<W>([&](int i) { return xv[i]; });
+            } else if constexpr (W > 0)
                 sum = pw_f32_seq<W>([&](int i) { return x[i]; });
             else
                 sum = pw_f32_rt(x, ws);
@@ -956,7 +974,7 @@ static int launch_finalize_rows(const FinalizeArgs &a, cudaStream_t s)
 {
     if (a.N == 0) return OK;
     SSB_REQUIRE(a.n % 8 == 0 && a.n % WORD_SEGMENTS == 0, "layout needs n % 16 == 0");
-    const size_t smem = sizeof(float) * ((size_t)ALPHABET + a.n + (size_t)FIN_WARPS * (a.n + WORD_SEGMENTS));
+    const size_t smem = sizeof(float) * ((size_t)ALPHABET + a.n + (size_t)FIN_WARPS * (a.n + 4 * WORD_SEGMENTS));
     const unsigned grid = (unsigned)std::min<int64_t>((a.N + FIN_WARPS - 1) / FIN_WARPS, (int64_t)num_sms() * 8);
     ProfScope ps("build_finalize", s,
                  (double)a.N * a.n * 4 * 2 + (a.Xb ? (double)a.N * (a.n * 2 + 12) : 0.0) +
