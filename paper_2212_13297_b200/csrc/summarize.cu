@@ -248,14 +248,25 @@ __global__ void __launch_bounds__(SA_ROWS)
     const bool live = row < N;
     const int rows_here = (int)min((int64_t)SA_ROWS, N - row0);
     const int nst = (n + W - 1) / W;
+    // thread t copies 16-byte piece t % CH of rows t / CH + k * (SA_ROWS / CH)
+    constexpr int RPP = SA_ROWS / CH;
+    const int pc = t % CH;
+    const float *rowp[CH];
+#pragma unroll
+    for (int k = 0; k < CH; k++) {
+        const int r = t / CH + k * RPP;
+        rowp[k] = r < rows_here ? X + (row0 + r) * n + pc * 4 : nullptr;
+    }
     auto load = [&](int st) {
         if (st < nst) {
-            const int c0 = st * W, ch = min(W, n - c0) / 4;
-            float4 *dst = stage4 + (size_t)(st % SA_STG) * SA_ROWS * CH;
-            for (int idx = t; idx < SA_ROWS * CH; idx += SA_ROWS) {
-                const int r = idx / CH, c = idx % CH;
-                if (r < rows_here && c < ch)
-                    cp_async16(dst + r * CH + sa_slot<W>(c, r), X + (row0 + r) * n + c0 + c * 4);
+            const int c0 = st * W;
+            if (pc * 4 < n - c0) {
+                float4 *dst = stage4 + (size_t)(st % SA_STG) * SA_ROWS * CH;
+#pragma unroll
+                for (int k = 0; k < CH; k++) {
+                    const int r = t / CH + k * RPP;
+                    if (rowp[k]) cp_async16(dst + r * CH + sa_slot<W>(pc, r), rowp[k] + c0);
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -351,7 +362,7 @@ int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, i
     SSB_REQUIRE(npts <= MAX_PTS, "too many distinct segment boundaries");
     if (N == 0 || m == 0) return OK;
     if ((n & 3) == 0 && !getenv("SSB_STATS_SYNC")) {
-        static const int w = getenv("SSB_STATS_W") ? atoi(getenv("SSB_STATS_W")) : 32;
+        static const int w = getenv("SSB_STATS_W") ? atoi(getenv("SSB_STATS_W")) : 16;
         return w != 16 ? launch_stats_async<32>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd, s, contig)
                        : launch_stats_async<16>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd, s, contig);
     }
