@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(CHUNK)
 constexpr int BS_STG = 3;
 
 template <int W>
-__global__ void __launch_bounds__(CHUNK)
+__global__ void __launch_bounds__(CHUNK, 7)
     build_stats_async_kernel(const float *__restrict__ X, int n, const uint32_t *__restrict__ perm,
                              const NodeDesc *__restrict__ nodes, const Chunk *__restrict__ chunks,
                              float *__restrict__ stats, int *__restrict__ nonfinite)
@@ -293,15 +293,20 @@ __global__ void __launch_bounds__(CHUNK)
         a = __dadd_rn(a, v);
         b = __dadd_rn(b, __dmul_rn(v, v));
     };
+    // per-thread constants, kept in registers (opaque to rematerialisation,
+    // which otherwise re-reads %tid and the CTA's shared window every chunk)
+    int xr = sa_slot<W>(0, t);
+    uint32_t mine = (uint32_t)__cvta_generic_to_shared(bs_stage + t * CH);
+    asm volatile("" : "+r"(xr), "+r"(mine));
     for (int st = 0; st < nst; st++) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();  // stage st landed for every thread; stage st-1 fully consumed
         load(st + 2);
         if (live) {
-            const float4 *src = bs_stage + (size_t)(st % BS_STG) * CHUNK * CH + t * CH;
+            const uint32_t src = mine + (uint32_t)((st % BS_STG) * CHUNK * CH * 16);
             const int c0 = st * W, nch = min(W, n - c0) / 4;
             for (int c = 0; c < nch; c++) {
-                const float4 f = src[sa_slot<W>(c, t)];
+                const float4 f = lds128(src + ((uint32_t)(c ^ xr) << 4));
                 const int col = c0 + c * 4;
                 if (ev >= col + 4) {  // no prefix event before any of the four
                     add(f.x);
@@ -478,6 +483,36 @@ __global__ void __launch_bounds__(RTHREADS)
     }
 }
 
+// K-argext: per (node, split-set column) the lowest member index attaining the
+// split-set minimum / maximum (K-eval's one-sided reductions need its side)
+__global__ void __launch_bounds__(RTHREADS)
+    build_argext_kernel(const NodeDesc *__restrict__ nodes, const Range *__restrict__ ranges,
+                        const float *__restrict__ stats, const uint32_t *__restrict__ emin,
+                        const uint32_t *__restrict__ emax, uint32_t *__restrict__ amin, uint32_t *__restrict__ amax)
+{
+    const Range rg = ranges[blockIdx.x];
+    const NodeDesc nd = nodes[rg.node];
+    const int col = blockIdx.y;
+    if (col >= 6 * nd.m) return;
+    const int seg = col % nd.m;
+    const int sa = seg ? nd.ep[seg - 1] : 0;
+    if (col >= 2 * nd.m && nd.ep[seg] - sa < 2) return;  // no halves
+    const float *v = stats + nd.stat_off + (int64_t)col * nd.count + rg.m0;
+    const uint32_t kmin = emin[nd.col_off + col], kmax = emax[nd.col_off + col];
+    uint32_t imin = 0xffffffffu, imax = 0xffffffffu;
+    for (uint32_t i = threadIdx.x; i < rg.cnt; i += RTHREADS) {
+        const uint32_t k = okey(v[i]);
+        if (k == kmin) imin = min(imin, rg.m0 + i);
+        if (k == kmax) imax = min(imax, rg.m0 + i);
+    }
+    imin = __reduce_min_sync(0xffffffffu, imin);
+    imax = __reduce_min_sync(0xffffffffu, imax);
+    if ((threadIdx.x & 31) == 0) {
+        if (imin != 0xffffffffu) atomicMin(&amin[nd.col_off + col], imin);
+        if (imax != 0xffffffffu) atomicMin(&amax[nd.col_off + col], imax);
+    }
+}
+
 // K-eval, warp per candidate: grid = (split-set range, candidate group).  The
 // CTA streams 64-member tiles of ALL the node's stat columns (column-major,
 // padded) into shared memory through a 2-stage cp.async ring; warp w owns
@@ -511,7 +546,9 @@ template <int S>  // result-task slots per lane: 2 * (m + 1) <= 32 * S
 __global__ void __launch_bounds__(EV_WARPS * 32)
     build_eval_warp_kernel(const NodeDesc *__restrict__ nodes, const EvTask *__restrict__ tasks,
                            const float *__restrict__ stats, const double *__restrict__ thr,
-                           const int32_t *__restrict__ valid, uint32_t *__restrict__ acc,
+                           const int32_t *__restrict__ valid, const uint32_t *__restrict__ emin,
+                           const uint32_t *__restrict__ emax, const uint32_t *__restrict__ amin,
+                           const uint32_t *__restrict__ amax, uint32_t *__restrict__ acc,
                            uint32_t *__restrict__ nleft)
 {
     extern __shared__ float4 ev_tile4[];  // [2][6m][EV_TS] floats
@@ -545,14 +582,25 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
     const int rcol = active ? route_col(m, c) * EV_TS : 0;
     const double th = active ? thr[nd.col_off + c] : 0.0;
     const float inf = __int_as_float(0x7f800000);
-    float lmin[S], lmax[S], rmin[S], rmax[S];
+    const int64_t cnt = nd.count;
+    // one-sided reductions: the side holding a column's split-set extreme (the
+    // member amin/amax) has that extreme; only the other side is reduced.
+    // flip = 0xffffffff when the extreme's member goes left (reduce the right side)
+    float omin[S], omax[S];
+    uint32_t fmin[S], fmax[S];
+    const float *rv = stats + nd.stat_off + (int64_t)(active ? route_col(m, c) : 0) * cnt;
 #pragma unroll
     for (int sl = 0; sl < S; sl++) {
-        lmin[sl] = rmin[sl] = inf;
-        lmax[sl] = rmax[sl] = -inf;
+        omin[sl] = inf;
+        omax[sl] = -inf;
+        fmin[sl] = fmax[sl] = 0u;
+        if (coff[sl] >= 0) {
+            const int col = coff[sl] / EV_TS;
+            fmin[sl] = (double)__ldg(rv + amin[nd.col_off + col]) < th ? 0xffffffffu : 0u;
+            fmax[sl] = (double)__ldg(rv + amax[nd.col_off + col]) < th ? 0xffffffffu : 0u;
+        }
     }
     uint32_t nl = 0;
-    const int64_t cnt = nd.count;
     const float *st = stats + nd.stat_off + tk.m0;
     const int ntiles = (int)((tk.cnt + EV_T - 1) / EV_T);
     auto load = [&](int tile) {
@@ -574,46 +622,58 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
         if (active) {
             const float *tb = ev_tile + (tile & 1) * stage_floats;
             const int tn = (int)min((uint32_t)EV_T, tk.cnt - (uint32_t)(tile * EV_T));
-            uint32_t mk[EV_T / 32];
+            uint32_t mk[EV_T / 32], lv[EV_T / 32];
 #pragma unroll
             for (int h = 0; h < EV_T / 32; h++) {
                 const int i = lane + 32 * h;
                 const bool left = i < tn && (double)tb[rcol + i] < th;
                 mk[h] = __ballot_sync(0xffffffffu, left);
+                lv[h] = __ballot_sync(0xffffffffu, i < tn);
                 nl += __popc(mk[h]);
             }
-            auto upd = [&](int sl, float k, bool bit) {
-                if (bit) {
-                    lmin[sl] = fminf(lmin[sl], k);
-                    lmax[sl] = fmaxf(lmax[sl], k);
-                } else {
-                    rmin[sl] = fminf(rmin[sl], k);
-                    rmax[sl] = fmaxf(rmax[sl], k);
-                }
-            };
 #pragma unroll
             for (int h = 0; h < EV_T / 32; h++) {
                 const int i0 = 32 * h;
-                const uint32_t b = mk[h];
                 if (tn - i0 >= 32) {  // full 32 members: unrolled, 16-byte loads, predicated updates
 #pragma unroll
                     for (int sl = 0; sl < S; sl++) {
+                        // the reduced sides (through an identity shuffle, executed by the
+                        // whole warp, so ptxas tests the bits with R2P, 7 per instruction,
+                        // instead of one LOP3 per bit)
+                        const uint32_t pn = __shfl_sync(0xffffffffu, mk[h] ^ fmin[sl], lane);
+                        const uint32_t px = __shfl_sync(0xffffffffu, mk[h] ^ fmax[sl], lane);
                         if (coff[sl] < 0) continue;
                         const float4 *src = reinterpret_cast<const float4 *>(tb + coff[sl] + i0);
 #pragma unroll
-                        for (int i4 = 0; i4 < 8; i4++) {
-                            const float4 k = src[i4];
-                            upd(sl, k.x, (b >> (4 * i4 + 0)) & 1u);
-                            upd(sl, k.y, (b >> (4 * i4 + 1)) & 1u);
-                            upd(sl, k.z, (b >> (4 * i4 + 2)) & 1u);
-                            upd(sl, k.w, (b >> (4 * i4 + 3)) & 1u);
+                        for (int g = 0; g < 2; g++) {  // 16 members: all min updates, then all max updates
+                            float kv[16];
+#pragma unroll
+                            for (int i4 = 0; i4 < 4; i4++) {
+                                const float4 k = src[4 * g + i4];
+                                kv[4 * i4] = k.x;
+                                kv[4 * i4 + 1] = k.y;
+                                kv[4 * i4 + 2] = k.z;
+                                kv[4 * i4 + 3] = k.w;
+                            }
+#pragma unroll
+                            for (int e = 0; e < 16; e++)
+                                if ((pn >> (16 * g + e)) & 1u) omin[sl] = fminf(omin[sl], kv[e]);
+#pragma unroll
+                            for (int e = 0; e < 16; e++)
+                                if ((px >> (16 * g + e)) & 1u) omax[sl] = fmaxf(omax[sl], kv[e]);
                         }
                     }
                 } else {
-                    for (int i = 0; i < tn - i0; i++)
 #pragma unroll
-                        for (int sl = 0; sl < S; sl++)
-                            if (coff[sl] >= 0) upd(sl, tb[coff[sl] + i0 + i], (b >> i) & 1u);
+                    for (int sl = 0; sl < S; sl++) {
+                        if (coff[sl] < 0) continue;
+                        const uint32_t pn = (mk[h] ^ fmin[sl]) & lv[h], px = (mk[h] ^ fmax[sl]) & lv[h];
+                        for (int i = 0; i < tn - i0; i++) {
+                            const float k = tb[coff[sl] + i0 + i];
+                            if ((pn >> i) & 1u) omin[sl] = fminf(omin[sl], k);
+                            if ((px >> i) & 1u) omax[sl] = fmaxf(omax[sl], k);
+                        }
+                    }
                 }
             }
         }
@@ -625,14 +685,14 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
     for (int sl = 0; sl < S; sl++) {
         if (coff[sl] < 0) continue;
         const int q = lane + 32 * sl, j = q >> 1, attr = q & 1;
-        if (lmin[sl] != inf) {
-            atomicMin(&nacc[acc_index(c, 0, j, attr, 0)], okey(lmin[sl]));
-            atomicMax(&nacc[acc_index(c, 0, j, attr, 1)], okey(lmax[sl]));
+        const int col = coff[sl] / EV_TS;
+        const int smin = fmin[sl] ? 0 : 1, smax = fmax[sl] ? 0 : 1;  // sides holding the extremes
+        if (tk.m0 == 0) {  // the extremes themselves, once per node
+            atomicMin(&nacc[acc_index(c, smin, j, attr, 0)], emin[nd.col_off + col]);
+            atomicMax(&nacc[acc_index(c, smax, j, attr, 1)], emax[nd.col_off + col]);
         }
-        if (rmin[sl] != inf) {
-            atomicMin(&nacc[acc_index(c, 1, j, attr, 0)], okey(rmin[sl]));
-            atomicMax(&nacc[acc_index(c, 1, j, attr, 1)], okey(rmax[sl]));
-        }
+        if (omin[sl] != inf) atomicMin(&nacc[acc_index(c, 1 - smin, j, attr, 0)], okey(omin[sl]));
+        if (omax[sl] != -inf) atomicMax(&nacc[acc_index(c, 1 - smax, j, attr, 1)], okey(omax[sl]));
     }
     if (lane == 0 && nl) atomicAdd(&nleft[nd.col_off + c], nl);
 }
@@ -1037,7 +1097,8 @@ static int fill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
 }
 
 static int launch_eval(const NodeDesc *nodes, const EvTask *tasks, int64_t ntasks, int maxm, const float *stats,
-                       const double *thr, const int32_t *valid, uint32_t *acc, uint32_t *nleft, cudaStream_t s)
+                       const double *thr, const int32_t *valid, const uint32_t *emin, const uint32_t *emax,
+                       const uint32_t *amin, const uint32_t *amax, uint32_t *acc, uint32_t *nleft, cudaStream_t s)
 {
     if (ntasks == 0) return OK;
     SSB_REQUIRE(ntasks < (1ll << 31), "too many K-eval tasks in one level");
@@ -1047,8 +1108,8 @@ static int launch_eval(const NodeDesc *nodes, const EvTask *tasks, int64_t ntask
     do {                                                                                                     \
         SSB_CUDA(cudaFuncSetAttribute(build_eval_warp_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                       (int)smem));                                                           \
-        build_eval_warp_kernel<SS><<<(unsigned)ntasks, EV_WARPS * 32, smem, s>>>(nodes, tasks, stats, thr, valid, \
-                                                                                 acc, nleft);                \
+        build_eval_warp_kernel<SS><<<(unsigned)ntasks, EV_WARPS * 32, smem, s>>>(                             \
+            nodes, tasks, stats, thr, valid, emin, emax, amin, amax, acc, nleft);                            \
     } while (0)
     if (slots <= 1)
         EV_CASE(1);
@@ -1210,7 +1271,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     uint32_t *perm = perm_a.as<uint32_t>(), *perm2 = perm_b.as<uint32_t>();
 
     std::vector<int32_t> frontier = {0};  // nodes needing stats this level
-    GrowBuf lv_stats, lv_flags, lv_scan, lv_tmp;  // per-level scratch, grown not re-allocated
+    GrowBuf lv_stats(true), lv_flags, lv_scan, lv_tmp;  // per-level scratch, grown not re-allocated
     int level = 0;
     lap("init");
     while (!frontier.empty()) {
@@ -1278,7 +1339,8 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             SSB_CUDA(cudaMemcpyAsync(d_evt.p, ev_tasks.data(), sizeof(EvTask) * ev_tasks.size(),
                                      cudaMemcpyHostToDevice, s));
         }
-        DevBuf d_nodes, d_chunks, d_cmin, d_cmax, d_emin, d_emax, d_thr, d_valid, d_acc, d_nleft, d_res;
+        DevBuf d_nodes, d_chunks, d_cmin, d_cmax, d_emin, d_emax, d_amin, d_amax, d_thr, d_valid, d_acc, d_nleft,
+            d_res;
         // the level's statistics live in the index's row array (allocated up front,
         // written only by the final row pass) when they fit: no pool growth
         const bool stats_in_x = (size_t)stat_off <= (size_t)N * n;
@@ -1328,14 +1390,22 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
             SSB_CUDA(d_acc.alloc(4 * (size_t)std::max<int64_t>(acc_off, 1), s));
             SSB_CUDA(d_nleft.alloc(4 * (size_t)col_off, s));
             SSB_CUDA(d_res.alloc(sizeof(NodeResult) * F, s));
+            SSB_CUDA(d_amin.alloc(4 * (size_t)col_off, s));
+            SSB_CUDA(d_amax.alloc(4 * (size_t)col_off, s));
             RC(fill_u32(d_emin.as<uint32_t>(), col_off, 0xffffffffu, s));
             RC(fill_u32(d_emax.as<uint32_t>(), col_off, 0u, s));
+            RC(fill_u32(d_amin.as<uint32_t>(), col_off, 0xffffffffu, s));
+            RC(fill_u32(d_amax.as<uint32_t>(), col_off, 0xffffffffu, s));
             RC(fill_u32(d_nleft.as<uint32_t>(), col_off, 0u, s));
             // accumulators: even slots are minima (+inf key), odd slots maxima (0)
             fill_acc_kernel<<<(unsigned)((acc_off + 255) / 256), 256, 0, s>>>(d_acc.as<uint32_t>(), acc_off);
             SSB_CHECK_LAUNCH();
             build_minmax_range_kernel<<<dim3((unsigned)r_ss.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
                 d_nodes.as<NodeDesc>(), d_r_ss, stats_p, d_emin.as<uint32_t>(), d_emax.as<uint32_t>(), 6);
+            SSB_CHECK_LAUNCH();
+            build_argext_kernel<<<dim3((unsigned)r_ss.size(), (unsigned)(6 * maxm)), RTHREADS, 0, s>>>(
+                d_nodes.as<NodeDesc>(), d_r_ss, stats_p, d_emin.as<uint32_t>(), d_emax.as<uint32_t>(),
+                d_amin.as<uint32_t>(), d_amax.as<uint32_t>());
             SSB_CHECK_LAUNCH();
             build_thr_kernel<<<F, 64, 0, s>>>(d_nodes.as<NodeDesc>(), F, d_emin.as<uint32_t>(),
                                               d_emax.as<uint32_t>(), d_thr.as<double>(), d_valid.as<int32_t>());
@@ -1345,7 +1415,8 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 for (int f = 0; f < F; f++) ev += (double)nd[f].ecount * 6 * nd[f].m * 4;
                 ProfScope ps("build_eval", s, ev);
                 RC(launch_eval(d_nodes.as<NodeDesc>(), d_evt.as<EvTask>(), (int64_t)ev_tasks.size(), maxm,
-                               stats_p, d_thr.as<double>(), d_valid.as<int32_t>(), d_acc.as<uint32_t>(),
+                               stats_p, d_thr.as<double>(), d_valid.as<int32_t>(), d_emin.as<uint32_t>(),
+                               d_emax.as<uint32_t>(), d_amin.as<uint32_t>(), d_amax.as<uint32_t>(), d_acc.as<uint32_t>(),
                                d_nleft.as<uint32_t>(), s));
             }
             SSB_CHECK_LAUNCH();

@@ -289,4 +289,11 @@ __device__ __forceinline__ int sa_slot(int c, int r)
     return W == 32 ? c ^ (r & 7) : c ^ ((r >> 1) & 3);  // 8 distinct 16-byte bank groups per 8 rows
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t saddr)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+    return v;
+}
+
 }  // namespace ssb

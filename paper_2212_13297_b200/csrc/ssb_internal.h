@@ -77,25 +77,43 @@ struct DevBuf {
 
 // Grow-only device buffer reused across iterations (e.g. the build's levels):
 // re-allocates with 25% headroom only when a request exceeds its capacity.
+// `direct`: plain cudaMalloc/cudaFree (synchronous) instead of the stream-ordered
+// pool -- for multi-GB scratch, where growing the pool costs far more than a
+// direct allocation.
 struct GrowBuf {
     void *p = nullptr;
     size_t cap = 0;
     cudaStream_t s = nullptr;
+    bool direct = false;
     GrowBuf() = default;
+    explicit GrowBuf(bool d) : direct(d) {}
     GrowBuf(const GrowBuf &) = delete;
     GrowBuf &operator=(const GrowBuf &) = delete;
     ~GrowBuf()
     {
-        if (p) cudaFreeAsync(p, s);
+        if (!p) return;
+        if (direct) {
+            cudaStreamSynchronize(s);
+            cudaFree(p);
+        } else {
+            cudaFreeAsync(p, s);
+        }
     }
     cudaError_t ensure(size_t bytes, cudaStream_t st)
     {
         s = st;
         if (bytes <= cap && p) return cudaSuccess;
-        if (p) cudaFreeAsync(p, st);
+        if (p) {
+            if (direct) {
+                cudaStreamSynchronize(st);
+                cudaFree(p);
+            } else {
+                cudaFreeAsync(p, st);
+            }
+        }
         p = nullptr;
-        cap = bytes + bytes / 4 + 256;
-        return cudaMallocAsync(&p, cap, st);
+        cap = direct ? 2 * bytes + 256 : bytes + bytes / 4 + 256;  // direct: few, large steps
+        return direct ? cudaMalloc(&p, cap) : cudaMallocAsync(&p, cap, st);
     }
     template <typename T>
     T *as() const

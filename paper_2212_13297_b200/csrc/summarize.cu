@@ -295,15 +295,20 @@ __global__ void __launch_bounds__(SA_ROWS)
         a = __dadd_rn(a, v);
         b = __dadd_rn(b, __dmul_rn(v, v));
     };
+    // per-thread constants, kept in registers (opaque to rematerialisation,
+    // which otherwise re-reads %tid and the CTA's shared window every chunk)
+    int xr = sa_slot<W>(0, t);
+    uint32_t mine = (uint32_t)__cvta_generic_to_shared(stage4 + t * CH);
+    asm volatile("" : "+r"(xr), "+r"(mine));
     for (int st = 0; st < nst; st++) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();  // stage st landed for every thread; stage st-1 fully consumed
         load(st + 2);
         if (live) {
-            const float4 *src = stage4 + (size_t)(st % SA_STG) * SA_ROWS * CH + t * CH;
+            const uint32_t src = mine + (uint32_t)((st % SA_STG) * SA_ROWS * CH * 16);
             const int c0 = st * W, ch = min(W, n - c0) / 4;
             for (int c = 0; c < ch; c++) {
-                const float4 f = src[sa_slot<W>(c, t)];
+                const float4 f = lds128(src + ((uint32_t)(c ^ xr) << 4));
                 const int col = c0 + c * 4;
                 if (nextp >= col + 4) {  // no boundary point before any of the four
                     add(f.x);

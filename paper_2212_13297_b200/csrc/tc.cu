@@ -49,8 +49,6 @@ namespace ssb {
 constexpr int TC_BM = 128;   // queries per block (MMA M)
 constexpr int TC_BN = 128;   // rows per tile (MMA N)
 constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
-constexpr int TC_EPI_THREADS = 256;  // 8 epilogue warps
-constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
 constexpr int TC_NACC = 3;           // TMEM accumulators (3 x 128 columns + A <= 128 columns)
 constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB K-chunks
@@ -202,8 +200,8 @@ static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
 
 // KTOP > 0: keep the k smallest upper bounds per thread (k <= KTOP);
 // KTOP == 0: filter against the given bounds only; KTOP < 0: debug dump of S.
-template <int KTOP>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int KTOP, int EPW>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
+__global__ void __launch_bounds__(64 + 32 * EPW, 1)
     tc_filter_kernel(const __grid_constant__ CUtensorMap mapB, TcParams p)
 {
     // mapB's box covers 128/CS rows: every CTA of the cluster loads one row
@@ -225,9 +223,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t *r_full = t_empty + TC_NACC;             // [TC_RS]
     uint64_t *r_empty = r_full + TC_RS;               // [TC_RS]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(r_empty + TC_RS);
-    uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [8 warps][TC_STAGE]
-    float *s_stage_lb = reinterpret_cast<float *>(s_stage + 8 * TC_STAGE);  // [8 warps][TC_STAGE]
-    unsigned *s_fill = reinterpret_cast<unsigned *>(s_stage_lb + 8 * TC_STAGE);  // [8 warps]
+    constexpr int STG = TC_STAGE * 8 / EPW;  // per-warp stage entries (same total)
+    constexpr int COLS = 512 / EPW;          // columns of a tile per epilogue thread
+    uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [EPW warps][STG]
+    float *s_stage_lb = reinterpret_cast<float *>(s_stage + 8 * TC_STAGE);  // [EPW warps][STG]
+    unsigned *s_fill = reinterpret_cast<unsigned *>(s_stage_lb + 8 * TC_STAGE);  // [EPW warps]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int CS = p.CS;
@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         for (int i = 0; i < TC_NACC; i++) {
             mbar_init(&t_full[i], 1);
-            mbar_init(&t_empty[i], TC_EPI_THREADS);
+            mbar_init(&t_empty[i], EPW * 32);
         }
         for (int i = 0; i < TC_RS; i++) {
             mbar_init(&r_full[i], 1);
-            mbar_init(&r_empty[i], TC_EPI_THREADS / 32);  // one arrive per epilogue warp
+            mbar_init(&r_empty[i], EPW);  // one arrive per epilogue warp
         }
         fence_barrier_init();
     }
@@ -398,11 +398,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else {
-        // ---------------- epilogue: 8 warps, two per TMEM lane quarter ----------------
+        // ---------------- epilogue: EPW warps, EPW/4 per TMEM lane quarter ----------------
         // thread <-> query m (TMEM lane), column half h of every 128-row tile
-        const int ew = warp - 2;                   // 0..7
+        const int ew = warp - 2;                   // 0..EPW-1
         const int lane_grp = warp & 3;             // TMEM lanes [32*lane_grp, +32)
-        const int h = ew >> 2;                     // column half
+        const int h = ew >> 2;                     // column group: columns [h*COLS, +COLS) of each tile
         const int m = lane_grp * 32 + lane;
         const int ql = qb * TC_BM + m;
         const bool qvalid = ql < p.nq;
@@ -455,13 +455,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t kk = (uint32_t)p.k;
         float bmax = __int_as_float(0x7f800000);  // last bucket bound read by this thread
         bool touched = false;
-        uint2 *stage = s_stage + ew * TC_STAGE;
-        float *stage_lb = s_stage_lb + ew * TC_STAGE;
-        unsigned *stage_fill = s_fill + ew;  // reserved slots of this warp's stage (may pass TC_STAGE)
+        uint2 *stage = s_stage + ew * STG;
+        float *stage_lb = s_stage_lb + ew * STG;
+        unsigned *stage_fill = s_fill + ew;  // reserved slots of this warp's stage (may pass STG)
         if (lane == 0) *stage_fill = 0;
         __syncwarp();
         auto flush = [&]() {  // warp-uniform
-            const unsigned n_st = min(*(volatile unsigned *)stage_fill, (unsigned)TC_STAGE);
+            const unsigned n_st = min(*(volatile unsigned *)stage_fill, (unsigned)STG);
             unsigned base_slot = 0;
             if (lane == 0 && n_st) base_slot = atomicAdd(p.cand_n, n_st);
             base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int t = 0; t < niter; t++) {
             const int s = t % TC_NACC;
             const int rs = t % TC_RS;
-            const int64_t row0 = tile_of(t) * TC_BN + h * 64;  // first row of this thread's half
+            const int64_t row0 = tile_of(t) * TC_BN + h * COLS;  // first row of this thread's columns
             const bool emit_ok = t >= nwarm;
             // second visit of a warm-up tile: its rows are already in this thread's
             // list (a row counted twice would make the k-th bound invalid)
@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
             const float gcur = qvalid ? ts.gb[m] : -1.f;
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
-            const float4 tcl = ts.tilec[2 * h], tcu = ts.tilec[2 * h + 1];
+            const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
+            const float4 tcl = ts.tilec[2 * hh], tcu = ts.tilec[2 * hh + 1];
             mbar_wait(&t_full[s], (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
@@ -498,10 +499,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 if (lane == 0) mbar_arrive(&r_empty[rs]);
                 continue;
             }
-            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * 64);
-            uint32_t v[64];
+            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
+            uint32_t v[COLS];
 #pragma unroll
-            for (int j = 0; j < 64; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
+            for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
             tmem_wait_ld();
             // the accumulator is in registers: release it to the MMA warp right away
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -529,28 +530,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     thr_s = emit_ok ? fminf(s_lo, s_need) : s_need;
                 }
             }
-            float mg[4];  // per 16-column group maxima
+            float mg[COLS / 16];  // per 16-column group maxima
 #pragma unroll
-            for (int g = 0; g < 4; g++) {
+            for (int g = 0; g < COLS / 16; g++) {
                 float a = fmaxf(__uint_as_float(v[16 * g]), __uint_as_float(v[16 * g + 1]));
 #pragma unroll
                 for (int i = 2; i < 16; i++) a = fmaxf(a, __uint_as_float(v[16 * g + i]));
                 mg[g] = a;
             }
-            float mx = fmaxf(fmaxf(mg[0], mg[1]), fmaxf(mg[2], mg[3]));
+            float mx = mg[0];
+#pragma unroll
+            for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
             if (p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: TMEM loads + max only
             if (__any_sync(0xffffffffu, mx >= thr_s)) {
                 // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
                 const int64_t left = p.N - row0;
-                const uint64_t valid = left >= 64 ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
-                const float4 *rows = ts.rowc + h * 64;
+                const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
+                const float4 *rows = ts.rowc + h * COLS;
                 auto row_lb = [&](int c0, int i) {
                     const float sd = sel16(v + c0, i);
                     const float4 rc = rows[c0 + i];
                     return fmaf(m2f, sd, fmaf(-QH, rc.z, fmaf(-QL, rc.w, alpha_l + rc.x)));
                 };
 #pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 16) {
+                for (int c0 = 0; c0 < COLS; c0 += 16) {
                     uint32_t emit = 0;
                     if (mg[c0 / 16] >= thr_s) {
                         uint32_t work = 0;
@@ -596,14 +599,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const unsigned cnt = __popc(emit);
                         unsigned slot = atomicAdd(stage_fill, cnt);
                         unsigned gslot = 0;
-                        if (slot + cnt > (unsigned)TC_STAGE)
-                            gslot = atomicAdd(p.cand_n, slot + cnt - max(slot, (unsigned)TC_STAGE));
+                        if (slot + cnt > (unsigned)STG)
+                            gslot = atomicAdd(p.cand_n, slot + cnt - max(slot, (unsigned)STG));
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
                             const float lbv = row_lb(c0, i);
                             const uint2 cv = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
-                            if (slot < (unsigned)TC_STAGE) {
+                            if (slot < (unsigned)STG) {
                                 stage_lb[slot] = lbv;
                                 stage[slot] = cv;
                             } else if ((int64_t)gslot < p.cand_cap) {
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (lane == 0) mbar_arrive(&r_empty[rs]);
             // drain the stage once it is half full (a tile adds at most 4 x 32 x 16
             // entries; reservations past its end already went to global memory)
-            if (*(volatile unsigned *)stage_fill >= (unsigned)(TC_STAGE / 2)) flush();
+            if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
             // refresh the bucket bound after this thread's own updates
             // (every 8th tile; the loads are independent so their latencies overlap)
             if (touched && ((t & p.rmask) == p.rmask || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
@@ -937,13 +940,20 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         p.skip_epi = d ? atoi(d) : 0;
     }
     const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
-                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 32;
+                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 64;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
+    // epilogue warps: 16 (32 columns per thread and tile) halve the per-thread
+    // serial epilogue work, which pays where the MMA per tile is long (n > 128:
+    // C2 +3%); at n = 96 (C3) 8 warps measured 5% faster.  The k = 32 list
+    // variant keeps 8 (register budget).  SSB_TC_EPW=8|16 overrides (A/B).
+    static const int epw_env = getenv("SSB_TC_EPW") ? atoi(getenv("SSB_TC_EPW")) : 0;
+    const int epw_pref = epw_env ? epw_env : (n > 128 ? 16 : 8);
+    const int epw = (epw_pref == 16 && !(k > 16 && k <= 32) && !dump) ? 16 : 8;
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(TC_THREADS);
+        cfg.blockDim = dim3(64 + 32 * epw);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -960,24 +970,26 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         return OK;
     };
     const bool nolist = getenv("SSB_TC_NOLIST") != nullptr;  // diagnostics: bucket bound only for k >= 2
+#define TC_GO(KT) (epw == 16 ? go(tc_filter_kernel<KT, 16>) : go(tc_filter_kernel<KT, 8>))
     if (dump)
-        rc = go(tc_filter_kernel<-1>);
+        rc = go(tc_filter_kernel<-1, 8>);
     else if (nolist && k >= 2)
-        rc = go(tc_filter_kernel<0>);
+        rc = TC_GO(0);
     else if (k <= 1)
-        rc = go(tc_filter_kernel<1>);
+        rc = TC_GO(1);
     else if (k <= 4)
-        rc = go(tc_filter_kernel<4>);
+        rc = TC_GO(4);
     else if (k <= 8)
-        rc = go(tc_filter_kernel<8>);
+        rc = TC_GO(8);
     else if (k <= 10)
-        rc = go(tc_filter_kernel<10>);  // the configs' k = 10: no idle stages in the insertion network
+        rc = TC_GO(10);  // the configs' k = 10: no idle stages in the insertion network
     else if (k <= 16)
-        rc = go(tc_filter_kernel<16>);
+        rc = TC_GO(16);
     else if (k <= 32)
-        rc = go(tc_filter_kernel<32>);
+        rc = go(tc_filter_kernel<32, 8>);
     else
-        rc = go(tc_filter_kernel<0>);
+        rc = TC_GO(0);
+#undef TC_GO
     if (rc) return rc;
     SSB_CHECK_LAUNCH();
     return OK;
