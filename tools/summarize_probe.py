@@ -23,7 +23,9 @@ def main():
     for name, fn in (("words", lambda: S.paa_words(X)), ("words+paa", lambda: S.paa_words(X, with_paa=True)),
                      ("segment_stats m=16", lambda: S.segment_stats_matrix(X, starts, ends)),
                      ("segment_stats m=16 overlapping",
-                      lambda: S.segment_stats_matrix(X, starts // 2, ends))):
+                      lambda: S.segment_stats_matrix(X, starts // 2, ends)),
+                     ("segment_stats m=1", lambda: S.segment_stats_matrix(X, np.array([0]), np.array([n]))),
+                     ("segment_stats m=4", lambda: S.segment_stats_matrix(X, np.arange(4) * 64, np.arange(1, 5) * 64))):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
