@@ -22,8 +22,9 @@
 // One CTA = one block of 128 queries (M = 128) x a contiguous range of
 // 128-row tiles (N = 128); two query blocks form a cluster and get every B
 // tile by TMA multicast.  Warp roles (10 warps): w0 producer (tile side data
-// by 1-D bulk copies into a 4-deep tile-slot ring; whole B tiles, KB 16 KB
-// K-chunks each, into a ring of tile slots), w1 TMEM allocation + MMA issue
+// by 1-D bulk copies into an 8-deep tile-slot ring; whole B tiles, KB K-chunks
+// of 64 columns (SWIZZLE_128B, 16 KB; 32-column SWIZZLE_64B chunks are an A/B
+// option) each, into a 192 KB ring of tile slots), w1 TMEM allocation + MMA issue
 // (A = the query block, resident in TMEM; 3 accumulators of 128 columns; one
 // barrier wait and one commit per tile), w2..w9 epilogue (two warps per TMEM
 // lane quarter, one query per thread, 64 columns per tile).  The first `warm`
@@ -51,7 +52,8 @@ constexpr int TC_BN = 128;   // rows per tile (MMA N)
 constexpr int TC_KMAX = 4;   // 64-column chunks (n <= 256)
 constexpr int TC_STAGE = 128;        // per-warp candidate staging (shared memory)
 constexpr int TC_NACC = 3;           // TMEM accumulators (3 x 128 columns + A <= 128 columns)
-constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB K-chunks
+constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB units (192 KB)
+constexpr int TC_NBAR = 24;          // tile-slot barriers: up to 192 KB / 8 KB tiles
 constexpr int TC_KTOP = 32;   // in-register top-k of upper bounds for k <= 32; larger k: buckets only
 
 // tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
@@ -59,12 +61,14 @@ constexpr int TC_KTOP = 32;   // in-register top-k of upper bounds for k <= 32; 
 constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                               ((uint32_t)(TC_BM >> 4) << 24);
 
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr)
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t smem_addr, int cw)
 {
-    // K-major SWIZZLE_128B canonical layout: 8-row groups 1024 B apart (SBO),
-    // LBO unused (1), version 1 (sm100), layout type 2 (128B swizzle)
-    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+    // K-major swizzled canonical layout, LBO unused (1), version 1 (sm100):
+    // cw = 64 columns: SWIZZLE_128B (type 2), 8-row groups 1024 B apart (SBO);
+    // cw = 32 columns: SWIZZLE_64B (type 4), 8-row groups 512 B apart
+    const uint64_t sbo = cw == 64 ? (1024 >> 4) : (512 >> 4), type = cw == 64 ? 2 : 4;
+    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | (sbo << 32) | ((uint64_t)1 << 46) |
+           (type << 61);
 }
 
 __device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int x, int y, uint64_t *bar)
@@ -162,8 +166,9 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 }
 
 struct TcParams {
-    int n;                 // series length (K, zero-padded to KB*64 by TMA)
-    int KB;                // 64-column chunks
+    int n;                 // series length (K, zero-padded to KB*CW by TMA)
+    int KB;                // K-chunks per tile
+    int CW;                // chunk width: 64 (SWIZZLE_128B) or 32 (SWIZZLE_64B) columns
     int64_t N;             // rows
     const uint4 *qb;       // BF16 queries, row-major (n per row), nq rows
     int nq;                // queries in this launch (<= QB*128)
@@ -186,11 +191,12 @@ struct TcParams {
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
     int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
-    int skip_epi;              // diagnostics (SSB_TC_DIAG=1): epilogue only releases TMEM
+    int skip_epi;              // diagnostics (SSB_TC_DIAG): 1 epilogue only releases TMEM, 2 TMEM loads + max,
+                               // 3 = 1 without MMAs (loads only), 4 = 1 without loads after the first ring (MMA only)
 };
 
 // per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
-constexpr int TC_RS = 4;  // tile-slot ring depth
+constexpr int TC_RS = 8;  // tile-slot ring depth (>= the B ring in tiles for KB >= 2: side data never throttles the loads)
 struct TileSlot {
     float4 rowc[TC_BN];  // row bound constants of the tile's 128 rows
     float4 tilec[4];     // per 64-row half: (min a_l, max u, max v, -), (min a_u, min u, min v, -)
@@ -211,14 +217,18 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     // (pointer arithmetic on smem_raw keeps the shared address space visible to the compiler)
     unsigned char *base = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
     const int KB = p.KB;
-    const uint32_t chunk_bytes = TC_BM * 128;  // 128 rows x 64 bf16
-    unsigned char *sRing = base;  // TC_NSLOT chunk slots (128 rows x 64 cols each)
-    TileSlot *slots = reinterpret_cast<TileSlot *>(sRing + TC_NSLOT * chunk_bytes);  // [TC_RS]
+    const int CW = p.CW;
+    const uint32_t row_bytes = (uint32_t)CW * 2;
+    const uint32_t chunk_bytes = TC_BN * row_bytes;  // 128 rows x CW bf16
+    const uint32_t ring_bytes = TC_NSLOT * TC_BN * 128;
+    const int NS = (int)(ring_bytes / (chunk_bytes * KB));  // tile slots (<= TC_NBAR)
+    unsigned char *sRing = base;  // NS tile slots of KB chunks
+    TileSlot *slots = reinterpret_cast<TileSlot *>(sRing + ring_bytes);  // [TC_RS]
     uint64_t *bars = reinterpret_cast<uint64_t *>(slots + TC_RS);
     uint64_t *a_full = bars + 0;
-    uint64_t *b_full = bars + 1;                      // [TC_NSLOT]
-    uint64_t *b_empty = b_full + TC_NSLOT;            // [TC_NSLOT]
-    uint64_t *t_full = b_empty + TC_NSLOT;            // [TC_NACC]
+    uint64_t *b_full = bars + 1;                      // [TC_NBAR]
+    uint64_t *b_empty = b_full + TC_NBAR;             // [TC_NBAR]
+    uint64_t *t_full = b_empty + TC_NBAR;             // [TC_NACC]
     uint64_t *t_empty = t_full + TC_NACC;             // [TC_NACC]
     uint64_t *r_full = t_empty + TC_NACC;             // [TC_RS]
     uint64_t *r_empty = r_full + TC_RS;               // [TC_RS]
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(a_full, 128);  // the four h == 0 epilogue warps write A into TMEM
-        for (int i = 0; i < TC_NSLOT; i++) {
+        for (int i = 0; i < NS; i++) {
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], CS);  // one multicast commit from every CTA of the cluster
         }
@@ -278,9 +288,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (ntile > 0) {
-            // ring of tile slots: a slot holds a whole B tile (KB K-chunks of 16 KB);
+            // ring of tile slots: a slot holds a whole B tile (KB K-chunks);
             // tile t -> slot t % NS, one barrier wait / commit per tile
-            const int NS = TC_NSLOT / KB;
             const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
             const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sRing);
             const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(b_full);
@@ -311,7 +320,17 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 const int row0 = (int)(tile * TC_BN) + rank * srows;
                 if (t >= NS) mbar_wait(&b_empty[slot], phase ^ 1u);
                 const uint32_t bar = full0 + (uint32_t)slot * 8;
-                const uint32_t dst0 = ring + (uint32_t)slot * tile_bytes + (uint32_t)(rank * srows * 128);
+                if (p.skip_epi == 4 && t >= NS) {  // diagnostics: MMA-only pipeline (stale B tiles)
+                    asm volatile("{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                                 "@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(bar)
+                                 : "memory");
+                    if (++slot == NS) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
+                    continue;
+                }
+                const uint32_t dst0 = ring + (uint32_t)slot * tile_bytes + (uint32_t)rank * srows * row_bytes;
                 // the whole tile (every CTA's row slice of every K-chunk) lands in this CTA's slot
                 asm volatile(
                     "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
@@ -325,14 +344,14 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
                             "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%4, {%2, %3}], [%1];\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * 64), "r"(row0), "l"(&mapB)
+                            "r"(bar), "r"(kb * CW), "r"(row0), "l"(&mapB)
                             : "memory");
                     else
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
                             "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
                             ".multicast::cluster [%0], [%4, {%2, %3}], [%1], %5;\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * 64), "r"(row0), "l"(&mapB), "h"(cmask)
+                            "r"(bar), "r"(kb * CW), "r"(row0), "l"(&mapB), "h"(cmask)
                             : "memory");
                 }
                 if (++slot == NS) {
@@ -346,11 +365,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         if (ntile > 0) {
             mbar_wait(a_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const int NS = TC_NSLOT / KB;
             const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
             const uint32_t a_tmem = tmem_base + TC_NACC * TC_BN;  // 8 columns per K=16 step
             const int KS = (p.n + 15) / 16;                        // K=16 steps with data
-            const uint64_t bdesc0 = umma_desc_sw128((uint32_t)__cvta_generic_to_shared(sRing));
+            const uint64_t bdesc0 = umma_desc_sw((uint32_t)__cvta_generic_to_shared(sRing), CW);
             const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(b_empty);
             const uint32_t tfull0 = (uint32_t)__cvta_generic_to_shared(t_full);
             int slot = 0;
@@ -361,13 +379,13 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 mbar_wait(&b_full[slot], phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
-                for (int kb = 0; kb < KB; kb++) {
-                    // descriptor start address advances 32 B (>> 4 = 2) per K=16 step, a chunk
-                    // (16 KB) per 64 columns; A advances 8 TMEM columns per K=16 step
+                for (int kb = 0; kb < KB && p.skip_epi != 3; kb++) {  // 3: diagnostics, loads only
+                    // descriptor start address advances 32 B (>> 4 = 2) per K=16 step inside
+                    // the swizzle atom, a chunk per CW columns; A advances 8 TMEM columns per K=16 step
                     const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)slot * tile_bytes + kb * chunk_bytes) >> 4);
-                    // K=16 steps of this chunk that hold data (n = 96: the last chunk has 2
-                    // of 4; the zero-filled rest is skipped)
-                    const int ksn = min(4, KS - kb * 4);
+                    // K=16 steps of this chunk that hold data (n = 96 with 64-column chunks:
+                    // the last chunk has 2 of 4; the zero-filled rest is skipped)
+                    const int ksn = min(CW / 16, KS - kb * (CW / 16));
                     asm volatile(
                         "{\n.reg .pred p, q, q1, q2, q3;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
                         "elect.sync _|q, 0xffffffff;\n"
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                         "@q1 tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
                         "@q2 tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
                         "@q3 tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n}" ::"r"(tmem_d),
-                        "r"(a_tmem + (uint32_t)(kb * 32)), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u), "r"(ksn)
+                        "r"(a_tmem + (uint32_t)(kb * (CW / 2))), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u), "r"(ksn)
                         : "memory");
                 }
                 // the slot is free in every CTA's producer (multicast), the accumulator is ready
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // zero past n (the B chunks are zero-filled there by TMA)
             const int rowv = p.n / 8;  // uint4 per row
             const uint32_t a_lane = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + TC_NACC * TC_BN;
-            for (int c0 = 0; c0 < KB * 32; c0 += 16) {
+            for (int c0 = 0; c0 < KB * CW / 2; c0 += 16) {
                 uint32_t r[16];
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
@@ -852,7 +870,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int box_rows = 128)
+static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int box_rows = 128, int cw = 64)
 {
     auto enc = get_encode();
     if (!enc) {
@@ -861,10 +879,11 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int 
     }
     cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)n * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)cw, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     cw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error(ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -889,7 +908,13 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     if (nq == 0 || N == 0) return OK;
     TcParams p;
     p.n = n;
-    p.KB = (n + 63) / 64;
+    // K-chunk width 64 (SWIZZLE_128B).  32-column chunks (SWIZZLE_64B; n = 96: 3 x 8 KB
+    // per tile instead of 2 x 16 KB, 8 tiles in flight instead of 6) measured slower
+    // on C3 (loads-only pipeline -10%: 64-byte TMA row segments; MMA-only -11%), so
+    // they are kept as the SSB_TC_CW=32 A/B switch (tested) only.
+    p.CW = 64;
+    if (const char *e = getenv("SSB_TC_CW")) p.CW = atoi(e) == 32 ? 32 : 64;  // diagnostics (A/B)
+    p.KB = (n + p.CW - 1) / p.CW;
     p.N = N;
     p.nq = nq;
     const int QB = (nq + TC_BM - 1) / TC_BM;
@@ -909,7 +934,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
     CUtensorMap mB;
-    int rc = make_map(&mB, Xb, N, n, TC_BN / CS);
+    int rc = make_map(&mB, Xb, N, n, TC_BN / CS, p.CW);
     if (rc) return rc;
     p.qb = reinterpret_cast<const uint4 *>(Qb);
     p.qn2 = qn2;
@@ -940,7 +965,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         p.skip_epi = d ? atoi(d) : 0;
     }
     const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
-                     8 * (1 + 2 * TC_NSLOT + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 64;
+                     8 * (1 + 2 * TC_NBAR + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 64;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
     // epilogue warps: 16 (32 columns per thread and tile) halve the per-thread
     // serial epilogue work, which pays where the MMA per tile is long (n > 128:
