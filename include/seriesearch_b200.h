@@ -193,6 +193,19 @@ int ssb_index_lb_eapca(const ssb_index *index, const float *Q, int32_t B, double
 int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const double *lower,
                const double *upper, int32_t n, double *out, void *stream);
 
+/* Ingest series [first, first + count) of a raw dataset file (headerless LE
+ * float32, n per series; core.py:113-159) into HBM at dst (device, count x n).
+ * Replaces the reference's chunked file reads feeding the build, build.py:414-451
+ * (DBuffer double buffering) and pscan.py:50-79: file -> pinned host double
+ * buffer (chunk_bytes each, <= 0: 64 MB; `threads` preads per chunk, <= 0: up
+ * to 16) -> cudaMemcpyAsync on `stream`, reading chunk i while chunk i-1 is
+ * copied.  count < 0 = to the end of the file.  Synchronizes `stream`.
+ * stats (host, optional): [0] bytes ingested, [1] wall seconds.
+ * Errors: io (missing/unreadable file, short read), usage (size not a whole
+ * number of series, range past the end) -- core.py series_count/read_series_file. */
+int ssb_ingest_file(const char *path, int64_t first, int64_t count, int32_t n, float *dst,
+                    int64_t chunk_bytes, int32_t threads, void *stream, double *stats);
+
 #ifdef __cplusplus
 }
 #endif

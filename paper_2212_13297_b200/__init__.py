@@ -4,7 +4,7 @@ Drop-in for the reference package ``seriesearch`` 0.1.0's index-build and
 query entry points; all compute runs in libseriesearch_b200.so (sm_100a).
 """
 
-from .build import BuildTrace, SeriesIndex, build_index, build_index_array
+from .build import BuildTrace, SeriesIndex, build_index, build_index_array, ingest_file
 from .errors import DataFileError, DeviceError, IntegrityError, SeriesearchError, UsageError
 from .persist import IndexSettings, QueryableIndex, load_index, write_index
 from .pscan import brute_force_knn, knn_batch, pscan, pscan_query
@@ -21,6 +21,7 @@ __all__ = [
     "build_index",
     "build_index_array",
     "exact_knn",
+    "ingest_file",
     "load_index",
     "write_index",
     "DataFileError",

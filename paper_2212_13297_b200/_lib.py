@@ -51,6 +51,7 @@ _SIGS = {
     "ssb_index_lb_eapca": [P, P, I32, P, P],
     "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
     "ssb_merge_topk": [P, I32, I32, I32, P, P, P],
+    "ssb_ingest_file": [ctypes.c_char_p, I64, I64, I32, P, I64, I32, P, P],
 }
 
 M_MAX = 32

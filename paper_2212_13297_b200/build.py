@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from ._device import device_f32, ptr, require_cuda, stream_handle
-from .core import read_series_file, series_count
+from .core import series_count
 from .errors import UsageError
 from .summarize import device_breakpoints
 from .tree import Node, tree_from_records
@@ -145,6 +145,33 @@ def build_index_array(data, settings, trace: BuildTrace | None = None, *, initia
     return idx
 
 
+def ingest_file(path: str, n: int, first: int = 0, count: int | None = None, *,
+                chunk_bytes: int = 64 << 20, threads: int = 0, stream=None):
+    """Series [first, first + count) of a raw dataset file into HBM.
+
+    The B200 form of the reference's chunked file reads feeding the build
+    (build.py:414-451, DBuffer double buffering) and the scan (pscan.py:50-79):
+    file -> pinned double buffer -> H2D copy, the read of chunk i overlapping the
+    copy of chunk i-1 (csrc/ingest.cu).  Returns ``(tensor (count, n) float32 on
+    the device, {"bytes", "seconds", "GBps"})``.  Missing file: DataFileError;
+    size not a whole number of series or range past the end: UsageError.
+    """
+    t = require_cuda()
+    total = series_count(path, n)  # DataFileError / UsageError before any allocation
+    if first < 0 or first > total:
+        raise UsageError(f"{path}: first series {first} outside [0, {total}]")
+    if count is None:
+        count = total - first
+    if count < 0 or first + count > total:
+        raise UsageError(f"{path}: requested series [{first}, {first + count}), file has {total}")
+    X = t.empty((count, n), dtype=t.float32, device="cuda")
+    st = (ctypes.c_double * 2)()
+    _lib.call("ssb_ingest_file", path.encode(), int(first), int(count), int(n), ptr(X), int(chunk_bytes),
+              int(threads), stream_handle(stream), st)
+    secs = st[1]
+    return X, {"bytes": int(st[0]), "seconds": secs, "GBps": (st[0] / secs / 1e9) if secs > 0 else None}
+
+
 def build_index(dataset_path: str, settings, num_threads: int, buffer_bytes: int | None = None,
                 dbsize: int | None = None, flush_threshold: int | None = None,
                 scratch_dir: str | None = None, trace: BuildTrace | None = None, **kw) -> SeriesIndex:
@@ -167,4 +194,8 @@ def build_index(dataset_path: str, settings, num_threads: int, buffer_bytes: int
         raise UsageError(
             f"buffer too small: each of {num_workers} regions holds {region_capacity} series, "
             f"need at least one chunk of {dbsize}")
-    return build_index_array(read_series_file(dataset_path, n), settings, trace, **kw)
+    # the file goes straight to HBM through the pinned double-buffer pipeline
+    X, ingest = ingest_file(dataset_path, n, 0, data_size, threads=max(1, num_threads))
+    if trace is not None:
+        trace.note(0, "ingest", **ingest)
+    return build_index_array(X, settings, trace, **kw)
