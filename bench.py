@@ -370,6 +370,21 @@ def main():
         del D
     if X_dev is None:
         X_dev = torch.from_numpy(X).cuda()
+    # device generator (documented Philox stream) on a sample of
+    # the shard size, beside the host generator time (data_gen_s)
+    from paper_2212_13297_b200 import generate as _G
+
+    g_rows = min(len(X), 4_000_000)
+    g_fn = _G.unit_gaussian_device if args.workload == "c3" else _G.random_walks_device
+    g_fn(1024, wl.n, 0)
+    torch.cuda.synchronize()
+    g0 = time.perf_counter()
+    g_out = g_fn(g_rows, wl.n, 0, start=lo)
+    torch.cuda.synchronize()
+    g_s = time.perf_counter() - g0
+    del g_out
+    device_gen = {"series_per_s": round(g_rows / g_s, 1), "rows": g_rows,
+                  "host_series_per_s": round(len(X) / t_gen, 1) if t_gen > 0 else None}
     # the calls of one step: every cell's queries are answered; cells with the
     # same k are batched into one call unless --per-cell (same queries, same
     # answers: the batch size is the engine's choice, the API takes any B)
@@ -515,7 +530,8 @@ def main():
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "build": dict(engine.build_info(hi - lo), **({"ingest": ingest} if ingest else {})),
+        "build": dict(engine.build_info(hi - lo), **({"ingest": ingest} if ingest else {}),
+                      device_gen=device_gen),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

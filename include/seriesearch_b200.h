@@ -206,6 +206,15 @@ int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const doub
 int ssb_ingest_file(const char *path, int64_t first, int64_t count, int32_t n, float *dst,
                     int64_t chunk_bytes, int32_t threads, void *stream, double *stats);
 
+/* Seeded synthetic series in HBM (out: device, count x n float32): series
+ * [start, start + count) of a documented Philox4x32-10 stream (csrc/generate.cu
+ * header; NOT numpy's bits).  kind 0: random walks -- float64 prefix sums of
+ * N(0,1), float32, z-normalised (the generate.py:42-55 / core.py:33-47 recipe);
+ * kind 1: unit-Gaussian rows (N(0,1) / float64 L2 norm; config-3 stand-in).
+ * Prefix-stable: series i depends only on (seed, i).  n <= 1024. */
+int ssb_generate(int32_t kind, int64_t start, int64_t count, int32_t n, uint64_t seed, float *out,
+                 void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -239,3 +239,64 @@ def best_split(members, endpoints, mu_min0=np.inf, mu_max0=-np.inf, allow_vsplit
         "gain": pol.gain,
         "n_left": pol.n_left,
     }
+
+
+# ---------------------------------------------------------------------------
+# device generator stream (csrc/generate.cu).  The reference's
+# generator is numpy's Philox(SeedSequence(seed, spawn_key=(i,))) (generate.py:
+# 27-81); the device generator keeps its recipe (walk = cumsum of N(0,1) in
+# float64 -> float32 -> z_normalize, core.py:33-47; unit rows = N(0,1) / L2
+# norm) on a documented NEW stream, restated here in numpy.  Philox4x32-10 is
+# pinned by the Random123 known-answer vectors (tests/test_oracle.py).
+
+_PH_M = (np.uint64(0xD2511F53), np.uint64(0xCD9E8D57))
+_PH_W = (0x9E3779B9, 0xBB67AE85)
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 (Salmon et al. SC'11) on arrays: ctr (..., 4) u32, key (2,) u32 -> (..., 4) u32."""
+    c = np.asarray(ctr, np.uint64).copy()
+    k0, k1 = int(key[0]), int(key[1])
+    m32 = np.uint64(0xFFFFFFFF)
+    for r in range(10):
+        if r:
+            k0 = (k0 + _PH_W[0]) & 0xFFFFFFFF
+            k1 = (k1 + _PH_W[1]) & 0xFFFFFFFF
+        p0 = _PH_M[0] * c[..., 0]
+        p1 = _PH_M[1] * c[..., 2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & m32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & m32
+        c = np.stack([hi1 ^ c[..., 1] ^ np.uint64(k0), lo1, hi0 ^ c[..., 3] ^ np.uint64(k1), lo0], axis=-1)
+    return c.astype(np.uint32)
+
+
+def gen_normals(start: int, count: int, n: int, seed: int, tag: int) -> np.ndarray:
+    """(count, n) float64 normals of the device stream (generate.cu gen_normal)."""
+    i = np.arange(start, start + count, dtype=np.uint64)[:, None]
+    b = np.arange((n + 1) // 2, dtype=np.uint64)[None, :]
+    ctr = np.stack(np.broadcast_arrays(b, i & np.uint64(0xFFFFFFFF), i >> np.uint64(32),
+                                       np.full_like(b, tag)), axis=-1)
+    x = philox4x32_10(ctr, (seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)).astype(np.float64)
+    u1 = (np.floor(x[..., 0] / 32) * 67108864.0 + np.floor(x[..., 1] / 64) + 0.5) / 9007199254740992.0
+    u2 = (np.floor(x[..., 2] / 32) * 67108864.0 + np.floor(x[..., 3] / 64) + 0.5) / 9007199254740992.0
+    r = np.sqrt(-2.0 * np.log(u1))
+    z = np.empty((count, 2 * b.shape[1]))
+    z[:, 0::2] = r * np.cos(2 * np.pi * u2)
+    z[:, 1::2] = r * np.sin(2 * np.pi * u2)
+    return z[:, :n]
+
+
+def gen_random_walks(start: int, count: int, n: int, seed: int) -> np.ndarray:
+    """Device stream kind 0: z_normalize(f32(cumsum(normals))) per series (core.py:33-47)."""
+    w = np.cumsum(gen_normals(start, count, n, seed, 0), axis=1).astype(np.float32).astype(np.float64)
+    mu = w.mean(axis=1, keepdims=True)
+    sd = w.std(axis=1, keepdims=True)
+    out = ((w - mu) / np.where(sd < 1e-8, 1.0, sd)).astype(np.float32)
+    out[(sd < 1e-8)[:, 0]] = 0
+    return out
+
+
+def gen_unit_gaussian(start: int, count: int, n: int, seed: int) -> np.ndarray:
+    """Device stream kind 1: normals / float64 L2 norm, float32."""
+    z = gen_normals(start, count, n, seed, 1)
+    return (z / np.linalg.norm(z, axis=1, keepdims=True)).astype(np.float32)

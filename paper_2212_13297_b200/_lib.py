@@ -52,6 +52,7 @@ _SIGS = {
     "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
     "ssb_merge_topk": [P, I32, I32, I32, P, P, P],
     "ssb_ingest_file": [ctypes.c_char_p, I64, I64, I32, P, I64, I32, P, P],
+    "ssb_generate": [I32, I64, I64, I32, ctypes.c_uint64, P, P],
 }
 
 M_MAX = 32

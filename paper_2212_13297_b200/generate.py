@@ -134,3 +134,32 @@ def unit_gaussian(count: int, n: int, seed: int, chunk: int = 65536,
         for c, blk in ex.map(_ug_chunk, jobs):
             out[c * chunk : c * chunk + len(blk)] = blk
     return out
+
+
+def _device_series(kind: int, count: int, n: int, seed: int, start: int, stream):
+    import ctypes
+
+    from . import _lib
+    from ._device import ptr, require_cuda, stream_handle
+
+    t = require_cuda()
+    out = t.empty((count, n), dtype=t.float32, device="cuda")
+    _lib.call("ssb_generate", int(kind), int(start), int(count), int(n), ctypes.c_uint64(seed & (2**64 - 1)),
+              ptr(out), stream_handle(stream))
+    return out
+
+
+def random_walks_device(count: int, n: int, seed: int, start: int = 0, stream=None):
+    """Series [start, start+count) of the DEVICE random-walk stream, in HBM.
+
+    Same recipe as ``random_walks`` (float64 cumsum of N(0,1) -> float32 ->
+    z-normalised, generate.py:42-55 / core.py:33-47) on a documented new
+    stream: Philox4x32-10 + Box-Muller (csrc/generate.cu), not numpy's bits.
+    Prefix-stable, so each rank of a sharded build generates only its rows.
+    """
+    return _device_series(0, count, n, seed, start, stream)
+
+
+def unit_gaussian_device(count: int, n: int, seed: int, start: int = 0, stream=None):
+    """Rows [start, start+count) of the DEVICE unit-Gaussian stream (N(0,1) / L2 norm)."""
+    return _device_series(1, count, n, seed, start, stream)

@@ -107,3 +107,16 @@ def test_reference_engine_equals_oracle_scan(oracle):
     for k in (1, 10):
         d2, _ = oracle.knn_scan(g["data"], g["queries"], k)
         assert np.array_equal(d2, g[f"d2_k{k}"]), k
+
+
+def test_philox_known_answers(oracle):
+    """Random123 kat_vectors for philox4x32-10 (the device generator's stream)."""
+    import numpy as np
+
+    kat = [((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+           ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+           ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+            (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
+    for ctr, key, want in kat:
+        got = oracle.philox4x32_10(np.array(ctr, np.uint32), key)
+        assert tuple(int(v) for v in got) == want
