@@ -154,7 +154,9 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
  * B x k device arrays (id = original index incl. id_base, pos = leaf-order
  * position); stats_host (nullable): B x 4 uint32 host array receiving
  * (candidate leaves, candidate series, seed-leaf rows, 0) per query.
- * Synchronizes `stream`. */
+ * Reads per-batch candidate counts / overflow flags back (host round trips
+ * inside the call); the outputs are complete in `stream` order when it
+ * returns (no final synchronization). */
 typedef struct {
     /* query.py:45 QueryConfig.eapca_th: a query whose seed bound keeps more than
      * (1 - eapca_th) of the leaves takes the dense "scan" path (K-tc tensor-core

@@ -1096,7 +1096,8 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
             stats_host[4 * q + 3] = d[q];  // 1 = candidate buffer overflowed once
         }
     }
-    SSB_CUDA(cudaStreamSynchronize(s));
+    // the results are stream-ordered on s (the scratch is freed stream-ordered
+    // too): no second host round trip
     return OK;
 }
 
