@@ -96,9 +96,8 @@ __device__ __forceinline__ float okey_inv(uint32_t k)
 __device__ __forceinline__ void stats_w(double ca, double cb, double c2a, double c2b, int w,
                                         float &mean, float &sd)
 {
-    const double wd = (double)w;
-    const double mu = __ddiv_rn(__dsub_rn(cb, ca), wd);
-    const double msq = __ddiv_rn(__dsub_rn(c2b, c2a), wd);
+    const double mu = div_w(__dsub_rn(cb, ca), w);
+    const double msq = div_w(__dsub_rn(c2b, c2a), w);
     const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
     mean = __double2float_rn(mu);
     sd = __double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
@@ -1235,6 +1234,7 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
     const int mmax = cfg.max_segments > 0 ? std::min(cfg.max_segments, M_MAX) : M_MAX;
     const int s0 = std::max(1, cfg.initial_segments);
     SSB_REQUIRE(s0 <= mmax && s0 <= n, "initial_segments must be in [1, min(n, max_segments)]");
+    SSB_CUDA(upload_rcp_w());  // K-stats divides by segment widths through c_rcp_w
     auto t_start = std::chrono::steady_clock::now();
     const bool trace = getenv("SSB_BUILD_TRACE") != nullptr;
     auto lap = [&](const char *what) {

@@ -57,6 +57,40 @@ constexpr int WORD_SEGMENTS = 16;  // SAX word length l (persist.py:70)
 constexpr int ALPHABET = 256;      // persist.py:84-85
 constexpr uint64_t KEY_EMPTY = ~0ull;
 
+// ---------------------------------------------------------------------------
+// float64 division by a segment width w in [1, MAX_SERIES_LEN], correctly
+// rounded, without a division: with y = RN(1/w) (host IEEE division, a
+// __constant__ table per translation unit), q0 = RN(a y), r = a - q0 w (exact
+// with one FMA) and q = RN(q0 + r y) = RN(a / w) (Markstein's theorem: y
+// within 1/2 ulp of 1/w, q0 within 1 ulp of a/w; also checked against a / w
+// on 4.1e9 sampled (a, w) pairs, w = 1..1024, no mismatch).  1 DMUL + 2 DFMA
+// instead of the ~10-instruction division sequence: the statistics kernels
+// divide twice per segment (summarize.py:53-66 stats_from_prefix).
+static __constant__ double c_rcp_w[MAX_SERIES_LEN + 1];
+
+static inline cudaError_t upload_rcp_w()
+{
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 64 && done[dev]) return cudaSuccess;
+    static double h[MAX_SERIES_LEN + 1];
+    h[0] = 0.0;
+    for (int w = 1; w <= MAX_SERIES_LEN; w++) h[w] = 1.0 / (double)w;
+    e = cudaMemcpyToSymbol(c_rcp_w, h, sizeof(h));
+    if (e == cudaSuccess && dev < 64) done[dev] = true;
+    return e;
+}
+
+__device__ __forceinline__ double div_w(double a, int w)
+{
+    const double y = c_rcp_w[w];
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-q0, (double)w, a);
+    return __fma_rn(r, y, q0);
+}
+
 // (d2, id) ordering key: d2 >= +0 so its IEEE bits order like the value;
 // ties break on the ORIGINAL series index (pscan.py:27 stable argsort).
 __host__ __device__ inline uint64_t make_key(float d2, uint32_t id)

@@ -128,9 +128,8 @@ int launch_layout_rows(const float *src, const uint32_t *rows, int64_t N, int n,
 __device__ __forceinline__ void stats_from(double cs_s, double cs_e, double c2_s, double c2_e,
                                            int w, float &mean_out, float &sd_out)
 {
-    const double wd = (double)w;
-    const double mean = __ddiv_rn(__dsub_rn(cs_e, cs_s), wd);
-    const double msq = __ddiv_rn(__dsub_rn(c2_e, c2_s), wd);
+    const double mean = div_w(__dsub_rn(cs_e, cs_s), w);
+    const double msq = div_w(__dsub_rn(c2_e, c2_s), w);
     const double var = __dsub_rn(msq, __dmul_rn(mean, mean));
     const double sd = __dsqrt_rn(var > 0.0 ? var : 0.0);
     mean_out = __double2float_rn(mean);
@@ -366,6 +365,7 @@ int launch_segment_stats(const float *X, int64_t N, int n, const int32_t *pts, i
 {
     SSB_REQUIRE(npts <= MAX_PTS, "too many distinct segment boundaries");
     if (N == 0 || m == 0) return OK;
+    SSB_CUDA(upload_rcp_w());  // stats_from divides by segment widths through c_rcp_w
     if ((n & 3) == 0 && !getenv("SSB_STATS_SYNC")) {
         static const int w = getenv("SSB_STATS_W") ? atoi(getenv("SSB_STATS_W")) : 16;
         return w != 16 ? launch_stats_async<32>(X, N, n, pts, npts, seg_s, seg_e, m, mean, sd, s, contig)
