@@ -131,3 +131,20 @@ def test_segment_stats_general_segments(ssb, oracle, starts, ends):
     omean, osd = oracle.segment_stats(X, np.array(starts), np.array(ends))
     assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
     assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))
+
+
+@pytest.mark.parametrize("m,N", [(16, 1037), (32, 129), (33, 300), (64, 1), (1, 128), (7, 3001)])
+def test_segment_stats_contiguous_partitions(ssb, oracle, m, N):
+    """Contiguous partitions of [0, n): m <= 32 takes the shared-memory staged
+    output path (coalesced block stores), larger m the direct stores; ragged
+    last CTA included."""
+    from paper_2212_13297_b200.summarize import segment_stats_matrix
+
+    n = 256
+    X = random_walks(N, n, 37 + m)
+    cuts = np.linspace(0, n, m + 1).astype(np.int64)
+    starts, ends = cuts[:-1], cuts[1:]
+    mean, sd = segment_stats_matrix(X, starts, ends)
+    omean, osd = oracle.segment_stats(X, starts, ends)
+    assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
+    assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))
