@@ -103,6 +103,7 @@ def parse():
     ap.add_argument("--engine", default="index", choices=("index", "bruteforce"))
     ap.add_argument("--cpu-sample", type=int, default=4, help="queries per cell for the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-multi", action="store_true", help="one ssb_query per call (not ssb_query_multi)")
     ap.add_argument("--ingest-gb", type=float, default=4.0,
                     help="file -> HBM ingest sample (GB of the shard; 0 = skip), reported under build.ingest")
     return ap.parse_args()
@@ -255,6 +256,10 @@ class IndexEngine:
     def query_host(self, Q_host, k):
         d2, ids, _ = self.engine.knn_device(Q_host, k, route=self.route)
         return d2.cpu().numpy(), ids.cpu().numpy()
+
+    def query_multi(self, calls):
+        """All of a step's calls (different k) through one ssb_query_multi."""
+        return [(d2, ids) for d2, ids, _ in self.engine.knn_device_multi(calls, route=self.route)]
 
 
 def merge_shards(d2, ids, k):
@@ -415,7 +420,14 @@ def main():
                 out.append(merge_shards(d2, ids, k) if world > 1 else ids)
         return out
 
+    # every call of a step through one multi-call (one host round trip per step
+    # instead of one per call); --no-multi answers them one ssb_query each
+    multi = not batch and hasattr(engine, "query_multi") and not args.no_multi
+
     def step():
+        if multi:
+            outs = engine.query_multi([(Q, k) for k, Q in Q_dev])
+            return [[merge_shards(d2, ids, k) if world > 1 else ids] for (k, _), (d2, ids) in zip(Q_dev, outs)]
         return [answer(Q, k) for k, Q in Q_dev]
 
     def barrier():
@@ -460,8 +472,12 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        for k, Qh in Q_host:
-            answer(Qh, k, host=True)
+        if multi:
+            outs = engine.query_multi([(Qh, k) for k, Qh in Q_host])
+            _ = [(d2.cpu().numpy(), ids.cpu().numpy()) for d2, ids in outs]
+        else:
+            for k, Qh in Q_host:
+                answer(Qh, k, host=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -521,6 +537,7 @@ def main():
         "data": "synthetic: reference generator recipe (seeded Philox streams; see DESIGN.md Inputs)",
         "config": {"workload": wl.desc, "engine": engine.name, "shards": world,
                    "calls_per_step": [{"k": k, "queries": len(Q)} for k, Q in calls],
+                   "api": "QueryEngine.knn_device_multi (ssb_query_multi: one host round trip per step)" if multi else "QueryEngine.knn_device per call",
                    "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (N * wl.n * 4 / 1e9),
                    "data_gen_s": round(t_gen, 1)},
         "roofline": roof,

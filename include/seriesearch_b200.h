@@ -174,6 +174,16 @@ typedef struct {
 int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, const ssb_query_cfg *cfg,
               float *out_d2, int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, void *stream);
 
+/* Several independent query blocks (call i: B[i] queries Q[i], k[i]; outputs
+ * out_d2[i]/out_id[i]/out_pos[i] as ssb_query) in one call.  The arrays of
+ * device pointers are HOST arrays of ncalls entries.  When every block takes
+ * the lean tensor-core path they are all enqueued before the host reads any
+ * count back (one round trip instead of one per block, e.g. the k = 1 and
+ * k = 10 cells of a workload); answers are those of one ssb_query per block. */
+int ssb_query_multi(const ssb_index *index, int32_t ncalls, const float *const *Q, const int32_t *B,
+                    const int32_t *k, const ssb_query_cfg *cfg, float *const *out_d2, int64_t *const *out_id,
+                    int64_t *const *out_pos, void *stream);
+
 /* K-merge: per query, the k smallest of m (d2, id) keys -- the merge after the
  * NCCL all-gather of per-shard top-k lists.  keys: B x m uint64
  * device array, key = (float bits of d2 << 32) | id, UINT64_MAX = empty;

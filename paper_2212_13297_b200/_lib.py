@@ -45,6 +45,7 @@ _SIGS = {
     "ssb_index_node": [P, I32, P],
     "ssb_index_arrays": [P, P, P, P, P],
     "ssb_query": [P, P, I32, I32, P, P, P, P, P, P],
+    "ssb_query_multi": [P, I32, P, P, P, P, P, P, P, P],
     "ssb_tc_dot_debug": [P, I32, P, I64, I32, P, P],
     "ssb_index_download": [P, P, P, P],
     "ssb_index_load": [P, P, P, I64, I32, I64, I64, P, I32, P, P, P],

@@ -119,6 +119,9 @@ int build_index(const float *X, int64_t N, int n, const double *bp_dev, const Bu
                 cudaStream_t s);
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
                 int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+int index_query_multi(const Index &ix, const QueryCfg &qc, int nc, const float *const *Q, const int32_t *B,
+                      const int32_t *K, float *const *out_d2, int64_t *const *out_id, int64_t *const *out_pos,
+                      cudaStream_t s);
 int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float *S, cudaStream_t s);
 int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_t *out_id, cudaStream_t s);
 int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t s);
@@ -351,6 +354,24 @@ int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, const ss
         qc.route = cfg->route;
     }
     return index_query(ix, qc, Q, B, k, ix.id_base, out_d2, out_id, out_pos, stats_host, (cudaStream_t)stream);
+}
+
+int ssb_query_multi(const ssb_index *h, int32_t ncalls, const float *const *Q, const int32_t *B, const int32_t *k,
+                    const ssb_query_cfg *cfg, float *const *out_d2, int64_t *const *out_id, int64_t *const *out_pos,
+                    void *stream)
+{
+    SSB_REQUIRE(h, "null index");
+    SSB_REQUIRE(ncalls == 0 || (Q && B && k && out_d2 && out_id && out_pos), "null call arrays");
+    const Index &ix = *h->ix;
+    QueryCfg qc;
+    if (cfg) {
+        SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
+        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
+                    "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
+        qc.eapca_th = cfg->eapca_th;
+        qc.route = cfg->route;
+    }
+    return index_query_multi(ix, qc, ncalls, Q, B, k, out_d2, out_id, out_pos, (cudaStream_t)stream);
 }
 
 int ssb_index_lb_eapca(const ssb_index *h, const float *Q, int32_t B, double *out, void *stream)

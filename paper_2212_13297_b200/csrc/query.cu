@@ -913,89 +913,191 @@ static int qfill_u32(uint32_t *p, int64_t count, uint32_t v, cudaStream_t s)
 // copies, K-tc, device-counted exact rescoring, K-select, and ONE host round
 // trip at the end.  *redo is set when a buffer overflowed (the caller then
 // answers the batch on the general path, which tightens bounds and rescans).
-static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_t *out_keys, uint32_t *st_cand_leaves,
-                          uint32_t *st_cand_series, uint32_t *st_seed_rows, uint32_t *st_over, uint32_t leaves_nonempty,
-                          bool want_stats, bool *redo, cudaStream_t s)
+// One tensor-core batch split in two phases so several batches (e.g. calls
+// with different k, ssb_query_multi) can be enqueued back to back before the
+// host reads any count: tc_submit allocates and launches prep, filter,
+// rescoring and selection; tc_check is the one host round trip (filter count,
+// per-query overflow flags, max |q|).
+struct TcWork {
+    DevBuf qlay, qb, qn2, qnrm, gb, cand, clb, cn, keys, cnt, thr, flags, qmax;
+    int B = 0, k = 0, cap = 0, attempt = 0;
+    int64_t tc_cap = 0;
+    bool ready = false;
+};
+
+static int tc_submit(const Index &ix, const float *Q, int B, int k, uint64_t *out_keys, uint32_t *st_cand_leaves,
+                     uint32_t *st_cand_series, uint32_t *st_seed_rows, uint32_t *st_over, uint32_t leaves_nonempty,
+                     bool want_stats, TcWork &w, cudaStream_t s)
 {
     const int n = ix.n;
-    *redo = false;
-    DevBuf qlay, qb, qn2, qnrm, gb, cand, clb, cn, keys, cnt, thr, flags, qmax;
-    const int nq_pad = (B + 127) / 128 * 128;
-    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
-    SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
-    SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
-    SSB_CUDA(qnrm.alloc(8 * (size_t)nq_pad, s));
-    SSB_CUDA(qmax.alloc(4, s));
-    SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
-    int rc = launch_tc_query_prep(Q, B, nq_pad, n, qlay.as<float>(), qb.p, qn2.as<float>(), qnrm.as<float2>(),
-                                  qmax.as<uint32_t>(), s);
-    if (rc) return rc;
-    const int64_t slots = tc_bound_slots(B);
-    SSB_CUDA(gb.alloc(4 * (size_t)slots, s));
-    rc = qfill_u32(gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)
-    if (rc) return rc;
-    // candidates emitted before the pooled bound settles grow with k
-    int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * std::max(8192, 192 * k));
-    if (const char *e = getenv("SSB_TEST_TC_CAP")) tc_cap = std::max<int64_t>(1, atoll(e));  // test hook
-    SSB_CUDA(cand.alloc(8 * (size_t)tc_cap, s));
-    SSB_CUDA(clb.alloc(4 * (size_t)tc_cap, s));
-    SSB_CUDA(cn.alloc(4, s));
-    int cap = std::max(16384, 4 * k);
-    if (const char *e = getenv("SSB_TEST_SELECT_CAP")) cap = std::max(k, atoi(e));  // test hook
-    SSB_CUDA(keys.alloc(8 * (size_t)B * cap, s));
-    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
-    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
-    SSB_CUDA(flags.alloc(4 * (size_t)B, s));
-    std::vector<int32_t> hf(B);
-    // a candidate-buffer overflow is retried with the bounds the filter ended
-    // with (valid, and much tighter than +inf); select overflows go to the caller
-    for (int attempt = 0;; attempt++) {
-    SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
-                          gb.as<unsigned int>(), cand.as<uint2>(), clb.as<float>(), cn.as<unsigned int>(), tc_cap,
-                          nullptr, s);
+    int rc;
+    if (!w.ready) {  // first attempt: buffers, query prep, no bound yet
+        w.B = B;
+        w.k = k;
+        const int nq_pad = (B + 127) / 128 * 128;
+        SSB_CUDA(w.qlay.alloc(4 * (size_t)B * n, s));
+        SSB_CUDA(w.qb.alloc(2 * (size_t)nq_pad * n, s));
+        SSB_CUDA(w.qn2.alloc(4 * (size_t)nq_pad, s));
+        SSB_CUDA(w.qnrm.alloc(8 * (size_t)nq_pad, s));
+        SSB_CUDA(w.qmax.alloc(4, s));
+        SSB_CUDA(cudaMemsetAsync(w.qmax.p, 0, 4, s));
+        rc = launch_tc_query_prep(Q, B, nq_pad, n, w.qlay.as<float>(), w.qb.p, w.qn2.as<float>(),
+                                  w.qnrm.as<float2>(), w.qmax.as<uint32_t>(), s);
+        if (rc) return rc;
+        const int64_t slots = tc_bound_slots(B);
+        SSB_CUDA(w.gb.alloc(4 * (size_t)slots, s));
+        rc = qfill_u32(w.gb.as<uint32_t>(), slots, 0x7f800000u, s);  // no bound yet (+inf)
+        if (rc) return rc;
+        // candidates emitted before the pooled bound settles grow with k
+        w.tc_cap = std::max<int64_t>(1 << 20, (int64_t)B * std::max(8192, 192 * k));
+        if (const char *e = getenv("SSB_TEST_TC_CAP")) w.tc_cap = std::max<int64_t>(1, atoll(e));  // test hook
+        SSB_CUDA(w.cand.alloc(8 * (size_t)w.tc_cap, s));
+        SSB_CUDA(w.clb.alloc(4 * (size_t)w.tc_cap, s));
+        SSB_CUDA(w.cn.alloc(4, s));
+        w.cap = std::max(16384, 4 * k);
+        if (const char *e = getenv("SSB_TEST_SELECT_CAP")) w.cap = std::max(k, atoi(e));  // test hook
+        SSB_CUDA(w.keys.alloc(8 * (size_t)B * w.cap, s));
+        SSB_CUDA(w.cnt.alloc(4 * (size_t)B, s));
+        SSB_CUDA(w.thr.alloc(8 * (size_t)B, s));
+        SSB_CUDA(w.flags.alloc(4 * (size_t)B, s));
+        w.ready = true;
+    }
+    // a retry (candidate-buffer overflow) keeps the bounds the filter ended with
+    SSB_CUDA(cudaMemsetAsync(w.cn.p, 0, 4, s));
+    rc = launch_tc_filter(w.qb.p, w.qn2.as<float>(), w.qnrm.as<float2>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+                          w.gb.as<unsigned int>(), w.cand.as<uint2>(), w.clb.as<float>(), w.cn.as<unsigned int>(),
+                          w.tc_cap, nullptr, s);
     if (rc) return rc;
     // exact rescoring of the candidates whose lower bound is within the final bound
-    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
-    ScanOut so{keys.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
-    rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, qlay.as<float>(), nullptr, cand.as<uint2>(), clb.as<float>(),
-                        gb.as<unsigned int>(), tc_cap, so, s, cn.as<unsigned int>());
+    SSB_CUDA(cudaMemsetAsync(w.cnt.p, 0, 4 * (size_t)B, s));
+    ScanOut so{w.keys.as<uint64_t>(), w.cnt.as<uint32_t>(), nullptr, w.cap};
+    rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, w.qlay.as<float>(), nullptr, w.cand.as<uint2>(),
+                        w.clb.as<float>(), w.gb.as<unsigned int>(), w.tc_cap, so, s, w.cn.as<unsigned int>());
     if (rc) return rc;
     if (want_stats) {  // QueryStats only
         SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
-        tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(cand.as<uint2>(), cn.as<unsigned int>(),
-                                                                       tc_cap, st_cand_series);
+        tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(w.cand.as<uint2>(), w.cn.as<unsigned int>(),
+                                                                       w.tc_cap, st_cand_series);
         SSB_CHECK_LAUNCH();
         rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
         if (rc) return rc;
         SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
     }
-    SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
-    rc = launch_select(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
-                       flags.as<int32_t>(), s);
+    SSB_CUDA(cudaMemsetAsync(w.thr.p, 0xff, 8 * (size_t)B, s));
+    rc = launch_select(w.keys.as<uint64_t>(), w.cnt.as<uint32_t>(), w.cap, B, k, w.thr.as<uint64_t>(), out_keys,
+                       w.flags.as<int32_t>(), s);
     if (rc) return rc;
-    if (st_over) SSB_CUDA(cudaMemcpyAsync(st_over, flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
-    // the one host round trip: filter count, per-query overflow flags, max |q|
+    if (st_over) SSB_CUDA(cudaMemcpyAsync(st_over, w.flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
+    return OK;
+}
+
+// *retry: the candidate buffer overflowed (resubmit: the bounds are kept);
+// *redo: give up on this path (a select overflow, or still overflowing after
+// two retries) -- the batch takes the general path
+static int tc_check(TcWork &w, bool *retry, bool *redo, cudaStream_t s)
+{
+    *retry = *redo = false;
+    std::vector<int32_t> hf(w.B);
     uint32_t hn = 0, qm_bits = 0;
-    SSB_CUDA(cudaMemcpyAsync(&hn, cn.p, 4, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaMemcpyAsync(hf.data(), flags.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(&hn, w.cn.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(&qm_bits, w.qmax.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(hf.data(), w.flags.p, 4 * (size_t)w.B, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
     float qm;
     std::memcpy(&qm, &qm_bits, 4);
     SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
     if (getenv("SSB_TC_TRACE"))
-        fprintf(stderr, "[ssb] tc batch B=%d k=%d attempt %d: %u candidates (cap %lld)\n", B, k, attempt, hn,
-                (long long)tc_cap);
-    if ((int64_t)hn > tc_cap) {
-        if (attempt < 2) continue;
-        *redo = true;
+        fprintf(stderr, "[ssb] tc batch B=%d k=%d attempt %d: %u candidates (cap %lld)\n", w.B, w.k, w.attempt, hn,
+                (long long)w.tc_cap);
+    if ((int64_t)hn > w.tc_cap) {
+        if (w.attempt++ < 2)
+            *retry = true;
+        else
+            *redo = true;
         return OK;
     }
-    for (int q = 0; q < B && !*redo; q++)
+    for (int q = 0; q < w.B && !*redo; q++)
         if (hf[q]) *redo = true;
     return OK;
+}
+
+static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_t *out_keys, uint32_t *st_cand_leaves,
+                          uint32_t *st_cand_series, uint32_t *st_seed_rows, uint32_t *st_over, uint32_t leaves_nonempty,
+                          bool want_stats, bool *redo, cudaStream_t s)
+{
+    TcWork w;
+    for (;;) {
+        int rc = tc_submit(ix, Q, B, k, out_keys, st_cand_leaves, st_cand_series, st_seed_rows, st_over,
+                           leaves_nonempty, want_stats, w, s);
+        if (rc) return rc;
+        bool retry = false;
+        rc = tc_check(w, &retry, redo, s);
+        if (rc || !retry) return rc;
     }
+}
+
+// every query on the tensor-core filter: forced, or (auto) when the dense
+// filter over all N rows costs less than the seed scan of one average leaf
+static bool tc_all_for(const Index &ix, const QueryCfg &qc, int k)
+{
+    const double avg_leaf = (double)ix.N / (double)std::max(1, ix.L);
+    return ix.Xb && k <= TC_KTOP_MAX &&
+           (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+}
+
+// Several independent calls (query blocks, each with its own k) answered with
+// ONE host round trip when every call takes the lean tensor-core path: all
+// calls are enqueued back to back, then each is checked; a call that
+// overflowed is resubmitted (retry) or answered by index_query (redo), and
+// calls off the lean path go through index_query directly.  Same answers as
+// one index_query per call.
+int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
+                int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
+
+int index_query_multi(const Index &ix, const QueryCfg &qc, int nc, const float *const *Q, const int32_t *B,
+                      const int32_t *K, float *const *out_d2, int64_t *const *out_id, int64_t *const *out_pos,
+                      cudaStream_t s)
+{
+    SSB_REQUIRE(nc >= 0 && nc <= 1024, "ncalls must be in [0, 1024]");
+    for (int i = 0; i < nc; i++) {
+        SSB_REQUIRE(K[i] >= 1, "k must be at least 1");
+        SSB_REQUIRE(K[i] <= 4096, "k above 4096 is not supported");
+        SSB_REQUIRE(B[i] >= 0 && B[i] < (1 << 26), "too many queries in one call");
+    }
+    std::vector<TcWork> work(nc);
+    std::vector<DevBuf> keys(nc);
+    std::vector<char> lean(nc, 0);
+    auto submit = [&](int i) -> int {
+        int rc = tc_submit(ix, Q[i], B[i], K[i], keys[i].as<uint64_t>(), nullptr, nullptr, nullptr, nullptr, 0, false,
+                           work[i], s);
+        if (rc) return rc;
+        return launch_keys_to_results(keys[i].as<uint64_t>(), (int64_t)B[i] * K[i], ix.inv, ix.id_base, out_d2[i],
+                                      out_id[i], out_pos[i], s);
+    };
+    for (int i = 0; i < nc; i++) {
+        lean[i] = B[i] > 0 && B[i] <= 8192 && tc_all_for(ix, qc, K[i]);
+        if (!lean[i]) continue;
+        SSB_CUDA(keys[i].alloc(8 * (size_t)B[i] * K[i], s));
+        const int rc = submit(i);
+        if (rc) return rc;
+    }
+    for (int i = 0; i < nc; i++) {
+        bool redo = false;
+        while (lean[i]) {
+            bool retry = false;
+            int rc = tc_check(work[i], &retry, &redo, s);
+            if (rc) return rc;
+            if (!retry) break;
+            rc = submit(i);
+            if (rc) return rc;
+        }
+        if (!lean[i] || redo) {
+            const int rc = index_query(ix, qc, Q[i], B[i], K[i], ix.id_base, out_d2[i], out_id[i], out_pos[i],
+                                       nullptr, s);
+            if (rc) return rc;
+        }
+    }
+    return OK;
 }
 
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
@@ -1009,9 +1111,7 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
     const int n = ix.n;
     // every query on the tensor-core filter: forced, or (auto) when the dense
     // filter over all N rows costs less than the seed scan of one average leaf
-    const double avg_leaf = (double)ix.N / (double)std::max(1, ix.L);
-    const bool tc_all = ix.Xb && k <= TC_KTOP_MAX &&
-                        (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    const bool tc_all = tc_all_for(ix, qc, k);
     uint32_t leaves_nonempty = 0;
     for (int32_t l : ix.leaves) leaves_nonempty += ix.nodes[l].count > 0 ? 1u : 0u;
     // statistic-rounding slack: delta * sqrt(2n) in distance

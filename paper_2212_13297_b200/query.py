@@ -172,6 +172,39 @@ class QueryEngine:
                   stats.ctypes.data_as(_lib.P) if want_stats else None, stream_handle())
         return (d2, ids, pos, stats) if want_stats else (d2, ids, pos)
 
+    def knn_device_multi(self, calls, eapca_th: float = 0.25, route: str = "auto"):
+        """Several query blocks in one call: ``calls`` = [(Q, k), ...] ->
+        [(d2, ids, pos), ...] CUDA tensors, each as ``knn_device(Q, k)``.
+        The blocks are enqueued back to back with one host round trip for all
+        of them (ssb_query_multi) instead of one per block."""
+        import ctypes as _ct
+
+        from . import _lib
+        from ._device import device_f32, ptr, require_cuda, stream_handle
+
+        t = require_cuda()
+        if route not in self.ROUTES:
+            raise UsageError(f"route must be one of {sorted(self.ROUTES)}")
+        nc = len(calls)
+        Xs, outs = [], []
+        for Q, k in calls:
+            if k < 1:
+                raise UsageError("k must be at least 1")
+            X = device_f32(Q, self.settings.series_length)
+            B = X.shape[0]
+            Xs.append(X)
+            outs.append((t.empty((B, k), dtype=t.float32, device=X.device),
+                         t.empty((B, k), dtype=t.int64, device=X.device),
+                         t.empty((B, k), dtype=t.int64, device=X.device)))
+        P = _ct.c_void_p * max(1, nc)
+        I = _ct.c_int32 * max(1, nc)
+        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route])
+        _lib.call("ssb_query_multi", self._si.handle, nc, P(*[X.data_ptr() for X in Xs]),
+                  I(*[X.shape[0] for X in Xs]), I(*[int(k) for _, k in calls]), _ct.byref(cfg),
+                  P(*[o[0].data_ptr() for o in outs]), P(*[o[1].data_ptr() for o in outs]),
+                  P(*[o[2].data_ptr() for o in outs]), stream_handle())
+        return outs
+
     def exact_knn_arrays(self, queries, k: int, eapca_th: float = 0.25):
         """Batched public form over HOST buffers: (d2, ids, pos) numpy arrays
         (B, k); the H2D copy of the queries and the D2H copy of the answers

@@ -172,3 +172,44 @@ def test_non_finite_queries_rejected(ssb, route, bad):
     Q[3, 17] = bad
     with pytest.raises(ssb.UsageError):
         ssb.QueryEngine(idx).knn_device(Q, 3, route=route)
+
+
+@pytest.mark.parametrize("route", ["auto", "tree"])
+def test_query_multi_equals_separate_calls(ssb, oracle, route):
+    """ssb_query_multi: blocks with different k (and an empty one) enqueued
+    together answer exactly like one call per block (lean tensor-core path for
+    route auto, the general path for route tree)."""
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(20_000, 256, 4, workers=4)
+    s = ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=1000)
+    eng = ssb.QueryEngine(ssb.build_index_array(X, s))
+    Q1 = G.noise_queries(X, 50, 0.1, 5)
+    Q2 = G.noise_queries(X, 70, 1.0, 6)
+    calls = [(Q1, 1), (Q2, 10), (Q1[:0], 3), (Q2[:9], 100)]
+    outs = eng.knn_device_multi(calls, route=route)
+    for (Q, k), (d2, ids, pos) in zip(calls, outs):
+        assert d2.shape == (len(Q), k)
+        if len(Q) == 0:
+            continue
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+        e2, eid, epos = eng.knn_device(Q, k, route=route)
+        assert np.array_equal(pos.cpu().numpy(), epos.cpu().numpy())
+
+
+def test_query_multi_overflow_retry(ssb, oracle, monkeypatch):
+    """A candidate-buffer overflow inside a multi call is retried per block."""
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(8000, 128, 8, workers=2)
+    s = ssb.IndexSettings(series_length=128, dataset_size=len(X), leaf_threshold=500)
+    eng = ssb.QueryEngine(ssb.build_index_array(X, s))
+    Q = G.noise_queries(X, 40, 1.0, 9)
+    monkeypatch.setenv("SSB_TEST_TC_CAP", "64")
+    outs = eng.knn_device_multi([(Q, 5), (Q[:7], 1)], route="tensor")
+    for (Qc, k), (d2, ids, _) in zip([(Q, 5), (Q[:7], 1)], outs):
+        od2, oid = oracle.knn_scan(X, Qc, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
