@@ -1,19 +1,26 @@
 """bench.py -- exact k-NN data-series search on B200.
 
-Default workload = BASELINE.json configs[1] ("c2"): 1M random-walk series x 256
-(float32, z-normalised, reference generator recipe, seed 0); 1000 noisy queries
-per sigma in {0.01, 0.1, 1.0} (seed 1); k in {1, 10}.  One step answers the
-whole workload (3 sigmas x 2 k x 1000 queries = 6000 exact k-NN answers).
-Other BASELINE.json configs: --workload c1 | c3 | c4 | c5 (explicit runs).
+Default workload = BASELINE.json configs[3] ("c4"), the largest configuration
+that is a query workload on one GPU: 25M random-walk series x 256 (float32,
+z-normalised, the reference generator's recipe, seed 0); 1000 noisy queries
+(sigma = 0.1, seed 1), k = 100, leaf threshold 10^4.  One step answers the
+whole workload.  Other configs: --workload c1 | c2 | c3 | c5.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2]
+                    [--workload c4]
 
-Multi-GPU (torchrun, one rank per GPU): the dataset is row-sharded (each rank
+Multi-GPU: one rank per GPU.  Launched by torchrun (RANK/WORLD_SIZE set) or,
+with ``--gpus N`` and no WORLD_SIZE, this script re-launches itself under
+``torch.distributed.run`` with N ranks.  The dataset is row-sharded (each rank
 generates and indexes only its shard), every rank answers every query over its
-shard, and the per-shard top-k lists are merged with one NCCL all-gather and
-the K-merge kernel (strong scaling: the dataset is fixed).
-Prints ONE JSON line on rank 0.
+shard, and inside the timed step the per-shard top-k lists are packed on the
+device, all-gathered (NCCL) and merged by the K-merge kernel (strong scaling:
+the dataset is fixed).  Prints ONE JSON line on rank 0.
+
+The answers are checked: the oracle's exact scan (test infrastructure, run
+only here in the cpu_baseline leg, as the checker) answers a bounded sample of
+the same queries, and the line carries "parity": {"checked", "mismatches"};
+any mismatch exits non-zero.
 """
 
 from __future__ import annotations
@@ -21,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -52,8 +60,9 @@ def make_workload(name: str, args) -> Workload:
     nq = args.queries
     if name == "c1":
         N, n = args.rows or 100_000, 256
-        cells = [("random-walk queries, seed 1", lambda: G.random_walks(100, n, 1, workers=1), 1)]
-        return Workload("c1", f"C1: {N} x {n} random walks (seed 0), 100 random-walk queries "
+        q1 = min(nq, 100)
+        cells = [("random-walk queries, seed 1", lambda: G.random_walks(q1, n, 1, workers=1), 1)]
+        return Workload("c1", f"C1: {N} x {n} random walks (seed 0), {q1} random-walk queries "
                               f"(seed 1), k=1, tau={args.tau or 1000}", N, n, args.tau or 1000, cells,
                         lambda lo, hi: G.random_walks(hi - lo, n, 0, start=lo))
     if name == "c2":
@@ -87,13 +96,13 @@ def make_workload(name: str, args) -> Workload:
     raise SystemExit(f"unknown workload {name}")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="c2", choices=("c1", "c2", "c3", "c4", "c5"))
+    ap.add_argument("--workload", default="c4", choices=("c1", "c2", "c3", "c4", "c5"))
     ap.add_argument("--rows", type=int, default=0, help="override the dataset size")
     ap.add_argument("--queries", type=int, default=1000)
     ap.add_argument("--tau", type=int, default=0, help="override the leaf threshold")
@@ -101,12 +110,58 @@ def parse():
     ap.add_argument("--per-cell", action="store_true",
                     help="one call per (sigma, k) cell instead of one call per k with the cells' queries batched")
     ap.add_argument("--engine", default="index", choices=("index", "bruteforce"))
-    ap.add_argument("--cpu-sample", type=int, default=4, help="queries per cell for the CPU baseline")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="CPU baseline + parity sample: oracle queries until about this many seconds")
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="fixed number of sampled queries per cell (overrides --cpu-seconds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-multi", action="store_true", help="one ssb_query per call (not ssb_query_multi)")
     ap.add_argument("--ingest-gb", type=float, default=4.0,
                     help="file -> HBM ingest sample (GB of the shard; 0 = skip), reported under build.ingest")
-    return ap.parse_args()
+    ap.add_argument("--backend", default="nccl", choices=("nccl", "gloo"),
+                    help="torch.distributed backend (gloo: CPU tests of the multi-rank plumbing)")
+    return ap.parse_args(argv)
+
+
+# --------------------------------------------------------------------------
+# host facts
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def load_peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def ref_build_baseline(N: int, n: int, tau: int):
+    """The reference's own build (pure Python) measured on the builder
+    container by tools/ref_build_probe.py (committed: profiles/ref_build_cpu.jsonl;
+    the reference is not installed on the GPU box), extrapolated linearly to N."""
+    try:
+        rows = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "ref_build_cpu.jsonl")) if l.strip()]
+    except (OSError, ValueError):
+        return None
+    rows = [r for r in rows if r.get("n") == n] or rows
+    if not rows:
+        return None
+    r = min(rows, key=lambda r: (abs(np.log(max(r["tau"], 1) / max(tau, 1))), -r["rows"]))
+    return {"value": r["series_per_s"], "unit": "series/s", "cores": r["num_threads"], "kind": "reference",
+            "sample": f"reference build_index (build.py:363-458, pure Python, num_threads={r['num_threads']}) "
+                      f"of {r['rows']} x {r['n']} random walks, tau={r['tau']}: {r['build_s']} s on the "
+                      f"builder container ({r['cores']} cores, {r['cpu_model']}); committed measurement "
+                      f"(profiles/ref_build_cpu.jsonl), not re-run on this host",
+            "extrapolated_s_for_this_shard": round(N / r["series_per_s"], 1)}
 
 
 # --------------------------------------------------------------------------
@@ -117,12 +172,15 @@ class Clocks:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int = 0):
+    def __init__(self, index: int = 0, enabled: bool = True):
         self.index = index
+        self.enabled = enabled
         self.proc = None
         self.lines: list[str] = []
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -166,6 +224,74 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------
+# device plumbing: CUDA events on the launching stream (the product), or host
+# clocks for the CPU test of the multi-rank plumbing (SSB_BENCH_TEST_ENGINE)
+
+class CudaDev:
+    cuda = True
+
+    def __init__(self, local):
+        import torch
+
+        self.torch = torch
+        torch.cuda.set_device(local)
+        self.device = torch.device("cuda", local)
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def region(self):
+        t = self.torch
+        ev0, ev1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        stream = t.cuda.current_stream()
+
+        class R:
+            def start(self):
+                ev0.record(stream)
+
+            def stop(self):
+                ev1.record(stream)
+                t.cuda.synchronize()
+                return ev0.elapsed_time(ev1)
+        return R()
+
+    def upload(self, arr):
+        return self.torch.from_numpy(arr).to(self.device)
+
+    def pinned(self, arr):
+        return self.torch.from_numpy(arr).pin_memory()
+
+
+class HostDev:
+    """CPU-only stand-in (tests of the multi-rank plumbing, gloo): host clocks."""
+    cuda = False
+
+    def __init__(self, local):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device("cpu")
+
+    def sync(self):
+        pass
+
+    def region(self):
+        class R:
+            def start(self):
+                self.t0 = time.perf_counter()
+
+            def stop(self):
+                return 1000.0 * (time.perf_counter() - self.t0)
+        return R()
+
+    def upload(self, arr):
+        return self.torch.from_numpy(arr)
+
+    def pinned(self, arr):
+        return self.torch.from_numpy(arr)
+
+
+# --------------------------------------------------------------------------
 # engines
 
 class BruteForceEngine:
@@ -185,10 +311,6 @@ class BruteForceEngine:
 
         return knn_batch(self.X, Q_dev, k, id_base=self.id_base)
 
-    def query_host(self, Q_host, k):
-        d2, ids = self.query(Q_host, k)
-        return d2.cpu().numpy(), ids.cpu().numpy()
-
 
 class IndexEngine:
     """The product path: level-synchronous GPU build, then batched exact
@@ -201,7 +323,7 @@ class IndexEngine:
     def __init__(self, X_dev, tau: int, id_base: int = 0, route: str = "auto"):
         import torch
 
-        from paper_2212_13297_b200 import IndexSettings, QueryEngine, build_index_array
+        from paper_2212_13297_b200 import IndexSettings, QueryEngine, _lib, build_index_array
 
         s = IndexSettings(series_length=X_dev.shape[1], dataset_size=X_dev.shape[0], leaf_threshold=tau)
         # warm-up build on a small prefix: module loading and pool growth stay out of
@@ -210,8 +332,6 @@ class IndexEngine:
         build_index_array(X_dev[:w], IndexSettings(series_length=X_dev.shape[1], dataset_size=w,
                                                    leaf_threshold=min(tau, max(1, w // 4))))
         torch.cuda.synchronize()
-        from paper_2212_13297_b200 import _lib
-
         _lib.prof_reset()
         _lib.prof_enable(True)  # per-kernel CUDA events of the build (ProfScope)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -243,10 +363,7 @@ class IndexEngine:
             name = "build_stats" if "build_stats" in self.build_prof else max(
                 self.build_prof.items(), key=lambda kv: kv[1][0])[0]
             kms, klaunch, kbytes, _ = self.build_prof[name]
-            try:
-                peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0))
-            except OSError:
-                peak = 6650.0
+            peak = float(load_peaks().get("hbm_gbs", 6650.0))
             gbs = kbytes / (kms / 1000.0) / 1e9
             out["roofline"] = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
                                "unit": "GB/s", "frac": round(gbs / peak, 4), "share_of_build": round(
@@ -258,67 +375,97 @@ class IndexEngine:
         d2, ids, _ = self.engine.knn_device(Q_dev, k, route=self.route)
         return d2, ids
 
-    def query_host(self, Q_host, k):
-        d2, ids, _ = self.engine.knn_device(Q_host, k, route=self.route)
-        return d2.cpu().numpy(), ids.cpu().numpy()
-
     def query_multi(self, calls):
         """All of a step's calls (different k) through one ssb_query_multi."""
         return [(d2, ids) for d2, ids, _ in self.engine.knn_device_multi(calls, route=self.route)]
 
 
-def merge_shards(d2, ids, k):
-    """One NCCL all-gather of every rank's top-k keys + the K-merge kernel."""
-    from paper_2212_13297_b200.distributed import merge_topk
+def test_engine():
+    """SSB_BENCH_TEST_ENGINE=module:Class -> a CPU engine for the plumbing tests."""
+    spec = os.environ.get("SSB_BENCH_TEST_ENGINE")
+    if not spec:
+        return None
+    import importlib
 
-    return merge_topk(d2, ids, k)
+    mod, cls = spec.split(":")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    return getattr(importlib.import_module(mod), cls)
 
 
 # --------------------------------------------------------------------------
-# reference arm: the oracle port timed on host cores
+# the oracle leg: CPU baseline + parity checker (the only place bench.py runs
+# oracle/, and only as the checker)
 
-def cpu_baseline(wl: Workload, X, cellq, sample: int):
+def oracle_sample(wl: Workload, X, cellq, sample: int, seconds: float, threads: int):
+    """Oracle answers of a bounded sample of every cell's queries (round robin
+    over the cells until `seconds` of CPU work, or `sample` per cell).
+    Returns ([(cell, j, k, d2 row, ids row)], seconds, queries)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
-    threads = os.cpu_count() or 1
+    out = []
     t0 = time.perf_counter()
-    nq = 0
-    for (_, _, k), Q in zip(wl.cells, cellq):
-        oracle.knn_scan(X, Q[:sample], k, threads=threads)
-        nq += min(sample, len(Q))
-    dt = time.perf_counter() - t0
-    return {"value": nq / dt, "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"{nq} queries ({sample} per cell) of workload {wl.name} through the C "
-                      f"oracle's exact scan (pscan.py:23-135 restated, {threads} threads)",
-            "seconds": dt}
+    j = 0
+    while True:
+        for c, ((_, _, k), Q) in enumerate(zip(wl.cells, cellq)):
+            if j < len(Q):
+                d2, ids = oracle.knn_scan(X, Q[j:j + 1], k, threads=threads)
+                out.append((c, j, k, d2[0], ids[0]))
+        j += 1
+        el = time.perf_counter() - t0
+        if sample:
+            if j >= sample:
+                break
+        elif el >= seconds or j >= max(len(Q) for Q in cellq):
+            break
+    return out, time.perf_counter() - t0
+
+
+def check_parity(answers, gpu_rows):
+    """answers: oracle rows; gpu_rows(cell, j) -> (d2 row, ids row) of our path.
+    Ids equal and d2 bit-equal (ties to the lowest original index)."""
+    bad = []
+    for c, j, k, od2, oid in answers:
+        gd2, gid = gpu_rows(c, j)
+        if not (np.array_equal(np.asarray(gid), oid) and
+                np.array_equal(np.asarray(gd2, np.float32).view(np.uint32), od2.view(np.uint32))):
+            bad.append({"cell": c, "query": j})
+    return {"checked": len(answers), "mismatches": len(bad), "first": bad[:5],
+            "rule": "ids identical to the oracle's exact scan (pscan.py:23-30 brute_force_knn, ties to the "
+                    "lowest index), squared distances bit-identical"}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (the oracle port of pscan's
+    exact scan; the reference itself is pure Python and not installed on the
+    GPU box) on all host cores, each step a bounded sample of the workload."""
     if rank != 0:
         return
     wl = make_workload(args.workload, args)
     X = wl.data_fn(0, wl.N)
     cellq = [fn() for _, fn, _ in wl.cells]
+    threads = os.cpu_count() or 1
+    per_step = args.cpu_sample or 0
+    secs = args.cpu_seconds / 2 if not per_step else 0
     for _ in range(args.warmup):
-        cpu_baseline(wl, X, cellq, 1)
-    vals = []
+        oracle_sample(wl, X, cellq, 1, 0, threads)
+    nq, tot = 0, 0.0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline(wl, X, cellq, args.cpu_sample))
+        ans, dt = oracle_sample(wl, X, cellq, per_step, secs, threads)
+        nq += len(ans)
+        tot += dt
     total = time.perf_counter() - t0
-    nq = sum(v["value"] * v["seconds"] for v in vals)
-    value = nq / sum(v["seconds"] for v in vals)
-    cb = dict(vals[-1])
-    cb["value"] = value
-    cb.pop("seconds", None)
+    value = nq / tot
+    cb = {"value": value, "unit": "queries/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+          "sample": f"{nq} queries over {args.steps} steps (round robin over the cells) of workload {wl.name} "
+                    f"through the C oracle's exact scan (pscan.py:23-135 restated, {threads} threads)"}
     line = {
         "impl": "reference", "metric": "exact kNN queries/s", "value": value, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator recipe)",
-        "config": {"workload": wl.desc + f"; each step is a bounded sample of {args.cpu_sample} "
-                                         "queries per cell"},
+        "config": {"workload": wl.desc + "; each step is a bounded sample of the workload's queries"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -327,24 +474,50 @@ def run_reference(args, rank, world):
 
 # --------------------------------------------------------------------------
 
+def relaunch(args) -> int:
+    """--gpus N without WORLD_SIZE: run this script under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    sys.exit(run_ours(args, rank, world))
 
+
+def run_ours(args, rank, world) -> int:
     import torch
 
     local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
+    TestEngine = test_engine()
+    dev = HostDev(local) if TestEngine else CudaDev(local)
+    comm = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2212_13297_b200 import _lib
-    from paper_2212_13297_b200.distributed import shard_range
+        if dev.cuda and args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev.device)
+        else:
+            dist.init_process_group("gloo")
+        # the communicator's rank count, checked with one collective
+        one = torch.ones(1, device=dev.device)
+        dist.all_reduce(one)
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "allreduce_ranks": int(one.item())}
+    from paper_2212_13297_b200.distributed import merge_topk, shard_range
 
     wl = make_workload(args.workload, args)
     N = wl.N
@@ -354,38 +527,280 @@ def main():
     cellq = [fn() for _, fn, _ in wl.cells]
     t_gen = time.perf_counter() - t_gen
     X_dev = None
-    ingest = None
-    if args.ingest_gb > 0:
-        # file -> pinned double buffer -> HBM (ssb_ingest_file), on a sample of
-        # the shard written to a local file first (page cache: the pipeline, not
-        # the disk, is measured); a sample covering the whole shard becomes X_dev
-        import tempfile
+    ingest = device_gen = None
+    if dev.cuda:
+        X_dev, ingest = ingest_sample(args, X, wl)
+        if X_dev is None:
+            X_dev = dev.upload(X)
+        device_gen = device_gen_sample(args, X, wl, lo)
+    else:
+        X_dev = dev.upload(X)
+    # the calls of one step: every cell's queries are answered; cells with the
+    # same k are batched into one call unless --per-cell (same queries, same
+    # answers: the batch size is the engine's choice, the API takes any B).
+    # where[c] = (call index, first row of cell c inside that call)
+    calls, where = [], []
+    for (_, _, k), Q in zip(wl.cells, cellq):
+        i = next((i for i, c in enumerate(calls) if c[0] == k), None) if not args.per_cell else None
+        if i is None:
+            calls.append((k, []))
+            i = len(calls) - 1
+        where.append((i, sum(len(q) for q in calls[i][1])))
+        calls[i][1].append(Q)
+    calls = [(k, np.concatenate(qs)) for k, qs in calls]
+    Q_dev = [(k, dev.upload(Q)) for k, Q in calls]
+    if TestEngine:
+        engine = TestEngine(X_dev, wl.tau, id_base=lo)
+    elif args.engine == "index":
+        engine = IndexEngine(X_dev, wl.tau, id_base=lo, route=args.route)
+    else:
+        engine = BruteForceEngine(X_dev, id_base=lo)
+    batch = wl.batch
+    merge_fn = getattr(engine, "merge_fn", None)
 
-        from paper_2212_13297_b200 import ingest_file
+    def merged(d2, ids, k):
+        if world == 1:
+            return d2, ids
+        return merge_topk(d2, ids, k, merge_fn=merge_fn)
 
-        rows = int(min(len(X), max(1, args.ingest_gb * 1e9 // (4 * wl.n))))
-        fd, path = tempfile.mkstemp(suffix=".bin")
+    # every call of a step through one multi-call (one host round trip per step
+    # instead of one per call); --no-multi answers them one ssb_query each
+    multi = not batch and hasattr(engine, "query_multi") and not args.no_multi
+
+    def step(qs):
+        """Answer every call of the step (shard top-k, then the merge at N > 1)."""
+        if multi:
+            outs = engine.query_multi([(Q, k) for k, Q in qs])
+            return [merged(d2, ids, k) for (k, _), (d2, ids) in zip(qs, outs)]
+        res = []
+        for k, Q in qs:
+            chunks = [Q] if not batch else [Q[i:i + batch] for i in range(0, len(Q), batch)]
+            parts = [merged(*engine.query(c, k), k) for c in chunks]
+            res.append(parts[0] if len(parts) == 1 else
+                       tuple(torch.cat([p[i] for p in parts]) for i in range(2)))
+        return res
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev.device if args.backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_ranks(v: float) -> list:
+        if world == 1:
+            return [v]
+        t = torch.tensor([v], dtype=torch.float64, device=dev.device if args.backend == "nccl" else "cpu")
+        out = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(out, t)
+        return [float(x.item()) for x in out]
+
+    for _ in range(args.warmup):
+        step(Q_dev)
+    dev.sync()
+
+    # ---- timed region (device-timed, max over ranks) -------------------------
+    from paper_2212_13297_b200 import _lib
+
+    if dev.cuda:
+        _lib.prof_reset()
+        _lib.prof_enable(True)
+        launches0 = _lib.launch_count()
+    region = dev.region()
+    with Clocks(local, enabled=dev.cuda) as clk:
+        barrier()
+        dev.sync()
+        region.start()
+        for _ in range(args.steps):
+            step(Q_dev)
+        ms_local = region.stop()
+        barrier()
+    prof, launches = {}, 0
+    if dev.cuda:
+        launches = _lib.launch_count() - launches0
+        _lib.prof_enable(False)
+        prof = _lib.prof_read()
+    ms = max_over_ranks(ms_local)
+    answers = sum(len(Q) for Q in cellq)
+    value = answers * args.steps / (ms / 1000.0)
+    # load balance: each rank's dominant-kernel time over the timed region
+    top_name = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    per_rank_ms = all_ranks(prof[top_name][0] if top_name else ms_local)
+
+    # ---- e2e: the public API with host buffers, copies inside the region ------
+    Q_host = [(k, dev.pinned(Q)) for k, Q in calls]
+    h2d = sum(Q.numel() * 4 for _, Q in Q_host)
+    d2h = sum(len(Q) * k * (4 + 8) for k, Q in calls)
+    barrier()
+    dev.sync()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        outs = step(Q_host)
+        host = [(d2.cpu().numpy(), ids.cpu().numpy()) for d2, ids in outs]
+    dev.sync()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = answers * args.steps / e2e_s
+
+    # ---- parity (and, at N = 1, the CPU baseline) through the oracle ----------
+    parity = cb = None
+    if not args.no_cpu_baseline:
+        threads = max(1, (os.cpu_count() or 1) // world)
+        # the same sample on every rank: each rank's oracle answers over its
+        # shard (global ids), merged like the GPU answers
+        budget = args.cpu_seconds if world == 1 else args.cpu_seconds / 2
+        sample = args.cpu_sample
+        if world > 1 and not sample:
+            sample = 2  # every rank must sample the same queries
+        ans, secs = oracle_sample(wl, X, cellq, sample, budget, threads)
+        if world > 1:
+            from paper_2212_13297_b200.distributed import pack_keys, gather_keys, host_merge
+
+            glob = []
+            for c, j, k, od2, oid in ans:
+                oid = np.where(oid >= 0, oid + lo, -1)
+                keys = torch.from_numpy(pack_keys(od2[None, :], oid[None, :]))
+                allk = gather_keys(keys.to(dev.device) if args.backend == "nccl" else keys)
+                gd2, gid = host_merge(allk.cpu(), k)
+                glob.append((c, j, k, gd2[0], gid[0]))
+            ans = glob
+
+        def gpu_rows(c, j):
+            i, off = where[c]
+            return host[i][0][off + j], host[i][1][off + j]
+
+        parity = check_parity(ans, gpu_rows)
+        if world == 1:
+            cb = {"value": len(ans) / secs, "unit": "queries/s", "cores": threads, "kind": "port",
+                  "cpu_model": cpu_model(),
+                  "sample": f"{len(ans)} queries (round robin over the {len(wl.cells)} cells, about "
+                            f"{args.cpu_seconds:.0f} s) of workload {wl.name} through the C oracle's exact scan "
+                            f"(pscan.py:23-135 restated, {threads} threads); the same queries are the parity sample",
+                  "build": ref_build_baseline(hi - lo, wl.n, wl.tau)}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0 if not parity or parity["mismatches"] == 0 else 3
+
+    # ---- roofline of the dominant kernel ---------------------------------------
+    peaks = load_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    roof = None
+    if top_name:
+        kms, klaunch, kbytes, kflops = prof[top_name]
+        avg_s = (kms / klaunch) / 1000.0
+        long_region = ms >= 1000.0
+        if kflops > 0:  # tensor-core kernel: FLOPs against the measured bf16 peak
+            burst = float(peaks.get("bf16_tflops", 1590.0))
+            sust = float(peaks.get("bf16_tflops_sustained", burst))
+            tf_peak = sust if long_region else burst
+            achieved = (kflops / klaunch) / avg_s / 1e12
+            roof = {"kernel": top_name, "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_peak,
+                    "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": None,
+                    "frac_vs_burst": round(achieved / burst, 4), "frac_vs_sustained": round(achieved / sust, 4),
+                    "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (timed region >= 1 s)" if long_region
+                                    else "MEASURED_PEAKS.json bf16_tflops (burst; timed region < 1 s)")
+                    if peaks else "fallback 1.59 PF",
+                    # bf16 operand bytes the launch feeds the tensor cores (each row once per
+                    # 256-query cluster) per second: NOT a DRAM rate (see traffic)
+                    "operand_GBps": round((kbytes / klaunch) / avg_s / 1e9, 1)}
+        else:
+            achieved = (kbytes / klaunch) / avg_s / 1e9
+            roof = {"kernel": top_name, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+        roof.update({"share_of_step": round(kms / ms, 4) if world == 1 else None,
+                     "avg_launch_ms": round(kms / klaunch, 4)})
+        # DRAM traffic per launch of this kernel from a committed `ncu --set full`
+        # capture of the same workload (profiles/traffic.json), when there is one
         try:
-            with os.fdopen(fd, "wb") as f:
-                X[:rows].tofile(f)
-            ingest_file(path, wl.n, 0, rows)  # warm the pinned buffers
-            D, st = ingest_file(path, wl.n, 0, rows)
-        finally:
-            os.unlink(path)
-        ingest = {"GBps": round(st["GBps"], 2), "bytes": st["bytes"], "rows": rows, "of_shard_rows": len(X),
-                  "source": "raw float32 file in the page cache, 64 MB pinned double buffer, "
-                            f"{min(16, os.cpu_count() or 1)} read threads"}
-        if rows == len(X):
-            X_dev = D
-        del D
-    if X_dev is None:
-        X_dev = torch.from_numpy(X).cuda()
-    # device generator (documented Philox stream) on a sample of
-    # the shard size, beside the host generator time (data_gen_s)
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(wl.name, {})
+            if tr.get("kernel") == top_name:
+                roof["traffic"] = tr["bytes_per_launch"]
+                roof["traffic_source"] = tr["source"]
+                roof["dram_GBps"] = round(tr["bytes_per_launch"] / avg_s / 1e9, 1)
+        except (OSError, ValueError, KeyError):
+            pass
+    mean_ms = sum(per_rank_ms) / len(per_rank_ms)
+    line = {
+        "metric": "exact kNN queries/s", "value": round(value, 1), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference generator recipe (seeded Philox streams; see DESIGN.md Inputs)",
+        "config": {"workload": wl.desc, "engine": getattr(engine, "name", type(engine).__name__),
+                   "shards": world,
+                   "calls_per_step": [{"k": k, "queries": len(Q)} for k, Q in calls],
+                   "api": ("QueryEngine.knn_device_multi (ssb_query_multi: one host round trip per step)" if multi
+                           else "QueryEngine.knn_device per call")
+                   + ("; per-shard top-k packed on the device, NCCL all-gather + K-merge inside the step"
+                      if world > 1 else ""),
+                   "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (N * wl.n * 4 / 1e9),
+                   "data_gen_s": round(t_gen, 1)},
+        "roofline": roof,
+        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3),
+                        "TFLOP": round(v[3] / 1e12, 3)} for k, v in prof.items()},
+        "load_balance": {"kernel": top_name or "step", "ms_per_rank": [round(x, 3) for x in per_rank_ms],
+                         "max_over_mean": round(max(per_rank_ms) / mean_ms, 4) if mean_ms > 0 else None},
+        "parity": parity,
+        "cpu_baseline": cb,
+        "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "build": dict(engine.build_info(hi - lo) or {}, **({"ingest": ingest} if ingest else {}),
+                      **({"device_gen": device_gen} if device_gen else {})),
+        "clocks": clk.summary(),
+    }
+    if comm:
+        line["comm"] = comm
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    if parity and parity["mismatches"]:
+        print(f"PARITY FAILURE: {parity['mismatches']} of {parity['checked']} sampled answers differ "
+              f"from the oracle", file=sys.stderr)
+        return 3
+    return 0
+
+
+def ingest_sample(args, X, wl):
+    """file -> pinned double buffer -> HBM (ssb_ingest_file) on a sample of the
+    shard written to a local file first (page cache: the pipeline, not the
+    disk, is measured); a sample covering the whole shard becomes X_dev."""
+    if args.ingest_gb <= 0:
+        return None, None
+    import tempfile
+
+    from paper_2212_13297_b200 import ingest_file
+
+    rows = int(min(len(X), max(1, args.ingest_gb * 1e9 // (4 * wl.n))))
+    fd, path = tempfile.mkstemp(suffix=".bin")
+    try:
+        with os.fdopen(fd, "wb") as f:
+            X[:rows].tofile(f)
+        ingest_file(path, wl.n, 0, rows)  # warm the pinned buffers
+        D, st = ingest_file(path, wl.n, 0, rows)
+    finally:
+        os.unlink(path)
+    info = {"GBps": round(st["GBps"], 2), "bytes": st["bytes"], "rows": rows, "of_shard_rows": len(X),
+            "source": "raw float32 file in the page cache, 64 MB pinned double buffer, "
+                      f"{min(16, os.cpu_count() or 1)} read threads"}
+    return (D if rows == len(X) else None), info
+
+
+def device_gen_sample(args, X, wl, lo):
+    """Device generator (documented Philox stream) on a sample of
+    the shard size, beside the host generator."""
+    import torch
+
     from paper_2212_13297_b200 import generate as _G
 
     g_rows = min(len(X), 4_000_000)
-    g_fn = _G.unit_gaussian_device if args.workload == "c3" else _G.random_walks_device
+    g_fn = _G.unit_gaussian_device if wl.name == "c3" else _G.random_walks_device
     g_fn(1024, wl.n, 0)
     torch.cuda.synchronize()
     g0 = time.perf_counter()
@@ -393,172 +808,7 @@ def main():
     torch.cuda.synchronize()
     g_s = time.perf_counter() - g0
     del g_out
-    device_gen = {"series_per_s": round(g_rows / g_s, 1), "rows": g_rows,
-                  "host_series_per_s": round(len(X) / t_gen, 1) if t_gen > 0 else None}
-    # the calls of one step: every cell's queries are answered; cells with the
-    # same k are batched into one call unless --per-cell (same queries, same
-    # answers: the batch size is the engine's choice, the API takes any B)
-    calls = []
-    for (_, _, k), Q in zip(wl.cells, cellq):
-        if not args.per_cell and calls and calls[-1][0] == k:
-            calls[-1][1].append(Q)
-        elif not args.per_cell and any(c[0] == k for c in calls):
-            next(c for c in calls if c[0] == k)[1].append(Q)
-        else:
-            calls.append((k, [Q]))
-    calls = [(k, np.concatenate(qs)) for k, qs in calls]
-    Q_dev = [(k, torch.from_numpy(Q).cuda()) for k, Q in calls]
-    if args.engine == "index":
-        engine = IndexEngine(X_dev, wl.tau, id_base=lo, route=args.route)
-    else:
-        engine = BruteForceEngine(X_dev, id_base=lo)
-    batch = wl.batch
-
-    def answer(Q, k, host=False):
-        chunks = [Q] if not batch else [Q[i:i + batch] for i in range(0, len(Q), batch)]
-        out = []
-        for c in chunks:
-            if host:
-                out.append(engine.query_host(c, k))
-            else:
-                d2, ids = engine.query(c, k)
-                out.append(merge_shards(d2, ids, k) if world > 1 else ids)
-        return out
-
-    # every call of a step through one multi-call (one host round trip per step
-    # instead of one per call); --no-multi answers them one ssb_query each
-    multi = not batch and hasattr(engine, "query_multi") and not args.no_multi
-
-    def step():
-        if multi:
-            outs = engine.query_multi([(Q, k) for k, Q in Q_dev])
-            return [[merge_shards(d2, ids, k) if world > 1 else ids] for (k, _), (d2, ids) in zip(Q_dev, outs)]
-        return [answer(Q, k) for k, Q in Q_dev]
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    # ---- timed region (device-timed, max over ranks) -------------------------
-    _lib.prof_reset()
-    _lib.prof_enable(True)
-    launches0 = _lib.launch_count()
-    stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    launches = _lib.launch_count() - launches0
-    _lib.prof_enable(False)
-    prof = _lib.prof_read()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    answers = sum(len(Q) for Q in cellq)
-    value = answers * args.steps / (ms / 1000.0)
-
-    # ---- e2e: the public API with host buffers, copies inside the region ------
-    Q_host = [(k, torch.from_numpy(Q).pin_memory()) for k, Q in calls]
-    h2d = sum(Q.numel() * 4 for _, Q in Q_host)
-    d2h = sum(len(Q) * k * (4 + 8) for k, Q in calls)
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        if multi:
-            outs = engine.query_multi([(Qh, k) for k, Qh in Q_host])
-            _ = [(d2.cpu().numpy(), ids.cpu().numpy()) for d2, ids in outs]
-        else:
-            for k, Qh in Q_host:
-                answer(Qh, k, host=True)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = answers * args.steps / e2e_s
-
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
-
-    # ---- roofline of the dominant kernel ---------------------------------------
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    top = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
-    roof = None
-    if top:
-        name, (kms, klaunch, kbytes, kflops) = top
-        avg_s = (kms / klaunch) / 1000.0
-        if kflops > 0:  # tensor-core kernel: FLOPs against the measured bf16 peak
-            tf_peak = float(peaks.get("bf16_tflops", 1590.0))
-            achieved = (kflops / klaunch) / avg_s / 1e12
-            roof = {"kernel": name, "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_peak,
-                    "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": None,
-                    "hbm_GBps": round((kbytes / klaunch) / avg_s / 1e9, 1),
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF"}
-        else:
-            achieved = (kbytes / klaunch) / avg_s / 1e9
-            roof = {"kernel": name, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
-        roof.update({"share_of_step": round(kms / ms, 4), "avg_launch_ms": round(kms / klaunch, 4)})
-        # DRAM traffic per launch of this kernel from a committed `ncu --set full`
-        # capture of the same workload (profiles/traffic.json), when there is one
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(wl.name, {})
-            if tr.get("kernel") == name:
-                roof["traffic"] = tr["bytes_per_launch"]
-                roof["traffic_source"] = tr["source"]
-        except (OSError, ValueError, KeyError):
-            pass
-    cb = None
-    if not args.no_cpu_baseline and world == 1:
-        cb = cpu_baseline(wl, X, cellq, args.cpu_sample)
-        cb.pop("seconds", None)
-    line = {
-        "metric": "exact kNN queries/s", "value": round(value, 1), "unit": "queries/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: reference generator recipe (seeded Philox streams; see DESIGN.md Inputs)",
-        "config": {"workload": wl.desc, "engine": engine.name, "shards": world,
-                   "calls_per_step": [{"k": k, "queries": len(Q)} for k, Q in calls],
-                   "api": "QueryEngine.knn_device_multi (ssb_query_multi: one host round trip per step)" if multi else "QueryEngine.knn_device per call",
-                   "l2": "inputs larger than L2 (dataset %.2f GB > 126 MB)" % (N * wl.n * 4 / 1e9),
-                   "data_gen_s": round(t_gen, 1)},
-        "roofline": roof,
-        "kernels": {k: {"ms": round(v[0], 3), "launches": v[1], "GB": round(v[2] / 1e9, 3),
-                        "TFLOP": round(v[3] / 1e12, 3)} for k, v in prof.items()},
-        "cpu_baseline": cb,
-        "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "build": dict(engine.build_info(hi - lo), **({"ingest": ingest} if ingest else {}),
-                      device_gen=device_gen),
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    return {"series_per_s": round(g_rows / g_s, 1), "rows": g_rows}
 
 
 if __name__ == "__main__":

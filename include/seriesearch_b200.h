@@ -150,25 +150,37 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
 /* ---- K-lbe + K-lbs + K-scan + K-select: exact k-NN over the index ------- */
 
 /* Exact k-NN of B device-resident queries.  Replaces query.py:296-348
- * QueryEngine.exact_knn (one call answers the block).  out_d2/out_id/out_pos:
- * B x k device arrays (id = original index incl. id_base, pos = leaf-order
- * position); stats_host (nullable): B x 4 uint32 host array receiving
- * (candidate leaves, candidate series, seed-leaf rows, 0) per query.
- * Reads per-batch candidate counts / overflow flags back (host round trips
- * inside the call); the outputs are complete in `stream` order when it
- * returns (no final synchronization). */
+ * QueryEngine.exact_knn (one call answers the block): LB_EAPCA of every leaf,
+ * an approximate phase over the best leaves (the bound), LB_EAPCA leaf pruning,
+ * LB_SAX series pruning and an early-abandoning exact scan -- or, per query,
+ * the tensor-core filter + exact rescoring when the cost model says so.
+ * out_d2/out_id/out_pos: B x k device arrays (id = original index incl.
+ * id_base, pos = leaf-order position).  stats_host (nullable): B x
+ * SSB_QUERY_STATS uint32 host array, per query:
+ *   [0] candidate leaves (LB_EAPCA survivors)       [1] candidate series (LB_SAX or filter survivors)
+ *   [2] series scanned exactly by the approximate phase
+ *   [3] 1 if the candidate buffer overflowed once (bound tightened, redone)
+ *   [4] leaves visited by the approximate phase      [5] SAX words tested (index) / rows read (filter)
+ *   [6] series abandoned early by the exact scan     [7] route: 0 index, 1 tensor-core filter
+ * Reads counts / flags back (host round trips inside the call); the outputs
+ * are complete in `stream` order when it returns (no final synchronization). */
+#define SSB_QUERY_STATS 8
+
 typedef struct {
-    /* query.py:45 QueryConfig.eapca_th: a query whose seed bound keeps more than
-     * (1 - eapca_th) of the leaves takes the dense "scan" path (K-tc tensor-core
-     * filter + exact rescoring) instead of LB_SAX + sparse exact scan
-     * (query.py:321-325).  Answers do not depend on it. */
+    /* query.py:45 QueryConfig.eapca_th, used by route 3 (the reference's rule,
+     * query.py:321-325): a query whose bound keeps more than (1 - eapca_th) of
+     * the leaves takes the dense "scan" path (tensor-core filter).  Answers do
+     * not depend on it. */
     float eapca_th;
     /* 0 auto: per query, the cheaper exact path by a B200-calibrated cost model
-     *   (tensor-core filter over N rows vs LB_SAX over the rows of the leaves the
-     *   seed bound keeps; the seed itself is skipped when the dense filter is
-     *   cheaper than it); 1 LB_SAX path only; 2 tensor-core path only;
-     * 3 the reference's eapca_th rule. */
+     *   (LB_SAX over the rows of the leaves the bound keeps vs the tensor-core
+     *   filter's share of one pass over the BF16 rows); 1 index path only;
+     *   2 tensor-core path only (one lean batch, no index stages); 3 the
+     *   reference's eapca_th rule. */
     int32_t route;
+    /* query.py:44 QueryConfig.lmax (>= 1): at most this many leaves are visited
+     * by the approximate phase (it stops earlier once they hold k series). */
+    int32_t lmax;
 } ssb_query_cfg;
 
 int ssb_query(const ssb_index *index, const float *Q, int32_t B, int32_t k, const ssb_query_cfg *cfg,
@@ -190,6 +202,11 @@ int ssb_query_multi(const ssb_index *index, int32_t ncalls, const float *const *
  * ids must fit in 32 bits.  out_d2 / out_id: B x k device arrays. */
 int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2,
                    int64_t *out_id, void *stream);
+
+/* Merge keys of count (d2, id) results (device arrays, e.g. one shard's B x k
+ * answers): key = (float bits of d2 << 32) | id, id < 0 -> UINT64_MAX (empty).
+ * The packing step before the all-gather of SURVEY 8e; ids must fit in 32 bits. */
+int ssb_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, void *stream);
 
 /* K-tc parity hook: S (B x N float32, device) = bf16(Q) . bf16(X)^T computed by
  * the tcgen05 kernel of the tensor-core filter (rows row-major, n <= 256). */

@@ -52,6 +52,7 @@ _SIGS = {
     "ssb_index_lb_eapca": [P, P, I32, P, P],
     "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
     "ssb_merge_topk": [P, I32, I32, I32, P, P, P],
+    "ssb_pack_keys": [P, P, I64, P, P],
     "ssb_ingest_file": [ctypes.c_char_p, I64, I64, I32, P, I64, I32, P, P],
     "ssb_generate": [I32, I64, I64, I32, ctypes.c_uint64, P, P],
 }
@@ -65,7 +66,10 @@ class BuildCfg(ctypes.Structure):
 
 
 class QueryCfg(ctypes.Structure):
-    _fields_ = [("eapca_th", ctypes.c_float), ("route", ctypes.c_int32)]
+    _fields_ = [("eapca_th", ctypes.c_float), ("route", ctypes.c_int32), ("lmax", ctypes.c_int32)]
+
+
+QUERY_STATS = 8  # SSB_QUERY_STATS columns per query
 
 
 class IndexInfo(ctypes.Structure):

@@ -1721,14 +1721,16 @@ int index_from_host(const float *rows, const uint8_t *words, const uint32_t *ori
         SSB_CUDA(cudaStreamSynchronize(s));
     }
     if (orig) {
-        SSB_CUDA(cudaMemcpy(ix->orig, orig, (size_t)N * 4, cudaMemcpyHostToDevice));
+        SSB_CUDA(cudaMemcpyAsync(ix->orig, orig, (size_t)N * 4, cudaMemcpyHostToDevice, s));
     } else {
         iota_u32_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N);
         SSB_CHECK_LAUNCH();
     }
     inv_from_orig_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ix->orig, N, ix->inv);
     SSB_CHECK_LAUNCH();
-    if (words) SSB_CUDA(cudaMemcpy(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice));
+    // stream-ordered on s (the inverse permutation kernel reads orig); the final
+    // synchronize below keeps the caller's host arrays alive until the copies land
+    if (words) SSB_CUDA(cudaMemcpyAsync(ix->words, words, (size_t)N * WORD_SEGMENTS, cudaMemcpyHostToDevice, s));
     uint32_t am = 0;
     SSB_CUDA(cudaMemcpyAsync(&am, amax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));

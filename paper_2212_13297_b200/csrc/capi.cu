@@ -350,8 +350,10 @@ int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, const ss
         SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
         SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
                     "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
+        SSB_REQUIRE(cfg->lmax >= 1, "lmax must be at least 1");
         qc.eapca_th = cfg->eapca_th;
         qc.route = cfg->route;
+        qc.lmax = cfg->lmax;
     }
     return index_query(ix, qc, Q, B, k, ix.id_base, out_d2, out_id, out_pos, stats_host, (cudaStream_t)stream);
 }
@@ -368,8 +370,10 @@ int ssb_query_multi(const ssb_index *h, int32_t ncalls, const float *const *Q, c
         SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
         SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
                     "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
+        SSB_REQUIRE(cfg->lmax >= 1, "lmax must be at least 1");
         qc.eapca_th = cfg->eapca_th;
         qc.route = cfg->route;
+        qc.lmax = cfg->lmax;
     }
     return index_query_multi(ix, qc, ncalls, Q, B, k, out_d2, out_id, out_pos, (cudaStream_t)stream);
 }
@@ -389,6 +393,12 @@ int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float 
                    void *stream)
 {
     return merge_topk(keys, B, m, k, out_d2, out_id, (cudaStream_t)stream);
+}
+
+int ssb_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, void *stream)
+{
+    SSB_REQUIRE(count >= 0, "count must be >= 0");
+    return launch_pack_keys(d2, ids, count, keys, (cudaStream_t)stream);
 }
 
 int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const double *lower, const double *upper,

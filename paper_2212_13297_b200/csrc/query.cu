@@ -1,36 +1,22 @@
-// query.cu -- batched exact k-NN over an HBM-resident index (K-lbe, K-lbs,
-// tile lists, K-scan sparse, K-select with bound tightening).
+// query.cu -- batched exact k-NN over an HBM-resident index: the host side of
+// one query block (ixq.cu's device-driven stages, the tensor-core route for the
+// queries the cost model sends there, K-select with bound tightening), the lean
+// all-tensor-core batch (tc_submit / tc_check) and the multi-call entry.
 //
-// Replaces query.py:296-348 QueryEngine.exact_knn and its phases
-// (approx_knn :167-198, find_candidate_leaves :200-214,
-// find_candidate_series :216-251, compute_results :253-270,
-// skip_sequential_scan :272-292), for a whole block of B queries at once:
-//
-//  A  seed    each query's best leaf by LB_EAPCA is scanned exactly; the k-th
-//             best (d2, id) key is the query's bound (an upper bound on the
-//             true k-th key: it is the k-th of k real distances).
-//  B1 K-lbe   LB_EAPCA of every (query, leaf) (summarize.py:170-181, exact
-//             float64 order); a leaf survives unless its bound provably
-//             exceeds the query's bound (safe test).
-//  B2 K-lbs   LB_SAX (summarize.py:136-153, exact order) of every row of the
-//             surviving leaves, through a per-query 16 x 256 gap table in
-//             shared memory; survivors become (tile, query, 32-bit mask).
-//  B3 entries sorted by (tile, query) -> tile CSR + union masks.
-//  B4 K-scan  exact d2 of the surviving pairs (scan.cu sparse); keys <= the
-//             bound are appended per query.
-//  B5 K-select top-k by (d2, id); a query whose buffer overflowed gets the
-//             k-th stored key as a tighter bound and is rescanned.
-// Ties resolve to the lowest original index, like brute_force_knn.
+// Replaces query.py:296-348 QueryEngine.exact_knn (approx_knn :167-198,
+// find_candidate_leaves :200-214, find_candidate_series :216-251,
+// compute_results :253-270, skip_sequential_scan :272-292) for a whole block of
+// B queries at once.  Ties resolve to the lowest original index, like
+// brute_force_knn (pscan.py:23-30).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
 #include <cstring>
+#include <memory>
 #include <vector>
 
+#include "../../include/seriesearch_b200.h"
 #include "ssb_common.cuh"
 #include "ssb_index.h"
 #include "ssb_internal.h"
@@ -41,364 +27,7 @@ int launch_query_prep(const float *Q, int B, int n, double *cs, double *c2, floa
                       cudaStream_t s);
 
 // ---------------------------------------------------------------------------
-// bounds
-
-// safe keep-test bound (in squared units) for a query whose current k-th key
-// is `thr`: a lower bound LB computed from float32-rounded statistics keeps
-// its element iff LB <= bound (relative slack for float32
-// distance rounding, absolute slack delta*sqrt(2n) for statistic rounding).
-__device__ __forceinline__ double keep_bound(uint64_t thr, double slack_abs)
-{
-    if (thr == KEY_EMPTY) return __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    const double d2 = (double)key_d2(thr);
-    const double r = sqrt(d2) * (1.0 + 1e-5) + slack_abs;
-    return r * r * (1.0 + 1e-12);
-}
-
-// LB_EAPCA of query q against leaf l (query.py:127-135 -> summarize.py:170-181)
-__device__ double lb_eapca_leaf(const double *cs, const double *c2, const int32_t *ep, const float *env,
-                                int m)
-{
-    double t[M_MAX];
-    int sa = 0;
-    for (int i = 0; i < m; i++) {
-        const int sb = ep[i];
-        const double wd = (double)(sb - sa);
-        const double mu = __ddiv_rn(__dsub_rn(cs[sb], cs[sa]), wd);
-        const double msq = __ddiv_rn(__dsub_rn(c2[sb], c2[sa]), wd);
-        const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
-        const double qm = (double)__double2float_rn(mu);
-        const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
-        const double mmin = (double)env[i * 4 + 0], mmax = (double)env[i * 4 + 1];
-        const double smin = (double)env[i * 4 + 2], smax = (double)env[i * 4 + 3];
-        double gm = fmax(__dsub_rn(mmin, qm), __dsub_rn(qm, mmax));
-        gm = fmax(gm, 0.0);
-        double gs = fmax(__dsub_rn(smin, qs), __dsub_rn(qs, smax));
-        gs = fmax(gs, 0.0);
-        t[i] = __dmul_rn(wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
-        sa = sb;
-    }
-    return pw_f64_small(t, m);
-}
-
-// K-lbe: one CTA per query; the query's prefix sums are staged in shared memory
-__global__ void lbe_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n,
-                           int L, const int32_t *__restrict__ leaf_m, const int32_t *__restrict__ leaf_ep,
-                           const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
-                           double *__restrict__ lbe, int32_t *__restrict__ best_leaf)
-{
-    extern __shared__ double sm[];
-    double *cs = sm, *c2 = sm + (n + 1);
-    const int q = blockIdx.x;
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
-        cs[i] = cs_g[(int64_t)q * (n + 1) + i];
-        c2[i] = c2_g[(int64_t)q * (n + 1) + i];
-    }
-    __syncthreads();
-    double bv = __longlong_as_double(0x7ff0000000000000ll);
-    int bl = 0x7fffffff;
-    for (int l = threadIdx.x; l < L; l += blockDim.x) {
-        const double v = lb_eapca_leaf(cs, c2, leaf_ep + (int64_t)l * M_MAX, leaf_env + (int64_t)l * M_MAX * 4,
-                                       leaf_m[l]);
-        lbe[(int64_t)q * L + l] = v;
-        if (leaf_count[l] && (v < bv || (v == bv && l < bl))) {
-            bv = v;
-            bl = l;
-        }
-    }
-    // block argmin (value, then lowest leaf index)
-    __shared__ double rv[32];
-    __shared__ int rl[32];
-    for (int off = 16; off; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
-        if (ov < bv || (ov == bv && ol < bl)) {
-            bv = ov;
-            bl = ol;
-        }
-    }
-    if ((threadIdx.x & 31) == 0) {
-        rv[threadIdx.x >> 5] = bv;
-        rl[threadIdx.x >> 5] = bl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
-            if (rv[w] < bv || (rv[w] == bv && rl[w] < bl)) {
-                bv = rv[w];
-                bl = rl[w];
-            }
-        best_leaf[q] = bl == 0x7fffffff ? -1 : bl;
-    }
-}
-
-// rows of the leaves whose LB_EAPCA equals the query's minimum: every valid
-// bound is >= d(NN) >= min LB, so these rows are candidates of the LB_SAX path
-// whatever the seed finds -- a seed-free lower bound on that path's cost.
-__global__ void floor_rows_kernel(const double *__restrict__ lbe, int L, const uint32_t *__restrict__ leaf_count,
-                                  uint64_t *__restrict__ floor_rows)
-{
-    const int q = blockIdx.x;
-    double mn = __longlong_as_double(0x7ff0000000000000ll);
-    for (int l = threadIdx.x; l < L; l += blockDim.x)
-        if (leaf_count[l]) mn = fmin(mn, lbe[(int64_t)q * L + l]);
-    for (int off = 16; off; off >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-    __shared__ double wm[32];
-    __shared__ unsigned long long wr[32];
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mn;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
-        for (int off = 16; off; off >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, off));
-        if (threadIdx.x == 0) wm[0] = m;
-    }
-    __syncthreads();
-    mn = wm[0];
-    unsigned long long rows = 0;
-    for (int l = threadIdx.x; l < L; l += blockDim.x)
-        if (leaf_count[l] && lbe[(int64_t)q * L + l] <= mn) rows += leaf_count[l];
-    for (int off = 16; off; off >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, off);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) wr[threadIdx.x >> 5] = rows;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wr[w];
-        floor_rows[q] = t;
-    }
-}
-
-// Entry = (tile, query, mask).  Appended with a global counter.
-struct EntryOut {
-    uint64_t *key;   // (tile << 32) | ((32 - popc(mask)) << 26) | query
-    uint32_t *mask;
-    uint32_t *count;
-    int64_t cap;
-};
-
-__device__ __forceinline__ void emit_entry(const EntryOut &eo, uint32_t tile, uint32_t q, uint32_t mask)
-{
-    const uint32_t slot = atomicAdd(eo.count, 1u);
-    if ((int64_t)slot < eo.cap) {
-        eo.key[slot] = ((uint64_t)tile << 32) | ((uint64_t)(32 - __popc(mask)) << 26) | q;
-        eo.mask[slot] = mask;
-    }
-}
-
-// phase A: the tiles of each query's best leaf (all its rows)
-__global__ void seed_entries_kernel(const int32_t *__restrict__ best_leaf, const uint32_t *__restrict__ leaf_first,
-                                    const uint32_t *__restrict__ leaf_count, int B, EntryOut eo,
-                                    uint32_t *__restrict__ seed_rows)
-{
-    const int q = blockIdx.x;
-    const int l = best_leaf[q];
-    if (l < 0) {
-        if (threadIdx.x == 0) seed_rows[q] = 0;
-        return;
-    }
-    const uint32_t a = leaf_first[l], b = a + leaf_count[l];
-    if (threadIdx.x == 0) seed_rows[q] = b - a;
-    for (uint32_t t = a / TILE_ROWS + threadIdx.x; t <= (b - 1) / TILE_ROWS; t += blockDim.x) {
-        const uint32_t r0 = t * TILE_ROWS;
-        const uint32_t lo = a > r0 ? a - r0 : 0;
-        const uint32_t hi = min(b - r0, (uint32_t)TILE_ROWS);
-        const uint32_t mask = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-        emit_entry(eo, t, (uint32_t)q, mask);
-    }
-}
-
-// K-lbs: one CTA per query; per-query gap^2 table T[seg][sym] in shared memory
-// (A.4: g = max(max(lo - q, q - hi), 0), LB = (n/16) * sum g^2).  The hot path
-// keeps the table and the sum in float32 (16 KB, one LDS.32 per lookup): the
-// float32 sum of 16 non-negative terms exceeds the exact float64 value by at
-// most ~17 * 2^-24 relatively, which the keep-bound absorbs (x (1 + 4e-6)), so
-// a row is never dropped that the exact LB_SAX would keep.  Each thread
-// evaluates 4 rows (ILP); survivors become (tile, query, mask) entries.
-constexpr int LBS_ROWS = 4;
-constexpr int TC_KTOP_MAX = 4096;  // the filter tightens its bound for every k (buckets)
-constexpr int LBS_STAGE = 1024;
-
-__global__ void __launch_bounds__(256)
-    lbs_kernel(const float *__restrict__ qpaa, const double *__restrict__ sym_lo, const double *__restrict__ sym_hi,
-               const uint4 *__restrict__ words, int n, int L, const uint32_t *__restrict__ leaf_first,
-               const uint32_t *__restrict__ leaf_count, const double *__restrict__ lbe,
-               const uint64_t *__restrict__ thr, double slack_abs,
-               EntryOut eo, uint32_t *__restrict__ cand_leaves, uint32_t *__restrict__ cand_series,
-               unsigned long long *__restrict__ prof_bytes, const int32_t *__restrict__ qlist)
-{
-    __shared__ float T[WORD_SEGMENTS * ALPHABET];  // 16 KB
-    const int q = qlist ? qlist[blockIdx.x] : blockIdx.x;
-    const double w = (double)(n / WORD_SEGMENTS);
-    for (int i = threadIdx.x; i < WORD_SEGMENTS * ALPHABET; i += blockDim.x) {
-        const int seg = i / ALPHABET, sym = i % ALPHABET;
-        const double qv = (double)qpaa[(int64_t)q * WORD_SEGMENTS + seg];
-        double g = fmax(__dsub_rn(sym_lo[sym], qv), __dsub_rn(qv, sym_hi[sym]));
-        g = fmax(g, 0.0);
-        T[i] = __double2float_rn(__dmul_rn(w, __dmul_rn(g, g)));  // w folded in
-    }
-    __syncthreads();
-    const double bound = keep_bound(thr[q], slack_abs);
-    const float fbound = isinf(bound) ? __int_as_float(0x7f800000)
-                                      : __double2float_ru(bound * (1.0 + 4e-6));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t my_series = 0, my_leaves = 0;
-    unsigned long long my_bytes = 0;
-    // entries are staged per CTA and flushed with ONE global reservation per
-    // LBS_STAGE entries (a single hot counter would serialise millions of atomics)
-    __shared__ uint64_t st_key[LBS_STAGE];
-    __shared__ uint32_t st_mask[LBS_STAGE];
-    __shared__ uint32_t st_n, st_base;
-    if (threadIdx.x == 0) st_n = 0;
-    __syncthreads();
-    auto flush = [&]() {
-        __syncthreads();
-        const uint32_t cnt = min(st_n, (uint32_t)LBS_STAGE);
-        if (threadIdx.x == 0) st_base = cnt ? atomicAdd(eo.count, cnt) : 0u;
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const uint32_t slot = st_base + i;
-            if ((int64_t)slot < eo.cap) {
-                eo.key[slot] = st_key[i];
-                eo.mask[slot] = st_mask[i];
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) st_n = 0;
-        __syncthreads();
-    };
-    for (int l = 0; l < L; l++) {
-        if (!(lbe[(int64_t)q * L + l] <= bound)) continue;  // NaN-safe: prune only if provably above (uniform)
-        const uint32_t a = leaf_first[l], b = a + leaf_count[l];
-        if (a == b) continue;
-        my_leaves++;
-        my_bytes += 16ull * (b - a);
-        const uint32_t t0 = a / TILE_ROWS, t1 = (b - 1) / TILE_ROWS;
-        // the CTA sweeps the leaf in rounds of nw*LBS_ROWS tiles; flush between rounds
-        for (uint32_t base = t0; base <= t1; base += (uint32_t)nw * LBS_ROWS) {
-            if (st_n > LBS_STAGE - (uint32_t)nw * LBS_ROWS) flush();
-            const uint32_t tb = base + (uint32_t)warp * LBS_ROWS;
-            uint4 wv[LBS_ROWS];
-            bool in[LBS_ROWS];
-#pragma unroll
-            for (int u = 0; u < LBS_ROWS; u++) {
-                const uint32_t pos = (tb + u) * TILE_ROWS + lane;
-                in[u] = (tb + u) <= t1 && pos >= a && pos < b;
-                wv[u] = in[u] ? __ldg(words + pos) : make_uint4(0, 0, 0, 0);
-            }
-            float lb[LBS_ROWS];
-#pragma unroll
-            for (int u = 0; u < LBS_ROWS; u++) {
-                const uint32_t wd[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
-                float acc = 0.f;
-#pragma unroll
-                for (int sg = 0; sg < 16; sg++) acc += T[sg * ALPHABET + ((wd[sg >> 2] >> (8 * (sg & 3))) & 0xffu)];
-                lb[u] = acc;
-            }
-#pragma unroll
-            for (int u = 0; u < LBS_ROWS; u++) {
-                const uint32_t mask = __ballot_sync(0xffffffffu, in[u] && lb[u] <= fbound);
-                if (lane == 0 && mask) {
-                    const uint32_t i = atomicAdd(&st_n, 1u);
-                    st_key[i] = ((uint64_t)(tb + u) << 32) | ((uint64_t)(32 - __popc(mask)) << 26) | (uint32_t)q;
-                    st_mask[i] = mask;
-                    my_series += __popc(mask);
-                }
-            }
-            __syncthreads();
-        }
-    }
-    flush();
-    if (lane == 0 && my_series) atomicAdd(&cand_series[q], my_series);
-    if (threadIdx.x == 0) {
-        cand_leaves[q] = my_leaves;
-        if (prof_bytes) atomicAdd(prof_bytes, my_bytes + 8ull * L);
-    }
-}
-
-// after sorting by (tile, query): tile boundaries -> tile list
-__global__ void tile_flags_kernel(const uint64_t *__restrict__ keys, int64_t E, uint32_t *__restrict__ flags)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i > E) return;
-    if (i == E) {
-        flags[i] = 0;
-        return;
-    }
-    flags[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1u : 0u;
-}
-
-__global__ void tile_build_kernel(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ masks,
-                                  int64_t E, const uint32_t *__restrict__ flags, const uint32_t *__restrict__ slot,
-                                  uint32_t *__restrict__ row0, uint32_t *__restrict__ umask,
-                                  uint32_t *__restrict__ eptr, uint2 *__restrict__ entries)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i > E) return;
-    if (i == E) {
-        eptr[slot[E]] = (uint32_t)E;
-        return;
-    }
-    const uint32_t t = (uint32_t)(keys[i] >> 32);
-    const uint32_t s = slot[i] - 1;  // inclusive scan of tile starts -> slot of entry i
-    if (flags[i]) {
-        row0[s] = t * TILE_ROWS;
-        eptr[s] = (uint32_t)i;
-    }
-    atomicOr(&umask[s], masks[i]);
-    entries[i] = make_uint2((uint32_t)(keys[i] & 0x3ffffffu), masks[i]);
-}
-
-__global__ void thr_from_keys_kernel(const uint64_t *__restrict__ keys, int B, int k, uint64_t *__restrict__ thr)
-{
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < B) thr[q] = keys[(int64_t)q * k + k - 1];
-}
-
-__global__ void active_entries_kernel(uint2 *__restrict__ entries, int64_t E, const int32_t *__restrict__ flags,
-                                      uint32_t *__restrict__ keepmask_store)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= E) return;
-    uint2 e = entries[i];
-    if (!flags[e.x]) {
-        keepmask_store[i] = e.y;
-        e.y = 0;
-        entries[i] = e;
-    } else {
-        keepmask_store[i] = e.y;
-    }
-}
-
-__global__ void restore_entries_kernel(uint2 *__restrict__ entries, int64_t E, const uint32_t *__restrict__ keep)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < E) entries[i].y = keep[i];
-}
-
-__global__ void entry_flags_kernel(const uint64_t *__restrict__ keys, int64_t E, const int32_t *__restrict__ qflags,
-                                   uint8_t *__restrict__ eflags)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < E) eflags[i] = qflags[keys[i] & 0x3ffffffu] ? 1 : 0;
-}
-
-__global__ void reset_flagged_kernel(uint32_t *__restrict__ cnt, const int32_t *__restrict__ flags, int B)
-{
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < B && flags[q]) cnt[q] = 0;
-}
-
-__global__ void qabsmax_kernel(const float *__restrict__ X, int64_t count, uint32_t *__restrict__ out)
-{
-    float m = 0.f;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float v = fabsf(X[i]);
-        m = (v != v) ? __int_as_float(0x7f800000) : fmaxf(m, v);  // NaN -> +inf (rejected)
-    }
-    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
-}
+// parity hooks
 
 // standalone LB_SAX of one query PAA against rows of words (parity tests)
 __global__ void lb_sax_rows_kernel(const float *__restrict__ qpaa, const uint8_t *__restrict__ words, int64_t rows,
@@ -436,78 +65,28 @@ int index_lbe(const Index &ix, const float *Q, int B, double *out, cudaStream_t 
 {
     if (B == 0) return OK;
     const int n = ix.n;
-    DevBuf cs, c2, qpaa, best;
+    DevBuf cs, c2, qpaa;
     SSB_CUDA(cs.alloc(8 * (size_t)B * (n + 1), s));
     SSB_CUDA(c2.alloc(8 * (size_t)B * (n + 1), s));
     SSB_CUDA(qpaa.alloc(4 * (size_t)B * WORD_SEGMENTS, s));
-    SSB_CUDA(best.alloc(4 * (size_t)B, s));
     int rc = launch_query_prep(Q, B, n, cs.as<double>(), c2.as<double>(), qpaa.as<float>(), s);
     if (rc) return rc;
-    lbe_kernel<<<B, 256, 16 * (n + 1), s>>>(cs.as<double>(), c2.as<double>(), n, ix.L, ix.leaf_m, ix.leaf_ep,
-                                            ix.leaf_env, ix.leaf_count, out, best.as<int32_t>());
-    SSB_CHECK_LAUNCH();
+    rc = launch_ix_lbe(ix, cs.as<double>(), c2.as<double>(), B, out, s);
+    if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
 }
 
 // ---------------------------------------------------------------------------
-// host: entry list -> tile list -> sparse scan -> select (with tightening)
+// one query block: ixq.cu's stages, the tensor-core filter for the queries the
+// cost model routes there, K-select with bound tightening
 
-// routing (query.py:321-325): leaves each query keeps under its seed bound
-// Cost model of the two exact paths (B200-measured, per row per query, in units
-// of one tensor-core filter row): LB_SAX filtering of a
-// candidate-leaf row costs ~14 units; the seed scan (exact float32 scan of a
-// query's best leaf, one query per leaf on typical batches) ~5000 per row.
-// The dense filter costs N units per query.
-constexpr double COST_TC_ROW = 1.0, COST_LBS_ROW = 14.0, COST_SEED_ROW = 5000.0;
+constexpr int TC_KTOP_MAX = 4096;  // the filter tightens its bound for every k (buckets)
 
-// routing: leaves (and their rows) each query keeps under its seed bound.
-// mode 0 auto (cost model), 1 tree, 2 tensor, 3 the reference's eapca_th rule
-// (query.py:321-325: eapca_pr < eapca_th -> "scan").
-__global__ void route_kernel(const double *__restrict__ lbe, int L, const uint64_t *__restrict__ thr, double slack_abs,
-                             const uint32_t *__restrict__ leaf_count, float eapca_th, int mode, int64_t N,
-                             uint32_t *__restrict__ cand_leaves, int32_t *__restrict__ use_tc)
+__global__ void reset_flagged_kernel(uint32_t *__restrict__ cnt, const int32_t *__restrict__ flags, int B)
 {
-    const int q = blockIdx.x;
-    const double bound = keep_bound(thr[q], slack_abs);
-    uint32_t c = 0;
-    unsigned long long rows = 0;
-    for (int l = threadIdx.x; l < L; l += blockDim.x)
-        if (leaf_count[l] && lbe[(int64_t)q * L + l] <= bound) {
-            c++;
-            rows += leaf_count[l];
-        }
-    for (int off = 16; off; off >>= 1) {
-        c += __shfl_xor_sync(0xffffffffu, c, off);
-        rows += __shfl_xor_sync(0xffffffffu, rows, off);
-    }
-    __shared__ uint32_t part[32];
-    __shared__ unsigned long long prow[32];
-    if ((threadIdx.x & 31) == 0) {
-        part[threadIdx.x >> 5] = c;
-        prow[threadIdx.x >> 5] = rows;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        unsigned long long rt = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-            t += part[w];
-            rt += prow[w];
-        }
-        cand_leaves[q] = t;
-        const double eapca_pr = 1.0 - (double)t / (double)(L > 0 ? L : 1);
-        int tc;
-        if (mode == 2)
-            tc = 1;
-        else if (mode == 1)
-            tc = 0;
-        else if (mode == 3)
-            tc = eapca_pr < (double)eapca_th ? 1 : 0;
-        else
-            tc = (double)rt * COST_LBS_ROW > (double)N * COST_TC_ROW ? 1 : 0;
-        use_tc[q] = tc;
-    }
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < B && flags[q]) cnt[q] = 0;
 }
 
 __global__ void seed_bound_kernel(const uint64_t *__restrict__ thr, const int32_t *__restrict__ qlist, int nq,
@@ -536,209 +115,65 @@ __global__ void tc_filter_flagged_kernel(const uint2 *__restrict__ cand, int64_t
     if (flags[qlist[c.x]]) out[atomicAdd(nout, 1u)] = c;
 }
 
-struct TileBufs {
-    DevBuf row0, umask, eptr, entries, keys, masks;  // keys/masks: the sorted entries
-    int64_t ntiles = 0;
-    int64_t E = 0;
-};
-
-static int build_tiles(DevBuf &ekey, DevBuf &emask, int64_t E, TileBufs &tb, cudaStream_t s, int64_t N)
+__global__ void skip_unflagged_kernel(const int32_t *__restrict__ flags, const int32_t *__restrict__ use_tc, int B,
+                                      int32_t *__restrict__ skip)
 {
-    int tbits = 1;
-    while ((1ll << tbits) <= N / TILE_ROWS + 1) tbits++;
-    const int end_bit = 32 + tbits;
-    tb.E = E;
-    tb.ntiles = 0;
-    if (E == 0) return OK;
-    DevBuf &k2 = tb.keys, &m2 = tb.masks;
-    DevBuf tmp, flags, slot;
-    SSB_CUDA(k2.alloc(8 * (size_t)E, s));
-    SSB_CUDA(m2.alloc(4 * (size_t)E, s));
-    size_t tb_bytes = 0;
-    SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
-                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, end_bit, s));
-    SSB_CUDA(tmp.alloc(tb_bytes, s));
-    SSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb_bytes, ekey.as<uint64_t>(), k2.as<uint64_t>(),
-                                             emask.as<uint32_t>(), m2.as<uint32_t>(), (int)E, 0, end_bit, s));
-    note_launch(1);
-    SSB_CUDA(flags.alloc(4 * (size_t)(E + 1), s));
-    SSB_CUDA(slot.alloc(4 * (size_t)(E + 1), s));
-    tile_flags_kernel<<<(unsigned)((E + 256) / 256), 256, 0, s>>>(k2.as<uint64_t>(), E, flags.as<uint32_t>());
-    SSB_CHECK_LAUNCH();
-    size_t sb = 0;
-    SSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, flags.as<uint32_t>(), slot.as<uint32_t>(), (int)(E + 1), s));
-    DevBuf tmp2;
-    SSB_CUDA(tmp2.alloc(sb, s));
-    SSB_CUDA(cub::DeviceScan::InclusiveSum(tmp2.p, sb, flags.as<uint32_t>(), slot.as<uint32_t>(), (int)(E + 1), s));
-    note_launch(1);
-    uint32_t nt = 0;
-    SSB_CUDA(cudaMemcpyAsync(&nt, slot.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    tb.ntiles = nt;
-    SSB_CUDA(tb.row0.alloc(4 * (size_t)nt, s));
-    SSB_CUDA(tb.umask.alloc(4 * (size_t)nt, s));
-    SSB_CUDA(tb.eptr.alloc(4 * (size_t)(nt + 1), s));
-    SSB_CUDA(tb.entries.alloc(8 * (size_t)E, s));
-    SSB_CUDA(cudaMemsetAsync(tb.umask.p, 0, 4 * (size_t)nt, s));
-    tile_build_kernel<<<(unsigned)((E + 256) / 256), 256, 0, s>>>(
-        k2.as<uint64_t>(), m2.as<uint32_t>(), E, flags.as<uint32_t>(), slot.as<uint32_t>(),
-        tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>());
-    SSB_CHECK_LAUNCH();
-    return OK;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < B) skip[q] = (!flags[q] || use_tc[q]) ? 1 : 0;
 }
 
-// one batch of queries (Bq <= cap-sized batch)
-static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, double slack_abs,
-                       uint64_t *out_keys,
-                       uint32_t *st_cand_leaves, uint32_t *st_cand_series, uint32_t *st_seed_rows,
-                       int32_t *st_rounds, uint32_t *st_over, int64_t entry_cap, cudaStream_t s)
+// returns -1 when a work buffer (items / entries) overflowed: the caller halves the block
+static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, uint64_t *out_keys,
+                       uint32_t *stats_host, cudaStream_t s)
 {
-    const int n = ix.n, L = ix.L;
-    DevBuf cs, c2, qpaa, lbe, best, thr, cand, cnt, flags, ekey, emask, ecount, symlo, symhi;
-    SSB_CUDA(cs.alloc(8 * (size_t)B * (n + 1), s));
-    SSB_CUDA(c2.alloc(8 * (size_t)B * (n + 1), s));
-    SSB_CUDA(qpaa.alloc(4 * (size_t)B * WORD_SEGMENTS, s));
-    SSB_CUDA(lbe.alloc(8 * (size_t)B * L, s));
-    SSB_CUDA(best.alloc(4 * (size_t)B, s));
-    SSB_CUDA(thr.alloc(8 * (size_t)B, s));
-    int rc = launch_query_prep(Q, B, n, cs.as<double>(), c2.as<double>(), qpaa.as<float>(), s);
+    const int n = ix.n;
+    int mode = ix.Xb ? qc.route : 1;
+    if (k > TC_KTOP_MAX && mode != 1) mode = 1;
+    const bool want = stats_host != nullptr;
+    // tensor-core filter cost of one query (bytes of BF16 rows it streams per
+    // query in a full 256-query cluster, or alone for small blocks)
+    const double tc_cost = (double)ix.N * 2.0 * n * IX_COST_TC_BYTE / (double)std::min(std::max(B, 1), 256);
+    // auto: when even a query that keeps every leaf is cheaper on the index
+    // route (small blocks: the filter's pass is shared by few queries), no
+    // query can take the filter -- no routing round trip
+    if (mode == 0 && (double)ix.N * IX_COST_LBS_ROW <= tc_cost) mode = 1;
+    IxWork w;
+    int rc = ix_front(ix, qc, Q, B, k, mode, tc_cost, want, w, s);
     if (rc) return rc;
-    DevBuf qlay;
-    SSB_CUDA(qlay.alloc(4 * (size_t)B * n, s));
-    rc = launch_layout_rows(Q, nullptr, B, n, qlay.as<float>(), true, s);
-    if (rc) return rc;
-    const float *Qp = qlay.as<float>();
-    {
-        const int smem = 16 * (n + 1);
-        ProfScope ps("lbe", s, (double)L * (M_MAX * 20 + 12) + 16.0 * B * (n + 1));
-        lbe_kernel<<<B, 256, smem, s>>>(cs.as<double>(), c2.as<double>(), n, L, ix.leaf_m, ix.leaf_ep,
-                                        ix.leaf_env, ix.leaf_count, lbe.as<double>(), best.as<int32_t>());
-    }
-    SSB_CHECK_LAUNCH();
-
-    // symbol bounds from the breakpoints (summarize.py:124-133)
-    {
-        std::vector<double> lo(ALPHABET), hi(ALPHABET), bp(ALPHABET - 1);
-        SSB_CUDA(cudaMemcpyAsync(bp.data(), ix.bp, 8 * (ALPHABET - 1), cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        lo[0] = -INFINITY;
-        for (int i = 1; i < ALPHABET; i++) lo[i] = bp[i - 1];
-        for (int i = 0; i < ALPHABET - 1; i++) hi[i] = bp[i];
-        hi[ALPHABET - 1] = INFINITY;
-        SSB_CUDA(symlo.alloc(8 * ALPHABET, s));
-        SSB_CUDA(symhi.alloc(8 * ALPHABET, s));
-        SSB_CUDA(cudaMemcpyAsync(symlo.p, lo.data(), 8 * ALPHABET, cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaMemcpyAsync(symhi.p, hi.data(), 8 * ALPHABET, cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-    }
-
-    // candidate capacity per query: generous, so the bound-tightening rescan is rare
     const int cap = (int)std::min<int64_t>(std::max<int64_t>(16384, ix.N / 16), 262144);
+    DevBuf cand, cnt, flags, skip, cser;
     SSB_CUDA(cand.alloc(8 * (size_t)B * cap, s));
     SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
     SSB_CUDA(flags.alloc(4 * (size_t)B, s));
-    SSB_CUDA(ecount.alloc(4, s));
-    SSB_CUDA(ekey.alloc(8 * (size_t)entry_cap, s));
-    SSB_CUDA(emask.alloc(4 * (size_t)entry_cap, s));
-
-    // ---- phase A: exact scan of each query's best leaf -> bound ------------------
-    // jobs: (leaf row chunk) x (<= 32 queries whose best leaf it is).
-    // Skipped when every query goes to the tensor-core filter anyway: forced,
-    // or (auto) when the dense filter over all N rows costs less than the seed
-    // scan alone (the filter derives its own bound from its upper bounds).
-    EntryOut eo{ekey.as<uint64_t>(), emask.as<uint32_t>(), ecount.as<uint32_t>(), entry_cap};
-    SSB_CUDA(cudaMemsetAsync(thr.p, 0xff, 8 * (size_t)B, s));
+    SSB_CUDA(skip.alloc(4 * (size_t)B, s));
+    SSB_CUDA(cser.alloc(4 * (size_t)B, s));
     SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
-    const double avg_leaf = (double)ix.N / (double)std::max(1, L);
-    const bool tc_ok = ix.Xb && k <= TC_KTOP_MAX;
-    const bool tc_all = tc_ok && (qc.route == 2 ||
-                                  (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
-    // auto: queries whose seed-free lower bound on the LB_SAX path already
-    // exceeds the dense filter skip the seed and go to the tensor cores
-    std::vector<int32_t> pre_tc(B, tc_all ? 1 : 0);
-    if (tc_ok && !tc_all && qc.route == 0) {
-        DevBuf fr;
-        SSB_CUDA(fr.alloc(8 * (size_t)B, s));
-        floor_rows_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, ix.leaf_count, fr.as<uint64_t>());
-        SSB_CHECK_LAUNCH();
-        std::vector<uint64_t> hfr(B);
-        SSB_CUDA(cudaMemcpyAsync(hfr.data(), fr.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemsetAsync(cser.p, 0, 4 * (size_t)B, s));
+    uint64_t *thr = w.thr.as<uint64_t>();
+    ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr, cap};
+
+    // routing: the host needs the tensor-core subset (one round trip) unless
+    // the mode excludes the filter
+    std::vector<int32_t> qtc;
+    if (mode != 1) {
+        std::vector<int32_t> h(B);
+        SSB_CUDA(cudaMemcpyAsync(h.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
-        for (int q = 0; q < B; q++) pre_tc[q] = (double)hfr[q] * COST_LBS_ROW > (double)ix.N * COST_TC_ROW ? 1 : 0;
-    }
-    if (tc_all) SSB_CUDA(cudaMemsetAsync(st_seed_rows, 0, 4 * (size_t)B, s));
-    if (!tc_all) {
-        std::vector<int32_t> hbest(B);
-        SSB_CUDA(cudaMemcpyAsync(hbest.data(), best.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        std::vector<std::vector<int32_t>> byleaf(L);
-        std::vector<uint32_t> seed_rows(B, 0);
         for (int q = 0; q < B; q++)
-            if (hbest[q] >= 0 && !pre_tc[q]) byleaf[hbest[q]].push_back(q);
-        std::vector<int32_t> qlist;
-        std::vector<ScanJob> jobs;
-        const uint32_t CH = 1024;  // rows per job
-        for (int l = 0; l < L; l++) {
-            if (byleaf[l].empty()) continue;
-            const TreeNode &tn = ix.nodes[ix.leaves[l]];
-            for (size_t g0 = 0; g0 < byleaf[l].size(); g0 += 32) {
-                const uint32_t qoff = (uint32_t)qlist.size();
-                const uint32_t qn = (uint32_t)std::min<size_t>(32, byleaf[l].size() - g0);
-                for (uint32_t i = 0; i < qn; i++) {
-                    qlist.push_back(byleaf[l][g0 + i]);
-                    seed_rows[byleaf[l][g0 + i]] = tn.count;
-                }
-                for (uint32_t r = tn.first; r < tn.first + tn.count; r += CH)
-                    jobs.push_back({r, std::min(tn.first + tn.count, r + CH), qoff, qn});
-            }
-        }
-        DevBuf djobs, dql;
-        SSB_CUDA(djobs.alloc(sizeof(ScanJob) * std::max<size_t>(jobs.size(), 1), s));
-        SSB_CUDA(dql.alloc(4 * std::max<size_t>(qlist.size(), 1), s));
-        SSB_CUDA(cudaMemcpyAsync(djobs.p, jobs.data(), sizeof(ScanJob) * jobs.size(), cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaMemcpyAsync(dql.p, qlist.data(), 4 * qlist.size(), cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaMemcpyAsync(st_seed_rows, seed_rows.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
-        ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
-        rc = launch_scan_jobs(ix.X, n, ix.orig, djobs.as<ScanJob>(), (int)jobs.size(), dql.as<int32_t>(), Qp, k,
-                              so, s);
-        if (rc) return rc;
-        rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
-                           flags.as<int32_t>(), s);
-        if (rc) return rc;
-        thr_from_keys_kernel<<<(B + 255) / 256, 256, 0, s>>>(out_keys, B, k, thr.as<uint64_t>());
-        SSB_CHECK_LAUNCH();
-        SSB_CUDA(cudaStreamSynchronize(s));  // host job vectors die here
+            if (h[q]) qtc.push_back(q);
     }
-    uint32_t E = 0;
+    // index route first (Q5 + Q6 of every query the plan kept on it)
+    rc = ix_back(ix, w, B, mode != 1 ? w.use_tc.as<int32_t>() : nullptr, so, cser.as<uint32_t>(), s);
+    if (rc) return rc;
 
-    // ---- routing: the reference's eapca_th rule (query.py:321-325) -------------
-    // a query whose seed bound keeps most leaves ("scan" in the reference) goes to
-    // the tensor-core filter; the others to LB_SAX + sparse exact scan.
-    DevBuf use_tc;
-    SSB_CUDA(use_tc.alloc(4 * (size_t)B, s));
-    int mode = ix.Xb ? qc.route : 1;
-    if (mode == 0 && k > TC_KTOP_MAX) mode = 1;
-    if (tc_all) mode = 2;
-    route_kernel<<<B, 256, 0, s>>>(lbe.as<double>(), L, thr.as<uint64_t>(), slack_abs, ix.leaf_count, qc.eapca_th,
-                                   mode, ix.N, st_cand_leaves, use_tc.as<int32_t>());
-    SSB_CHECK_LAUNCH();
-    std::vector<int32_t> h_tc(B);
-    SSB_CUDA(cudaMemcpyAsync(h_tc.data(), use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    for (int q = 0; q < B; q++) h_tc[q] |= pre_tc[q];
-    std::vector<int32_t> qtree, qtc;
-    for (int q = 0; q < B; q++) (h_tc[q] ? qtc : qtree).push_back(q);
-    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
-    SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
-    ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr.as<uint64_t>(), cap};
-
-    // ---- tensor-core path ---------------------------------------------------------
+    // ---- tensor-core route: K-tc over all N rows, exact rescoring -------------
     DevBuf d_qtc, tc_cand, tc_lb, tc_n, gb;
     int64_t tc_nc = 0;
     if (!qtc.empty()) {
         const int nq = (int)qtc.size();
         const int nq_pad = (nq + 127) / 128 * 128;
-        const int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)nq * 8192);
+        int64_t tc_cap = std::max<int64_t>(1 << 20, (int64_t)nq * std::max(8192, 64 * k));
+        if (const char *e = getenv("SSB_TEST_TC_CAP")) tc_cap = std::max<int64_t>(1, atoll(e));  // test hook
         DevBuf qb, qn2, qnrm;
         SSB_CUDA(d_qtc.alloc(4 * (size_t)nq, s));
         SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * n, s));
@@ -748,89 +183,84 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(nq), s));
         SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
         SSB_CUDA(tc_lb.alloc(4 * (size_t)tc_cap, s));
-        SSB_CUDA(tc_n.alloc(4, s));
+        SSB_CUDA(tc_n.alloc(8, s));
         SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
-        SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 4, s));
         rc = launch_to_bf16_norms(Q, d_qtc.as<int32_t>(), nq, n, false, qb.p, qn2.as<float>(), qnrm.as<float2>(), true, s);
         if (rc) return rc;
-        seed_bound_kernel<<<(nq + 255) / 256, 256, 0, s>>>(thr.as<uint64_t>(), d_qtc.as<int32_t>(), nq,
-                                                          gb.as<unsigned int>());
+        // the approximate phase's k-th distance is the filter's starting bound
+        seed_bound_kernel<<<(nq + 255) / 256, 256, 0, s>>>(thr, d_qtc.as<int32_t>(), nq, gb.as<unsigned int>());
         SSB_CHECK_LAUNCH();
-        rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
-                              gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(), tc_n.as<unsigned int>(),
-                              tc_cap, nullptr, s);
-        if (rc) return rc;
-        uint32_t hn = 0;
-        SSB_CUDA(cudaMemcpyAsync(&hn, tc_n.p, 4, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        if ((int64_t)hn > tc_cap) {  // too many candidates: answer these queries on the tree path
-            for (int q : qtc) qtree.push_back(q);
-            std::sort(qtree.begin(), qtree.end());
+        uint64_t hn = 0;
+        for (int attempt = 0; attempt < 3; attempt++) {  // a retry keeps the bounds the filter ended with
+            SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 8, s));
+            rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+                                  gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
+                                  tc_n.as<unsigned long long>(), tc_cap, nullptr, s);
+            if (rc) return rc;
+            SSB_CUDA(cudaMemcpyAsync(&hn, tc_n.p, 8, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+            if ((int64_t)hn <= tc_cap) break;
+        }
+        if ((int64_t)hn > tc_cap) {
+            // still too many candidates: these queries take the index route
+            SSB_CUDA(cudaMemsetAsync(w.use_tc.p, 0, 4 * (size_t)B, s));
+            rc = ix_replan_tree(ix, qc, w, d_qtc.as<int32_t>(), nq, s);
+            if (rc) return rc;
+            std::vector<int32_t> hs(B, 1);
+            for (int q : qtc) hs[q] = 0;
+            SSB_CUDA(cudaMemcpyAsync(skip.p, hs.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+            rc = ix_back(ix, w, B, skip.as<int32_t>(), so, cser.as<uint32_t>(), s);
+            if (rc) return rc;
+            SSB_CUDA(cudaStreamSynchronize(s));  // hs dies here
             qtc.clear();
         } else {
-            tc_nc = hn;
-            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, Qp, d_qtc.as<int32_t>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
-                                gb.as<unsigned int>(), tc_nc, so, s);
+            tc_nc = (int64_t)hn;
+            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, w.qlay.as<float>(), d_qtc.as<int32_t>(),
+                                tc_cand.as<uint2>(), tc_lb.as<float>(), gb.as<unsigned int>(), tc_nc, so, s);
             if (rc) return rc;
-            if (tc_nc) {
+            if (tc_nc && want) {
                 tc_count_kernel<<<(unsigned)((tc_nc + 255) / 256), 256, 0, s>>>(tc_cand.as<uint2>(), tc_nc,
-                                                                              d_qtc.as<int32_t>(), st_cand_series);
+                                                                              d_qtc.as<int32_t>(), cser.as<uint32_t>());
                 SSB_CHECK_LAUNCH();
             }
         }
     }
 
-    // ---- tree path: LB_SAX filtering, exact scan of survivors --------------------
-    TileBufs tb;
-    TileList tl{nullptr, nullptr, nullptr, nullptr, 0};
-    E = 0;
-    if (!qtree.empty()) {
-        DevBuf d_qt;
-        SSB_CUDA(d_qt.alloc(4 * qtree.size(), s));
-        SSB_CUDA(cudaMemcpyAsync(d_qt.p, qtree.data(), 4 * qtree.size(), cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaMemsetAsync(ecount.p, 0, 4, s));
-        {
-            ProfScope ps("lbs", s, 0.0);
-            lbs_kernel<<<(unsigned)qtree.size(), 256, 0, s>>>(
-                qpaa.as<float>(), symlo.as<double>(), symhi.as<double>(), reinterpret_cast<const uint4 *>(ix.words), n,
-                L, ix.leaf_first, ix.leaf_count, lbe.as<double>(), thr.as<uint64_t>(), slack_abs, eo, st_cand_leaves,
-                st_cand_series, ps.counter(), d_qt.as<int32_t>());
-        }
-        SSB_CHECK_LAUNCH();
-        SSB_CUDA(cudaMemcpyAsync(&E, ecount.p, 4, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        if ((int64_t)E > entry_cap) {
-            set_error(ERR_USAGE, "candidate entry buffer overflow");
-            return -1;  // caller splits the batch
-        }
-        rc = build_tiles(ekey, emask, E, tb, s, ix.N);
-        if (rc) return rc;
-        tl = TileList{tb.row0.as<uint32_t>(), tb.umask.as<uint32_t>(), tb.eptr.as<uint32_t>(), tb.entries.as<uint2>(),
-                      tb.ntiles};
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl, Qp, so, s);
-        if (rc) return rc;
-    }
-
-    // ---- select; overflowed queries get a tighter bound and are rescanned ---------
-    std::vector<int32_t> hflags(B);
+    // ---- select; overflowed queries get a tighter bound and are redone --------
+    std::vector<int32_t> hflags(B), hover(B, 0);
+    unsigned long long h_items = 0, h_ents = 0;
+    uint32_t h_bad = 0;
     for (int round = 0;; round++) {
-        rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr.as<uint64_t>(), out_keys,
-                           flags.as<int32_t>(), s);
+        rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, thr, out_keys, flags.as<int32_t>(), s);
         if (rc) return rc;
         SSB_CUDA(cudaMemcpyAsync(hflags.data(), flags.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        if (round == 0) {
+            SSB_CUDA(cudaMemcpyAsync(&h_items, w.n_items.p, 8, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaMemcpyAsync(&h_ents, w.n_ents.p, 8, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaMemcpyAsync(&h_bad, w.bad.p, 4, cudaMemcpyDeviceToHost, s));
+        }
         SSB_CUDA(cudaStreamSynchronize(s));
+        if (round == 0) {
+            SSB_REQUIRE(!h_bad, "queries must be finite");
+            if ((int64_t)h_items > w.item_cap || (int64_t)h_ents > w.ent_cap) {
+                set_error(ERR_USAGE, "index work buffer overflow");
+                return -1;  // caller splits the block
+            }
+            hover = hflags;
+        }
         int over = 0;
         for (int q = 0; q < B; q++) over += hflags[q];
-        if (round == 0 && st_over)
-            SSB_CUDA(cudaMemcpyAsync(st_over, flags.p, 4 * (size_t)B, cudaMemcpyDeviceToDevice, s));
-        if (!over) {
-            if (st_rounds) *st_rounds = round;
-            break;
-        }
+        if (!over) break;
         SSB_REQUIRE(round < 64, "bound tightening did not converge");
         reset_flagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), flags.as<int32_t>(), B);
         SSB_CHECK_LAUNCH();
+        // index-route queries: their items again under the tighter bound
+        skip_unflagged_kernel<<<(B + 255) / 256, 256, 0, s>>>(flags.as<int32_t>(), w.use_tc.as<int32_t>(), B,
+                                                               skip.as<int32_t>());
+        SSB_CHECK_LAUNCH();
+        rc = ix_back(ix, w, B, skip.as<int32_t>(), so, nullptr, s);
+        if (rc) return rc;
         // tensor-core queries: rescore their candidates again under the tighter bound
         if (tc_nc) {
             DevBuf sub, nsub;
@@ -844,47 +274,40 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             uint32_t ns = 0;
             SSB_CUDA(cudaMemcpyAsync(&ns, nsub.p, 4, cudaMemcpyDeviceToHost, s));
             SSB_CUDA(cudaStreamSynchronize(s));
-            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, Qp, d_qtc.as<int32_t>(), sub.as<uint2>(), nullptr, nullptr, ns, so,
-                                s);
+            rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, w.qlay.as<float>(), d_qtc.as<int32_t>(), sub.as<uint2>(),
+                                nullptr, nullptr, ns, so, s);
             if (rc) return rc;
-            SSB_CUDA(cudaStreamSynchronize(s));
         }
-        if (tb.E == 0) continue;
-        // tree queries: rescan only the overflowed queries' (compacted) entries
-        DevBuf ef, ck, cm, nsel, tmp;
-        SSB_CUDA(ef.alloc((size_t)std::max<int64_t>(tb.E, 1), s));
-        SSB_CUDA(ck.alloc(8 * (size_t)std::max<int64_t>(tb.E, 1), s));
-        SSB_CUDA(cm.alloc(4 * (size_t)std::max<int64_t>(tb.E, 1), s));
-        SSB_CUDA(nsel.alloc(8, s));
-        entry_flags_kernel<<<(unsigned)((tb.E + 255) / 256), 256, 0, s>>>(tb.keys.as<uint64_t>(), tb.E,
-                                                                       flags.as<int32_t>(), ef.as<uint8_t>());
-        SSB_CHECK_LAUNCH();
-        size_t tbytes = 0, t2 = 0;
-        SSB_CUDA(cub::DeviceSelect::Flagged(nullptr, tbytes, tb.keys.as<uint64_t>(), ef.as<uint8_t>(),
-                                            ck.as<uint64_t>(), nsel.as<int64_t>(), tb.E, s));
-        SSB_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, tb.masks.as<uint32_t>(), ef.as<uint8_t>(),
-                                            cm.as<uint32_t>(), nsel.as<int64_t>(), tb.E, s));
-        SSB_CUDA(tmp.alloc(std::max(tbytes, t2), s));
-        SSB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tbytes, tb.keys.as<uint64_t>(), ef.as<uint8_t>(),
-                                            ck.as<uint64_t>(), nsel.as<int64_t>(), tb.E, s));
-        SSB_CUDA(cub::DeviceSelect::Flagged(tmp.p, t2, tb.masks.as<uint32_t>(), ef.as<uint8_t>(),
-                                            cm.as<uint32_t>(), nsel.as<int64_t>(), tb.E, s));
-        note_launch(2);
-        int64_t E2 = 0;
-        SSB_CUDA(cudaMemcpyAsync(&E2, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (want) {
+        std::vector<uint32_t> kl(B), sl(B), sr(B), sw(B), ab(B), cs(B);
+        std::vector<unsigned long long> kr(B);
+        std::vector<int32_t> tc(B);
+        SSB_CUDA(cudaMemcpyAsync(kl.data(), w.kept_leaves.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(kr.data(), w.kept_rows.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(sl.data(), w.seed_leaves.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(sr.data(), w.seed_rows.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(sw.data(), w.seed_words.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(ab.data(), w.abandoned.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(cs.data(), cser.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(tc.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
-        TileBufs tb2;
-        rc = build_tiles(ck, cm, E2, tb2, s, ix.N);
-        if (rc) return rc;
-        TileList tl2{tb2.row0.as<uint32_t>(), tb2.umask.as<uint32_t>(), tb2.eptr.as<uint32_t>(),
-                     tb2.entries.as<uint2>(), tb2.ntiles};
-        rc = launch_scan_sparse(ix.X, n, ix.orig, tl2, Qp, so, s, "scan_retry");
-        if (rc) return rc;
-        SSB_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < B; q++) {
+            uint32_t *o = stats_host + (size_t)q * SSB_QUERY_STATS;
+            const bool t = mode != 1 && tc[q];
+            o[0] = kl[q];                                            // candidate leaves
+            o[1] = cs[q];                                            // candidate series (LB_SAX or filter survivors)
+            o[2] = sr[q];                                            // seed rows scanned exactly
+            o[3] = (uint32_t)hover[q];                               // candidate buffer overflowed once
+            o[4] = sl[q];                                            // leaves visited by the approximate phase
+            o[5] = t ? (uint32_t)std::min<int64_t>(ix.N, 0xffffffffll)  // rows whose bytes the filter read
+                     : (uint32_t)std::min<unsigned long long>(kr[q] + sw[q], 0xffffffffull);  // words tested
+            o[6] = ab[q];                                            // rows abandoned early
+            o[7] = t ? 1u : 0u;                                      // route: 1 tensor-core filter
+        }
     }
     return OK;
 }
-
 
 __global__ void qfill_u32_kernel(uint32_t *__restrict__ p, int64_t count, uint32_t v)
 {
@@ -892,10 +315,10 @@ __global__ void qfill_u32_kernel(uint32_t *__restrict__ p, int64_t count, uint32
     if (i < count) p[i] = v;
 }
 
-__global__ void tc_count_dev_kernel(const uint2 *__restrict__ cand, const unsigned int *__restrict__ nc_dev,
+__global__ void tc_count_dev_kernel(const uint2 *__restrict__ cand, const unsigned long long *__restrict__ nc_dev,
                                     int64_t cap, uint32_t *__restrict__ cand_series)
 {
-    const int64_t nc = min(cap, (int64_t)*nc_dev);
+    const int64_t nc = (int64_t)min((unsigned long long)cap, *nc_dev);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&cand_series[cand[i].x], 1u);
 }
@@ -953,7 +376,7 @@ static int tc_submit(const Index &ix, const float *Q, int B, int k, uint64_t *ou
         if (const char *e = getenv("SSB_TEST_TC_CAP")) w.tc_cap = std::max<int64_t>(1, atoll(e));  // test hook
         SSB_CUDA(w.cand.alloc(8 * (size_t)w.tc_cap, s));
         SSB_CUDA(w.clb.alloc(4 * (size_t)w.tc_cap, s));
-        SSB_CUDA(w.cn.alloc(4, s));
+        SSB_CUDA(w.cn.alloc(8, s));
         w.cap = std::max(16384, 4 * k);
         if (const char *e = getenv("SSB_TEST_SELECT_CAP")) w.cap = std::max(k, atoi(e));  // test hook
         SSB_CUDA(w.keys.alloc(8 * (size_t)B * w.cap, s));
@@ -963,20 +386,20 @@ static int tc_submit(const Index &ix, const float *Q, int B, int k, uint64_t *ou
         w.ready = true;
     }
     // a retry (candidate-buffer overflow) keeps the bounds the filter ended with
-    SSB_CUDA(cudaMemsetAsync(w.cn.p, 0, 4, s));
+    SSB_CUDA(cudaMemsetAsync(w.cn.p, 0, 8, s));
     rc = launch_tc_filter(w.qb.p, w.qn2.as<float>(), w.qnrm.as<float2>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
-                          w.gb.as<unsigned int>(), w.cand.as<uint2>(), w.clb.as<float>(), w.cn.as<unsigned int>(),
+                          w.gb.as<unsigned int>(), w.cand.as<uint2>(), w.clb.as<float>(), w.cn.as<unsigned long long>(),
                           w.tc_cap, nullptr, s);
     if (rc) return rc;
     // exact rescoring of the candidates whose lower bound is within the final bound
     SSB_CUDA(cudaMemsetAsync(w.cnt.p, 0, 4 * (size_t)B, s));
     ScanOut so{w.keys.as<uint64_t>(), w.cnt.as<uint32_t>(), nullptr, w.cap};
     rc = launch_rescore(ix.X, n, ix.orig, ix.tcperm, w.qlay.as<float>(), nullptr, w.cand.as<uint2>(),
-                        w.clb.as<float>(), w.gb.as<unsigned int>(), w.tc_cap, so, s, w.cn.as<unsigned int>());
+                        w.clb.as<float>(), w.gb.as<unsigned int>(), w.tc_cap, so, s, w.cn.as<unsigned long long>());
     if (rc) return rc;
     if (want_stats) {  // QueryStats only
         SSB_CUDA(cudaMemsetAsync(st_cand_series, 0, 4 * (size_t)B, s));
-        tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(w.cand.as<uint2>(), w.cn.as<unsigned int>(),
+        tc_count_dev_kernel<<<(unsigned)(num_sms() * 4), 256, 0, s>>>(w.cand.as<uint2>(), w.cn.as<unsigned long long>(),
                                                                        w.tc_cap, st_cand_series);
         SSB_CHECK_LAUNCH();
         rc = qfill_u32(st_cand_leaves, B, leaves_nonempty, s);
@@ -998,8 +421,9 @@ static int tc_check(TcWork &w, bool *retry, bool *redo, cudaStream_t s)
 {
     *retry = *redo = false;
     std::vector<int32_t> hf(w.B);
-    uint32_t hn = 0, qm_bits = 0;
-    SSB_CUDA(cudaMemcpyAsync(&hn, w.cn.p, 4, cudaMemcpyDeviceToHost, s));
+    uint64_t hn = 0;
+    uint32_t qm_bits = 0;
+    SSB_CUDA(cudaMemcpyAsync(&hn, w.cn.p, 8, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaMemcpyAsync(&qm_bits, w.qmax.p, 4, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaMemcpyAsync(hf.data(), w.flags.p, 4 * (size_t)w.B, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
@@ -1007,7 +431,7 @@ static int tc_check(TcWork &w, bool *retry, bool *redo, cudaStream_t s)
     std::memcpy(&qm, &qm_bits, 4);
     SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
     if (getenv("SSB_TC_TRACE"))
-        fprintf(stderr, "[ssb] tc batch B=%d k=%d attempt %d: %u candidates (cap %lld)\n", w.B, w.k, w.attempt, hn,
+        fprintf(stderr, "[ssb] tc batch B=%d k=%d attempt %d: %llu candidates (cap %lld)\n", w.B, w.k, w.attempt, (unsigned long long)hn,
                 (long long)w.tc_cap);
     if ((int64_t)hn > w.tc_cap) {
         if (w.attempt++ < 2)
@@ -1036,13 +460,13 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     }
 }
 
-// every query on the tensor-core filter: forced, or (auto) when the dense
-// filter over all N rows costs less than the seed scan of one average leaf
 static bool tc_all_for(const Index &ix, const QueryCfg &qc, int k)
 {
-    const double avg_leaf = (double)ix.N / (double)std::max(1, ix.L);
-    return ix.Xb && k <= TC_KTOP_MAX &&
-           (qc.route == 2 || (qc.route == 0 && (double)ix.N * COST_TC_ROW < avg_leaf * COST_SEED_ROW));
+    // the lean all-tensor-core batch: route "tensor"; "auto" runs the index
+    // stages and routes per query (SSB_AUTO_LEAN=1: auto takes the lean batch
+    // too -- an A/B switch for measurements)
+    static const bool auto_lean = getenv("SSB_AUTO_LEAN") != nullptr;
+    return ix.Xb && k <= TC_KTOP_MAX && (qc.route == 2 || (qc.route == 0 && auto_lean));
 }
 
 // Several independent calls (query blocks, each with its own k) answered with
@@ -1064,141 +488,125 @@ int index_query_multi(const Index &ix, const QueryCfg &qc, int nc, const float *
         SSB_REQUIRE(K[i] <= 4096, "k above 4096 is not supported");
         SSB_REQUIRE(B[i] >= 0 && B[i] < (1 << 26), "too many queries in one call");
     }
-    std::vector<TcWork> work(nc);
+    std::vector<std::unique_ptr<TcWork>> work(nc);
     std::vector<DevBuf> keys(nc);
     std::vector<char> lean(nc, 0);
     auto submit = [&](int i) -> int {
         int rc = tc_submit(ix, Q[i], B[i], K[i], keys[i].as<uint64_t>(), nullptr, nullptr, nullptr, nullptr, 0, false,
-                           work[i], s);
+                           *work[i], s);
         if (rc) return rc;
         return launch_keys_to_results(keys[i].as<uint64_t>(), (int64_t)B[i] * K[i], ix.inv, ix.id_base, out_d2[i],
                                       out_id[i], out_pos[i], s);
+    };
+    // calls are checked (one host round trip) and their scratch released in
+    // order; submission runs ahead of the checks only while the in-flight
+    // scratch (candidate buffers + select keys) stays under a byte budget
+    const size_t budget = (size_t)4 << 30;
+    size_t inflight = 0;
+    int checked = 0;
+    auto scratch_of = [&](int i) -> size_t {
+        const TcWork &w = *work[i];
+        return (size_t)w.tc_cap * 12 + (size_t)w.B * (size_t)w.cap * 8 + (size_t)w.B * ix.n * 6;
+    };
+    auto check = [&](int i) -> int {
+        bool redo = false;
+        if (lean[i]) {
+            inflight -= scratch_of(i);
+            for (;;) {
+                bool retry = false;
+                int rc = tc_check(*work[i], &retry, &redo, s);
+                if (rc) return rc;
+                if (!retry) break;
+                rc = submit(i);
+                if (rc) return rc;
+            }
+            work[i].reset();  // scratch freed stream-ordered
+        }
+        if (!lean[i] || redo)
+            return index_query(ix, qc, Q[i], B[i], K[i], ix.id_base, out_d2[i], out_id[i], out_pos[i], nullptr, s);
+        return OK;
     };
     for (int i = 0; i < nc; i++) {
         lean[i] = B[i] > 0 && B[i] <= 8192 && tc_all_for(ix, qc, K[i]);
         if (!lean[i]) continue;
         SSB_CUDA(keys[i].alloc(8 * (size_t)B[i] * K[i], s));
+        work[i].reset(new TcWork());
         const int rc = submit(i);
         if (rc) return rc;
+        inflight += scratch_of(i);
+        while (inflight > budget && checked < i) {
+            const int rc2 = check(checked++);
+            if (rc2) return rc2;
+        }
     }
-    for (int i = 0; i < nc; i++) {
-        bool redo = false;
-        while (lean[i]) {
-            bool retry = false;
-            int rc = tc_check(work[i], &retry, &redo, s);
-            if (rc) return rc;
-            if (!retry) break;
-            rc = submit(i);
-            if (rc) return rc;
-        }
-        if (!lean[i] || redo) {
-            const int rc = index_query(ix, qc, Q[i], B[i], K[i], ix.id_base, out_d2[i], out_id[i], out_pos[i],
-                                       nullptr, s);
-            if (rc) return rc;
-        }
+    for (; checked < nc; checked++) {
+        const int rc = check(checked);
+        if (rc) return rc;
     }
     return OK;
 }
 
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
-                int64_t *out_id, int64_t *out_pos,
-                uint32_t *stats_host /* B x 4: cand_leaves, cand_series, seed_rows, rounds */, cudaStream_t s)
+                int64_t *out_id, int64_t *out_pos, uint32_t *stats_host /* B x SSB_QUERY_STATS */, cudaStream_t s)
 {
     SSB_REQUIRE(k >= 1, "k must be at least 1");
     SSB_REQUIRE(k <= 4096, "k above 4096 is not supported");
     SSB_REQUIRE(B < (1 << 26), "too many queries in one call");
     if (B == 0) return OK;
     const int n = ix.n;
-    // every query on the tensor-core filter: forced, or (auto) when the dense
-    // filter over all N rows costs less than the seed scan of one average leaf
     const bool tc_all = tc_all_for(ix, qc, k);
     uint32_t leaves_nonempty = 0;
     for (int32_t l : ix.leaves) leaves_nonempty += ix.nodes[l].count > 0 ? 1u : 0u;
-    // statistic-rounding slack: delta * sqrt(2n) in distance
-    // units; needs max |q| on the host, so only the general path computes it
-    double slack_abs = -1.0;
-    auto need_slack = [&]() -> int {
-        if (slack_abs >= 0.0) return OK;
-        DevBuf qmax;
-        SSB_CUDA(qmax.alloc(4, s));
-        SSB_CUDA(cudaMemsetAsync(qmax.p, 0, 4, s));
-        qabsmax_kernel<<<64, 256, 0, s>>>(Q, (int64_t)B * n, qmax.as<uint32_t>());
-        SSB_CHECK_LAUNCH();
-        uint32_t qm_bits = 0;
-        SSB_CUDA(cudaMemcpyAsync(&qm_bits, qmax.p, 4, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        float qm;
-        std::memcpy(&qm, &qm_bits, 4);
-        SSB_REQUIRE(std::isfinite(qm), "queries must be finite");
-        const double M = std::max((double)qm, (double)ix.max_abs);
-        slack_abs = std::ldexp(M, -19) * std::sqrt(2.0 * n);
-        return OK;
-    };
-    if (!tc_all) {
-        const int rc0 = need_slack();
-        if (rc0) return rc0;
-    }
-
-    DevBuf keys, stl, sts, str, sto;
+    DevBuf keys;
     SSB_CUDA(keys.alloc(8 * (size_t)B * k, s));
-    SSB_CUDA(sto.alloc(4 * (size_t)B, s));
-    SSB_CUDA(stl.alloc(4 * (size_t)B, s));
-    SSB_CUDA(sts.alloc(4 * (size_t)B, s));
-    SSB_CUDA(str.alloc(4 * (size_t)B, s));
-    // batches bounded by the entry buffer: worst case every row of every leaf survives
-    const int64_t per_query_worst = ix.N / TILE_ROWS + 2 * (int64_t)ix.L + 2;
-    const int64_t budget = 96ll << 20;  // entries (12 B each)
-    int bq = (int)std::max<int64_t>(1, std::min<int64_t>(B, std::max<int64_t>(256, budget / per_query_worst)));
-    std::vector<int32_t> rounds;
+    // blocks bounded by the index path's work buffers: worst case every leaf kept
+    const int64_t per_query_worst = ix.N / 512 + ix.L + 1;
+    int bq = (int)std::max<int64_t>(1, std::min<int64_t>(B, std::max<int64_t>(64, (24ll << 20) / per_query_worst)));
     for (int q0 = 0; q0 < B;) {
         if (tc_all) {
             const int nb = std::min(8192, B - q0);
             bool redo = false;
+            DevBuf stl, sts, str, sto;
+            SSB_CUDA(stl.alloc(4 * (size_t)nb, s));
+            SSB_CUDA(sts.alloc(4 * (size_t)nb, s));
+            SSB_CUDA(str.alloc(4 * (size_t)nb, s));
+            SSB_CUDA(sto.alloc(4 * (size_t)nb, s));
             const int rc1 = query_batch_tc(ix, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
-                                           stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0,
-                                           sto.as<uint32_t>() + q0, leaves_nonempty, stats_host != nullptr, &redo, s);
+                                           stl.as<uint32_t>(), sts.as<uint32_t>(), str.as<uint32_t>(),
+                                           sto.as<uint32_t>(), leaves_nonempty, stats_host != nullptr, &redo, s);
             if (rc1) return rc1;
             if (!redo) {
+                if (stats_host) {
+                    std::vector<uint32_t> cs(nb), ov(nb);
+                    SSB_CUDA(cudaMemcpyAsync(cs.data(), sts.p, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+                    SSB_CUDA(cudaMemcpyAsync(ov.data(), sto.p, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+                    SSB_CUDA(cudaStreamSynchronize(s));
+                    for (int q = 0; q < nb; q++) {
+                        uint32_t *o = stats_host + (size_t)(q0 + q) * SSB_QUERY_STATS;
+                        const uint32_t row[SSB_QUERY_STATS] = {leaves_nonempty, cs[q], 0u, ov[q], 0u,
+                                                               (uint32_t)std::min<int64_t>(ix.N, 0xffffffffll), 0u, 1u};
+                        std::memcpy(o, row, sizeof(row));
+                    }
+                }
                 q0 += nb;
                 continue;
             }
-            const int rc2 = need_slack();  // a buffer overflowed: this batch takes the general path
-            if (rc2) return rc2;
+            // a buffer overflowed: this block takes the general path
         }
         const int nb = std::min(bq, B - q0);
-        const int64_t ecap = std::min<int64_t>((int64_t)nb * per_query_worst, budget);
-        int32_t r = 0;
-        int rc = query_batch(ix, qc, Q + (int64_t)q0 * n, nb, k, slack_abs, keys.as<uint64_t>() + (int64_t)q0 * k,
-                             stl.as<uint32_t>() + q0, sts.as<uint32_t>() + q0, str.as<uint32_t>() + q0, &r,
-                             sto.as<uint32_t>() + q0, ecap, s);
-        if (rc == -1) {  // entry overflow: halve the batch and retry
-            SSB_REQUIRE(nb > 1, "a single query overflowed the candidate entry buffer");
+        const int rc = query_batch(ix, qc, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
+                                   stats_host ? stats_host + (size_t)q0 * SSB_QUERY_STATS : nullptr, s);
+        if (rc == -1) {  // a work buffer overflowed: halve the block and retry
+            SSB_REQUIRE(nb > 1, "a single query overflowed the index work buffers");
             bq = std::max(1, nb / 2);
             continue;
         }
         if (rc) return rc;
         q0 += nb;
     }
-    int rc = launch_keys_to_results(keys.as<uint64_t>(), (int64_t)B * k, ix.inv, id_base, out_d2, out_id,
-                                    out_pos, s);
-    if (rc) return rc;
-    if (stats_host) {
-        std::vector<uint32_t> a(B), b(B), c(B), d(B);
-        SSB_CUDA(cudaMemcpyAsync(d.data(), sto.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaMemcpyAsync(a.data(), stl.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaMemcpyAsync(b.data(), sts.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaMemcpyAsync(c.data(), str.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));
-        for (int q = 0; q < B; q++) {
-            stats_host[4 * q + 0] = a[q];
-            stats_host[4 * q + 1] = b[q];
-            stats_host[4 * q + 2] = c[q];
-            stats_host[4 * q + 3] = d[q];  // 1 = candidate buffer overflowed once
-        }
-    }
     // the results are stream-ordered on s (the scratch is freed stream-ordered
-    // too): no second host round trip
-    return OK;
+    // too): no further host round trip
+    return launch_keys_to_results(keys.as<uint64_t>(), (int64_t)B * k, ix.inv, id_base, out_d2, out_id, out_pos, s);
 }
 
 }  // namespace ssb

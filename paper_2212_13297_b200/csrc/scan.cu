@@ -2,7 +2,7 @@
 //
 // Replaces: core.py:50-57 ed2_batch (the canonical f32 distance),
 // pscan.py:23-30 brute_force_knn / pscan.py:33-135 pscan_query (full scans),
-// query.py:177-192, 253-292 (leaf scans, candidate refinement).
+// and K-select for every path.
 //
 // Layout: rows are 4n-byte f32 vectors, contiguous; a "tile" is <= 32
 // consecutive rows.  Tiles are staged into shared memory with TMA 1-D bulk
@@ -11,14 +11,11 @@
 // q[8i+j]) and walks the tile rows; lane j is numpy's pairwise accumulator
 // r[j], so d2 is bit-identical to ed2_batch (ssb_common.cuh group_ed2).
 //
-// Two launch shapes share that arithmetic:
-//  * dense  (brute force): CTA = (row range) x (block of 4*WARPS queries); each
-//    group keeps a sorted top-k of its range in shared memory and dumps it to
-//    the per-query candidate buffer at the end.
-//  * sparse (index path): CTA walks a list of tiles; each tile carries
-//    (query, 32-bit row mask) entries; a pair whose (d2, id) key is <= the
-//    query's bound is appended to the query's candidate buffer.
-// K-select then sorts each query's candidates and keeps the first k.
+// The dense launch shape (brute force): CTA = (row range) x (block of 4*WARPS
+// queries); each group keeps a sorted top-k of its range in shared memory and
+// dumps it to the per-query candidate buffer at the end.  (The index path's
+// early-abandoning scan of LB_SAX survivors lives in ixq.cu.)  K-select then
+// sorts each query's candidates and keeps the first k.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -122,245 +119,6 @@ __global__ void __launch_bounds__(WARPS * 32)
             if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = mylist[e];
         }
     }
-}
-
-// ---------------------------------------------------------------------------
-// sparse scan over (tile, query, row-mask) work lists.
-// Rows AND queries are in the lane-transposed layout (layout.cuh): one LDS.128
-// per lane per 4 elements, one shared-memory wavefront per 8-lane group.  A
-// group owns one entry (query, mask) at a time; the next entry's query is
-// prefetched into registers while the current one is computed.
-
-template <int NT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    scan_sparse_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
-                       TileList tl, const float *__restrict__ Qp, ScanOut out)
-{
-    constexpr int G = WARPS * 4;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *tiles = reinterpret_cast<float *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(tiles + 2 * TILE_ROWS * NT);
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int g = warp * 4 + (lane >> 3);
-    const int j = lane & 7;
-    const unsigned gmask = 0xffu << (lane & 24);
-
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    // static round-robin tile assignment: tile = blockIdx.x + it * gridDim.x
-    const int64_t my_tiles =
-        tl.ntiles > (int64_t)blockIdx.x ? (tl.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    auto issue = [&](int64_t it) {
-        int64_t t = blockIdx.x + it * gridDim.x;
-        uint32_t row0 = tl.row0[t];
-        uint32_t um = tl.umask[t];
-        float *buf = tiles + (it & 1) * TILE_ROWS * NT;
-        uint64_t *bar = &bars[it & 1];
-        mbar_expect_tx(bar, (unsigned)__popc(um) * NT * 4u);
-        while (um) {
-            int r = __ffs(um) - 1;
-            um &= um - 1;
-            bulk_g2s(buf + r * NT, X + (int64_t)(row0 + r) * NT, NT * 4u, bar);
-        }
-    };
-    if (tid == 0 && my_tiles > 0) issue(0);
-    unsigned long long my_bytes = 0;
-
-    for (int64_t it = 0; it < my_tiles; it++) {
-        if (tid == 0 && it + 1 < my_tiles) issue(it + 1);
-        const int64_t t = blockIdx.x + it * gridDim.x;
-        const uint32_t row0 = tl.row0[t];
-        const uint32_t e0 = tl.eptr[t], e1 = tl.eptr[t + 1];
-        if (tid == 0 && tl.bytes)
-            my_bytes += (unsigned long long)__popc(tl.umask[t]) * NT * 4 + 12ull + 8ull * (e1 - e0);
-        // first entry's query load overlaps the tile's TMA
-        uint32_t e = e0 + g;
-        float qv[NT / 8], qn[NT / 8];
-        uint2 ent = make_uint2(0, 0), entn = make_uint2(0, 0);
-        if (e < e1) {
-            ent = tl.entries[e];
-            lay_load_q<NT>(Qp + (int64_t)ent.x * NT, qv, j);
-        }
-        mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
-        const float *buf = tiles + (it & 1) * TILE_ROWS * NT;
-        for (; e < e1; e += G) {
-            const bool more = e + G < e1;
-            if (more) {
-                entn = tl.entries[e + G];
-                lay_load_q<NT>(Qp + (int64_t)entn.x * NT, qn, j);
-            }
-            const int q = (int)ent.x;
-            uint32_t mask = ent.y;
-            const uint64_t bound = out.thr[q];
-            while (mask) {
-                const int r0 = __ffs(mask) - 1;
-                mask &= mask - 1;
-                float d0, d1 = 0.f;
-                int r1 = -1;
-                if (mask) {
-                    r1 = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    lay_ed2_x2<NT>(buf + r0 * NT, buf + r1 * NT, qv, j, gmask, d0, d1);
-                } else {
-                    d0 = lay_ed2<NT>(buf + r0 * NT, qv, j, gmask);
-                }
-                if (j == 0) {
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const int r = h ? r1 : r0;
-                        if (r < 0) break;
-                        const uint32_t pos = row0 + r;
-                        const uint64_t key = make_key(h ? d1 : d0, row_id ? row_id[pos] : pos);
-                        if (key <= bound) {
-                            const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
-                            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
-                        }
-                    }
-                }
-            }
-            if (more) {
-#pragma unroll
-                for (int i = 0; i < NT / 8; i++) qv[i] = qn[i];
-                ent = entn;
-            }
-        }
-        __syncthreads();
-    }
-    if (tid == 0 && tl.bytes && my_bytes) atomicAdd(tl.bytes, my_bytes);
-}
-
-// ---------------------------------------------------------------------------
-// job scan (layout rows): each CTA scans a contiguous row range for up to
-// 4*WARPS queries (one per 8-lane group, all groups on the same row: the
-// LDS.128 addresses are shared), keeping a per-query top-k of the range in
-// shared memory and dumping it to the query's candidate buffer.  Used for the
-// seed phase (each query's best leaf).
-
-template <int NT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    scan_jobs_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id, const ScanJob *__restrict__ jobs,
-                     const int32_t *__restrict__ qlist, const float *__restrict__ Qp, int k, ScanOut out)
-{
-    constexpr int G = WARPS * 4;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *tiles = reinterpret_cast<float *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(tiles + 2 * TILE_ROWS * NT);
-    uint64_t *lists = bars + 2;
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int g = warp * 4 + (lane >> 3);
-    const int j = lane & 7;
-    const unsigned gmask = 0xffu << (lane & 24);
-    const ScanJob job = jobs[blockIdx.x];
-    const bool active = g < (int)job.qn;
-    const int q = active ? qlist[job.qoff + g] : 0;
-
-    for (int e = tid; e < G * k; e += blockDim.x) lists[e] = KEY_EMPTY;
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        fence_barrier_init();
-    }
-    float qv[NT / 8];
-    if (active) lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
-    __syncthreads();
-
-    const int64_t r0 = job.r0, r1 = job.r1;
-    const int64_t ntiles = (r1 - r0 + TILE_ROWS - 1) / TILE_ROWS;
-    auto issue = [&](int64_t t) {
-        const int64_t row = r0 + t * TILE_ROWS;
-        const int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row);
-        const unsigned bytes = (unsigned)nr * NT * 4u;
-        mbar_expect_tx(&bars[t & 1], bytes);
-        bulk_g2s(tiles + (t & 1) * TILE_ROWS * NT, X + row * NT, bytes, &bars[t & 1]);
-    };
-    if (tid == 0 && ntiles > 0) issue(0);
-    uint64_t *mylist = lists + (size_t)g * k;
-    for (int64_t t = 0; t < ntiles; t++) {
-        if (tid == 0 && t + 1 < ntiles) issue(t + 1);
-        mbar_wait(&bars[t & 1], (unsigned)((t >> 1) & 1));
-        const int64_t row0 = r0 + t * TILE_ROWS;
-        const int nr = (int)tmin<int64_t>(TILE_ROWS, r1 - row0);
-        const float *buf = tiles + (t & 1) * TILE_ROWS * NT;
-        if (active) {
-            for (int r = 0; r < nr; r += 2) {
-                float d0, d1 = 0.f;
-                const bool two = r + 1 < nr;
-                if (two)
-                    lay_ed2_x2<NT>(buf + r * NT, buf + (r + 1) * NT, qv, j, gmask, d0, d1);
-                else
-                    d0 = lay_ed2<NT>(buf + r * NT, qv, j, gmask);
-                if (j == 0) {
-                    for (int h = 0; h < (two ? 2 : 1); h++) {
-                        const uint32_t pos = (uint32_t)(row0 + r + h);
-                        const uint64_t key = make_key(h ? d1 : d0, row_id ? row_id[pos] : pos);
-                        if (key < mylist[k - 1]) {
-                            int p = k - 1;
-                            while (p > 0 && mylist[p - 1] > key) {
-                                mylist[p] = mylist[p - 1];
-                                p--;
-                            }
-                            mylist[p] = key;
-                        }
-                    }
-                }
-                __syncwarp(gmask);
-            }
-        }
-        __syncthreads();
-    }
-    if (active) {
-        const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
-        int c = 0;
-        uint32_t base = 0;
-        if (j == 0) {
-            while (c < k && mylist[c] != KEY_EMPTY && mylist[c] <= bound) c++;
-            base = c ? atomicAdd(&out.cnt[q], (uint32_t)c) : 0u;
-        }
-        c = __shfl_sync(gmask, c, lane & 24);
-        base = __shfl_sync(gmask, base, lane & 24);
-        for (int e = j; e < c; e += 8) {
-            const uint32_t slot = base + e;
-            if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = mylist[e];
-        }
-    }
-}
-
-template <int NT>
-static int launch_jobs_t(const float *X, const uint32_t *row_id, const ScanJob *jobs, int njobs,
-                         const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s)
-{
-    constexpr int WARPS = 8;
-    const int smem = 2 * TILE_ROWS * NT * 4 + 16 + WARPS * 4 * k * 8;
-    SSB_REQUIRE(smem <= 227 * 1024, "k too large for the job scan");
-    SSB_CUDA(cudaFuncSetAttribute(scan_jobs_kernel<NT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    ProfScope ps("scan_jobs", s, 0.0);
-    scan_jobs_kernel<NT, WARPS><<<njobs, WARPS * 32, smem, s>>>(X, row_id, jobs, qlist, Qp, k, out);
-    SSB_CHECK_LAUNCH();
-    return OK;
-}
-
-int launch_scan_jobs(const float *X, int n, const uint32_t *row_id, const ScanJob *jobs, int njobs,
-                     const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s)
-{
-    if (njobs == 0) return OK;
-    switch (n) {
-    case 64: return launch_jobs_t<64>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
-    case 96: return launch_jobs_t<96>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
-    case 128: return launch_jobs_t<128>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
-    case 256: return launch_jobs_t<256>(X, row_id, jobs, njobs, qlist, Qp, k, out, s);
-    default: break;
-    }
-    set_error(ERR_USAGE, "series length " + std::to_string(n) + " has no compiled scan kernel");
-    return ERR_USAGE;
 }
 
 // ---------------------------------------------------------------------------
@@ -541,40 +299,6 @@ int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const in
     return ERR_USAGE;
 }
 
-template <int NT>
-static int launch_sparse_t(const float *X, const uint32_t *row_id, const TileList &tl,
-                           const float *Q, ScanOut out, cudaStream_t s, const char *tag)
-{
-    constexpr int WARPS = 8;
-    int smem = 2 * TILE_ROWS * NT * 4 + 16;
-    SSB_CUDA(cudaFuncSetAttribute(scan_sparse_kernel<NT, WARPS>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int64_t grid = std::min<int64_t>(tl.ntiles, (int64_t)num_sms() * 4);
-    if (grid < 1) return OK;
-    ProfScope ps(tag, s, 0.0);
-    TileList t2 = tl;
-    t2.bytes = ps.counter();
-    scan_sparse_kernel<NT, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(X, row_id, t2, Q, out);
-    SSB_CHECK_LAUNCH();
-    return OK;
-}
-
-int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
-                       const float *Q, ScanOut out, cudaStream_t s, const char *tag)
-{
-    if (tl.ntiles == 0) return OK;
-    switch (n) {
-    case 64: return launch_sparse_t<64>(X, row_id, tl, Q, out, s, tag);
-    case 96: return launch_sparse_t<96>(X, row_id, tl, Q, out, s, tag);
-    case 128: return launch_sparse_t<128>(X, row_id, tl, Q, out, s, tag);
-    case 256: return launch_sparse_t<256>(X, row_id, tl, Q, out, s, tag);
-    default: break;
-    }
-    set_error(ERR_USAGE, "series length " + std::to_string(n) +
-                          " has no compiled scan kernel (supported: 64, 96, 128, 256)");
-    return ERR_USAGE;
-}
-
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s)
 {
@@ -614,6 +338,26 @@ int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_
                            flags.as<int32_t>(), s);
     if (rc) return rc;
     return launch_keys_to_results(out.as<uint64_t>(), (int64_t)nq * k, nullptr, 0, out_d2, out_id, nullptr, s);
+}
+
+// (d2, id) results -> merge keys (d2 bits << 32 | id), id < 0 -> KEY_EMPTY: the
+// per-shard top-k lists of the row-sharded path, packed on the device for the
+// all-gather
+__global__ void pack_keys_kernel(const float *__restrict__ d2, const int64_t *__restrict__ ids, int64_t count,
+                                 uint64_t *__restrict__ keys)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t id = ids[i];
+    keys[i] = id < 0 ? KEY_EMPTY : make_key(d2[i], (uint32_t)id);
+}
+
+int launch_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, cudaStream_t s)
+{
+    if (count == 0) return OK;
+    pack_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(d2, ids, count, keys);
+    SSB_CHECK_LAUNCH();
+    return OK;
 }
 
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,

@@ -85,6 +85,9 @@ static inline cudaError_t upload_rcp_w()
 
 __device__ __forceinline__ double div_w(double a, int w)
 {
+    // segments wider than the table (n > MAX_SERIES_LEN, ssb_segment_stats
+    // accepts any n): the IEEE division itself
+    if (w > MAX_SERIES_LEN) return __ddiv_rn(a, (double)w);
     const double y = c_rcp_w[w];
     const double q0 = __dmul_rn(a, y);
     const double r = __fma_rn(-q0, (double)w, a);

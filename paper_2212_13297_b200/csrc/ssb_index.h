@@ -67,12 +67,36 @@ struct Index {
 
 struct QueryCfg {
     float eapca_th = 0.25f;  // query.py:45 default; < eapca_th -> tensor-core "scan" path
-    int route = 0;           // 0 auto, 1 tree only, 2 tensor-core for every query
+    int route = 0;           // 0 auto, 1 tree only, 2 tensor-core for every query, 3 eapca_th rule
+    int lmax = 80;           // query.py:44: leaves the approximate phase may visit
 };
+
+// index-path routing cost model (ixq.cu ix_plan_kernel), in
+// bytes streamed: a candidate-leaf row costs IX_COST_LBS_ROW (its 16-byte SAX
+// word plus the LB_SAX arithmetic and its share of the exact scan); the
+// tensor-core filter costs IX_COST_TC_BYTE per BF16 byte it streams per query
+constexpr double IX_COST_LBS_ROW = 24.0;
+constexpr double IX_COST_TC_BYTE = 1.0;
+
+// Everything of one query block on the index path, stream-ordered; the
+// per-stage outputs the caller needs afterwards (bounds, routing, counters)
+// live in IxWork.
+struct IxWork {
+    DevBuf cs, c2, qpaa, qlay, tbl, slack, bad, lbe, thr, use_tc, kept_leaves, kept_rows, items, n_items, ents, n_ents;
+    DevBuf seed_leaves, seed_rows, seed_words, abandoned;
+    int64_t item_cap = 0, ent_cap = 0;
+};
+
+
+int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int mode, double tc_cost_per_query,
+             bool stats, IxWork &w, cudaStream_t s);
+int ix_back(const Index &ix, IxWork &w, int B, const int32_t *qskip, ScanOut so, uint32_t *cand_series, cudaStream_t s);
+int ix_replan_tree(const Index &ix, const QueryCfg &qc, IxWork &w, const int32_t *qlist, int nq, cudaStream_t s);
+int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, double *lbe, cudaStream_t s);
 
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
-                     uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
+                     uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s);
 int64_t tc_bound_slots(int nq);
 int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *out, cudaStream_t s);
@@ -84,6 +108,6 @@ int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, 
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
                    const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
-                   cudaStream_t s, const unsigned int *nc_dev = nullptr);
+                   cudaStream_t s, const unsigned long long *nc_dev = nullptr);
 
 }  // namespace ssb

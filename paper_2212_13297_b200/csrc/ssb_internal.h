@@ -19,31 +19,12 @@ struct ScanOut {
     int cap;
 };
 
-// sparse scan work: tiles of <= 32 consecutive rows, each with (query, row mask) entries
-struct TileList {
-    const uint32_t *row0;   // [ntiles] first row (position) of the tile
-    const uint32_t *umask;  // [ntiles] union of the entry masks (rows to stage)
-    const uint32_t *eptr;   // [ntiles + 1] CSR into entries
-    const uint2 *entries;   // (query, row mask)
-    int64_t ntiles;
-    unsigned long long *bytes = nullptr;  // profiling: algorithmic bytes (nullable)
-};
-
-struct ScanJob {
-    uint32_t r0, r1;  // row range
-    uint32_t qoff;    // offset into the job query list
-    uint32_t qn;      // queries (<= 32)
-};
-int launch_scan_jobs(const float *X, int n, const uint32_t *row_id, const ScanJob *jobs, int njobs,
-                     const int32_t *qlist, const float *Qp, int k, ScanOut out, cudaStream_t s);
-
 int64_t dense_ranges(int64_t N, int nq, int k, int cap);
 int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
                       int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
-int launch_scan_sparse(const float *X, int n, const uint32_t *row_id, const TileList &tl,
-                       const float *Q, ScanOut out, cudaStream_t s, const char *tag = "scan_sparse");
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s);
+int launch_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, cudaStream_t s);
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s);
 

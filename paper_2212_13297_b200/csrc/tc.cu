@@ -186,13 +186,20 @@ struct TcParams {
     int k;
     uint2 *cand;               // (query, row) candidates
     float *cand_lb;            // their lower bounds (rescoring skips rows above the final bound)
-    unsigned int *cand_n;
+    unsigned long long *cand_n;  // 64-bit: degenerate queries can emit > 2^32 rows
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
     int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
     int skip_epi;              // diagnostics (SSB_TC_DIAG): 1 epilogue only releases TMEM, 2 TMEM loads + max,
                                // 3 = 1 without MMAs (loads only), 4 = 1 without loads after the first ring (MMA only)
+    // group lockstep (L2 reuse): the CTAs of every query-block group that stream
+    // the same tile chunk publish their progress and stay within `window` tiles
+    // of each other, so each BF16 tile comes from DRAM about once and the other
+    // groups hit it in L2 (0 = off: needs every CTA co-resident)
+    unsigned int *prog;        // [ctas_per_qb][groups][CS] tiles issued
+    int groups;
+    int window;
 };
 
 // per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
@@ -298,8 +305,22 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const int srows = TC_BN / CS;
             int slot = 0;
             uint32_t phase = 0;
+            volatile unsigned int *prog_chunk =
+                p.window ? p.prog + (size_t)chunk * p.groups * CS : nullptr;  // this chunk's entries
+            const int me = (cid / p.ctas_per_qb) * CS + rank;
             for (int t = 0; t < niter; t++) {
                 const int64_t tile = tile_of(t);
+                if (prog_chunk && (t & 7) == 0) {
+                    // publish, then wait until every CTA on this chunk is within the window
+                    if (lane == 0) {
+                        prog_chunk[me] = (unsigned)t;
+                        __threadfence();
+                        const unsigned need = t > p.window ? (unsigned)(t - p.window) : 0u;
+                        for (int o = 0; o < p.groups * CS; o++)
+                            while (prog_chunk[o] < need) __nanosleep(256);
+                    }
+                    __syncwarp();
+                }
                 // side data of this tile: row constants, half-tile extremes, bounds snapshot
                 const int rs = t % TC_RS;
                 if (t >= TC_RS) mbar_wait(&r_empty[rs], (unsigned)(((t / TC_RS) - 1) & 1));
@@ -359,6 +380,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     phase ^= 1u;
                 }
             }
+        }
+        if (p.window && lane == 0) {  // done: never hold the others back
+            p.prog[(size_t)chunk * p.groups * CS + (cid / p.ctas_per_qb) * CS + rank] = 0x7fffffffu;
+            __threadfence();
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
@@ -480,8 +505,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         __syncwarp();
         auto flush = [&]() {  // warp-uniform
             const unsigned n_st = min(*(volatile unsigned *)stage_fill, (unsigned)STG);
-            unsigned base_slot = 0;
-            if (lane == 0 && n_st) base_slot = atomicAdd(p.cand_n, n_st);
+            unsigned long long base_slot = 0;
+            if (lane == 0 && n_st) base_slot = atomicAdd(p.cand_n, (unsigned long long)n_st);
             base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
             for (unsigned i = lane; i < n_st; i += 32)
                 if ((int64_t)(base_slot + i) < p.cand_cap) {
@@ -616,9 +641,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     if (emit) {
                         const unsigned cnt = __popc(emit);
                         unsigned slot = atomicAdd(stage_fill, cnt);
-                        unsigned gslot = 0;
+                        unsigned long long gslot = 0;
                         if (slot + cnt > (unsigned)STG)
-                            gslot = atomicAdd(p.cand_n, slot + cnt - max(slot, (unsigned)STG));
+                            gslot = atomicAdd(p.cand_n, (unsigned long long)(slot + cnt - max(slot, (unsigned)STG)));
                         while (emit) {
                             const int i = __ffs(emit) - 1;
                             emit &= emit - 1;
@@ -900,7 +925,7 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 // gbound: per-query float bits (initialised by the caller: the seed bound).
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
                      const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
-                     uint2 *cand, float *cand_lb, unsigned int *cand_n, int64_t cand_cap, float *dump,
+                     uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s)
 {
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
@@ -967,6 +992,18 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         const char *d = getenv("SSB_TC_DIAG");
         p.skip_epi = d ? atoi(d) : 0;
     }
+    p.groups = groups;
+    p.prog = nullptr;
+    p.window = 0;
+    DevBuf prog;
+    int window = 48;  // tiles (3 MB of BF16 rows per chunk at n = 256)
+    if (const char *e = getenv("SSB_TC_WINDOW")) window = std::max(0, atoi(e));  // diagnostics (0 = off)
+    if (groups > 1 && window > 0) {
+        SSB_CUDA(prog.alloc(4 * (size_t)p.ctas_per_qb * groups * CS, s));
+        SSB_CUDA(cudaMemsetAsync(prog.p, 0, 4 * (size_t)p.ctas_per_qb * groups * CS, s));
+        p.prog = prog.as<unsigned int>();
+        p.window = std::max(window, 16);
+    }
     const int smem = 1024 + TC_NSLOT * TC_BM * 128 + TC_RS * (int)sizeof(TileSlot) +
                      8 * (1 + 2 * TC_NBAR + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 64;
     const unsigned grid = (unsigned)(p.QB * p.ctas_per_qb);
@@ -991,6 +1028,13 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (p.window) {  // the lockstep spins: every CTA must be resident at once
+            int maxc = 0;
+            if (cudaOccupancyMaxActiveClusters(&maxc, (void *)kern, &cfg) != cudaSuccess ||
+                (int64_t)maxc * p.CS < (int64_t)grid)
+                p.window = 0;
+            cudaGetLastError();
+        }
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
         ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
                      2.0 * (double)nq * (double)N * (double)n);  // algorithmic FLOPs (unpadded K)
@@ -1037,10 +1081,10 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     SSB_CUDA(xnm.alloc(8 * (size_t)N, s));
     SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(B), s));
     SSB_CUDA(cand.alloc(8, s));
-    SSB_CUDA(cn.alloc(4, s));
+    SSB_CUDA(cn.alloc(8, s));
     SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)Bp * n, s));
     SSB_CUDA(cudaMemsetAsync(gb.p, 0, 4 * (size_t)tc_bound_slots(B), s));
-    SSB_CUDA(cudaMemsetAsync(cn.p, 0, 4, s));
+    SSB_CUDA(cudaMemsetAsync(cn.p, 0, 8, s));
     int rc = launch_to_bf16_norms(Q, nullptr, B, n, false, qb.p, qn2.as<float>(), qnm.as<float2>(), true, s);
     if (rc) return rc;
     rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float2>(), false, s);
@@ -1054,7 +1098,7 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     rc = launch_tc_tile_consts(rcb.as<float4>(), N, tcb.as<float4>(), s);
     if (rc) return rc;
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
-                          1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned int>(), 0, S, s);
+                          1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
@@ -1068,11 +1112,11 @@ __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__re
                                const float *__restrict__ Qp, const int32_t *__restrict__ qmap,
                                const uint2 *__restrict__ cand, const float *__restrict__ cand_lb,
                                const unsigned int *__restrict__ fbound, int64_t nc,
-                               const unsigned int *__restrict__ nc_dev, ScanOut out)
+                               const unsigned long long *__restrict__ nc_dev, ScanOut out)
 {
     // candidate count from the host (nc) or, without a host round trip, from
     // the filter's device counter (clamped to the buffer: nc is then its capacity)
-    if (nc_dev) nc = min(nc, (int64_t)*nc_dev);
+    if (nc_dev) nc = (int64_t)min((unsigned long long)nc, *nc_dev);
     const int lane = threadIdx.x & 31, j = lane & 7;
     const unsigned gmask = 0xffu << (lane & 24);
     const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
@@ -1100,7 +1144,7 @@ __global__ void rescore_kernel(const float *__restrict__ X, const uint32_t *__re
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
                    const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,
-                   cudaStream_t s, const unsigned int *nc_dev)
+                   cudaStream_t s, const unsigned long long *nc_dev)
 {
     if (nc == 0) return OK;
     // host count: one 8-lane group per pair; device count: a grid-stride sweep

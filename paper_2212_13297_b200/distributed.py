@@ -14,7 +14,10 @@ from __future__ import annotations
 
 import numpy as np
 
-EMPTY = np.iinfo(np.int64).max
+# an empty slot (k > N): all bits set, i.e. UINT64_MAX read as unsigned -- the
+# K-merge kernel's KEY_EMPTY.  Keys travel as int64 tensors (collectives have
+# no uint64); every host-side ordering views them as uint64.
+EMPTY = -1
 
 
 def shard_range(N: int, rank: int, world: int) -> tuple[int, int]:
@@ -24,29 +27,51 @@ def shard_range(N: int, rank: int, world: int) -> tuple[int, int]:
 
 def pack_keys(d2, ids):
     """(d2 float32, ids int64) -> int64 keys (d2 bits << 32 | id); missing -> EMPTY.
-    Works on numpy arrays and torch tensors (CPU or CUDA)."""
+
+    CUDA tensors are packed on the device by ``ssb_pack_keys`` (one kernel);
+    numpy arrays and CPU tensors (the gloo tests) on the host."""
     try:
         import torch
 
         if isinstance(d2, torch.Tensor):
-            keys = (d2.contiguous().view(torch.int32).to(torch.int64) << 32) | ids.clamp_min(0)
-            return torch.where(ids < 0, torch.full_like(keys, EMPTY), keys)
+            if d2.is_cuda:
+                from . import _lib
+                from ._device import ptr, stream_handle
+
+                d2c, idc = d2.contiguous(), ids.contiguous()
+                keys = torch.empty(d2c.shape, dtype=torch.int64, device=d2c.device)
+                _lib.call("ssb_pack_keys", ptr(d2c), ptr(idc), d2c.numel(), ptr(keys), stream_handle())
+                return keys
+            return torch.from_numpy(pack_keys(d2.numpy(), ids.numpy()))
     except ImportError:  # pragma: no cover
         pass
     d2 = np.ascontiguousarray(d2, np.float32)
-    keys = (d2.view(np.int32).astype(np.int64) << 32) | np.maximum(ids, 0)
-    return np.where(ids < 0, EMPTY, keys)
+    ids = np.asarray(ids, np.int64)
+    keys = (d2.view(np.uint32).astype(np.uint64) << np.uint64(32)) | (ids & 0xFFFFFFFF).astype(np.uint64)
+    keys = np.where(ids < 0, np.uint64(0xFFFFFFFFFFFFFFFF), keys)
+    return keys.view(np.int64)
 
 
 def unpack_keys(keys):
-    """int64 keys -> (d2 float32, ids int64) with (inf, -1) for EMPTY (numpy)."""
-    keys = np.asarray(keys)
-    empty = keys == EMPTY
-    d2 = (keys >> 32).astype(np.int32).view(np.float32)
-    ids = (keys & 0xFFFFFFFF).astype(np.int64)
+    """int64 (or uint64) keys -> (d2 float32, ids int64) with (inf, -1) for EMPTY (numpy)."""
+    keys = np.ascontiguousarray(keys)
+    u = keys.view(np.uint64) if keys.dtype == np.int64 else keys.astype(np.uint64)
+    empty = u == np.uint64(0xFFFFFFFFFFFFFFFF)
+    d2 = (u >> np.uint64(32)).astype(np.uint32).view(np.float32)
+    ids = (u & np.uint64(0xFFFFFFFF)).astype(np.int64)
     d2 = np.where(empty, np.float32(np.inf), d2)
     ids = np.where(empty, -1, ids)
     return d2, ids
+
+
+def host_merge(all_keys, k: int):
+    """Host K-merge (tests, gloo): the k smallest keys of each row, unsigned order."""
+    a = all_keys.numpy() if hasattr(all_keys, "numpy") else np.asarray(all_keys)
+    u = np.sort(np.ascontiguousarray(a).view(np.uint64), axis=1)[:, :k]
+    if u.shape[1] < k:
+        pad = np.full((u.shape[0], k - u.shape[1]), np.uint64(0xFFFFFFFFFFFFFFFF))
+        u = np.concatenate([u, pad], axis=1)
+    return unpack_keys(u)
 
 
 def gather_keys(keys, group=None):

@@ -123,10 +123,11 @@ class QueryEngine:
     returns ``(ResultSet, QueryStats)``; ``exact_knn_batch`` answers a whole
     block in one device pass (the only API addition); and
     ``knn_device`` is the zero-copy form for device-resident query blocks.
-    ``lmax``, ``eapca_th``, ``sax_th`` and ``num_threads`` are validated and
-    only select the reported phase label: the device pipeline always runs
-    every pruning stage, and the answers do not depend on them (the
-    reference's path-invariance property, test_query.py:213-228).
+    ``lmax`` bounds the leaves the approximate phase visits and ``eapca_th``
+    feeds the reference's routing rule (route="eapca"); ``sax_th`` and
+    ``num_threads`` are validated and only select the reported phase label.
+    The answers do not depend on any of them (the reference's path-invariance
+    property, test_query.py:213-228).
     """
 
     def __init__(self, index):
@@ -144,8 +145,9 @@ class QueryEngine:
     ROUTES = {"auto": 0, "tree": 1, "tensor": 2, "eapca": 3}
 
     def knn_device(self, Q, k: int, want_stats: bool = False, eapca_th: float = 0.25,
-                   route: str = "auto"):
-        """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,4) u32].
+                   route: str = "auto", lmax: int = 80):
+        """(d2 (B,k) f32, ids (B,k) i64, pos (B,k) i64) CUDA tensors [+ stats (B,8) u32,
+        the SSB_QUERY_STATS columns of include/seriesearch_b200.h].
 
         ``route``: "auto" picks, per query, the cheaper exact path by a
         B200-calibrated cost model; "eapca" applies the
@@ -162,17 +164,19 @@ class QueryEngine:
         d2 = t.empty((B, k), dtype=t.float32, device=X.device)
         ids = t.empty((B, k), dtype=t.int64, device=X.device)
         pos = t.empty((B, k), dtype=t.int64, device=X.device)
-        stats = np.zeros((B, 4), dtype=np.uint32) if want_stats else None
+        stats = np.zeros((B, _lib.QUERY_STATS), dtype=np.uint32) if want_stats else None
         if route not in self.ROUTES:
             raise UsageError(f"route must be one of {sorted(self.ROUTES)}")
-        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route])
+        if lmax < 1:
+            raise UsageError("lmax must be at least 1")
+        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route], int(lmax))
         import ctypes as _ct
 
         _lib.call("ssb_query", self._si.handle, ptr(X), B, k, _ct.byref(cfg), ptr(d2), ptr(ids), ptr(pos),
                   stats.ctypes.data_as(_lib.P) if want_stats else None, stream_handle())
         return (d2, ids, pos, stats) if want_stats else (d2, ids, pos)
 
-    def knn_device_multi(self, calls, eapca_th: float = 0.25, route: str = "auto"):
+    def knn_device_multi(self, calls, eapca_th: float = 0.25, route: str = "auto", lmax: int = 80):
         """Several query blocks in one call: ``calls`` = [(Q, k), ...] ->
         [(d2, ids, pos), ...] CUDA tensors, each as ``knn_device(Q, k)``.
         The blocks are enqueued back to back with one host round trip for all
@@ -198,7 +202,7 @@ class QueryEngine:
                          t.empty((B, k), dtype=t.int64, device=X.device)))
         P = _ct.c_void_p * max(1, nc)
         I = _ct.c_int32 * max(1, nc)
-        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route])
+        cfg = _lib.QueryCfg(float(eapca_th), self.ROUTES[route], int(lmax))
         _lib.call("ssb_query_multi", self._si.handle, nc, P(*[X.data_ptr() for X in Xs]),
                   I(*[X.shape[0] for X in Xs]), I(*[int(k) for _, k in calls]), _ct.byref(cfg),
                   P(*[o[0].data_ptr() for o in outs]), P(*[o[1].data_ptr() for o in outs]),
@@ -213,16 +217,24 @@ class QueryEngine:
         return d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
 
     def _stats(self, row, cfg: QueryConfig, wall: float) -> QueryStats:
+        """QueryStats (query.py:102-114) from one row of the device counters.
+
+        ``series_read`` counts the series whose raw values the query actually
+        read (the reference's SeriesStore accounting, persist.py:88-122): on the
+        index route the approximate phase's exactly scanned series plus the
+        LB_SAX survivors (an early-abandoned survivor was read in part); on the
+        tensor-core route every row (its BF16 copy streams through the filter)."""
         n = self.settings.series_length
         cand_leaves, cand_series, seed_rows = int(row[0]), int(row[1]), int(row[2])
+        seed_leaves, words, tc = int(row[4]), int(row[5]), int(row[7])
         st = QueryStats()
-        st.visited_leaves = 1 if seed_rows else 0
+        st.visited_leaves = seed_leaves
         st.candidate_leaves = cand_leaves
         st.candidate_series = cand_series
         st.eapca_pr = 1.0 - cand_leaves / max(1, self.total_leaves)
         st.sax_pr = 1.0 - cand_series / max(1, self.total_series)
         # phase label by the reference's decision rules (query.py:321-341)
-        if st.eapca_pr < cfg.eapca_th:
+        if tc or st.eapca_pr < cfg.eapca_th:
             st.phase_reached = "scan2"
         elif st.sax_pr < cfg.sax_th:
             st.phase_reached = "scan3"
@@ -232,13 +244,17 @@ class QueryEngine:
             st.phase_reached = "3"
         else:
             st.phase_reached = "1"
-        st.series_read = min(self.total_series, seed_rows + cand_series)
-        st.bytes_read = st.series_read * n * 4
+        if tc:
+            st.series_read = self.total_series
+            st.bytes_read = self.total_series * n * 2 + cand_series * n * 4  # BF16 pass + exact rescoring
+        else:
+            st.series_read = min(self.total_series, seed_rows + cand_series)
+            st.bytes_read = st.series_read * n * 4 + words * 16  # rows + SAX words tested
         st.fraction_data_accessed = st.series_read / max(1, self.total_series)
         st.wall_seconds = wall
         return st
 
-    def exact_knn_batch(self, queries, cfg: QueryConfig):
+    def exact_knn_batch(self, queries, cfg: QueryConfig, route: str = "auto"):
         import time
 
         cfg.validate()
@@ -249,7 +265,8 @@ class QueryEngine:
         if not np.isfinite(Q).all():
             raise UsageError("queries must be finite (documented deviation: NaN keys break ordering)")
         t0 = time.perf_counter()
-        d2, ids, pos, stats = self.knn_device(Q, cfg.k, want_stats=True, eapca_th=cfg.eapca_th)
+        d2, ids, pos, stats = self.knn_device(Q, cfg.k, want_stats=True, eapca_th=cfg.eapca_th, lmax=cfg.lmax,
+                                              route=route)
         d2, ids, pos = d2.cpu().numpy(), ids.cpu().numpy(), pos.cpu().numpy()
         wall = (time.perf_counter() - t0) / max(1, Q.shape[0])
         return [(ResultSet.from_arrays(d2[i], pos[i], ids[i]), self._stats(stats[i], cfg, wall))

@@ -22,10 +22,9 @@ def _free_port():
 
 
 def _host_merge(all_keys, k):
-    from paper_2212_13297_b200.distributed import unpack_keys
+    from paper_2212_13297_b200.distributed import host_merge
 
-    keys = np.sort(all_keys.numpy(), axis=1)[:, :k]
-    return unpack_keys(keys)
+    return host_merge(all_keys, k)
 
 
 def _worker(rank, world, port, X, Q, k, out):
@@ -88,3 +87,19 @@ def test_shard_ranges_cover_and_pack_roundtrip():
     ids = np.array([[3, 2**31 + 5, -1]], np.int64)
     back = unpack_keys(pack_keys(d2, ids))
     assert np.array_equal(back[0], d2) and np.array_equal(back[1], ids)
+    # empty slots are all-ones keys (the K-merge kernel's KEY_EMPTY) and sort last
+    keys = pack_keys(d2, ids)
+    assert keys[0, 2] == -1 and keys.view(np.uint64)[0, 2] == np.uint64(2**64 - 1)
+
+
+def test_host_merge_pads_k_above_n():
+    """k > total rows: missing answers come back as (inf, -1), like query.py:70-75."""
+    import torch
+
+    from paper_2212_13297_b200.distributed import host_merge, pack_keys
+
+    a = pack_keys(np.array([[1.0, np.inf]], np.float32), np.array([[4, -1]], np.int64))
+    b = pack_keys(np.array([[0.5, np.inf]], np.float32), np.array([[9, -1]], np.int64))
+    d2, ids = host_merge(torch.from_numpy(np.concatenate([a, b], axis=1)), 5)
+    assert list(ids[0]) == [9, 4, -1, -1, -1]
+    assert d2[0, 0] == np.float32(0.5) and np.isinf(d2[0, 2:]).all()

@@ -148,3 +148,18 @@ def test_segment_stats_contiguous_partitions(ssb, oracle, m, N):
     omean, osd = oracle.segment_stats(X, starts, ends)
     assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
     assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))
+
+
+@pytest.mark.parametrize("starts,ends", [([0, 1000, 1500], [1500, 2048, 1501]),  # widths 1500, 1048, 1
+                                         ([0], [2048])])                          # one 2048-wide segment
+def test_segment_stats_wide_segments(ssb, oracle, starts, ends):
+    """Segments wider than the reciprocal table (w > 1024, n = 2048): the
+    division falls back to IEEE division and stays bit-identical to
+    summarize.py:79-82."""
+    from paper_2212_13297_b200.summarize import segment_stats_matrix
+
+    X = random_walks(700, 2048, 41)
+    mean, sd = segment_stats_matrix(X, np.array(starts), np.array(ends))
+    omean, osd = oracle.segment_stats(X, np.array(starts), np.array(ends))
+    assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
+    assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))
