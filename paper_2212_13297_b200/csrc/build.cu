@@ -49,6 +49,7 @@ namespace ssb {
 
 Index::~Index()
 {
+    free_small_graphs(*this);
     void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec,
                     tcperm};
     for (void *p : ptrs)

@@ -32,6 +32,7 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 }
 
 void note_launch(int count) { g_launches.fetch_add(count, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
 
 // keep freed stream-ordered allocations cached in the device's default pool
 // (the default release threshold of 0 hands them back to the driver at every
@@ -73,6 +74,12 @@ __global__ void iota_kernel(int32_t *a, int n)
     if (i < n) a[i] = i;
 }
 
+__global__ void fill_u32_kernel(uint32_t *p, int n, uint32_t v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
 int bruteforce_knn(const float *X, int64_t N, int n, const float *Q, int B, int k, int64_t id_base,
                    float *out_d2, int64_t *out_id, cudaStream_t s)
 {
@@ -81,8 +88,11 @@ int bruteforce_knn(const float *X, int64_t N, int n, const float *Q, int B, int 
     SSB_REQUIRE(N >= 0 && B >= 0, "negative sizes");
     SSB_REQUIRE(N + id_base < (1ll << 32), "row ids must fit in 32 bits");
     if (B == 0) return OK;
-    // capacity: each row range dumps <= k keys per query (see launch_scan_dense)
-    const int cap = (int)(dense_ranges(N, B, k, 16384) * k);
+    // few queries: the row-parallel early-abandoning scan (every group on
+    // its own rows); otherwise the dense shape (one query per group)
+    const bool rows = B <= 4 && N > 0 && (n == 64 || n == 96 || n == 128 || n == 256);
+    // capacity: each row range dumps <= k keys per query
+    const int cap = rows ? rowscan_ranges(N, k) * k : (int)(dense_ranges(N, B, k, 16384) * k);
     DevBuf cand, cnt, keys, flags, qidx;
     SSB_CUDA(cand.alloc((size_t)B * cap * 8, s));
     SSB_CUDA(cnt.alloc((size_t)B * 4, s));
@@ -93,7 +103,15 @@ int bruteforce_knn(const float *X, int64_t N, int n, const float *Q, int B, int 
     iota_kernel<<<(B + 255) / 256, 256, 0, s>>>(qidx.as<int32_t>(), B);
     SSB_CHECK_LAUNCH();
     ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), nullptr, cap};
-    int rc = launch_scan_dense(X, N, n, Q, qidx.as<int32_t>(), B, k, (uint32_t)id_base, so, s);
+    int rc;
+    if (rows) {
+        // every range dumps exactly k keys (KEY_EMPTY past the rows): counts are known
+        fill_u32_kernel<<<(B + 255) / 256, 256, 0, s>>>(cnt.as<uint32_t>(), B, (uint32_t)cap);
+        SSB_CHECK_LAUNCH();
+        rc = launch_scan_rows(X, N, n, Q, B, k, (uint32_t)id_base, so, s);
+    } else {
+        rc = launch_scan_dense(X, N, n, Q, qidx.as<int32_t>(), B, k, (uint32_t)id_base, so, s);
+    }
     if (rc) return rc;
     // no bound array: select never tightens here (dense dumps cannot overflow)
     DevBuf thr;

@@ -131,8 +131,8 @@ __global__ void ix_lbe_kernel(const double *__restrict__ cs_g, const double *__r
         for (int i = 0; i < m; i++) {
             const int sb = ep[i];
             const double wd = (double)(sb - sa);
-            const double mu = __ddiv_rn(__dsub_rn(cs[sb], cs[sa]), wd);
-            const double msq = __ddiv_rn(__dsub_rn(c2[sb], c2[sa]), wd);
+            const double mu = div_w(__dsub_rn(cs[sb], cs[sa]), sb - sa);
+            const double msq = div_w(__dsub_rn(c2[sb], c2[sa]), sb - sa);
             const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
             const double qm = (double)__double2float_rn(mu);
             const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
@@ -148,6 +148,45 @@ __global__ void ix_lbe_kernel(const double *__restrict__ cs_g, const double *__r
         v = pw_f64_small(t, m);
     }
     lbe[(int64_t)q * L + l] = v;
+}
+
+// Q2 for small blocks: a warp per leaf, a lane per segment (the divisions of
+// one leaf run in parallel), the terms summed by lane 0 in numpy's pairwise
+// order -- the same bits as ix_lbe_kernel
+__global__ void __launch_bounds__(256)
+    ix_lbe_warp_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n, int L,
+                       const int32_t *__restrict__ leaf_m, const int32_t *__restrict__ leaf_ep,
+                       const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
+                       double *__restrict__ lbe)
+{
+    __shared__ double terms[8][M_MAX];
+    const int q = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int l = blockIdx.x * 8 + warp;
+    if (l >= L) return;
+    const double *cs = cs_g + (int64_t)q * (n + 1), *c2 = c2_g + (int64_t)q * (n + 1);
+    if (!leaf_count[l]) {
+        if (lane == 0) lbe[(int64_t)q * L + l] = __longlong_as_double(0x7ff0000000000000ll);
+        return;
+    }
+    const int m = leaf_m[l];
+    if (lane < m) {
+        const int32_t *ep = leaf_ep + (int64_t)l * M_MAX;
+        const float *env = leaf_env + (int64_t)l * M_MAX * 4 + lane * 4;
+        const int sa = lane ? ep[lane - 1] : 0, sb = ep[lane];
+        const double wd = (double)(sb - sa);
+        const double mu = div_w(__dsub_rn(cs[sb], cs[sa]), sb - sa);
+        const double msq = div_w(__dsub_rn(c2[sb], c2[sa]), sb - sa);
+        const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
+        const double qm = (double)__double2float_rn(mu);
+        const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
+        double gm = fmax(__dsub_rn((double)env[0], qm), __dsub_rn(qm, (double)env[1]));
+        gm = fmax(gm, 0.0);
+        double gs = fmax(__dsub_rn((double)env[2], qs), __dsub_rn(qs, (double)env[3]));
+        gs = fmax(gs, 0.0);
+        terms[warp][lane] = __dmul_rn(wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
+    }
+    __syncwarp();
+    if (lane == 0) lbe[(int64_t)q * L + l] = pw_f64_small(terms[warp], m);
 }
 
 // ---------------------------------------------------------------------------
@@ -253,7 +292,7 @@ struct SeedOut {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     ix_seed_kernel(const float *__restrict__ X, const uint4 *__restrict__ words, const uint32_t *__restrict__ orig,
                    int L, const uint32_t *__restrict__ leaf_first, const uint32_t *__restrict__ leaf_count,
                    const double *__restrict__ lbe, const float *__restrict__ tbl, const float *__restrict__ Qp,
@@ -264,8 +303,8 @@ __global__ void __launch_bounds__(256)
     __shared__ uint32_t cand[IX_CMAX];
     __shared__ uint64_t keys[IX_CMAX];
     __shared__ int32_t picked[IX_SEED_MAX];
-    __shared__ double rv[8];
-    __shared__ int rl[8];
+    __shared__ double rv[32];
+    __shared__ int rl[32];
     __shared__ uint32_t s_np, s_rows, s_cut, s_nc;
     const int q = qlist ? qlist[blockIdx.x] : blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -310,7 +349,7 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();
         if (tid == 0) {
-            for (int w = 1; w < 8; w++)
+            for (int w = 1; w < (int)(blockDim.x >> 5); w++)
                 if (rv[w] < bv || (rv[w] == bv && rl[w] < bl)) {
                     bv = rv[w];
                     bl = rl[w];
@@ -393,7 +432,7 @@ __global__ void __launch_bounds__(256)
         const unsigned gmask = 0xffu << (lane & 24);
         float qv[NT / 8];
         lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
-        for (int c = g; c < nc; c += 32) {
+        for (int c = g; c < nc; c += (int)(blockDim.x >> 3)) {
             const uint32_t pos = cand[c];
             float d2 = 0.f;
             int rd;
@@ -433,7 +472,11 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Q4: leaf pruning + work items + routing.  One CTA (256 threads) per query.
+// Q4: leaf pruning (find_candidate_leaves, query.py:200-214).  One CTA (256
+// threads) per query.  Pass 0 counts each query's kept leaves / rows / items
+// (and applies the device-side route rules: 1 index, 2 filter, 3 the
+// reference's eapca_th rule); pass 1 emits the items of the queries routed to
+// the index (use_tc[q] == 0).
 
 struct PlanOut {
     uint4 *items;            // (query, first row, end row, leaf)
@@ -442,15 +485,16 @@ struct PlanOut {
     int32_t *use_tc;         // [B] 1 = tensor-core filter for this query
     uint32_t *kept_leaves;   // [B]
     unsigned long long *kept_rows;  // [B]
+    uint32_t *q_items;       // [B]
 };
 
 __global__ void __launch_bounds__(256)
     ix_plan_kernel(int L, const uint32_t *__restrict__ leaf_first, const uint32_t *__restrict__ leaf_count,
                    const double *__restrict__ lbe, const uint64_t *__restrict__ thr, const double *__restrict__ slack,
-                   int mode, float eapca_th, double tc_cost_per_query, double lbs_cost_row, PlanOut po,
-                   const int32_t *__restrict__ qlist)
+                   int pass, int mode, float eapca_th, PlanOut po, const int32_t *__restrict__ qlist)
 {
     const int q = qlist ? qlist[blockIdx.x] : blockIdx.x;
+    if (pass == 1 && po.use_tc[q]) return;  // uniform
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double bound = ix_keep_bound(thr[q], slack[q]);
     const double *lq = lbe + (int64_t)q * L;
@@ -466,7 +510,6 @@ __global__ void __launch_bounds__(256)
     }
     __shared__ uint32_t s_nl[8], s_ni[8];
     __shared__ unsigned long long s_nr[8];
-    __shared__ int s_tc;
     __shared__ unsigned long long s_base;
     uint32_t a = nl, b = ni;
     unsigned long long r = nr;
@@ -495,23 +538,22 @@ __global__ void __launch_bounds__(256)
             ti += s_ni[w];
             tr += s_nr[w];
         }
-        int tc;
-        if (mode == 2)
-            tc = 1;
-        else if (mode == 1)
-            tc = 0;
-        else if (mode == 3)  // the reference's rule (query.py:321-325): weak envelope pruning -> scan
-            tc = (1.0 - (double)tl / (double)(L > 0 ? L : 1)) < (double)eapca_th ? 1 : 0;
-        else  // B200 cost model, in streamed bytes
-            tc = (double)tr * lbs_cost_row > tc_cost_per_query ? 1 : 0;
-        s_tc = tc;
-        po.use_tc[q] = tc;
-        po.kept_leaves[q] = tl;
-        po.kept_rows[q] = tr;
-        s_base = tc || ti == 0 ? 0ull : atomicAdd(po.n_items, (unsigned long long)ti);
+        if (pass == 0) {
+            int tc = 0;
+            if (mode == 2)
+                tc = 1;
+            else if (mode == 3)  // the reference's rule (query.py:321-325): weak envelope pruning -> scan
+                tc = (1.0 - (double)tl / (double)(L > 0 ? L : 1)) < (double)eapca_th ? 1 : 0;
+            po.use_tc[q] = tc;  // auto: decided on the host from these counts
+            po.kept_leaves[q] = tl;
+            po.kept_rows[q] = tr;
+            po.q_items[q] = ti;
+        } else {
+            s_base = ti ? atomicAdd(po.n_items, (unsigned long long)ti) : 0ull;
+        }
     }
+    if (pass == 0) return;
     __syncthreads();
-    if (s_tc) return;
     // item slots: warp offsets from the per-warp totals
     unsigned long long base = s_base;
     for (int w = 0; w < warp; w++) base += s_ni[w];
@@ -684,7 +726,10 @@ static int launch_seed_t(const Index &ix, const double *lbe, const float *tbl, c
 {
     const int target = std::min(IX_CMAX / 2, std::max(64, 4 * k));
     ProfScope ps("ix_seed", s, 0.0);
-    ix_seed_kernel<NT><<<B, 256, 0, s>>>(ix.X, reinterpret_cast<const uint4 *>(ix.words), ix.orig, ix.L, ix.leaf_first,
+    // one CTA per query: small blocks take 1024 threads so a single query's
+    // approximate phase still spreads over a whole SM
+    const int threads = B <= 2 * num_sms() ? 1024 : 256;
+    ix_seed_kernel<NT><<<B, threads, 0, s>>>(ix.X, reinterpret_cast<const uint4 *>(ix.words), ix.orig, ix.L, ix.leaf_first,
                                          ix.leaf_count, lbe, tbl, Qp, k, lmax, target, so, qlist);
     SSB_CHECK_LAUNCH();
     return OK;
@@ -730,15 +775,20 @@ int launch_query_prep(const float *Q, int B, int n, double *cs, double *c2, floa
 int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, double *lbe, cudaStream_t s)
 {
     if (ix.L == 0 || B == 0) return OK;
+    SSB_CUDA(upload_rcp_w());  // div_w's reciprocal table (a no-op after the first call)
     ProfScope ps("ix_lbe", s, (double)ix.L * (M_MAX * 20 + 12) + 16.0 * B * (ix.n + 1));
-    ix_lbe_kernel<<<dim3((unsigned)((ix.L + 127) / 128), (unsigned)B), 128, 16 * (ix.n + 1), s>>>(
-        cs, c2, ix.n, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_env, ix.leaf_count, lbe);
+    if ((int64_t)B * ix.L <= 64 * 1024)  // small blocks: a warp per leaf (latency)
+        ix_lbe_warp_kernel<<<dim3((unsigned)((ix.L + 7) / 8), (unsigned)B), 256, 0, s>>>(
+            cs, c2, ix.n, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_env, ix.leaf_count, lbe);
+    else
+        ix_lbe_kernel<<<dim3((unsigned)((ix.L + 127) / 128), (unsigned)B), 128, 16 * (ix.n + 1), s>>>(
+            cs, c2, ix.n, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_env, ix.leaf_count, lbe);
     SSB_CHECK_LAUNCH();
     return OK;
 }
 
-int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int mode, double tc_cost_per_query,
-             bool stats, IxWork &w, cudaStream_t s)
+int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int mode, bool stats, IxWork &w,
+             cudaStream_t s)
 {
     const int n = ix.n, L = ix.L;
     SSB_CUDA(w.cs.alloc(8 * (size_t)B * (n + 1), s));
@@ -753,6 +803,7 @@ int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, 
     SSB_CUDA(w.use_tc.alloc(4 * (size_t)B, s));
     SSB_CUDA(w.kept_leaves.alloc(4 * (size_t)B, s));
     SSB_CUDA(w.kept_rows.alloc(8 * (size_t)B, s));
+    SSB_CUDA(w.q_items.alloc(4 * (size_t)B, s));
     SSB_CUDA(w.n_items.alloc(8, s));
     SSB_CUDA(w.n_ents.alloc(8, s));
     if (stats) {
@@ -762,13 +813,6 @@ int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, 
         SSB_CUDA(w.abandoned.alloc(4 * (size_t)B, s));
         SSB_CUDA(cudaMemsetAsync(w.abandoned.p, 0, 4 * (size_t)B, s));
     }
-    // work items: the rows of every kept leaf, in <= IX_ITEM row chunks; the
-    // worst case (every leaf kept) bounds the buffer
-    const int64_t per_query_worst = ix.N / IX_ITEM + L + 1;
-    w.item_cap = std::min<int64_t>((int64_t)B * per_query_worst, 24ll << 20);
-    w.ent_cap = std::min<int64_t>(w.item_cap * (IX_ITEM / 32), 24ll << 20);
-    SSB_CUDA(w.items.alloc(16 * (size_t)w.item_cap, s));
-    SSB_CUDA(w.ents.alloc(16 * (size_t)w.ent_cap, s));
     SSB_CUDA(cudaMemsetAsync(w.n_items.p, 0, 8, s));
     SSB_CUDA(cudaMemsetAsync(w.n_ents.p, 0, 8, s));
     SSB_CUDA(cudaMemsetAsync(w.bad.p, 0, 4, s));
@@ -786,24 +830,32 @@ int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, 
                stats ? w.seed_rows.as<uint32_t>() : nullptr, stats ? w.seed_words.as<uint32_t>() : nullptr};
     rc = launch_seed(ix, w.lbe.as<double>(), w.tbl.as<float>(), w.qlay.as<float>(), B, k, qc.lmax, so, nullptr, s);
     if (rc) return rc;
-    PlanOut po{w.items.as<uint4>(), w.n_items.as<unsigned long long>(), w.item_cap, w.use_tc.as<int32_t>(),
-               w.kept_leaves.as<uint32_t>(), w.kept_rows.as<unsigned long long>()};
+    PlanOut po{nullptr, w.n_items.as<unsigned long long>(), 0, w.use_tc.as<int32_t>(), w.kept_leaves.as<uint32_t>(),
+               w.kept_rows.as<unsigned long long>(), w.q_items.as<uint32_t>()};
     ix_plan_kernel<<<B, 256, 0, s>>>(L, ix.leaf_first, ix.leaf_count, w.lbe.as<double>(), w.thr.as<uint64_t>(),
-                                     w.slack.as<double>(), mode, qc.eapca_th, tc_cost_per_query, IX_COST_LBS_ROW, po,
-                                     nullptr);
+                                     w.slack.as<double>(), 0, mode, qc.eapca_th, po, nullptr);
     SSB_CHECK_LAUNCH();
     return OK;
 }
 
-// the plan again for the queries in qlist with the index route forced (their
-// tensor-core filter overflowed): their items are appended to the work list
-int ix_replan_tree(const Index &ix, const QueryCfg &qc, IxWork &w, const int32_t *qlist, int nq, cudaStream_t s)
+// the work items of the queries routed to the index (use_tc[q] == 0), qlist
+// (nullable) restricting the queries considered; the buffers grow to `items`
+// items (and the worst-case entry count of those items, capped)
+int ix_emit(const Index &ix, IxWork &w, int B, const int32_t *qlist, int nq, int64_t items, cudaStream_t s)
 {
-    if (nq == 0) return OK;
+    if (items > w.item_cap) {
+        w.item_cap = items;
+        SSB_CUDA(w.items.alloc(16 * (size_t)std::max<int64_t>(items, 1), s));
+    }
+    const int64_t ents = std::min<int64_t>(w.item_cap * (IX_ITEM / 32), 64ll << 20);
+    if (ents > w.ent_cap || !w.ents.p) {
+        w.ent_cap = ents;
+        SSB_CUDA(w.ents.alloc(16 * (size_t)std::max<int64_t>(ents, 1), s));
+    }
     PlanOut po{w.items.as<uint4>(), w.n_items.as<unsigned long long>(), w.item_cap, w.use_tc.as<int32_t>(),
-               w.kept_leaves.as<uint32_t>(), w.kept_rows.as<unsigned long long>()};
-    ix_plan_kernel<<<nq, 256, 0, s>>>(ix.L, ix.leaf_first, ix.leaf_count, w.lbe.as<double>(), w.thr.as<uint64_t>(),
-                                      w.slack.as<double>(), 1, qc.eapca_th, 0.0, IX_COST_LBS_ROW, po, qlist);
+               w.kept_leaves.as<uint32_t>(), w.kept_rows.as<unsigned long long>(), w.q_items.as<uint32_t>()};
+    ix_plan_kernel<<<qlist ? nq : B, 256, 0, s>>>(ix.L, ix.leaf_first, ix.leaf_count, w.lbe.as<double>(),
+                                                  w.thr.as<uint64_t>(), w.slack.as<double>(), 1, 1, 0.f, po, qlist);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -826,6 +878,16 @@ int ix_back(const Index &ix, IxWork &w, int B, const int32_t *qskip, ScanOut so,
     }
     return launch_ixscan(ix, w.ents.as<uint4>(), w.n_ents.as<unsigned long long>(), w.ent_cap, w.qlay.as<float>(), so,
                          w.abandoned.p ? w.abandoned.as<uint32_t>() : nullptr, s);
+}
+
+// one-time device state of this translation unit (div_w's reciprocal table,
+// the occupancy-sized grids), set up before any CUDA-graph capture
+int ix_prepare()
+{
+    SSB_CUDA(upload_rcp_w());
+    (void)occupancy_grid((const void *)ix_lbs_kernel, 256, 0, 4);
+    (void)num_sms();
+    return OK;
 }
 
 }  // namespace ssb

@@ -52,6 +52,12 @@ ProfScope::ProfScope(const char *name, cudaStream_t s, double bytes, double flop
     cudaEventRecord((cudaEvent_t)a_, s_);
 }
 
+bool prof_enabled()
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    return g_on;
+}
+
 unsigned long long *ProfScope::counter()
 {
     std::lock_guard<std::mutex> g(g_mu);

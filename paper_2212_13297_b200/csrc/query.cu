@@ -123,6 +123,15 @@ __global__ void skip_unflagged_kernel(const int32_t *__restrict__ flags, const i
 }
 
 // returns -1 when a work buffer (items / entries) overflowed: the caller halves the block
+// blocks that take the index route entirely and emit their work without a
+// host round trip (query_batch's direct path): the CUDA-graph candidates
+static bool small_block_ok(const Index &ix, const QueryCfg &qc, int B)
+{
+    int mode = ix.Xb ? qc.route : 1;
+    if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= (double)ix.N * IX_NS_TC_ROW) mode = 1;
+    return mode == 1 && B <= 64 && (int64_t)B * (ix.N / 512 + ix.L + 1) <= (256 << 10);
+}
+
 static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, uint64_t *out_keys,
                        uint32_t *stats_host, cudaStream_t s)
 {
@@ -130,17 +139,19 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     int mode = ix.Xb ? qc.route : 1;
     if (k > TC_KTOP_MAX && mode != 1) mode = 1;
     const bool want = stats_host != nullptr;
-    // tensor-core filter cost of one query (bytes of BF16 rows it streams per
-    // query in a full 256-query cluster, or alone for small blocks)
-    const double tc_cost = (double)ix.N * 2.0 * n * IX_COST_TC_BYTE / (double)std::min(std::max(B, 1), 256);
     // auto: when even a query that keeps every leaf is cheaper on the index
-    // route (small blocks: the filter's pass is shared by few queries), no
-    // query can take the filter -- no routing round trip
-    if (mode == 0 && (double)ix.N * IX_COST_LBS_ROW <= tc_cost) mode = 1;
+    // route than a filter pass shared by the whole block (small blocks), no
+    // query takes the filter
+    const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW;
+    if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= tc_group_ns) mode = 1;
     IxWork w;
-    int rc = ix_front(ix, qc, Q, B, k, mode, tc_cost, want, w, s);
+    int rc = ix_front(ix, qc, Q, B, k, mode, want, w, s);
     if (rc) return rc;
-    const int cap = (int)std::min<int64_t>(std::max<int64_t>(16384, ix.N / 16), 262144);
+    // candidate keys per query: generous (bound tightening makes an overflow
+    // cost one more round, not an error), at most 2 GB per block
+    const int cap = (int)std::max<int64_t>(
+        std::max(4 * k, 4096), std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(16384, ix.N / 16), 262144),
+                                                 (2ll << 30) / (8 * (int64_t)B)));
     DevBuf cand, cnt, flags, skip, cser;
     SSB_CUDA(cand.alloc(8 * (size_t)B * cap, s));
     SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
@@ -152,16 +163,60 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     uint64_t *thr = w.thr.as<uint64_t>();
     ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), thr, cap};
 
-    // routing: the host needs the tensor-core subset (one round trip) unless
-    // the mode excludes the filter
+    // ---- routing -----------------------------------------------------------------
+    // Small index-only blocks emit their work items without a host round trip
+    // (worst-case buffers); otherwise the host reads each query's kept rows and
+    // items, routes (auto: the set of queries for the filter that minimises the
+    // modelled time, in whole 256-query groups), and sizes the items exactly.
+    const int64_t per_query_worst = ix.N / 512 + ix.L + 1;
     std::vector<int32_t> qtc;
-    if (mode != 1) {
-        std::vector<int32_t> h(B);
-        SSB_CUDA(cudaMemcpyAsync(h.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+    if (mode == 1 && (int64_t)B * per_query_worst <= (256 << 10)) {
+        rc = ix_emit(ix, w, B, nullptr, 0, (int64_t)B * per_query_worst, s);
+        if (rc) return rc;
+    } else {
+        std::vector<unsigned long long> kr(B);
+        std::vector<uint32_t> qi(B);
+        std::vector<int32_t> tc(B);
+        SSB_CUDA(cudaMemcpyAsync(kr.data(), w.kept_rows.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(qi.data(), w.q_items.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(tc.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
-        for (int q = 0; q < B; q++)
-            if (h[q]) qtc.push_back(q);
+        if (mode == 0) {
+            // queries by index cost, most expensive first; the filter takes a
+            // prefix of them, t in {0, 256, 512, ..., B} (within a group the
+            // filter's pass is already paid)
+            std::vector<int32_t> order(B);
+            for (int q = 0; q < B; q++) order[q] = q;
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return kr[a] > kr[b]; });
+            std::vector<double> suffix(B + 1, 0.0);
+            for (int i = B - 1; i >= 0; i--) suffix[i] = suffix[i + 1] + (double)kr[order[i]] * IX_NS_IX_ROW;
+            int best_t = 0;
+            double best = suffix[0];
+            for (int t = 256;; t += 256) {
+                const int tt = std::min(t, B);
+                const double cost = (double)((tt + 255) / 256) * tc_group_ns + suffix[tt];
+                if (cost < best) {
+                    best = cost;
+                    best_t = tt;
+                }
+                if (tt == B) break;
+            }
+            std::fill(tc.begin(), tc.end(), 0);
+            for (int i = 0; i < best_t; i++) tc[order[i]] = 1;
+            SSB_CUDA(cudaMemcpyAsync(w.use_tc.p, tc.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+        }
+        int64_t items = 0;
+        for (int q = 0; q < B; q++) {
+            if (tc[q])
+                qtc.push_back(q);
+            else
+                items += qi[q];
+        }
+        rc = ix_emit(ix, w, B, nullptr, 0, items, s);
+        if (rc) return rc;
+        SSB_CUDA(cudaStreamSynchronize(s));  // tc (the uploaded routes) dies here
     }
+
     // index route first (Q5 + Q6 of every query the plan kept on it)
     rc = ix_back(ix, w, B, mode != 1 ? w.use_tc.as<int32_t>() : nullptr, so, cser.as<uint32_t>(), s);
     if (rc) return rc;
@@ -205,7 +260,23 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         if ((int64_t)hn > tc_cap) {
             // still too many candidates: these queries take the index route
             SSB_CUDA(cudaMemsetAsync(w.use_tc.p, 0, 4 * (size_t)B, s));
-            rc = ix_replan_tree(ix, qc, w, d_qtc.as<int32_t>(), nq, s);
+            int64_t items = 0;
+            {
+                std::vector<uint32_t> qi(B);
+                SSB_CUDA(cudaMemcpyAsync(qi.data(), w.q_items.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+                SSB_CUDA(cudaStreamSynchronize(s));
+                for (int q : qtc) items += qi[q];
+            }
+            // the index queries' items stay; the filter's queries are appended
+            unsigned long long have = 0;
+            SSB_CUDA(cudaMemcpyAsync(&have, w.n_items.p, 8, cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+            if ((int64_t)(have + items) > w.item_cap) {  // grow: re-emit every index query
+                SSB_CUDA(cudaMemsetAsync(w.n_items.p, 0, 8, s));
+                rc = ix_emit(ix, w, B, nullptr, 0, (int64_t)have + items, s);
+            } else {
+                rc = ix_emit(ix, w, B, d_qtc.as<int32_t>(), nq, w.item_cap, s);
+            }
             if (rc) return rc;
             std::vector<int32_t> hs(B, 1);
             for (int q : qtc) hs[q] = 0;
@@ -475,6 +546,182 @@ static bool tc_all_for(const Index &ix, const QueryCfg &qc, int k)
 // overflowed is resubmitted (retry) or answered by index_query (redo), and
 // calls off the lean path go through index_query directly.  Same answers as
 // one index_query per call.
+// ---------------------------------------------------------------------------
+// Small blocks on the index route (the reference's own usage is one query per
+// call: query.py:296-348, bench.py:40-63): the whole route -- prep, LB_EAPCA,
+// approximate phase, plan, LB_SAX, early-abandoning scan, K-select -- is
+// captured once per (stream, B, k, lmax) as a CUDA graph and replayed; one
+// copy in, one graph launch, one round trip for the flags, one result kernel.
+// A replay whose flags report an overflow falls back to query_batch.
+
+struct SmallGraph {
+    cudaStream_t stream = nullptr;
+    int B = 0, k = 0, lmax = 0;
+    cudaGraphExec_t exec = nullptr;
+    float *qin = nullptr;       // B x n (device)
+    uint64_t *keys = nullptr;   // B x k (device)
+    void *dstat = nullptr;      // device status: flags[B] | bad | n_items | n_ents
+    int32_t *hstat = nullptr;   // pinned copy of it
+    int64_t item_cap = 0, ent_cap = 0;
+    int64_t launches = 0;       // kernels per replay
+    ~SmallGraph()
+    {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (qin) cudaFree(qin);
+        if (keys) cudaFree(keys);
+        if (dstat) cudaFree(dstat);
+        if (hstat) cudaFreeHost(hstat);
+    }
+};
+
+void free_small_graphs(Index &ix)
+{
+    for (SmallGraph *g : ix.graphs) delete g;
+    ix.graphs.clear();
+}
+
+// pinned status block of a replay: flags[B] (select overflow) | bad | n_items |
+// n_ents | stats[B][SSB_QUERY_STATS]
+static size_t stat_off_bad(int B) { return ((size_t)B * 4 + 7) / 8 * 8; }
+static size_t stat_off_stats(int B) { return stat_off_bad(B) + 24; }
+static size_t stat_bytes(int B) { return stat_off_stats(B) + (size_t)B * SSB_QUERY_STATS * 4; }
+
+__global__ void pack_stats_kernel(int B, const uint32_t *__restrict__ kept_leaves, const uint32_t *__restrict__ cser,
+                                  const uint32_t *__restrict__ seed_rows, const int32_t *__restrict__ over,
+                                  const uint32_t *__restrict__ seed_leaves,
+                                  const unsigned long long *__restrict__ kept_rows,
+                                  const uint32_t *__restrict__ seed_words, const uint32_t *__restrict__ abandoned,
+                                  uint32_t *__restrict__ out)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= B) return;
+    uint32_t *o = out + (size_t)q * SSB_QUERY_STATS;
+    o[0] = kept_leaves[q];
+    o[1] = cser[q];
+    o[2] = seed_rows[q];
+    o[3] = over[q] ? 1u : 0u;
+    o[4] = seed_leaves[q];
+    o[5] = (uint32_t)min(kept_rows[q] + seed_words[q], 0xffffffffull);
+    o[6] = abandoned[q];
+    o[7] = 0u;
+}
+
+// the route's stream-ordered work, without a host round trip (capturable)
+static int small_block_work(const Index &ix, const QueryCfg &qc, SmallGraph &g, cudaStream_t s)
+{
+    const int B = g.B, k = g.k;
+    IxWork w;
+    int rc = ix_front(ix, qc, g.qin, B, k, 1, true, w, s);
+    if (rc) return rc;
+    rc = ix_emit(ix, w, B, nullptr, 0, g.item_cap, s);
+    if (rc) return rc;
+    g.ent_cap = w.ent_cap;
+    const int cap = (int)std::max<int64_t>(std::max(4 * k, 4096),
+                                           std::min<int64_t>(std::max<int64_t>(16384, ix.N / 16), 262144));
+    DevBuf cand, cnt, cser;
+    SSB_CUDA(cand.alloc(8 * (size_t)B * cap, s));
+    SSB_CUDA(cnt.alloc(4 * (size_t)B, s));
+    SSB_CUDA(cser.alloc(4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)B, s));
+    SSB_CUDA(cudaMemsetAsync(cser.p, 0, 4 * (size_t)B, s));
+    ScanOut so{cand.as<uint64_t>(), cnt.as<uint32_t>(), w.thr.as<uint64_t>(), cap};
+    rc = ix_back(ix, w, B, nullptr, so, cser.as<uint32_t>(), s);
+    if (rc) return rc;
+    char *st = reinterpret_cast<char *>(g.dstat);
+    int32_t *flags = reinterpret_cast<int32_t *>(st);
+    rc = launch_select(cand.as<uint64_t>(), cnt.as<uint32_t>(), cap, B, k, w.thr.as<uint64_t>(), g.keys, flags, s);
+    if (rc) return rc;
+    SSB_CUDA(cudaMemcpyAsync(st + stat_off_bad(B), w.bad.p, 4, cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(st + stat_off_bad(B) + 8, w.n_items.p, 8, cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(st + stat_off_bad(B) + 16, w.n_ents.p, 8, cudaMemcpyDeviceToDevice, s));
+    pack_stats_kernel<<<(B + 127) / 128, 128, 0, s>>>(
+        B, w.kept_leaves.as<uint32_t>(), cser.as<uint32_t>(), w.seed_rows.as<uint32_t>(), flags,
+        w.seed_leaves.as<uint32_t>(), w.kept_rows.as<unsigned long long>(), w.seed_words.as<uint32_t>(),
+        w.abandoned.as<uint32_t>(), reinterpret_cast<uint32_t *>(st + stat_off_stats(B)));
+    SSB_CHECK_LAUNCH();
+    SSB_CUDA(cudaMemcpyAsync(g.hstat, g.dstat, stat_bytes(B), cudaMemcpyDeviceToHost, s));
+    return OK;
+}
+
+static int small_graph_get(const Index &ixc, const QueryCfg &qc, int B, int k, cudaStream_t s, SmallGraph **out)
+{
+    Index &ix = const_cast<Index &>(ixc);  // the graph cache is the only mutable part
+    for (SmallGraph *g : ix.graphs)
+        if (g->stream == s && g->B == B && g->k == k && g->lmax == qc.lmax) {
+            *out = g;
+            return OK;
+        }
+    std::unique_ptr<SmallGraph> g(new SmallGraph());
+    g->stream = s;
+    g->B = B;
+    g->k = k;
+    g->lmax = qc.lmax;
+    g->item_cap = (int64_t)B * (ix.N / 512 + ix.L + 1);
+    SSB_CUDA(cudaMalloc(&g->qin, 4 * (size_t)B * ix.n));
+    SSB_CUDA(cudaMalloc(&g->keys, 8 * (size_t)B * k));
+    SSB_CUDA(cudaMalloc(&g->dstat, stat_bytes(B)));
+    SSB_CUDA(cudaMallocHost(reinterpret_cast<void **>(&g->hstat), stat_bytes(B)));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    // warm: one-time uploads / attribute queries must not happen inside the capture
+    {
+        const int rc0 = ix_prepare();
+        if (rc0) return rc0;
+    }
+    const int64_t l0 = launch_count();
+    SSB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = small_block_work(ix, qc, *g, s);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s, &graph);
+    g->launches = launch_count() - l0;
+    note_launch(-(int)g->launches);  // captured, not launched
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    SSB_CUDA(e);
+    const cudaError_t e2 = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    SSB_CUDA(e2);
+    if (ix.graphs.size() >= 16) {  // bounded cache: drop the oldest
+        delete ix.graphs.front();
+        ix.graphs.erase(ix.graphs.begin());
+    }
+    ix.graphs.push_back(g.get());
+    *out = g.release();
+    return OK;
+}
+
+// 1: answered (out_keys written, stream-ordered); 0: take query_batch instead
+static int small_block_graph(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, uint64_t *out_keys,
+                             uint32_t *stats_host, int *done, cudaStream_t s)
+{
+    *done = 0;
+    Index &ixm = const_cast<Index &>(ix);
+    std::lock_guard<std::mutex> lock(ixm.graph_mu);
+    SmallGraph *g = nullptr;
+    int rc = small_graph_get(ix, qc, B, k, s, &g);
+    if (rc) return rc;
+    SSB_CUDA(cudaMemcpyAsync(g->qin, Q, 4 * (size_t)B * ix.n, cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaGraphLaunch(g->exec, s));
+    note_launch((int)g->launches);
+    SSB_CUDA(cudaStreamSynchronize(s));
+    const char *hs = reinterpret_cast<const char *>(g->hstat);
+    uint32_t bad;
+    unsigned long long n_items, n_ents;
+    std::memcpy(&bad, hs + stat_off_bad(B), 4);
+    std::memcpy(&n_items, hs + stat_off_bad(B) + 8, 8);
+    std::memcpy(&n_ents, hs + stat_off_bad(B) + 16, 8);
+    SSB_REQUIRE(!bad, "queries must be finite");
+    if ((int64_t)n_items > g->item_cap || (int64_t)n_ents > g->ent_cap) return OK;
+    for (int q = 0; q < B; q++)
+        if (g->hstat[q]) return OK;  // a candidate buffer overflowed: the general path tightens
+    // the keys leave the shared buffer before the lock is released (stream order)
+    SSB_CUDA(cudaMemcpyAsync(out_keys, g->keys, 8 * (size_t)B * k, cudaMemcpyDeviceToDevice, s));
+    if (stats_host) std::memcpy(stats_host, hs + stat_off_stats(B), (size_t)B * SSB_QUERY_STATS * 4);
+    *done = 1;
+    return OK;
+}
+
 int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int64_t id_base, float *out_d2,
                 int64_t *out_id, int64_t *out_pos, uint32_t *stats_host, cudaStream_t s);
 
@@ -559,9 +806,9 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
     for (int32_t l : ix.leaves) leaves_nonempty += ix.nodes[l].count > 0 ? 1u : 0u;
     DevBuf keys;
     SSB_CUDA(keys.alloc(8 * (size_t)B * k, s));
-    // blocks bounded by the index path's work buffers: worst case every leaf kept
-    const int64_t per_query_worst = ix.N / 512 + ix.L + 1;
-    int bq = (int)std::max<int64_t>(1, std::min<int64_t>(B, std::max<int64_t>(64, (24ll << 20) / per_query_worst)));
+    // blocks of up to 8192 queries (the index path sizes its work buffers per
+    // block; a block whose buffers still overflow is halved)
+    int bq = std::min(B, 8192);
     for (int q0 = 0; q0 < B;) {
         if (tc_all) {
             const int nb = std::min(8192, B - q0);
@@ -594,6 +841,17 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
             // a buffer overflowed: this block takes the general path
         }
         const int nb = std::min(bq, B - q0);
+        if (small_block_ok(ix, qc, nb) && !prof_enabled() && !getenv("SSB_NO_GRAPH")) {
+            int done = 0;
+            const int rcg = small_block_graph(ix, qc, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
+                                              stats_host ? stats_host + (size_t)q0 * SSB_QUERY_STATS : nullptr, &done,
+                                              s);
+            if (rcg) return rcg;
+            if (done) {
+                q0 += nb;
+                continue;
+            }
+        }
         const int rc = query_batch(ix, qc, Q + (int64_t)q0 * n, nb, k, keys.as<uint64_t>() + (int64_t)q0 * k,
                                    stats_host ? stats_host + (size_t)q0 * SSB_QUERY_STATS : nullptr, s);
         if (rc == -1) {  // a work buffer overflowed: halve the block and retry

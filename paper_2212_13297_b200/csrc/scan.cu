@@ -122,6 +122,145 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---------------------------------------------------------------------------
+// row-parallel scan for few queries (B <= ROWSCAN_MAX_B): the 32 groups of a
+// CTA take different rows of its range for the SAME query (the dense shape
+// keeps one query per group and would idle 31 of 32 groups at B = 1).  Rows
+// come straight from global memory (L2/HBM; no reuse to stage for), each
+// group keeps its own sorted top-k in shared memory, and rows are abandoned
+// early against the tightest bound known: the group's own k-th key, the
+// CTA's (the minimum over its groups) or the query's global one (the minimum
+// over every CTA's published k-th), all bounds by k real distances.  At the
+// end the CTA's 32 lists are sorted together and its best k dumped.
+
+constexpr int ROWSCAN_MAX_B = 4;
+
+template <int NT>
+__global__ void __launch_bounds__(256)
+    scan_rows_kernel(const float *__restrict__ X, int64_t N, const float *__restrict__ Q, int k, uint32_t id_base,
+                     int64_t rows_per_range, int ranges, unsigned int *__restrict__ gbound, ScanOut out,
+                     unsigned long long *__restrict__ prof_bytes)
+{
+    extern __shared__ __align__(16) uint64_t lists[];  // 32 groups x k, later the CTA merge
+    __shared__ unsigned int cbound;
+    const int tid = threadIdx.x, lane = tid & 31, g = tid >> 3, j = tid & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const int q = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_range, r1 = tmin<int64_t>(N, r0 + rows_per_range);
+    for (int e = tid; e < 32 * k; e += blockDim.x) lists[e] = KEY_EMPTY;
+    if (tid == 0) cbound = 0x7f800000u;
+    float qv[NT / 8];
+#pragma unroll
+    for (int i = 0; i < NT / 8; i++) qv[i] = Q[(int64_t)q * NT + 8 * i + j];
+    __syncthreads();
+    uint64_t *mylist = lists + (size_t)g * k;
+    unsigned int *gq = gbound + q;
+    unsigned long long steps = 0;
+    int it = 0;
+    for (int64_t r = r0 + g; r < r1; r += 32, it++) {
+        const uint64_t kth = mylist[k - 1];
+        float bd2 = kth == KEY_EMPTY ? __int_as_float(0x7f800000) : key_d2(kth);
+        bd2 = fminf(bd2, __uint_as_float(*(volatile unsigned int *)&cbound));
+        if ((it & 7) == 0) bd2 = fminf(bd2, __uint_as_float(*(volatile unsigned int *)gq));
+        bd2 = __shfl_sync(gmask, bd2, lane & 24);  // one bound per group (the abandon test must be uniform)
+        float d2 = 0.f;
+        int rd = 0;
+        const bool alive = group_ed2_ab<NT>(X + r * NT, qv, j, gmask, bd2, d2, rd);
+        steps += (unsigned long long)rd;
+        if (alive && j == 0) {
+            const uint64_t key = make_key(d2, id_base + (uint32_t)r);
+            if (key < mylist[k - 1]) {
+                int p = k - 1;
+                while (p > 0 && mylist[p - 1] > key) {
+                    mylist[p] = mylist[p - 1];
+                    p--;
+                }
+                mylist[p] = key;
+                const uint64_t nk = mylist[k - 1];
+                if (nk != KEY_EMPTY) {
+                    const unsigned int b = (unsigned int)(nk >> 32);  // d2 bits of the k-th (>= 0: ordered)
+                    if (b < cbound) atomicMin(&cbound, b);
+                    if ((it & 7) == 0 && b < *(volatile unsigned int *)gq) atomicMin(gq, b);
+                }
+            }
+        }
+        __syncwarp(gmask);
+    }
+    // publish this CTA's bound, then its best k of the 32 group lists
+    __syncthreads();
+    if (tid == 0 && cbound < 0x7f800000u) atomicMin(gq, cbound);
+    int p2 = 1;
+    while (p2 < 32 * k) p2 <<= 1;
+    for (int e = 32 * k + tid; e < p2; e += blockDim.x) lists[e] = KEY_EMPTY;
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < p2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const uint64_t a = lists[lo], b = lists[hi];
+                if ((a > b) == up) {
+                    lists[lo] = b;
+                    lists[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < k; e += blockDim.x)
+        out.cand[(size_t)q * out.cap + (size_t)blockIdx.x * k + e] = lists[e];
+    if (prof_bytes) {
+        for (int off = 16; off; off >>= 1) steps += __shfl_xor_sync(0xffffffffu, steps, off);
+        if (lane == 0 && steps) atomicAdd(prof_bytes, steps * 4ull);
+    }
+}
+
+int rowscan_ranges(int64_t N, int k)
+{
+    const int64_t want = 4 * (int64_t)num_sms();
+    const int64_t by_rows = std::max<int64_t>(1, N / 256);
+    const int64_t by_smem = std::max<int64_t>(1, 262144 / std::max(k, 1));  // k keys dumped per range
+    return (int)std::max<int64_t>(1, std::min(std::min(want, by_rows), by_smem));
+}
+
+template <int NT>
+static int launch_rows_t(const float *X, int64_t N, const float *Q, int nq, int k, uint32_t id_base, ScanOut out,
+                         cudaStream_t s)
+{
+    int p2 = 1;
+    while (p2 < 32 * k) p2 <<= 1;
+    const int smem = p2 * 8;
+    SSB_REQUIRE(smem <= 227 * 1024, "k too large for the row scan");
+    SSB_CUDA(cudaFuncSetAttribute(scan_rows_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int ranges = rowscan_ranges(N, k);
+    const int64_t rpr = (N + ranges - 1) / ranges;
+    DevBuf gb;
+    SSB_CUDA(gb.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(cudaMemsetAsync(gb.p, 0x7f, 4 * (size_t)nq, s));  // 0x7f7f7f7f: a huge finite bound until set
+    ProfScope ps("scan_rows", s, 0.0);
+    scan_rows_kernel<NT><<<dim3((unsigned)ranges, (unsigned)nq), 256, smem, s>>>(
+        X, N, Q, k, id_base, rpr, ranges, gb.as<unsigned int>(), out, ps.counter());
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+int launch_scan_rows(const float *X, int64_t N, int n, const float *Q, int nq, int k, uint32_t id_base, ScanOut out,
+                     cudaStream_t s)
+{
+    if (nq == 0 || N == 0) return OK;
+    switch (n) {
+    case 64: return launch_rows_t<64>(X, N, Q, nq, k, id_base, out, s);
+    case 96: return launch_rows_t<96>(X, N, Q, nq, k, id_base, out, s);
+    case 128: return launch_rows_t<128>(X, N, Q, nq, k, id_base, out, s);
+    case 256: return launch_rows_t<256>(X, N, Q, nq, k, id_base, out, s);
+    default: break;
+    }
+    set_error(ERR_USAGE, "series length " + std::to_string(n) +
+                          " has no compiled scan kernel (supported: 64, 96, 128, 256)");
+    return ERR_USAGE;
+}
+
+// ---------------------------------------------------------------------------
 // K-select: per query, the k smallest (d2, id) keys of its candidate buffer.
 // Up to SELECT_SMALL candidates: bitonic sort in shared memory.  Above that:
 // an exact MSB radix select of the k-th key (8 passes of 8 bits over the

@@ -271,6 +271,66 @@ __device__ __forceinline__ float group_ed2(const float *__restrict__ xs, const f
     return group_block<0, NT, NT / 8>(xs, qv, j, gmask);
 }
 
+// group_ed2 of a row in GLOBAL memory (logical element order) with early
+// abandoning: lane j's elements 8i + j are loaded a stage of 8 steps (64
+// elements of the row) ahead of the arithmetic; after every stage but the
+// last, the partial sum (the same xor-shuffle tree) is a lower bound of the
+// final float32 sum -- round-to-nearest is monotone and every term is >= 0 --
+// and the row is abandoned once it exceeds bd2.  Returns false when
+// abandoned (the final d2 > bd2); otherwise d2 == group_ed2 bit for bit.
+template <int NT>
+__device__ __forceinline__ bool group_ed2_ab(const float *__restrict__ x, const float (&qv)[NT / 8], int j,
+                                             unsigned gmask, float bd2, float &d2, int &steps_read)
+{
+    constexpr int NI = NT / 8;                      // steps per lane
+    constexpr int BI = (NT > 128 ? 128 : NT) / 8;   // steps per pairwise block
+    constexpr int ST = 8;                           // steps per stage
+    constexpr int NS = (NI + ST - 1) / ST;
+    static_assert(NT % 8 == 0 && (NT <= 128 || NT == 256), "supported series lengths");
+    float v[NI];
+#pragma unroll
+    for (int i = 0; i < (2 * ST < NI ? 2 * ST : NI); i++) v[i] = __ldg(x + 8 * i + j);
+    int read = 2 * ST < NI ? 2 * ST : NI;
+    float acc = 0.f, done = 0.f;
+#pragma unroll
+    for (int st = 0; st < NS; st++) {
+#pragma unroll
+        for (int i = st * ST; i < (st + 1) * ST && i < NI; i++) {
+            const float d = __fsub_rn(v[i], qv[i]);
+            acc = (i % BI == 0) ? __fmul_rn(d, d) : __fadd_rn(acc, __fmul_rn(d, d));
+            if (i % BI == BI - 1) {
+                float a = __fadd_rn(acc, __shfl_xor_sync(gmask, acc, 1));
+                a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 2));
+                a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 4));
+                done = i / BI == 0 ? a : __fadd_rn(done, a);
+            }
+        }
+        if (st == NS - 1) break;
+        const int last = (st + 1) * ST - 1;
+        float lbv;
+        if (last % BI == BI - 1) {
+            lbv = done;
+        } else {
+            float a = __fadd_rn(acc, __shfl_xor_sync(gmask, acc, 1));
+            a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 2));
+            a = __fadd_rn(a, __shfl_xor_sync(gmask, a, 4));
+            lbv = last < BI ? a : __fadd_rn(done, a);
+        }
+        if (lbv > bd2) {  // uniform within the group
+            steps_read = read;
+            return false;
+        }
+#pragma unroll
+        for (int i = (st + 2) * ST; i < (st + 3) * ST && i < NI; i++) {
+            v[i] = __ldg(x + 8 * i + j);
+            read++;
+        }
+    }
+    steps_read = read;
+    d2 = done;
+    return true;
+}
+
 // cp.async.bulk (TMA 1-D bulk copy) global -> shared, completion on an mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
 {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <vector>
 
 #include "ssb_internal.h"
@@ -62,8 +63,14 @@ struct Index {
     float4 *tilec = nullptr;  // per 64-row half tile: two float4 of extremes of rowc
     double build_ms = 0.0;
     int32_t levels = 0;
+    // small query blocks on the index route replay a captured CUDA graph
+    // (query.cu SmallGraph; one per (stream, B, k, lmax)), freed with the index
+    std::mutex graph_mu;
+    std::vector<struct SmallGraph *> graphs;
     ~Index();
 };
+
+void free_small_graphs(Index &ix);
 
 struct QueryCfg {
     float eapca_th = 0.25f;  // query.py:45 default; < eapca_th -> tensor-core "scan" path
@@ -71,27 +78,30 @@ struct QueryCfg {
     int lmax = 80;           // query.py:44: leaves the approximate phase may visit
 };
 
-// index-path routing cost model (ixq.cu ix_plan_kernel), in
-// bytes streamed: a candidate-leaf row costs IX_COST_LBS_ROW (its 16-byte SAX
-// word plus the LB_SAX arithmetic and its share of the exact scan); the
-// tensor-core filter costs IX_COST_TC_BYTE per BF16 byte it streams per query
-constexpr double IX_COST_LBS_ROW = 24.0;
-constexpr double IX_COST_TC_BYTE = 1.0;
+// routing cost model (query.cu query_batch), B200-measured,
+// in nanoseconds: the tensor-core filter costs IX_NS_TC_ROW per row for every
+// group of 256 queries it answers (one pass over the BF16 rows per group); the
+// index route costs IX_NS_IX_ROW per row of the leaves a query keeps (its SAX
+// word, the LB_SAX arithmetic and its share of the exact scan of survivors)
+constexpr double IX_NS_TC_ROW = 0.14;
+constexpr double IX_NS_IX_ROW = 0.03;
 
 // Everything of one query block on the index path, stream-ordered; the
 // per-stage outputs the caller needs afterwards (bounds, routing, counters)
 // live in IxWork.
 struct IxWork {
-    DevBuf cs, c2, qpaa, qlay, tbl, slack, bad, lbe, thr, use_tc, kept_leaves, kept_rows, items, n_items, ents, n_ents;
+    DevBuf cs, c2, qpaa, qlay, tbl, slack, bad, lbe, thr, use_tc, kept_leaves, kept_rows, q_items, items, n_items, ents,
+        n_ents;
     DevBuf seed_leaves, seed_rows, seed_words, abandoned;
     int64_t item_cap = 0, ent_cap = 0;
 };
 
 
-int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int mode, double tc_cost_per_query,
-             bool stats, IxWork &w, cudaStream_t s);
+int ix_front(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, int mode, bool stats, IxWork &w,
+             cudaStream_t s);
+int ix_emit(const Index &ix, IxWork &w, int B, const int32_t *qlist, int nq, int64_t items, cudaStream_t s);
 int ix_back(const Index &ix, IxWork &w, int B, const int32_t *qskip, ScanOut so, uint32_t *cand_series, cudaStream_t s);
-int ix_replan_tree(const Index &ix, const QueryCfg &qc, IxWork &w, const int32_t *qlist, int nq, cudaStream_t s);
+int ix_prepare();
 int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, double *lbe, cudaStream_t s);
 
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,

@@ -20,6 +20,9 @@ struct ScanOut {
 };
 
 int64_t dense_ranges(int64_t N, int nq, int k, int cap);
+int rowscan_ranges(int64_t N, int k);
+int launch_scan_rows(const float *X, int64_t N, int n, const float *Q, int nq, int k, uint32_t id_base, ScanOut out,
+                     cudaStream_t s);
 int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const int32_t *qidx,
                       int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
@@ -123,5 +126,7 @@ class ProfScope {
 
 // host-side launch accounting (counts kernels this library launched)
 void note_launch(int count = 1);
+int64_t launch_count();
+bool prof_enabled();
 
 }  // namespace ssb

@@ -365,3 +365,29 @@ def test_sharded_forest_merge_on_device(ssb, oracle):
     assert np.array_equal(gids.cpu().numpy(), oid)
     assert np.array_equal(bits(gd2.cpu().numpy()), bits(od2))
     assert list(gids.cpu().numpy()[-1][:2]) == [7, 8500]
+
+
+def test_small_blocks_cuda_graph_path(ssb, oracle):
+    """Blocks of <= 64 queries on the index route replay a captured CUDA graph
+    (one per stream, B, k, lmax); repeated calls, different k / lmax / block
+    sizes and the per-query API all give the oracle's answers, with stats."""
+    from paper_2212_13297_b200 import generate as G
+
+    X = G.random_walks(60_000, 256, 3, workers=4)
+    idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=256, dataset_size=len(X), leaf_threshold=2000))
+    eng = ssb.QueryEngine(idx)
+    Q = np.concatenate([G.noise_queries(X, 12, 0.05, 4), G.random_walks(4, 256, 5, workers=1)])
+    for k in (1, 10, 100):
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        for B in (1, 3, 16):
+            for rep in range(2):  # capture, then replay
+                for q0 in range(0, len(Q), B):
+                    d2, ids, _, st = eng.knn_device(Q[q0:q0 + B], k, want_stats=True)
+                    assert np.array_equal(ids.cpu().numpy(), oid[q0:q0 + B]), (k, B, q0)
+                    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2[q0:q0 + B])), (k, B, q0)
+                    assert (st[:, 7] == 0).all() and (st[:, 4] >= 1).all()
+    for lmax in (1, 80):
+        rs, qs = eng.exact_knn(Q[0], ssb.QueryConfig(k=5, lmax=lmax))
+        od2, oid = oracle.knn_scan(X, Q[:1], 5)
+        assert rs.ids() == list(oid[0]) and qs.visited_leaves <= lmax
+    del eng, idx  # the graphs are freed with the index

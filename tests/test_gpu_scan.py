@@ -163,3 +163,29 @@ def test_segment_stats_wide_segments(ssb, oracle, starts, ends):
     omean, osd = oracle.segment_stats(X, np.array(starts), np.array(ends))
     assert np.array_equal(bits(mean.cpu().numpy()), bits(omean))
     assert np.array_equal(bits(sd.cpu().numpy()), bits(osd))
+
+
+@pytest.mark.parametrize("n,N,B,k", [(256, 300_007, 1, 1), (256, 300_007, 1, 100), (96, 120_001, 2, 10),
+                                     (64, 50_000, 4, 256), (128, 1_000, 3, 7), (256, 37, 1, 50)])
+def test_bruteforce_few_queries_row_scan(ssb, oracle, n, N, B, k):
+    """B <= 4: the row-parallel early-abandoning scan (every group on its own
+    rows, bounds shared across groups and CTAs) -- ids and d2 bits equal the
+    oracle; N < k pads with (inf, -1)."""
+    X = random_walks(N, n, 3000 + N)
+    Q = np.concatenate([random_walks(B - 1, n, 4000 + B), X[[N // 2]]]) if B > 1 else X[[N // 3]] + 0.01
+    d2, ids = ssb.knn_batch(X, Q.astype(np.float32), k)
+    od2, oid = oracle.knn_scan(X, Q.astype(np.float32), k, threads=8)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+def test_bruteforce_row_scan_ties(ssb, oracle):
+    X = random_walks(70_000, 256, 77)
+    for i in (5, 33_333, 69_999):
+        X[i] = X[40_000]           # exact duplicates across CTAs and groups
+    Q = X[[40_000]].copy()
+    d2, ids = ssb.knn_batch(X, Q, 3)
+    assert list(ids.cpu().numpy()[0]) == [5, 33_333, 40_000]
+    od2, oid = oracle.knn_scan(X, Q, 10)
+    d2, ids = ssb.knn_batch(X, Q, 10)
+    assert np.array_equal(ids.cpu().numpy(), oid)
