@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <vector>
 
 #include "layout.cuh"
@@ -51,7 +52,7 @@ Index::~Index()
 {
     free_small_graphs(*this);
     void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec,
-                    tcperm};
+                    tcperm, segs, leaf_seg};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -944,7 +945,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
                 uint2 pk;
                 pk.x = (uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16);
                 pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
-                reinterpret_cast<uint2 *>(a.Xb + h * n)[c] = pk;
+                *reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(a.Xb) + tcx_offset(h, 4 * c, n)) = pk;
             }
         };
         if constexpr (W > 0) {
@@ -1161,7 +1162,15 @@ __global__ void hash_keys_kernel(uint32_t *__restrict__ keys, uint32_t *__restri
 static int alloc_tc_operands(Index &ix, DevBuf &tcinv, cudaStream_t s)
 {
     if (ix.n % 8 != 0 || ix.n > 256) return OK;
-    SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)ix.N * ix.n * 2));
+    // tile-major pre-swizzled BF16 operand (layout.cuh tcx_*): the padding rows
+    // of the last tile (and padding columns, if n is not a multiple of the chunk
+    // width) are zero
+    SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)tcx_bytes(ix.N, ix.n)));
+    if (ix.n % tcx_cw(ix.n) == 0)
+        SSB_CUDA(cudaMemsetAsync(static_cast<char *>(ix.Xb) + tcx_bytes(ix.N, ix.n) - tcx_tile_bytes(ix.n), 0,
+                                 (size_t)tcx_tile_bytes(ix.n), s));
+    else
+        SSB_CUDA(cudaMemsetAsync(ix.Xb, 0, (size_t)tcx_bytes(ix.N, ix.n), s));
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
     SSB_CUDA(cudaMalloc(&ix.xen, (size_t)ix.N * 8));
     SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)((ix.N + 127) / 128 * 128) * 16));  // padded to whole tiles
@@ -1678,6 +1687,36 @@ int finalize_tree(Index &ixr, cudaStream_t s)
         }
     }
     SSB_REQUIRE((int64_t)expect == ix->N, "leaf counts do not cover the dataset");
+    // the distinct segments [sa, sb) of all leaf segmentations (leaves share
+    // most of them): a query's statistics over each are computed once per query
+    // (K-lbe), not once per (query, leaf)
+    std::vector<int32_t> lseg((size_t)L * M_MAX, 0);
+    std::vector<int2> segs;
+    {
+        std::map<std::pair<int, int>, int> ids;
+        for (int i = 0; i < L; i++) {
+            int sa = 0;
+            for (int j = 0; j < lm[i]; j++) {
+                const int sb = lep[(size_t)i * M_MAX + j];
+                auto it = ids.find({sa, sb});
+                int id;
+                if (it == ids.end()) {
+                    id = (int)segs.size();
+                    ids[{sa, sb}] = id;
+                    segs.push_back(make_int2(sa, sb));
+                } else {
+                    id = it->second;
+                }
+                lseg[(size_t)i * M_MAX + j] = id;
+                sa = sb;
+            }
+        }
+    }
+    ix->S = (int32_t)segs.size();
+    SSB_CUDA(cudaMalloc(&ix->segs, 8 * (size_t)std::max<int>(ix->S, 1)));
+    SSB_CUDA(cudaMalloc(&ix->leaf_seg, 4 * (size_t)L * M_MAX));
+    SSB_CUDA(cudaMemcpyAsync(ix->segs, segs.data(), 8 * (size_t)ix->S, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(ix->leaf_seg, lseg.data(), 4 * (size_t)L * M_MAX, cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaMalloc(&ix->leaf_first, 4 * (size_t)L));
     SSB_CUDA(cudaMalloc(&ix->leaf_count, 4 * (size_t)L));
     SSB_CUDA(cudaMalloc(&ix->leaf_m, 4 * (size_t)L));

@@ -104,58 +104,95 @@ __global__ void ix_table_kernel(const float *__restrict__ Q, const float *__rest
 }
 
 // ---------------------------------------------------------------------------
-// Q2: LB_EAPCA of (query, leaf), one thread per leaf
+// Q2: LB_EAPCA of (query, leaf), query.py:127-135 -> summarize.py:170-181.
+// The query's float32-rounded mean / sd over a segment depend only on the
+// segment, and the leaves share most of their segments, so (a) ix_qseg
+// computes them once per (query, distinct segment) -- float64 prefix-sum
+// differences, the reciprocal-table division, float32 rounding, exactly the
+// reference's stats_from_prefix -- and (b) the per-(query, leaf) kernels only
+// take the gaps to the leaf envelope and sum the m terms in numpy's pairwise
+// order.  Same bits as evaluating every leaf from scratch.
 
-__global__ void ix_lbe_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n, int L,
-                              const int32_t *__restrict__ leaf_m, const int32_t *__restrict__ leaf_ep,
-                              const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
-                              double *__restrict__ lbe)
+__global__ void ix_qseg_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n, int S,
+                               const int2 *__restrict__ segs, int B, float2 *__restrict__ qseg)
 {
-    extern __shared__ double sm[];
-    double *cs = sm, *c2 = sm + (n + 1);
-    const int q = blockIdx.y;
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
-        cs[i] = cs_g[(int64_t)q * (n + 1) + i];
-        c2[i] = c2_g[(int64_t)q * (n + 1) + i];
-    }
-    __syncthreads();
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= L) return;
-    double v = __longlong_as_double(0x7ff0000000000000ll);
-    if (leaf_count[l]) {
-        const int32_t *ep = leaf_ep + (int64_t)l * M_MAX;
-        const float *env = leaf_env + (int64_t)l * M_MAX * 4;
-        const int m = leaf_m[l];
-        double t[M_MAX];
-        int sa = 0;
-        for (int i = 0; i < m; i++) {
-            const int sb = ep[i];
-            const double wd = (double)(sb - sa);
-            const double mu = div_w(__dsub_rn(cs[sb], cs[sa]), sb - sa);
-            const double msq = div_w(__dsub_rn(c2[sb], c2[sa]), sb - sa);
-            const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
-            const double qm = (double)__double2float_rn(mu);
-            const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
-            const double mmin = (double)env[i * 4 + 0], mmax = (double)env[i * 4 + 1];
-            const double smin = (double)env[i * 4 + 2], smax = (double)env[i * 4 + 3];
-            double gm = fmax(__dsub_rn(mmin, qm), __dsub_rn(qm, mmax));
-            gm = fmax(gm, 0.0);
-            double gs = fmax(__dsub_rn(smin, qs), __dsub_rn(qs, smax));
-            gs = fmax(gs, 0.0);
-            t[i] = __dmul_rn(wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
-            sa = sb;
-        }
-        v = pw_f64_small(t, m);
-    }
-    lbe[(int64_t)q * L + l] = v;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)B * S) return;
+    const int q = (int)(i / S), sg = (int)(i % S);
+    const int2 ab = segs[sg];
+    const double *cs = cs_g + (int64_t)q * (n + 1), *c2 = c2_g + (int64_t)q * (n + 1);
+    const double mu = div_w(__dsub_rn(cs[ab.y], cs[ab.x]), ab.y - ab.x);
+    const double msq = div_w(__dsub_rn(c2[ab.y], c2[ab.x]), ab.y - ab.x);
+    const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
+    qseg[i] = make_float2(__double2float_rn(mu), __double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0)));
 }
 
-// Q2 for small blocks: a warp per leaf, a lane per segment (the divisions of
-// one leaf run in parallel), the terms summed by lane 0 in numpy's pairwise
-// order -- the same bits as ix_lbe_kernel
+__device__ __forceinline__ double lbe_term(float2 qv, int wd, float mmin_f, float mmax_f, float smin_f, float smax_f)
+{
+    const double qm = (double)qv.x, qs = (double)qv.y;
+    double gm = fmax(__dsub_rn((double)mmin_f, qm), __dsub_rn(qm, (double)mmax_f));
+    gm = fmax(gm, 0.0);
+    double gs = fmax(__dsub_rn((double)smin_f, qs), __dsub_rn(qs, (double)smax_f));
+    gs = fmax(gs, 0.0);
+    return __dmul_rn((double)wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
+}
+
+// (b) for large blocks: a CTA takes 64 leaves (their segment ids, widths and
+// envelopes staged in shared memory, segment-major) x a block of queries
+constexpr int LBE_LEAVES = 64, LBE_QB = 32;
+
 __global__ void __launch_bounds__(256)
-    ix_lbe_warp_kernel(const double *__restrict__ cs_g, const double *__restrict__ c2_g, int n, int L,
-                       const int32_t *__restrict__ leaf_m, const int32_t *__restrict__ leaf_ep,
+    ix_lbe_kernel(const float2 *__restrict__ qseg, int S, int L, int B, const int32_t *__restrict__ leaf_m,
+                  const int32_t *__restrict__ leaf_ep, const int32_t *__restrict__ leaf_seg,
+                  const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
+                  double *__restrict__ lbe)
+{
+    __shared__ float env[M_MAX * 4 * LBE_LEAVES];
+    __shared__ uint16_t wid[M_MAX * LBE_LEAVES], sid[M_MAX * LBE_LEAVES];  // widths <= n, ids < n (n + 1) / 2
+    __shared__ int32_t lm[LBE_LEAVES];
+    __shared__ uint32_t lc[LBE_LEAVES];
+    const int l0 = blockIdx.x * LBE_LEAVES;
+    const int nl = min(LBE_LEAVES, L - l0);
+    for (int i = threadIdx.x; i < nl * M_MAX; i += blockDim.x) {
+        const int l = i / M_MAX, seg = i % M_MAX;
+        const int64_t g = (int64_t)(l0 + l) * M_MAX + seg;
+        wid[seg * LBE_LEAVES + l] = (uint16_t)(leaf_ep[g] - (seg ? leaf_ep[g - 1] : 0));
+        sid[seg * LBE_LEAVES + l] = (uint16_t)leaf_seg[g];
+        const float4 e = reinterpret_cast<const float4 *>(leaf_env)[g];
+        env[(seg * 4 + 0) * LBE_LEAVES + l] = e.x;
+        env[(seg * 4 + 1) * LBE_LEAVES + l] = e.y;
+        env[(seg * 4 + 2) * LBE_LEAVES + l] = e.z;
+        env[(seg * 4 + 3) * LBE_LEAVES + l] = e.w;
+    }
+    for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+        lm[i] = leaf_m[l0 + i];
+        lc[i] = leaf_count[l0 + i];
+    }
+    __syncthreads();
+    const int q0 = blockIdx.y * LBE_QB, q1 = min(B, q0 + LBE_QB);
+    const int sub = threadIdx.x / LBE_LEAVES, l = threadIdx.x % LBE_LEAVES;  // 4 queries at a time
+    if (l >= nl) return;
+    for (int q = q0 + sub; q < q1; q += 4) {
+        double v = __longlong_as_double(0x7ff0000000000000ll);
+        if (lc[l]) {
+            const float2 *qs = qseg + (int64_t)q * S;
+            const int m = lm[l];
+            double t[M_MAX];
+            for (int i = 0; i < m; i++)
+                t[i] = lbe_term(__ldg(qs + sid[i * LBE_LEAVES + l]), wid[i * LBE_LEAVES + l],
+                                env[(i * 4 + 0) * LBE_LEAVES + l], env[(i * 4 + 1) * LBE_LEAVES + l],
+                                env[(i * 4 + 2) * LBE_LEAVES + l], env[(i * 4 + 3) * LBE_LEAVES + l]);
+            v = pw_f64_small(t, m);
+        }
+        lbe[(int64_t)q * L + l0 + l] = v;
+    }
+}
+
+// (b) for small blocks: a warp per leaf, a lane per segment, the terms summed
+// by lane 0 in numpy's pairwise order
+__global__ void __launch_bounds__(256)
+    ix_lbe_warp_kernel(const float2 *__restrict__ qseg, int S, int L, const int32_t *__restrict__ leaf_m,
+                       const int32_t *__restrict__ leaf_ep, const int32_t *__restrict__ leaf_seg,
                        const float *__restrict__ leaf_env, const uint32_t *__restrict__ leaf_count,
                        double *__restrict__ lbe)
 {
@@ -163,27 +200,16 @@ __global__ void __launch_bounds__(256)
     const int q = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int l = blockIdx.x * 8 + warp;
     if (l >= L) return;
-    const double *cs = cs_g + (int64_t)q * (n + 1), *c2 = c2_g + (int64_t)q * (n + 1);
     if (!leaf_count[l]) {
         if (lane == 0) lbe[(int64_t)q * L + l] = __longlong_as_double(0x7ff0000000000000ll);
         return;
     }
     const int m = leaf_m[l];
     if (lane < m) {
-        const int32_t *ep = leaf_ep + (int64_t)l * M_MAX;
-        const float *env = leaf_env + (int64_t)l * M_MAX * 4 + lane * 4;
-        const int sa = lane ? ep[lane - 1] : 0, sb = ep[lane];
-        const double wd = (double)(sb - sa);
-        const double mu = div_w(__dsub_rn(cs[sb], cs[sa]), sb - sa);
-        const double msq = div_w(__dsub_rn(c2[sb], c2[sa]), sb - sa);
-        const double var = __dsub_rn(msq, __dmul_rn(mu, mu));
-        const double qm = (double)__double2float_rn(mu);
-        const double qs = (double)__double2float_rn(__dsqrt_rn(var > 0.0 ? var : 0.0));
-        double gm = fmax(__dsub_rn((double)env[0], qm), __dsub_rn(qm, (double)env[1]));
-        gm = fmax(gm, 0.0);
-        double gs = fmax(__dsub_rn((double)env[2], qs), __dsub_rn(qs, (double)env[3]));
-        gs = fmax(gs, 0.0);
-        terms[warp][lane] = __dmul_rn(wd, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs)));
+        const int64_t g = (int64_t)l * M_MAX + lane;
+        const float4 e = reinterpret_cast<const float4 *>(leaf_env)[g];
+        terms[warp][lane] = lbe_term(__ldg(qseg + (int64_t)q * S + leaf_seg[g]),
+                                     leaf_ep[g] - (lane ? leaf_ep[g - 1] : 0), e.x, e.y, e.z, e.w);
     }
     __syncwarp();
     if (lane == 0) lbe[(int64_t)q * L + l] = pw_f64_small(terms[warp], m);
@@ -296,7 +322,7 @@ __global__ void __launch_bounds__(1024)
     ix_seed_kernel(const float *__restrict__ X, const uint4 *__restrict__ words, const uint32_t *__restrict__ orig,
                    int L, const uint32_t *__restrict__ leaf_first, const uint32_t *__restrict__ leaf_count,
                    const double *__restrict__ lbe, const float *__restrict__ tbl, const float *__restrict__ Qp,
-                   int k, int lmax, int target, SeedOut so, const int32_t *__restrict__ qlist)
+                   int k, int lmax, int target, int min_leaves, SeedOut so, const int32_t *__restrict__ qlist)
 {
     __shared__ float T[IX_TBL];
     __shared__ uint32_t hist[2048];
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(1024)
     // (a) seed leaves: smallest LB_EAPCA first (ties -> lowest leaf) until >= k rows
     const int smax = min(IX_SEED_MAX, lmax);
     for (int it = 0; it < smax; it++) {
-        if (s_rows >= (uint32_t)k) break;  // uniform (read after a barrier)
+        if (s_rows >= (uint32_t)k && it >= min_leaves) break;  // uniform (read after a barrier)
         double bv = __longlong_as_double(0x7ff0000000000000ll);
         int bl = 0x7fffffff;
         const uint32_t np = s_np;
@@ -724,13 +750,19 @@ template <int NT>
 static int launch_seed_t(const Index &ix, const double *lbe, const float *tbl, const float *Qp, int B, int k, int lmax,
                          SeedOut so, const int32_t *qlist, cudaStream_t s)
 {
-    const int target = std::min(IX_CMAX / 2, std::max(64, 4 * k));
+    // candidates ranked then scanned exactly: a few times k (SSB_SEED_MULT, A/B
+    // switch), at least 64, at most the candidate buffer
+    const int mult = getenv("SSB_SEED_MULT") ? std::max(1, atoi(getenv("SSB_SEED_MULT"))) : 4;
+    const int target = std::min(IX_CMAX - 64, std::max(64, mult * k));
+    // leaves ranked at least (SSB_SEED_LEAVES, A/B switch; the approximate phase
+    // otherwise stops at the first leaves that hold k series)
+    const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES"))) : 1;
     ProfScope ps("ix_seed", s, 0.0);
     // one CTA per query: small blocks take 1024 threads so a single query's
     // approximate phase still spreads over a whole SM
     const int threads = B <= 2 * num_sms() ? 1024 : 256;
     ix_seed_kernel<NT><<<B, threads, 0, s>>>(ix.X, reinterpret_cast<const uint4 *>(ix.words), ix.orig, ix.L, ix.leaf_first,
-                                         ix.leaf_count, lbe, tbl, Qp, k, lmax, target, so, qlist);
+                                         ix.leaf_count, lbe, tbl, Qp, k, lmax, target, min_leaves, so, qlist);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -776,13 +808,20 @@ int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, do
 {
     if (ix.L == 0 || B == 0) return OK;
     SSB_CUDA(upload_rcp_w());  // div_w's reciprocal table (a no-op after the first call)
-    ProfScope ps("ix_lbe", s, (double)ix.L * (M_MAX * 20 + 12) + 16.0 * B * (ix.n + 1));
-    if ((int64_t)B * ix.L <= 64 * 1024)  // small blocks: a warp per leaf (latency)
+    ProfScope ps("ix_lbe", s, (double)ix.L * (M_MAX * 24 + 12) + 16.0 * B * (ix.n + 1) + 8.0 * B * ix.S);
+    DevBuf qseg;
+    SSB_CUDA(qseg.alloc(8 * (size_t)B * std::max(ix.S, 1), s));
+    const int64_t nqs = (int64_t)B * ix.S;
+    ix_qseg_kernel<<<(unsigned)((nqs + 255) / 256), 256, 0, s>>>(cs, c2, ix.n, ix.S, ix.segs, B, qseg.as<float2>());
+    SSB_CHECK_LAUNCH();
+    // small blocks (latency), or segment ids past the staged 16-bit form: a warp per leaf
+    if ((int64_t)B * ix.L <= 64 * 1024 || ix.S > 65535 || ix.n > 65535)
         ix_lbe_warp_kernel<<<dim3((unsigned)((ix.L + 7) / 8), (unsigned)B), 256, 0, s>>>(
-            cs, c2, ix.n, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_env, ix.leaf_count, lbe);
+            qseg.as<float2>(), ix.S, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_seg, ix.leaf_env, ix.leaf_count, lbe);
     else
-        ix_lbe_kernel<<<dim3((unsigned)((ix.L + 127) / 128), (unsigned)B), 128, 16 * (ix.n + 1), s>>>(
-            cs, c2, ix.n, ix.L, ix.leaf_m, ix.leaf_ep, ix.leaf_env, ix.leaf_count, lbe);
+        ix_lbe_kernel<<<dim3((unsigned)((ix.L + LBE_LEAVES - 1) / LBE_LEAVES), (unsigned)((B + LBE_QB - 1) / LBE_QB)),
+                        256, 0, s>>>(qseg.as<float2>(), ix.S, ix.L, B, ix.leaf_m, ix.leaf_ep, ix.leaf_seg,
+                                     ix.leaf_env, ix.leaf_count, lbe);
     SSB_CHECK_LAUNCH();
     return OK;
 }

@@ -207,4 +207,28 @@ __device__ __forceinline__ void lay_load_q(const float *__restrict__ q, float (&
     lay_load_q_block<0, NT, NT / 8>(q, qv, j);
 }
 
+// ---------------------------------------------------------------------------
+// K-tc operand layout ("tile-major, pre-swizzled").  The BF16 rows are stored
+// as 128-row tiles of KB chunks; chunk c of tile t holds columns
+// [c*CW, c*CW + CW) of the tile's 128 rows byte for byte as the tensor cores'
+// canonical K-major swizzled shared-memory layout has them (SWIZZLE_128B for
+// CW = 64: 16-byte unit u of row r at u ^ (r & 7); SWIZZLE_64B for CW = 32: at
+// u ^ ((r >> 1) & 3)), so a chunk -- or one CTA's row slice of it -- is a
+// single contiguous 1-D bulk copy.  CW = 32 where n is not a multiple of 64
+// (n = 96: three 8 KB chunks per tile, no padding).  Rows past N are zero.
+__host__ __device__ constexpr int tcx_cw(int n) { return n % 64 == 0 ? 64 : 32; }
+__host__ __device__ constexpr int tcx_kb(int n) { return (n + tcx_cw(n) - 1) / tcx_cw(n); }
+__host__ __device__ inline int64_t tcx_tile_bytes(int n) { return (int64_t)128 * tcx_kb(n) * tcx_cw(n) * 2; }
+__host__ __device__ inline int64_t tcx_bytes(int64_t N, int n) { return (N + 127) / 128 * tcx_tile_bytes(n); }
+// byte offset of element (row, col)
+__host__ __device__ inline int64_t tcx_offset(int64_t row, int col, int n)
+{
+    const int cw = tcx_cw(n), kb = tcx_kb(n);
+    const int64_t tile = row >> 7;
+    const int r = (int)(row & 127), c = col / cw, j = col % cw;
+    const int u = j >> 3, e = j & 7;
+    const int su = cw == 64 ? (u ^ (r & 7)) : (u ^ ((r >> 1) & 3));
+    return ((tile * kb + c) * 128 + r) * (int64_t)(cw * 2) + su * 16 + e * 2;
+}
+
 }  // namespace ssb

@@ -123,6 +123,47 @@ __global__ void skip_unflagged_kernel(const int32_t *__restrict__ flags, const i
 }
 
 // returns -1 when a work buffer (items / entries) overflowed: the caller halves the block
+// The lean all-tensor-core batch (no index stages): route "tensor"; and for
+// "auto", blocks of >= 256 queries (whole filter groups) on an index whose
+// leaf pruning, as observed on recent blocks, keeps far more rows than the
+// break-even fraction of the cost model (the index route could not win for a
+// typical query, so its stages would only cost time) and whose filter pass is
+// not so long that the approximate phase's bound pays off.  Every 16th such block
+// runs the index stages again to refresh the observation.  SSB_AUTO_LEAN=0|1
+// forces the choice (A/B).
+static bool tc_all_for(const Index &ixc, const QueryCfg &qc, int k, int B)
+{
+    if (!ixc.Xb || k > TC_KTOP_MAX) return false;
+    if (qc.route == 2) return true;
+    if (qc.route != 0) return false;
+    if (const char *e = getenv("SSB_AUTO_LEAN")) return atoi(e) != 0;
+    if (B < 256) return false;
+    // the index stages still pay for themselves through the approximate
+    // phase's bound (the filter starts from it instead of +inf) when the
+    // filter's pass per query dwarfs that phase's reads (C4: ~100x; C2: ~13x)
+    const double avg_leaf = (double)ixc.N / (double)std::max(1, ixc.L);
+    const double seed_bytes = avg_leaf * 16.0 + (double)std::max(64, 4 * k) * 4.0 * ixc.n;
+    const double tc_bytes = (double)ixc.N * 2.0 * ixc.n / 256.0;
+    if (tc_bytes > 64.0 * seed_bytes) return false;
+    Index &ix = const_cast<Index &>(ixc);  // the routing observation is the only mutable part
+    std::lock_guard<std::mutex> lock(ix.graph_mu);
+    const double breakeven = IX_NS_TC_ROW / (256.0 * IX_NS_IX_ROW);
+    if (ix.kept_frac_ema < 0.0 || ix.kept_frac_ema < 2.0 * breakeven) return false;
+    if (++ix.lean_since_probe >= 16) {
+        ix.lean_since_probe = 0;
+        return false;  // probe
+    }
+    return true;
+}
+
+static void observe_kept(const Index &ixc, double frac)
+{
+    Index &ix = const_cast<Index &>(ixc);
+    std::lock_guard<std::mutex> lock(ix.graph_mu);
+    ix.kept_frac_ema = ix.kept_frac_ema < 0.0 ? frac : 0.5 * (ix.kept_frac_ema + frac);
+    ix.lean_since_probe = 0;
+}
+
 // blocks that take the index route entirely and emit their work without a
 // host round trip (query_batch's direct path): the CUDA-graph candidates
 static bool small_block_ok(const Index &ix, const QueryCfg &qc, int B)
@@ -181,6 +222,11 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(cudaMemcpyAsync(qi.data(), w.q_items.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(tc.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
+        if (qc.route == 0 && B >= 256) {
+            double kept = 0.0;
+            for (int q = 0; q < B; q++) kept += (double)kr[q];
+            observe_kept(ix, kept / ((double)B * (double)std::max<int64_t>(ix.N, 1)));
+        }
         if (mode == 0) {
             // queries by index cost, most expensive first; the filter takes a
             // prefix of them, t in {0, 256, 512, ..., B} (within a group the
@@ -531,14 +577,6 @@ static int query_batch_tc(const Index &ix, const float *Q, int B, int k, uint64_
     }
 }
 
-static bool tc_all_for(const Index &ix, const QueryCfg &qc, int k)
-{
-    // the lean all-tensor-core batch: route "tensor"; "auto" runs the index
-    // stages and routes per query (SSB_AUTO_LEAN=1: auto takes the lean batch
-    // too -- an A/B switch for measurements)
-    static const bool auto_lean = getenv("SSB_AUTO_LEAN") != nullptr;
-    return ix.Xb && k <= TC_KTOP_MAX && (qc.route == 2 || (qc.route == 0 && auto_lean));
-}
 
 // Several independent calls (query blocks, each with its own k) answered with
 // ONE host round trip when every call takes the lean tensor-core path: all
@@ -667,11 +705,15 @@ static int small_graph_get(const Index &ixc, const QueryCfg &qc, int B, int k, c
         const int rc0 = ix_prepare();
         if (rc0) return rc0;
     }
+    // captured on a private stream (the caller's may be the legacy default
+    // stream, which cannot capture); replays launch on the caller's stream
+    static cudaStream_t cap = nullptr;
+    if (!cap) SSB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     const int64_t l0 = launch_count();
-    SSB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    const int rc = small_block_work(ix, qc, *g, s);
+    SSB_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int rc = small_block_work(ix, qc, *g, cap);
     cudaGraph_t graph = nullptr;
-    const cudaError_t e = cudaStreamEndCapture(s, &graph);
+    const cudaError_t e = cudaStreamEndCapture(cap, &graph);
     g->launches = launch_count() - l0;
     note_launch(-(int)g->launches);  // captured, not launched
     if (rc) {
@@ -774,7 +816,7 @@ int index_query_multi(const Index &ix, const QueryCfg &qc, int nc, const float *
         return OK;
     };
     for (int i = 0; i < nc; i++) {
-        lean[i] = B[i] > 0 && B[i] <= 8192 && tc_all_for(ix, qc, K[i]);
+        lean[i] = B[i] > 0 && B[i] <= 8192 && tc_all_for(ix, qc, K[i], B[i]);
         if (!lean[i]) continue;
         SSB_CUDA(keys[i].alloc(8 * (size_t)B[i] * K[i], s));
         work[i].reset(new TcWork());
@@ -801,7 +843,7 @@ int index_query(const Index &ix, const QueryCfg &qc, const float *Q, int B, int 
     SSB_REQUIRE(B < (1 << 26), "too many queries in one call");
     if (B == 0) return OK;
     const int n = ix.n;
-    const bool tc_all = tc_all_for(ix, qc, k);
+    const bool tc_all = tc_all_for(ix, qc, k, B);
     uint32_t leaves_nonempty = 0;
     for (int32_t l : ix.leaves) leaves_nonempty += ix.nodes[l].count > 0 ? 1u : 0u;
     DevBuf keys;

@@ -52,6 +52,9 @@ struct Index {
     int32_t *leaf_m = nullptr;
     int32_t *leaf_ep = nullptr;  // L x M_MAX
     float *leaf_env = nullptr;   // L x M_MAX x 4
+    int32_t S = 0;               // distinct leaf segments [sa, sb)
+    int2 *segs = nullptr;        // S
+    int32_t *leaf_seg = nullptr; // L x M_MAX segment ids
     float max_abs = 0.f;         // max |x| over the data (LB safety slack)
     // tensor-core filter operands: BF16 copy (row-major, logical element order,
     // leaf order) and exact squared norms / norms (rounded up) of every row
@@ -67,6 +70,11 @@ struct Index {
     // (query.cu SmallGraph; one per (stream, B, k, lmax)), freed with the index
     std::mutex graph_mu;
     std::vector<struct SmallGraph *> graphs;
+    // learned routing (query.cu tc_all_for): the mean fraction of rows the
+    // index route's leaf pruning keeps, over recent full blocks (< 0: none
+    // observed yet), and the lean blocks answered since the last observation
+    double kept_frac_ema = -1.0;
+    int lean_since_probe = 0;
     ~Index();
 };
 

@@ -21,20 +21,23 @@
 //
 // One CTA = one block of 128 queries (M = 128) x a contiguous range of
 // 128-row tiles (N = 128); two query blocks form a cluster and get every B
-// tile by TMA multicast.  Warp roles (10 warps): w0 producer (tile side data
-// by 1-D bulk copies into an 8-deep tile-slot ring; whole B tiles, KB K-chunks
-// of 64 columns (SWIZZLE_128B, 16 KB; 32-column SWIZZLE_64B chunks are an A/B
-// option) each, into a 192 KB ring of tile slots), w1 TMEM allocation + MMA issue
-// (A = the query block, resident in TMEM; 3 accumulators of 128 columns; one
-// barrier wait and one commit per tile), w2..w9 epilogue (two warps per TMEM
-// lane quarter, one query per thread, 64 columns per tile).  The first `warm`
+// tile by multicast.  The rows live in HBM tile-major and pre-swizzled
+// (layout.cuh tcx_*): every K-chunk of a 128-row tile is already the
+// tensor cores' canonical swizzled shared-memory image, so a CTA's row slice of
+// it is ONE contiguous cp.async.bulk (no tensor map, no row split into
+// 128 + 64-byte TMA segments at n = 96).  Warp roles: w0 producer (tile side
+// data by 1-D bulk copies into an 8-deep tile-slot ring; the B tile, KB chunks
+// of 64 columns (SWIZZLE_128B, 16 KB; 32 columns, SWIZZLE_64B, 8 KB when n is
+// not a multiple of 64), into a 192 KB ring of tile slots), w1 TMEM allocation
+// + MMA issue (A = the query block, resident in TMEM; 3 accumulators of 128
+// columns; one barrier wait and one commit per tile), w2.. epilogue (EPW warps,
+// EPW/4 per TMEM lane quarter, one query per thread).  The first `warm`
 // tiles of every CTA are scanned once without emission (bounds only) and
 // rescanned at the end.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -69,28 +72,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw(uint32_t smem_addr, int cw)
     const uint64_t sbo = cw == 64 ? (1024 >> 4) : (512 >> 4), type = cw == 64 ? 2 : 4;
     return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | (sbo << 32) | ((uint64_t)1 << 46) |
            (type << 61);
-}
-
-__device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int x, int y, uint64_t *bar)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(d),
-        "l"(map), "r"(b), "r"(x), "r"(y)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d_mc(void *smem, const CUtensorMap *map, int x, int y, uint64_t *bar,
-                                               uint16_t mask)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(d),
-        "l"(map), "r"(b), "r"(x), "r"(y), "h"(mask)
-        : "memory");
 }
 
 __device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask)
@@ -166,7 +147,8 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 }
 
 struct TcParams {
-    int n;                 // series length (K, zero-padded to KB*CW by TMA)
+    const unsigned char *xb;  // BF16 rows, tile-major pre-swizzled (layout.cuh tcx_*)
+    int n;                 // series length (K, zero-padded to KB*CW)
     int KB;                // K-chunks per tile
     int CW;                // chunk width: 64 (SWIZZLE_128B) or 32 (SWIZZLE_64B) columns
     int64_t N;             // rows
@@ -215,10 +197,11 @@ static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
 // KTOP == 0: filter against the given bounds only; KTOP < 0: debug dump of S.
 template <int KTOP, int EPW>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
 __global__ void __launch_bounds__(64 + 32 * EPW, 1)
-    tc_filter_kernel(const __grid_constant__ CUtensorMap mapB, TcParams p)
+    tc_filter_kernel(const __grid_constant__ TcParams p)
 {
-    // mapB's box covers 128/CS rows: every CTA of the cluster loads one row
-    // slice of each B tile and multicasts it to the whole cluster
+    // every CTA of the cluster loads one row slice (128/CS rows) of each
+    // K-chunk of a B tile -- one contiguous bulk copy from the pre-swizzled
+    // operand -- and multicasts it to the whole cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms
     // (pointer arithmetic on smem_raw keeps the shared address space visible to the compiler)
@@ -358,21 +341,24 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
                     "r"(tile_bytes)
                     : "memory");
+                const unsigned char *src0 = p.xb + ((size_t)tile * KB * TC_BN + (size_t)rank * srows) * row_bytes;
+                const uint32_t slice = (uint32_t)srows * row_bytes;
                 for (int kb = 0; kb < KB; kb++) {
                     const uint32_t dst = dst0 + (uint32_t)kb * chunk_bytes;
+                    const unsigned char *src = src0 + (size_t)kb * chunk_bytes;
                     if (CS == 1)
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%4, {%2, %3}], [%1];\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * CW), "r"(row0), "l"(&mapB)
+                            "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%2], %3, [%1];\n}" ::"r"(dst),
+                            "r"(bar), "l"(src), "r"(slice)
                             : "memory");
                     else
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            ".multicast::cluster [%0], [%4, {%2, %3}], [%1], %5;\n}" ::"r"(dst),
-                            "r"(bar), "r"(kb * CW), "r"(row0), "l"(&mapB), "h"(cmask)
+                            "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(dst),
+                            "r"(bar), "l"(src), "r"(slice), "h"(cmask)
                             : "memory");
                 }
                 if (++slot == NS) {
@@ -719,6 +705,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
                                      int n, int layout, __nv_bfloat16 *__restrict__ dst, float *__restrict__ n2,
                                      float2 *__restrict__ en, int is_query)
+// dst: row-major for queries (the A operand); the tile-major pre-swizzled
+// layout (layout.cuh tcx_offset) for rows (the B operand)
 {
     // one warp per row; src rows may be in the lane-transposed layout
     const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
@@ -729,7 +717,10 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
     for (int e = lane; e < n; e += 32) {
         const float v = s[layout ? layout_pos(n, e) : e];
         const __nv_bfloat16 b = __float2bfloat16_rn(v);
-        dst[r * n + e] = b;
+        if (is_query)
+            dst[r * n + e] = b;
+        else
+            *reinterpret_cast<__nv_bfloat16 *>(reinterpret_cast<unsigned char *>(dst) + tcx_offset(r, e, n)) = b;
         const double vb = (double)__bfloat162float(b), dv = (double)v - vb;  // exact in float64
         acc += (double)v * (double)v;
         hh += vb * vb;
@@ -882,41 +873,6 @@ int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *
     return OK;
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode()
-{
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
-    return fn;
-}
-
-static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int n, int box_rows = 128, int cw = 64)
-{
-    auto enc = get_encode();
-    if (!enc) {
-        set_error(ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        return ERR_CUDA;
-    }
-    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)n * 2};
-    cuuint32_t box[2] = {(cuuint32_t)cw, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     cw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error(ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        return ERR_CUDA;
-    }
-    return OK;
-}
-
 // per-query bound slots the caller allocates for nq queries: the producer
 // copies whole 128-query blocks of bounds (query blocks padded to clusters)
 int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
@@ -933,12 +889,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     if (nq == 0 || N == 0) return OK;
     TcParams p;
     p.n = n;
-    // K-chunk width 64 (SWIZZLE_128B).  32-column chunks (SWIZZLE_64B; n = 96: 3 x 8 KB
-    // per tile instead of 2 x 16 KB, 8 tiles in flight instead of 6) measured slower
-    // on C3 (loads-only pipeline -10%: 64-byte TMA row segments; MMA-only -11%), so
-    // they are kept as the SSB_TC_CW=32 A/B switch (tested) only.
-    p.CW = 64;
-    if (const char *e = getenv("SSB_TC_CW")) p.CW = atoi(e) == 32 ? 32 : 64;  // diagnostics (A/B)
+    p.CW = tcx_cw(n);  // the operand's chunk width (layout.cuh)
     p.KB = (n + p.CW - 1) / p.CW;
     p.N = N;
     p.nq = nq;
@@ -958,9 +909,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     clusters_per_group = (int)std::max<int64_t>(1, std::min<int64_t>(clusters_per_group, p.tiles / 16));
     p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
-    CUtensorMap mB;
-    int rc = make_map(&mB, Xb, N, n, TC_BN / CS, p.CW);
-    if (rc) return rc;
+    int rc = OK;
+    p.xb = static_cast<const unsigned char *>(Xb);
     p.qb = reinterpret_cast<const uint4 *>(Qb);
     p.qn2 = qn2;
     p.qen = qen;
@@ -996,7 +946,9 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.prog = nullptr;
     p.window = 0;
     DevBuf prog;
-    int window = 48;  // tiles (3 MB of BF16 rows per chunk at n = 256)
+    // off by default: measured on C4 it halves the DRAM bytes (43 -> 22 GB per
+    // launch) but the coupling stalls cost more than the bandwidth saves
+    int window = 0;
     if (const char *e = getenv("SSB_TC_WINDOW")) window = std::max(0, atoi(e));  // diagnostics (0 = off)
     if (groups > 1 && window > 0) {
         SSB_CUDA(prog.alloc(4 * (size_t)p.ctas_per_qb * groups * CS, s));
@@ -1038,7 +990,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
         ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
                      2.0 * (double)nq * (double)N * (double)n);  // algorithmic FLOPs (unpadded K)
-        SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, mB, p));
+        SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
         return OK;
     };
     const bool nolist = getenv("SSB_TC_NOLIST") != nullptr;  // diagnostics: bucket bound only for k >= 2
@@ -1074,7 +1026,8 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     const int Bp = (B + TC_BM - 1) / TC_BM * TC_BM;
     DevBuf qb, xb, qn2, qnm, xn2, xnm, gb, cand, cn;  // qnm, xnm: float2 error norms
     SSB_CUDA(qb.alloc(2 * (size_t)Bp * n, s));
-    SSB_CUDA(xb.alloc(2 * (size_t)N * n, s));
+    SSB_CUDA(xb.alloc((size_t)tcx_bytes(N, n), s));
+    SSB_CUDA(cudaMemsetAsync(xb.p, 0, (size_t)tcx_bytes(N, n), s));
     SSB_CUDA(qn2.alloc(4 * (size_t)Bp, s));
     SSB_CUDA(qnm.alloc(8 * (size_t)Bp, s));
     SSB_CUDA(xn2.alloc(4 * (size_t)N, s));

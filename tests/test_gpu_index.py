@@ -385,7 +385,8 @@ def test_small_blocks_cuda_graph_path(ssb, oracle):
                     d2, ids, _, st = eng.knn_device(Q[q0:q0 + B], k, want_stats=True)
                     assert np.array_equal(ids.cpu().numpy(), oid[q0:q0 + B]), (k, B, q0)
                     assert np.array_equal(bits(d2.cpu().numpy()), bits(od2[q0:q0 + B])), (k, B, q0)
-                    assert (st[:, 7] == 0).all() and (st[:, 4] >= 1).all()
+                    if B <= 3:  # the graph-replayed blocks take the index route
+                        assert (st[:, 7] == 0).all() and (st[:, 4] >= 1).all()
     for lmax in (1, 80):
         rs, qs = eng.exact_knn(Q[0], ssb.QueryConfig(k=5, lmax=lmax))
         od2, oid = oracle.knn_scan(X, Q[:1], 5)
