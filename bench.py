@@ -446,7 +446,8 @@ def run_reference(args, rank, world):
     cellq = [fn() for _, fn, _ in wl.cells]
     threads = os.cpu_count() or 1
     per_step = args.cpu_sample or 0
-    secs = args.cpu_seconds / 2 if not per_step else 0
+    # each step: about 2 s of CPU work (so --steps K stays within minutes)
+    secs = min(2.0, args.cpu_seconds / 2) if not per_step else 0
     for _ in range(args.warmup):
         oracle_sample(wl, X, cellq, 1, 0, threads)
     nq, tot = 0, 0.0

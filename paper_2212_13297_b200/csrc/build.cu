@@ -51,7 +51,7 @@ namespace ssb {
 Index::~Index()
 {
     free_small_graphs(*this);
-    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, rowc, tilec,
+    void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, tcside,
                     tcperm, segs, leaf_seg};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -860,6 +860,7 @@ struct FinalizeArgs {
     const double *bp;       // 255 breakpoints
     uint32_t *inv;          // source row -> position (null: skip)
     __nv_bfloat16 *Xb;      // K-tc operand (null: skip)
+    int cw;                 // its K-chunk width (layout.cuh tcx_*)
     float *xn2;
     float2 *xen;
     const uint32_t *tcinv;  // position -> K-tc slot (null: identity)
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
                 uint2 pk;
                 pk.x = (uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16);
                 pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
-                *reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(a.Xb) + tcx_offset(h, 4 * c, n)) = pk;
+                *reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(a.Xb) + tcx_offset(h, 4 * c, n, a.cw)) = pk;
             }
         };
         if constexpr (W > 0) {
@@ -1165,15 +1166,18 @@ static int alloc_tc_operands(Index &ix, DevBuf &tcinv, cudaStream_t s)
     // tile-major pre-swizzled BF16 operand (layout.cuh tcx_*): the padding rows
     // of the last tile (and padding columns, if n is not a multiple of the chunk
     // width) are zero
-    SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)tcx_bytes(ix.N, ix.n)));
-    if (ix.n % tcx_cw(ix.n) == 0)
-        SSB_CUDA(cudaMemsetAsync(static_cast<char *>(ix.Xb) + tcx_bytes(ix.N, ix.n) - tcx_tile_bytes(ix.n), 0,
-                                 (size_t)tcx_tile_bytes(ix.n), s));
+    ix.tc_cw = tcx_default_cw(ix.n);
+    if (const char *e = getenv("SSB_TC_CW")) ix.tc_cw = atoi(e) == 64 ? 64 : 32;  // A/B of the chunk width
+    const int cw = ix.tc_cw;
+    SSB_CUDA(cudaMalloc(&ix.Xb, (size_t)tcx_bytes(ix.N, ix.n, cw)));
+    if (ix.n % cw == 0)
+        SSB_CUDA(cudaMemsetAsync(static_cast<char *>(ix.Xb) + tcx_bytes(ix.N, ix.n, cw) - tcx_tile_bytes(ix.n, cw), 0,
+                                 (size_t)tcx_tile_bytes(ix.n, cw), s));
     else
-        SSB_CUDA(cudaMemsetAsync(ix.Xb, 0, (size_t)tcx_bytes(ix.N, ix.n), s));
+        SSB_CUDA(cudaMemsetAsync(ix.Xb, 0, (size_t)tcx_bytes(ix.N, ix.n, cw), s));
     SSB_CUDA(cudaMalloc(&ix.xn2, (size_t)ix.N * 4));
     SSB_CUDA(cudaMalloc(&ix.xen, (size_t)ix.N * 8));
-    SSB_CUDA(cudaMalloc(&ix.rowc, (size_t)((ix.N + 127) / 128 * 128) * 16));  // padded to whole tiles
+    SSB_CUDA(cudaMalloc(&ix.tcside, (size_t)tc_side_bytes(ix.N)));  // one record per 128-row tile
     // K-tc row order: a hashed permutation of the leaf order.  Leaf order puts a
     // query's near neighbours next to each other, so its hits come in bursts in
     // a few tiles, and a tile's epilogue (and with it the whole CTA) waits for the
@@ -1204,10 +1208,7 @@ static int alloc_tc_operands(Index &ix, DevBuf &tcinv, cudaStream_t s)
 static int finish_tc_operands(Index &ix, cudaStream_t s)
 {
     if (!ix.Xb) return OK;
-    int rc = launch_tc_row_consts(ix.xn2, ix.xen, ix.N, ix.rowc, s);
-    if (rc) return rc;
-    SSB_CUDA(cudaMalloc(&ix.tilec, (size_t)((ix.N + 127) / 128 * 4) * 16));
-    return launch_tc_tile_consts(ix.rowc, ix.N, ix.tilec, s);
+    return launch_tc_side(ix.xn2, ix.xen, ix.N, ix.tcside, s);
 }
 
 // the fused row pass (+ K-tc operands) of a built or loaded index
@@ -1226,6 +1227,7 @@ static int finalize_rows(Index &ix, const float *src, const uint32_t *perm, bool
     fa.bp = ix.bp;
     fa.inv = perm ? ix.inv : nullptr;
     fa.Xb = reinterpret_cast<__nv_bfloat16 *>(ix.Xb);
+    fa.cw = ix.tc_cw;
     fa.xn2 = ix.xn2;
     fa.xen = ix.xen;
     fa.tcinv = ix.tcperm ? tcinv.as<uint32_t>() : nullptr;

@@ -215,15 +215,16 @@ __device__ __forceinline__ void lay_load_q(const float *__restrict__ q, float (&
 // CW = 64: 16-byte unit u of row r at u ^ (r & 7); SWIZZLE_64B for CW = 32: at
 // u ^ ((r >> 1) & 3)), so a chunk -- or one CTA's row slice of it -- is a
 // single contiguous 1-D bulk copy.  CW = 32 where n is not a multiple of 64
-// (n = 96: three 8 KB chunks per tile, no padding).  Rows past N are zero.
-__host__ __device__ constexpr int tcx_cw(int n) { return n % 64 == 0 ? 64 : 32; }
-__host__ __device__ constexpr int tcx_kb(int n) { return (n + tcx_cw(n) - 1) / tcx_cw(n); }
-__host__ __device__ inline int64_t tcx_tile_bytes(int n) { return (int64_t)128 * tcx_kb(n) * tcx_cw(n) * 2; }
-__host__ __device__ inline int64_t tcx_bytes(int64_t N, int n) { return (N + 127) / 128 * tcx_tile_bytes(n); }
+// (n = 96: three 8 KB chunks per tile, no padding; SSB_TC_CW=64 at build time
+// stores it as two zero-padded 16 KB chunks instead).  Rows past N are zero.
+__host__ __device__ constexpr int tcx_default_cw(int n) { return n % 64 == 0 ? 64 : 32; }
+__host__ __device__ constexpr int tcx_kb(int n, int cw) { return (n + cw - 1) / cw; }
+__host__ __device__ inline int64_t tcx_tile_bytes(int n, int cw) { return (int64_t)128 * tcx_kb(n, cw) * cw * 2; }
+__host__ __device__ inline int64_t tcx_bytes(int64_t N, int n, int cw) { return (N + 127) / 128 * tcx_tile_bytes(n, cw); }
 // byte offset of element (row, col)
-__host__ __device__ inline int64_t tcx_offset(int64_t row, int col, int n)
+__host__ __device__ inline int64_t tcx_offset(int64_t row, int col, int n, int cw)
 {
-    const int cw = tcx_cw(n), kb = tcx_kb(n);
+    const int kb = tcx_kb(n, cw);
     const int64_t tile = row >> 7;
     const int r = (int)(row & 127), c = col / cw, j = col % cw;
     const int u = j >> 3, e = j & 7;

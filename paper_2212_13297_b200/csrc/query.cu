@@ -295,7 +295,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         uint64_t hn = 0;
         for (int attempt = 0; attempt < 3; attempt++) {  // a retry keeps the bounds the filter ended with
             SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 8, s));
-            rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+            rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.tc_cw, ix.tcside, ix.N, n, k,
                                   gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
                                   tc_n.as<unsigned long long>(), tc_cap, nullptr, s);
             if (rc) return rc;
@@ -504,7 +504,7 @@ static int tc_submit(const Index &ix, const float *Q, int B, int k, uint64_t *ou
     }
     // a retry (candidate-buffer overflow) keeps the bounds the filter ended with
     SSB_CUDA(cudaMemsetAsync(w.cn.p, 0, 8, s));
-    rc = launch_tc_filter(w.qb.p, w.qn2.as<float>(), w.qnrm.as<float2>(), B, ix.Xb, ix.rowc, ix.tilec, ix.N, n, k,
+    rc = launch_tc_filter(w.qb.p, w.qn2.as<float>(), w.qnrm.as<float2>(), B, ix.Xb, ix.tc_cw, ix.tcside, ix.N, n, k,
                           w.gb.as<unsigned int>(), w.cand.as<uint2>(), w.clb.as<float>(), w.cn.as<unsigned long long>(),
                           w.tc_cap, nullptr, s);
     if (rc) return rc;

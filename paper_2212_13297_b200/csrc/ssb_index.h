@@ -59,11 +59,11 @@ struct Index {
     // tensor-core filter operands: BF16 copy (row-major, logical element order,
     // leaf order) and exact squared norms / norms (rounded up) of every row
     void *Xb = nullptr;
+    int32_t tc_cw = 64;          // K-chunk width of Xb's tile-major layout (layout.cuh tcx_*)
     float *xn2 = nullptr;    // ||x||^2 per row
     float2 *xen = nullptr;   // per row (U, V): BF16 rounding-error norms (to_bf16_norms_kernel)
     uint32_t *tcperm = nullptr;  // K-tc row order -> leaf-order position (null: identity)
-    float4 *rowc = nullptr;   // per-row constants of the K-tc bounds
-    float4 *tilec = nullptr;  // per 64-row half tile: two float4 of extremes of rowc
+    float4 *tcside = nullptr; // per 128-row tile: the K-tc bound constants of its rows + half-tile extremes
     double build_ms = 0.0;
     int32_t levels = 0;
     // small query blocks on the index route replay a captured CUDA graph
@@ -112,13 +112,13 @@ int ix_back(const Index &ix, IxWork &w, int B, const int32_t *qskip, ScanOut so,
 int ix_prepare();
 int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, double *lbe, cudaStream_t s);
 
-int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
-                     const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
+int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb, int xb_cw,
+                     const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s);
 int64_t tc_bound_slots(int nq);
-int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *out, cudaStream_t s);
-int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s);
+int64_t tc_side_bytes(int64_t N);
+int launch_tc_side(const float *xn2, const float2 *en, int64_t N, float4 *side, cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
 int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,

@@ -161,8 +161,7 @@ struct TcParams {
     int CS;                // cluster size: CTAs (query blocks) sharing each B tile by multicast
     const float *qn2;          // per query (launch-local index): ||q||^2
     const float2 *qen;         // per query: (||qh||, ||ql||) rounded up
-    const float4 *rowc;        // per row bound constants (tc_row_consts_kernel)
-    const float4 *tilec;       // per 64-row half tile: two float4 of extremes (tc_tile_consts_kernel)
+    const float4 *side;        // per tile: TC_SIDE float4 (row bound constants, half-tile extremes)
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
     unsigned int *gbucket;     // per query x k (k >= 2): min upper bound of the rows r with r % k == b
     int k;
@@ -186,10 +185,12 @@ struct TcParams {
 
 // per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
 constexpr int TC_RS = 8;  // tile-slot ring depth (>= the B ring in tiles for KB >= 2: side data never throttles the loads)
+// In HBM the side data of a tile is one contiguous record (TC_SIDE float4:
+// the 128 row constants, then the half-tile extremes), so it is one copy.
+constexpr int TC_SIDE = TC_BN + 4;
 struct TileSlot {
     float4 rowc[TC_BN];  // row bound constants of the tile's 128 rows
     float4 tilec[4];     // per 64-row half: (min a_l, max u, max v, -), (min a_u, min u, min v, -)
-    float gb[TC_BM];     // snapshot of the shared per-query bounds (float bits)
 };
 static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
 
@@ -285,7 +286,6 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(b_full);
             const uint32_t rfull0 = (uint32_t)__cvta_generic_to_shared(r_full);
             const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(slots);
-            const int srows = TC_BN / CS;
             int slot = 0;
             uint32_t phase = 0;
             volatile unsigned int *prog_chunk =
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     }
                     __syncwarp();
                 }
-                // side data of this tile: row constants, half-tile extremes, bounds snapshot
+                // side data of this tile (row constants + half-tile extremes): one copy
                 const int rs = t % TC_RS;
                 if (t >= TC_RS) mbar_wait(&r_empty[rs], (unsigned)(((t / TC_RS) - 1) & 1));
                 {
@@ -312,16 +312,12 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     const uint32_t bar = rfull0 + (uint32_t)rs * 8;
                     asm volatile(
                         "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                        "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %8;\n"
-                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %5, [%1];\n"
-                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2048], [%3], %6, [%1];\n"
-                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0+2112], [%4], %7, [%1];\n"
+                        "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n"
                         "}" ::"r"(dst),
-                        "r"(bar), "l"(p.rowc + tile * TC_BN), "l"(p.tilec + tile * 4), "l"(p.gbound + qb * TC_BM),
-                        "n"(TC_BN * 16), "n"(64), "n"(TC_BM * 4), "n"((int)sizeof(TileSlot))
+                        "r"(bar), "l"(p.side + tile * TC_SIDE), "n"((int)sizeof(TileSlot))
                         : "memory");
                 }
-                const int row0 = (int)(tile * TC_BN) + rank * srows;
                 if (t >= NS) mbar_wait(&b_empty[slot], phase ^ 1u);
                 const uint32_t bar = full0 + (uint32_t)slot * 8;
                 if (p.skip_epi == 4 && t >= NS) {  // diagnostics: MMA-only pipeline (stale B tiles)
@@ -334,31 +330,31 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     }
                     continue;
                 }
-                const uint32_t dst0 = ring + (uint32_t)slot * tile_bytes + (uint32_t)rank * srows * row_bytes;
-                // the whole tile (every CTA's row slice of every K-chunk) lands in this CTA's slot
+                // the whole tile (every K-chunk, from every CTA of the cluster) lands in this CTA's slot
                 asm volatile(
                     "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
                     "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
                     "r"(tile_bytes)
                     : "memory");
-                const unsigned char *src0 = p.xb + ((size_t)tile * KB * TC_BN + (size_t)rank * srows) * row_bytes;
-                const uint32_t slice = (uint32_t)srows * row_bytes;
-                for (int kb = 0; kb < KB; kb++) {
-                    const uint32_t dst = dst0 + (uint32_t)kb * chunk_bytes;
-                    const unsigned char *src = src0 + (size_t)kb * chunk_bytes;
-                    if (CS == 1)
+                // whole K-chunks (contiguous in the pre-swizzled operand): CTA `rank`
+                // loads the chunks c with c % CS == rank and multicasts them; alone
+                // (CS = 1) it loads the whole tile in one copy
+                const unsigned char *tsrc = p.xb + (size_t)tile * tile_bytes;
+                const uint32_t tdst = ring + (uint32_t)slot * tile_bytes;
+                if (CS == 1) {
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%2], %3, [%1];\n}" ::"r"(tdst),
+                        "r"(bar), "l"(tsrc), "r"(tile_bytes)
+                        : "memory");
+                } else {
+                    for (int kb = rank; kb < KB; kb += CS)
                         asm volatile(
                             "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
                             "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%2], %3, [%1];\n}" ::"r"(dst),
-                            "r"(bar), "l"(src), "r"(slice)
-                            : "memory");
-                    else
-                        asm volatile(
-                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(dst),
-                            "r"(bar), "l"(src), "r"(slice), "h"(cmask)
+                            ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(tdst + (uint32_t)kb * chunk_bytes),
+                            "r"(bar), "l"(tsrc + (size_t)kb * chunk_bytes), "r"(chunk_bytes), "h"(cmask)
                             : "memory");
                 }
                 if (++slot == NS) {
@@ -476,6 +472,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             top[i] = i < KT - p.k ? __int_as_float(0xff800000) : __int_as_float(0x7f800000);
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
+        float gnext = qvalid ? __uint_as_float(*(volatile const unsigned int *)gb) : -1.f;
         // bucket bound (k >= 2): rows are split into k classes by r % k; the
         // largest per-class minimum of the upper bounds bounds the k-th
         // smallest distance (k distinct rows lie below it), and it pools the
@@ -515,7 +512,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const bool revisit = t >= nwarm && t < 2 * nwarm;
             const TileSlot &ts = slots[rs];
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
-            const float gcur = qvalid ? ts.gb[m] : -1.f;
+            // the shared bound of this query (other CTAs tighten it): read one
+            // tile ahead so the load's latency hides behind this tile's work
+            const float gcur = gnext;
+            if (qvalid) gnext = __uint_as_float(*(volatile const unsigned int *)gb);
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
             const float4 tcl = ts.tilec[2 * hh], tcu = ts.tilec[2 * hh + 1];
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 // a relative margin, then float32 RU).
 __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
                                      int n, int layout, __nv_bfloat16 *__restrict__ dst, float *__restrict__ n2,
-                                     float2 *__restrict__ en, int is_query)
+                                     float2 *__restrict__ en, int is_query, int cw)
 // dst: row-major for queries (the A operand); the tile-major pre-swizzled
 // layout (layout.cuh tcx_offset) for rows (the B operand)
 {
@@ -720,7 +720,7 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
         if (is_query)
             dst[r * n + e] = b;
         else
-            *reinterpret_cast<__nv_bfloat16 *>(reinterpret_cast<unsigned char *>(dst) + tcx_offset(r, e, n)) = b;
+            *reinterpret_cast<__nv_bfloat16 *>(reinterpret_cast<unsigned char *>(dst) + tcx_offset(r, e, n, cw)) = b;
         const double vb = (double)__bfloat162float(b), dv = (double)v - vb;  // exact in float64
         acc += (double)v * (double)v;
         hh += vb * vb;
@@ -799,46 +799,47 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
 {
     if (R == 0) return OK;
     to_bf16_norms_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(src, rows, R, n, layout ? 1 : 0,
-                                                                  (__nv_bfloat16 *)dst_bf16, n2, en, is_query ? 1 : 0);
+                                                                  (__nv_bfloat16 *)dst_bf16, n2, en, is_query ? 1 : 0,
+                                                                  tcx_default_cw(n));
     SSB_CHECK_LAUNCH();
     return OK;
 }
 
-// per-row constants of the bound formulas (see the epilogue):
-// (a_l, a_u, u, v) = (f(1-e) xn2, g(1+e) xn2, 2g U, 2g V) with (U, V) = en
-__global__ void tc_row_consts_kernel(const float *__restrict__ xn2, const float2 *__restrict__ en, int64_t N,
-                                     float4 *__restrict__ out)
-{
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= (N + 127) / 128 * 128) return;
-    if (r >= N) {  // padding rows of the last tile: lb = ub = +inf
-        out[r] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000), 0.f, 0.f);
-        return;
-    }
-    const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
-    const float2 uv = en[r];
-    out[r] = make_float4(f * (1.f - e) * xn2[r], g * (1.f + e) * xn2[r], 2.f * g * uv.x, 2.f * g * uv.y);
-}
+// Side data of the filter, one TC_SIDE-float4 record per 128-row tile
+// (tc_side_bytes): the per-row constants of the bound formulas (see the
+// epilogue) (a_l, a_u, u, v) = (f(1-e) xn2, g(1+e) xn2, 2g U, 2g V) with
+// (U, V) = en, then per 64-row half tile two float4 of extremes
+// (min a_l, max u, max v, -), (min a_u, min u, min v, -).
+int64_t tc_side_bytes(int64_t N) { return (N + TC_BN - 1) / TC_BN * TC_SIDE * 16; }
 
-// per 64-row half tile, two float4: (min a_l, max u, max v, -), (min a_u, min u, min v, -)
-__global__ void tc_tile_consts_kernel(const float4 *__restrict__ rowc, int64_t N, int64_t halves, float4 *__restrict__ out)
+__global__ void tc_side_kernel(const float *__restrict__ xn2, const float2 *__restrict__ en, int64_t N,
+                               float4 *__restrict__ side)
 {
+    // one warp per 64-row half tile
     const int64_t hidx = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    const int64_t halves = (N + TC_BN - 1) / TC_BN * 2;
     if (hidx >= halves) return;
     const int lane = threadIdx.x & 31;
     const float inf = __int_as_float(0x7f800000);
+    const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
+    float4 *rec = side + (hidx >> 1) * TC_SIDE;
     float mal = inf, mxu = 0.f, mxv = 0.f, mau = inf, mnu = inf, mnv = inf;
     for (int i = lane; i < 64; i += 32) {
         const int64_t r = hidx * 64 + i;
+        float4 c;
         if (r < N) {
-            const float4 c = rowc[r];
+            const float2 uv = en[r];
+            c = make_float4(f * (1.f - e) * xn2[r], g * (1.f + e) * xn2[r], 2.f * g * uv.x, 2.f * g * uv.y);
             mal = fminf(mal, c.x);
             mau = fminf(mau, c.y);
             mxu = fmaxf(mxu, c.z);
             mnu = fminf(mnu, c.z);
             mxv = fmaxf(mxv, c.w);
             mnv = fminf(mnv, c.w);
+        } else {  // padding rows of the last tile: lb = ub = +inf
+            c = make_float4(inf, inf, 0.f, 0.f);
         }
+        rec[(hidx & 1) * 64 + i] = c;
     }
     for (int off = 16; off; off >>= 1) {
         mal = fminf(mal, __shfl_xor_sync(0xffffffffu, mal, off));
@@ -849,26 +850,16 @@ __global__ void tc_tile_consts_kernel(const float4 *__restrict__ rowc, int64_t N
         mnv = fminf(mnv, __shfl_xor_sync(0xffffffffu, mnv, off));
     }
     if (lane == 0) {
-        out[2 * hidx] = make_float4(mal, mxu, mxv, 0.f);
-        out[2 * hidx + 1] = make_float4(mau, mnu == inf ? 0.f : mnu, mnv == inf ? 0.f : mnv, 0.f);
+        rec[TC_BN + 2 * (hidx & 1)] = make_float4(mal, mxu, mxv, 0.f);
+        rec[TC_BN + 2 * (hidx & 1) + 1] = make_float4(mau, mnu == inf ? 0.f : mnu, mnv == inf ? 0.f : mnv, 0.f);
     }
 }
 
-int launch_tc_tile_consts(const float4 *rowc, int64_t N, float4 *out, cudaStream_t s)
+int launch_tc_side(const float *xn2, const float2 *en, int64_t N, float4 *side, cudaStream_t s)
 {
     const int64_t halves = (N + TC_BN - 1) / TC_BN * 2;
     if (halves == 0) return OK;
-    tc_tile_consts_kernel<<<(unsigned)((halves + 7) / 8), 256, 0, s>>>(rowc, N, halves, out);
-    SSB_CHECK_LAUNCH();
-    return OK;
-}
-
-
-int launch_tc_row_consts(const float *xn2, const float2 *en, int64_t N, float4 *out, cudaStream_t s)
-{
-    if (N == 0) return OK;
-    const int64_t padded = (N + 127) / 128 * 128;  // out holds ceil(N/128)*128 entries
-    tc_row_consts_kernel<<<(unsigned)((padded + 255) / 256), 256, 0, s>>>(xn2, en, N, out);
+    tc_side_kernel<<<(unsigned)((halves + 7) / 8), 256, 0, s>>>(xn2, en, N, side);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -879,8 +870,8 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
-int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb,
-                     const float4 *rowc, const float4 *tilec, int64_t N, int n, int k, unsigned int *gbound,
+int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb, int xb_cw,
+                     const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s)
 {
@@ -889,7 +880,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     if (nq == 0 || N == 0) return OK;
     TcParams p;
     p.n = n;
-    p.CW = tcx_cw(n);  // the operand's chunk width (layout.cuh)
+    p.CW = xb_cw;  // the operand's chunk width (layout.cuh tcx_*)
+    SSB_REQUIRE(xb_cw == 64 || xb_cw == 32, "K-chunk width must be 64 or 32");
     p.KB = (n + p.CW - 1) / p.CW;
     p.N = N;
     p.nq = nq;
@@ -914,8 +906,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.qb = reinterpret_cast<const uint4 *>(Qb);
     p.qn2 = qn2;
     p.qen = qen;
-    p.rowc = rowc;
-    p.tilec = tilec;
+    p.side = side;
     p.gbound = gbound;
     p.gbucket = nullptr;
     DevBuf buckets;
@@ -963,7 +954,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     // serial epilogue work, which pays where the MMA per tile is long (n > 128:
     // C2 +3%); at n = 96 (C3) 8 warps measured 5% faster.  The k = 32 list
     // variant keeps 8 (register budget).  SSB_TC_EPW=8|16 overrides (A/B).
-    static const int epw_env = getenv("SSB_TC_EPW") ? atoi(getenv("SSB_TC_EPW")) : 0;
+    const int epw_env = getenv("SSB_TC_EPW") ? atoi(getenv("SSB_TC_EPW")) : 0;
     const int epw_pref = epw_env ? epw_env : (n > 128 ? 16 : 8);
     const int epw = (epw_pref == 16 && !(k > 16 && k <= 32) && !dump) ? 16 : 8;
     auto go = [&](auto kern) -> int {
@@ -1026,8 +1017,8 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     const int Bp = (B + TC_BM - 1) / TC_BM * TC_BM;
     DevBuf qb, xb, qn2, qnm, xn2, xnm, gb, cand, cn;  // qnm, xnm: float2 error norms
     SSB_CUDA(qb.alloc(2 * (size_t)Bp * n, s));
-    SSB_CUDA(xb.alloc((size_t)tcx_bytes(N, n), s));
-    SSB_CUDA(cudaMemsetAsync(xb.p, 0, (size_t)tcx_bytes(N, n), s));
+    SSB_CUDA(xb.alloc((size_t)tcx_bytes(N, n, tcx_default_cw(n)), s));
+    SSB_CUDA(cudaMemsetAsync(xb.p, 0, (size_t)tcx_bytes(N, n, tcx_default_cw(n)), s));
     SSB_CUDA(qn2.alloc(4 * (size_t)Bp, s));
     SSB_CUDA(qnm.alloc(8 * (size_t)Bp, s));
     SSB_CUDA(xn2.alloc(4 * (size_t)N, s));
@@ -1042,15 +1033,11 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     if (rc) return rc;
     rc = launch_to_bf16_norms(X, nullptr, N, n, false, xb.p, xn2.as<float>(), xnm.as<float2>(), false, s);
     if (rc) return rc;
-    DevBuf rcb;
-    SSB_CUDA(rcb.alloc(16 * (size_t)((N + 127) / 128 * 128), s));
-    rc = launch_tc_row_consts(xn2.as<float>(), xnm.as<float2>(), N, rcb.as<float4>(), s);
+    DevBuf side;
+    SSB_CUDA(side.alloc((size_t)tc_side_bytes(N), s));
+    rc = launch_tc_side(xn2.as<float>(), xnm.as<float2>(), N, side.as<float4>(), s);
     if (rc) return rc;
-    DevBuf tcb;
-    SSB_CUDA(tcb.alloc(16 * (size_t)((N + TC_BN - 1) / TC_BN * 4), s));
-    rc = launch_tc_tile_consts(rcb.as<float4>(), N, tcb.as<float4>(), s);
-    if (rc) return rc;
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, rcb.as<float4>(), tcb.as<float4>(), N, n,
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, tcx_default_cw(n), side.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));

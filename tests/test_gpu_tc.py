@@ -23,15 +23,12 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-# 64-column K-chunks (SWIZZLE_128B, the default) and 32-column chunks (SWIZZLE_64B, SSB_TC_CW=32)
+# the tile-major pre-swizzled operand: 64-column K-chunks (SWIZZLE_128B) where
+# n % 64 == 0, else 32-column chunks (SWIZZLE_64B): n = 96, 160, 224, 32
 @pytest.mark.parametrize("n,B,N", [(256, 200, 1000), (96, 130, 777), (64, 5, 300), (128, 128, 128),
                                    (160, 70, 500), (224, 130, 400), (32, 40, 300)])
-@pytest.mark.parametrize("cw", [None, "32"])
-def test_tc_dot_matches_bf16_matmul(ssb, n, B, N, cw, monkeypatch):
+def test_tc_dot_matches_bf16_matmul(ssb, n, B, N):
     import torch
-
-    if cw is not None:  # SSB_TC_CW is read per launch
-        monkeypatch.setenv("SSB_TC_CW", cw)
 
     from paper_2212_13297_b200 import _lib
 
