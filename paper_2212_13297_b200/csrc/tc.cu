@@ -163,7 +163,8 @@ struct TcParams {
     const float2 *qen;         // per query: (||qh||, ||ql||) rounded up
     const float4 *side;        // per tile: TC_SIDE float4 (row bound constants, half-tile extremes)
     unsigned int *gbound;      // per query: float bits of the shared bound (d^2 units)
-    unsigned int *gbucket;     // per query x k (k >= 2): min upper bound of the rows r with r % k == b
+    unsigned int *gbucket;     // per query x kstride (k >= 2): min upper bound of the rows hashed to bucket b
+    int kstride;               // bucket stride per query: k rounded up to 4 (16-byte rows for the refresh loads)
     int k;
     uint2 *cand;               // (query, row) candidates
     float *cand_lb;            // their lower bounds (rescoring skips rows above the final bound)
@@ -472,12 +473,12 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             top[i] = i < KT - p.k ? __int_as_float(0xff800000) : __int_as_float(0x7f800000);
         float kth = __int_as_float(0x7f800000);
         unsigned int *gb = qvalid ? &p.gbound[ql] : nullptr;
-        float gnext = qvalid ? __uint_as_float(*(volatile const unsigned int *)gb) : -1.f;
+        float gnext = qvalid ? __uint_as_float(*(volatile const unsigned int *)gb) : -1.f, gseen = gnext;
         // bucket bound (k >= 2): rows are split into k classes by r % k; the
         // largest per-class minimum of the upper bounds bounds the k-th
         // smallest distance (k distinct rows lie below it), and it pools the
         // upper bounds of every thread and CTA that scans this query
-        unsigned int *bk = (qvalid && p.gbucket) ? p.gbucket + (int64_t)ql * p.k : nullptr;
+        unsigned int *bk = (qvalid && p.gbucket) ? p.gbucket + (int64_t)ql * p.kstride : nullptr;
         const uint32_t kk = (uint32_t)p.k;
         float bmax = __int_as_float(0x7f800000);  // last bucket bound read by this thread
         bool touched = false;
@@ -512,10 +513,14 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const bool revisit = t >= nwarm && t < 2 * nwarm;
             const TileSlot &ts = slots[rs];
             mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
-            // the shared bound of this query (other CTAs tighten it): read one
-            // tile ahead so the load's latency hides behind this tile's work
-            const float gcur = gnext;
-            if (qvalid) gnext = __uint_as_float(*(volatile const unsigned int *)gb);
+            // the shared bound of this query (other CTAs tighten it): read every
+            // 8th tile, used from the 8th tile after, so the L2 round trip never
+            // sits on a tile's critical path
+            if ((t & 7) == 0) {
+                gseen = gnext;
+                if (qvalid) gnext = __uint_as_float(*(volatile const unsigned int *)gb);
+            }
+            const float gcur = gseen;
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
             const float4 tcl = ts.tilec[2 * hh], tcu = ts.tilec[2 * hh + 1];
@@ -656,21 +661,31 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // drain the stage once it is half full (a tile adds at most 4 x 32 x 16
             // entries; reservations past its end already went to global memory)
             if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
-            // refresh the bucket bound after this thread's own updates
-            // (every 8th tile; the loads are independent so their latencies overlap)
-            if (touched && ((t & p.rmask) == p.rmask || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
+            // refresh the bucket bound after this thread's own updates, every
+            // rmask+1 tiles, the epilogue warps staggered (never all on the same
+            // tile: a refresh is a few L2 round trips and the MMA runs only two
+            // tiles ahead); 16-byte loads, 32 buckets per batch in flight
+            if (touched && (((t + ew) & p.rmask) == p.rmask || t == niter - 1 || !(bmax < __int_as_float(0x7f800000)))) {
                 uint32_t mxb = 0;
                 if constexpr (KTOP > 0) {
 #pragma unroll
                     for (int b = 0; b < KT; b++)
                         if (b < (int)kk) mxb = max(mxb, __ldcg(bk + b));
                 } else {
-                    for (uint32_t b0 = 0; b0 < kk; b0 += 16) {
-                        uint32_t x[16];
+                    const uint4 *b4 = reinterpret_cast<const uint4 *>(bk);
+                    for (uint32_t b0 = 0; b0 < kk; b0 += 32) {
+                        uint4 x[8];
 #pragma unroll
-                        for (int j = 0; j < 16; j++) x[j] = b0 + j < kk ? __ldcg(bk + b0 + j) : 0u;
+                        for (int j = 0; j < 8; j++)
+                            x[j] = b0 + 4 * j < kk ? __ldcg(b4 + b0 / 4 + j) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-                        for (int j = 0; j < 16; j++) mxb = max(mxb, x[j]);
+                        for (int j = 0; j < 8; j++) {
+                            const uint32_t bb = b0 + 4 * j;
+                            mxb = max(mxb, bb < kk ? x[j].x : 0u);
+                            mxb = max(mxb, bb + 1 < kk ? x[j].y : 0u);
+                            mxb = max(mxb, bb + 2 < kk ? x[j].z : 0u);
+                            mxb = max(mxb, bb + 3 < kk ? x[j].w : 0u);
+                        }
                     }
                 }
                 bmax = fminf(bmax, __uint_as_float(mxb));  // 0xffffffff (unset) reads as NaN: ignored
@@ -909,9 +924,11 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.side = side;
     p.gbound = gbound;
     p.gbucket = nullptr;
+    p.kstride = k;
     DevBuf buckets;
     if (k >= 2 && !dump && !(getenv("SSB_TC_NOBUCKET") && k <= TC_KTOP)) {  // env: diagnostics
-        const size_t bytes = 4 * (size_t)tc_bound_slots(nq) * (size_t)k;
+        p.kstride = (k + 3) & ~3;
+        const size_t bytes = 4 * (size_t)tc_bound_slots(nq) * (size_t)p.kstride;
         SSB_CUDA(buckets.alloc(bytes, s));
         SSB_CUDA(cudaMemsetAsync(buckets.p, 0xff, bytes, s));  // unset (NaN bits; atomicMin on the bits)
         p.gbucket = buckets.as<unsigned int>();

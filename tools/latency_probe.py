@@ -44,6 +44,33 @@ def main():
     idx = build_index_array(Xd, IndexSettings(series_length=wl.n, dataset_size=wl.N, leaf_threshold=wl.tau))
     eng = QueryEngine(idx)
     routes = a.routes.split(",")
+    import paper_2212_13297_b200 as ssb
+
+    for label, fn, k in wl.cells[:1]:
+        # the brute-force scan of ONE query (pscan.brute_force_knn; B <= 4 takes
+        # the row-parallel early-abandoning scan): latency and scan-equivalent GB/s
+        Q = fn()
+        od2, oid = oracle.knn_scan(X, Q[:3], k, threads=os.cpu_count())
+        lat, ok = [], True
+        _lib.prof_reset()
+        _lib.prof_enable(True)
+        for i in range(a.single + 2):
+            q = torch.from_numpy(Q[i % 3:i % 3 + 1]).cuda()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d2, ids = ssb.knn_batch(Xd, q, k)
+            torch.cuda.synchronize()
+            if i >= 2:
+                lat.append(time.perf_counter() - t0)
+            ok &= bool(np.array_equal(ids.cpu().numpy()[0], oid[i % 3]))
+        _lib.prof_enable(False)
+        kp = _lib.prof_read()
+        ms = statistics.median(lat) * 1000
+        print(json.dumps({"workload": wl.name, "cell": label, "k": k, "route": "bruteforce B=1",
+                          "single_ms_median": round(ms, 3), "parity_ok": ok,
+                          "scan_equivalent_GBps": round(wl.N * wl.n * 4 / (ms / 1000) / 1e9, 1),
+                          "kernels_ms_GB": {kk: [round(v[0] / (a.single + 2), 4), round(v[2] / (a.single + 2) / 1e9, 3)]
+                                            for kk, v in kp.items()}}), flush=True)
     for label, fn, k in wl.cells:
         Q = fn()
         od2, oid = oracle.knn_scan(X, Q[:a.check], k, threads=os.cpu_count())
