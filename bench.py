@@ -118,6 +118,9 @@ def parse(argv=None):
     ap.add_argument("--no-multi", action="store_true", help="one ssb_query per call (not ssb_query_multi)")
     ap.add_argument("--ingest-gb", type=float, default=4.0,
                     help="file -> HBM ingest sample (GB of the shard; 0 = skip), reported under build.ingest")
+    ap.add_argument("--clock-ms", type=int, default=100,
+                    help="nvidia-smi sampling period during the timed region (0 = off; NVML queries contend "
+                         "with the driver, so keep it coarse)")
     ap.add_argument("--backend", default="nccl", choices=("nccl", "gloo"),
                     help="torch.distributed backend (gloo: CPU tests of the multi-rank plumbing)")
     return ap.parse_args(argv)
@@ -172,9 +175,10 @@ class Clocks:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int = 0, enabled: bool = True):
+    def __init__(self, index: int = 0, enabled: bool = True, period_ms: int = 100):
         self.index = index
-        self.enabled = enabled
+        self.enabled = enabled and period_ms > 0
+        self.period_ms = period_ms
         self.proc = None
         self.lines: list[str] = []
 
@@ -184,7 +188,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -204,10 +208,19 @@ class Clocks:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def mark(self):
+        self.marks = getattr(self, "marks", []) + [len(self.lines)]
+
     def summary(self) -> dict:
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
+        marks = getattr(self, "marks", [])
+        lines = self.lines
+        if len(marks) == 2 and marks[1] > marks[0]:
+            lines = lines[marks[0]:marks[1] + 1]  # the samples inside the timed region (+ the next)
+        elif len(marks) == 2:
+            lines = lines[marks[0]:marks[0] + 2]  # region shorter than one sampling period
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -600,7 +613,14 @@ def run_ours(args, rank, world) -> int:
         torch.distributed.all_gather(out, t)
         return [float(x.item()) for x in out]
 
+    # the clock sampler starts before the warm-up: nvidia-smi's start-up (NVML
+    # init) contends with the driver, so it must be over -- with the GPU kept
+    # busy, not idle -- before the timed region opens
+    clk = Clocks(local, enabled=dev.cuda, period_ms=args.clock_ms).__enter__()
+    t_settle = time.perf_counter()
     for _ in range(args.warmup):
+        step(Q_dev)
+    while dev.cuda and time.perf_counter() - t_settle < 0.5:
         step(Q_dev)
     dev.sync()
 
@@ -612,14 +632,18 @@ def run_ours(args, rank, world) -> int:
         _lib.prof_enable(True)
         launches0 = _lib.launch_count()
     region = dev.region()
-    with Clocks(local, enabled=dev.cuda) as clk:
+    try:
         barrier()
         dev.sync()
+        clk.mark()  # only the samples taken inside the region count
         region.start()
         for _ in range(args.steps):
             step(Q_dev)
         ms_local = region.stop()
+        clk.mark()
         barrier()
+    finally:
+        clk.__exit__(None, None, None)
     prof, launches = {}, 0
     if dev.cuda:
         launches = _lib.launch_count() - launches0
@@ -645,6 +669,26 @@ def run_ours(args, rank, world) -> int:
     dev.sync()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e = answers * args.steps / e2e_s
+
+    # ---- single-query latency through the reference's own per-query API ------
+    # (QueryEngine.exact_knn, query.py:296-348: one query per call, host
+    # buffers, QueryStats included; N = 1 only -- a sharded query is a block)
+    single = None
+    if world == 1 and isinstance(engine, IndexEngine):
+        from paper_2212_13297_b200 import QueryConfig
+
+        k0, Q0 = calls[0]
+        lat, routes = [], []
+        for i in range(22):
+            t0 = time.perf_counter()
+            _, st = engine.engine.exact_knn(Q0[i % len(Q0)], QueryConfig(k=k0))
+            if i >= 2:
+                lat.append(time.perf_counter() - t0)
+                routes.append(st.phase_reached)
+        single = {"api": "QueryEngine.exact_knn (one query per call, host buffers)", "k": k0,
+                  "median_ms": round(1000 * statistics.median(lat), 3), "p90_ms": round(
+                      1000 * sorted(lat)[int(0.9 * len(lat))], 3), "calls": len(lat),
+                  "phase_reached": sorted(set(routes))}
 
     # ---- parity (and, at N = 1, the CPU baseline) through the oracle ----------
     parity = cb = None
@@ -751,6 +795,7 @@ def run_ours(args, rank, world) -> int:
         "cpu_baseline": cb,
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
+        "single_query": single,
         "gpu_launches": launches,
         "build": dict(engine.build_info(hi - lo) or {}, **({"ingest": ingest} if ingest else {}),
                       **({"device_gen": device_gen} if device_gen else {})),

@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(256)
 // four 8-lane groups take the survivor rows round robin.
 
 template <int NT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     ix_scan_kernel(const float *__restrict__ X, const uint32_t *__restrict__ orig, const uint4 *__restrict__ ent,
                    const unsigned long long *__restrict__ n_ent, int64_t ent_cap, const float *__restrict__ Qp,
                    ScanOut out, uint32_t *__restrict__ abandoned, unsigned long long *__restrict__ prof_bytes)
@@ -752,11 +752,13 @@ static int launch_seed_t(const Index &ix, const double *lbe, const float *tbl, c
 {
     // candidates ranked then scanned exactly: a few times k (SSB_SEED_MULT, A/B
     // switch), at least 64, at most the candidate buffer
-    const int mult = getenv("SSB_SEED_MULT") ? std::max(1, atoi(getenv("SSB_SEED_MULT"))) : 4;
+    // (small blocks -- latency, one SM per query anyway -- rank more: a tighter
+    // bound shrinks the LB_SAX survivors and the candidates that follow)
+    const int mult = getenv("SSB_SEED_MULT") ? std::max(1, atoi(getenv("SSB_SEED_MULT"))) : (B <= 64 ? 10 : 4);
     const int target = std::min(IX_CMAX - 64, std::max(64, mult * k));
     // leaves ranked at least (SSB_SEED_LEAVES, A/B switch; the approximate phase
     // otherwise stops at the first leaves that hold k series)
-    const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES"))) : 1;
+    const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES"))) : (B <= 64 ? 4 : 1);
     ProfScope ps("ix_seed", s, 0.0);
     // one CTA per query: small blocks take 1024 threads so a single query's
     // approximate phase still spreads over a whole SM

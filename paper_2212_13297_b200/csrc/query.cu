@@ -122,45 +122,69 @@ __global__ void skip_unflagged_kernel(const int32_t *__restrict__ flags, const i
     if (q < B) skip[q] = (!flags[q] || use_tc[q]) ? 1 : 0;
 }
 
-// returns -1 when a work buffer (items / entries) overflowed: the caller halves the block
+// ---------------------------------------------------------------------------
+// Routing between the index route and the lean tensor-core batch (DESIGN.md
+// "Routing").  The index keeps an observation of its route's work per query
+// (the fraction of rows its leaf pruning keeps, the LB_SAX survivors per kept
+// row), refreshed by every block that runs the index stages; with it the
+// modelled index time per query is compared with the filter's share of one
+// pass over the rows.
+
+// modelled index-route time of a query keeping `kept` rows (ns)
+static double idx_ns(const Index &ix, double kept)
+{
+    if (ix.kept_frac_ema < 0.0) return kept * IX_NS_IX_ROW;  // nothing observed yet
+    return kept * (IX_NS_WORD + ix.surv_per_kept_ema * IX_NS_SURVIVOR * ix.n / 256.0);
+}
+
 // The lean all-tensor-core batch (no index stages): route "tensor"; and for
-// "auto", blocks of >= 256 queries (whole filter groups) on an index whose
-// leaf pruning, as observed on recent blocks, keeps far more rows than the
-// break-even fraction of the cost model (the index route could not win for a
-// typical query, so its stages would only cost time) and whose filter pass is
-// not so long that the approximate phase's bound pays off.  Every 16th such block
-// runs the index stages again to refresh the observation.  SSB_AUTO_LEAN=0|1
-// forces the choice (A/B).
+// "auto", blocks whose typical query -- as observed on recent blocks -- costs
+// the index route more than twice its share of a filter pass (C2 / C3 / C4
+// batches: LB_EAPCA keeps 25-100% of the leaves), unless the filter's pass per
+// query dwarfs the approximate phase's reads so much that the index stages
+// pay for themselves through the bound they hand the filter (C4: ~100x).
+// Every 16th such block runs the index stages again to refresh the
+// observation.  SSB_AUTO_LEAN=0|1 forces the choice (A/B).
 static bool tc_all_for(const Index &ixc, const QueryCfg &qc, int k, int B)
 {
     if (!ixc.Xb || k > TC_KTOP_MAX) return false;
     if (qc.route == 2) return true;
     if (qc.route != 0) return false;
     if (const char *e = getenv("SSB_AUTO_LEAN")) return atoi(e) != 0;
-    if (B < 256) return false;
-    // the index stages still pay for themselves through the approximate
-    // phase's bound (the filter starts from it instead of +inf) when the
-    // filter's pass per query dwarfs that phase's reads (C4: ~100x; C2: ~13x)
+    const int G = std::min(B, 256);  // queries sharing one filter pass
+    const double tc_ns = (double)ixc.N * IX_NS_TC_ROW * ixc.n / 256.0 / (double)G;
     const double avg_leaf = (double)ixc.N / (double)std::max(1, ixc.L);
     const double seed_bytes = avg_leaf * 16.0 + (double)std::max(64, 4 * k) * 4.0 * ixc.n;
-    const double tc_bytes = (double)ixc.N * 2.0 * ixc.n / 256.0;
-    if (tc_bytes > 64.0 * seed_bytes) return false;
+    const double tc_bytes = (double)ixc.N * 2.0 * ixc.n / (double)G;
+    if (B >= 32 && tc_bytes > 64.0 * seed_bytes) {
+        if (getenv("SSB_ROUTE_TRACE"))
+            fprintf(stderr, "[ssb] route B=%d k=%d filter/seed bytes %.1f -> index stages\n", B, k, tc_bytes / seed_bytes);
+        return false;
+    }
     Index &ix = const_cast<Index &>(ixc);  // the routing observation is the only mutable part
     std::lock_guard<std::mutex> lock(ix.graph_mu);
-    const double breakeven = IX_NS_TC_ROW / (256.0 * IX_NS_IX_ROW);
-    if (ix.kept_frac_ema < 0.0 || ix.kept_frac_ema < 2.0 * breakeven) return false;
-    if (++ix.lean_since_probe >= 16) {
+    const double ix_ns = idx_ns(ix, ix.kept_frac_ema * (double)ix.N);
+    bool lean = true;
+    if (ix.kept_frac_ema < 0.0 || ix_ns < 2.0 * tc_ns) {
+        lean = false;
+    } else if (++ix.lean_since_probe >= 16) {
         ix.lean_since_probe = 0;
-        return false;  // probe
+        lean = false;  // probe
     }
-    return true;
+    if (getenv("SSB_ROUTE_TRACE"))
+        fprintf(stderr, "[ssb] route B=%d k=%d kept_frac=%.4f surv/kept=%.4f index %.1f us filter %.1f us/query -> %s\n",
+                B, k, ix.kept_frac_ema, ix.surv_per_kept_ema, ix_ns / 1000, tc_ns / 1000, lean ? "lean" : "index stages");
+    return lean;
 }
 
-static void observe_kept(const Index &ixc, double frac)
+// a block ran the index stages: its queries kept `kept` rows and `surv`
+// LB_SAX survivors in total (index-routed queries only for surv)
+static void observe_route(const Index &ixc, double kept_frac, double surv_per_kept)
 {
     Index &ix = const_cast<Index &>(ixc);
     std::lock_guard<std::mutex> lock(ix.graph_mu);
-    ix.kept_frac_ema = ix.kept_frac_ema < 0.0 ? frac : 0.5 * (ix.kept_frac_ema + frac);
+    ix.kept_frac_ema = ix.kept_frac_ema < 0.0 ? kept_frac : 0.5 * (ix.kept_frac_ema + kept_frac);
+    if (surv_per_kept >= 0.0) ix.surv_per_kept_ema = 0.5 * (ix.surv_per_kept_ema + surv_per_kept);
     ix.lean_since_probe = 0;
 }
 
@@ -173,6 +197,7 @@ static bool small_block_ok(const Index &ix, const QueryCfg &qc, int B)
     return mode == 1 && B <= 64 && (int64_t)B * (ix.N / 512 + ix.L + 1) <= (256 << 10);
 }
 
+// returns -1 when a work buffer (items / entries) overflowed: the caller halves the block
 static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int B, int k, uint64_t *out_keys,
                        uint32_t *stats_host, cudaStream_t s)
 {
@@ -183,7 +208,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     // auto: when even a query that keeps every leaf is cheaper on the index
     // route than a filter pass shared by the whole block (small blocks), no
     // query takes the filter
-    const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW;
+    const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW * n / 256.0;
     if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= tc_group_ns) mode = 1;
     IxWork w;
     int rc = ix_front(ix, qc, Q, B, k, mode, want, w, s);
@@ -222,11 +247,6 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(cudaMemcpyAsync(qi.data(), w.q_items.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(tc.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
-        if (qc.route == 0 && B >= 256) {
-            double kept = 0.0;
-            for (int q = 0; q < B; q++) kept += (double)kr[q];
-            observe_kept(ix, kept / ((double)B * (double)std::max<int64_t>(ix.N, 1)));
-        }
         if (mode == 0) {
             // queries by index cost, most expensive first; the filter takes a
             // prefix of them, t in {0, 256, 512, ..., B} (within a group the
@@ -235,7 +255,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             for (int q = 0; q < B; q++) order[q] = q;
             std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return kr[a] > kr[b]; });
             std::vector<double> suffix(B + 1, 0.0);
-            for (int i = B - 1; i >= 0; i--) suffix[i] = suffix[i + 1] + (double)kr[order[i]] * IX_NS_IX_ROW;
+            for (int i = B - 1; i >= 0; i--) suffix[i] = suffix[i + 1] + idx_ns(ix, (double)kr[order[i]]);
             int best_t = 0;
             double best = suffix[0];
             for (int t = 256;; t += 256) {
@@ -395,6 +415,25 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
                                 nullptr, nullptr, ns, so, s);
             if (rc) return rc;
         }
+    }
+    if (qc.route == 0) {  // the routing observation (kept rows of every query, survivors of the index-routed)
+        std::vector<unsigned long long> kr(B);
+        std::vector<uint32_t> sv(B);
+        std::vector<int32_t> tc(B);
+        SSB_CUDA(cudaMemcpyAsync(kr.data(), w.kept_rows.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(sv.data(), cser.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(tc.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        double kept = 0.0, kept_ix = 0.0, surv_ix = 0.0;
+        for (int q = 0; q < B; q++) {
+            kept += (double)kr[q];
+            if (!tc[q]) {
+                kept_ix += (double)kr[q];
+                surv_ix += (double)sv[q];
+            }
+        }
+        observe_route(ix, kept / ((double)B * (double)std::max<int64_t>(ix.N, 1)),
+                      kept_ix > 0.0 ? surv_ix / kept_ix : -1.0);
     }
     if (want) {
         std::vector<uint32_t> kl(B), sl(B), sr(B), sw(B), ab(B), cs(B);
@@ -757,6 +796,18 @@ static int small_block_graph(const Index &ix, const QueryCfg &qc, const float *Q
     if ((int64_t)n_items > g->item_cap || (int64_t)n_ents > g->ent_cap) return OK;
     for (int q = 0; q < B; q++)
         if (g->hstat[q]) return OK;  // a candidate buffer overflowed: the general path tightens
+    // the routing observation (kept rows incl. the approximate phase's, LB_SAX survivors)
+    if (qc.route == 0) {
+        const uint32_t *st = reinterpret_cast<const uint32_t *>(hs + stat_off_stats(B));
+        double kept = 0.0, surv = 0.0;
+        for (int q = 0; q < B; q++) {
+            kept += st[q * SSB_QUERY_STATS + 5];
+            surv += st[q * SSB_QUERY_STATS + 1];
+        }
+        ixm.kept_frac_ema = ixm.kept_frac_ema < 0.0 ? kept / ((double)B * (double)ix.N)
+                                                    : 0.5 * (ixm.kept_frac_ema + kept / ((double)B * (double)ix.N));
+        if (kept > 0.0) ixm.surv_per_kept_ema = 0.5 * (ixm.surv_per_kept_ema + surv / kept);
+    }
     // the keys leave the shared buffer before the lock is released (stream order)
     SSB_CUDA(cudaMemcpyAsync(out_keys, g->keys, 8 * (size_t)B * k, cudaMemcpyDeviceToDevice, s));
     if (stats_host) std::memcpy(stats_host, hs + stat_off_stats(B), (size_t)B * SSB_QUERY_STATS * 4);

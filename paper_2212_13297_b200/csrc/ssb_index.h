@@ -74,6 +74,7 @@ struct Index {
     // index route's leaf pruning keeps, over recent full blocks (< 0: none
     // observed yet), and the lean blocks answered since the last observation
     double kept_frac_ema = -1.0;
+    double surv_per_kept_ema = 0.0;  // LB_SAX survivors (exactly scanned) per kept row
     int lean_since_probe = 0;
     ~Index();
 };
@@ -93,6 +94,11 @@ struct QueryCfg {
 // word, the LB_SAX arithmetic and its share of the exact scan of survivors)
 constexpr double IX_NS_TC_ROW = 0.14;
 constexpr double IX_NS_IX_ROW = 0.03;
+// ... refined once the route has run on the index: IX_NS_WORD per kept row
+// (its SAX word and the LB_SAX arithmetic) + IX_NS_SURVIVOR per exactly scanned
+// survivor at n = 256 (the rows read before abandonment; scaled by n / 256)
+constexpr double IX_NS_WORD = 0.01;
+constexpr double IX_NS_SURVIVOR = 0.5;
 
 // Everything of one query block on the index path, stream-ordered; the
 // per-stage outputs the caller needs afterwards (bounds, routing, counters)

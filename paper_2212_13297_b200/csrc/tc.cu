@@ -337,27 +337,26 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
                     "r"(tile_bytes)
                     : "memory");
-                // whole K-chunks (contiguous in the pre-swizzled operand): CTA `rank`
-                // loads the chunks c with c % CS == rank and multicasts them; alone
-                // (CS = 1) it loads the whole tile in one copy
-                const unsigned char *tsrc = p.xb + (size_t)tile * tile_bytes;
-                const uint32_t tdst = ring + (uint32_t)slot * tile_bytes;
-                if (CS == 1) {
+                // a tile is contiguous both in the pre-swizzled operand and in its
+                // ring slot: CTA `rank` multicasts the rank-th 1/CS of its bytes
+                // (one copy per CTA and tile, balanced whatever KB is)
+                const uint32_t part = tile_bytes / (uint32_t)CS;
+                const unsigned char *tsrc = p.xb + (size_t)tile * tile_bytes + (size_t)rank * part;
+                const uint32_t tdst = ring + (uint32_t)slot * tile_bytes + (uint32_t)rank * part;
+                if (CS == 1)
                     asm volatile(
                         "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
                         "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                         " [%0], [%2], %3, [%1];\n}" ::"r"(tdst),
-                        "r"(bar), "l"(tsrc), "r"(tile_bytes)
+                        "r"(bar), "l"(tsrc), "r"(part)
                         : "memory");
-                } else {
-                    for (int kb = rank; kb < KB; kb += CS)
-                        asm volatile(
-                            "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
-                            "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(tdst + (uint32_t)kb * chunk_bytes),
-                            "r"(bar), "l"(tsrc + (size_t)kb * chunk_bytes), "r"(chunk_bytes), "h"(cmask)
-                            : "memory");
-                }
+                else
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(tdst),
+                        "r"(bar), "l"(tsrc), "r"(part), "h"(cmask)
+                        : "memory");
                 if (++slot == NS) {
                     slot = 0;
                     phase ^= 1u;

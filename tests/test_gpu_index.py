@@ -367,6 +367,31 @@ def test_sharded_forest_merge_on_device(ssb, oracle):
     assert list(gids.cpu().numpy()[-1][:2]) == [7, 8500]
 
 
+def test_device_merge_pads_k_above_total(ssb, oracle):
+    """Shards holding fewer than k rows in total: the device packing marks the
+    missing answers as empty keys and the K-merge returns (inf, -1) for them,
+    like query.py:70-75."""
+    import torch
+
+    from paper_2212_13297_b200.distributed import merge_device, pack_keys
+
+    X = random_walks(7, 64, 33)
+    Q = X[[2, 5]]
+    k = 10
+    parts = []
+    for lo, hi in ((0, 3), (3, 7)):
+        d2, ids = ssb.knn_batch(X[lo:hi], Q, k, id_base=lo)
+        keys = pack_keys(d2, ids)
+        assert keys.is_cuda and (keys[:, hi - lo:] == -1).all()
+        parts.append(keys)
+    all_keys = torch.cat(parts, dim=1).contiguous()
+    gd2, gids = merge_device(all_keys, k)
+    od2, oid = oracle.knn_scan(X, Q, k)
+    assert np.array_equal(gids.cpu().numpy(), oid)
+    assert (gids.cpu().numpy()[:, 7:] == -1).all() and np.isinf(gd2.cpu().numpy()[:, 7:]).all()
+    assert np.array_equal(bits(gd2.cpu().numpy()[:, :7]), bits(od2[:, :7]))
+
+
 def test_small_blocks_cuda_graph_path(ssb, oracle):
     """Blocks of <= 64 queries on the index route replay a captured CUDA graph
     (one per stream, B, k, lmax); repeated calls, different k / lmax / block
