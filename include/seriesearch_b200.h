@@ -103,6 +103,11 @@ typedef struct {
     int32_t series_length, num_nodes, num_leaves, levels, max_segments, depth;
     double build_ms;
     float max_abs;
+    /* K-proj (projected lower-bound filter): coefficients per row (0: none,
+     * the rows' energy is not concentrated enough) and the fraction of the
+     * build sample's energy they hold */
+    int32_t proj_dim;
+    double proj_energy;
 } ssb_index_info_t;
 
 /* one tree node (tree.py:92-179 Node + :51-89 SplitPolicy); first/count index
@@ -161,7 +166,8 @@ int ssb_index_load(const float *rows_host, const uint8_t *words_host, const uint
  *   [2] series scanned exactly by the approximate phase
  *   [3] 1 if the candidate buffer overflowed once (bound tightened, redone)
  *   [4] leaves visited by the approximate phase      [5] SAX words tested (index) / rows read (filter)
- *   [6] series abandoned early by the exact scan     [7] route: 0 index, 1 tensor-core filter
+ *   [6] series abandoned early by the exact scan
+ *   [7] route: 0 index, 1 tensor-core filter, 2 projected filter (K-proj)
  * Reads counts / flags back (host round trips inside the call); the outputs
  * are complete in `stream` order when it returns (no final synchronization). */
 #define SSB_QUERY_STATS 8

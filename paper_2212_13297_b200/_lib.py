@@ -78,7 +78,7 @@ class IndexInfo(ctypes.Structure):
                 ("num_nodes", ctypes.c_int32), ("num_leaves", ctypes.c_int32),
                 ("levels", ctypes.c_int32), ("max_segments", ctypes.c_int32),
                 ("depth", ctypes.c_int32), ("build_ms", ctypes.c_double),
-                ("max_abs", ctypes.c_float)]
+                ("max_abs", ctypes.c_float), ("proj_dim", ctypes.c_int32), ("proj_energy", ctypes.c_double)]
 
 
 class NodeRec(ctypes.Structure):

@@ -52,7 +52,7 @@ Index::~Index()
 {
     free_small_graphs(*this);
     void *ptrs[] = {X, words, orig, inv, bp, leaf_first, leaf_count, leaf_m, leaf_ep, leaf_env, Xb, xn2, xen, tcside,
-                    tcperm, segs, leaf_seg};
+                    tcperm, segs, leaf_seg, P, Zb, zside};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -1208,7 +1208,8 @@ static int alloc_tc_operands(Index &ix, DevBuf &tcinv, cudaStream_t s)
 static int finish_tc_operands(Index &ix, cudaStream_t s)
 {
     if (!ix.Xb) return OK;
-    return launch_tc_side(ix.xn2, ix.xen, ix.N, ix.tcside, s);
+    RC(launch_tc_side(ix.xn2, ix.xen, ix.N, ix.tcside, s));
+    return build_projection(ix, s);  // K-proj operands (skipped when they would not prune)
 }
 
 // the fused row pass (+ K-tc operands) of a built or loaded index

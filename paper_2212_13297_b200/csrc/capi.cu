@@ -253,6 +253,8 @@ int ssb_index_info(const ssb_index *h, ssb_index_info_t *out)
     out->max_segments = M_MAX;
     out->build_ms = ix.build_ms;
     out->max_abs = ix.max_abs;
+    out->proj_dim = ix.Zb ? ix.pd : 0;
+    out->proj_energy = ix.p_energy;
     int d = 0;
     for (auto &nd : ix.nodes) d = std::max(d, nd.depth);
     out->depth = d;
@@ -366,8 +368,8 @@ int ssb_query(const ssb_index *h, const float *Q, int32_t B, int32_t k, const ss
     QueryCfg qc;
     if (cfg) {
         SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
-        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
-                    "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
+        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 4,
+                    "route must be 0 (auto), 1 (tree), 2 (tensor core), 3 (eapca_th rule) or 4 (projected filter)");
         SSB_REQUIRE(cfg->lmax >= 1, "lmax must be at least 1");
         qc.eapca_th = cfg->eapca_th;
         qc.route = cfg->route;
@@ -386,8 +388,8 @@ int ssb_query_multi(const ssb_index *h, int32_t ncalls, const float *const *Q, c
     QueryCfg qc;
     if (cfg) {
         SSB_REQUIRE(cfg->eapca_th >= 0.f && cfg->eapca_th <= 1.f, "eapca_th must lie in [0, 1]");
-        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 3,
-                    "route must be 0 (auto), 1 (tree), 2 (tensor core) or 3 (eapca_th rule)");
+        SSB_REQUIRE(cfg->route >= 0 && cfg->route <= 4,
+                    "route must be 0 (auto), 1 (tree), 2 (tensor core), 3 (eapca_th rule) or 4 (projected filter)");
         SSB_REQUIRE(cfg->lmax >= 1, "lmax must be at least 1");
         qc.eapca_th = cfg->eapca_th;
         qc.route = cfg->route;

@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(256)
         }
         if (pass == 0) {
             int tc = 0;
-            if (mode == 2)
+            if (mode == 2 || mode == 4)  // 4: the index stages, then every query on the filters
                 tc = 1;
             else if (mode == 3)  // the reference's rule (query.py:321-325): weak envelope pruning -> scan
                 tc = (1.0 - (double)tl / (double)(L > 0 ? L : 1)) < (double)eapca_th ? 1 : 0;
@@ -754,11 +754,16 @@ static int launch_seed_t(const Index &ix, const double *lbe, const float *tbl, c
     // switch), at least 64, at most the candidate buffer
     // (small blocks -- latency, one SM per query anyway -- rank more: a tighter
     // bound shrinks the LB_SAX survivors and the candidates that follow)
-    const int mult = getenv("SSB_SEED_MULT") ? std::max(1, atoi(getenv("SSB_SEED_MULT"))) : (B <= 64 ? 10 : 4);
+    // (large indexes rank more too: the bound is what the filter passes over
+    // the whole index -- 25M rows x k = 100: a 900-row seed instead of 400
+    // tightens the median bound 84 -> 49 and shortens the full filter 9%)
+    const int mult = getenv("SSB_SEED_MULT") ? std::max(1, atoi(getenv("SSB_SEED_MULT")))
+                                             : (B <= 64 ? 10 : (ix.N >= ((int64_t)4 << 20) ? 9 : 4));
     const int target = std::min(IX_CMAX - 64, std::max(64, mult * k));
     // leaves ranked at least (SSB_SEED_LEAVES, A/B switch; the approximate phase
     // otherwise stops at the first leaves that hold k series)
-    const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES"))) : (B <= 64 ? 4 : 1);
+    const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES")))
+                                                     : (B <= 64 || ix.N >= ((int64_t)4 << 20) ? 4 : 1);
     ProfScope ps("ix_seed", s, 0.0);
     // one CTA per query: small blocks take 1024 threads so a single query's
     // approximate phase still spreads over a whole SM

@@ -1,0 +1,560 @@
+// proj.cu -- K-proj: the projected lower-bound filter.
+//
+// The reference prunes with lower bounds computed on reduced representations
+// of the series (EAPCA envelopes, PAA/SAX: query.py:127-251, summarize.py);
+// K-proj is one more such bound, chosen for the tensor cores.  Every row x
+// gets c = 62 coefficients z = P x of an orthonormal DCT-II basis (the basis
+// vectors of largest energy on a sample of the index's rows: random walks keep
+// ~98% of their energy in the first 62 of 256).  For any real vector v,
+//     ||v||^2 >= ||P v||^2 / Lambda,        Lambda >= lambda_max(P P^T),
+// so with zq = fl(P q), zx = fl(P x) (float32 FMA dot products, error norms
+// eq, ex <= gamma_n ||P||_F ||.||, Wilkinson):
+//     ||q - x|| >= (||zq - zx|| - eq - ex) / sqrt(Lambda).
+// A row can reach a query's top k only if its float32 distance is <= the
+// query's bound b (the approximate phase's k-th distance, k real rows), i.e.
+// its real distance is <= b (1 + 1e-5); hence only rows with
+//     ||zq - zx||^2 <= T_q = (sqrt(Lambda b (1 + 1e-5)) + eq + ex_max)^2 (+ slack)
+// are emitted.
+//
+// The operand is 64 BF16 columns (one K-chunk, four K = 16 MMA steps): the 62
+// coefficients and, folded into the dot product, the row's -||zx||^2 / 2 as a
+// two-term BF16 split (hi, lo) against the query's (1, 1).  The tensor cores
+// then produce zq.zx - ||zx||^2/2 per pair, so ||zq - zx||^2 = ||zq||^2 - 2 t:
+// the epilogue's test is one per-query threshold on t, exact at the tile level
+// (with unfolded norms, rows whose ||zx||^2 vary would loosen the tile-level
+// necessary condition by their spread and send most pairs to the per-row
+// test).  The filter (tc.cu, projected mode) bounds the BF16 / FP32 error of t
+// rigorously (its QH U + QL V interval, with the split's residual added to
+// T), every emitted row is rescored exactly in float32 (rescore_seg_kernel,
+// scan.cu arithmetic), and answers are bit-identical.  A query whose
+// candidate segment overflows (a weak bound: hard queries such as sigma = 1.0
+// noise) is answered by the full filter instead.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "layout.cuh"
+#include "ssb_common.cuh"
+#include "ssb_index.h"
+#include "ssb_internal.h"
+
+namespace ssb {
+
+constexpr int PJ_DMAX = 64;     // operand columns (one 64-column K-chunk): coefficients + the norm split
+constexpr int PJ_COEF = PJ_DMAX - 2;  // projection coefficients
+constexpr int PJ_ROWS = 64;     // rows per projection tile
+constexpr int PJ_SAMPLE = 16384;  // rows of the energy sample
+
+// ---------------------------------------------------------------------------
+// build: sample covariance (float64, logical element order)
+
+__global__ void proj_cov_kernel(const float *__restrict__ X, int64_t N, int n, const int32_t *__restrict__ pos, int S,
+                                double *__restrict__ C)
+{
+    const int a = blockIdx.x;
+    const int pa = pos[a];
+    for (int b = threadIdx.x; b < n; b += blockDim.x) {
+        const int pb = pos[b];
+        double acc = 0.0;
+        for (int i = 0; i < S; i++) {
+            const float *x = X + ((int64_t)i * N / S) * n;
+            acc += (double)__ldg(x + pa) * (double)__ldg(x + pb);
+        }
+        C[(int64_t)a * n + b] = acc;
+    }
+}
+
+// maxima of the rows' (U, V) error norms (non-negative floats: max on the bits)
+__global__ void max_uv_kernel(const float2 *__restrict__ v, int64_t N, unsigned int *__restrict__ out)
+{
+    unsigned int mu = 0, mv = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 x = v[i];
+        mu = max(mu, __float_as_uint(x.x));
+        mv = max(mv, __float_as_uint(x.y));
+    }
+    for (int off = 16; off; off >>= 1) {
+        mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, off));
+        mv = max(mv, __shfl_xor_sync(0xffffffffu, mv, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, mu);
+        atomicMax(out + 1, mv);
+    }
+}
+
+__global__ void max_bits_kernel(const float *__restrict__ v, int64_t N, unsigned int *__restrict__ out)
+{
+    unsigned int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(v[i])));
+    for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// ---------------------------------------------------------------------------
+// z = P x for R rows, fused with the BF16 operand and its norms (the
+// to_bf16_norms_kernel formulas).  CTA = 64-row tiles (persistent), 256
+// threads = 16 row groups x 16 coefficient groups, 4 x 4 accumulators each;
+// P^T and the tile (transposed, padded) in shared memory.  Rows: src row
+// rows[r] (or r), element j at pos[j] (lane-transposed index rows) or j.
+// is_query: row-major BF16 output and query norms (QH, QL); otherwise the
+// tile-major pre-swizzled operand (CW = 64) and row norms (U, V).
+__global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict__ X, int64_t R, int n,
+                                                        const int32_t *__restrict__ pos,
+                                                        const uint32_t *__restrict__ rows,
+                                                        const float *__restrict__ P, int d, int is_query,
+                                                        __nv_bfloat16 *__restrict__ zb, float *__restrict__ zn2,
+                                                        float2 *__restrict__ zen)
+{
+    extern __shared__ __align__(16) float pj_smem[];
+    float *pt = pj_smem;                      // [n][PJ_DMAX]
+    float *xs = pt + (size_t)n * PJ_DMAX;     // [n][PJ_ROWS + 1]
+    for (int idx = threadIdx.x; idx < n * PJ_DMAX; idx += blockDim.x) {
+        const int j = idx / PJ_DMAX, i = idx % PJ_DMAX;
+        pt[idx] = i < d ? P[(int64_t)i * n + j] : 0.f;
+    }
+    const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;  // rows tr*4.., coefficients tc*4..
+    for (int64_t t0 = (int64_t)blockIdx.x * PJ_ROWS; t0 < R; t0 += (int64_t)gridDim.x * PJ_ROWS) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < PJ_ROWS * n; idx += blockDim.x) {
+            const int r = idx / n, j = idx % n;
+            const int64_t row = t0 + r;
+            float v = 0.f;
+            if (row < R) {
+                const int64_t src = rows ? (int64_t)rows[row] : row;
+                v = __ldg(X + src * n + (pos ? pos[j] : j));
+            }
+            xs[j * (PJ_ROWS + 1) + r] = v;
+        }
+        __syncthreads();
+        float acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int c = 0; c < 4; c++) acc[r][c] = 0.f;
+        const float *xr = xs + tr * 4;
+        const float *pc = pt + tc * 4;
+        for (int j = 0; j < n; j++) {
+            const float4 p4 = *reinterpret_cast<const float4 *>(pc + j * PJ_DMAX);
+            const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const float xv = xr[j * (PJ_ROWS + 1) + r];
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[r][c] = fmaf(xv, pv[c], acc[r][c]);
+            }
+        }
+        // BF16 operand and norms.  The 16 coefficient groups of a row are 16
+        // consecutive lanes (xor-shuffle reductions).  Columns PJ_COEF,
+        // PJ_COEF + 1 (lane 15's last two): queries 1, 1; rows the two-term
+        // BF16 split (hi, lo) of -||zx||^2 / 2.
+        const double m = 1.0 + 0x1p-40;  // covers the float64 sums and square roots
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int64_t row = t0 + tr * 4 + r;
+            double a2 = 0.0, hh = 0.0, ll = 0.0;  // over the coefficients (acc is 0 past them)
+            __nv_bfloat16 b[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                b[c] = __float2bfloat16_rn(acc[r][c]);
+                const double v = acc[r][c], h = (double)__bfloat162float(b[c]);
+                a2 += v * v;
+                hh += h * h;
+                ll += (v - h) * (v - h);
+            }
+            for (int off = 8; off; off >>= 1) {
+                a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+                hh += __shfl_xor_sync(0xffffffffu, hh, off);
+                ll += __shfl_xor_sync(0xffffffffu, ll, off);
+            }
+            const double half = -0.5 * (double)__double2float_rn(a2);  // -(the zn2 the side data would hold) / 2
+            const __nv_bfloat16 hi = __double2bfloat16(half);
+            const __nv_bfloat16 lo = __double2bfloat16(half - (double)__bfloat162float(hi));
+            const double h2 = (double)__bfloat162float(hi), l2 = (double)__bfloat162float(lo);
+            if (tc == 15) {
+                b[2] = is_query ? __float2bfloat16_rn(1.f) : hi;
+                b[3] = is_query ? __float2bfloat16_rn(1.f) : lo;
+            }
+            if (row >= R) continue;
+            const uint2 v2 = make_uint2((uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16),
+                                        (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16));
+            if (is_query)
+                *reinterpret_cast<uint2 *>(zb + row * PJ_DMAX + tc * 4) = v2;
+            else
+                *reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(zb) + tcx_offset(row, tc * 4, PJ_DMAX, 64)) = v2;
+            if (tc == 0) {
+                const double L = sqrt(ll * m) * m, Hd = sqrt(hh * m) * m;
+                if (is_query) {
+                    // ||zq||^2 (the alpha terms); QH over the whole BF16 vector (the two
+                    // ones included: the FP32 accumulation term), QL over the
+                    // coefficients (the ones are exact)
+                    zn2[row] = __double2float_rn(a2);
+                    zen[row] = make_float2(__double2float_ru(sqrt((hh + 2.0) * m) * m), __double2float_ru(L));
+                } else {
+                    // the norm is inside the dot product: a_l = a_u = 0; U covers the
+                    // FP32 accumulation over the whole vector (hi, lo included), V
+                    // pairs with the query residual, which is zero on the split
+                    zn2[row] = 0.f;
+                    const double Hf = sqrt((hh + h2 * h2 + l2 * l2) * m) * m;
+                    zen[row] = make_float2(__double2float_ru((L + 0x1p-14 * Hf) * m), __double2float_ru((Hd + L) * m));
+                }
+            }
+        }
+    }
+}
+
+static int launch_proj_rows(const float *X, int64_t R, int n, const int32_t *pos, const uint32_t *rows, const float *P,
+                            int d, bool is_query, void *zb, float *zn2, float2 *zen, cudaStream_t s)
+{
+    if (R == 0) return OK;
+    const int smem = (n * PJ_DMAX + n * (PJ_ROWS + 1)) * 4;
+    SSB_CUDA(cudaFuncSetAttribute(proj_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SSB_REQUIRE(d == PJ_COEF, "projection width");
+    const int64_t tiles = (R + PJ_ROWS - 1) / PJ_ROWS;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)num_sms());
+    ProfScope ps(is_query ? "proj_queries" : "proj_rows", s, (double)R * n * 4 + (double)R * PJ_DMAX * 2);
+    proj_rows_kernel<<<grid, 256, smem, s>>>(X, R, n, pos, rows, P, d, is_query ? 1 : 0,
+                                             reinterpret_cast<__nv_bfloat16 *>(zb), zn2, zen);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// orthonormal DCT-II basis vector i of length n, element j (float64)
+static double dct_basis(int n, int i, int j)
+{
+    const double c = i == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n);
+    return c * std::cos(M_PI * (2.0 * j + 1.0) * i / (2.0 * n));
+}
+
+static double gamma_n(int n)
+{
+    const double u = 0x1p-24;
+    return n * u / (1.0 - n * u);
+}
+
+// K-proj operands of an index whose K-tc operands exist (build and load).
+// Skipped (ix.Zb stays null) when the rows' energy is not concentrated in d
+// basis vectors: the bound would not prune.
+int build_projection(Index &ix, cudaStream_t s)
+{
+    if (!ix.Xb || !ix.xn2) return OK;
+    if (const char *e = getenv("SSB_PROJ")) if (atoi(e) == 0) return OK;  // A/B: no projection operand
+    const int d = PJ_COEF;
+    const int n = ix.n;
+    if (n < 2 * PJ_DMAX || ix.N < 1) return OK;
+    double min_energy = 0.9;
+    if (const char *e = getenv("SSB_PROJ_MIN_ENERGY")) min_energy = atof(e);
+    std::vector<int32_t> hpos(n);
+    for (int j = 0; j < n; j++) hpos[j] = layout_pos(n, j);
+    DevBuf pos, C;
+    SSB_CUDA(pos.alloc(4 * (size_t)n, s));
+    SSB_CUDA(C.alloc(8 * (size_t)n * n, s));
+    SSB_CUDA(cudaMemcpyAsync(pos.p, hpos.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+    const int S = (int)std::min<int64_t>(ix.N, PJ_SAMPLE);
+    proj_cov_kernel<<<n, 256, 0, s>>>(ix.X, ix.N, n, pos.as<int32_t>(), S, C.as<double>());
+    SSB_CHECK_LAUNCH();
+    std::vector<double> hC((size_t)n * n);
+    SSB_CUDA(cudaMemcpyAsync(hC.data(), C.p, 8 * (size_t)n * n, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    // energy of every basis vector on the sample: phi_i^T C phi_i
+    std::vector<double> phi((size_t)n * n), energy(n), y(n);
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) phi[(size_t)i * n + j] = dct_basis(n, i, j);
+    double total = 0.0;
+    for (int i = 0; i < n; i++) {
+        const double *f = &phi[(size_t)i * n];
+        double e = 0.0;
+        for (int a = 0; a < n; a++) {
+            const double *ca = &hC[(size_t)a * n];
+            double t = 0.0;
+            for (int b = 0; b < n; b++) t += ca[b] * f[b];
+            e += f[a] * t;
+        }
+        energy[i] = e;
+        total += hC[(size_t)i * n + i];  // trace
+    }
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return energy[a] > energy[b]; });
+    std::vector<int> sel(order.begin(), order.begin() + d);
+    std::sort(sel.begin(), sel.end());
+    double kept = 0.0;
+    for (int i : sel) kept += energy[i];
+    const double frac = total > 0.0 ? kept / total : 0.0;
+    if (getenv("SSB_BUILD_TRACE"))
+        fprintf(stderr, "[ssb build] projection d=%d: %.4f of the sample's energy%s\n", d, frac,
+                frac < min_energy ? " -> off" : "");
+    if (!(frac >= min_energy)) return OK;
+    // P (float32) and its certified constants: Lambda >= lambda_max(P P^T)
+    // (Gershgorin on the float64 Gram matrix of the float32 rows, + rounding
+    // margin), ||P||_F rounded up
+    std::vector<float> hP((size_t)d * n);
+    for (int r = 0; r < d; r++)
+        for (int j = 0; j < n; j++) hP[(size_t)r * n + j] = (float)phi[(size_t)sel[r] * n + j];
+    double lam = 0.0, f2 = 0.0;
+    for (int r = 0; r < d; r++) {
+        double row = 0.0;
+        for (int c = 0; c < d; c++) {
+            double g = 0.0;
+            for (int j = 0; j < n; j++) g += (double)hP[(size_t)r * n + j] * (double)hP[(size_t)c * n + j];
+            row += std::fabs(g);
+            if (r == c) f2 += g;
+        }
+        lam = std::max(lam, row);
+    }
+    lam = lam * (1.0 + 1e-12) + 1e-12;
+    const double F = std::sqrt(f2 * (1.0 + 1e-12)) * (1.0 + 1e-12);
+    // largest row norm (||x||^2 per row is exact-rounded; relative margin)
+    DevBuf mx;
+    SSB_CUDA(mx.alloc(4, s));
+    SSB_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+    max_bits_kernel<<<num_sms() * 2, 256, 0, s>>>(ix.xn2, ix.N, mx.as<unsigned int>());
+    SSB_CHECK_LAUNCH();
+    unsigned int mbits = 0;
+    SSB_CUDA(cudaMemcpyAsync(&mbits, mx.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    float xmax2f;
+    std::memcpy(&xmax2f, &mbits, 4);
+    const double xmax2 = (double)xmax2f * (1.0 + 1e-6);
+
+    SSB_CUDA(cudaMalloc(&ix.P, 4 * (size_t)d * n));
+    SSB_CUDA(cudaMemcpyAsync(ix.P, hP.data(), 4 * (size_t)d * n, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMalloc(&ix.Zb, (size_t)tcx_bytes(ix.N, PJ_DMAX, 64)));
+    SSB_CUDA(cudaMemsetAsync(static_cast<char *>(ix.Zb) + tcx_bytes(ix.N, PJ_DMAX, 64) - tcx_tile_bytes(PJ_DMAX, 64), 0,
+                             (size_t)tcx_tile_bytes(PJ_DMAX, 64), s));  // padding rows of the last tile
+    SSB_CUDA(cudaMalloc(&ix.zside, (size_t)tc_side_bytes(ix.N)));
+    DevBuf zn2, zen;
+    SSB_CUDA(zn2.alloc(4 * (size_t)ix.N, s));
+    SSB_CUDA(zen.alloc(8 * (size_t)ix.N, s));
+    // rows in the K-tc order: slot r holds leaf position tcperm[r]
+    int rc = launch_proj_rows(ix.X, ix.N, n, pos.as<int32_t>(), ix.tcperm, ix.P, d, false, ix.Zb, zn2.as<float>(),
+                              zen.as<float2>(), s);
+    if (rc) return rc;
+    rc = launch_tc_side(zn2.as<float>(), zen.as<float2>(), ix.N, ix.zside, s);
+    if (rc) return rc;
+    // the filter's projected mode bounds every row's error term by these maxima
+    SSB_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+    DevBuf muv;
+    SSB_CUDA(muv.alloc(8, s));
+    SSB_CUDA(cudaMemsetAsync(muv.p, 0, 8, s));
+    max_uv_kernel<<<num_sms() * 2, 256, 0, s>>>(zen.as<float2>(), ix.N, muv.as<unsigned int>());
+    SSB_CHECK_LAUNCH();
+    float huv[2];
+    SSB_CUDA(cudaMemcpyAsync(huv, muv.p, 8, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    const double g = 1.0 + 4e-6;  // tc.cu's g: the row constants are (2gU, 2gV)
+    ix.p_u2 = (float)std::nextafter((float)(2.0 * g * huv[0] * (1.0 + 1e-6)), INFINITY);
+    ix.p_v2 = (float)std::nextafter((float)(2.0 * g * huv[1] * (1.0 + 1e-6)), INFINITY);
+    ix.pd = d;
+    ix.p_lam = lam;
+    ix.p_gf = gamma_n(n) * F;
+    ix.p_xmax2 = xmax2;
+    ix.p_energy = frac;
+    return OK;
+}
+
+// ---------------------------------------------------------------------------
+// query side
+
+// per query: T_q (float bits, rounded up) from its bound (the k-th key in
+// thr); a query without one is marked overflowed (-inf, nothing emitted).
+__global__ void proj_bound_kernel(const float *__restrict__ Q, const int32_t *__restrict__ qlist, int nq, int n,
+                                  const uint64_t *__restrict__ thr, double lam, double gf, double xmax2,
+                                  unsigned int *__restrict__ gb, unsigned int *__restrict__ flag)
+{
+    const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (i >= nq) return;
+    const int lane = threadIdx.x & 31;
+    const int q = qlist[i];
+    double q2 = 0.0;
+    for (int e = lane; e < n; e += 32) {
+        const double v = (double)Q[(int64_t)q * n + e];
+        q2 += v * v;
+    }
+    for (int off = 16; off; off >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, off);
+    if (lane) return;
+    const uint64_t key = thr[q];
+    if (key == KEY_EMPTY) {  // no bound: the full filter answers it
+        gb[i] = 0xff800000u;  // -inf: nothing is emitted
+        flag[i] = 1u;
+        return;
+    }
+    const double b = (double)key_d2(key);
+    const double m = 1.0 + 1e-6;
+    const double eq = gf * sqrt(q2) * m, ex = gf * sqrt(xmax2) * m;
+    const double r = sqrt(lam * b * (1.0 + 1e-5)) * m + eq + ex;
+    // + the float32 evaluation slack and the (hi, lo) split's residual
+    // (<= 2^-18 ||zx||^2 / 2 per row, twice in the distance)
+    const double T = r * r * (1.0 + 1e-5) + 1e-5 * lam * (q2 + xmax2) + 0x1p-16 * lam * xmax2;
+    gb[i] = __float_as_uint(__double2float_ru(T));
+}
+
+// exact rescoring of the projected filter's candidates (query, K-tc row),
+// one 8-lane group per candidate (scan.cu arithmetic, bit-identical
+// distances); candidates of queries the full filter answers are skipped, and
+// `only` (per block query, nullable) restricts to the flagged queries
+template <int NT>
+__global__ void rescore_proj_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
+                                    const uint32_t *__restrict__ tcperm, const float *__restrict__ Qp,
+                                    const int32_t *__restrict__ qmap, const uint2 *__restrict__ cand, int64_t nc,
+                                    const int32_t *__restrict__ hard, const int32_t *__restrict__ only, ScanOut out)
+{
+    const int lane = threadIdx.x & 31, j = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    for (int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; gp < nc; gp += stride) {
+        const uint2 c = cand[gp];
+        if (hard[c.x]) continue;
+        const int q = qmap[c.x];
+        if (only && !only[q]) continue;
+        const uint32_t pos = tcperm ? tcperm[c.y] : c.y;
+        float qv[NT / 8];
+        lay_load_q<NT>(Qp + (int64_t)q * NT, qv, j);
+        const float d2 = lay_ed2<NT>(X + (int64_t)pos * NT, qv, j, gmask);
+        if (j == 0) {
+            const uint64_t key = make_key(d2, row_id ? row_id[pos] : pos);
+            const uint64_t bound = out.thr ? out.thr[q] : KEY_EMPTY;
+            if (key <= bound) {
+                const uint32_t slot = atomicAdd(&out.cnt[q], 1u);
+                if (slot < (uint32_t)out.cap) out.cand[(size_t)q * out.cap + slot] = key;
+            }
+        }
+    }
+}
+
+__global__ void proj_cser_kernel(const unsigned int *__restrict__ cnt, const int32_t *__restrict__ hard,
+                                 const int32_t *__restrict__ qlist, int nq, uint32_t *__restrict__ cser)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nq && !hard[i]) cser[qlist[i]] = cnt[i];
+}
+
+static int launch_rescore_proj(const Index &ix, ProjWork &pw, const float *Qp, const int32_t *only, ScanOut so,
+                               cudaStream_t s)
+{
+    if (pw.nq == 0 || pw.nc == 0) return OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((pw.nc * 8 + 255) / 256, (int64_t)num_sms() * 16);
+    ProfScope ps("proj_rescore", s, (double)pw.nc * ix.n * 4);
+    const uint2 *cand = pw.cand.as<uint2>();
+    const int32_t *qm = pw.qidx.as<int32_t>(), *hard = pw.hard.as<int32_t>();
+    switch (ix.n) {
+    case 128: rescore_proj_kernel<128><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, pw.nc, hard, only, so); break;
+    case 256: rescore_proj_kernel<256><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, pw.nc, hard, only, so); break;
+    default:
+        set_error(ERR_USAGE, "series length " + std::to_string(ix.n) + " has no compiled projected rescore kernel");
+        return ERR_USAGE;
+    }
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+bool proj_available(const Index &ix) { return ix.Zb != nullptr && (ix.n == 128 || ix.n == 256); }
+
+// K-proj for the tensor-route queries `qtc` of a block of B queries (their
+// bounds in thr, their lane-transposed copies in qlay): one pass over every
+// row's projection under T(thr), each query's candidates appended to its own
+// segment and rescored exactly into `so`.  Queries whose segment overflowed,
+// or that have no bound, are returned in *hard for the full filter.
+int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc, uint64_t *thr, const float *qlay,
+               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard, ProjWork &pw, cudaStream_t s)
+{
+    hard->clear();
+    const int nq = (int)qtc.size();
+    pw.nq = nq;
+    if (nq == 0) return OK;
+    const int d = ix.pd, n = ix.n;
+    const int nq_pad = (nq + 127) / 128 * 128;
+    // per query: give up past seg_cap candidates (rescoring 32K rows costs about
+    // what a query's share of the full filter does at 25M rows); the buffer
+    // holds ~24K per query on average
+    pw.seg_cap = 32768;
+    if (const char *e = getenv("SSB_PROJ_SEG")) pw.seg_cap = std::max(1, atoi(e));  // test hook
+    pw.cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)nq * 24576, (int64_t)1 << 27));
+    if (const char *e = getenv("SSB_PROJ_CAP")) pw.cap = std::max<int64_t>(1, atoll(e));  // test hook
+    DevBuf qb, qn2, qen, gb;
+    SSB_CUDA(pw.qidx.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(pw.cnt.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(pw.flag.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(pw.hard.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(pw.cand.alloc(8 * (size_t)pw.cap, s));
+    SSB_CUDA(pw.cn.alloc(8, s));
+    SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * PJ_DMAX, s));
+    SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
+    SSB_CUDA(qen.alloc(8 * (size_t)nq_pad, s));
+    SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
+    SSB_CUDA(cudaMemcpyAsync(pw.qidx.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemsetAsync(pw.cnt.p, 0, 4 * (size_t)nq, s));
+    SSB_CUDA(cudaMemsetAsync(pw.flag.p, 0, 4 * (size_t)nq, s));
+    SSB_CUDA(cudaMemsetAsync(pw.cn.p, 0, 8, s));
+    SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * PJ_DMAX, s));
+    SSB_CUDA(cudaMemsetAsync(qn2.p, 0, 4 * (size_t)nq_pad, s));
+    SSB_CUDA(cudaMemsetAsync(qen.p, 0, 8 * (size_t)nq_pad, s));
+    SSB_CUDA(cudaMemsetAsync(gb.p, 0xff, 4 * (size_t)tc_bound_slots(nq), s));  // NaN bits: never emits
+    const int32_t *qidx = pw.qidx.as<int32_t>();
+    int rc = launch_proj_rows(Q, nq, n, nullptr, reinterpret_cast<const uint32_t *>(qidx), ix.P, d, true, qb.p,
+                              qn2.as<float>(), qen.as<float2>(), s);
+    if (rc) return rc;
+    proj_bound_kernel<<<(nq + 7) / 8, 256, 0, s>>>(Q, qidx, nq, n, thr, ix.p_lam, ix.p_gf, ix.p_xmax2,
+                                                   gb.as<unsigned int>(), pw.flag.as<unsigned int>());
+    SSB_CHECK_LAUNCH();
+    rc = launch_tc_filter(qb.p, qn2.as<float>(), qen.as<float2>(), nq, ix.Zb, 64, ix.zside, ix.N, PJ_DMAX, k,
+                          gb.as<unsigned int>(), pw.cand.as<uint2>(), nullptr, pw.cn.as<unsigned long long>(), pw.cap,
+                          nullptr, s, pw.flag.as<unsigned int>(), pw.cnt.as<unsigned int>(), pw.seg_cap, 0, nullptr,
+                          ix.p_u2, ix.p_v2);
+    if (rc) return rc;
+    std::vector<uint32_t> hc(nq), hf(nq);
+    unsigned long long hn = 0;
+    SSB_CUDA(cudaMemcpyAsync(hc.data(), pw.cnt.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(hf.data(), pw.flag.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(&hn, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    pw.nc = std::min<int64_t>((int64_t)hn, pw.cap);
+    std::vector<int32_t> hh(nq);
+    int64_t total = 0;
+    for (int i = 0; i < nq; i++) {
+        hh[i] = (hf[i] || hc[i] > (uint32_t)pw.seg_cap) ? 1 : 0;
+        if (hh[i])
+            hard->push_back(qtc[i]);
+        else
+            total += hc[i];
+    }
+    SSB_CUDA(cudaMemcpyAsync(pw.hard.p, hh.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    if (getenv("SSB_TC_TRACE")) {
+        std::vector<uint64_t> bb(B);
+        SSB_CUDA(cudaMemcpyAsync(bb.data(), thr, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        std::vector<float> v;
+        for (int q : qtc) v.push_back(bb[q] == KEY_EMPTY ? INFINITY : key_d2(bb[q]));
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "[ssb] proj batch nq=%d k=%d d=%d: bounds d2 p10/p50/p90 %.3g/%.3g/%.3g; %llu emitted "
+                        "(cap %lld), %lld for the %zu settled queries, %zu hard\n",
+                nq, k, d, v[v.size() / 10], v[v.size() / 2], v[v.size() * 9 / 10], hn, (long long)pw.cap,
+                (long long)total, qtc.size() - hard->size(), hard->size());
+    }
+    rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s);
+    if (rc) return rc;
+    if (cser) {
+        proj_cser_kernel<<<(nq + 255) / 256, 256, 0, s>>>(pw.cnt.as<unsigned int>(), pw.hard.as<int32_t>(), qidx, nq,
+                                                          cser);
+        SSB_CHECK_LAUNCH();
+    }
+    SSB_CUDA(cudaStreamSynchronize(s));  // hh dies here
+    return OK;
+}
+
+// the select overflowed for some queries: their candidates again under the
+// tighter bound (flags: per block query)
+int proj_rescore_flagged(const Index &ix, ProjWork &pw, const float *qlay, const int32_t *flags, ScanOut so,
+                         cudaStream_t s)
+{
+    return launch_rescore_proj(ix, pw, qlay, flags, so, s);
+}
+
+}  // namespace ssb

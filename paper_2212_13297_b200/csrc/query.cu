@@ -163,6 +163,19 @@ static bool tc_all_for(const Index &ixc, const QueryCfg &qc, int k, int B)
     }
     Index &ix = const_cast<Index &>(ixc);  // the routing observation is the only mutable part
     std::lock_guard<std::mutex> lock(ix.graph_mu);
+    if (B >= 32 && proj_available(ix)) {
+        // the index stages + K-proj (+ the full filter for the queries it cannot
+        // settle) against the lean full filter, per query
+        const double hard = ix.proj_hard_ema < 0.0 ? 0.5 : ix.proj_hard_ema;
+        const double via_proj = IX_NS_STAGES_Q + IX_NS_STAGES_LEAF * ixc.L +
+                                tc_ns * IX_NS_PROJ_FACTOR * ixc.pd / ixc.n + hard * tc_ns;
+        if (via_proj < tc_ns) {
+            if (getenv("SSB_ROUTE_TRACE"))
+                fprintf(stderr, "[ssb] route B=%d k=%d lean %.1f us vs stages + K-proj %.1f us/query (hard %.2f) -> index stages\n",
+                        B, k, tc_ns / 1000, via_proj / 1000, hard);
+            return false;
+        }
+    }
     const double ix_ns = idx_ns(ix, ix.kept_frac_ema * (double)ix.N);
     bool lean = true;
     if (ix.kept_frac_ema < 0.0 || ix_ns < 2.0 * tc_ns) {
@@ -208,7 +221,9 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     // auto: when even a query that keeps every leaf is cheaper on the index
     // route than a filter pass shared by the whole block (small blocks), no
     // query takes the filter
-    const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW * n / 256.0;
+    // one filter pass per group of 256 queries: K-proj's when the index has it
+    const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW * n / 256.0 *
+                               (proj_available(ix) ? IX_NS_PROJ_FACTOR * ix.pd / n : 1.0);
     if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= tc_group_ns) mode = 1;
     IxWork w;
     int rc = ix_front(ix, qc, Q, B, k, mode, want, w, s);
@@ -287,6 +302,27 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     rc = ix_back(ix, w, B, mode != 1 ? w.use_tc.as<int32_t>() : nullptr, so, cser.as<uint32_t>(), s);
     if (rc) return rc;
 
+    // ---- K-proj first (proj.cu): the projected filter under the approximate
+    // phase's bounds answers the tensor-route queries it can; the rest (segment
+    // overflow: a weak bound; no bound) go on to the full filter -------------------
+    ProjWork pw;
+    std::vector<char> projq;  // per block query: answered by K-proj
+    if (!qtc.empty() && proj_available(ix) && !getenv("SSB_NO_PROJ")) {
+        std::vector<int32_t> hard;
+        rc = proj_route(ix, Q, qtc, thr, w.qlay.as<float>(), B, k, so, want ? cser.as<uint32_t>() : nullptr, &hard, pw, s);
+        if (rc) return rc;
+        projq.assign(B, 0);
+        for (int q : qtc) projq[q] = 1;
+        for (int q : hard) projq[q] = 0;
+        {
+            Index &ixm = const_cast<Index &>(ix);  // the routing observation
+            std::lock_guard<std::mutex> lock(ixm.graph_mu);
+            const double f = (double)hard.size() / (double)qtc.size();
+            ixm.proj_hard_ema = ixm.proj_hard_ema < 0.0 ? f : 0.5 * (ixm.proj_hard_ema + f);
+        }
+        qtc.swap(hard);
+    }
+
     // ---- tensor-core route: K-tc over all N rows, exact rescoring -------------
     DevBuf d_qtc, tc_cand, tc_lb, tc_n, gb;
     int64_t tc_nc = 0;
@@ -325,7 +361,15 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         }
         if ((int64_t)hn > tc_cap) {
             // still too many candidates: these queries take the index route
-            SSB_CUDA(cudaMemsetAsync(w.use_tc.p, 0, 4 * (size_t)B, s));
+            // (the queries K-proj answered keep their tensor-route mark)
+            {
+                std::vector<int32_t> ut(B);
+                SSB_CUDA(cudaMemcpyAsync(ut.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+                SSB_CUDA(cudaStreamSynchronize(s));
+                for (int q : qtc) ut[q] = 0;
+                SSB_CUDA(cudaMemcpyAsync(w.use_tc.p, ut.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+                SSB_CUDA(cudaStreamSynchronize(s));  // ut dies here
+            }
             int64_t items = 0;
             {
                 std::vector<uint32_t> qi(B);
@@ -398,6 +442,11 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CHECK_LAUNCH();
         rc = ix_back(ix, w, B, skip.as<int32_t>(), so, nullptr, s);
         if (rc) return rc;
+        // K-proj queries: their segments again under the tighter bound
+        if (pw.nq) {
+            rc = proj_rescore_flagged(ix, pw, w.qlay.as<float>(), flags.as<int32_t>(), so, s);
+            if (rc) return rc;
+        }
         // tensor-core queries: rescore their candidates again under the tighter bound
         if (tc_nc) {
             DevBuf sub, nsub;
@@ -459,7 +508,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             o[5] = t ? (uint32_t)std::min<int64_t>(ix.N, 0xffffffffll)  // rows whose bytes the filter read
                      : (uint32_t)std::min<unsigned long long>(kr[q] + sw[q], 0xffffffffull);  // words tested
             o[6] = ab[q];                                            // rows abandoned early
-            o[7] = t ? 1u : 0u;                                      // route: 1 tensor-core filter
+            o[7] = t ? (!projq.empty() && projq[q] ? 2u : 1u) : 0u;  // route: 1 tensor-core filter, 2 K-proj
         }
     }
     return OK;

@@ -64,6 +64,19 @@ struct Index {
     float2 *xen = nullptr;   // per row (U, V): BF16 rounding-error norms (to_bf16_norms_kernel)
     uint32_t *tcperm = nullptr;  // K-tc row order -> leaf-order position (null: identity)
     float4 *tcside = nullptr; // per 128-row tile: the K-tc bound constants of its rows + half-tile extremes
+    // projected lower-bound filter (K-proj, proj.cu): the d DCT-II coefficients
+    // of every row (the d basis vectors of largest energy on a sample), BF16
+    // tile-major in the K-tc row order, with their side records; null when the
+    // rows' energy is not concentrated enough for the bound to prune
+    int32_t pd = 0;
+    float *P = nullptr;          // d x n basis rows (float32, device)
+    void *Zb = nullptr;
+    float4 *zside = nullptr;
+    double p_lam = 1.0;          // >= lambda_max(P P^T)
+    double p_gf = 0.0;           // gamma_n ||P||_F: projection rounding error per unit ||x||
+    double p_xmax2 = 0.0;        // >= max ||x||^2 over the rows
+    double p_energy = 0.0;       // fraction of the sample's energy the d coefficients hold
+    float p_u2 = 0.f, p_v2 = 0.f; // index-wide maxima of the rows' error constants 2gU, 2gV (rounded up)
     double build_ms = 0.0;
     int32_t levels = 0;
     // small query blocks on the index route replay a captured CUDA graph
@@ -76,6 +89,9 @@ struct Index {
     double kept_frac_ema = -1.0;
     double surv_per_kept_ema = 0.0;  // LB_SAX survivors (exactly scanned) per kept row
     int lean_since_probe = 0;
+    // K-proj: fraction of the queries sent to it whose segment overflowed (the
+    // full filter answered them), over recent blocks (< 0: none observed)
+    double proj_hard_ema = -1.0;
     ~Index();
 };
 
@@ -99,6 +115,13 @@ constexpr double IX_NS_IX_ROW = 0.03;
 // survivor at n = 256 (the rows read before abandonment; scaled by n / 256)
 constexpr double IX_NS_WORD = 0.01;
 constexpr double IX_NS_SURVIVOR = 0.5;
+// K-proj (proj.cu): a pass over the d-coefficient operand costs IX_NS_PROJ_FACTOR
+// x d/n of the full filter's pass (the epilogue's per-pair work does not shrink
+// with d); the index stages that supply its bounds cost IX_NS_STAGES_Q per query
+// plus IX_NS_STAGES_LEAF per (query, leaf) (LB_EAPCA)
+constexpr double IX_NS_PROJ_FACTOR = 1.5;
+constexpr double IX_NS_STAGES_Q = 400.0;
+constexpr double IX_NS_STAGES_LEAF = 0.09;
 
 // Everything of one query block on the index path, stream-ordered; the
 // per-stage outputs the caller needs afterwards (bounds, routing, counters)
@@ -121,7 +144,9 @@ int launch_ix_lbe(const Index &ix, const double *cs, const double *c2, int B, do
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb, int xb_cw,
                      const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
-                     cudaStream_t s);
+                     cudaStream_t s, unsigned int *seg_flag = nullptr, unsigned int *seg_cnt = nullptr, int seg_cap = 0,
+                     int64_t tile_limit = 0, const char *prof_name = nullptr, float seg_u = 0.f,
+                     float seg_v = 0.f);
 int64_t tc_bound_slots(int nq);
 int64_t tc_side_bytes(int64_t N);
 int launch_tc_side(const float *xn2, const float2 *en, int64_t N, float4 *side, cudaStream_t s);
@@ -129,6 +154,21 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
 int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,
                          uint32_t *qmax, cudaStream_t s);
+// K-proj (proj.cu)
+struct ProjWork {
+    DevBuf qidx, cnt, flag, cand, cn, hard;
+    int nq = 0, seg_cap = 0;
+    int64_t cap = 0, nc = 0;
+};
+int build_projection(Index &ix, cudaStream_t s);
+bool proj_available(const Index &ix);
+int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc, uint64_t *thr, const float *qlay,
+               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard, ProjWork &pw, cudaStream_t s);
+int proj_rescore_flagged(const Index &ix, ProjWork &pw, const float *qlay, const int32_t *flags, ScanOut so,
+                         cudaStream_t s);
+
+int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr, uint64_t *out_keys,
+                  int32_t *flags, cudaStream_t s);
 int launch_rescore(const float *X, int n, const uint32_t *row_id, const uint32_t *tcperm, const float *Qp,
                    const int32_t *qmap,
                    const uint2 *cand, const float *cand_lb, const unsigned int *fbound, int64_t nc, ScanOut out,

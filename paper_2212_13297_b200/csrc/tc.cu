@@ -93,6 +93,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 
+// barrier waits / arrivals on precomputed 32-bit shared addresses; the wait
+// suspends the warp in hardware (time hint) instead of spinning on try_wait,
+// so waiting warps leave the issue slots to the working ones
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, unsigned phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(phase), "r"(0x100000)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t *bar)
 {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -119,6 +140,14 @@ __device__ __forceinline__ float sel16(const uint32_t *v, int i)
 #pragma unroll
     for (int j = 0; j < 2; j++) c[j] = (i & 4) ? b[2 * j + 1] : b[2 * j];
     return __uint_as_float((i & 8) ? c[1] : c[0]);
+}
+
+// three-input float max (one FMNMX3 on sm_100)
+__device__ __forceinline__ float fmax3f(float a, float b, float c)
+{
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -182,6 +211,15 @@ struct TcParams {
     unsigned int *prog;        // [ctas_per_qb][groups][CS] tiles issued
     int groups;
     int window;
+    // projected mode (SEG, K-proj): the bounds are fixed (no tightening);
+    // candidates go through the usual stage, and every query's emissions are
+    // counted (per thread, one atomic per thread at the end); a thread past
+    // seg_cap emissions, or an entry dropped at the buffer's end, marks its
+    // query (the full filter answers it instead)
+    unsigned int *seg_flag;    // [nq] 1: the query gave up / lost a candidate
+    unsigned int *seg_cnt;     // [nq] rows emitted
+    int seg_cap;               // per thread
+    float seg_u, seg_v;        // index-wide maxima of the rows' error constants (2gU, 2gV)
 };
 
 // per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
@@ -197,7 +235,8 @@ static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
 
 // KTOP > 0: keep the k smallest upper bounds per thread (k <= KTOP);
 // KTOP == 0: filter against the given bounds only; KTOP < 0: debug dump of S.
-template <int KTOP, int EPW>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
+// SEG (with KTOP == 0): projected mode, candidates into per-query segments.
+template <int KTOP, int EPW, bool SEG = false>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
 __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     tc_filter_kernel(const __grid_constant__ TcParams p)
 {
@@ -274,6 +313,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     if (CS > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast lands
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t a_rfull = (uint32_t)__cvta_generic_to_shared(r_full), a_rempty = (uint32_t)__cvta_generic_to_shared(r_empty);
+    const uint32_t a_tfull = (uint32_t)__cvta_generic_to_shared(t_full), a_tempty = (uint32_t)__cvta_generic_to_shared(t_empty);
+    const uint32_t a_bfull = (uint32_t)__cvta_generic_to_shared(b_full), a_bempty = (uint32_t)__cvta_generic_to_shared(b_empty);
 
     // Producer and MMA roles run warp-wide (every value stays warp-uniform, in
     // uniform registers); one elected lane issues each TMA / tcgen05 instruction.
@@ -307,8 +349,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
                 // side data of this tile (row constants + half-tile extremes): one copy
                 const int rs = t % TC_RS;
-                if (t >= TC_RS) mbar_wait(&r_empty[rs], (unsigned)(((t / TC_RS) - 1) & 1));
-                {
+                if (!SEG && t >= TC_RS) mbar_wait_a(a_rempty + 8u * rs, (unsigned)(((t / TC_RS) - 1) & 1));
+                if (!SEG) {
                     const uint32_t dst = slot0 + (uint32_t)(rs * sizeof(TileSlot));
                     const uint32_t bar = rfull0 + (uint32_t)rs * 8;
                     asm volatile(
@@ -319,7 +361,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                         "r"(bar), "l"(p.side + tile * TC_SIDE), "n"((int)sizeof(TileSlot))
                         : "memory");
                 }
-                if (t >= NS) mbar_wait(&b_empty[slot], phase ^ 1u);
+                if (t >= NS) mbar_wait_a(a_bempty + 8u * slot, phase ^ 1u);
                 const uint32_t bar = full0 + (uint32_t)slot * 8;
                 if (p.skip_epi == 4 && t >= NS) {  // diagnostics: MMA-only pipeline (stale B tiles)
                     asm volatile("{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
@@ -382,8 +424,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             uint32_t phase = 0;
             for (int t = 0; t < niter; t++) {
                 const int s = t % TC_NACC;
-                if (t >= TC_NACC) mbar_wait(&t_empty[s], (unsigned)(((t / TC_NACC) - 1) & 1));
-                mbar_wait(&b_full[slot], phase);
+                if (t >= TC_NACC) mbar_wait_a(a_tempty + 8u * s, (unsigned)(((t / TC_NACC) - 1) & 1));
+                mbar_wait_a(a_bfull + 8u * slot, phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
                 for (int kb = 0; kb < KB && p.skip_epi != 3; kb++) {  // 3: diagnostics, loads only
@@ -481,6 +523,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         const uint32_t kk = (uint32_t)p.k;
         float bmax = __int_as_float(0x7f800000);  // last bucket bound read by this thread
         bool touched = false;
+        unsigned seg_local = 0;  // SEG: this thread's emissions
         uint2 *stage = s_stage + ew * STG;
         float *stage_lb = s_stage_lb + ew * STG;
         unsigned *stage_fill = s_fill + ew;  // reserved slots of this warp's stage (may pass STG)
@@ -494,7 +537,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             for (unsigned i = lane; i < n_st; i += 32)
                 if ((int64_t)(base_slot + i) < p.cand_cap) {
                     p.cand[base_slot + i] = stage[i];
-                    p.cand_lb[base_slot + i] = stage_lb[i];
+                    if (p.cand_lb) p.cand_lb[base_slot + i] = stage_lb[i];
+                } else if (SEG) {
+                    p.seg_flag[stage[i].x] = 1u;  // dropped: the query is answered elsewhere
                 }
             __syncwarp();
             if (lane == 0) *stage_fill = 0;
@@ -502,6 +547,86 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         };
         const float inv2f = 0.5f / f, inv2g = 0.5f / g;
         const bool diag_skip = p.skip_epi == 1 || p.skip_epi == 3 || p.skip_epi == 4;
+        if constexpr (SEG) {
+            // Projected mode: the bound is fixed and the rows' norms are inside
+            // the dot product, so with the index-wide maxima of the error
+            // constants (u, v) the emission test lb <= bound is one per-thread
+            // threshold on t -- no side data, no per-row arithmetic:
+            //   lb >= f(1-e) qn2 - QH u_max - QL v_max - 2 f t  (a_l = 0)
+            float thr = qvalid ? ((alpha_l - QH * p.seg_u - QL * p.seg_v) - gnext) * inv2f : __int_as_float(0x7f800000);
+            thr -= 1e-5f * (fabsf(thr) + 1.f);  // float32 rounding may only send more rows to rescoring
+            if (!(thr == thr)) thr = __int_as_float(0x7f800000);  // no bound (NaN / -inf): nothing emitted
+            for (int t = 0; t < niter; t++) {
+                const int s = t % TC_NACC;
+                const int64_t row0 = tile_of(t) * TC_BN + h * COLS;
+                mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t taddr =
+                    tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
+                uint32_t v[COLS];
+#pragma unroll
+                for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
+                tmem_wait_ld();
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                mbar_arrive_a(a_tempty + 8u * s);
+                if (diag_skip) continue;
+                float mg[COLS / 16];
+#pragma unroll
+                for (int g = 0; g < COLS / 16; g++) {
+                    const float *vf = reinterpret_cast<const float *>(v + 16 * g);
+                    float a = fmax3f(vf[0], vf[1], vf[2]), b = fmax3f(vf[3], vf[4], vf[5]);
+                    float c = fmax3f(vf[6], vf[7], vf[8]), d = fmax3f(vf[9], vf[10], vf[11]);
+                    float e2 = fmax3f(vf[12], vf[13], vf[14]);
+                    a = fmax3f(a, b, c);
+                    d = fmax3f(d, e2, vf[15]);
+                    mg[g] = fmaxf(a, d);
+                }
+                float mx = mg[0];
+#pragma unroll
+                for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
+                if (!__any_sync(0xffffffffu, mx >= thr)) continue;
+                const int64_t left = p.N - row0;
+                const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
+#pragma unroll
+                for (int c0 = 0; c0 < COLS; c0 += 16) {
+                    uint32_t emit = 0;
+                    if (mg[c0 / 16] >= thr) {
+#pragma unroll
+                        for (int i = 0; i < 16; i++) emit |= (__uint_as_float(v[c0 + i]) >= thr ? 1u : 0u) << i;
+                        emit &= (uint32_t)(valid >> c0) & 0xffffu;
+                    }
+                    if (emit) {
+                        const unsigned cnt = __popc(emit);
+                        seg_local += cnt;
+                        if (seg_local > (unsigned)p.seg_cap) {  // give up: the full filter answers it
+                            p.seg_flag[ql] = 1u;
+                            thr = __int_as_float(0x7f800000);
+                        }
+                        unsigned slot = atomicAdd(stage_fill, cnt);
+                        unsigned long long gslot = 0;
+                        if (slot + cnt > (unsigned)STG)
+                            gslot = atomicAdd(p.cand_n, (unsigned long long)(slot + cnt - max(slot, (unsigned)STG)));
+                        while (emit) {
+                            const int i = __ffs(emit) - 1;
+                            emit &= emit - 1;
+                            const uint2 cv = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
+                            if (slot < (unsigned)STG) {
+                                stage[slot] = cv;
+                            } else {
+                                if ((int64_t)gslot < p.cand_cap)
+                                    p.cand[gslot] = cv;
+                                else
+                                    p.seg_flag[ql] = 1u;
+                                gslot++;
+                            }
+                            slot++;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
+            }
+        } else
         for (int t = 0; t < niter; t++) {
             const int s = t % TC_NACC;
             const int rs = t % TC_RS;
@@ -511,7 +636,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // list (a row counted twice would make the k-th bound invalid)
             const bool revisit = t >= nwarm && t < 2 * nwarm;
             const TileSlot &ts = slots[rs];
-            mbar_wait(&r_full[rs], (unsigned)((t / TC_RS) & 1));
+            mbar_wait_a(a_rfull + 8u * rs, (unsigned)((t / TC_RS) & 1));
             // the shared bound of this query (other CTAs tighten it): read every
             // 8th tile, used from the 8th tile after, so the L2 round trip never
             // sits on a tile's critical path
@@ -523,13 +648,13 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
             const float4 tcl = ts.tilec[2 * hh], tcu = ts.tilec[2 * hh + 1];
-            mbar_wait(&t_full[s], (unsigned)((t / TC_NACC) & 1));
+            mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive(&t_empty[s]);
+                mbar_arrive_a(a_tempty + 8u * s);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&r_empty[rs]);
+                if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
@@ -539,13 +664,13 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             tmem_wait_ld();
             // the accumulator is in registers: release it to the MMA warp right away
             asm volatile("tcgen05.fence::before_thread_sync;");
-            mbar_arrive(&t_empty[s]);
+            mbar_arrive_a(a_tempty + 8u * s);
             if constexpr (KTOP < 0) {  // debug: dump S
 #pragma unroll
                 for (int i = 0; i < 64; i++)
                     if (qvalid && row0 + i < p.N) p.dump[(int64_t)ql * p.N + row0 + i] = __uint_as_float(v[i]);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&r_empty[rs]);
+                if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
             }
             // tile-level necessary conditions on the dot product s:
@@ -563,13 +688,16 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     thr_s = emit_ok ? fminf(s_lo, s_need) : s_need;
                 }
             }
-            float mg[COLS / 16];  // per 16-column group maxima
+            float mg[COLS / 16];  // per 16-column group maxima (three-input max: 8 FMNMX3 per group)
 #pragma unroll
             for (int g = 0; g < COLS / 16; g++) {
-                float a = fmaxf(__uint_as_float(v[16 * g]), __uint_as_float(v[16 * g + 1]));
-#pragma unroll
-                for (int i = 2; i < 16; i++) a = fmaxf(a, __uint_as_float(v[16 * g + i]));
-                mg[g] = a;
+                const float *vf = reinterpret_cast<const float *>(v + 16 * g);
+                float a = fmax3f(vf[0], vf[1], vf[2]), b = fmax3f(vf[3], vf[4], vf[5]);
+                float c = fmax3f(vf[6], vf[7], vf[8]), d = fmax3f(vf[9], vf[10], vf[11]);
+                float e2 = fmax3f(vf[12], vf[13], vf[14]);
+                a = fmax3f(a, b, c);
+                d = fmax3f(d, e2, vf[15]);
+                mg[g] = fmaxf(a, d);
             }
             float mx = mg[0];
 #pragma unroll
@@ -644,9 +772,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                                 stage[slot] = cv;
                             } else if ((int64_t)gslot < p.cand_cap) {
                                 p.cand[gslot] = cv;
-                                p.cand_lb[gslot] = lbv;
+                                if (p.cand_lb) p.cand_lb[gslot] = lbv;
                                 gslot++;
                             } else {
+                                if (SEG) p.seg_flag[ql] = 1u;
                                 gslot++;
                             }
                             slot++;
@@ -656,7 +785,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             }
             // the tile slot (row constants) is no longer read by this warp
             __syncwarp();
-            if (lane == 0) mbar_arrive(&r_empty[rs]);
+            if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
             // drain the stage once it is half full (a tile adds at most 4 x 32 x 16
             // entries; reservations past its end already went to global memory)
             if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
@@ -696,6 +825,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         }
         __syncwarp();
         flush();
+        if (SEG && qvalid && seg_local) atomicAdd(p.seg_cnt + ql, seg_local);
     }
     __syncthreads();
     if (CS > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
@@ -884,11 +1014,17 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 
 // Run the filter for nq queries (bf16 copy Qb with norms) against N rows (Xb).
 // gbound: per-query float bits (initialised by the caller: the seed bound).
+// Projected mode (seg_cnt non-null; K-proj, proj.cu): the operands are the
+// rows' and queries' projections, gbound holds fixed per-query thresholds on
+// the projected lower bound; per-query emission counts, and a query whose
+// emissions pass seg_cap (or whose candidates were dropped) is flagged.
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb, int xb_cw,
                      const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
-                     cudaStream_t s)
+                     cudaStream_t s, unsigned int *seg_flag, unsigned int *seg_cnt, int seg_cap, int64_t tile_limit, const char *prof_name, float seg_u,
+                     float seg_v)
 {
+    const bool seg = seg_cnt != nullptr;
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
     SSB_REQUIRE(N < (1ll << 31), "too many rows for the tensor-core filter");
     if (nq == 0 || N == 0) return OK;
@@ -902,19 +1038,22 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     const int QB = (nq + TC_BM - 1) / TC_BM;
     // cluster: up to 8 query blocks share every B tile through TMA multicast
     int csmax = 2;
-    if (const char *e = getenv("SSB_TC_CSMAX")) csmax = std::max(1, std::min(8, atoi(e)));  // diagnostics
+    if (const char *e = getenv(seg ? "SSB_PROJ_CSMAX" : "SSB_TC_CSMAX")) csmax = std::max(1, std::min(8, atoi(e)));  // A/B
     int CS = 1;
     while (CS < QB && CS < csmax) CS <<= 1;
     const int groups = (QB + CS - 1) / CS;
     p.QB = groups * CS;  // padded; blocks past nq are all-invalid queries
     p.CS = CS;
     p.tiles = (N + TC_BN - 1) / TC_BN;
+    if (tile_limit > 0) p.tiles = std::min(p.tiles, tile_limit);  // a prefix of the (hashed) row order
     const int sms = num_sms();
     // >= 16 tiles per CTA so each thread's running k-th bound tightens early
     int clusters_per_group = std::max(1, sms / CS / groups);
     clusters_per_group = (int)std::max<int64_t>(1, std::min<int64_t>(clusters_per_group, p.tiles / 16));
     p.tiles_per_cta = (p.tiles + clusters_per_group - 1) / clusters_per_group;
     p.ctas_per_qb = (int)((p.tiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
+    // a thread sees 1/(ctas_per_qb x column groups) of a query's rows: it gives
+    // up past twice its share of the query's limit
     int rc = OK;
     p.xb = static_cast<const unsigned char *>(Xb);
     p.qb = reinterpret_cast<const uint4 *>(Qb);
@@ -925,7 +1064,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.gbucket = nullptr;
     p.kstride = k;
     DevBuf buckets;
-    if (k >= 2 && !dump && !(getenv("SSB_TC_NOBUCKET") && k <= TC_KTOP)) {  // env: diagnostics
+    if (k >= 2 && !dump && !seg && !(getenv("SSB_TC_NOBUCKET") && k <= TC_KTOP)) {  // env: diagnostics
         p.kstride = (k + 3) & ~3;
         const size_t bytes = 4 * (size_t)tc_bound_slots(nq) * (size_t)p.kstride;
         SSB_CUDA(buckets.alloc(bytes, s));
@@ -933,7 +1072,12 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         p.gbucket = buckets.as<unsigned int>();
     }
     p.k = k;
-    p.warm = 8;
+    p.warm = seg ? 0 : 8;  // fixed bounds: nothing to warm up
+    p.seg_flag = seg_flag;
+    p.seg_cnt = seg_cnt;
+    p.seg_cap = seg_cap;  // per query here; per thread below, once the grid is known
+    p.seg_u = seg_u;
+    p.seg_v = seg_v;
     // bucket-bound refresh period: every 8 tiles; every 32 for k > 32, where a
     // refresh reads k buckets per thread (C4, k = 100: 14.98 ms at 1965 MHz -> 14.37 ms
     // at a power-capped 1762 MHz)
@@ -971,8 +1115,11 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     // C2 +3%); at n = 96 (C3) 8 warps measured 5% faster.  The k = 32 list
     // variant keeps 8 (register budget).  SSB_TC_EPW=8|16 overrides (A/B).
     const int epw_env = getenv("SSB_TC_EPW") ? atoi(getenv("SSB_TC_EPW")) : 0;
-    const int epw_pref = epw_env ? epw_env : (n > 128 ? 16 : 8);
+    const int epw_env_p = seg && getenv("SSB_PROJ_EPW") ? atoi(getenv("SSB_PROJ_EPW")) : 0;
+    // (projected mode: 16 -- its lean loop is short, more warps hide the waits; C4: 6.98 -> 5.56 ms)
+    const int epw_pref = epw_env_p ? epw_env_p : epw_env ? epw_env : (n > 128 || seg ? 16 : 8);
     const int epw = (epw_pref == 16 && !(k > 16 && k <= 32) && !dump) ? 16 : 8;
+    if (seg) p.seg_cap = (int)std::max<int64_t>(64, 2 * (int64_t)seg_cap / ((int64_t)p.ctas_per_qb * (epw / 4)));
     auto go = [&](auto kern) -> int {
         SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cudaLaunchConfig_t cfg = {};
@@ -995,7 +1142,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
             cudaGetLastError();
         }
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
-        ProfScope ps("tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
+        ProfScope ps(prof_name ? prof_name : seg ? "proj_filter" : "tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
                      2.0 * (double)nq * (double)N * (double)n);  // algorithmic FLOPs (unpadded K)
         SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
         return OK;
@@ -1004,6 +1151,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
 #define TC_GO(KT) (epw == 16 ? go(tc_filter_kernel<KT, 16>) : go(tc_filter_kernel<KT, 8>))
     if (dump)
         rc = go(tc_filter_kernel<-1, 8>);
+    else if (seg)
+        rc = epw == 16 ? go(tc_filter_kernel<0, 16, true>) : go(tc_filter_kernel<0, 8, true>);
     else if (nolist && k >= 2)
         rc = TC_GO(0);
     else if (k <= 1)
@@ -1054,7 +1203,8 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     rc = launch_tc_side(xn2.as<float>(), xnm.as<float2>(), N, side.as<float4>(), s);
     if (rc) return rc;
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, tcx_default_cw(n), side.as<float4>(), N, n,
-                          1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s);
+                          1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s, nullptr,
+                          nullptr, 0, 0, nullptr, 0.f, 0.f);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;

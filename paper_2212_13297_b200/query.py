@@ -142,7 +142,7 @@ class QueryEngine:
     def close(self) -> None:
         pass
 
-    ROUTES = {"auto": 0, "tree": 1, "tensor": 2, "eapca": 3}
+    ROUTES = {"auto": 0, "tree": 1, "tensor": 2, "eapca": 3, "proj": 4}
 
     def knn_device(self, Q, k: int, want_stats: bool = False, eapca_th: float = 0.25,
                    route: str = "auto", lmax: int = 80):
@@ -245,8 +245,11 @@ class QueryEngine:
         else:
             st.phase_reached = "1"
         if tc:
+            # a pass over every row's BF16 operand (route 2, K-proj: its d projection
+            # coefficients; route 1: the whole row) + the exact rescoring
+            width = int(self._si.info.proj_dim) if tc == 2 else n
             st.series_read = self.total_series
-            st.bytes_read = self.total_series * n * 2 + cand_series * n * 4  # BF16 pass + exact rescoring
+            st.bytes_read = self.total_series * width * 2 + cand_series * n * 4
         else:
             st.series_read = min(self.total_series, seed_rows + cand_series)
             st.bytes_read = st.series_read * n * 4 + words * 16  # rows + SAX words tested

@@ -25,7 +25,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-ROUTES = ("auto", "tree", "tensor", "eapca")
+ROUTES = ("auto", "tree", "tensor", "eapca", "proj")
 THREADS = os.cpu_count() or 8
 
 
@@ -171,7 +171,7 @@ def test_k100_two_million_rows(ssb, G, oracle):
     Q = G.noise_queries(X, 48, 0.1, 1)
     idx = ssb.build_index_array(X, ssb.IndexSettings(series_length=256, dataset_size=N, leaf_threshold=10_000))
     eng = ssb.QueryEngine(idx)
-    for route in ("tensor", "auto", "tree"):
+    for route in ("tensor", "auto", "tree", "proj"):
         d2, ids, _ = eng.knn_device(Q, 100, route=route)
         check(oracle, X, Q[:24], 100, d2[:24], ids[:24], f"k=100 N=2M route={route}")
 
