@@ -762,8 +762,11 @@ static int launch_seed_t(const Index &ix, const double *lbe, const float *tbl, c
     const int target = std::min(IX_CMAX - 64, std::max(64, mult * k));
     // leaves ranked at least (SSB_SEED_LEAVES, A/B switch; the approximate phase
     // otherwise stops at the first leaves that hold k series)
+    // (and so do large indexes with small leaves: a few leaves' words are cheap
+    // to rank; with 100K-row leaves (C5) one leaf already holds plenty)
+    const int64_t avg_leaf = ix.N / std::max(1, ix.L);
     const int min_leaves = getenv("SSB_SEED_LEAVES") ? std::max(1, atoi(getenv("SSB_SEED_LEAVES")))
-                                                     : (B <= 64 || ix.N >= ((int64_t)4 << 20) ? 4 : 1);
+                                                     : (B <= 64 || (ix.N >= ((int64_t)4 << 20) && avg_leaf <= 16384) ? 4 : 1);
     ProfScope ps("ix_seed", s, 0.0);
     // one CTA per query: small blocks take 1024 threads so a single query's
     // approximate phase still spreads over a whole SM

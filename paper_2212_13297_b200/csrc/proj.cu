@@ -36,6 +36,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -71,6 +72,29 @@ __global__ void proj_cov_kernel(const float *__restrict__ X, int64_t N, int n, c
 }
 
 // maxima of the rows' (U, V) error norms (non-negative floats: max on the bits)
+// e_i = phi_i^T C phi_i (float64), one CTA per basis vector
+__global__ void proj_energy_kernel(const double *__restrict__ C, const double *__restrict__ phi, int n,
+                                   double *__restrict__ energy)
+{
+    const int i = blockIdx.x;
+    const double *f = phi + (int64_t)i * n;
+    double e = 0.0;
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        double t = 0.0;
+        for (int b = 0; b < n; b++) t += C[(int64_t)a * n + b] * f[b];
+        e += f[a] * t;
+    }
+    __shared__ double red[32];
+    for (int off = 16; off; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+        energy[i] = t;
+    }
+}
+
 __global__ void max_uv_kernel(const float2 *__restrict__ v, int64_t N, unsigned int *__restrict__ out)
 {
     unsigned int mu = 0, mv = 0;
@@ -103,7 +127,8 @@ __global__ void max_bits_kernel(const float *__restrict__ v, int64_t N, unsigned
 // to_bf16_norms_kernel formulas).  CTA = 64-row tiles (persistent), 256
 // threads = 16 row groups x 16 coefficient groups, 4 x 4 accumulators each;
 // P^T and the tile (transposed, padded) in shared memory.  Rows: src row
-// rows[r] (or r), element j at pos[j] (lane-transposed index rows) or j.
+// rows[r] (or r); pos (nullable) maps a physical position of the row to its
+// logical element (the inverse of the lane-transposed layout).
 // is_query: row-major BF16 output and query norms (QH, QL); otherwise the
 // tile-major pre-swizzled operand (CW = 64) and row norms (U, V).
 __global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict__ X, int64_t R, int n,
@@ -123,15 +148,23 @@ __global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict_
     const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;  // rows tr*4.., coefficients tc*4..
     for (int64_t t0 = (int64_t)blockIdx.x * PJ_ROWS; t0 < R; t0 += (int64_t)gridDim.x * PJ_ROWS) {
         __syncthreads();
-        for (int idx = threadIdx.x; idx < PJ_ROWS * n; idx += blockDim.x) {
-            const int r = idx / n, j = idx % n;
+        // 16-byte loads in the rows' physical order, scattered to the logical
+        // element (ipos: physical -> logical position; null: identity)
+        const int n4 = n / 4;
+        for (int idx = threadIdx.x; idx < PJ_ROWS * n4; idx += blockDim.x) {
+            const int r = idx / n4, c4 = idx - r * n4;
             const int64_t row = t0 + r;
-            float v = 0.f;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (row < R) {
                 const int64_t src = rows ? (int64_t)rows[row] : row;
-                v = __ldg(X + src * n + (pos ? pos[j] : j));
+                v = __ldg(reinterpret_cast<const float4 *>(X + src * n) + c4);
             }
-            xs[j * (PJ_ROWS + 1) + r] = v;
+            const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int j = pos ? pos[4 * c4 + e] : 4 * c4 + e;
+                xs[j * (PJ_ROWS + 1) + r] = e4[e];
+            }
         }
         __syncthreads();
         float acc[4][4];
@@ -251,35 +284,33 @@ int build_projection(Index &ix, cudaStream_t s)
     if (n < 2 * PJ_DMAX || ix.N < 1) return OK;
     double min_energy = 0.9;
     if (const char *e = getenv("SSB_PROJ_MIN_ENERGY")) min_energy = atof(e);
-    std::vector<int32_t> hpos(n);
-    for (int j = 0; j < n; j++) hpos[j] = layout_pos(n, j);
-    DevBuf pos, C;
-    SSB_CUDA(pos.alloc(4 * (size_t)n, s));
+    std::vector<int32_t> hpos(2 * n);  // [0, n): logical -> physical; [n, 2n): physical -> logical
+    for (int j = 0; j < n; j++) {
+        hpos[j] = layout_pos(n, j);
+        hpos[n + hpos[j]] = j;
+    }
+    DevBuf pos, C, ener;
+    SSB_CUDA(pos.alloc(8 * (size_t)n, s));
     SSB_CUDA(C.alloc(8 * (size_t)n * n, s));
-    SSB_CUDA(cudaMemcpyAsync(pos.p, hpos.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(ener.alloc(8 * (size_t)n, s));
+    SSB_CUDA(cudaMemcpyAsync(pos.p, hpos.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s));
     const int S = (int)std::min<int64_t>(ix.N, PJ_SAMPLE);
     proj_cov_kernel<<<n, 256, 0, s>>>(ix.X, ix.N, n, pos.as<int32_t>(), S, C.as<double>());
     SSB_CHECK_LAUNCH();
-    std::vector<double> hC((size_t)n * n);
-    SSB_CUDA(cudaMemcpyAsync(hC.data(), C.p, 8 * (size_t)n * n, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    // energy of every basis vector on the sample: phi_i^T C phi_i
-    std::vector<double> phi((size_t)n * n), energy(n), y(n);
+    // energy of every basis vector on the sample: phi_i^T C phi_i (one CTA per i)
+    std::vector<double> phi((size_t)n * n), energy(n), hdiag(n);
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++) phi[(size_t)i * n + j] = dct_basis(n, i, j);
+    DevBuf dphi;
+    SSB_CUDA(dphi.alloc(8 * (size_t)n * n, s));
+    SSB_CUDA(cudaMemcpyAsync(dphi.p, phi.data(), 8 * (size_t)n * n, cudaMemcpyHostToDevice, s));
+    proj_energy_kernel<<<n, 256, 0, s>>>(C.as<double>(), dphi.as<double>(), n, ener.as<double>());
+    SSB_CHECK_LAUNCH();
+    SSB_CUDA(cudaMemcpyAsync(energy.data(), ener.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpy2DAsync(hdiag.data(), 8, C.p, 8 * (size_t)(n + 1), 8, n, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
     double total = 0.0;
-    for (int i = 0; i < n; i++) {
-        const double *f = &phi[(size_t)i * n];
-        double e = 0.0;
-        for (int a = 0; a < n; a++) {
-            const double *ca = &hC[(size_t)a * n];
-            double t = 0.0;
-            for (int b = 0; b < n; b++) t += ca[b] * f[b];
-            e += f[a] * t;
-        }
-        energy[i] = e;
-        total += hC[(size_t)i * n + i];  // trace
-    }
+    for (int i = 0; i < n; i++) total += hdiag[i];  // trace
     std::vector<int> order(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return energy[a] > energy[b]; });
@@ -334,7 +365,7 @@ int build_projection(Index &ix, cudaStream_t s)
     SSB_CUDA(zn2.alloc(4 * (size_t)ix.N, s));
     SSB_CUDA(zen.alloc(8 * (size_t)ix.N, s));
     // rows in the K-tc order: slot r holds leaf position tcperm[r]
-    int rc = launch_proj_rows(ix.X, ix.N, n, pos.as<int32_t>(), ix.tcperm, ix.P, d, false, ix.Zb, zn2.as<float>(),
+    int rc = launch_proj_rows(ix.X, ix.N, n, pos.as<int32_t>() + n, ix.tcperm, ix.P, d, false, ix.Zb, zn2.as<float>(),
                               zen.as<float2>(), s);
     if (rc) return rc;
     rc = launch_tc_side(zn2.as<float>(), zen.as<float2>(), ix.N, ix.zside, s);
@@ -381,6 +412,10 @@ __global__ void proj_bound_kernel(const float *__restrict__ Q, const int32_t *__
     for (int off = 16; off; off >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, off);
     if (lane) return;
     const uint64_t key = thr[q];
+    if (flag[i]) {  // gave up in an earlier part: the full filter answers it
+        gb[i] = 0xff800000u;
+        return;
+    }
     if (key == KEY_EMPTY) {  // no bound: the full filter answers it
         gb[i] = 0xff800000u;  // -inf: nothing is emitted
         flag[i] = 1u;
@@ -394,6 +429,18 @@ __global__ void proj_bound_kernel(const float *__restrict__ Q, const int32_t *__
     // (<= 2^-18 ||zx||^2 / 2 per row, twice in the distance)
     const double T = r * r * (1.0 + 1e-5) + 1e-5 * lam * (q2 + xmax2) + 0x1p-16 * lam * xmax2;
     gb[i] = __float_as_uint(__double2float_ru(T));
+}
+
+// thr[q] <- min(thr[q], the k-th key of the candidates rescored so far) for the
+// queries still on K-proj (k real rows: a valid bound)
+__global__ void proj_tighten_kernel(const uint64_t *__restrict__ keys, int k, const int32_t *__restrict__ qlist,
+                                    const unsigned int *__restrict__ flag, int nq, uint64_t *__restrict__ thr)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq || flag[i]) return;
+    const int q = qlist[i];
+    const uint64_t kth = keys[(size_t)q * k + k - 1];
+    if (kth < thr[q]) thr[q] = kth;
 }
 
 // exact rescoring of the projected filter's candidates (query, K-tc row),
@@ -429,6 +476,16 @@ __global__ void rescore_proj_kernel(const float *__restrict__ X, const uint32_t 
     }
 }
 
+// queries handed to the full filter start over: drop what earlier ranges
+// rescored for them (the full filter re-emits every row; duplicates would
+// break the selection)
+__global__ void proj_reset_hard_kernel(const int32_t *__restrict__ hard, const int32_t *__restrict__ qlist, int nq,
+                                       uint32_t *__restrict__ cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nq && hard[i]) cnt[qlist[i]] = 0;
+}
+
 __global__ void proj_cser_kernel(const unsigned int *__restrict__ cnt, const int32_t *__restrict__ hard,
                                  const int32_t *__restrict__ qlist, int nq, uint32_t *__restrict__ cser)
 {
@@ -436,17 +493,19 @@ __global__ void proj_cser_kernel(const unsigned int *__restrict__ cnt, const int
     if (i < nq && !hard[i]) cser[qlist[i]] = cnt[i];
 }
 
+// candidates [c0, c1) of the list; `hard` (per launch-local query) skips queries
 static int launch_rescore_proj(const Index &ix, ProjWork &pw, const float *Qp, const int32_t *only, ScanOut so,
-                               cudaStream_t s)
+                               cudaStream_t s, int64_t c0, int64_t c1, const int32_t *hard)
 {
-    if (pw.nq == 0 || pw.nc == 0) return OK;
-    const unsigned grid = (unsigned)std::min<int64_t>((pw.nc * 8 + 255) / 256, (int64_t)num_sms() * 16);
-    ProfScope ps("proj_rescore", s, (double)pw.nc * ix.n * 4);
-    const uint2 *cand = pw.cand.as<uint2>();
-    const int32_t *qm = pw.qidx.as<int32_t>(), *hard = pw.hard.as<int32_t>();
+    const int64_t nc = c1 - c0;
+    if (pw.nq == 0 || nc <= 0) return OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((nc * 8 + 255) / 256, (int64_t)num_sms() * 16);
+    ProfScope ps("proj_rescore", s, (double)nc * ix.n * 4);
+    const uint2 *cand = pw.cand.as<uint2>() + c0;
+    const int32_t *qm = pw.qidx.as<int32_t>();
     switch (ix.n) {
-    case 128: rescore_proj_kernel<128><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, pw.nc, hard, only, so); break;
-    case 256: rescore_proj_kernel<256><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, pw.nc, hard, only, so); break;
+    case 128: rescore_proj_kernel<128><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, hard, only, so); break;
+    case 256: rescore_proj_kernel<256><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, hard, only, so); break;
     default:
         set_error(ERR_USAGE, "series length " + std::to_string(ix.n) + " has no compiled projected rescore kernel");
         return ERR_USAGE;
@@ -457,75 +516,230 @@ static int launch_rescore_proj(const Index &ix, ProjWork &pw, const float *Qp, c
 
 bool proj_available(const Index &ix) { return ix.Zb != nullptr && (ix.n == 128 || ix.n == 256); }
 
-// K-proj for the tensor-route queries `qtc` of a block of B queries (their
-// bounds in thr, their lane-transposed copies in qlay): one pass over every
-// row's projection under T(thr), each query's candidates appended to its own
-// segment and rescored exactly into `so`.  Queries whose segment overflowed,
-// or that have no bound, are returned in *hard for the full filter.
-int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc, uint64_t *thr, const float *qlay,
-               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard, ProjWork &pw, cudaStream_t s)
+// Queries of one K-proj phase: projection, BF16 operand and norms, their
+// candidate list and counters.
+static int phase_setup(const Index &ix, const float *Q, const std::vector<int32_t> &ql, int64_t cap, ProjWork &pw,
+                       DevBuf &qb, DevBuf &qn2, DevBuf &qen, DevBuf &gb, cudaStream_t s)
 {
-    hard->clear();
-    const int nq = (int)qtc.size();
-    pw.nq = nq;
-    if (nq == 0) return OK;
-    const int d = ix.pd, n = ix.n;
+    const int nq = (int)ql.size();
     const int nq_pad = (nq + 127) / 128 * 128;
-    // per query: give up past seg_cap candidates (rescoring 32K rows costs about
-    // what a query's share of the full filter does at 25M rows); the buffer
-    // holds ~24K per query on average
-    pw.seg_cap = 32768;
-    if (const char *e = getenv("SSB_PROJ_SEG")) pw.seg_cap = std::max(1, atoi(e));  // test hook
-    pw.cap = std::max<int64_t>(1 << 20, std::min<int64_t>((int64_t)nq * 24576, (int64_t)1 << 27));
-    if (const char *e = getenv("SSB_PROJ_CAP")) pw.cap = std::max<int64_t>(1, atoll(e));  // test hook
-    DevBuf qb, qn2, qen, gb;
+    pw.nq = nq;
+    pw.cap = cap;
     SSB_CUDA(pw.qidx.alloc(4 * (size_t)nq, s));
     SSB_CUDA(pw.cnt.alloc(4 * (size_t)nq, s));
     SSB_CUDA(pw.flag.alloc(4 * (size_t)nq, s));
     SSB_CUDA(pw.hard.alloc(4 * (size_t)nq, s));
-    SSB_CUDA(pw.cand.alloc(8 * (size_t)pw.cap, s));
+    SSB_CUDA(pw.cand.alloc(8 * (size_t)cap, s));
     SSB_CUDA(pw.cn.alloc(8, s));
     SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * PJ_DMAX, s));
     SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
     SSB_CUDA(qen.alloc(8 * (size_t)nq_pad, s));
     SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
-    SSB_CUDA(cudaMemcpyAsync(pw.qidx.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(pw.qidx.p, ql.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaMemsetAsync(pw.cnt.p, 0, 4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(pw.flag.p, 0, 4 * (size_t)nq, s));
+    SSB_CUDA(cudaMemsetAsync(pw.hard.p, 0, 4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(pw.cn.p, 0, 8, s));
     SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * PJ_DMAX, s));
     SSB_CUDA(cudaMemsetAsync(qn2.p, 0, 4 * (size_t)nq_pad, s));
     SSB_CUDA(cudaMemsetAsync(qen.p, 0, 8 * (size_t)nq_pad, s));
     SSB_CUDA(cudaMemsetAsync(gb.p, 0xff, 4 * (size_t)tc_bound_slots(nq), s));  // NaN bits: never emits
-    const int32_t *qidx = pw.qidx.as<int32_t>();
-    int rc = launch_proj_rows(Q, nq, n, nullptr, reinterpret_cast<const uint32_t *>(qidx), ix.P, d, true, qb.p,
-                              qn2.as<float>(), qen.as<float2>(), s);
-    if (rc) return rc;
-    proj_bound_kernel<<<(nq + 7) / 8, 256, 0, s>>>(Q, qidx, nq, n, thr, ix.p_lam, ix.p_gf, ix.p_xmax2,
-                                                   gb.as<unsigned int>(), pw.flag.as<unsigned int>());
+    return launch_proj_rows(Q, nq, ix.n, nullptr, reinterpret_cast<const uint32_t *>(pw.qidx.p), ix.P, ix.pd, true,
+                            qb.p, qn2.as<float>(), qen.as<float2>(), s);
+}
+
+// One filter launch over tiles [lo, hi) under T(thr); `allow` = each query's
+// give-up allowance for the range
+static int phase_range(const Index &ix, const float *Q, uint64_t *thr, int k, ProjWork &pw, DevBuf &qb, DevBuf &qn2,
+                       DevBuf &qen, DevBuf &gb, int64_t lo, int64_t hi, int64_t allow, cudaStream_t s)
+{
+    const int nq = pw.nq;
+    proj_bound_kernel<<<(nq + 7) / 8, 256, 0, s>>>(Q, pw.qidx.as<int32_t>(), nq, ix.n, thr, ix.p_lam, ix.p_gf,
+                                                   ix.p_xmax2, gb.as<unsigned int>(), pw.flag.as<unsigned int>());
     SSB_CHECK_LAUNCH();
-    rc = launch_tc_filter(qb.p, qn2.as<float>(), qen.as<float2>(), nq, ix.Zb, 64, ix.zside, ix.N, PJ_DMAX, k,
-                          gb.as<unsigned int>(), pw.cand.as<uint2>(), nullptr, pw.cn.as<unsigned long long>(), pw.cap,
-                          nullptr, s, pw.flag.as<unsigned int>(), pw.cnt.as<unsigned int>(), pw.seg_cap, 0, nullptr,
-                          ix.p_u2, ix.p_v2);
-    if (rc) return rc;
-    std::vector<uint32_t> hc(nq), hf(nq);
+    return launch_tc_filter(qb.p, qn2.as<float>(), qen.as<float2>(), nq, ix.Zb, 64, ix.zside, ix.N, PJ_DMAX, k,
+                            gb.as<unsigned int>(), pw.cand.as<uint2>(), nullptr, pw.cn.as<unsigned long long>(), pw.cap,
+                            nullptr, s, pw.flag.as<unsigned int>(), pw.cnt.as<unsigned int>(),
+                            (int)std::max<int64_t>(1, std::min<int64_t>(allow, INT32_MAX)), lo, hi, nullptr, ix.p_u2,
+                            ix.p_v2);
+}
+
+// Rescore the candidates [nc_done, current) of a phase (queries flagged so far
+// skipped), then tighten every query's bound to the k-th key found so far.
+static int phase_tighten(const Index &ix, ProjWork &pw, const float *qlay, int B, int k, ScanOut so, uint64_t *thr,
+                         int64_t *nc_done, cudaStream_t s)
+{
     unsigned long long hn = 0;
-    SSB_CUDA(cudaMemcpyAsync(hc.data(), pw.cnt.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaMemcpyAsync(hf.data(), pw.flag.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaMemcpyAsync(&hn, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaStreamSynchronize(s));
-    pw.nc = std::min<int64_t>((int64_t)hn, pw.cap);
-    std::vector<int32_t> hh(nq);
-    int64_t total = 0;
+    const int64_t nc_now = std::min<int64_t>((int64_t)hn, pw.cap);
+    int rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, *nc_done, nc_now,
+                                 reinterpret_cast<const int32_t *>(pw.flag.p));
+    if (rc) return rc;
+    *nc_done = nc_now;
+    DevBuf pk, pt, pf;
+    SSB_CUDA(pk.alloc(8 * (size_t)B * k, s));
+    SSB_CUDA(pt.alloc(8 * (size_t)B, s));
+    SSB_CUDA(pf.alloc(4 * (size_t)B, s));
+    rc = launch_select(so.cand, so.cnt, so.cap, B, k, pt.as<uint64_t>(), pk.as<uint64_t>(), pf.as<int32_t>(), s);
+    if (rc) return rc;
+    proj_tighten_kernel<<<(pw.nq + 255) / 256, 256, 0, s>>>(pk.as<uint64_t>(), k, pw.qidx.as<int32_t>(),
+                                                            pw.flag.as<unsigned int>(), pw.nq, thr);
+    SSB_CHECK_LAUNCH();
+    return OK;
+}
+
+// K-proj for the tensor-route queries `qtc` of a block of B queries (their
+// bounds in thr, their lane-transposed copies in qlay); candidates rescored
+// exactly into `so`.  The rows are scanned in ranges of the hashed order
+// (random samples):
+//  * the sample phase: the first 1/64 of the rows for every query; its
+//    candidate counts predict each query's total, and a query predicted past
+//    seg_cap (a weak bound, e.g. sigma = 1.0 noise) leaves for the full filter
+//    before costing the main pass anything -- unless only a few are, which
+//    stay with a larger allowance (a full-filter pass of its own for a handful
+//    of queries costs more than their candidates);
+//  * the main phase, for the remaining queries only (fewer query blocks), over
+//    the rest of the rows in split - 1 ranges; after every range but the last,
+//    its candidates are rescored and each bound tightens to the k-th exact key
+//    found so far (C4: median bound 48.8 -> 42, candidates 13.2M -> 7.0M).
+// Queries that still overflow, or have no bound, are returned in *hard.
+int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc, uint64_t *thr, const float *qlay,
+               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard,
+               std::vector<std::unique_ptr<ProjWork>> &pws, cudaStream_t s)
+{
+    hard->clear();
+    pws.clear();
+    const int nq = (int)qtc.size();
+    if (nq == 0) return OK;
+    // per query: give up past seg_cap candidates (a query the full filter answers
+    // costs that filter a whole pass over the index: C4's 15-100 such queries at
+    // 32K cost 1.9 ms, rescoring their candidates instead ~0.3 ms)
+    int64_t seg_cap = 131072;
+    if (const char *e = getenv("SSB_PROJ_SEG")) seg_cap = std::max(1, atoi(e));  // test hook
+    const int64_t tiles = (ix.N + 127) / 128;
+    int split = 4;
+    if (const char *e = getenv("SSB_PROJ_SPLIT")) split = std::max(1, std::min(8, atoi(e)));
+    if (tiles < 64 * split) split = 1;
+    const int64_t t0 = split > 1 ? std::max<int64_t>(1, tiles / 64) : 0;
+    int64_t seg_eff = seg_cap;
+    std::vector<char> is_hard(nq, 0);  // per qtc index
+    std::vector<uint32_t> total(nq, 0);
+    int predicted_hard = 0;
+
+    // ---- sample phase ----------------------------------------------------------
+    if (t0 > 0) {
+        pws.emplace_back(new ProjWork());
+        ProjWork &pw = *pws.back();
+        DevBuf qb, qn2, qen, gb;
+        // allowance 8 x the range's share: only a clearly hard query gives up here
+        const int64_t allow = 8 * seg_cap * t0 / tiles;
+        int rc = phase_setup(ix, Q, qtc, std::max<int64_t>(1 << 20, (int64_t)nq * 2 * allow), pw, qb, qn2, qen, gb, s);
+        if (rc) return rc;
+        rc = phase_range(ix, Q, thr, k, pw, qb, qn2, qen, gb, 0, t0, allow, s);
+        if (rc) return rc;
+        std::vector<uint32_t> c0(nq), f0(nq);
+        SSB_CUDA(cudaMemcpyAsync(c0.data(), pw.cnt.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(f0.data(), pw.flag.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < nq; i++) {
+            is_hard[i] = f0[i] || (double)c0[i] * (double)tiles / (double)t0 > (double)seg_cap;
+            predicted_hard += is_hard[i];
+        }
+        if (predicted_hard < 64 && !std::any_of(f0.begin(), f0.end(), [](uint32_t f) { return f != 0; })) {
+            seg_eff = 8 * seg_cap;  // keep them, with the sample's larger allowance
+            std::fill(is_hard.begin(), is_hard.end(), 0);
+        } else {
+            for (int i = 0; i < nq; i++) f0[i] = is_hard[i] ? 1u : 0u;
+            SSB_CUDA(cudaMemcpyAsync(pw.flag.p, f0.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+        }
+        for (int i = 0; i < nq; i++) total[i] = c0[i];
+        int64_t nc_done = 0;
+        rc = phase_tighten(ix, pw, qlay, B, k, so, thr, &nc_done, s);  // syncs: f0 may die after
+        if (rc) return rc;
+        pw.nc = nc_done;
+    }
+
+    // ---- main phase: the remaining queries over the rest of the rows -----------
+    std::vector<int32_t> live;
+    std::vector<int> live_at;  // live index -> qtc index
+    for (int i = 0; i < nq; i++)
+        if (!is_hard[i]) {
+            live.push_back(qtc[i]);
+            live_at.push_back(i);
+        }
+    unsigned long long hn = 0;
+    if (!live.empty()) {
+        pws.emplace_back(new ProjWork());
+        ProjWork &pw = *pws.back();
+        DevBuf qb, qn2, qen, gb;
+        const int nl = (int)live.size();
+        // candidates up to every query's give-up point in the first range, ~24K per
+        // query for the rest (a drop hands its query to the full filter; the few
+        // queries kept with a larger allowance fit in the slack)
+        const int64_t cap = std::max<int64_t>(
+            1 << 20, std::min<int64_t>((int64_t)nl * (24576 + 2 * seg_cap / std::max(1, split - 1)), (int64_t)1 << 27));
+        int rc = phase_setup(ix, Q, live, cap, pw, qb, qn2, qen, gb, s);
+        if (rc) return rc;
+        const int parts = split > 1 ? split - 1 : 1;
+        int64_t nc_done = 0;
+        for (int part = 0; part < parts; part++) {
+            const int64_t lo = t0 + (tiles - t0) * part / parts, hi = t0 + (tiles - t0) * (part + 1) / parts;
+            rc = phase_range(ix, Q, thr, k, pw, qb, qn2, qen, gb, lo, hi, seg_eff * (hi - lo) / tiles, s);
+            if (rc) return rc;
+            if (part + 1 < parts) {
+                rc = phase_tighten(ix, pw, qlay, B, k, so, thr, &nc_done, s);
+                if (rc) return rc;
+            }
+        }
+        std::vector<uint32_t> hc(nl), hf(nl);
+        SSB_CUDA(cudaMemcpyAsync(hc.data(), pw.cnt.p, 4 * (size_t)nl, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(hf.data(), pw.flag.p, 4 * (size_t)nl, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaMemcpyAsync(&hn, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        pw.nc = std::min<int64_t>((int64_t)hn, pw.cap);
+        std::vector<int32_t> hh(nl);
+        for (int j = 0; j < nl; j++) {
+            const int i = live_at[j];
+            total[i] += hc[j];
+            hh[j] = (hf[j] || (int64_t)total[i] > seg_eff) ? 1 : 0;
+            is_hard[i] = (char)hh[j];
+        }
+        SSB_CUDA(cudaMemcpyAsync(pw.hard.p, hh.data(), 4 * (size_t)nl, cudaMemcpyHostToDevice, s));
+        // the last range's candidates (hard queries excluded)
+        rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, nc_done, pw.nc, pw.hard.as<int32_t>());
+        if (rc) return rc;
+        SSB_CUDA(cudaStreamSynchronize(s));  // hh dies here
+    }
+    // the sample phase's view of the final decision (for the flagged re-rescoring)
+    std::vector<int32_t> h32(nq);
+    int64_t settled = 0;
     for (int i = 0; i < nq; i++) {
-        hh[i] = (hf[i] || hc[i] > (uint32_t)pw.seg_cap) ? 1 : 0;
-        if (hh[i])
+        h32[i] = is_hard[i] ? 1 : 0;
+        if (is_hard[i])
             hard->push_back(qtc[i]);
         else
-            total += hc[i];
+            settled += total[i];
     }
-    SSB_CUDA(cudaMemcpyAsync(pw.hard.p, hh.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    if (t0 > 0) SSB_CUDA(cudaMemcpyAsync(pws[0]->hard.p, h32.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    // queries handed to the full filter start over there (what the ranges
+    // rescored for them would be duplicates)
+    DevBuf dh, dq, dc;
+    SSB_CUDA(dh.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(dq.alloc(4 * (size_t)nq, s));
+    SSB_CUDA(cudaMemcpyAsync(dh.p, h32.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(dq.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    proj_reset_hard_kernel<<<(nq + 255) / 256, 256, 0, s>>>(dh.as<int32_t>(), dq.as<int32_t>(), nq, so.cnt);
+    SSB_CHECK_LAUNCH();
+    if (cser) {
+        std::vector<uint32_t> tt(total.begin(), total.end());
+        SSB_CUDA(dc.alloc(4 * (size_t)nq, s));
+        SSB_CUDA(cudaMemcpyAsync(dc.p, tt.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+        proj_cser_kernel<<<(nq + 255) / 256, 256, 0, s>>>(dc.as<unsigned int>(), dh.as<int32_t>(), dq.as<int32_t>(), nq,
+                                                          cser);
+        SSB_CHECK_LAUNCH();
+        SSB_CUDA(cudaStreamSynchronize(s));  // tt dies here
+    }
     if (getenv("SSB_TC_TRACE")) {
         std::vector<uint64_t> bb(B);
         SSB_CUDA(cudaMemcpyAsync(bb.data(), thr, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
@@ -533,28 +747,25 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         std::vector<float> v;
         for (int q : qtc) v.push_back(bb[q] == KEY_EMPTY ? INFINITY : key_d2(bb[q]));
         std::sort(v.begin(), v.end());
-        fprintf(stderr, "[ssb] proj batch nq=%d k=%d d=%d: bounds d2 p10/p50/p90 %.3g/%.3g/%.3g; %llu emitted "
-                        "(cap %lld), %lld for the %zu settled queries, %zu hard\n",
-                nq, k, d, v[v.size() / 10], v[v.size() / 2], v[v.size() * 9 / 10], hn, (long long)pw.cap,
-                (long long)total, qtc.size() - hard->size(), hard->size());
+        fprintf(stderr, "[ssb] proj batch nq=%d k=%d d=%d split %d: sample predicted %d hard, main phase %zu queries; "
+                        "final bounds d2 p10/p50/p90 %.3g/%.3g/%.3g; %lld candidates for the %zu settled queries, %zu hard\n",
+                nq, k, ix.pd, split, predicted_hard, live.size(), v[v.size() / 10], v[v.size() / 2],
+                v[v.size() * 9 / 10], (long long)settled, qtc.size() - hard->size(), hard->size());
     }
-    rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s);
-    if (rc) return rc;
-    if (cser) {
-        proj_cser_kernel<<<(nq + 255) / 256, 256, 0, s>>>(pw.cnt.as<unsigned int>(), pw.hard.as<int32_t>(), qidx, nq,
-                                                          cser);
-        SSB_CHECK_LAUNCH();
-    }
-    SSB_CUDA(cudaStreamSynchronize(s));  // hh dies here
+    SSB_CUDA(cudaStreamSynchronize(s));  // h32 dies here
     return OK;
 }
 
 // the select overflowed for some queries: their candidates again under the
 // tighter bound (flags: per block query)
-int proj_rescore_flagged(const Index &ix, ProjWork &pw, const float *qlay, const int32_t *flags, ScanOut so,
-                         cudaStream_t s)
+int proj_rescore_flagged(const Index &ix, std::vector<std::unique_ptr<ProjWork>> &pws, const float *qlay,
+                         const int32_t *flags, ScanOut so, cudaStream_t s)
 {
-    return launch_rescore_proj(ix, pw, qlay, flags, so, s);
+    for (auto &pw : pws) {
+        const int rc = launch_rescore_proj(ix, *pw, qlay, flags, so, s, 0, pw->nc, pw->hard.as<int32_t>());
+        if (rc) return rc;
+    }
+    return OK;
 }
 
 }  // namespace ssb

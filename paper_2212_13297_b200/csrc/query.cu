@@ -251,6 +251,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     // modelled time, in whole 256-query groups), and sizes the items exactly.
     const int64_t per_query_worst = ix.N / 512 + ix.L + 1;
     std::vector<int32_t> qtc;
+    std::vector<unsigned long long> kept;  // rows of the leaves each query's bound keeps (host copy)
     if (mode == 1 && (int64_t)B * per_query_worst <= (256 << 10)) {
         rc = ix_emit(ix, w, B, nullptr, 0, (int64_t)B * per_query_worst, s);
         if (rc) return rc;
@@ -296,6 +297,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         rc = ix_emit(ix, w, B, nullptr, 0, items, s);
         if (rc) return rc;
         SSB_CUDA(cudaStreamSynchronize(s));  // tc (the uploaded routes) dies here
+        kept.swap(kr);
     }
 
     // index route first (Q5 + Q6 of every query the plan kept on it)
@@ -305,12 +307,36 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     // ---- K-proj first (proj.cu): the projected filter under the approximate
     // phase's bounds answers the tensor-route queries it can; the rest (segment
     // overflow: a weak bound; no bound) go on to the full filter -------------------
-    ProjWork pw;
+    std::vector<std::unique_ptr<ProjWork>> pws;
     std::vector<char> projq;  // per block query: answered by K-proj
     if (!qtc.empty() && proj_available(ix) && !getenv("SSB_NO_PROJ")) {
-        std::vector<int32_t> hard;
-        rc = proj_route(ix, Q, qtc, thr, w.qlay.as<float>(), B, k, so, want ? cser.as<uint32_t>() : nullptr, &hard, pw, s);
+        // queries whose LB_EAPCA keeps nearly all of the index (weak bounds:
+        // sigma = 1.0 noise keeps 95-98%, C4's sigma = 0.1 at most ~70%) would
+        // overflow K-proj's segments: straight to the full filter
+        double maxkept = 0.9;
+        if (const char *e = getenv("SSB_PROJ_MAXKEPT")) maxkept = atof(e);
+        {  // only worth a full-filter pass of its own when enough queries take it
+            int nd = 0;
+            for (int q : qtc) nd += !kept.empty() && (double)kept[q] > maxkept * (double)ix.N;
+            if (nd < 128) maxkept = 2.0;
+        }
+        std::vector<int32_t> pq, direct, hard;
+        for (int q : qtc) {
+            if (!kept.empty() && (double)kept[q] > maxkept * (double)ix.N)
+                direct.push_back(q);
+            else
+                pq.push_back(q);
+        }
+        if (getenv("SSB_TC_TRACE") && !kept.empty()) {
+            std::vector<double> f;
+            for (int q : qtc) f.push_back((double)kept[q] / (double)ix.N);
+            std::sort(f.begin(), f.end());
+            fprintf(stderr, "[ssb] proj routing: kept fraction p10/p50/p90 %.3f/%.3f/%.3f; %zu to K-proj, %zu direct\n",
+                    f[f.size() / 10], f[f.size() / 2], f[f.size() * 9 / 10], pq.size(), direct.size());
+        }
+        rc = proj_route(ix, Q, pq, thr, w.qlay.as<float>(), B, k, so, want ? cser.as<uint32_t>() : nullptr, &hard, pws, s);
         if (rc) return rc;
+        hard.insert(hard.end(), direct.begin(), direct.end());
         projq.assign(B, 0);
         for (int q : qtc) projq[q] = 1;
         for (int q : hard) projq[q] = 0;
@@ -443,8 +469,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         rc = ix_back(ix, w, B, skip.as<int32_t>(), so, nullptr, s);
         if (rc) return rc;
         // K-proj queries: their segments again under the tighter bound
-        if (pw.nq) {
-            rc = proj_rescore_flagged(ix, pw, w.qlay.as<float>(), flags.as<int32_t>(), so, s);
+        if (!pws.empty()) {
+            rc = proj_rescore_flagged(ix, pws, w.qlay.as<float>(), flags.as<int32_t>(), so, s);
             if (rc) return rc;
         }
         // tensor-core queries: rescore their candidates again under the tighter bound

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -145,7 +146,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
                      const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s, unsigned int *seg_flag = nullptr, unsigned int *seg_cnt = nullptr, int seg_cap = 0,
-                     int64_t tile_limit = 0, const char *prof_name = nullptr, float seg_u = 0.f,
+                     int64_t tile_lo = 0, int64_t tile_hi = 0, const char *prof_name = nullptr, float seg_u = 0.f,
                      float seg_v = 0.f);
 int64_t tc_bound_slots(int nq);
 int64_t tc_side_bytes(int64_t N);
@@ -155,17 +156,18 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
 int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,
                          uint32_t *qmax, cudaStream_t s);
 // K-proj (proj.cu)
-struct ProjWork {
+struct ProjWork {  // one phase: its queries, candidate list and counters
     DevBuf qidx, cnt, flag, cand, cn, hard;
-    int nq = 0, seg_cap = 0;
+    int nq = 0;
     int64_t cap = 0, nc = 0;
 };
 int build_projection(Index &ix, cudaStream_t s);
 bool proj_available(const Index &ix);
 int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc, uint64_t *thr, const float *qlay,
-               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard, ProjWork &pw, cudaStream_t s);
-int proj_rescore_flagged(const Index &ix, ProjWork &pw, const float *qlay, const int32_t *flags, ScanOut so,
-                         cudaStream_t s);
+               int B, int k, ScanOut so, uint32_t *cser, std::vector<int32_t> *hard,
+               std::vector<std::unique_ptr<ProjWork>> &pws, cudaStream_t s);
+int proj_rescore_flagged(const Index &ix, std::vector<std::unique_ptr<ProjWork>> &pws, const float *qlay,
+                         const int32_t *flags, ScanOut so, cudaStream_t s);
 
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr, uint64_t *out_keys,
                   int32_t *flags, cudaStream_t s);

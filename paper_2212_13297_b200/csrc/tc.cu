@@ -184,7 +184,8 @@ struct TcParams {
     const uint4 *qb;       // BF16 queries, row-major (n per row), nq rows
     int nq;                // queries in this launch (<= QB*128)
     int QB;                // query blocks
-    int64_t tiles;         // ceil(N / 128)
+    int64_t tiles;         // tiles this launch scans (from tile0)
+    int64_t tile0;         // first tile (a range of the K-tc row order)
     int64_t tiles_per_cta; // contiguous tile chunk per CTA (per cluster)
     int ctas_per_qb;       // chunks
     int CS;                // cluster size: CTAs (query blocks) sharing each B tile by multicast
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     // are never emitted against an infinite bound
     const int nwarm = min(p.warm, ntile);
     const int niter = ntile + nwarm;
-    auto tile_of = [&](int t) -> int64_t { return t_begin + (t < nwarm ? t : t - nwarm); };
+    auto tile_of = [&](int t) -> int64_t { return p.tile0 + t_begin + (t < nwarm ? t : t - nwarm); };
 
     if (threadIdx.x == 0) {
         mbar_init(a_full, 128);  // the four h == 0 epilogue warps write A into TMEM
@@ -556,20 +557,28 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             float thr = qvalid ? ((alpha_l - QH * p.seg_u - QL * p.seg_v) - gnext) * inv2f : __int_as_float(0x7f800000);
             thr -= 1e-5f * (fabsf(thr) + 1.f);  // float32 rounding may only send more rows to rescoring
             if (!(thr == thr)) thr = __int_as_float(0x7f800000);  // no bound (NaN / -inf): nothing emitted
+            // (accumulator index and phase kept incrementally: the loop body is
+            // issue-bound, every instruction per tile counts x EPW warps)
+            const uint32_t tbase = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(h * COLS);
+            const int64_t rbase = (p.tile0 + t_begin) * TC_BN + h * COLS;  // nwarm = 0: tile t = t_begin + t
+            uint32_t s = 0, ph = 0;
+            unsigned gave_up = 0;  // another thread of this query gave up (read every 16th tile, used at the next)
             for (int t = 0; t < niter; t++) {
-                const int s = t % TC_NACC;
-                const int64_t row0 = tile_of(t) * TC_BN + h * COLS;
-                mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
+                if ((t & 15) == 0 && qvalid) {
+                    if (gave_up) thr = __int_as_float(0x7f800000);
+                    gave_up = *(volatile const unsigned int *)(p.seg_flag + ql);
+                }
+                const uint32_t sa = 8u * s, taddr = tbase + s * (uint32_t)TC_BN;
+                if (++s == TC_NACC) s = 0;
+                mbar_wait_a(a_tfull + sa, ph);
+                if (s == 0) ph ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t taddr =
-                    tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
                 uint32_t v[COLS];
 #pragma unroll
                 for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
                 tmem_wait_ld();
                 asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive_a(a_tempty + 8u * s);
-                if (diag_skip) continue;
+                mbar_arrive_a(a_tempty + sa);
                 float mg[COLS / 16];
 #pragma unroll
                 for (int g = 0; g < COLS / 16; g++) {
@@ -585,6 +594,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 #pragma unroll
                 for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
                 if (!__any_sync(0xffffffffu, mx >= thr)) continue;
+                const int64_t row0 = rbase + (int64_t)t * TC_BN;
                 const int64_t left = p.N - row0;
                 const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
 #pragma unroll
@@ -1021,7 +1031,7 @@ int64_t tc_bound_slots(int nq) { return (int64_t)(nq + 1023) / 1024 * 1024; }
 int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq, const void *Xb, int xb_cw,
                      const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
-                     cudaStream_t s, unsigned int *seg_flag, unsigned int *seg_cnt, int seg_cap, int64_t tile_limit, const char *prof_name, float seg_u,
+                     cudaStream_t s, unsigned int *seg_flag, unsigned int *seg_cnt, int seg_cap, int64_t tile_lo, int64_t tile_hi, const char *prof_name, float seg_u,
                      float seg_v)
 {
     const bool seg = seg_cnt != nullptr;
@@ -1045,7 +1055,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.QB = groups * CS;  // padded; blocks past nq are all-invalid queries
     p.CS = CS;
     p.tiles = (N + TC_BN - 1) / TC_BN;
-    if (tile_limit > 0) p.tiles = std::min(p.tiles, tile_limit);  // a prefix of the (hashed) row order
+    // a range [tile_lo, tile_hi) of the (hashed) row order: a random sample of the rows
+    if (tile_hi > 0) p.tiles = std::min(p.tiles, tile_hi);
+    p.tile0 = std::max<int64_t>(0, std::min(tile_lo, p.tiles));
+    p.tiles -= p.tile0;
     const int sms = num_sms();
     // >= 16 tiles per CTA so each thread's running k-th bound tightens early
     int clusters_per_group = std::max(1, sms / CS / groups);
@@ -1142,8 +1155,9 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
             cudaGetLastError();
         }
         // algorithmic bytes: every row's bf16 copy once per cluster group + the queries
-        ProfScope ps(prof_name ? prof_name : seg ? "proj_filter" : "tc_filter", s, (double)groups * N * n * 2 + (double)nq * n * 2,
-                     2.0 * (double)nq * (double)N * (double)n);  // algorithmic FLOPs (unpadded K)
+        const double rows = std::min<double>((double)N, (double)p.tiles * TC_BN);  // rows this launch scans
+        ProfScope ps(prof_name ? prof_name : seg ? "proj_filter" : "tc_filter", s, (double)groups * rows * n * 2 + (double)nq * n * 2,
+                     2.0 * (double)nq * rows * (double)n);  // algorithmic FLOPs (unpadded K)
         SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
         return OK;
     };
@@ -1204,7 +1218,7 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     if (rc) return rc;
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, tcx_default_cw(n), side.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s, nullptr,
-                          nullptr, 0, 0, nullptr, 0.f, 0.f);
+                          nullptr, 0, 0, 0, nullptr, 0.f, 0.f);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
