@@ -96,6 +96,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 // barrier waits / arrivals on precomputed 32-bit shared addresses; the wait
 // suspends the warp in hardware (time hint) instead of spinning on try_wait,
 // so waiting warps leave the issue slots to the working ones
+__device__ __forceinline__ void mbar_spin_a(uint32_t a, unsigned phase)  // latency-critical single warps
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, unsigned phase)
 {
     asm volatile(
@@ -320,7 +333,112 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 
     // Producer and MMA roles run warp-wide (every value stays warp-uniform, in
     // uniform registers); one elected lane issues each TMA / tcgen05 instruction.
-    if (warp == 0) {
+    // Projected mode: tiles are small (16 KB), so the B loads go in units of
+    // SEG_U consecutive tiles (contiguous in the tile-major operand and in the
+    // ring: one bulk copy of 64 KB), the CTAs of a cluster taking whole units in
+    // turn (the per-tile half-tile copies cap the load stream at ~3.5 TB/s)
+    constexpr int SEG_U = 4;
+    const int NSU = NS / SEG_U;  // unit slots in the ring
+    if (SEG && warp == 0) {
+        // ---------------- TMA producer (units) ----------------
+        const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
+        const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sRing);
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int u = 0, t = 0; t < niter; u++, t += SEG_U) {
+            const int nt = min(SEG_U, niter - t);
+            if (u >= NSU) mbar_spin_a(a_bempty + 8u * slot, phase ^ 1u);
+            const uint32_t bar = a_bfull + 8u * slot, bytes = (uint32_t)nt * tile_bytes;
+            asm volatile(
+                "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
+                "r"(bytes)
+                : "memory");
+            if (u % CS == rank) {
+                const unsigned char *src = p.xb + (size_t)tile_of(t) * tile_bytes;  // nwarm = 0: contiguous tiles
+                const uint32_t dst = ring + (uint32_t)slot * SEG_U * tile_bytes;
+                if (CS == 1)
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%2], %3, [%1];\n}" ::"r"(dst),
+                        "r"(bar), "l"(src), "r"(bytes)
+                        : "memory");
+                else
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        ".multicast::cluster [%0], [%2], %3, [%1], %4;\n}" ::"r"(dst),
+                        "r"(bar), "l"(src), "r"(bytes), "h"(cmask)
+                        : "memory");
+            }
+            if (++slot == NSU) {
+                slot = 0;
+                phase ^= 1u;
+            }
+        }
+    } else if (SEG && warp == 1) {
+        // ---------------- MMA issuer (units) ----------------
+        if (ntile > 0) {
+            mbar_wait(a_full, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
+            const uint32_t a_tmem = tmem_base + TC_NACC * TC_BN;
+            const int KS = (p.n + 15) / 16;
+            const uint64_t bdesc0 = umma_desc_sw((uint32_t)__cvta_generic_to_shared(sRing), CW);
+            int slot = 0;
+            uint32_t phase = 0;
+            int s = 0;
+            uint32_t tph = 0;
+            for (int u = 0, t = 0; t < niter; u++, t += SEG_U) {
+                const int nt = min(SEG_U, niter - t);
+                mbar_spin_a(a_bfull + 8u * slot, phase);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                for (int i = 0; i < nt; i++) {
+                    if (t + i >= TC_NACC) mbar_spin_a(a_tempty + 8u * s, tph ^ 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
+                    for (int kb = 0; kb < KB && p.skip_epi != 3; kb++) {
+                        const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)(slot * SEG_U + i) * tile_bytes + kb * chunk_bytes) >> 4);
+                        const int ksn = min(CW / 16, KS - kb * (CW / 16));
+                        asm volatile(
+                            "{\n.reg .pred p, q, q1, q2, q3;\n.reg .b64 d1, d2, d3;\n.reg .b32 a1, a2, a3;\n"
+                            "elect.sync _|q, 0xffffffff;\n"
+                            "setp.ne.b32 p, %4, 0;\n"
+                            "setp.gt.and.s32 q1, %5, 1, q;\nsetp.gt.and.s32 q2, %5, 2, q;\nsetp.gt.and.s32 q3, %5, 3, q;\n"
+                            "add.s64 d1, %2, 2;\nadd.s64 d2, %2, 4;\nadd.s64 d3, %2, 6;\n"
+                            "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+                            "@q1 tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
+                            "@q2 tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
+                            "@q3 tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n}" ::"r"(tmem_d),
+                            "r"(a_tmem + (uint32_t)(kb * (CW / 2))), "l"(bdesc), "r"(TC_IDESC), "r"(kb ? 1u : 0u), "r"(ksn)
+                            : "memory");
+                    }
+                    asm volatile(
+                        "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+                            a_tfull + 8u * s)
+                        : "memory");
+                    if (++s == TC_NACC) {
+                        s = 0;
+                        tph ^= 1u;
+                    }
+                }
+                // the unit's slot is free in every CTA of the cluster once these MMAs are done
+                asm volatile(
+                    "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+                    "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                    " [%0], %1;\n}" ::"r"(a_bempty + 8u * slot),
+                    "h"(cmask)
+                    : "memory");
+                if (++slot == NSU) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (ntile > 0) {
             // ring of tile slots: a slot holds a whole B tile (KB K-chunks);
@@ -350,7 +468,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
                 // side data of this tile (row constants + half-tile extremes): one copy
                 const int rs = t % TC_RS;
-                if (!SEG && t >= TC_RS) mbar_wait_a(a_rempty + 8u * rs, (unsigned)(((t / TC_RS) - 1) & 1));
+                if (!SEG && t >= TC_RS) mbar_spin_a(a_rempty + 8u * rs, (unsigned)(((t / TC_RS) - 1) & 1));
                 if (!SEG) {
                     const uint32_t dst = slot0 + (uint32_t)(rs * sizeof(TileSlot));
                     const uint32_t bar = rfull0 + (uint32_t)rs * 8;
@@ -362,7 +480,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                         "r"(bar), "l"(p.side + tile * TC_SIDE), "n"((int)sizeof(TileSlot))
                         : "memory");
                 }
-                if (t >= NS) mbar_wait_a(a_bempty + 8u * slot, phase ^ 1u);
+                if (t >= NS) mbar_spin_a(a_bempty + 8u * slot, phase ^ 1u);
                 const uint32_t bar = full0 + (uint32_t)slot * 8;
                 if (p.skip_epi == 4 && t >= NS) {  // diagnostics: MMA-only pipeline (stale B tiles)
                     asm volatile("{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
@@ -425,8 +543,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             uint32_t phase = 0;
             for (int t = 0; t < niter; t++) {
                 const int s = t % TC_NACC;
-                if (t >= TC_NACC) mbar_wait_a(a_tempty + 8u * s, (unsigned)(((t / TC_NACC) - 1) & 1));
-                mbar_wait_a(a_bfull + 8u * slot, phase);
+                if (t >= TC_NACC) mbar_spin_a(a_tempty + 8u * s, (unsigned)(((t / TC_NACC) - 1) & 1));
+                mbar_spin_a(a_bfull + 8u * slot, phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tmem_d = tmem_base + (uint32_t)(s * TC_BN);
                 for (int kb = 0; kb < KB && p.skip_epi != 3; kb++) {  // 3: diagnostics, loads only
@@ -561,24 +679,29 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // issue-bound, every instruction per tile counts x EPW warps)
             const uint32_t tbase = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(h * COLS);
             const int64_t rbase = (p.tile0 + t_begin) * TC_BN + h * COLS;  // nwarm = 0: tile t = t_begin + t
-            uint32_t s = 0, ph = 0;
-            unsigned gave_up = 0;  // another thread of this query gave up (read every 16th tile, used at the next)
-            for (int t = 0; t < niter; t++) {
-                if ((t & 15) == 0 && qvalid) {
-                    if (gave_up) thr = __int_as_float(0x7f800000);
-                    gave_up = *(volatile const unsigned int *)(p.seg_flag + ql);
+            // (a one-tile register prefetch -- tile t + 1's accumulator loaded and
+            // released before tile t is examined -- measured 7% slower on C4)
+            uint32_t fs = 0, fph = 0;  // next accumulator to fetch, its phase
+            auto fetch = [&](uint32_t(&v)[COLS]) {
+                const uint32_t sa = 8u * fs, taddr = tbase + fs * (uint32_t)TC_BN;
+                mbar_wait_a(a_tfull + sa, fph);
+                if (++fs == TC_NACC) {
+                    fs = 0;
+                    fph ^= 1u;
                 }
-                const uint32_t sa = 8u * s, taddr = tbase + s * (uint32_t)TC_BN;
-                if (++s == TC_NACC) s = 0;
-                mbar_wait_a(a_tfull + sa, ph);
-                if (s == 0) ph ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                uint32_t v[COLS];
 #pragma unroll
                 for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
                 tmem_wait_ld();
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 mbar_arrive_a(a_tempty + sa);
+            };
+            unsigned gave_up = 0;  // another thread of this query gave up (read every 16th tile, used at the next)
+            auto examine = [&](const uint32_t(&v)[COLS], int t) {
+                if ((t & 15) == 0 && qvalid) {
+                    if (gave_up) thr = __int_as_float(0x7f800000);
+                    gave_up = *(volatile const unsigned int *)(p.seg_flag + ql);
+                }
                 float mg[COLS / 16];
 #pragma unroll
                 for (int g = 0; g < COLS / 16; g++) {
@@ -593,7 +716,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 float mx = mg[0];
 #pragma unroll
                 for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
-                if (!__any_sync(0xffffffffu, mx >= thr)) continue;
+                if (!__any_sync(0xffffffffu, mx >= thr)) return;
                 const int64_t row0 = rbase + (int64_t)t * TC_BN;
                 const int64_t left = p.N - row0;
                 const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
@@ -635,6 +758,11 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
                 __syncwarp();
                 if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
+            };
+            for (int t = 0; t < niter; t++) {
+                uint32_t v[COLS];
+                fetch(v);
+                if (!diag_skip) examine(v, t);
             }
         } else
         for (int t = 0; t < niter; t++) {
