@@ -447,16 +447,24 @@ __global__ void proj_tighten_kernel(const uint64_t *__restrict__ keys, int k, co
 // one 8-lane group per candidate (scan.cu arithmetic, bit-identical
 // distances); candidates of queries the full filter answers are skipped, and
 // `only` (per block query, nullable) restricts to the flagged queries
+// (the range may come from the device: [*lo_dev, min(*hi_dev, cap)), no host round trip)
 template <int NT>
 __global__ void rescore_proj_kernel(const float *__restrict__ X, const uint32_t *__restrict__ row_id,
                                     const uint32_t *__restrict__ tcperm, const float *__restrict__ Qp,
                                     const int32_t *__restrict__ qmap, const uint2 *__restrict__ cand, int64_t nc,
+                                    const unsigned long long *__restrict__ lo_dev,
+                                    const unsigned long long *__restrict__ hi_dev, int64_t cap,
                                     const int32_t *__restrict__ hard, const int32_t *__restrict__ only, ScanOut out)
 {
     const int lane = threadIdx.x & 31, j = lane & 7;
     const unsigned gmask = 0xffu << (lane & 24);
     const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
-    for (int64_t gp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; gp < nc; gp += stride) {
+    int64_t g0 = 0;
+    if (hi_dev) {
+        g0 = (int64_t)*lo_dev;
+        nc = (int64_t)min((unsigned long long)cap, *hi_dev);
+    }
+    for (int64_t gp = g0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3); gp < nc; gp += stride) {
         const uint2 c = cand[gp];
         if (hard[c.x]) continue;
         const int q = qmap[c.x];
@@ -494,18 +502,23 @@ __global__ void proj_cser_kernel(const unsigned int *__restrict__ cnt, const int
 }
 
 // candidates [c0, c1) of the list; `hard` (per launch-local query) skips queries
+// c1 < 0: the range is [pw.done, the filter's count) on the device
 static int launch_rescore_proj(const Index &ix, ProjWork &pw, const float *Qp, const int32_t *only, ScanOut so,
                                cudaStream_t s, int64_t c0, int64_t c1, const int32_t *hard)
 {
-    const int64_t nc = c1 - c0;
-    if (pw.nq == 0 || nc <= 0) return OK;
-    const unsigned grid = (unsigned)std::min<int64_t>((nc * 8 + 255) / 256, (int64_t)num_sms() * 16);
+    const bool dev = c1 < 0;
+    const int64_t nc = dev ? 0 : c1 - c0;
+    if (pw.nq == 0 || (!dev && nc <= 0)) return OK;
+    const unsigned grid = dev ? (unsigned)(num_sms() * 16)
+                              : (unsigned)std::min<int64_t>((nc * 8 + 255) / 256, (int64_t)num_sms() * 16);
     ProfScope ps("proj_rescore", s, (double)nc * ix.n * 4);
-    const uint2 *cand = pw.cand.as<uint2>() + c0;
+    const uint2 *cand = pw.cand.as<uint2>() + (dev ? 0 : c0);
+    const unsigned long long *lo = dev ? pw.done.as<unsigned long long>() : nullptr;
+    const unsigned long long *hi = dev ? pw.cn.as<unsigned long long>() : nullptr;
     const int32_t *qm = pw.qidx.as<int32_t>();
     switch (ix.n) {
-    case 128: rescore_proj_kernel<128><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, hard, only, so); break;
-    case 256: rescore_proj_kernel<256><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, hard, only, so); break;
+    case 128: rescore_proj_kernel<128><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, lo, hi, pw.cap, hard, only, so); break;
+    case 256: rescore_proj_kernel<256><<<grid, 256, 0, s>>>(ix.X, ix.orig, ix.tcperm, Qp, qm, cand, nc, lo, hi, pw.cap, hard, only, so); break;
     default:
         set_error(ERR_USAGE, "series length " + std::to_string(ix.n) + " has no compiled projected rescore kernel");
         return ERR_USAGE;
@@ -531,6 +544,8 @@ static int phase_setup(const Index &ix, const float *Q, const std::vector<int32_
     SSB_CUDA(pw.hard.alloc(4 * (size_t)nq, s));
     SSB_CUDA(pw.cand.alloc(8 * (size_t)cap, s));
     SSB_CUDA(pw.cn.alloc(8, s));
+    SSB_CUDA(pw.done.alloc(8, s));
+    SSB_CUDA(cudaMemsetAsync(pw.done.p, 0, 8, s));
     SSB_CUDA(qb.alloc(2 * (size_t)nq_pad * PJ_DMAX, s));
     SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
     SSB_CUDA(qen.alloc(8 * (size_t)nq_pad, s));
@@ -564,19 +579,22 @@ static int phase_range(const Index &ix, const float *Q, uint64_t *thr, int k, Pr
                             ix.p_v2);
 }
 
-// Rescore the candidates [nc_done, current) of a phase (queries flagged so far
-// skipped), then tighten every query's bound to the k-th key found so far.
-static int phase_tighten(const Index &ix, ProjWork &pw, const float *qlay, int B, int k, ScanOut so, uint64_t *thr,
-                         int64_t *nc_done, cudaStream_t s)
+__global__ void proj_mark_done_kernel(const unsigned long long *__restrict__ cn, int64_t cap,
+                                      unsigned long long *__restrict__ done)
 {
-    unsigned long long hn = 0;
-    SSB_CUDA(cudaMemcpyAsync(&hn, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaStreamSynchronize(s));
-    const int64_t nc_now = std::min<int64_t>((int64_t)hn, pw.cap);
-    int rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, *nc_done, nc_now,
-                                 reinterpret_cast<const int32_t *>(pw.flag.p));
+    *done = min((unsigned long long)cap, *cn);
+}
+
+// Rescore the candidates the phase emitted since the last call (queries flagged
+// so far skipped; the range lives on the device: no host round trip), then
+// tighten every query's bound to the k-th key found so far.
+static int phase_tighten(const Index &ix, ProjWork &pw, const float *qlay, int B, int k, ScanOut so, uint64_t *thr,
+                         cudaStream_t s)
+{
+    int rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, 0, -1, reinterpret_cast<const int32_t *>(pw.flag.p));
     if (rc) return rc;
-    *nc_done = nc_now;
+    proj_mark_done_kernel<<<1, 1, 0, s>>>(pw.cn.as<unsigned long long>(), pw.cap, pw.done.as<unsigned long long>());
+    SSB_CHECK_LAUNCH();
     DevBuf pk, pt, pf;
     SSB_CUDA(pk.alloc(8 * (size_t)B * k, s));
     SSB_CUDA(pt.alloc(8 * (size_t)B, s));
@@ -654,10 +672,12 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
             SSB_CUDA(cudaMemcpyAsync(pw.flag.p, f0.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
         }
         for (int i = 0; i < nq; i++) total[i] = c0[i];
-        int64_t nc_done = 0;
-        rc = phase_tighten(ix, pw, qlay, B, k, so, thr, &nc_done, s);  // syncs: f0 may die after
+        rc = phase_tighten(ix, pw, qlay, B, k, so, thr, s);
         if (rc) return rc;
-        pw.nc = nc_done;
+        unsigned long long hn0 = 0;
+        SSB_CUDA(cudaMemcpyAsync(&hn0, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));  // f0 dies here
+        pw.nc = std::min<int64_t>((int64_t)hn0, pw.cap);
     }
 
     // ---- main phase: the remaining queries over the rest of the rows -----------
@@ -682,16 +702,17 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         int rc = phase_setup(ix, Q, live, cap, pw, qb, qn2, qen, gb, s);
         if (rc) return rc;
         const int parts = split > 1 ? split - 1 : 1;
-        int64_t nc_done = 0;
         for (int part = 0; part < parts; part++) {
             const int64_t lo = t0 + (tiles - t0) * part / parts, hi = t0 + (tiles - t0) * (part + 1) / parts;
             rc = phase_range(ix, Q, thr, k, pw, qb, qn2, qen, gb, lo, hi, seg_eff * (hi - lo) / tiles, s);
             if (rc) return rc;
             if (part + 1 < parts) {
-                rc = phase_tighten(ix, pw, qlay, B, k, so, thr, &nc_done, s);
+                rc = phase_tighten(ix, pw, qlay, B, k, so, thr, s);
                 if (rc) return rc;
             }
         }
+        unsigned long long done = 0;
+        SSB_CUDA(cudaMemcpyAsync(&done, pw.done.p, 8, cudaMemcpyDeviceToHost, s));
         std::vector<uint32_t> hc(nl), hf(nl);
         SSB_CUDA(cudaMemcpyAsync(hc.data(), pw.cnt.p, 4 * (size_t)nl, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(hf.data(), pw.flag.p, 4 * (size_t)nl, cudaMemcpyDeviceToHost, s));
@@ -707,7 +728,7 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         }
         SSB_CUDA(cudaMemcpyAsync(pw.hard.p, hh.data(), 4 * (size_t)nl, cudaMemcpyHostToDevice, s));
         // the last range's candidates (hard queries excluded)
-        rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, nc_done, pw.nc, pw.hard.as<int32_t>());
+        rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, (int64_t)done, pw.nc, pw.hard.as<int32_t>());
         if (rc) return rc;
         SSB_CUDA(cudaStreamSynchronize(s));  // hh dies here
     }

@@ -157,7 +157,7 @@ int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, 
                          uint32_t *qmax, cudaStream_t s);
 // K-proj (proj.cu)
 struct ProjWork {  // one phase: its queries, candidate list and counters
-    DevBuf qidx, cnt, flag, cand, cn, hard;
+    DevBuf qidx, cnt, flag, cand, cn, hard, done;
     int nq = 0;
     int64_t cap = 0, nc = 0;
 };

@@ -702,20 +702,21 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     if (gave_up) thr = __int_as_float(0x7f800000);
                     gave_up = *(volatile const unsigned int *)(p.seg_flag + ql);
                 }
+                // maxima of column triples (kept: a triple below the threshold
+                // needs no per-column test), then of the 16-column groups
+                float tri[COLS / 16][5];
                 float mg[COLS / 16];
 #pragma unroll
                 for (int g = 0; g < COLS / 16; g++) {
                     const float *vf = reinterpret_cast<const float *>(v + 16 * g);
-                    float a = fmax3f(vf[0], vf[1], vf[2]), b = fmax3f(vf[3], vf[4], vf[5]);
-                    float c = fmax3f(vf[6], vf[7], vf[8]), d = fmax3f(vf[9], vf[10], vf[11]);
-                    float e2 = fmax3f(vf[12], vf[13], vf[14]);
-                    a = fmax3f(a, b, c);
-                    d = fmax3f(d, e2, vf[15]);
-                    mg[g] = fmaxf(a, d);
+#pragma unroll
+                    for (int j = 0; j < 5; j++) tri[g][j] = fmax3f(vf[3 * j], vf[3 * j + 1], vf[3 * j + 2]);
+                    mg[g] = fmaxf(fmax3f(tri[g][0], tri[g][1], tri[g][2]), fmax3f(tri[g][3], tri[g][4], vf[15]));
                 }
                 float mx = mg[0];
 #pragma unroll
                 for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
+                if (p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: loads + max, no emission
                 if (!__any_sync(0xffffffffu, mx >= thr)) return;
                 const int64_t row0 = rbase + (int64_t)t * TC_BN;
                 const int64_t left = p.N - row0;
@@ -724,8 +725,15 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 for (int c0 = 0; c0 < COLS; c0 += 16) {
                     uint32_t emit = 0;
                     if (mg[c0 / 16] >= thr) {
+                        const float *vf = reinterpret_cast<const float *>(v + c0);
 #pragma unroll
-                        for (int i = 0; i < 16; i++) emit |= (__uint_as_float(v[c0 + i]) >= thr ? 1u : 0u) << i;
+                        for (int j = 0; j < 5; j++)
+                            if (tri[c0 / 16][j] >= thr) {
+                                if (vf[3 * j] >= thr) emit |= 1u << (3 * j);
+                                if (vf[3 * j + 1] >= thr) emit |= 2u << (3 * j);
+                                if (vf[3 * j + 2] >= thr) emit |= 4u << (3 * j);
+                            }
+                        if (vf[15] >= thr) emit |= 1u << 15;
                         emit &= (uint32_t)(valid >> c0) & 0xffffu;
                     }
                     if (emit) {
@@ -762,7 +770,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             for (int t = 0; t < niter; t++) {
                 uint32_t v[COLS];
                 fetch(v);
-                if (!diag_skip) examine(v, t);
+                if (!diag_skip && p.skip_epi != 5) examine(v, t);  // 5: diagnostics, TMEM loads only
             }
         } else
         for (int t = 0; t < niter; t++) {
