@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -49,8 +50,8 @@ namespace ssb {
 
 constexpr int PJ_DMAX = 64;     // operand columns (one 64-column K-chunk): coefficients + the norm split
 constexpr int PJ_COEF = PJ_DMAX - 2;  // projection coefficients
-constexpr int PJ_ROWS = 64;     // rows per projection tile
-constexpr int PJ_SAMPLE = 16384;  // rows of the energy sample
+constexpr int PJ_ROWS = 128;    // rows per projection tile
+constexpr int PJ_SAMPLE = 4096;  // rows of the energy sample
 
 // ---------------------------------------------------------------------------
 // build: sample covariance (float64, logical element order)
@@ -62,9 +63,11 @@ __global__ void proj_cov_kernel(const float *__restrict__ X, int64_t N, int n, c
     const int pa = pos[a];
     for (int b = threadIdx.x; b < n; b += blockDim.x) {
         const int pb = pos[b];
+        const int64_t stride = N / S;  // S <= N: every stride-th row
         double acc = 0.0;
+#pragma unroll 8
         for (int i = 0; i < S; i++) {
-            const float *x = X + ((int64_t)i * N / S) * n;
+            const float *x = X + (int64_t)i * stride * n;
             acc += (double)__ldg(x + pa) * (double)__ldg(x + pb);
         }
         C[(int64_t)a * n + b] = acc;
@@ -124,14 +127,15 @@ __global__ void max_bits_kernel(const float *__restrict__ v, int64_t N, unsigned
 
 // ---------------------------------------------------------------------------
 // z = P x for R rows, fused with the BF16 operand and its norms (the
-// to_bf16_norms_kernel formulas).  CTA = 64-row tiles (persistent), 256
-// threads = 16 row groups x 16 coefficient groups, 4 x 4 accumulators each;
-// P^T and the tile (transposed, padded) in shared memory.  Rows: src row
-// rows[r] (or r); pos (nullable) maps a physical position of the row to its
-// logical element (the inverse of the lane-transposed layout).
-// is_query: row-major BF16 output and query norms (QH, QL); otherwise the
-// tile-major pre-swizzled operand (CW = 64) and row norms (U, V).
-__global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict__ X, int64_t R, int n,
+// to_bf16_norms_kernel formulas).  CTA = 128-row tiles (persistent), 512
+// threads = 32 row groups x 16 coefficient groups, 4 rows x 4 coefficients
+// each (one CTA per SM: 16 warps hide the shared-memory latency).  P^T and
+// the tile (transposed, padded) in shared memory.  Rows: src row rows[r] (or
+// r); pos (nullable) maps a physical position of the row to its logical
+// element (the inverse of the lane-transposed layout).  is_query: row-major
+// BF16 output and query norms (QH, QL); otherwise the tile-major pre-swizzled
+// operand (CW = 64) and row norms (U, V).
+__global__ void __launch_bounds__(512) proj_rows_kernel(const float *__restrict__ X, int64_t R, int n,
                                                         const int32_t *__restrict__ pos,
                                                         const uint32_t *__restrict__ rows,
                                                         const float *__restrict__ P, int d, int is_query,
@@ -141,29 +145,43 @@ __global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict_
     extern __shared__ __align__(16) float pj_smem[];
     float *pt = pj_smem;                      // [n][PJ_DMAX]
     float *xs = pt + (size_t)n * PJ_DMAX;     // [n][PJ_ROWS + 1]
+    // rows stay in their physical element order in shared memory (coalesced,
+    // conflict-free fill); P's columns are permuted to match instead (the sum
+    // is over the same products, in another order: the error bound holds)
     for (int idx = threadIdx.x; idx < n * PJ_DMAX; idx += blockDim.x) {
-        const int j = idx / PJ_DMAX, i = idx % PJ_DMAX;
-        pt[idx] = i < d ? P[(int64_t)i * n + j] : 0.f;
+        const int k = idx / PJ_DMAX, i = idx % PJ_DMAX;
+        pt[idx] = i < d ? P[(int64_t)i * n + (pos ? pos[k] : k)] : 0.f;
     }
     const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;  // rows tr*4.., coefficients tc*4..
     for (int64_t t0 = (int64_t)blockIdx.x * PJ_ROWS; t0 < R; t0 += (int64_t)gridDim.x * PJ_ROWS) {
         __syncthreads();
-        // 16-byte loads in the rows' physical order, scattered to the logical
-        // element (ipos: physical -> logical position; null: identity)
-        const int n4 = n / 4;
-        for (int idx = threadIdx.x; idx < PJ_ROWS * n4; idx += blockDim.x) {
-            const int r = idx / n4, c4 = idx - r * n4;
-            const int64_t row = t0 + r;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < R) {
-                const int64_t src = rows ? (int64_t)rows[row] : row;
-                v = __ldg(reinterpret_cast<const float4 *>(X + src * n) + c4);
-            }
-            const float e4[4] = {v.x, v.y, v.z, v.w};
+        // 16-byte loads in the rows' physical order
+        // (8 loads in flight per thread before their stores: the rows are
+        // gathered through the K-tc permutation, one dependent load away)
+        const int n4 = n / 4, total = PJ_ROWS * n4;
+        for (int base = 0; base < total; base += 8 * (int)blockDim.x) {
+            float4 v[8];
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int j = pos ? pos[4 * c4 + e] : 4 * c4 + e;
-                xs[j * (PJ_ROWS + 1) + r] = e4[e];
+            for (int u = 0; u < 8; u++) {
+                const int idx = base + u * (int)blockDim.x + (int)threadIdx.x;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int r = idx / n4, c4 = idx - r * n4;
+                const int64_t row = t0 + r;
+                if (idx < total && row < R) {
+                    const int64_t src = rows ? (int64_t)__ldg(rows + row) : row;
+                    v[u] = __ldg(reinterpret_cast<const float4 *>(X + src * n) + c4);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int idx = base + u * (int)blockDim.x + (int)threadIdx.x;
+                if (idx >= total) continue;
+                const int r = idx / n4, c4 = idx - r * n4;
+                float *dst = xs + (4 * c4) * (PJ_ROWS + 1) + r;
+                dst[0] = v[u].x;
+                dst[PJ_ROWS + 1] = v[u].y;
+                dst[2 * (PJ_ROWS + 1)] = v[u].z;
+                dst[3 * (PJ_ROWS + 1)] = v[u].w;
             }
         }
         __syncthreads();
@@ -174,9 +192,10 @@ __global__ void __launch_bounds__(256) proj_rows_kernel(const float *__restrict_
             for (int c = 0; c < 4; c++) acc[r][c] = 0.f;
         const float *xr = xs + tr * 4;
         const float *pc = pt + tc * 4;
+#pragma unroll 4
         for (int j = 0; j < n; j++) {
-            const float4 p4 = *reinterpret_cast<const float4 *>(pc + j * PJ_DMAX);
-            const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+            const float4 pa = *reinterpret_cast<const float4 *>(pc + j * PJ_DMAX);
+            const float pv[4] = {pa.x, pa.y, pa.z, pa.w};
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 const float xv = xr[j * (PJ_ROWS + 1) + r];
@@ -253,7 +272,7 @@ static int launch_proj_rows(const float *X, int64_t R, int n, const int32_t *pos
     const int64_t tiles = (R + PJ_ROWS - 1) / PJ_ROWS;
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)num_sms());
     ProfScope ps(is_query ? "proj_queries" : "proj_rows", s, (double)R * n * 4 + (double)R * PJ_DMAX * 2);
-    proj_rows_kernel<<<grid, 256, smem, s>>>(X, R, n, pos, rows, P, d, is_query ? 1 : 0,
+    proj_rows_kernel<<<grid, 512, smem, s>>>(X, R, n, pos, rows, P, d, is_query ? 1 : 0,
                                              reinterpret_cast<__nv_bfloat16 *>(zb), zn2, zen);
     SSB_CHECK_LAUNCH();
     return OK;
@@ -279,6 +298,14 @@ int build_projection(Index &ix, cudaStream_t s)
 {
     if (!ix.Xb || !ix.xn2) return OK;
     if (const char *e = getenv("SSB_PROJ")) if (atoi(e) == 0) return OK;  // A/B: no projection operand
+    const bool trace = getenv("SSB_BUILD_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[ssb build]   projection: %-20s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     const int d = PJ_COEF;
     const int n = ix.n;
     if (n < 2 * PJ_DMAX || ix.N < 1) return OK;
@@ -311,6 +338,7 @@ int build_projection(Index &ix, cudaStream_t s)
     SSB_CUDA(cudaStreamSynchronize(s));
     double total = 0.0;
     for (int i = 0; i < n; i++) total += hdiag[i];  // trace
+    lap("sample energies");
     std::vector<int> order(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return energy[a] > energy[b]; });
@@ -354,6 +382,7 @@ int build_projection(Index &ix, cudaStream_t s)
     float xmax2f;
     std::memcpy(&xmax2f, &mbits, 4);
     const double xmax2 = (double)xmax2f * (1.0 + 1e-6);
+    lap("basis");
 
     SSB_CUDA(cudaMalloc(&ix.P, 4 * (size_t)d * n));
     SSB_CUDA(cudaMemcpyAsync(ix.P, hP.data(), 4 * (size_t)d * n, cudaMemcpyHostToDevice, s));
@@ -368,6 +397,7 @@ int build_projection(Index &ix, cudaStream_t s)
     int rc = launch_proj_rows(ix.X, ix.N, n, pos.as<int32_t>() + n, ix.tcperm, ix.P, d, false, ix.Zb, zn2.as<float>(),
                               zen.as<float2>(), s);
     if (rc) return rc;
+    lap("rows");
     rc = launch_tc_side(zn2.as<float>(), zen.as<float2>(), ix.N, ix.zside, s);
     if (rc) return rc;
     // the filter's projected mode bounds every row's error term by these maxima
