@@ -1209,6 +1209,7 @@ static int finish_tc_operands(Index &ix, cudaStream_t s)
 {
     if (!ix.Xb) return OK;
     RC(launch_tc_side(ix.xn2, ix.xen, ix.N, ix.tcside, s));
+    RC(tc_uniform_stats(ix.xn2, ix.xen, ix.N, &ix.tc_uni, ix.tc_uni_c, s));
     return build_projection(ix, s);  // K-proj operands (skipped when they would not prune)
 }
 

@@ -379,7 +379,8 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             SSB_CUDA(cudaMemsetAsync(tc_n.p, 0, 8, s));
             rc = launch_tc_filter(qb.p, qn2.as<float>(), qnrm.as<float2>(), nq, ix.Xb, ix.tc_cw, ix.tcside, ix.N, n, k,
                                   gb.as<unsigned int>(), tc_cand.as<uint2>(), tc_lb.as<float>(),
-                                  tc_n.as<unsigned long long>(), tc_cap, nullptr, s);
+                                  tc_n.as<unsigned long long>(), tc_cap, nullptr, s, nullptr, nullptr, 0, 0, 0, nullptr,
+                                  0.f, 0.f, ix.tc_uni ? ix.tc_uni_c : nullptr);
             if (rc) return rc;
             SSB_CUDA(cudaMemcpyAsync(&hn, tc_n.p, 8, cudaMemcpyDeviceToHost, s));
             SSB_CUDA(cudaStreamSynchronize(s));
@@ -620,7 +621,8 @@ static int tc_submit(const Index &ix, const float *Q, int B, int k, uint64_t *ou
     SSB_CUDA(cudaMemsetAsync(w.cn.p, 0, 8, s));
     rc = launch_tc_filter(w.qb.p, w.qn2.as<float>(), w.qnrm.as<float2>(), B, ix.Xb, ix.tc_cw, ix.tcside, ix.N, n, k,
                           w.gb.as<unsigned int>(), w.cand.as<uint2>(), w.clb.as<float>(), w.cn.as<unsigned long long>(),
-                          w.tc_cap, nullptr, s);
+                          w.tc_cap, nullptr, s, nullptr, nullptr, 0, 0, 0, nullptr, 0.f, 0.f,
+                          ix.tc_uni ? ix.tc_uni_c : nullptr);
     if (rc) return rc;
     // exact rescoring of the candidates whose lower bound is within the final bound
     SSB_CUDA(cudaMemsetAsync(w.cnt.p, 0, 4 * (size_t)B, s));

@@ -65,6 +65,10 @@ struct Index {
     float2 *xen = nullptr;   // per row (U, V): BF16 rounding-error norms (to_bf16_norms_kernel)
     uint32_t *tcperm = nullptr;  // K-tc row order -> leaf-order position (null: identity)
     float4 *tcside = nullptr; // per 128-row tile: the K-tc bound constants of its rows + half-tile extremes
+    // uniform row constants (z-normalised / unit-norm data): the index-wide
+    // (min a_l, max a_u, max 2gU, max 2gV) replace the side data (K-tc UNI mode)
+    bool tc_uni = false;
+    float tc_uni_c[4] = {0.f, 0.f, 0.f, 0.f};
     // projected lower-bound filter (K-proj, proj.cu): the d DCT-II coefficients
     // of every row (the d basis vectors of largest energy on a sample), BF16
     // tile-major in the K-tc row order, with their side records; null when the
@@ -147,10 +151,11 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s, unsigned int *seg_flag = nullptr, unsigned int *seg_cnt = nullptr, int seg_cap = 0,
                      int64_t tile_lo = 0, int64_t tile_hi = 0, const char *prof_name = nullptr, float seg_u = 0.f,
-                     float seg_v = 0.f);
+                     float seg_v = 0.f, const float *uni = nullptr);
 int64_t tc_bound_slots(int nq);
 int64_t tc_side_bytes(int64_t N);
 int launch_tc_side(const float *xn2, const float2 *en, int64_t N, float4 *side, cudaStream_t s);
+int tc_uniform_stats(const float *xn2, const float2 *en, int64_t N, bool *uniform, float uni[4], cudaStream_t s);
 int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n, bool layout, void *dst_bf16,
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
 int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,

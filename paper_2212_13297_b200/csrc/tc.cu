@@ -234,6 +234,7 @@ struct TcParams {
     unsigned int *seg_cnt;     // [nq] rows emitted
     int seg_cap;               // per thread
     float seg_u, seg_v;        // index-wide maxima of the rows' error constants (2gU, 2gV)
+    float uni_al, uni_au;      // UNI: index-wide min a_l, max a_u
 };
 
 // per-tile side data staged by the producer next to the B chunks (1-D bulk copies)
@@ -250,7 +251,9 @@ static_assert(sizeof(TileSlot) % 16 == 0, "bulk copies move 16-byte multiples");
 // KTOP > 0: keep the k smallest upper bounds per thread (k <= KTOP);
 // KTOP == 0: filter against the given bounds only; KTOP < 0: debug dump of S.
 // SEG (with KTOP == 0): projected mode, candidates into per-query segments.
-template <int KTOP, int EPW, bool SEG = false>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
+// UNI: uniform row constants (z-normalised / unit-norm rows): the index-wide
+// extremes (uni_al, uni_au, seg_u, seg_v) replace the per-tile side data.
+template <int KTOP, int EPW, bool SEG = false, bool UNI = false>  // EPW: epilogue warps (8: 64 columns per thread and tile, 16: 32)
 __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     tc_filter_kernel(const __grid_constant__ TcParams p)
 {
@@ -468,8 +471,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
                 // side data of this tile (row constants + half-tile extremes): one copy
                 const int rs = t % TC_RS;
-                if (!SEG && t >= TC_RS) mbar_spin_a(a_rempty + 8u * rs, (unsigned)(((t / TC_RS) - 1) & 1));
-                if (!SEG) {
+                if (!SEG && !UNI && t >= TC_RS) mbar_spin_a(a_rempty + 8u * rs, (unsigned)(((t / TC_RS) - 1) & 1));
+                if (!SEG && !UNI) {
                     const uint32_t dst = slot0 + (uint32_t)(rs * sizeof(TileSlot));
                     const uint32_t bar = rfull0 + (uint32_t)rs * 8;
                     asm volatile(
@@ -782,7 +785,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // list (a row counted twice would make the k-th bound invalid)
             const bool revisit = t >= nwarm && t < 2 * nwarm;
             const TileSlot &ts = slots[rs];
-            mbar_wait_a(a_rfull + 8u * rs, (unsigned)((t / TC_RS) & 1));
+            if (!UNI) mbar_wait_a(a_rfull + 8u * rs, (unsigned)((t / TC_RS) & 1));
             // the shared bound of this query (other CTAs tighten it): read every
             // 8th tile, used from the 8th tile after, so the L2 round trip never
             // sits on a tile's critical path
@@ -793,14 +796,15 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const float gcur = gseen;
             float bound = qvalid ? fminf(fminf(gcur, kth), bmax) : -1.f;
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
-            const float4 tcl = ts.tilec[2 * hh], tcu = ts.tilec[2 * hh + 1];
+            const float4 tcl = UNI ? make_float4(p.uni_al, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh];
+            const float4 tcu = UNI ? make_float4(p.uni_au, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh + 1];
             mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 mbar_arrive_a(a_tempty + 8u * s);
                 __syncwarp();
-                if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
+                if (!UNI && lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
@@ -854,9 +858,11 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 const int64_t left = p.N - row0;
                 const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
                 const float4 *rows = ts.rowc + h * COLS;
+                const float4 rcu = make_float4(p.uni_al, p.uni_au, p.seg_u, p.seg_v);  // UNI: every row's constants
+                auto row_c = [&](int c) { return UNI ? rcu : rows[c]; };
                 auto row_lb = [&](int c0, int i) {
                     const float sd = sel16(v + c0, i);
-                    const float4 rc = rows[c0 + i];
+                    const float4 rc = row_c(c0 + i);
                     return fmaf(m2f, sd, fmaf(-QH, rc.z, fmaf(-QL, rc.w, alpha_l + rc.x)));
                 };
 #pragma unroll
@@ -866,11 +872,12 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                         uint32_t work = 0;
 #pragma unroll
                         for (int i = 0; i < 16; i++) work |= (__uint_as_float(v[c0 + i]) >= thr_s ? 1u : 0u) << i;
+                        work &= (uint32_t)(valid >> c0) & 0xffffu;  // rows past N (UNI: their constants are not +inf)
                         while (work) {
                             const int i = __ffs(work) - 1;
                             work &= work - 1;
                             const float sd = sel16(v + c0, i);
-                            const float4 rc = rows[c0 + i];
+                            const float4 rc = row_c(c0 + i);
                             const float lb = fmaf(m2f, sd, fmaf(-QH, rc.z, fmaf(-QL, rc.w, alpha_l + rc.x)));
                             emit |= (emit_ok && lb <= bound ? 1u : 0u) << i;
                             if (lb < bound && (tighten || bk)) {  // ub >= lb: only then can ub tighten the bound
@@ -931,7 +938,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             }
             // the tile slot (row constants) is no longer read by this warp
             __syncwarp();
-            if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
+            if (!UNI && lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
             // drain the stage once it is half full (a tile adds at most 4 x 32 x 16
             // entries; reservations past its end already went to global memory)
             if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
@@ -1145,6 +1152,54 @@ __global__ void tc_side_kernel(const float *__restrict__ xn2, const float2 *__re
     }
 }
 
+// index-wide extremes of the row constants: min a_l, max a_u, max 2gU, max 2gV
+// (non-negative floats: min / max on the bits)
+__global__ void tc_uniform_kernel(const float *__restrict__ xn2, const float2 *__restrict__ en, int64_t N,
+                                  unsigned int *__restrict__ out)
+{
+    const float f = 1.f - 4e-6f, g = 1.f + 4e-6f, e = 2e-6f;
+    unsigned int mal = 0x7f800000u, mau = 0, mu = 0, mv = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 uv = en[i];
+        mal = min(mal, __float_as_uint(f * (1.f - e) * xn2[i]));
+        mau = max(mau, __float_as_uint(g * (1.f + e) * xn2[i]));
+        mu = max(mu, __float_as_uint(2.f * g * uv.x));
+        mv = max(mv, __float_as_uint(2.f * g * uv.y));
+    }
+    for (int off = 16; off; off >>= 1) {
+        mal = min(mal, __shfl_xor_sync(0xffffffffu, mal, off));
+        mau = max(mau, __shfl_xor_sync(0xffffffffu, mau, off));
+        mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, off));
+        mv = max(mv, __shfl_xor_sync(0xffffffffu, mv, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, mal);
+        atomicMax(out + 1, mau);
+        atomicMax(out + 2, mu);
+        atomicMax(out + 3, mv);
+    }
+}
+
+// Rows whose squared norms agree to 1e-4 (z-normalised: n, unit-norm: 1) lose
+// nothing to the index-wide extremes: the filter then runs without side data
+// (UNI mode).  `uni` = (min a_l, max a_u, max 2gU, max 2gV) -- the same
+// per-row formulas as tc_side_kernel, so the bounds stay valid.
+int tc_uniform_stats(const float *xn2, const float2 *en, int64_t N, bool *uniform, float uni[4], cudaStream_t s)
+{
+    *uniform = false;
+    if (N == 0 || getenv("SSB_TC_NOUNI")) return OK;  // A/B
+    DevBuf out;
+    SSB_CUDA(out.alloc(16, s));
+    const unsigned init[4] = {0x7f800000u, 0u, 0u, 0u};
+    SSB_CUDA(cudaMemcpyAsync(out.p, init, 16, cudaMemcpyHostToDevice, s));
+    tc_uniform_kernel<<<num_sms() * 2, 256, 0, s>>>(xn2, en, N, out.as<unsigned int>());
+    SSB_CHECK_LAUNCH();
+    SSB_CUDA(cudaMemcpyAsync(uni, out.p, 16, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    *uniform = std::isfinite(uni[0]) && uni[1] <= uni[0] * (1.f + 1e-4f) + 1e-30f;
+    return OK;
+}
+
 int launch_tc_side(const float *xn2, const float2 *en, int64_t N, float4 *side, cudaStream_t s)
 {
     const int64_t halves = (N + TC_BN - 1) / TC_BN * 2;
@@ -1168,8 +1223,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
                      const float4 *side, int64_t N, int n, int k, unsigned int *gbound,
                      uint2 *cand, float *cand_lb, unsigned long long *cand_n, int64_t cand_cap, float *dump,
                      cudaStream_t s, unsigned int *seg_flag, unsigned int *seg_cnt, int seg_cap, int64_t tile_lo, int64_t tile_hi, const char *prof_name, float seg_u,
-                     float seg_v)
+                     float seg_v, const float *uni)
 {
+    // uni (host, 4 floats; null: per-tile side data): min a_l, max a_u, max 2gU, max 2gV of the index
+    const bool un = uni != nullptr && !seg_cnt && !dump;
     const bool seg = seg_cnt != nullptr;
     SSB_REQUIRE(n % 8 == 0 && n <= 64 * TC_KMAX, "tensor-core filter needs n % 8 == 0 and n <= 256");
     SSB_REQUIRE(N < (1ll << 31), "too many rows for the tensor-core filter");
@@ -1225,8 +1282,10 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.seg_flag = seg_flag;
     p.seg_cnt = seg_cnt;
     p.seg_cap = seg_cap;  // per query here; per thread below, once the grid is known
-    p.seg_u = seg_u;
-    p.seg_v = seg_v;
+    p.seg_u = un ? uni[2] : seg_u;
+    p.seg_v = un ? uni[3] : seg_v;
+    p.uni_al = un ? uni[0] : 0.f;
+    p.uni_au = un ? uni[1] : 0.f;
     // bucket-bound refresh period: every 8 tiles; every 32 for k > 32, where a
     // refresh reads k buckets per thread (C4, k = 100: 14.98 ms at 1965 MHz -> 14.37 ms
     // at a power-capped 1762 MHz)
@@ -1298,7 +1357,8 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
         return OK;
     };
     const bool nolist = getenv("SSB_TC_NOLIST") != nullptr;  // diagnostics: bucket bound only for k >= 2
-#define TC_GO(KT) (epw == 16 ? go(tc_filter_kernel<KT, 16>) : go(tc_filter_kernel<KT, 8>))
+#define TC_GO(KT) (un ? (epw == 16 ? go(tc_filter_kernel<KT, 16, false, true>) : go(tc_filter_kernel<KT, 8, false, true>)) \
+                     : (epw == 16 ? go(tc_filter_kernel<KT, 16>) : go(tc_filter_kernel<KT, 8>)))
     if (dump)
         rc = go(tc_filter_kernel<-1, 8>);
     else if (seg)
@@ -1316,7 +1376,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     else if (k <= 16)
         rc = TC_GO(16);
     else if (k <= 32)
-        rc = go(tc_filter_kernel<32, 8>);
+        rc = un ? go(tc_filter_kernel<32, 8, false, true>) : go(tc_filter_kernel<32, 8>);
     else
         rc = TC_GO(0);
 #undef TC_GO
@@ -1354,7 +1414,7 @@ int tc_dot_debug(const float *Q, int B, const float *X, int64_t N, int n, float 
     if (rc) return rc;
     rc = launch_tc_filter(qb.p, qn2.as<float>(), qnm.as<float2>(), B, xb.p, tcx_default_cw(n), side.as<float4>(), N, n,
                           1, gb.as<unsigned int>(), cand.as<uint2>(), nullptr, cn.as<unsigned long long>(), 0, S, s, nullptr,
-                          nullptr, 0, 0, 0, nullptr, 0.f, 0.f);
+                          nullptr, 0, 0, 0, nullptr, 0.f, 0.f, nullptr);
     if (rc) return rc;
     SSB_CUDA(cudaStreamSynchronize(s));
     return OK;
