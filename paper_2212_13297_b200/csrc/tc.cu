@@ -215,6 +215,7 @@ struct TcParams {
     int64_t cand_cap;
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
+    int unit;                  // SEG / UNI: tiles per bulk load (divides warm)
     int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
     int skip_epi;              // diagnostics (SSB_TC_DIAG): 1 epilogue only releases TMEM, 2 TMEM loads + max,
                                // 3 = 1 without MMAs (loads only), 4 = 1 without loads after the first ring (MMA only)
@@ -336,13 +337,17 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 
     // Producer and MMA roles run warp-wide (every value stays warp-uniform, in
     // uniform registers); one elected lane issues each TMA / tcgen05 instruction.
-    // Projected mode: tiles are small (16 KB), so the B loads go in units of
-    // SEG_U consecutive tiles (contiguous in the tile-major operand and in the
-    // ring: one bulk copy of 64 KB), the CTAs of a cluster taking whole units in
-    // turn (the per-tile half-tile copies cap the load stream at ~3.5 TB/s)
-    constexpr int SEG_U = 4;
+    // Without side data (SEG, UNI) the B loads go in units of p.unit
+    // consecutive tiles (contiguous in the tile-major operand and in the ring:
+    // one bulk copy of up to 64 KB), the CTAs of a cluster taking whole units
+    // in turn (per-tile half-tile copies of small tiles cap the load stream:
+    // K-proj's 16 KB tiles at ~3.5 TB/s, units of 4 reach 7.7 TB/s from L2)
+    // tiles per unit (SEG / UNI): a unit must not straddle the warm-up wrap, so
+    // a CTA whose warm-up count is not a multiple loads tile by tile (the CTAs
+    // of a cluster share the tile range: they agree)
+    const int SEG_U = (nwarm % p.unit == 0) ? p.unit : 1;
     const int NSU = NS / SEG_U;  // unit slots in the ring
-    if (SEG && warp == 0) {
+    if ((SEG || UNI) && warp == 0) {
         // ---------------- TMA producer (units) ----------------
         const uint32_t tile_bytes = (uint32_t)KB * chunk_bytes;
         const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sRing);
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 "r"(bytes)
                 : "memory");
             if (u % CS == rank) {
-                const unsigned char *src = p.xb + (size_t)tile_of(t) * tile_bytes;  // nwarm = 0: contiguous tiles
+                const unsigned char *src = p.xb + (size_t)tile_of(t) * tile_bytes;  // a unit never straddles the warm-up wrap
                 const uint32_t dst = ring + (uint32_t)slot * SEG_U * tile_bytes;
                 if (CS == 1)
                     asm volatile(
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 phase ^= 1u;
             }
         }
-    } else if (SEG && warp == 1) {
+    } else if ((SEG || UNI) && warp == 1) {
         // ---------------- MMA issuer (units) ----------------
         if (ntile > 0) {
             mbar_wait(a_full, 0);
@@ -1279,6 +1284,13 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     }
     p.k = k;
     p.warm = seg ? 0 : 8;  // fixed bounds: nothing to warm up
+    {   // load units (SEG / UNI): up to 64 KB, at least three in the ring
+        const int ns = (int)((int64_t)TC_NSLOT * TC_BN * 128 / ((int64_t)TC_BN * p.CW * 2 * p.KB));
+        p.unit = 1;
+        while (p.unit < 4 && ns / (2 * p.unit) >= 3 && (int64_t)2 * p.unit * TC_BN * p.CW * 2 * p.KB <= (64 << 10))
+            p.unit *= 2;
+        if (const char *e = getenv("SSB_TC_UNIT")) p.unit = std::max(1, std::min(4, atoi(e)));  // A/B (1, 2, 4)
+    }
     p.seg_flag = seg_flag;
     p.seg_cnt = seg_cnt;
     p.seg_cap = seg_cap;  // per query here; per thread below, once the grid is known
