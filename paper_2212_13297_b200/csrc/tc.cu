@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         }
         for (int i = 0; i < TC_NACC; i++) {
             mbar_init(&t_full[i], 1);
-            mbar_init(&t_empty[i], EPW * 32);
+            mbar_init(&t_empty[i], EPW);  // one arrival per epilogue warp (after a __syncwarp)
         }
         for (int i = 0; i < TC_RS; i++) {
             mbar_init(&r_full[i], 1);
@@ -702,7 +702,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
                 tmem_wait_ld();
                 asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive_a(a_tempty + sa);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(a_tempty + sa);
             };
             unsigned gave_up = 0;  // another thread of this query gave up (read every 16th tile, used at the next)
             auto examine = [&](const uint32_t(&v)[COLS], int t) {
@@ -807,7 +808,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive_a(a_tempty + 8u * s);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(a_tempty + 8u * s);
                 __syncwarp();
                 if (!UNI && lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
@@ -819,7 +821,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             tmem_wait_ld();
             // the accumulator is in registers: release it to the MMA warp right away
             asm volatile("tcgen05.fence::before_thread_sync;");
-            mbar_arrive_a(a_tempty + 8u * s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(a_tempty + 8u * s);
             if constexpr (KTOP < 0) {  // debug: dump S
 #pragma unroll
                 for (int i = 0; i < 64; i++)
