@@ -571,10 +571,23 @@ def run_ours(args, rank, world) -> int:
         engine = BruteForceEngine(X_dev, id_base=lo)
     batch = wl.batch
     merge_fn = getattr(engine, "merge_fn", None)
+    # NCCL ranks: the library's own communicator (ssb_comm: pack -> ncclAllGather
+    # -> K-merge in one call; the index shares its approximate bounds across the
+    # shards with ncclAllReduce(MIN) before filtering)
+    ssb_comm = None
+    if world > 1 and dev.cuda and args.backend == "nccl" and not TestEngine:
+        from paper_2212_13297_b200.distributed import Comm
+
+        ssb_comm = Comm(rank, world)
+        if isinstance(engine, IndexEngine):
+            ssb_comm.attach(engine.index)
+        comm["library_comm"] = "ssb_comm (NCCL all-gather merge + all-reduce(MIN) of the approximate bounds)"
 
     def merged(d2, ids, k):
         if world == 1:
             return d2, ids
+        if ssb_comm is not None:
+            return ssb_comm.merge(d2, ids, k)
         return merge_topk(d2, ids, k, merge_fn=merge_fn)
 
     # every call of a step through one multi-call (one host round trip per step

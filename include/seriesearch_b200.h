@@ -209,6 +209,27 @@ int ssb_query_multi(const ssb_index *index, int32_t ncalls, const float *const *
 int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float *out_d2,
                    int64_t *out_id, void *stream);
 
+/* Row-shard communicator (the reference is single-node and
+ * has none): one process per GPU, NCCL inside (libnccl.so.2, loaded on first
+ * use).  Rank 0 creates the id (SSB_COMM_ID_BYTES opaque bytes) and the caller
+ * broadcasts it (e.g. over torch.distributed); every rank then calls
+ * ssb_comm_init with it.  Errors: nccl (5). */
+#define SSB_COMM_ID_BYTES 128
+typedef struct ssb_comm ssb_comm;
+int ssb_comm_unique_id(uint8_t *id);
+int ssb_comm_init(int32_t nranks, int32_t rank, const uint8_t *id, ssb_comm **out);
+int ssb_comm_free(ssb_comm *comm);
+/* The shard merge in one call: this rank's B x k (d2, id) answers (device)
+ * packed into keys, ncclAllGather'd, K-merged -> the global B x k answers on
+ * every rank (out_d2 / out_id device; ids global, < 2^32). */
+int ssb_comm_merge_topk(ssb_comm *comm, const float *d2, const int64_t *ids, int32_t B, int32_t k,
+                        float *out_d2, int64_t *out_id, void *stream);
+/* Attach a communicator to a shard's index (null: detach): each query block
+ * then all-reduces (MIN) its approximate-phase bounds across the shards before
+ * filtering, and routes rank-independently (every rank calls ssb_query /
+ * ssb_query_multi with the same query blocks). */
+int ssb_index_set_comm(ssb_index *index, ssb_comm *comm);
+
 /* Merge keys of count (d2, id) results (device arrays, e.g. one shard's B x k
  * answers): key = (float bits of d2 << 32) | id, id < 0 -> UINT64_MAX (empty).
  * The packing step before the all-gather of SURVEY 8e; ids must fit in 32 bits. */

@@ -53,6 +53,11 @@ _SIGS = {
     "ssb_lb_sax": [P, P, I64, P, P, I32, P, P],
     "ssb_merge_topk": [P, I32, I32, I32, P, P, P],
     "ssb_pack_keys": [P, P, I64, P, P],
+    "ssb_comm_unique_id": [P],
+    "ssb_comm_init": [I32, I32, P, P],
+    "ssb_comm_free": [P],
+    "ssb_comm_merge_topk": [P, P, P, I32, I32, P, P, P],
+    "ssb_index_set_comm": [P, P],
     "ssb_ingest_file": [ctypes.c_char_p, I64, I64, I32, P, I64, I32, P, P],
     "ssb_generate": [I32, I64, I64, I32, ctypes.c_uint64, P, P],
 }

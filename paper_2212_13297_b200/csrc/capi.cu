@@ -415,6 +415,38 @@ int ssb_merge_topk(const uint64_t *keys, int32_t B, int32_t m, int32_t k, float 
     return merge_topk(keys, B, m, k, out_d2, out_id, (cudaStream_t)stream);
 }
 
+int ssb_comm_unique_id(uint8_t *id)
+{
+    SSB_REQUIRE(id, "null argument");
+    return comm_unique_id(id);
+}
+
+int ssb_comm_init(int32_t nranks, int32_t rank, const uint8_t *id, ssb_comm **out)
+{
+    SSB_REQUIRE(id && out, "null argument");
+    void *c = nullptr;
+    const int rc = comm_init(nranks, rank, id, &c);
+    if (rc) return rc;
+    *out = reinterpret_cast<ssb_comm *>(c);
+    return OK;
+}
+
+int ssb_comm_free(ssb_comm *comm) { return comm_free(comm); }
+
+int ssb_comm_merge_topk(ssb_comm *comm, const float *d2, const int64_t *ids, int32_t B, int32_t k, float *out_d2,
+                        int64_t *out_id, void *stream)
+{
+    SSB_REQUIRE(comm && d2 && ids && out_d2 && out_id, "null argument");
+    return comm_merge_topk(comm, d2, ids, B, k, out_d2, out_id, (cudaStream_t)stream);
+}
+
+int ssb_index_set_comm(ssb_index *index, ssb_comm *comm)
+{
+    SSB_REQUIRE(index, "null argument");
+    index->ix->comm = comm;
+    return OK;
+}
+
 int ssb_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, void *stream)
 {
     SSB_REQUIRE(count >= 0, "count must be >= 0");

@@ -150,6 +150,8 @@ static bool tc_all_for(const Index &ixc, const QueryCfg &qc, int k, int B)
     if (!ixc.Xb || k > TC_KTOP_MAX) return false;
     if (qc.route == 2) return true;
     if (qc.route != 0) return false;
+    // sharded: every rank must reach the bound all-reduce (the index stages)
+    if (comm_nranks(ixc.comm) > 1) return false;
     if (const char *e = getenv("SSB_AUTO_LEAN")) return atoi(e) != 0;
     const int G = std::min(B, 256);  // queries sharing one filter pass
     const double tc_ns = (double)ixc.N * IX_NS_TC_ROW * ixc.n / 256.0 / (double)G;
@@ -205,6 +207,7 @@ static void observe_route(const Index &ixc, double kept_frac, double surv_per_ke
 // host round trip (query_batch's direct path): the CUDA-graph candidates
 static bool small_block_ok(const Index &ix, const QueryCfg &qc, int B)
 {
+    if (comm_nranks(ix.comm) > 1) return false;  // the replayed graph holds no collective
     int mode = ix.Xb ? qc.route : 1;
     if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= (double)ix.N * IX_NS_TC_ROW) mode = 1;
     return mode == 1 && B <= 64 && (int64_t)B * (ix.N / 512 + ix.L + 1) <= (256 << 10);
@@ -227,6 +230,9 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= tc_group_ns) mode = 1;
     IxWork w;
     int rc = ix_front(ix, qc, Q, B, k, mode, want, w, s);
+    if (rc) return rc;
+    // row shards: every query's bound becomes the minimum over the shards
+    rc = comm_min_bounds(ix.comm, w.thr.as<uint64_t>(), B, s);
     if (rc) return rc;
     // candidate keys per query: generous (bound tightening makes an overflow
     // cost one more round, not an error), at most 2 GB per block

@@ -97,6 +97,10 @@ struct Index {
     // K-proj: fraction of the queries sent to it whose segment overflowed (the
     // full filter answered them), over recent blocks (< 0: none observed)
     double proj_hard_ema = -1.0;
+    // row-shard communicator (comm.cu; null: single GPU): every query block
+    // all-reduces its approximate bounds (MIN) across the shards, and the
+    // routing stays rank-independent (no lean batches, no graph replays)
+    void *comm = nullptr;
     ~Index();
 };
 
@@ -120,6 +124,15 @@ constexpr double IX_NS_IX_ROW = 0.03;
 // survivor at n = 256 (the rows read before abandonment; scaled by n / 256)
 constexpr double IX_NS_WORD = 0.01;
 constexpr double IX_NS_SURVIVOR = 0.5;
+// row-shard communicator (comm.cu)
+int comm_unique_id(uint8_t *id);
+int comm_init(int nranks, int rank, const uint8_t *id, void **out);
+int comm_free(void *comm);
+int comm_nranks(const void *comm);
+int comm_merge_topk(void *comm, const float *d2, const int64_t *ids, int B, int k, float *out_d2, int64_t *out_id,
+                    cudaStream_t s);
+int comm_min_bounds(const void *comm, uint64_t *thr, int B, cudaStream_t s);
+
 // K-proj (proj.cu): a pass over the d-coefficient operand costs IX_NS_PROJ_FACTOR
 // x d/n of the full filter's pass (the epilogue's per-pair work does not shrink
 // with d); the index stages that supply its bounds cost IX_NS_STAGES_Q per query
@@ -160,6 +173,15 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
                          float *n2, float2 *en, bool is_query, cudaStream_t s);
 int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, void *qb, float *qn2, float2 *qen,
                          uint32_t *qmax, cudaStream_t s);
+// row-shard communicator (comm.cu)
+int comm_unique_id(uint8_t *id);
+int comm_init(int nranks, int rank, const uint8_t *id, void **out);
+int comm_free(void *comm);
+int comm_nranks(const void *comm);
+int comm_merge_topk(void *comm, const float *d2, const int64_t *ids, int B, int k, float *out_d2, int64_t *out_id,
+                    cudaStream_t s);
+int comm_min_bounds(const void *comm, uint64_t *thr, int B, cudaStream_t s);
+
 // K-proj (proj.cu)
 struct ProjWork {  // one phase: its queries, candidate list and counters
     DevBuf qidx, cnt, flag, cand, cn, hard, done;

@@ -216,6 +216,7 @@ struct TcParams {
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
     int unit;                  // SEG / UNI: tiles per bulk load (divides warm)
+    int spin_epi;              // epilogue warps spin on the accumulator barrier (A/B; default: suspend)
     int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
     int skip_epi;              // diagnostics (SSB_TC_DIAG): 1 epilogue only releases TMEM, 2 TMEM loads + max,
                                // 3 = 1 without MMAs (loads only), 4 = 1 without loads after the first ring (MMA only)
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             uint32_t fs = 0, fph = 0;  // next accumulator to fetch, its phase
             auto fetch = [&](uint32_t(&v)[COLS]) {
                 const uint32_t sa = 8u * fs, taddr = tbase + fs * (uint32_t)TC_BN;
-                mbar_wait_a(a_tfull + sa, fph);
+                if (p.spin_epi) mbar_spin_a(a_tfull + sa, fph); else mbar_wait_a(a_tfull + sa, fph);
                 if (++fs == TC_NACC) {
                     fs = 0;
                     fph ^= 1u;
@@ -804,7 +805,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
             const float4 tcl = UNI ? make_float4(p.uni_al, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh];
             const float4 tcu = UNI ? make_float4(p.uni_au, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh + 1];
-            mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
+            if (p.spin_epi)
+                mbar_spin_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
+            else
+                mbar_wait_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (diag_skip) {
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1287,6 +1291,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     }
     p.k = k;
     p.warm = seg ? 0 : 8;  // fixed bounds: nothing to warm up
+    p.spin_epi = getenv("SSB_TC_SPIN") ? atoi(getenv("SSB_TC_SPIN")) : 0;
     {   // load units (SEG / UNI): up to 64 KB, at least three in the ring
         const int ns = (int)((int64_t)TC_NSLOT * TC_BN * 128 / ((int64_t)TC_BN * p.CW * 2 * p.KB));
         p.unit = 1;

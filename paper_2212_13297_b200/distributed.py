@@ -115,6 +115,64 @@ def merge_topk(d2, ids, k: int, group=None, merge_fn=None):
     return (merge_fn or merge_device)(all_keys, k)
 
 
+class Comm:
+    """The library's row-shard communicator (``ssb_comm``: NCCL inside the C
+    ABI).  Rank 0 creates the NCCL id and it is broadcast over the default
+    torch.distributed group; every rank then joins.  ``merge`` is the whole
+    shard merge in one library call (pack -> ncclAllGather -> K-merge), and
+    ``attach`` hands the communicator to this rank's index, whose query blocks
+    then all-reduce (MIN) their approximate bounds across the shards."""
+
+    ID_BYTES = 128
+
+    def __init__(self, rank: int | None = None, world: int | None = None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self._lib = _lib
+        rank = dist.get_rank() if rank is None else rank
+        world = dist.get_world_size() if world is None else world
+        uid = (ctypes.c_uint8 * self.ID_BYTES)()
+        if rank == 0:
+            _lib.call("ssb_comm_unique_id", uid)
+        if world > 1:
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                             device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.broadcast(t, 0)
+            uid = (ctypes.c_uint8 * self.ID_BYTES)(*t.cpu().tolist())
+        self.handle = ctypes.c_void_p()
+        _lib.call("ssb_comm_init", world, rank, uid, ctypes.byref(self.handle))
+        self.rank, self.world = rank, world
+
+    def merge(self, d2, ids, k: int):
+        """Global (B, k) answers from this rank's (B, k) CUDA tensors."""
+        import torch
+
+        from ._device import ptr, stream_handle
+
+        d2c, idc = d2.contiguous(), ids.contiguous()
+        B = d2c.shape[0]
+        out_d2 = torch.empty((B, k), dtype=torch.float32, device=d2c.device)
+        out_id = torch.empty((B, k), dtype=torch.int64, device=d2c.device)
+        self._lib.call("ssb_comm_merge_topk", self.handle, ptr(d2c), ptr(idc), B, k, ptr(out_d2), ptr(out_id),
+                       stream_handle())
+        return out_d2, out_id
+
+    def attach(self, index):
+        """Share the approximate bounds of ``index``'s query blocks across the shards."""
+        si = index.index if hasattr(index, "index") else index
+        self._lib.call("ssb_index_set_comm", si.handle, self.handle)
+
+    def close(self):
+        if self.handle:
+            self._lib.call("ssb_comm_free", self.handle)
+            self.handle = None
+
+
 class ShardedIndex:
     """This rank's shard of a row-sharded index (build + query + merge)."""
 
