@@ -578,10 +578,14 @@ def run_ours(args, rank, world) -> int:
     if world > 1 and dev.cuda and args.backend == "nccl" and not TestEngine:
         from paper_2212_13297_b200.distributed import Comm
 
-        ssb_comm = Comm(rank, world)
-        if isinstance(engine, IndexEngine):
-            ssb_comm.attach(engine.index)
-        comm["library_comm"] = "ssb_comm (NCCL all-gather merge + all-reduce(MIN) of the approximate bounds)"
+        try:
+            ssb_comm = Comm(rank, world)
+        except Exception as e:  # the torch.distributed merge still works: report, carry on
+            comm["library_comm"] = f"unavailable ({e}); torch.distributed all-gather + K-merge"
+        else:
+            if isinstance(engine, IndexEngine):
+                ssb_comm.attach(engine.index)
+            comm["library_comm"] = "ssb_comm (NCCL all-gather merge + all-reduce(MIN) of the approximate bounds)"
 
     def merged(d2, ids, k):
         if world == 1:
