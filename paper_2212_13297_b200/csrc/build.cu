@@ -859,7 +859,7 @@ struct FinalizeArgs {
     uint8_t *words;         // N x 16 (null: skip)
     const double *bp;       // 255 breakpoints
     uint32_t *inv;          // source row -> position (null: skip)
-    __nv_bfloat16 *Xb;      // K-tc operand (null: skip)
+    tc_op_t *Xb;            // K-tc operand (null: skip)
     int cw;                 // its K-chunk width (layout.cuh tcx_*)
     float *xn2;
     float2 *xen;
@@ -934,18 +934,18 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
 #pragma unroll
             for (int k = 0; k < 4; k++) amx = fmaxf(amx, fabsf(v[k]));
             if (a.Xb) {
-                __nv_bfloat16 b[4];
+                tc_op_t b[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    b[k] = __float2bfloat16_rn(v[k]);
-                    const double vb = (double)__bfloat162float(b[k]), dv = (double)v[k] - vb;  // exact
+                    b[k] = tc_op(v[k]);
+                    const double vb = (double)tc_op_f(b[k]), dv = (double)v[k] - vb;  // exact
                     acc += (double)v[k] * (double)v[k];
                     hh += vb * vb;
                     ll += dv * dv;
                 }
                 uint2 pk;
-                pk.x = (uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16);
-                pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
+                pk.x = tc_op_pack(b[0], b[1]);
+                pk.y = tc_op_pack(b[2], b[3]);
                 *reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(a.Xb) + tcx_offset(h, 4 * c, n, a.cw)) = pk;
             }
         };
@@ -1228,7 +1228,7 @@ static int finalize_rows(Index &ix, const float *src, const uint32_t *perm, bool
     fa.words = want_words ? ix.words : nullptr;
     fa.bp = ix.bp;
     fa.inv = perm ? ix.inv : nullptr;
-    fa.Xb = reinterpret_cast<__nv_bfloat16 *>(ix.Xb);
+    fa.Xb = reinterpret_cast<tc_op_t *>(ix.Xb);
     fa.cw = ix.tc_cw;
     fa.xn2 = ix.xn2;
     fa.xen = ix.xen;

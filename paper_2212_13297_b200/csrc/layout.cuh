@@ -13,6 +13,8 @@
 // all reported values are computed on the logical (reference) element order.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "ssb_common.cuh"
 
 namespace ssb {
@@ -206,6 +208,19 @@ __device__ __forceinline__ void lay_load_q(const float *__restrict__ q, float (&
 {
     lay_load_q_block<0, NT, NT / 8>(q, qv, j);
 }
+
+// ---------------------------------------------------------------------------
+// K-tc / K-proj operand element: FP16 (an 11-bit significand: the certified
+// dot-product interval is 8x tighter than with BF16's 8 bits, and tcgen05
+// kind::f16 runs both at the same rate).  Values saturate at +-65504; the
+// exactly computed residual norms then carry the difference, so the interval
+// stays valid (only looser) for data outside the FP16 range.
+typedef __half tc_op_t;
+__device__ __forceinline__ tc_op_t tc_op(float v) { return __float2half_rn(fminf(fmaxf(v, -65504.f), 65504.f)); }
+__device__ __forceinline__ tc_op_t tc_op_d(double v) { return __double2half(fmin(fmax(v, -65504.0), 65504.0)); }
+__device__ __forceinline__ float tc_op_f(tc_op_t h) { return __half2float(h); }
+__device__ __forceinline__ uint32_t tc_op_bits(tc_op_t h) { return (uint32_t)__half_as_ushort(h); }
+__device__ __forceinline__ uint32_t tc_op_pack(tc_op_t a, tc_op_t b) { return tc_op_bits(a) | (tc_op_bits(b) << 16); }
 
 // ---------------------------------------------------------------------------
 // K-tc operand layout ("tile-major, pre-swizzled").  The BF16 rows are stored

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(512) proj_rows_kernel(const float *__restrict_
                                                         const int32_t *__restrict__ pos,
                                                         const uint32_t *__restrict__ rows,
                                                         const float *__restrict__ P, int d, int is_query,
-                                                        __nv_bfloat16 *__restrict__ zb, float *__restrict__ zn2,
+                                                        tc_op_t *__restrict__ zb, float *__restrict__ zn2,
                                                         float2 *__restrict__ zen)
 {
     extern __shared__ __align__(16) float pj_smem[];
@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(512) proj_rows_kernel(const float *__restrict_
         for (int r = 0; r < 4; r++) {
             const int64_t row = t0 + tr * 4 + r;
             double a2 = 0.0, hh = 0.0, ll = 0.0;  // over the coefficients (acc is 0 past them)
-            __nv_bfloat16 b[4];
+            tc_op_t b[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                b[c] = __float2bfloat16_rn(acc[r][c]);
-                const double v = acc[r][c], h = (double)__bfloat162float(b[c]);
+                b[c] = tc_op(acc[r][c]);
+                const double v = acc[r][c], h = (double)tc_op_f(b[c]);
                 a2 += v * v;
                 hh += h * h;
                 ll += (v - h) * (v - h);
@@ -227,16 +227,15 @@ __global__ void __launch_bounds__(512) proj_rows_kernel(const float *__restrict_
                 ll += __shfl_xor_sync(0xffffffffu, ll, off);
             }
             const double half = -0.5 * (double)__double2float_rn(a2);  // -(the zn2 the side data would hold) / 2
-            const __nv_bfloat16 hi = __double2bfloat16(half);
-            const __nv_bfloat16 lo = __double2bfloat16(half - (double)__bfloat162float(hi));
-            const double h2 = (double)__bfloat162float(hi), l2 = (double)__bfloat162float(lo);
+            const tc_op_t hi = tc_op_d(half);  // |half| <= 60000 (build_projection's range check)
+            const tc_op_t lo = tc_op_d(half - (double)tc_op_f(hi));
+            const double h2 = (double)tc_op_f(hi), l2 = (double)tc_op_f(lo);
             if (tc == 15) {
-                b[2] = is_query ? __float2bfloat16_rn(1.f) : hi;
-                b[3] = is_query ? __float2bfloat16_rn(1.f) : lo;
+                b[2] = is_query ? tc_op(1.f) : hi;
+                b[3] = is_query ? tc_op(1.f) : lo;
             }
             if (row >= R) continue;
-            const uint2 v2 = make_uint2((uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16),
-                                        (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16));
+            const uint2 v2 = make_uint2(tc_op_pack(b[0], b[1]), tc_op_pack(b[2], b[3]));
             if (is_query)
                 *reinterpret_cast<uint2 *>(zb + row * PJ_DMAX + tc * 4) = v2;
             else
@@ -273,7 +272,7 @@ static int launch_proj_rows(const float *X, int64_t R, int n, const int32_t *pos
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)num_sms());
     ProfScope ps(is_query ? "proj_queries" : "proj_rows", s, (double)R * n * 4 + (double)R * PJ_DMAX * 2);
     proj_rows_kernel<<<grid, 512, smem, s>>>(X, R, n, pos, rows, P, d, is_query ? 1 : 0,
-                                             reinterpret_cast<__nv_bfloat16 *>(zb), zn2, zen);
+                                             reinterpret_cast<tc_op_t *>(zb), zn2, zen);
     SSB_CHECK_LAUNCH();
     return OK;
 }
@@ -383,6 +382,13 @@ int build_projection(Index &ix, cudaStream_t s)
     std::memcpy(&xmax2f, &mbits, 4);
     const double xmax2 = (double)xmax2f * (1.0 + 1e-6);
     lap("basis");
+    // the folded -||zx||^2 / 2 must fit the FP16 operand (two-term split,
+    // |hi| <= 65504): rows far from the origin (far-offset data) keep the full
+    // filter only
+    if (lam * xmax2 / 2.0 > 60000.0) {
+        if (trace) fprintf(stderr, "[ssb build] projection: row norms past the FP16 range -> off\n");
+        return OK;
+    }
 
     SSB_CUDA(cudaMalloc(&ix.P, 4 * (size_t)d * n));
     SSB_CUDA(cudaMemcpyAsync(ix.P, hP.data(), 4 * (size_t)d * n, cudaMemcpyHostToDevice, s));

@@ -59,10 +59,10 @@ constexpr int TC_NSLOT = 12;         // B pipeline depth in 16 KB units (192 KB)
 constexpr int TC_NBAR = 24;          // tile-slot barriers: up to 192 KB / 8 KB tiles
 constexpr int TC_KTOP = 32;   // in-register top-k of upper bounds for k <= 32; larger k: buckets only
 
-// tcgen05 instruction descriptor: F32 accumulate, BF16 A/B, K-major both,
-// N = 128 (>>3 = 16 at bit 17), M = 128 (>>4 = 8 at bit 24)
-constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
-                              ((uint32_t)(TC_BM >> 4) << 24);
+// tcgen05 instruction descriptor: F32 accumulate (bit 4), FP16 A/B (atype /
+// btype 0 at bits 7 / 10; BF16 would be 1), K-major both, N = 128 (>>3 = 16 at
+// bit 17), M = 128 (>>4 = 8 at bit 24)
+constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ uint64_t umma_desc_sw(uint32_t smem_addr, int cw)
 {
@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 // Rows get en = (U, V), queries en = (QH, QL), all rounded up (float64 sums with
 // a relative margin, then float32 RU).
 __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_t *__restrict__ rows, int64_t R,
-                                     int n, int layout, __nv_bfloat16 *__restrict__ dst, float *__restrict__ n2,
+                                     int n, int layout, tc_op_t *__restrict__ dst, float *__restrict__ n2,
                                      float2 *__restrict__ en, int is_query, int cw)
 // dst: row-major for queries (the A operand); the tile-major pre-swizzled
 // layout (layout.cuh tcx_offset) for rows (the B operand)
@@ -1025,12 +1025,12 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
     double acc = 0.0, hh = 0.0, ll = 0.0;
     for (int e = lane; e < n; e += 32) {
         const float v = s[layout ? layout_pos(n, e) : e];
-        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        const tc_op_t b = tc_op(v);
         if (is_query)
             dst[r * n + e] = b;
         else
-            *reinterpret_cast<__nv_bfloat16 *>(reinterpret_cast<unsigned char *>(dst) + tcx_offset(r, e, n, cw)) = b;
-        const double vb = (double)__bfloat162float(b), dv = (double)v - vb;  // exact in float64
+            *reinterpret_cast<tc_op_t *>(reinterpret_cast<unsigned char *>(dst) + tcx_offset(r, e, n, cw)) = b;
+        const double vb = (double)tc_op_f(b), dv = (double)v - vb;  // exact in float64
         acc += (double)v * (double)v;
         hh += vb * vb;
         ll += dv * dv;
@@ -1054,14 +1054,14 @@ __global__ void to_bf16_norms_kernel(const float *__restrict__ src, const int32_
 // lane-transposed float32 copy for rescoring, the BF16 operand, ||q||^2, the
 // rounding-error norms (QH, QL) and max |q| (NaN -> +inf, rejected by the host).
 __global__ void tc_query_prep_kernel(const float *__restrict__ Q, int B, int nq_pad, int n, float *__restrict__ qlay,
-                                     __nv_bfloat16 *__restrict__ qb, float *__restrict__ qn2,
+                                     tc_op_t *__restrict__ qb, float *__restrict__ qn2,
                                      float2 *__restrict__ qen, uint32_t *__restrict__ qmax)
 {
     const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (r >= nq_pad) return;
     const int lane = threadIdx.x & 31;
     if (r >= B) {
-        for (int e = lane; e < n; e += 32) qb[(int64_t)r * n + e] = __float2bfloat16_rn(0.f);
+        for (int e = lane; e < n; e += 32) qb[(int64_t)r * n + e] = tc_op(0.f);
         return;
     }
     const float *s = Q + (int64_t)r * n;
@@ -1070,9 +1070,9 @@ __global__ void tc_query_prep_kernel(const float *__restrict__ Q, int B, int nq_
     for (int e = lane; e < n; e += 32) {
         const float v = __ldg(s + e);
         qlay[(int64_t)r * n + layout_pos(n, e)] = v;
-        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        const tc_op_t b = tc_op(v);
         qb[(int64_t)r * n + e] = b;
-        const double vb = (double)__bfloat162float(b), dv = (double)v - vb;
+        const double vb = (double)tc_op_f(b), dv = (double)v - vb;
         acc += (double)v * (double)v;
         hh += vb * vb;
         ll += dv * dv;
@@ -1097,7 +1097,7 @@ int launch_tc_query_prep(const float *Q, int B, int nq_pad, int n, float *qlay, 
                          uint32_t *qmax, cudaStream_t s)
 {
     if (nq_pad == 0) return OK;
-    tc_query_prep_kernel<<<(unsigned)((nq_pad + 7) / 8), 256, 0, s>>>(Q, B, nq_pad, n, qlay, (__nv_bfloat16 *)qb, qn2,
+    tc_query_prep_kernel<<<(unsigned)((nq_pad + 7) / 8), 256, 0, s>>>(Q, B, nq_pad, n, qlay, (tc_op_t *)qb, qn2,
                                                                       qen, qmax);
     SSB_CHECK_LAUNCH();
     return OK;
@@ -1108,7 +1108,7 @@ int launch_to_bf16_norms(const float *src, const int32_t *rows, int64_t R, int n
 {
     if (R == 0) return OK;
     to_bf16_norms_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(src, rows, R, n, layout ? 1 : 0,
-                                                                  (__nv_bfloat16 *)dst_bf16, n2, en, is_query ? 1 : 0,
+                                                                  (tc_op_t *)dst_bf16, n2, en, is_query ? 1 : 0,
                                                                   tcx_default_cw(n));
     SSB_CHECK_LAUNCH();
     return OK;

@@ -27,7 +27,9 @@ def bits(a):
 # n % 64 == 0, else 32-column chunks (SWIZZLE_64B): n = 96, 160, 224, 32
 @pytest.mark.parametrize("n,B,N", [(256, 200, 1000), (96, 130, 777), (64, 5, 300), (128, 128, 128),
                                    (160, 70, 500), (224, 130, 400), (32, 40, 300)])
-def test_tc_dot_matches_bf16_matmul(ssb, n, B, N):
+def test_tc_dot_matches_fp16_matmul(ssb, n, B, N):
+    """The tcgen05 dot products of the FP16 operands (the filters' operand
+    format) against a float64 matmul of the same FP16-rounded values."""
     import torch
 
     from paper_2212_13297_b200 import _lib
@@ -37,7 +39,7 @@ def test_tc_dot_matches_bf16_matmul(ssb, n, B, N):
     S = torch.full((B, N), float("nan"), dtype=torch.float32, device="cuda")
     _lib.call("ssb_tc_dot_debug", ctypes.c_void_p(Q.data_ptr()), B, ctypes.c_void_p(X.data_ptr()), N, n,
               ctypes.c_void_p(S.data_ptr()), None)
-    ref = Q.bfloat16().double() @ X.bfloat16().double().T
+    ref = Q.half().double() @ X.half().double().T
     err = (S.double() - ref).abs().max().item()
     assert np.isfinite(S.cpu().numpy()).all()
     assert err < 1e-3, err
