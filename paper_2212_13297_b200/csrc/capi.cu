@@ -51,6 +51,46 @@ static void tune_mempool()
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
+// Pinned staging for the small host -> device uploads of a query call: an
+// upload from pageable memory first synchronises the stream (the GPU drains
+// while the host stages), one from pinned memory is asynchronous.  One arena
+// per host thread, bump-allocated; stage_reset() at the start of a call whose
+// previous calls ended with a stream synchronisation (no upload in flight).
+namespace {
+struct StageArena {
+    char *base = nullptr;
+    size_t cap = 0, used = 0;
+    ~StageArena()
+    {
+        if (base) cudaFreeHost(base);
+    }
+};
+thread_local StageArena g_stage;
+}  // namespace
+
+void stage_reset() { g_stage.used = 0; }
+
+int stage_upload(void *dst, const void *src, size_t bytes, cudaStream_t s)
+{
+    if (bytes == 0) return OK;
+    const size_t need = (bytes + 255) & ~(size_t)255;
+    if (g_stage.used + need > g_stage.cap) {
+        if (g_stage.used > 0) {  // arena in use: this upload goes the pageable (synchronising) way
+            SSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+            return OK;
+        }
+        if (g_stage.base) cudaFreeHost(g_stage.base);
+        g_stage.base = nullptr;
+        g_stage.cap = std::max<size_t>(need, (size_t)1 << 20);
+        SSB_CUDA(cudaMallocHost(reinterpret_cast<void **>(&g_stage.base), g_stage.cap));
+    }
+    char *p = g_stage.base + g_stage.used;
+    g_stage.used += need;
+    std::memcpy(p, src, bytes);
+    SSB_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+    return OK;
+}
+
 int num_sms()
 {
     tune_mempool();

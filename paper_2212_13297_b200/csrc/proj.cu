@@ -48,6 +48,12 @@
 
 namespace ssb {
 
+#define RC(x)                \
+    do {                     \
+        const int _rc = (x); \
+        if (_rc) return _rc; \
+    } while (0)
+
 constexpr int PJ_DMAX = 64;     // operand columns (one 64-column K-chunk): coefficients + the norm split
 constexpr int PJ_COEF = PJ_DMAX - 2;  // projection coefficients
 constexpr int PJ_ROWS = 128;    // rows per projection tile
@@ -586,7 +592,7 @@ static int phase_setup(const Index &ix, const float *Q, const std::vector<int32_
     SSB_CUDA(qn2.alloc(4 * (size_t)nq_pad, s));
     SSB_CUDA(qen.alloc(8 * (size_t)nq_pad, s));
     SSB_CUDA(gb.alloc(4 * (size_t)tc_bound_slots(nq), s));
-    SSB_CUDA(cudaMemcpyAsync(pw.qidx.p, ql.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    RC(stage_upload(pw.qidx.p, ql.data(), 4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(pw.cnt.p, 0, 4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(pw.flag.p, 0, 4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(pw.hard.p, 0, 4 * (size_t)nq, s));
@@ -705,7 +711,7 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
             std::fill(is_hard.begin(), is_hard.end(), 0);
         } else {
             for (int i = 0; i < nq; i++) f0[i] = is_hard[i] ? 1u : 0u;
-            SSB_CUDA(cudaMemcpyAsync(pw.flag.p, f0.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+            RC(stage_upload(pw.flag.p, f0.data(), 4 * (size_t)nq, s));
         }
         for (int i = 0; i < nq; i++) total[i] = c0[i];
         rc = phase_tighten(ix, pw, qlay, B, k, so, thr, s);
@@ -762,11 +768,10 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
             hh[j] = (hf[j] || (int64_t)total[i] > seg_eff) ? 1 : 0;
             is_hard[i] = (char)hh[j];
         }
-        SSB_CUDA(cudaMemcpyAsync(pw.hard.p, hh.data(), 4 * (size_t)nl, cudaMemcpyHostToDevice, s));
+        RC(stage_upload(pw.hard.p, hh.data(), 4 * (size_t)nl, s));
         // the last range's candidates (hard queries excluded)
         rc = launch_rescore_proj(ix, pw, qlay, nullptr, so, s, (int64_t)done, pw.nc, pw.hard.as<int32_t>());
         if (rc) return rc;
-        SSB_CUDA(cudaStreamSynchronize(s));  // hh dies here
     }
     // the sample phase's view of the final decision (for the flagged re-rescoring)
     std::vector<int32_t> h32(nq);
@@ -778,24 +783,23 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         else
             settled += total[i];
     }
-    if (t0 > 0) SSB_CUDA(cudaMemcpyAsync(pws[0]->hard.p, h32.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    if (t0 > 0) RC(stage_upload(pws[0]->hard.p, h32.data(), 4 * (size_t)nq, s));
     // queries handed to the full filter start over there (what the ranges
     // rescored for them would be duplicates)
     DevBuf dh, dq, dc;
     SSB_CUDA(dh.alloc(4 * (size_t)nq, s));
     SSB_CUDA(dq.alloc(4 * (size_t)nq, s));
-    SSB_CUDA(cudaMemcpyAsync(dh.p, h32.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
-    SSB_CUDA(cudaMemcpyAsync(dq.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+    RC(stage_upload(dh.p, h32.data(), 4 * (size_t)nq, s));
+    RC(stage_upload(dq.p, qtc.data(), 4 * (size_t)nq, s));
     proj_reset_hard_kernel<<<(nq + 255) / 256, 256, 0, s>>>(dh.as<int32_t>(), dq.as<int32_t>(), nq, so.cnt);
     SSB_CHECK_LAUNCH();
     if (cser) {
         std::vector<uint32_t> tt(total.begin(), total.end());
         SSB_CUDA(dc.alloc(4 * (size_t)nq, s));
-        SSB_CUDA(cudaMemcpyAsync(dc.p, tt.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+        RC(stage_upload(dc.p, tt.data(), 4 * (size_t)nq, s));
         proj_cser_kernel<<<(nq + 255) / 256, 256, 0, s>>>(dc.as<unsigned int>(), dh.as<int32_t>(), dq.as<int32_t>(), nq,
                                                           cser);
         SSB_CHECK_LAUNCH();
-        SSB_CUDA(cudaStreamSynchronize(s));  // tt dies here
     }
     if (getenv("SSB_TC_TRACE")) {
         std::vector<uint64_t> bb(B);
@@ -809,7 +813,6 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
                 nq, k, ix.pd, split, predicted_hard, live.size(), v[v.size() / 10], v[v.size() / 2],
                 v[v.size() * 9 / 10], (long long)settled, qtc.size() - hard->size(), hard->size());
     }
-    SSB_CUDA(cudaStreamSynchronize(s));  // h32 dies here
     return OK;
 }
 

@@ -23,6 +23,12 @@
 
 namespace ssb {
 
+#define RC_(x)               \
+    do {                     \
+        const int _rc = (x); \
+        if (_rc) return _rc; \
+    } while (0)
+
 int launch_query_prep(const float *Q, int B, int n, double *cs, double *c2, float *qpaa,
                       cudaStream_t s);
 
@@ -228,6 +234,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
     const double tc_group_ns = (double)ix.N * IX_NS_TC_ROW * n / 256.0 *
                                (proj_available(ix) ? IX_NS_PROJ_FACTOR * ix.pd / n : 1.0);
     if (mode == 0 && (double)ix.N * IX_NS_IX_ROW * std::min(B, 256) <= tc_group_ns) mode = 1;
+    stage_reset();  // the previous call ended with a synchronisation
     IxWork w;
     int rc = ix_front(ix, qc, Q, B, k, mode, want, w, s);
     if (rc) return rc;
@@ -291,7 +298,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             }
             std::fill(tc.begin(), tc.end(), 0);
             for (int i = 0; i < best_t; i++) tc[order[i]] = 1;
-            SSB_CUDA(cudaMemcpyAsync(w.use_tc.p, tc.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+            RC_(stage_upload(w.use_tc.p, tc.data(), 4 * (size_t)B, s));
         }
         int64_t items = 0;
         for (int q = 0; q < B; q++) {
@@ -302,9 +309,11 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         }
         rc = ix_emit(ix, w, B, nullptr, 0, items, s);
         if (rc) return rc;
-        SSB_CUDA(cudaStreamSynchronize(s));  // tc (the uploaded routes) dies here
         kept.swap(kr);
     }
+    // every query on the filters (C4-like blocks): the routing observation
+    // needs no device counters (no index-routed survivors to count)
+    bool all_tc = !kept.empty() && (int)qtc.size() == B;
 
     // index route first (Q5 + Q6 of every query the plan kept on it)
     rc = ix_back(ix, w, B, mode != 1 ? w.use_tc.as<int32_t>() : nullptr, so, cser.as<uint32_t>(), s);
@@ -373,7 +382,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         SSB_CUDA(tc_cand.alloc(8 * (size_t)tc_cap, s));
         SSB_CUDA(tc_lb.alloc(4 * (size_t)tc_cap, s));
         SSB_CUDA(tc_n.alloc(8, s));
-        SSB_CUDA(cudaMemcpyAsync(d_qtc.p, qtc.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, s));
+        RC_(stage_upload(d_qtc.p, qtc.data(), 4 * (size_t)nq, s));
         SSB_CUDA(cudaMemsetAsync(qb.p, 0, 2 * (size_t)nq_pad * n, s));
         rc = launch_to_bf16_norms(Q, d_qtc.as<int32_t>(), nq, n, false, qb.p, qn2.as<float>(), qnrm.as<float2>(), true, s);
         if (rc) return rc;
@@ -395,6 +404,7 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
         if ((int64_t)hn > tc_cap) {
             // still too many candidates: these queries take the index route
             // (the queries K-proj answered keep their tensor-route mark)
+            all_tc = false;
             {
                 std::vector<int32_t> ut(B);
                 SSB_CUDA(cudaMemcpyAsync(ut.data(), w.use_tc.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
@@ -498,7 +508,11 @@ static int query_batch(const Index &ix, const QueryCfg &qc, const float *Q, int 
             if (rc) return rc;
         }
     }
-    if (qc.route == 0) {  // the routing observation (kept rows of every query, survivors of the index-routed)
+    if (qc.route == 0 && all_tc) {
+        double kept_sum = 0.0;
+        for (int q = 0; q < B; q++) kept_sum += (double)kept[q];
+        observe_route(ix, kept_sum / ((double)B * (double)std::max<int64_t>(ix.N, 1)), -1.0);
+    } else if (qc.route == 0) {  // the routing observation (kept rows of every query, survivors of the index-routed)
         std::vector<unsigned long long> kr(B);
         std::vector<uint32_t> sv(B);
         std::vector<int32_t> tc(B);

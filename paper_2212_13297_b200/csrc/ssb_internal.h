@@ -10,6 +10,9 @@
 namespace ssb {
 
 int num_sms();
+// small host -> device uploads through a pinned arena (capi.cu): asynchronous
+void stage_reset();
+int stage_upload(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 // per-query candidate buffers written by the scan kernels
 struct ScanOut {
