@@ -391,34 +391,52 @@ __global__ void __launch_bounds__(1024)
         __syncthreads();
     }
     const int np = (int)s_np;
-    // rows of the picked leaves, as one virtual range
-    auto row_of = [&](uint32_t i, uint32_t &pos) -> bool {
+    // rows of the picked leaves, as one virtual range: the picked leaves' row
+    // ranges and prefix offsets staged once in shared memory (the per-row leaf
+    // walk otherwise chases global loads on every row)
+    __shared__ uint32_t pk_first[IX_SEED_MAX], pk_off[IX_SEED_MAX + 1];
+    if (tid == 0) {
+        uint32_t acc = 0;
         for (int p = 0; p < np; p++) {
-            const uint32_t c = leaf_count[picked[p]];
-            if (i < c) {
-                pos = leaf_first[picked[p]] + i;
-                return true;
-            }
-            i -= c;
+            pk_first[p] = leaf_first[picked[p]];
+            pk_off[p] = acc;
+            acc += leaf_count[picked[p]];
         }
-        return false;
+        pk_off[np] = acc;
+    }
+    __syncthreads();
+    const uint32_t R = pk_off[np];
+    auto row_of = [&](uint32_t i, uint32_t &pos) -> bool {
+        int p = 0;
+        while (p + 1 < np && i >= pk_off[p + 1]) p++;
+        pos = pk_first[p] + (i - pk_off[p]);
+        return i < R;
     };
-    uint32_t R = 0;
-    for (int p = 0; p < np; p++) R += leaf_count[picked[p]];
-    auto lb_sax = [&](uint32_t pos) -> float {
-        const uint4 wv = __ldg(words + pos);
+    auto lb_sax_w = [&](const uint4 wv) -> float {
         const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
         float acc = 0.f;
 #pragma unroll
         for (int sg = 0; sg < 16; sg++) acc += T[sg * ALPHABET + ((wd[sg >> 2] >> (8 * (sg & 3))) & 0xffu)];
         return acc;
     };
+    // rows in batches of 4 per thread: the words' loads are issued together
+    constexpr int WB = 4;
+    auto for_rows = [&](auto &&fn) {
+        for (uint32_t i0 = tid; i0 < R; i0 += WB * blockDim.x) {
+            uint32_t pos[WB];
+            uint4 wv[WB];
+#pragma unroll
+            for (int u = 0; u < WB; u++) {
+                const uint32_t i = i0 + u * blockDim.x;
+                if (row_of(i, pos[u])) wv[u] = __ldg(words + pos[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < WB; u++)
+                if (i0 + u * blockDim.x < R) fn(pos[u], lb_sax_w(wv[u]));
+        }
+    };
     // (b) LB_SAX histogram (float bits >> 20: exponent + 3 mantissa bits; LB >= 0)
-    for (uint32_t i = tid; i < R; i += blockDim.x) {
-        uint32_t pos;
-        row_of(i, pos);
-        atomicAdd(&hist[__float_as_uint(lb_sax(pos)) >> 20], 1u);
-    }
+    for_rows([&](uint32_t, float lb) { atomicAdd(&hist[__float_as_uint(lb) >> 20], 1u); });
     __syncthreads();
     // (c) the cut: the smallest bin edge with >= target rows below it
     if (warp == 0) {
@@ -442,14 +460,12 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     const uint32_t cut_bits = ((s_cut + 1) << 20) - 1u;
-    for (uint32_t i = tid; i < R; i += blockDim.x) {
-        uint32_t pos;
-        row_of(i, pos);
-        if (__float_as_uint(lb_sax(pos)) <= cut_bits) {
+    for_rows([&](uint32_t pos, float lb) {
+        if (__float_as_uint(lb) <= cut_bits) {
             const uint32_t slot = atomicAdd(&s_nc, 1u);
             if (slot < IX_CMAX) cand[slot] = pos;
         }
-    }
+    });
     __syncthreads();
     const int nc = (int)min(s_nc, (uint32_t)IX_CMAX);
     // (d) exact distances of the ranked candidates: 32 groups of 8 lanes
