@@ -262,6 +262,23 @@ int ssb_lb_sax(const float *qpaa, const uint8_t *words, int64_t rows, const doub
 int ssb_ingest_file(const char *path, int64_t first, int64_t count, int32_t n, float *dst,
                     int64_t chunk_bytes, int32_t threads, void *stream, double *stats);
 
+/* Streamed exact k-NN over a dataset FILE of any size (replaces pscan.py:33-135
+ * pscan_query and :138-149 pscan, the reference's double-buffered scan: a reader
+ * thread filling a two-slot chunk buffer, workers scanning it against the
+ * shared best-so-far).  File -> pinned double buffer (`threads` preads) ->
+ * device slot on a copy stream -> K-scan of the chunk against the running
+ * k-th key -> K-select -> merge into the running top-k, the three stages
+ * overlapped; neither HBM nor host memory has to hold the file.  Q: device,
+ * B x n float32; rows [first, first + count) of the file (count < 0: to the
+ * end); out_d2 / out_id: device, B x k, ordered by (d2, id), ids = file row
+ * positions, missing = (+inf, -1).  chunk_bytes <= 0: 256 MB.  n in {64, 96,
+ * 128, 256}, k <= 256, first + count < 2^32.  Synchronizes `stream`.
+ * stats (host, optional): [0] bytes streamed, [1] wall seconds, [2] chunks.
+ * Errors as ssb_ingest_file, usage for k / n out of range. */
+int ssb_scan_file(const char *path, int64_t first, int64_t count, int32_t n, const float *Q, int32_t B,
+                  int32_t k, int64_t chunk_bytes, int32_t threads, float *out_d2, int64_t *out_id,
+                  void *stream, double *stats);
+
 /* Seeded synthetic series in HBM (out: device, count x n float32): series
  * [start, start + count) of a documented Philox4x32-10 stream (csrc/generate.cu
  * header; NOT numpy's bits).  kind 0: random walks -- float64 prefix sums of

@@ -7,7 +7,7 @@ query entry points; all compute runs in libseriesearch_b200.so (sm_100a).
 from .build import BuildTrace, SeriesIndex, build_index, build_index_array, ingest_file
 from .errors import DataFileError, DeviceError, IntegrityError, SeriesearchError, UsageError
 from .persist import IndexSettings, QueryableIndex, load_index, write_index
-from .pscan import brute_force_knn, knn_batch, pscan, pscan_query
+from .pscan import brute_force_knn, knn_batch, pscan, pscan_query, scan_file
 from .query import QueryConfig, QueryEngine, QueryStats, ResultSet, exact_knn
 
 __version__ = "0.1.0"
@@ -36,5 +36,6 @@ __all__ = [
     "knn_batch",
     "pscan",
     "pscan_query",
+    "scan_file",
     "__version__",
 ]

@@ -59,6 +59,7 @@ _SIGS = {
     "ssb_comm_merge_topk": [P, P, P, I32, I32, P, P, P],
     "ssb_index_set_comm": [P, P],
     "ssb_ingest_file": [ctypes.c_char_p, I64, I64, I32, P, I64, I32, P, P],
+    "ssb_scan_file": [ctypes.c_char_p, I64, I64, I32, P, I32, I32, I64, I32, P, P, P, P],
     "ssb_generate": [I32, I64, I64, I32, ctypes.c_uint64, P, P],
 }
 

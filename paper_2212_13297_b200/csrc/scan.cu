@@ -215,6 +215,15 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// the row scan's per-query d2 bound from an inclusive key bound (k real
+// distances <= its d2), KEY_EMPTY = none
+__global__ void gbound_from_thr_kernel(const uint64_t *__restrict__ thr, int nq, unsigned int *__restrict__ gb)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq || thr[q] == KEY_EMPTY) return;
+    gb[q] = tmin<unsigned int>(gb[q], (unsigned int)(thr[q] >> 32));
+}
+
 int rowscan_ranges(int64_t N, int k)
 {
     const int64_t want = 4 * (int64_t)num_sms();
@@ -237,6 +246,10 @@ static int launch_rows_t(const float *X, int64_t N, const float *Q, int nq, int 
     DevBuf gb;
     SSB_CUDA(gb.alloc(4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(gb.p, 0x7f, 4 * (size_t)nq, s));  // 0x7f7f7f7f: a huge finite bound until set
+    if (out.thr) {  // a bound carried in (the streamed file scan's running k-th key): abandon from the start
+        gbound_from_thr_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out.thr, nq, gb.as<unsigned int>());
+        SSB_CHECK_LAUNCH();
+    }
     ProfScope ps("scan_rows", s, 0.0);
     scan_rows_kernel<NT><<<dim3((unsigned)ranges, (unsigned)nq), 256, smem, s>>>(
         X, N, Q, k, id_base, rpr, ranges, gb.as<unsigned int>(), out, ps.counter());
@@ -477,6 +490,38 @@ int merge_topk(const uint64_t *keys, int nq, int m, int k, float *out_d2, int64_
                            flags.as<int32_t>(), s);
     if (rc) return rc;
     return launch_keys_to_results(out.as<uint64_t>(), (int64_t)nq * k, nullptr, 0, out_d2, out_id, nullptr, s);
+}
+
+// running[q] (k sorted keys) <- the k smallest of running[q] and chunk[q] (k
+// sorted keys each; KEY_EMPTY last), written to out; thr[q] <- its k-th key.
+// One thread per query, a two-pointer merge: the streamed file scan folds each
+// chunk's top-k into the answer so far (pscan.py:96-105 results.insert).
+__global__ void merge_sorted_kernel(const uint64_t *__restrict__ run, const uint64_t *__restrict__ chunk, int nq,
+                                    int k, uint64_t *__restrict__ out, uint64_t *__restrict__ thr)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t *a = run + (size_t)q * k, *b = chunk + (size_t)q * k;
+    uint64_t *o = out + (size_t)q * k;
+    int i = 0, j = 0;
+    uint64_t last = KEY_EMPTY;
+    for (int e = 0; e < k; e++) {
+        const uint64_t x = a[i], y = b[j];
+        last = x <= y ? x : y;
+        if (x <= y) i++;
+        else j++;
+        o[e] = last;
+    }
+    thr[q] = last;
+}
+
+int launch_merge_sorted(const uint64_t *run, const uint64_t *chunk, int nq, int k, uint64_t *out, uint64_t *thr,
+                        cudaStream_t s)
+{
+    if (nq == 0) return OK;
+    merge_sorted_kernel<<<(nq + 127) / 128, 128, 0, s>>>(run, chunk, nq, k, out, thr);
+    SSB_CHECK_LAUNCH();
+    return OK;
 }
 
 // (d2, id) results -> merge keys (d2 bits << 32 | id), id < 0 -> KEY_EMPTY: the

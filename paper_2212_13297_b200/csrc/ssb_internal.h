@@ -30,6 +30,8 @@ int launch_scan_dense(const float *X, int64_t N, int n, const float *Q, const in
                       int nq, int k, uint32_t id_base, ScanOut out, cudaStream_t s);
 int launch_select(const uint64_t *cand, uint32_t *cnt, int cap, int nq, int k, uint64_t *thr,
                   uint64_t *out_keys, int32_t *flags, cudaStream_t s);
+int launch_merge_sorted(const uint64_t *run, const uint64_t *chunk, int nq, int k, uint64_t *out, uint64_t *thr,
+                        cudaStream_t s);
 int launch_pack_keys(const float *d2, const int64_t *ids, int64_t count, uint64_t *keys, cudaStream_t s);
 int launch_keys_to_results(const uint64_t *keys, int64_t count, const uint32_t *inv_perm, int64_t id_base,
                            float *out_d2, int64_t *out_id, int64_t *out_pos, cudaStream_t s);

@@ -189,3 +189,86 @@ def test_bruteforce_row_scan_ties(ssb, oracle):
     od2, oid = oracle.knn_scan(X, Q, 10)
     d2, ids = ssb.knn_batch(X, Q, 10)
     assert np.array_equal(ids.cpu().numpy(), oid)
+
+
+# ---------------------------------------------------------------------------
+# streamed file scan (pscan.py:33-149 pscan_query / pscan; csrc/ingest.cu
+# scan_file): chunks read, copied and scanned in a pipeline, the running k-th
+# key carried from chunk to chunk.  Small chunk sizes force many chunks (and a
+# ragged last one) so every bound hand-over is exercised.
+
+def _write(tmp_path, X, name="data.bin"):
+    p = tmp_path / name
+    np.ascontiguousarray(X, np.float32).tofile(p)
+    return str(p)
+
+
+@pytest.mark.parametrize("n,N,B,k,chunk_rows", [(256, 50_003, 1, 10, 4096), (256, 50_003, 3, 100, 7000),
+                                                (96, 40_001, 37, 10, 5000), (64, 30_000, 200, 1, 30_000),
+                                                (128, 9_999, 5, 256, 1000), (256, 2_000, 1, 1, 333)])
+def test_scan_file_matches_oracle(ssb, oracle, tmp_path, n, N, B, k, chunk_rows):
+    X = random_walks(N, n, 5000 + N)
+    Q = np.concatenate([random_walks(B - 1, n, 6000 + B), X[[N // 2]] + np.float32(0.01)]).astype(np.float32)
+    path = _write(tmp_path, X)
+    d2, ids, st = ssb.scan_file(path, n, Q, k, chunk_bytes=chunk_rows * 4 * n, threads=4)
+    assert st["chunks"] == (N + chunk_rows - 1) // chunk_rows and st["bytes"] == X.nbytes
+    od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+def test_scan_file_ties_across_chunks(ssb, oracle, tmp_path):
+    """Exact duplicates in different chunks: the lowest file position wins
+    (pscan.py's answers equal the nested-loop scan's, ties to the lower id)."""
+    X = random_walks(20_000, 256, 91)
+    for i in (3, 7_777, 19_999):
+        X[i] = X[12_345]
+    path = _write(tmp_path, X)
+    for B in (1, 9):  # row shape and dense shape
+        Q = np.repeat(X[[12_345]], B, axis=0)
+        d2, ids, _ = ssb.scan_file(path, 256, Q, 3, chunk_bytes=3000 * 1024)
+        assert [list(r) for r in ids.cpu().numpy()] == [[3, 7_777, 12_345]] * B
+        assert (d2.cpu().numpy() == 0).all()
+
+
+def test_scan_file_subrange_edges_and_errors(ssb, oracle, tmp_path):
+    X = random_walks(5_000, 64, 17)
+    path = _write(tmp_path, X)
+    Q = random_walks(6, 64, 18)
+    # rows [1000, 3000): ids are file positions
+    d2, ids, _ = ssb.scan_file(path, 64, Q, 5, first=1000, count=2000, chunk_bytes=700 * 256)
+    od2, oid = oracle.knn_scan(X[1000:3000], Q, 5)
+    assert np.array_equal(ids.cpu().numpy(), oid + 1000)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+    # k > rows pads with (inf, -1); an empty range answers nothing
+    d2, ids, _ = ssb.scan_file(path, 64, Q[:2], 8, first=4995, chunk_bytes=2 * 256)
+    assert (ids.cpu().numpy()[:, 5:] == -1).all() and np.isinf(d2.cpu().numpy()[:, 5:]).all()
+    d2, ids, _ = ssb.scan_file(path, 64, Q, 4, first=5000)
+    assert (ids.cpu().numpy() == -1).all()
+    with pytest.raises(ssb.DataFileError):
+        ssb.scan_file(str(tmp_path / "missing.bin"), 64, Q, 1)
+    with pytest.raises(ssb.UsageError):
+        ssb.scan_file(path, 96, Q, 1)          # 5000 x 64 floats is not a whole number of 96-point series
+    with pytest.raises(ssb.UsageError):
+        ssb.scan_file(path, 64, Q, 1, first=4000, count=2000)
+    with pytest.raises(ssb.UsageError):
+        ssb.scan_file(path, 64, Q, 0)
+
+
+def test_pscan_entry_points_stream_the_file(ssb, oracle, tmp_path):
+    """pscan_query / pscan (pscan.py:33-149) through the streamed scan: the same
+    ResultSets as the oracle, whatever chunk_series / num_threads say."""
+    X = random_walks(30_000, 256, 23)
+    path = _write(tmp_path, X)
+    Q = random_walks(4, 256, 24)
+    od2, oid = oracle.knn_scan(X, Q, 7)
+    for t, cs in ((1, 16384), (4, 100), (16, 1 << 20)):
+        rs = ssb.pscan_query(path, 256, Q[1], 7, num_threads=t, chunk_series=cs)
+        assert [p for _, p in rs.entries()] == list(oid[1])
+        assert rs.distances_sq() == [float(v) for v in od2[1]]
+    rss = ssb.pscan(path, 256, Q, 7, num_threads=2)
+    assert [[p for _, p in r.entries()] for r in rss] == [list(r) for r in oid]
+    with pytest.raises(ssb.UsageError):
+        ssb.pscan_query(path, 256, Q[0], 7, num_threads=0)
+    with pytest.raises(ssb.UsageError):
+        ssb.pscan_query(path, 256, Q[0][:100], 7)
