@@ -691,9 +691,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // (a one-tile register prefetch -- tile t + 1's accumulator loaded and
             // released before tile t is examined -- measured 7% slower on C4)
             uint32_t fs = 0, fph = 0;  // next accumulator to fetch, its phase
-            auto fetch = [&](uint32_t(&v)[COLS]) {
+            auto fetch = [&](uint32_t(&v)[COLS], const bool LEAN) {
                 const uint32_t sa = 8u * fs, taddr = tbase + fs * (uint32_t)TC_BN;
-                if (p.spin_epi) mbar_spin_a(a_tfull + sa, fph); else mbar_wait_a(a_tfull + sa, fph);
+                if (!LEAN && p.spin_epi) mbar_spin_a(a_tfull + sa, fph); else mbar_wait_a(a_tfull + sa, fph);
                 if (++fs == TC_NACC) {
                     fs = 0;
                     fph ^= 1u;
@@ -707,11 +707,14 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 if (lane == 0) mbar_arrive_a(a_tempty + sa);
             };
             unsigned gave_up = 0;  // another thread of this query gave up (read every 16th tile, used at the next)
-            auto examine = [&](const uint32_t(&v)[COLS], int t) {
-                if ((t & 15) == 0 && qvalid) {
+            auto check_gave_up = [&]() {
+                if (qvalid) {
                     if (gave_up) thr = __int_as_float(0x7f800000);
                     gave_up = *(volatile const unsigned int *)(p.seg_flag + ql);
                 }
+            };
+            auto examine = [&](const uint32_t(&v)[COLS], int t, const bool LEAN) {
+                if (!LEAN && (t & 15) == 0) check_gave_up();
                 // maxima of column triples (kept: a triple below the threshold
                 // needs no per-column test), then of the 16-column groups
                 float tri[COLS / 16][5];
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 float mx = mg[0];
 #pragma unroll
                 for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
-                if (p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: loads + max, no emission
+                if (!LEAN && p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: loads + max, no emission
                 if (!__any_sync(0xffffffffu, mx >= thr)) return;
                 const int64_t row0 = rbase + (int64_t)t * TC_BN;
                 const int64_t left = p.N - row0;
@@ -777,10 +780,25 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 __syncwarp();
                 if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
             };
-            for (int t = 0; t < niter; t++) {
-                uint32_t v[COLS];
-                fetch(v);
-                if (!diag_skip && p.skip_epi != 5) examine(v, t);  // 5: diagnostics, TMEM loads only
+            if (p.skip_epi == 0 && p.spin_epi == 0) {
+                // the hot loop (the epilogue issues about as many instructions
+                // per tile as the MMA takes cycles): no diagnostics switches,
+                // the give-up flags read once per 16 tiles outside the tile loop
+                for (int t0 = 0; t0 < niter; t0 += 16) {
+                    check_gave_up();
+                    const int t1 = min(niter, t0 + 16);
+                    for (int t = t0; t < t1; t++) {
+                        uint32_t v[COLS];
+                        fetch(v, true);
+                        examine(v, t, true);
+                    }
+                }
+            } else {
+                for (int t = 0; t < niter; t++) {
+                    uint32_t v[COLS];
+                    fetch(v, false);
+                    if (!diag_skip && p.skip_epi != 5) examine(v, t, false);  // 5: diagnostics, TMEM loads only
+                }
             }
         } else
         for (int t = 0; t < niter; t++) {
