@@ -16,6 +16,7 @@
 // dumps it to the per-query candidate buffer at the end.  (The index path's
 // early-abandoning scan of LB_SAX survivors lives in ixq.cu.)  K-select then
 // sorts each query's candidates and keeps the first k.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -215,6 +216,213 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---------------------------------------------------------------------------
+// streamed row scan (the default for B <= ROWSCAN_MAX_B): one persistent CTA
+// per SM and row range.  A producer warp streams the FIRST pairwise block of
+// every row (min(n, 128) floats: numpy sums a longer row as block + block) into
+// a shared-memory ring: ONE tensor-map TMA copy per stage of RS_TR rows (the
+// rows seen as [chunk of 32 floats][row][chunk index], SWIZZLE_128B, so a stage
+// is chunk-major in shared memory and the four groups of a warp -- rows two
+// apart -- read distinct bank octets; per-row bulk copies top out at one copy
+// per ~64 cycles and SM: 2.3 TB/s).  64 consumer groups take one staged row
+// each: the block's sum is a lower bound of the row's float32 d2
+// (round-to-nearest is monotone, every term is >= 0), so a row whose first
+// block already exceeds the bound is abandoned without its second half ever
+// leaving HBM; the few survivors read it straight from global memory.  The
+// bound: the rows of a query are split into k classes by a hash of the row
+// number; the largest per-class minimum of the exact distances seen so far
+// (global atomicMin, every CTA of the query) is >= k real distances of
+// distinct rows -- it tightens to about the (ln k / rows-per-class) quantile
+// after one stage per CTA, orders of magnitude below a group's own k-th
+// distance.  A bound carried in (out.thr: the streamed file scan's running k-th
+// key) applies from the first row.  d2 of every surviving row == group_ed2 bit
+// for bit.
+
+constexpr int RS_TR = 64;       // rows per stage == consumer groups
+constexpr int RS_CW = 16;       // consumer warps
+constexpr int RS_MAXST = 6;     // ring stages (as many as fit)
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar)
+{
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(32 * (RS_CW + 1), 1)
+    scan_rows_stream_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ X, int64_t N,
+                            const float *__restrict__ Q, int k, uint32_t id_base, int64_t rows_per_range,
+                            const unsigned int *__restrict__ gbound, unsigned int *__restrict__ gbucket, int kstride,
+                            int nstage, ScanOut out, unsigned long long *__restrict__ prof_bytes)
+{
+    constexpr int HB = NT > 128 ? 128 : NT;               // floats of the first pairwise block
+    constexpr int CHUNKF = RS_TR * 32;                    // floats per staged chunk (all rows' 32 floats)
+    constexpr int STAGEF = RS_TR * HB;                    // floats per stage
+    static_assert((NT <= 128 && NT % 32 == 0) || NT == 256, "supported series lengths");
+    extern __shared__ __align__(1024) unsigned char rs_smem[];
+    uint64_t *lists = reinterpret_cast<uint64_t *>(rs_smem);                 // RS_TR groups x k (later: the CTA sort)
+    float *ring = reinterpret_cast<float *>(rs_smem + (((size_t)RS_TR * k * 8 + 1023) & ~(size_t)1023));
+    __shared__ uint64_t full[RS_MAXST], empty[RS_MAXST];
+    __shared__ unsigned int cbound;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_range, r1 = tmin<int64_t>(N, r0 + rows_per_range);
+    const int ntiles = r1 > r0 ? (int)((r1 - r0 + RS_TR - 1) / RS_TR) : 0;
+    for (int e = tid; e < RS_TR * k; e += blockDim.x) lists[e] = KEY_EMPTY;
+    if (tid == 0) {
+        for (int i = 0; i < nstage; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], RS_CW);
+        }
+        cbound = tmin<unsigned int>(0x7f800000u, gbound[q]);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    unsigned int *bk = gbucket + (size_t)q * kstride;
+    unsigned long long steps = 0;
+    if (warp == RS_CW) {
+        // ---------------- producer: one tensor copy per stage, and the bucket bound ----------------
+        const uint64_t tm = reinterpret_cast<uint64_t>(&tmap);
+        for (int t = 0; t < ntiles; t++) {
+            const int st = t % nstage;
+            if (t >= nstage) mbar_wait(&empty[st], (unsigned)((t / nstage - 1) & 1));
+            if (lane == 0) {
+                // rows past N are zero-filled and count: every stage is a full box
+                mbar_expect_tx(&full[st], (unsigned)STAGEF * 4u);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (size_t)st * STAGEF);
+                const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[st]);
+                const int row0 = (int)(r0 + (int64_t)t * RS_TR);
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+                    "l"(tm), "r"(0), "r"(row0), "r"(0), "r"(bar)
+                    : "memory");
+            }
+            // the largest class minimum, once every class has one (first stages: every stage)
+            if (t < 8 || (t & 7) == 0) {
+                unsigned int mx = 0;
+                for (int b = lane; b < k; b += 32) mx = max(mx, __ldcg(bk + b));
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                if (lane == 0 && mx < 0x7f800000u && mx < *(volatile unsigned int *)&cbound)
+                    *(volatile unsigned int *)&cbound = mx;
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- consumers: one staged row per group and stage ----------------
+        const int g = tid >> 3, j = tid & 7;
+        const unsigned gmask = 0xffu << (lane & 24);
+        // the four groups of a warp take rows two apart (distinct swizzle patterns, see above)
+        const int rt = 2 * (lane >> 3) + (warp & 1) + 8 * (warp >> 1);
+        int so[4];  // float offsets of (row rt, element 8 (i & 3) + j) inside a chunk, swizzled
+#pragma unroll
+        for (int m = 0; m < 4; m++) so[m] = rt * 32 + (((2 * m + (j >> 2)) ^ (rt & 7)) << 2) + (j & 3);
+        float qv[NT / 8];
+#pragma unroll
+        for (int i = 0; i < NT / 8; i++) qv[i] = Q[(int64_t)q * NT + 8 * i + j];
+        uint64_t *mylist = lists + (size_t)g * k;
+        for (int t = 0; t < ntiles; t++) {
+            const int st = t % nstage;
+            mbar_wait(&full[st], (unsigned)((t / nstage) & 1));
+            const int64_t row = r0 + (int64_t)t * RS_TR + rt;
+            const bool have = row < r1;
+            float d2 = 0.f;
+            if (have) {
+                const float *sr = ring + (size_t)st * STAGEF;
+#pragma unroll
+                for (int i = 0; i < HB / 8; i++) {
+                    const float d = __fsub_rn(sr[(i >> 2) * CHUNKF + so[i & 3]], qv[i]);
+                    d2 = i == 0 ? __fmul_rn(d, d) : __fadd_rn(d2, __fmul_rn(d, d));
+                }
+                d2 = __fadd_rn(d2, __shfl_xor_sync(gmask, d2, 1));
+                d2 = __fadd_rn(d2, __shfl_xor_sync(gmask, d2, 2));
+                d2 = __fadd_rn(d2, __shfl_xor_sync(gmask, d2, 4));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta(&empty[st]);  // the stage's rows are summed
+            if (!have) continue;
+            steps += HB / 8;
+            const uint64_t kth = mylist[k - 1];
+            float bd2 = kth == KEY_EMPTY ? __int_as_float(0x7f800000) : key_d2(kth);
+            bd2 = fminf(bd2, __uint_as_float(*(volatile unsigned int *)&cbound));
+            bd2 = __shfl_sync(gmask, bd2, lane & 24);  // one bound per group (the abandon test must be uniform)
+            if (d2 > bd2) continue;
+            if constexpr (NT > HB) {
+                d2 = __fadd_rn(d2, group_block<HB, NT - HB, NT / 8>(X + row * NT, qv, j, gmask));
+                steps += (NT - HB) / 8;
+                if (d2 > bd2) continue;
+            }
+            if (j == 0) {
+                const uint32_t r = id_base + (uint32_t)row;
+                atomicMin(bk + __umulhi(r * 0x9E3779B1u, (uint32_t)k), __float_as_uint(d2));
+                const uint64_t key = make_key(d2, r);
+                if (key < mylist[k - 1]) {
+                    int p = k - 1;
+                    while (p > 0 && mylist[p - 1] > key) {
+                        mylist[p] = mylist[p - 1];
+                        p--;
+                    }
+                    mylist[p] = key;
+                }
+            }
+            __syncwarp(gmask);
+        }
+    }
+    // the CTA's best k of its group lists
+    __syncthreads();
+    int p2 = 1;
+    while (p2 < RS_TR * k) p2 <<= 1;
+    for (int e = RS_TR * k + tid; e < p2; e += blockDim.x) lists[e] = KEY_EMPTY;
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < p2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const uint64_t a = lists[lo], b = lists[hi];
+                if ((a > b) == up) {
+                    lists[lo] = b;
+                    lists[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < k; e += blockDim.x)
+        out.cand[(size_t)q * out.cap + (size_t)blockIdx.x * k + e] = lists[e];
+    if (prof_bytes) {
+        for (int off = 16; off; off >>= 1) steps += __shfl_xor_sync(0xffffffffu, steps, off);
+        if (lane == 0 && steps) atomicAdd(prof_bytes, steps * 4ull);
+    }
+}
+
+// the rows as a 3-D tensor for the streamed scan: [32 floats][row][chunk of 32
+// floats]; box = all of a stage's rows x the chunks of the first pairwise block
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool rows_tensor_map(CUtensorMap *tm, const float *X, int64_t N, int n, int hb)
+{
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {32, (cuuint64_t)N, (cuuint64_t)(n / 32)};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * 4, 128};  // bytes: row, chunk
+    const cuuint32_t box[3] = {32, (cuuint32_t)RS_TR, (cuuint32_t)(hb / 32)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(X), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // the row scan's per-query d2 bound from an inclusive key bound (k real
 // distances <= its d2), KEY_EMPTY = none
 __global__ void gbound_from_thr_kernel(const uint64_t *__restrict__ thr, int nq, unsigned int *__restrict__ gb)
@@ -226,7 +434,7 @@ __global__ void gbound_from_thr_kernel(const uint64_t *__restrict__ thr, int nq,
 
 int rowscan_ranges(int64_t N, int k)
 {
-    const int64_t want = 4 * (int64_t)num_sms();
+    const int64_t want = (int64_t)num_sms();  // one persistent CTA per SM and query
     const int64_t by_rows = std::max<int64_t>(1, N / 256);
     const int64_t by_smem = std::max<int64_t>(1, 262144 / std::max(k, 1));  // k keys dumped per range
     return (int)std::max<int64_t>(1, std::min(std::min(want, by_rows), by_smem));
@@ -236,20 +444,47 @@ template <int NT>
 static int launch_rows_t(const float *X, int64_t N, const float *Q, int nq, int k, uint32_t id_base, ScanOut out,
                          cudaStream_t s)
 {
-    int p2 = 1;
-    while (p2 < 32 * k) p2 <<= 1;
-    const int smem = p2 * 8;
-    SSB_REQUIRE(smem <= 227 * 1024, "k too large for the row scan");
-    SSB_CUDA(cudaFuncSetAttribute(scan_rows_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int ranges = rowscan_ranges(N, k);
-    const int64_t rpr = (N + ranges - 1) / ranges;
-    DevBuf gb;
+    DevBuf gb, buckets;
     SSB_CUDA(gb.alloc(4 * (size_t)nq, s));
     SSB_CUDA(cudaMemsetAsync(gb.p, 0x7f, 4 * (size_t)nq, s));  // 0x7f7f7f7f: a huge finite bound until set
     if (out.thr) {  // a bound carried in (the streamed file scan's running k-th key): abandon from the start
         gbound_from_thr_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out.thr, nq, gb.as<unsigned int>());
         SSB_CHECK_LAUNCH();
     }
+    // the streamed kernel: lists + as many ring stages as fit (the tensor map needs 16-byte aligned rows)
+    constexpr int HB = NT > 128 ? 128 : NT;
+    const size_t list_bytes = ((size_t)RS_TR * k * 8 + 1023) & ~(size_t)1023;
+    const size_t stage_bytes = (size_t)RS_TR * HB * 4;
+    const size_t budget = 227 * 1024 - 1024;  // the static barriers and bound, padded to the ring's 1024-byte alignment
+    const int nstage = list_bytes + 2 * stage_bytes <= budget
+                           ? (int)std::min<size_t>(RS_MAXST, (budget - list_bytes) / stage_bytes) : 0;
+    CUtensorMap tmap;
+    if (nstage >= 2 && ((uintptr_t)X & 15) == 0 && N < (1ll << 31) && !getenv("SSB_ROWSCAN_DIRECT") &&  // env: A/B
+        rows_tensor_map(&tmap, X, N, NT, HB)) {
+        size_t p2 = 1;
+        while (p2 < (size_t)RS_TR * k) p2 <<= 1;
+        const int smem = (int)std::max(list_bytes + nstage * stage_bytes, p2 * 8);
+        SSB_CUDA(cudaFuncSetAttribute(scan_rows_stream_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int64_t rpr = (N + ranges - 1) / ranges;
+        rpr = (rpr + RS_TR - 1) / RS_TR * RS_TR;
+        const int kstride = (k + 3) & ~3;
+        SSB_CUDA(buckets.alloc(4 * (size_t)nq * kstride, s));
+        SSB_CUDA(cudaMemsetAsync(buckets.p, 0xff, 4 * (size_t)nq * kstride, s));  // unset
+        ProfScope ps("scan_rows", s, 0.0);
+        scan_rows_stream_kernel<NT><<<dim3((unsigned)ranges, (unsigned)nq), 32 * (RS_CW + 1), smem, s>>>(
+            tmap, X, N, Q, k, id_base, rpr, gb.as<unsigned int>(), buckets.as<unsigned int>(), kstride, nstage, out,
+            ps.counter());
+        SSB_CHECK_LAUNCH();
+        return OK;
+    }
+    // rows that are not 16-byte aligned: loads straight from global memory
+    int p2 = 1;
+    while (p2 < 32 * k) p2 <<= 1;
+    const int smem = p2 * 8;
+    SSB_REQUIRE(smem <= 227 * 1024, "k too large for the row scan");
+    SSB_CUDA(cudaFuncSetAttribute(scan_rows_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t rpr = (N + ranges - 1) / ranges;
     ProfScope ps("scan_rows", s, 0.0);
     scan_rows_kernel<NT><<<dim3((unsigned)ranges, (unsigned)nq), 256, smem, s>>>(
         X, N, Q, k, id_base, rpr, ranges, gb.as<unsigned int>(), out, ps.counter());

@@ -179,6 +179,49 @@ def test_bruteforce_few_queries_row_scan(ssb, oracle, n, N, B, k):
     assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
 
 
+@pytest.mark.parametrize("n,N,B,k", [(256, 100_003, 1, 100), (96, 30_001, 2, 10)])
+def test_bruteforce_row_scan_direct_kernel(ssb, oracle, monkeypatch, n, N, B, k):
+    """The direct-load row scan (the path of rows that are not 16-byte aligned;
+    forced here by the A/B switch) and a misaligned view of the rows answer
+    like the streamed kernel: the oracle's ids and d2 bits."""
+    import torch
+    X = random_walks(N, n, 3100 + N)
+    Q = (X[[N // 3, N // 5][:B]] + np.float32(0.02)).astype(np.float32)
+    od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+    monkeypatch.setenv("SSB_ROWSCAN_DIRECT", "1")
+    d2, ids = ssb.knn_batch(X, Q, k)
+    monkeypatch.delenv("SSB_ROWSCAN_DIRECT")
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+    # rows starting 4 bytes past a 16-byte boundary
+    buf = torch.empty(N * n + 1, dtype=torch.float32, device="cuda")
+    buf[1:].copy_(torch.from_numpy(X).reshape(-1))
+    Xm = buf[1:].view(N, n)
+    assert Xm.data_ptr() % 16 == 4
+    d2, ids = ssb.knn_batch(Xm, Q, k)
+    assert np.array_equal(ids.cpu().numpy(), oid)
+    assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
+def test_bruteforce_row_scan_easy_and_hard_bounds(ssb, oracle):
+    """The class-minimum bound of the streamed row scan: a query with many
+    near-duplicates (the bound collapses at once: nearly every row abandoned
+    after its first block), a far query (nothing abandoned early) and k larger
+    than the rows of a range."""
+    N, n = 200_000, 256
+    X = random_walks(N, n, 4242)
+    rng = np.random.default_rng(7)
+    for i in range(300):                       # 300 near copies of row 1000 spread over the ranges
+        X[(i * 661 + 17) % N] = X[1000] + np.float32(1e-3) * rng.standard_normal(n).astype(np.float32)
+    near = X[[1000]].copy()
+    far = (X[[5]] * np.float32(-3.0) + np.float32(2.0)).astype(np.float32)
+    for Q, k in ((near, 100), (near, 256), (far, 100), (np.concatenate([near, far]), 1)):
+        d2, ids = ssb.knn_batch(X, Q, k)
+        od2, oid = oracle.knn_scan(X, Q, k, threads=8)
+        assert np.array_equal(ids.cpu().numpy(), oid)
+        assert np.array_equal(bits(d2.cpu().numpy()), bits(od2))
+
+
 def test_bruteforce_row_scan_ties(ssb, oracle):
     X = random_walks(70_000, 256, 77)
     for i in (5, 33_333, 69_999):
