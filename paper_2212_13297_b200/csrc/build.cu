@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32)
         nd = nodes[tk.node];
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
     const int m = nd.m, ncol = 6 * m;
     const int stage_floats = ncol * EV_TS;
     const int c = (int)tk.cg * EV_WARPS + warp;
@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4) finalize_rows_kernel(Finali
     const int padn = n + PAD * WORD_SEGMENTS;
     float *thr = fin_sm;                                       // [ALPHABET]
     int *ilay = reinterpret_cast<int *>(fin_sm + ALPHABET);    // physical -> logical
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
     float *buf = fin_sm + ALPHABET + n + warp * padn;
     for (int i = threadIdx.x; i < ALPHABET; i += blockDim.x)
         thr[i] = i < ALPHABET - 1 ? __double2float_ru(a.bp[i]) : __int_as_float(0x7f800000);

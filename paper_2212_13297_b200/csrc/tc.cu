@@ -274,7 +274,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     const int NS = (int)(ring_bytes / (chunk_bytes * KB));  // tile slots (<= TC_NBAR)
     unsigned char *sRing = base;  // NS tile slots of KB chunks
     TileSlot *slots = reinterpret_cast<TileSlot *>(sRing + ring_bytes);  // [TC_RS]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(slots + TC_RS);
+    // (projected mode has no side data: its barriers follow the ring, and the side ring's
+    // and the stages' bytes hold the per-warp candidate queues)
+    uint64_t *bars = SEG ? reinterpret_cast<uint64_t *>(sRing + ring_bytes) : reinterpret_cast<uint64_t *>(slots + TC_RS);
     uint64_t *a_full = bars + 0;
     uint64_t *b_full = bars + 1;                      // [TC_NBAR]
     uint64_t *b_empty = b_full + TC_NBAR;             // [TC_NBAR]
@@ -284,10 +286,23 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     uint64_t *r_empty = r_full + TC_RS;               // [TC_RS]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(r_empty + TC_RS);
     constexpr int STG = TC_STAGE * 8 / EPW;  // per-warp stage entries (same total)
-    constexpr int COLS = 512 / EPW;          // columns of a tile per epilogue thread
+    // projected mode with 16 epilogue warps: two groups of 8 take alternate tiles (64
+    // columns per thread), so one group's accumulator wait and TMEM loads overlap the
+    // other group's max tree instead of all 16 warps doing each phase in lockstep
+    constexpr bool ALT = SEG && EPW == 16;
+    constexpr int COLS = ALT ? 64 : 512 / EPW;  // columns of a tile per epilogue thread
     uint2 *s_stage = reinterpret_cast<uint2 *>(tmem_slot + 4);  // [EPW warps][STG]
     float *s_stage_lb = reinterpret_cast<float *>(s_stage + 8 * TC_STAGE);  // [EPW warps][STG]
     unsigned *s_fill = reinterpret_cast<unsigned *>(s_stage_lb + 8 * TC_STAGE);  // [EPW warps]
+    // SEG: per epilogue warp 32 emission counters + SQ_CAP queue entries of 80 bytes (16
+    // accumulator columns, then threshold, first row, owner lane)
+    constexpr int SQ_CAP = 21, SQ_STRIDE = 1824;
+    static_assert(128 + SQ_CAP * 80 <= SQ_STRIDE && SQ_STRIDE % 16 == 0, "queue layout");
+    static_assert((8 * (1 + 2 * TC_NBAR + 2 * TC_NACC + 2 * TC_RS) + 24) % 16 == 0, "queue alignment");
+    static_assert(!SEG || 8 * (1 + 2 * TC_NBAR + 2 * TC_NACC + 2 * TC_RS) + 24 + 16 * SQ_STRIDE <=
+                              TC_RS * (int)sizeof(TileSlot) + 8 * (1 + 2 * TC_NBAR + 2 * TC_NACC + 2 * TC_RS) + 16 + 8 * TC_STAGE * 12 + 64,
+                  "the queues fit in the side ring's and the stages' bytes");
+    unsigned char *s_segq = reinterpret_cast<unsigned char *>(tmem_slot + 6);  // 16-byte aligned (ring_bytes + 592)
 
     // the warp index through a shuffle: the compiler then knows the role branches are
     // warp-uniform and keeps the producer's and the MMA issuer's values in uniform
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         }
         for (int i = 0; i < TC_NACC; i++) {
             mbar_init(&t_full[i], 1);
-            mbar_init(&t_empty[i], EPW);  // one arrival per epilogue warp (after a __syncwarp)
+            mbar_init(&t_empty[i], ALT ? EPW / 2 : EPW);  // one arrival per epilogue warp of the tile (after a __syncwarp)
         }
         for (int i = 0; i < TC_RS; i++) {
             mbar_init(&r_full[i], 1);
@@ -601,11 +616,13 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         // thread <-> query m (TMEM lane), column half h of every 128-row tile
         const int ew = warp - 2;                   // 0..EPW-1
         const int lane_grp = warp & 3;             // TMEM lanes [32*lane_grp, +32)
-        const int h = ew >> 2;                     // column group: columns [h*COLS, +COLS) of each tile
+        const int h = ALT ? (ew >> 2) & 1 : ew >> 2;  // column group: columns [h*COLS, +COLS) of each tile
+        const int tgrp = ALT ? ew >> 3 : 0;        // ALT: this warp's tiles are tgrp, tgrp + 2, ...
+        constexpr int TSTEP = ALT ? 2 : 1;
         const int m = lane_grp * 32 + lane;
         const int ql = qb * TC_BM + m;
         const bool qvalid = ql < p.nq;
-        if (h == 0 && ntile > 0) {
+        if (ew < 4 && ntile > 0) {
             // stage this thread's query row as A: TMEM lane m, column c = bf16 pair (2c, 2c+1),
             // zero past n (the B chunks are zero-filled there by TMA)
             const int rowv = p.n / 8;  // uint4 per row
@@ -659,7 +676,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         uint2 *stage = s_stage + ew * STG;
         float *stage_lb = s_stage_lb + ew * STG;
         unsigned *stage_fill = s_fill + ew;  // reserved slots of this warp's stage (may pass STG)
-        if (lane == 0) *stage_fill = 0;
+        if (!SEG && lane == 0) *stage_fill = 0;
         __syncwarp();
         auto flush = [&]() {  // warp-uniform
             const unsigned n_st = min(*(volatile unsigned *)stage_fill, (unsigned)STG);
@@ -694,12 +711,69 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const int64_t rbase = (p.tile0 + t_begin) * TC_BN + h * COLS;  // nwarm = 0: tile t = t_begin + t
             // (a one-tile register prefetch -- tile t + 1's accumulator loaded and
             // released before tile t is examined -- measured 7% slower on C4)
-            uint32_t fs = 0, fph = 0;  // next accumulator to fetch, its phase
+            uint32_t fs = (uint32_t)tgrp, fph = 0;  // next accumulator to fetch, its phase
+            unsigned char *wq = s_segq + ew * SQ_STRIDE + 128;                      // this warp's queue entries
+            unsigned *wcnt = reinterpret_cast<unsigned *>(s_segq + ew * SQ_STRIDE);  // emissions per lane (owner)
+            wcnt[lane] = 0;
+            __syncwarp();
+            int qn = 0;  // queued entries (warp-uniform)
+            auto drain = [&]() {  // warp-uniform: lane e tests entry e's 16 columns and emits its candidates
+                __syncwarp();
+                unsigned emit = 0, erow = 0, eown = 0;
+                if (lane < qn) {
+                    const uint4 *e = reinterpret_cast<const uint4 *>(wq + lane * 80);
+                    const uint4 x0 = e[0], x1 = e[1], x2 = e[2], x3 = e[3], tg = e[4];
+                    const float et = __uint_as_float(tg.x);
+                    erow = tg.y;
+                    eown = tg.z;
+                    const uint32_t xs[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w,
+                                             x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
+#pragma unroll
+                    for (int i = 0; i < 16; i++) emit |= (__uint_as_float(xs[i]) >= et ? 1u : 0u) << i;
+                    const int64_t left = p.N - (int64_t)erow;  // rows past N (zero-filled tiles) never qualify
+                    emit &= left >= 16 ? 0xffffu : (left > 0 ? (1u << left) - 1u : 0u);
+                }
+                const unsigned cnt = __popc(emit);
+                unsigned incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned nb = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += nb;
+                }
+                const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total) {
+                    unsigned long long base_slot = 0;
+                    if (lane == 0) base_slot = atomicAdd(p.cand_n, (unsigned long long)total);
+                    base_slot = __shfl_sync(0xffffffffu, base_slot, 0) + (incl - cnt);
+                    const unsigned eq = (unsigned)(ql - lane) + eown;  // the owner's query
+                    if (cnt) atomicAdd(wcnt + eown, cnt);
+                    while (emit) {
+                        const int i = __ffs(emit) - 1;
+                        emit &= emit - 1;
+                        if ((int64_t)base_slot < p.cand_cap)
+                            p.cand[base_slot] = make_uint2(eq, erow + (unsigned)i);
+                        else
+                            p.seg_flag[eq] = 1u;  // dropped: the query is answered elsewhere
+                        base_slot++;
+                    }
+                    __syncwarp();
+                    seg_local = wcnt[lane];
+                    if (seg_local > (unsigned)p.seg_cap && qvalid) {  // give up: the full filter answers it
+                        p.seg_flag[ql] = 1u;
+                        thr = __int_as_float(0x7f800000);
+                    }
+                }
+                qn = 0;
+                __syncwarp();
+            };
             auto fetch = [&](uint32_t(&v)[COLS], const bool LEAN) {
                 const uint32_t sa = 8u * fs, taddr = tbase + fs * (uint32_t)TC_BN;
+                // (one 64-column load instead of four 16-column ones, spinning, and a few plain
+                // probes before the suspending wait all measured the same on C4)
                 if (!LEAN && p.spin_epi) mbar_spin_a(a_tfull + sa, fph); else mbar_wait_a(a_tfull + sa, fph);
-                if (++fs == TC_NACC) {
-                    fs = 0;
+                fs += TSTEP;
+                if (fs >= TC_NACC) {
+                    fs -= TC_NACC;
                     fph ^= 1u;
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -718,71 +792,49 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
             };
             auto examine = [&](const uint32_t(&v)[COLS], int t, const bool LEAN) {
-                if (!LEAN && (t & 15) == 0) check_gave_up();
-                // maxima of column triples (kept: a triple below the threshold
-                // needs no per-column test), then of the 16-column groups
-                float tri[COLS / 16][5];
+                if (!LEAN && ((t - tgrp) & 15) == 0) check_gave_up();
+                // maxima of the 16-column groups, through column triples (recomputed
+                // for a group that passes: a triple below the threshold needs no
+                // per-column test, and keeping 5 maxima per group costs registers)
                 float mg[COLS / 16];
 #pragma unroll
                 for (int g = 0; g < COLS / 16; g++) {
                     const float *vf = reinterpret_cast<const float *>(v + 16 * g);
+                    float tr[5];
 #pragma unroll
-                    for (int j = 0; j < 5; j++) tri[g][j] = fmax3f(vf[3 * j], vf[3 * j + 1], vf[3 * j + 2]);
-                    mg[g] = fmaxf(fmax3f(tri[g][0], tri[g][1], tri[g][2]), fmax3f(tri[g][3], tri[g][4], vf[15]));
+                    for (int j = 0; j < 5; j++) tr[j] = fmax3f(vf[3 * j], vf[3 * j + 1], vf[3 * j + 2]);
+                    mg[g] = fmaxf(fmax3f(tr[0], tr[1], tr[2]), fmax3f(tr[3], tr[4], vf[15]));
                 }
                 float mx = mg[0];
 #pragma unroll
                 for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
                 if (!LEAN && p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: loads + max, no emission
                 if (!__any_sync(0xffffffffu, mx >= thr)) return;
-                const int64_t row0 = rbase + (int64_t)t * TC_BN;
-                const int64_t left = p.N - row0;
-                const uint64_t valid = left >= COLS ? ~0ull : (left > 0 ? (1ull << left) - 1ull : 0ull);
+                // a 16-column group that may hold candidates goes into the warp's queue as it
+                // is (5 vector stores); the per-column tests and the emission run for a whole
+                // queue at once, every lane on one entry, instead of one or two lanes walking
+                // a divergent path while the accumulator pipeline waits for this warp
+                const uint32_t row0 = (uint32_t)(rbase + (int64_t)t * TC_BN);
 #pragma unroll
-                for (int c0 = 0; c0 < COLS; c0 += 16) {
-                    uint32_t emit = 0;
-                    if (mg[c0 / 16] >= thr) {
-                        const float *vf = reinterpret_cast<const float *>(v + c0);
-#pragma unroll
-                        for (int j = 0; j < 5; j++)
-                            if (tri[c0 / 16][j] >= thr) {
-                                if (vf[3 * j] >= thr) emit |= 1u << (3 * j);
-                                if (vf[3 * j + 1] >= thr) emit |= 2u << (3 * j);
-                                if (vf[3 * j + 2] >= thr) emit |= 4u << (3 * j);
-                            }
-                        if (vf[15] >= thr) emit |= 1u << 15;
-                        emit &= (uint32_t)(valid >> c0) & 0xffffu;
-                    }
-                    if (emit) {
-                        const unsigned cnt = __popc(emit);
-                        seg_local += cnt;
-                        if (seg_local > (unsigned)p.seg_cap) {  // give up: the full filter answers it
-                            p.seg_flag[ql] = 1u;
-                            thr = __int_as_float(0x7f800000);
+                for (int g = 0; g < COLS / 16; g++) {
+                    unsigned m = __ballot_sync(0xffffffffu, mg[g] >= thr);
+                    while (m) {
+                        const int rank = __popc(m & ((1u << lane) - 1u));
+                        const bool mine = ((m >> lane) & 1u) && rank < SQ_CAP - qn;
+                        if (mine) {
+                            uint4 *e = reinterpret_cast<uint4 *>(wq + (qn + rank) * 80);
+                            e[0] = make_uint4(v[16 * g], v[16 * g + 1], v[16 * g + 2], v[16 * g + 3]);
+                            e[1] = make_uint4(v[16 * g + 4], v[16 * g + 5], v[16 * g + 6], v[16 * g + 7]);
+                            e[2] = make_uint4(v[16 * g + 8], v[16 * g + 9], v[16 * g + 10], v[16 * g + 11]);
+                            e[3] = make_uint4(v[16 * g + 12], v[16 * g + 13], v[16 * g + 14], v[16 * g + 15]);
+                            e[4] = make_uint4(__float_as_uint(thr), row0 + 16u * g, (unsigned)lane, 0u);
                         }
-                        unsigned slot = atomicAdd(stage_fill, cnt);
-                        unsigned long long gslot = 0;
-                        if (slot + cnt > (unsigned)STG)
-                            gslot = atomicAdd(p.cand_n, (unsigned long long)(slot + cnt - max(slot, (unsigned)STG)));
-                        while (emit) {
-                            const int i = __ffs(emit) - 1;
-                            emit &= emit - 1;
-                            const uint2 cv = make_uint2((unsigned)ql, (unsigned)(row0 + c0 + i));
-                            if (slot < (unsigned)STG) {
-                                stage[slot] = cv;
-                            } else {
-                                if ((int64_t)gslot < p.cand_cap)
-                                    p.cand[gslot] = cv;
-                                else
-                                    p.seg_flag[ql] = 1u;
-                                gslot++;
-                            }
-                            slot++;
-                        }
+                        const unsigned took = __ballot_sync(0xffffffffu, mine);
+                        qn += __popc(took);
+                        m &= ~took;
+                        if (qn == SQ_CAP) drain();
                     }
                 }
-                __syncwarp();
-                if (*(volatile unsigned *)stage_fill >= (unsigned)(STG / 2)) flush();
             };
             if (p.skip_epi == 0 && p.spin_epi == 0) {
                 // the hot loop (the epilogue issues about as many instructions
@@ -791,19 +843,20 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 for (int t0 = 0; t0 < niter; t0 += 16) {
                     check_gave_up();
                     const int t1 = min(niter, t0 + 16);
-                    for (int t = t0; t < t1; t++) {
+                    for (int t = t0 + tgrp; t < t1; t += TSTEP) {
                         uint32_t v[COLS];
                         fetch(v, true);
                         examine(v, t, true);
                     }
                 }
             } else {
-                for (int t = 0; t < niter; t++) {
+                for (int t = tgrp; t < niter; t += TSTEP) {
                     uint32_t v[COLS];
                     fetch(v, false);
                     if (!diag_skip && p.skip_epi != 5) examine(v, t, false);  // 5: diagnostics, TMEM loads only
                 }
             }
+            if (qn) drain();
         } else
         for (int t = 0; t < niter; t++) {
             const int s = t % TC_NACC;
@@ -1011,7 +1064,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             if (qvalid && mine < gcur) atomicMin(gb, __float_as_uint(mine));
         }
         __syncwarp();
-        flush();
+        if constexpr (!SEG) flush();
         if (SEG && qvalid && seg_local) atomicAdd(p.seg_cnt + ql, seg_local);
     }
     __syncthreads();
