@@ -701,7 +701,10 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         std::vector<uint32_t> c0(nq), f0(nq);
         SSB_CUDA(cudaMemcpyAsync(c0.data(), pw.cnt.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaMemcpyAsync(f0.data(), pw.flag.p, 4 * (size_t)nq, cudaMemcpyDeviceToHost, s));
+        unsigned long long hn0 = 0;  // the sample's candidate count (the tightening below does not change it)
+        SSB_CUDA(cudaMemcpyAsync(&hn0, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
         SSB_CUDA(cudaStreamSynchronize(s));
+        pw.nc = std::min<int64_t>((int64_t)hn0, pw.cap);
         for (int i = 0; i < nq; i++) {
             is_hard[i] = f0[i] || (double)c0[i] * (double)tiles / (double)t0 > (double)seg_cap;
             predicted_hard += is_hard[i];
@@ -716,10 +719,6 @@ int proj_route(const Index &ix, const float *Q, const std::vector<int32_t> &qtc,
         for (int i = 0; i < nq; i++) total[i] = c0[i];
         rc = phase_tighten(ix, pw, qlay, B, k, so, thr, s);
         if (rc) return rc;
-        unsigned long long hn0 = 0;
-        SSB_CUDA(cudaMemcpyAsync(&hn0, pw.cn.p, 8, cudaMemcpyDeviceToHost, s));
-        SSB_CUDA(cudaStreamSynchronize(s));  // f0 dies here
-        pw.nc = std::min<int64_t>((int64_t)hn0, pw.cap);
     }
 
     // ---- main phase: the remaining queries over the rest of the rows -----------

@@ -216,6 +216,7 @@ struct TcParams {
     float *dump;               // debug: full S matrix (nq x N) when non-null
     int warm;                  // warm-up tiles per CTA (bounds only, rescanned with emission)
     int unit;                  // SEG / UNI: tiles per bulk load (divides warm)
+    int no_lean;               // A/B: the generic MMA issue loop (SSB_TC_NOLEAN)
     int spin_epi;              // epilogue warps spin on the accumulator barrier (A/B; default: suspend)
     int rmask;                 // bucket refresh every rmask+1 tiles (when this thread updated one)
     int skip_epi;              // diagnostics (SSB_TC_DIAG): 1 epilogue only releases TMEM, 2 TMEM loads + max,
@@ -418,10 +419,42 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             uint32_t phase = 0;
             int s = 0;
             uint32_t tph = 0;
+            const bool lean6 = KB == 3 && KS == 6 && CW == 32 && p.skip_epi != 3 && !p.no_lean;
             for (int u = 0, t = 0; t < niter; u++, t += SEG_U) {
                 const int nt = min(SEG_U, niter - t);
                 mbar_spin_a(a_bfull + 8u * slot, phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lean6) {
+                    // n = 96 as three 32-column chunks of two K-steps: the tile's six MMAs and
+                    // its commit in one block (one election, the descriptors by increments) --
+                    // with 6 K-steps per tile this warp's instruction stream paces the kernel
+                    uint64_t bd = bdesc0 + (uint64_t)(((uint32_t)(slot * SEG_U) * tile_bytes) >> 4);
+                    const uint64_t cb = (uint64_t)(chunk_bytes >> 4);
+                    for (int i = 0; i < nt; i++) {
+                        if (t + i >= TC_NACC) mbar_spin_a(a_tempty + 8u * s, tph ^ 1u);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        asm volatile(
+                            "{\n.reg .pred q;\n.reg .b64 d1, d2, d3, d4, d5;\n.reg .b32 a1, a2, a3, a4, a5;\n"
+                            "elect.sync _|q, 0xffffffff;\n"
+                            "add.s64 d1, %2, 2;\nadd.s64 d2, %2, %5;\nadd.s64 d3, d2, 2;\nadd.s64 d4, d2, %5;\nadd.s64 d5, d4, 2;\n"
+                            "add.s32 a1, %1, 8;\nadd.s32 a2, %1, 16;\nadd.s32 a3, %1, 24;\nadd.s32 a4, %1, 32;\nadd.s32 a5, %1, 40;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], d4, %3, 1;\n"
+                            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], d5, %3, 1;\n"
+                            "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(
+                                tmem_base + (uint32_t)(s * TC_BN)),
+                            "r"(a_tmem), "l"(bd), "r"(TC_IDESC), "r"(a_tfull + 8u * s), "l"(cb)
+                            : "memory");
+                        bd += tile_bytes >> 4;
+                        if (++s == TC_NACC) {
+                            s = 0;
+                            tph ^= 1u;
+                        }
+                    }
+                } else
                 for (int i = 0; i < nt; i++) {
                     if (t + i >= TC_NACC) mbar_spin_a(a_tempty + 8u * s, tph ^ 1u);
                     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -857,8 +890,71 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 }
             }
             if (qn) drain();
-        } else
+        } else {
+        float thr_c = -__int_as_float(0x7f800000);  // the last tile-level threshold (see the steady state below)
+        // per-16-column-group maxima of a thread's columns (three-input max: 8 FMNMX3 per group)
+        auto max_tree = [&](const uint32_t(&v)[COLS], float(&mg)[COLS / 16]) -> float {
+#pragma unroll
+            for (int g = 0; g < COLS / 16; g++) {
+                const float *vf = reinterpret_cast<const float *>(v + 16 * g);
+                float a = fmax3f(vf[0], vf[1], vf[2]), b = fmax3f(vf[3], vf[4], vf[5]);
+                float c = fmax3f(vf[6], vf[7], vf[8]), d = fmax3f(vf[9], vf[10], vf[11]);
+                float e2 = fmax3f(vf[12], vf[13], vf[14]);
+                a = fmax3f(a, b, c);
+                d = fmax3f(d, e2, vf[15]);
+                mg[g] = fmaxf(a, d);
+            }
+            float mx = mg[0];
+#pragma unroll
+            for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
+            return mx;
+        };
+        const uint32_t tlane = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(h * COLS);
         for (int t = 0; t < niter; t++) {
+            uint32_t v[COLS];
+            float mg[COLS / 16];
+            float mx = 0.f;
+            bool have = false;  // v / mg / mx of tile t already loaded by the steady-state run
+            if constexpr (UNI && KTOP >= 0) {
+                // Steady state (uniform row constants, past the warm-up): a tile none of whose
+                // maxima reaches the last threshold this thread computed cannot matter -- that
+                // threshold came from a bound that has only tightened since, so it is the lower
+                // (more cautious) one -- and nothing of the general body (bound, thresholds,
+                // stage, buckets, the published bound) would change.  Such tiles run through
+                // this loop: wait, load, release, max tree, one vote (~60 instructions per
+                // warp and tile against ~140 of the general body; the 8 epilogue warps'
+                // instruction count, not the tensor pipe or HBM, paced the n = 96 filter).
+                // The first tile that may matter, or a pending bucket refresh, falls
+                // through to the general body with its columns already in registers.
+                if (t >= 2 * nwarm && p.skip_epi == 0 && !p.spin_epi) {
+                    uint32_t ls = (uint32_t)(t % TC_NACC), lph = (uint32_t)((t / TC_NACC) & 1);
+                    for (; t < niter; t++) {
+                        if ((t & 7) == 0) {
+                            gseen = gnext;
+                            if (qvalid) gnext = __uint_as_float(*(volatile const unsigned int *)gb);
+                        }
+                        mbar_wait_a(a_tfull + 8u * ls, lph);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t taddr = tlane + ls * (uint32_t)TC_BN;
+#pragma unroll
+                        for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
+                        tmem_wait_ld();
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_a(a_tempty + 8u * ls);
+                        if (++ls == TC_NACC) {
+                            ls = 0;
+                            lph ^= 1u;
+                        }
+                        mx = max_tree(v, mg);
+                        if (__any_sync(0xffffffffu, mx >= thr_c || touched)) {  // (`touched` is per thread)
+                            have = true;
+                            break;
+                        }
+                    }
+                    if (!have) break;  // every tile done
+                }
+            }
             const int s = t % TC_NACC;
             const int rs = t % TC_RS;
             const int64_t row0 = tile_of(t) * TC_BN + h * COLS;  // first row of this thread's columns
@@ -871,7 +967,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // the shared bound of this query (other CTAs tighten it): read every
             // 8th tile, used from the 8th tile after, so the L2 round trip never
             // sits on a tile's critical path
-            if ((t & 7) == 0) {
+            if (!have && (t & 7) == 0) {
                 gseen = gnext;
                 if (qvalid) gnext = __uint_as_float(*(volatile const unsigned int *)gb);
             }
@@ -880,6 +976,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             const int hh = h * COLS / 64;  // its 64-row half tile (extremes over a superset: valid)
             const float4 tcl = UNI ? make_float4(p.uni_al, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh];
             const float4 tcu = UNI ? make_float4(p.uni_au, p.seg_u, p.seg_v, 0.f) : ts.tilec[2 * hh + 1];
+            if (!have) {
             if (p.spin_epi)
                 mbar_spin_a(a_tfull + 8u * s, (unsigned)((t / TC_NACC) & 1));
             else
@@ -893,8 +990,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 if (!UNI && lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
             }
-            const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(s * TC_BN + h * COLS);
-            uint32_t v[COLS];
+            const uint32_t taddr = tlane + (uint32_t)(s * TC_BN);
 #pragma unroll
             for (int j = 0; j < COLS; j += 16) tmem_ld16_nowait(taddr + (uint32_t)j, v + j);
             tmem_wait_ld();
@@ -909,6 +1005,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_a(a_rempty + 8u * rs);
                 continue;
+            }
+            mx = max_tree(v, mg);
             }
             // tile-level necessary conditions on the dot product s:
             //   lb_r <= bound  =>  s >= s_lo ;   ub_r < kth  =>  s > s_need
@@ -925,20 +1023,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
                     thr_s = emit_ok ? fminf(s_lo, s_need) : s_need;
                 }
             }
-            float mg[COLS / 16];  // per 16-column group maxima (three-input max: 8 FMNMX3 per group)
-#pragma unroll
-            for (int g = 0; g < COLS / 16; g++) {
-                const float *vf = reinterpret_cast<const float *>(v + 16 * g);
-                float a = fmax3f(vf[0], vf[1], vf[2]), b = fmax3f(vf[3], vf[4], vf[5]);
-                float c = fmax3f(vf[6], vf[7], vf[8]), d = fmax3f(vf[9], vf[10], vf[11]);
-                float e2 = fmax3f(vf[12], vf[13], vf[14]);
-                a = fmax3f(a, b, c);
-                d = fmax3f(d, e2, vf[15]);
-                mg[g] = fmaxf(a, d);
-            }
-            float mx = mg[0];
-#pragma unroll
-            for (int g = 1; g < COLS / 16; g++) mx = fmaxf(mx, mg[g]);
+            if (emit_ok) thr_c = thr_s;
             if (p.skip_epi == 2) mx = -__int_as_float(0x7f800000);  // diagnostics: TMEM loads + max only
             if (__any_sync(0xffffffffu, mx >= thr_s)) {
                 // rows past N (TMA zero fill; lb = +inf) never qualify, even with bound = +inf
@@ -1062,6 +1147,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             // publish this thread's bound for the other CTAs of the query block
             const float mine = fminf(kth, bmax);
             if (qvalid && mine < gcur) atomicMin(gb, __float_as_uint(mine));
+        }
         }
         __syncwarp();
         if constexpr (!SEG) flush();
@@ -1367,6 +1453,7 @@ int launch_tc_filter(const void *Qb, const float *qn2, const float2 *qen, int nq
     p.k = k;
     p.warm = seg ? 0 : 8;  // fixed bounds: nothing to warm up
     p.spin_epi = getenv("SSB_TC_SPIN") ? atoi(getenv("SSB_TC_SPIN")) : 0;
+    p.no_lean = getenv("SSB_TC_NOLEAN") ? 1 : 0;
     {   // load units (SEG / UNI): up to 64 KB, at least three in the ring
         const int ns = (int)((int64_t)TC_NSLOT * TC_BN * 128 / ((int64_t)TC_BN * p.CW * 2 * p.KB));
         p.unit = 1;
