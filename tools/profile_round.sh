@@ -19,7 +19,9 @@ bench)
 ref)
   timeout 900 python bench.py --impl reference > $O/${TAG}_bench_reference_c4.json 2> $O/${TAG}_bench_reference_c4.err ;;
 launches)
-  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+  # the query step's kernels (the two timed builds launch ~800 kernels first: filter by name)
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none \
+    -k regex:"tc_filter|rescore|ix_|select|proj_b|proj_t|proj_m|proj_q|query_prep|keys_to|seed_bound|merge|pack" -c 600 --csv \
     --log-file $O/${TAG}_c4_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --ingest-gb 0 \
     > $O/${TAG}_c4_launches.log 2>&1 ;;
 full)
