@@ -182,20 +182,29 @@ class Clocks:
         self.proc = None
         self.lines: list[str] = []
 
+    _NAMES = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap"))
+
+    def _one(self, nv, h, reasons_fn, mx):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = reasons_fn(h)
+        flags = ", ".join("Active" if r & bit else "Not Active" for bit, _ in self._NAMES)
+        # the same columns as the nvidia-smi query below (no power query: the slowest NVML call)
+        self.lines.append(f"{sm}, {mx}, 0, {r:#x}, {flags}")
+
     def _nvml_loop(self, nv, h):
-        names = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap"))
         reasons_fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        self._nv = (nv, h, reasons_fn, mx)
         while not self.stop.is_set():
             try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = reasons_fn(h)
-                flags = ",".join("Active" if r & bit else "Not Active" for bit, _ in names)
-                # the same columns as the nvidia-smi query below
-                self.lines.append(f"{sm}, {mx}, 0, {r:#x}, {flags.replace(',', ', ')}")  # (no power query: the slowest NVML call)
+                self._one(nv, h, reasons_fn, mx)
             except Exception:  # noqa: BLE001 -- a failed sample is skipped
                 pass
-            self.stop.wait(self.period_ms / 1000.0)
+            while True:  # sleep a period; rearm() restarts the period (no sample right at a region's start)
+                self.again.clear()
+                self.stop.wait(self.period_ms / 1000.0)
+                if self.stop.is_set() or not self.again.is_set():
+                    break
 
     def __enter__(self):
         if not self.enabled:
@@ -209,6 +218,7 @@ class Clocks:
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.index)
             self.stop = threading.Event()
+            self.again = threading.Event()
             self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
             self.t.start()
             self.nvml = True
@@ -244,6 +254,22 @@ class Clocks:
 
     def mark(self):
         self.marks = getattr(self, "marks", []) + [len(self.lines)]
+
+    def sample_now(self):
+        """One sample from the calling thread (the end of a timed region: still under load)."""
+        if getattr(self, "nvml", False):
+            try:
+                self._one(*self._nv)
+            except Exception:  # noqa: BLE001
+                pass
+
+    def rearm(self):
+        """Restart the sampling period: the next sample is one period from now.  A sample
+        stalls the CUDA calls it collides with (2-3 ms as a rule, 20-150 ms now and then:
+        per-step host times under SSB_BENCH_TRACE=1); the settle loop's 0.5 s used to put one
+        on the first steps of every timed region."""
+        if getattr(self, "nvml", False):
+            self.again.set()
 
     def summary(self) -> dict:
         sm, mx, reasons = [], None, set()
@@ -687,12 +713,14 @@ def run_ours(args, rank, world) -> int:
     clk = Clocks(local, enabled=dev.cuda, period_ms=args.clock_ms).__enter__()
     from paper_2212_13297_b200 import _lib
 
-    # (C3's 70 ms timed region -- 20 steps of 4 calls, each a few host round trips -- is
-    # an outlier in about one run in four on some boxes, 50K-250K against 300K queries/s,
-    # with the per-kernel profiler on or off (SSB_BENCH_NOPROF=1) and the clock sampler
-    # on or off (--clock-ms 0); the end-to-end region right after never is.  The kernels'
-    # times are the same in those runs: the host side stalls.  SSB_BENCH_TRACE=1 prints
-    # the per-step host times.)
+    # (C3's 70 ms timed region -- 20 steps of 4 calls -- was an outlier in one run in three,
+    # 50K-250K against 300K queries/s, always one stalled step among the first four
+    # (SSB_BENCH_TRACE=1 prints the per-step host times).  Three things met there: the clock
+    # sampler's sixth sample (0.5 s of settling = five periods: now re-armed at the region's
+    # start), the profiler's lazy counter allocation inside its first launch (now done when
+    # it is enabled) and the first routing probe of the region (every 16th lean call runs
+    # the index stages).  What is left: that probe call still costs 5-8 ms instead of 3.3,
+    # and 14-76 ms in two runs of ten.)
     prof_on = dev.cuda and not os.environ.get("SSB_BENCH_NOPROF")
     t_settle = time.perf_counter()
     for _ in range(args.warmup):
@@ -711,6 +739,7 @@ def run_ours(args, rank, world) -> int:
     try:
         barrier()
         dev.sync()
+        clk.rearm()
         clk.mark()  # only the samples taken inside the region count
         region.start()
         step_s = []
@@ -719,6 +748,7 @@ def run_ours(args, rank, world) -> int:
             step(Q_dev)
             step_s.append(time.perf_counter() - t_step)
         ms_local = region.stop()
+        clk.sample_now()  # (after the region's closing event: a short region may hold no periodic sample)
         if os.environ.get("SSB_BENCH_TRACE"):
             print("[bench] host ms per timed step: " + " ".join(f"{1000 * x:.2f}" for x in step_s), file=sys.stderr)
         clk.mark()

@@ -89,6 +89,17 @@ void ssb_prof_enable(int32_t on)
 {
     std::lock_guard<std::mutex> g(g_mu);
     g_on = on != 0;
+    if (!g_on) return;
+    // everything a profiled launch needs exists before the first one: a lazy cudaMalloc of
+    // the counter block inside a launch (synchronous, 0.06-0.19 s when it lands behind
+    // queued kernels) was the outlier of bench.py's short timed regions
+    if (!g_slots && cudaMalloc(&g_slots, sizeof(unsigned long long) * PROF_SLOTS) == cudaSuccess)
+        cudaMemset(g_slots, 0, sizeof(unsigned long long) * PROF_SLOTS);
+    while (g_pool.size() < 4096) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) break;
+        g_pool.push_back(e);
+    }
 }
 
 void ssb_prof_reset(void)
