@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 // over every CTA's published k-th), all bounds by k real distances.  At the
 // end the CTA's 32 lists are sorted together and its best k dumped.
 
-constexpr int ROWSCAN_MAX_B = 4;
+[[maybe_unused]] constexpr int ROWSCAN_MAX_B = 4;  // (the callers' B <= 4 test: capi.cu, ingest.cu)
 
 template <int NT>
 __global__ void __launch_bounds__(256)
